@@ -1,0 +1,225 @@
+/*
+ * flexcomm_b200.h — C-ABI of the B200-native Top-k gradient-sync path.
+ *
+ * This is the drop-in boundary for the hot path of the reference
+ * (arXiv 2312.02493, "flexcomm", /root/reference/proj/include/flexcomm).
+ * The reference is header-only C++ with no FFI; its hot path is the pair
+ *
+ *   artopk_step(const Cluster&, const std::vector<DenseGrad>& g_o,
+ *               ResidualStore&, CompressionRatio, SelectionMode, ReduceAlgo,
+ *               long step, SelectionLog*, ReduceOp, double payload_scale)
+ *                                           -- inc/artopk.hpp:62-111
+ *   ag_step(const Cluster&, const std::vector<DenseGrad>&, ResidualStore&,
+ *           CompressionRatio, CompressorKind, double, int)
+ *                                           -- inc/artopk.hpp:128-161
+ *
+ * plus the pieces they call (error_feedback compress.hpp:114, topk_exact
+ * compress.hpp:57, select_star/select_var artopk.hpp:27/35, the three
+ * collectives collectives.hpp:39-94, densify core.hpp:72).  Every entry
+ * point below names the reference symbol it replaces.  The C++ facade in
+ * include/flexcomm_b200/ re-exposes the reference signatures on top of it
+ * and re-throws the reference's exception types from the status codes.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  All functions return an fc_status;
+ *    fc_last_error() gives a thread-local message for the last failure.
+ *  - One host thread per context; calls are not reentrant.  Work is ordered
+ *    on the context's CUDA stream; a step returns after completion unless
+ *    FC_FLAG_ASYNC was given at creation.
+ *  - The ABI owns every device buffer (gradients, residuals, aggregate,
+ *    workspaces).  Host pointers passed in are caller-owned and only read /
+ *    written during the call.  *_ptr() getters give zero-copy device
+ *    pointers for callers whose gradients already live in HBM.
+ *  - Values are fp32, indices uint32 (G < 2^31).  The reference is fp64 with
+ *    size_t indices; the facade converts.
+ */
+#ifndef FLEXCOMM_B200_H_
+#define FLEXCOMM_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FC_ABI_VERSION 1
+
+/* Status codes.  The facade maps them onto the reference's exceptions
+ * (inc/artopk.hpp:68-78, inc/core.hpp:49,91, inc/compress.hpp:20-29,140). */
+typedef enum fc_status {
+  FC_OK = 0,
+  FC_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+  FC_ERR_OUT_OF_RANGE = 2,     /* std::out_of_range    */
+  FC_ERR_RUNTIME = 3,          /* std::runtime_error   */
+  FC_ERR_CUDA = 4,             /* CUDA runtime failure (runtime_error)  */
+  FC_ERR_NCCL = 5,             /* NCCL failure (runtime_error)          */
+  FC_ERR_NO_DEVICE = 6         /* no sm_100 device: the path never falls back to CPU */
+} fc_status;
+
+/* inc/artopk.hpp:13 */
+typedef enum fc_selection_mode { FC_STAR = 0, FC_VAR = 1 } fc_selection_mode;
+/* inc/collectives.hpp:36 */
+typedef enum fc_reduce_algo { FC_RING = 0, FC_TREE = 1 } fc_reduce_algo;
+/* inc/collectives.hpp:35 */
+typedef enum fc_reduce_op { FC_SUM = 0, FC_AVG = 1 } fc_reduce_op;
+/* inc/artopk.hpp:113 (only Exact is on the path; the others are §8f "next") */
+typedef enum fc_compressor { FC_EXACT = 0, FC_LAYERWISE = 1, FC_THRESHOLD = 2 } fc_compressor;
+/* memory kind of a caller pointer */
+typedef enum fc_memkind { FC_HOST = 0, FC_DEVICE = 1 } fc_memkind;
+
+/* creation flags */
+#define FC_FLAG_ASYNC 0x1u        /* do not synchronize at the end of a step      */
+#define FC_FLAG_NO_TIMING 0x2u    /* skip per-phase CUDA events                   */
+
+#define FC_NCCL_UID_BYTES 128
+
+typedef struct fc_opts {
+  int device;           /* CUDA ordinal for this context                       */
+  int n_local;          /* logical workers held by this context (loopback)     */
+  int world;            /* total workers; == n_local for loopback              */
+  int rank;             /* this context's first global rank                    */
+  const unsigned char* nccl_uid; /* FC_NCCL_UID_BYTES, NULL => loopback          */
+  uint64_t grad_len;    /* G, 1 <= G < 2^31                                     */
+  double max_cr;        /* largest compression ratio that will be used (sizes
+                           the k-length buffers); 0 => 1.0                     */
+  unsigned flags;
+} fc_opts;
+
+/* Per-step statistics.  Phase times come from CUDA events on the context
+ * stream (0 when FC_FLAG_NO_TIMING).  Byte counters are algorithmic bytes
+ * (SURVEY §8d), not measured traffic. */
+typedef struct fc_step_stats {
+  int selected_rank;        /* ART: broadcasting worker; AG: -1               */
+  int collective;           /* 0 AG, 1 ART_RING, 2 ART_TREE                    */
+  uint64_t k;               /* k_of(c, G), inc/compress.hpp:28                 */
+  float ms_total;           /* first kernel -> last kernel of the step         */
+  float ms_ef;              /* error feedback (+ candidate emission)           */
+  float ms_select;          /* threshold select + ordered compaction           */
+  float ms_exchange;        /* VAR norm exchange, broadcast, gather, allreduce
+                               or allgather                                    */
+  float ms_decode;          /* dense decode                                    */
+  double hbm_bytes;         /* algorithmic HBM bytes, this context             */
+  double bus_bytes;         /* NCCL-tests bus bytes, this context              */
+  uint64_t launches;        /* kernels this library launched for the step      */
+  int fallback;             /* 1 if the sampled candidate bound missed         */
+} fc_step_stats;
+
+/* Per-worker numbers of the last step (gain inputs, VAR norm, threshold). */
+typedef struct fc_worker_stats {
+  double ge_norm2;          /* ||g_e||^2                                       */
+  double kept_norm2;        /* sum of g_e^2 at the broadcast / own indices     */
+  double topk_norm2;        /* ||top-k values||^2 (VAR score, artopk.hpp:41)   */
+  uint32_t threshold_key;   /* |v| bit pattern of the k-th largest magnitude   */
+  uint64_t candidates;      /* elements kept by the sampled candidate bound    */
+  uint64_t count_above;     /* elements strictly above the threshold           */
+  int fallback;
+} fc_worker_stats;
+
+typedef struct fc_ctx fc_ctx;
+
+/* ---- status / library ---------------------------------------------------- */
+const char* fc_status_string(int status);
+const char* fc_last_error(void);
+int fc_abi_version(void);
+/* number of kernel launches since library load (all contexts) */
+uint64_t fc_launch_count(void);
+
+/* ---- sizing helpers (host) ------------------------------------------------ */
+/* k = clamp(ceil(c*G - 1e-9), 1, G)                     inc/compress.hpp:28-33 */
+int fc_k_of(double c, uint64_t grad_len, uint64_t* k_out);
+/* round-robin selection: step % n                       inc/artopk.hpp:27-30   */
+int fc_select_star(long step, int n, int* rank_out);
+
+/* ---- lifetime -------------------------------------------------------------- */
+/* ncclGetUniqueId; rank 0 calls it and ships the bytes to the other ranks.  */
+int fc_get_unique_id(unsigned char uid_out[FC_NCCL_UID_BYTES]);
+/* Loopback (nccl_uid == NULL): n_local logical workers on one device; the
+ * collectives are in-HBM with the reference's rank-ascending order, so the
+ * results are bit-identical to the fp32 oracle (the analogue of the
+ * reference's in-process Cluster, inc/collectives.hpp:15-33).
+ * NCCL (nccl_uid != NULL): one worker per context, world ranks; one
+ * Ring-forced and one Tree-forced communicator are created. */
+int fc_create(fc_ctx** out, const fc_opts* opts);
+int fc_destroy(fc_ctx* ctx);
+int fc_num_workers(const fc_ctx* ctx, int* n_local, int* world, int* rank);
+
+/* ---- state I/O (mirrors std::vector<DenseGrad> g_o and ResidualStore) ------ */
+/* worker is a LOCAL index in [0, n_local); out of range => FC_ERR_OUT_OF_RANGE
+ * (ResidualStore::of uses vector::at, inc/core.hpp:91). */
+int fc_set_grad(fc_ctx* ctx, int worker, const float* src, int memkind);
+int fc_grad_ptr(fc_ctx* ctx, int worker, float** dev_ptr);
+int fc_fill_synthetic(fc_ctx* ctx, int worker, uint64_t seed, uint32_t rank, uint64_t step,
+                      int dist);
+int fc_set_residual(fc_ctx* ctx, int worker, const float* src, int memkind);
+int fc_get_residual(fc_ctx* ctx, int worker, float* dst, int memkind);
+int fc_residual_ptr(fc_ctx* ctx, int worker, float** dev_ptr);
+int fc_reset_residuals(fc_ctx* ctx);
+/* dense aggregate of the last step (identical on every worker) */
+int fc_get_aggregate(fc_ctx* ctx, float* dst, int memkind);
+int fc_aggregate_ptr(fc_ctx* ctx, float** dev_ptr);
+/* last top-k computed for a worker: ascending indices and their values.
+ * idx/val may be NULL to query k only. */
+int fc_get_topk(fc_ctx* ctx, int worker, uint32_t* idx, float* val, uint64_t* k_out);
+int fc_get_worker_stats(fc_ctx* ctx, int worker, fc_worker_stats* out);
+/* checkpoint-restore of the residual store for the MOO controller's explore
+ * (Trainer::snapshot/restore, inc/trainer.hpp:160-190; moo.hpp:205,232) */
+int fc_snapshot(fc_ctx* ctx);
+int fc_restore(fc_ctx* ctx);
+
+/* ---- the hot path ---------------------------------------------------------- */
+/* AR-Top-k step (Alg. 1).  Replaces flexcomm::artopk_step, inc/artopk.hpp:62.
+ * mode FC_STAR|FC_VAR, algo FC_RING|FC_TREE, op FC_SUM|FC_AVG.
+ * Per worker: g_e = g_o + residual (in place in the residual store), exact
+ * top-k of |g_e| (ties -> lower index); the selected worker's index set is
+ * broadcast; each worker gathers g_e at those indices and zeroes its
+ * residual there; the k values are allreduced; the dense aggregate is
+ * decoded.  selected rank in stats->selected_rank (stats may be NULL). */
+int fc_artopk_step(fc_ctx* ctx, double cr, int mode, int algo, long step, int op,
+                   fc_step_stats* stats);
+/* AG-Top-k step.  Replaces flexcomm::ag_step, inc/artopk.hpp:128 (Exact
+ * compressor).  Per worker EF + top-k + residual_update; allgather of the
+ * (index,value) pairs; rank-ordered scatter-add; every element divided by N. */
+int fc_ag_step(fc_ctx* ctx, double cr, int compressor, fc_step_stats* stats);
+/* Dense baseline: allreduce of g_o, inc/trainer.hpp:240-244 */
+int fc_dense_step(fc_ctx* ctx, int algo, int op, fc_step_stats* stats);
+/* Stand-alone exact top-k of a worker's gradient buffer (no error feedback);
+ * replaces flexcomm::topk_exact, inc/compress.hpp:57.  Read with fc_get_topk. */
+int fc_topk_exact(fc_ctx* ctx, int worker, double cr, fc_step_stats* stats);
+
+/* ---- host cost model (inc/costmodel.hpp, kept unchanged) ------------------ */
+/* NetParams{alpha s, bandwidth bit/s} x MessageSpec{m_bytes, c, n}.
+ * out8 = CostBreakdown in declaration order: ps, ring_ar, tree_ar, broadcast,
+ * allgather_dense, ag_compressed, art_ring, art_tree (costmodel.hpp:42-52). */
+int fc_cost_primitives(double alpha, double bandwidth, double m_bytes, double c, int n,
+                       double* out8);
+/* select_collective, costmodel.hpp:153-167: choice 0 AG, 1 ART_RING, 2 ART_TREE */
+int fc_select_collective(double alpha, double bandwidth, double m_bytes, double c, int n,
+                         int* choice, double* costs8);
+/* prefer_ring_over_tree / _ring_over_ag / _tree_over_ag (which = 0/1/2),
+ * costmodel.hpp:124-146 */
+int fc_prefer(double alpha, double bandwidth, double m_bytes, double c, int n, int which,
+              int* out);
+/* crossover_cr, costmodel.hpp:180-203 (pair 0 ring/tree, 1 ring/AG, 2 tree/AG) */
+int fc_crossover_cr(double alpha, double bandwidth, double m_bytes, int n, int pair,
+                    double* c_out, int* has);
+/* derive_m_from_ag, costmodel.hpp:171-175 */
+int fc_derive_m_from_ag(double alpha, double bandwidth, double c, int n, double seconds,
+                        double* m_out);
+
+/* Synchronize the context stream (for FC_FLAG_ASYNC users). */
+int fc_sync(fc_ctx* ctx);
+/* The context's CUDA stream (cudaStream_t), so callers can record their own
+ * CUDA events around steps on the stream the kernels run on. */
+int fc_stream(fc_ctx* ctx, void** stream_out);
+/* Device time of the last N kernels named by the phase (diagnostics): the
+ * library keeps CUDA-event timings of its dominant kernel (error feedback)
+ * for the roofline computation in bench.py.  Returns mean ms per launch
+ * since the last reset and the number of launches timed. */
+int fc_ef_kernel_timing(fc_ctx* ctx, double* mean_ms, uint64_t* launches, int reset);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FLEXCOMM_B200_H_ */

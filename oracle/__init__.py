@@ -1,0 +1,267 @@
+"""ORACLE — test infrastructure only.
+
+Python access to the CPU checkers:
+  * ``F32``  — liboracle_f32.so, the fp32 restatement of the reference hot path
+  * ``Ref``  — _ref/libflexcomm_ref.so, the UNMODIFIED reference headers
+               (/root/reference/proj/include) behind a C shim
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline
+leg may import this package, and only as the checker / the timed CPU
+baseline.  The product path (``paper_2312_02493_b200``) never imports it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+F32_LIB = HERE / "liboracle_f32.so"
+REF_LIB = HERE / "_ref" / "libflexcomm_ref.so"
+REF_INCLUDE = Path("/root/reference/proj/include")
+
+
+def build() -> None:
+    """Compile the restatement and, when /root/reference exists, the reference shim."""
+    res = subprocess.run(["make", "-s", "-C", str(HERE)], capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("oracle build failed:\n" + res.stdout + res.stderr)
+
+
+def _f32p(a):
+    return a.ctypes.data_as(C.POINTER(C.c_float))
+
+
+def _u32p(a):
+    return a.ctypes.data_as(C.POINTER(C.c_uint32))
+
+
+def _f64p(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+class F32:
+    """fp32 restatement (oracle/oracle_f32.cpp)."""
+
+    def __init__(self):
+        if not F32_LIB.exists():
+            build()
+        lib = C.CDLL(str(F32_LIB))
+        u64, d, i, P = C.c_uint64, C.c_double, C.c_int, C.c_void_p
+        lib.orc_k_of.argtypes, lib.orc_k_of.restype = [d, u64], u64
+        lib.orc_topk_exact.argtypes, lib.orc_topk_exact.restype = [P, u64, d, P, P], u64
+        lib.orc_squared_norm.argtypes, lib.orc_squared_norm.restype = [P, u64], d
+        lib.orc_artopk_step.argtypes = [i, u64, P, P, d, i, C.c_long, i, P, P, P, P]
+        lib.orc_artopk_step.restype = u64
+        lib.orc_ag_step.argtypes, lib.orc_ag_step.restype = [i, u64, P, P, d, P], u64
+        lib.orc_dense.argtypes, lib.orc_dense.restype = [i, u64, P, i, P], None
+        lib.orc_fill_synth.argtypes, lib.orc_fill_synth.restype = [P, u64, u64, C.c_uint32, u64, i], None
+        self.lib = lib
+
+    def k_of(self, c, g):
+        return int(self.lib.orc_k_of(c, g))
+
+    def synth(self, g, seed, rank, step, dist=0):
+        out = np.empty(g, dtype=np.float32)
+        self.lib.orc_fill_synth(out.ctypes.data, g, seed, rank, step, dist)
+        return out
+
+    def topk_exact(self, v, c):
+        v = np.ascontiguousarray(v, dtype=np.float32)
+        k = self.k_of(c, v.size)
+        idx = np.empty(k, dtype=np.uint32)
+        val = np.empty(k, dtype=np.float32)
+        self.lib.orc_topk_exact(v.ctypes.data, v.size, c, idx.ctypes.data, val.ctypes.data)
+        return idx, val
+
+    def squared_norm(self, v):
+        v = np.ascontiguousarray(v, dtype=np.float32)
+        return float(self.lib.orc_squared_norm(v.ctypes.data, v.size))
+
+    def artopk_step(self, g_o, res, c, mode, step, op=1):
+        """g_o, res: (n, G) float32; res is updated in place."""
+        n, g = g_o.shape
+        g_o = np.ascontiguousarray(g_o, dtype=np.float32)
+        assert res.dtype == np.float32 and res.flags.c_contiguous
+        k = self.k_of(c, g)
+        agg = np.empty(g, dtype=np.float32)
+        sel = C.c_int()
+        bidx = np.empty(k, dtype=np.uint32)
+        norms = np.empty(n, dtype=np.float64)
+        r = self.lib.orc_artopk_step(n, g, g_o.ctypes.data, res.ctypes.data, c, mode, step, op,
+                                     agg.ctypes.data, C.addressof(sel), bidx.ctypes.data,
+                                     norms.ctypes.data)
+        if r == 0:
+            raise ValueError("oracle rejected arguments")
+        return agg, sel.value, bidx, norms
+
+    def ag_step(self, g_o, res, c):
+        n, g = g_o.shape
+        g_o = np.ascontiguousarray(g_o, dtype=np.float32)
+        agg = np.empty(g, dtype=np.float32)
+        if self.lib.orc_ag_step(n, g, g_o.ctypes.data, res.ctypes.data, c, agg.ctypes.data) == 0:
+            raise ValueError("oracle rejected arguments")
+        return agg
+
+    def dense(self, g_o, op=1):
+        n, g = g_o.shape
+        g_o = np.ascontiguousarray(g_o, dtype=np.float32)
+        agg = np.empty(g, dtype=np.float32)
+        self.lib.orc_dense(n, g, g_o.ctypes.data, op, agg.ctypes.data)
+        return agg
+
+
+class Ref:
+    """The unmodified reference (oracle/_ref/libflexcomm_ref.so), fp64."""
+
+    def __init__(self):
+        if not REF_LIB.exists():
+            if REF_INCLUDE.exists():
+                build()
+            if not REF_LIB.exists():
+                raise FileNotFoundError(f"{REF_LIB} not built (needs /root/reference once)")
+        lib = C.CDLL(str(REF_LIB))
+        u64, d, i, P, L = C.c_uint64, C.c_double, C.c_int, C.c_void_p, C.c_long
+        lib.ref_k_of.argtypes, lib.ref_k_of.restype = [d, u64, P], i
+        lib.ref_topk_exact.argtypes, lib.ref_topk_exact.restype = [P, u64, d, P, P, P], i
+        lib.ref_artopk_step.argtypes = [i, u64, P, P, d, i, i, L, i, d, d, d, P, P, P]
+        lib.ref_artopk_step.restype = i
+        lib.ref_ag_step.argtypes = [i, u64, P, P, d, d, d, d, P, P]
+        lib.ref_ag_step.restype = i
+        lib.ref_select_collective.argtypes = [d, d, d, d, i, P, P]
+        lib.ref_select_collective.restype = i
+        lib.ref_crossover_cr.argtypes, lib.ref_crossover_cr.restype = [d, d, d, i, i, P, P], i
+        lib.ref_candidate_ladder.argtypes, lib.ref_candidate_ladder.restype = [d, d, d, P, i], i
+        lib.ref_choose_cr.argtypes = [P, i, d, d, d, i, P, P, P]
+        lib.ref_choose_cr.restype = i
+        lib.ref_state_create.argtypes, lib.ref_state_create.restype = [i, u64], P
+        lib.ref_state_destroy.argtypes, lib.ref_state_destroy.restype = [P], None
+        lib.ref_state_fill_synth.argtypes = [P, i, u64, C.c_uint32, u64, i]
+        lib.ref_state_fill_synth.restype = None
+        lib.ref_state_step.argtypes, lib.ref_state_step.restype = [P, d, i, i, L], d
+        lib.ref_state_selected.argtypes, lib.ref_state_selected.restype = [P], i
+        lib.ref_state_aggregate.argtypes, lib.ref_state_aggregate.restype = [P, P], None
+        lib.ref_state_residual.argtypes, lib.ref_state_residual.restype = [P, i, P], None
+        self.lib = lib
+
+    def k_of(self, c, g):
+        k = C.c_uint64()
+        rc = self.lib.ref_k_of(c, g, C.addressof(k))
+        if rc:
+            raise ValueError(f"reference raised (code {rc})")
+        return k.value
+
+    def topk_exact(self, v, c):
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        kmax = max(1, v.size)
+        idx = np.empty(kmax, dtype=np.uint64)
+        val = np.empty(kmax, dtype=np.float64)
+        k = C.c_uint64()
+        rc = self.lib.ref_topk_exact(v.ctypes.data, v.size, c, idx.ctypes.data, val.ctypes.data,
+                                     C.addressof(k))
+        if rc:
+            raise ValueError(f"reference raised (code {rc})")
+        return idx[: k.value].copy(), val[: k.value].copy()
+
+    def artopk_step(self, g_o, res, c, mode, algo, step, op=1, payload_scale=1.0,
+                    alpha=0.001, bandwidth=1e9):
+        n, g = g_o.shape
+        g_o = np.ascontiguousarray(g_o, dtype=np.float64)
+        assert res.dtype == np.float64 and res.flags.c_contiguous
+        agg = np.empty(g, dtype=np.float64)
+        sel, charge = C.c_int(), C.c_double()
+        rc = self.lib.ref_artopk_step(n, g, g_o.ctypes.data, res.ctypes.data, c, mode, algo, step,
+                                      op, payload_scale, alpha, bandwidth, agg.ctypes.data,
+                                      C.addressof(sel), C.addressof(charge))
+        if rc:
+            raise ValueError(f"reference raised (code {rc})")
+        return agg, sel.value, charge.value
+
+    def ag_step(self, g_o, res, c, payload_scale=1.0, alpha=0.001, bandwidth=1e9):
+        n, g = g_o.shape
+        g_o = np.ascontiguousarray(g_o, dtype=np.float64)
+        agg = np.empty(g, dtype=np.float64)
+        charge = C.c_double()
+        rc = self.lib.ref_ag_step(n, g, g_o.ctypes.data, res.ctypes.data, c, payload_scale, alpha,
+                                  bandwidth, agg.ctypes.data, C.addressof(charge))
+        if rc:
+            raise ValueError(f"reference raised (code {rc})")
+        return agg, charge.value
+
+    def select_collective(self, alpha, bandwidth, m_bytes, c, n):
+        ch = C.c_int()
+        costs = np.empty(8, dtype=np.float64)
+        rc = self.lib.ref_select_collective(alpha, bandwidth, m_bytes, c, n, C.addressof(ch),
+                                            costs.ctypes.data)
+        if rc:
+            raise ValueError(f"reference raised (code {rc})")
+        return ch.value, costs
+
+    def crossover_cr(self, alpha, bandwidth, m_bytes, n, pair):
+        c, has = C.c_double(), C.c_int()
+        rc = self.lib.ref_crossover_cr(alpha, bandwidth, m_bytes, n, pair, C.addressof(c),
+                                       C.addressof(has))
+        if rc:
+            raise ValueError(f"reference raised (code {rc})")
+        return c.value if has.value else None
+
+    def candidate_ladder(self, c_low=0.001, c_high=0.1, factor=3.0):
+        out = np.empty(64, dtype=np.float64)
+        m = self.lib.ref_candidate_ladder(c_low, c_high, factor, out.ctypes.data, 64)
+        if m < 0:
+            raise ValueError("reference raised")
+        return list(out[:m])
+
+    def choose_cr(self, rows, alpha, bandwidth, m_bytes, n):
+        rows = np.ascontiguousarray(rows, dtype=np.float64)
+        m = rows.shape[0]
+        mask = np.zeros(m, dtype=np.int32)
+        chosen, coll = C.c_double(), C.c_int()
+        rc = self.lib.ref_choose_cr(rows.ctypes.data, m, alpha, bandwidth, m_bytes, n,
+                                    mask.ctypes.data, C.addressof(chosen), C.addressof(coll))
+        if rc:
+            raise ValueError(f"reference raised (code {rc})")
+        return mask.astype(bool), chosen.value, coll.value
+
+
+class RefState:
+    """Persistent reference state for timing the CPU baseline (bench.py)."""
+
+    def __init__(self, ref: Ref, n: int, g: int):
+        self.ref, self.n, self.g = ref, n, g
+        self.p = ref.lib.ref_state_create(n, g)
+        if not self.p:
+            raise MemoryError("reference state allocation failed")
+
+    def fill_synth(self, worker, seed, rank, step, dist=0):
+        self.ref.lib.ref_state_fill_synth(self.p, worker, seed, rank, step, dist)
+
+    def step(self, c, mode, algo, step):
+        """mode 0 STAR, 1 VAR, 2 AG.  Returns seconds inside the reference call."""
+        t = self.ref.lib.ref_state_step(self.p, c, mode, algo, step)
+        if t < 0:
+            raise RuntimeError("reference step raised")
+        return t
+
+    def selected(self):
+        return self.ref.lib.ref_state_selected(self.p)
+
+    def aggregate(self):
+        out = np.empty(self.g, dtype=np.float64)
+        self.ref.lib.ref_state_aggregate(self.p, out.ctypes.data)
+        return out
+
+    def residual(self, worker):
+        out = np.empty(self.g, dtype=np.float64)
+        self.ref.lib.ref_state_residual(self.p, worker, out.ctypes.data)
+        return out
+
+    def close(self):
+        if self.p:
+            self.ref.lib.ref_state_destroy(self.p)
+            self.p = None
+
+    def __del__(self):
+        self.close()

@@ -1,0 +1,177 @@
+"""ctypes binding of the C-ABI in include/flexcomm_b200.h.
+
+Loads the in-tree ``libfc_b200.so``.  There is no fallback: if the library
+is missing or cannot be loaded, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libfc_b200.so"
+
+FC_OK = 0
+FC_ERR_INVALID_ARGUMENT = 1
+FC_ERR_OUT_OF_RANGE = 2
+FC_ERR_RUNTIME = 3
+FC_ERR_CUDA = 4
+FC_ERR_NCCL = 5
+FC_ERR_NO_DEVICE = 6
+
+FC_STAR, FC_VAR = 0, 1
+FC_RING, FC_TREE = 0, 1
+FC_SUM, FC_AVG = 0, 1
+FC_EXACT, FC_LAYERWISE, FC_THRESHOLD = 0, 1, 2
+FC_HOST, FC_DEVICE = 0, 1
+FC_FLAG_ASYNC = 0x1
+FC_FLAG_NO_TIMING = 0x2
+FC_NCCL_UID_BYTES = 128
+FC_DIST_NORMAL, FC_DIST_TIES, FC_DIST_LAYERED = 0, 1, 2
+
+
+class fc_opts(C.Structure):
+    _fields_ = [
+        ("device", C.c_int),
+        ("n_local", C.c_int),
+        ("world", C.c_int),
+        ("rank", C.c_int),
+        ("nccl_uid", C.c_void_p),
+        ("grad_len", C.c_uint64),
+        ("max_cr", C.c_double),
+        ("flags", C.c_uint),
+    ]
+
+
+class fc_step_stats(C.Structure):
+    _fields_ = [
+        ("selected_rank", C.c_int),
+        ("collective", C.c_int),
+        ("k", C.c_uint64),
+        ("ms_total", C.c_float),
+        ("ms_ef", C.c_float),
+        ("ms_select", C.c_float),
+        ("ms_exchange", C.c_float),
+        ("ms_decode", C.c_float),
+        ("hbm_bytes", C.c_double),
+        ("bus_bytes", C.c_double),
+        ("launches", C.c_uint64),
+        ("fallback", C.c_int),
+    ]
+
+
+class fc_worker_stats(C.Structure):
+    _fields_ = [
+        ("ge_norm2", C.c_double),
+        ("kept_norm2", C.c_double),
+        ("topk_norm2", C.c_double),
+        ("threshold_key", C.c_uint32),
+        ("candidates", C.c_uint64),
+        ("count_above", C.c_uint64),
+        ("fallback", C.c_int),
+    ]
+
+
+def _load() -> C.CDLL:
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(the B200 path has no CPU fallback)"
+        )
+    lib = C.CDLL(str(LIB_PATH))
+    P = C.c_void_p
+    i, u64, d, f = C.c_int, C.c_uint64, C.c_double, C.c_float
+    sigs = {
+        "fc_status_string": ([i], C.c_char_p),
+        "fc_last_error": ([], C.c_char_p),
+        "fc_abi_version": ([], i),
+        "fc_launch_count": ([], u64),
+        "fc_k_of": ([d, u64, C.POINTER(u64)], i),
+        "fc_select_star": ([C.c_long, i, C.POINTER(i)], i),
+        "fc_get_unique_id": ([C.c_char_p], i),
+        "fc_create": ([C.POINTER(P), C.POINTER(fc_opts)], i),
+        "fc_destroy": ([P], i),
+        "fc_num_workers": ([P, C.POINTER(i), C.POINTER(i), C.POINTER(i)], i),
+        "fc_set_grad": ([P, i, P, i], i),
+        "fc_grad_ptr": ([P, i, C.POINTER(P)], i),
+        "fc_fill_synthetic": ([P, i, u64, C.c_uint32, u64, i], i),
+        "fc_set_residual": ([P, i, P, i], i),
+        "fc_get_residual": ([P, i, P, i], i),
+        "fc_residual_ptr": ([P, i, C.POINTER(P)], i),
+        "fc_reset_residuals": ([P], i),
+        "fc_get_aggregate": ([P, P, i], i),
+        "fc_aggregate_ptr": ([P, C.POINTER(P)], i),
+        "fc_get_topk": ([P, i, P, P, C.POINTER(u64)], i),
+        "fc_get_worker_stats": ([P, i, C.POINTER(fc_worker_stats)], i),
+        "fc_snapshot": ([P], i),
+        "fc_restore": ([P], i),
+        "fc_artopk_step": ([P, d, i, i, C.c_long, i, C.POINTER(fc_step_stats)], i),
+        "fc_ag_step": ([P, d, i, C.POINTER(fc_step_stats)], i),
+        "fc_dense_step": ([P, i, i, C.POINTER(fc_step_stats)], i),
+        "fc_topk_exact": ([P, i, d, C.POINTER(fc_step_stats)], i),
+        "fc_sync": ([P], i),
+        "fc_stream": ([P, C.POINTER(P)], i),
+        "fc_ef_kernel_timing": ([P, C.POINTER(d), C.POINTER(u64), i], i),
+        # host cost model (csrc/fc_costmodel.cpp)
+        "fc_cost_primitives": ([d, d, d, d, i, C.POINTER(d)], i),
+        "fc_select_collective": ([d, d, d, d, i, C.POINTER(i), C.POINTER(d)], i),
+        "fc_prefer": ([d, d, d, d, i, i, C.POINTER(i)], i),
+        "fc_crossover_cr": ([d, d, d, i, i, C.POINTER(d), C.POINTER(i)], i),
+        "fc_derive_m_from_ag": ([d, d, d, i, d, C.POINTER(d)], i),
+    }
+    for name, (args, res) in sigs.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    return lib
+
+
+lib = _load()
+
+# Exported symbols the header declares (checked by tests/test_abi.py).
+EXPORTS = [
+    "fc_status_string", "fc_last_error", "fc_abi_version", "fc_launch_count", "fc_k_of",
+    "fc_select_star", "fc_get_unique_id", "fc_create", "fc_destroy", "fc_num_workers",
+    "fc_set_grad", "fc_grad_ptr", "fc_fill_synthetic", "fc_set_residual", "fc_get_residual",
+    "fc_residual_ptr", "fc_reset_residuals", "fc_get_aggregate", "fc_aggregate_ptr",
+    "fc_get_topk", "fc_get_worker_stats", "fc_snapshot", "fc_restore", "fc_artopk_step",
+    "fc_ag_step", "fc_dense_step", "fc_topk_exact", "fc_sync", "fc_stream", "fc_ef_kernel_timing",
+    "fc_cost_primitives", "fc_select_collective", "fc_prefer", "fc_crossover_cr",
+    "fc_derive_m_from_ag",
+]
+
+
+class FlexcommError(RuntimeError):
+    """Base of the errors raised from C-ABI status codes."""
+
+
+class InvalidArgument(FlexcommError, ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class OutOfRange(FlexcommError, IndexError):
+    """std::out_of_range in the reference."""
+
+
+class RuntimeFailure(FlexcommError):
+    """std::runtime_error in the reference (and CUDA / NCCL failures)."""
+
+
+class NoDevice(FlexcommError):
+    """No sm_100 device: the path never falls back to the CPU."""
+
+
+_ERRS = {
+    FC_ERR_INVALID_ARGUMENT: InvalidArgument,
+    FC_ERR_OUT_OF_RANGE: OutOfRange,
+    FC_ERR_RUNTIME: RuntimeFailure,
+    FC_ERR_CUDA: RuntimeFailure,
+    FC_ERR_NCCL: RuntimeFailure,
+    FC_ERR_NO_DEVICE: NoDevice,
+}
+
+
+def check(status: int) -> None:
+    if status != FC_OK:
+        msg = lib.fc_last_error().decode(errors="replace")
+        raise _ERRS.get(status, FlexcommError)(f"{lib.fc_status_string(status).decode()}: {msg}")

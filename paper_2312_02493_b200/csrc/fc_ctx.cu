@@ -1,0 +1,771 @@
+// fc_ctx.cu — host side of the C-ABI (include/flexcomm_b200.h).
+//
+// Orchestrates one step of the reference protocol over the kernels in
+// fc_kernels.cu and NCCL:
+//   artopk_step  inc/artopk.hpp:62-111   -> fc_artopk_step
+//   ag_step      inc/artopk.hpp:128-161  -> fc_ag_step
+//   Dense sync   inc/trainer.hpp:240-244 -> fc_dense_step
+//   topk_exact   inc/compress.hpp:57-65  -> fc_topk_exact
+// Loopback contexts hold all N logical workers on one device and perform the
+// collectives in HBM with the reference's rank-ascending order; NCCL contexts
+// hold one worker per process (one GPU each) and use a Ring-forced and a
+// Tree-forced communicator (ReduceAlgo, inc/collectives.hpp:36).
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "fc_device.cuh"
+#include "fc_synth.h"
+#include "flexcomm_b200.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(x)                                                                        \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess) return fail(FC_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+#define NCCL_TRY(x)                                                                        \
+  do {                                                                                     \
+    ncclResult_t r_ = (x);                                                                 \
+    if (r_ != ncclSuccess) return fail(FC_ERR_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+#define LAUNCHED() CUDA_TRY(cudaGetLastError())
+
+uint64_t k_of_host(double c, uint64_t g) {
+  // inc/compress.hpp:28-33 verbatim semantics: clamp(ceil(c*G - 1e-9), 1, G)
+  const double raw = std::ceil(c * static_cast<double>(g) - 1e-9);
+  uint64_t k = raw <= 0.0 ? 0 : static_cast<uint64_t>(raw);
+  return std::min<uint64_t>(std::max<uint64_t>(k, 1), g);
+}
+
+bool cr_valid(double c) { return c > 0.0 && c <= 1.0; }
+
+struct Worker {
+  float* g_o = nullptr;
+  float* ge = nullptr;  // the residual store; holds g_e between EF and gather
+  float* snap = nullptr;
+  fcb::Ctl* ctl = nullptr;
+  fcb::TileWs ws{};
+  unsigned* pack = nullptr;  // [idx k | val k], capacity 2*kmax
+  float* contrib = nullptr;  // capacity kmax
+  bool has_topk = false;
+  uint64_t topk_k = 0;
+};
+
+}  // namespace
+
+struct fc_ctx {
+  int device = 0, n_local = 1, world = 1, rank = 0;
+  uint64_t G = 0, gstride = 0, kmax = 0, ntd = 0;  // gstride: per-worker stride (256 B aligned)
+  unsigned flags = 0;
+  bool nccl = false;
+  ncclComm_t comm_ring = nullptr, comm_tree = nullptr;
+  cudaStream_t stream = nullptr;
+  std::vector<Worker> w;
+  std::vector<void*> allocs;
+  float* g_o_all = nullptr;
+  float* ge_all = nullptr;
+  float* agg = nullptr;
+  unsigned* pack_all = nullptr;
+  float* contrib_all = nullptr;
+  float* reduced = nullptr;
+  unsigned* bidx = nullptr;
+  unsigned* ag_recv = nullptr;
+  unsigned* bounds = nullptr;
+  double* dnorms = nullptr;
+  double* h_norms = nullptr;  // pinned
+  bool has_agg = false;
+  // phase events
+  cudaEvent_t ev[5] = {};
+  bool timing = false;
+  // EF-kernel timing (dominant kernel, for the roofline)
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ef_pending;
+  std::vector<cudaEvent_t> ev_pool;
+  double ef_ms_sum = 0.0;
+  uint64_t ef_n = 0;
+
+  template <typename T>
+  int alloc(T** p, uint64_t count) {
+    void* q = nullptr;
+    CUDA_TRY(cudaMalloc(&q, std::max<uint64_t>(count, 1) * sizeof(T)));
+    allocs.push_back(q);
+    *p = static_cast<T*>(q);
+    return FC_OK;
+  }
+  cudaEvent_t take_event() {
+    if (!ev_pool.empty()) {
+      cudaEvent_t e = ev_pool.back();
+      ev_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+
+namespace {
+
+#define TRY(x)                 \
+  do {                         \
+    int s_ = (x);              \
+    if (s_ != FC_OK) return s_; \
+  } while (0)
+
+int check_worker(const fc_ctx* c, int worker) {
+  if (!c) return fail(FC_ERR_INVALID_ARGUMENT, "null context");
+  if (worker < 0 || worker >= c->n_local) return fail(FC_ERR_OUT_OF_RANGE, "worker index out of range");
+  return FC_OK;
+}
+
+int copy_in(fc_ctx* c, float* dst, const float* src, int memkind) {
+  if (!src) return fail(FC_ERR_INVALID_ARGUMENT, "null source pointer");
+  CUDA_TRY(cudaMemcpyAsync(dst, src, c->G * sizeof(float),
+                           memkind == FC_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                           c->stream));
+  if (!(c->flags & FC_FLAG_ASYNC) || memkind != FC_DEVICE) CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return FC_OK;
+}
+
+int copy_out(fc_ctx* c, float* dst, const float* src, uint64_t n, int memkind) {
+  if (!dst) return fail(FC_ERR_INVALID_ARGUMENT, "null destination pointer");
+  CUDA_TRY(cudaMemcpyAsync(dst, src, n * sizeof(float),
+                           memkind == FC_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                           c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return FC_OK;
+}
+
+void record(fc_ctx* c, int i) {
+  if (c->timing) cudaEventRecord(c->ev[i], c->stream);
+}
+
+// EF + (optionally) candidate emission for worker i; times the EF kernel of
+// local worker 0 (the dominant kernel) for the roofline.
+int run_ef(fc_ctx* c, int i, uint64_t k, bool topk) {
+  Worker& w = c->w[i];
+  const bool force_fb = std::getenv("FC_FORCE_FALLBACK") != nullptr;
+  CUDA_TRY(cudaMemsetAsync(w.ctl, 0, sizeof(fcb::Ctl), c->stream));
+  if (topk) {
+    fcb::launch_sample(w.g_o, w.ge, c->G, k, w.ctl, 1, force_fb ? 1 : 0, c->stream);
+    LAUNCHED();
+  }
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (i == 0 && c->timing) {
+    e0 = c->take_event();
+    e1 = c->take_event();
+    cudaEventRecord(e0, c->stream);
+  }
+  fcb::launch_ef(w.g_o, w.ge, c->G, k, w.ctl, w.ws, 1, topk ? 1 : 0, c->stream);
+  LAUNCHED();
+  if (e0) {
+    cudaEventRecord(e1, c->stream);
+    c->ef_pending.emplace_back(e0, e1);
+  }
+  if (topk) {
+    fcb::launch_fallback(w.ge, c->G, k, w.ctl, w.ws, c->stream);
+    LAUNCHED();
+  }
+  return FC_OK;
+}
+
+int run_select(fc_ctx* c, int i, uint64_t k, bool zero_own) {
+  Worker& w = c->w[i];
+  fcb::launch_refine(k, w.ctl, w.ws, c->stream);
+  LAUNCHED();
+  fcb::launch_emit(w.ctl, w.ws, w.pack, reinterpret_cast<float*>(w.pack + k), w.ge, zero_own ? 1 : 0,
+                   c->stream);
+  LAUNCHED();
+  w.has_topk = true;
+  w.topk_k = k;
+  return FC_OK;
+}
+
+// Folds completed EF-kernel event pairs into the running mean (events are
+// recycled, so long runs do not accumulate them).
+int drain_ef_events(fc_ctx* c) {
+  for (auto& pr : c->ef_pending) {
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, pr.first, pr.second));
+    c->ef_ms_sum += ms;
+    c->ef_n += 1;
+    c->ev_pool.push_back(pr.first);
+    c->ev_pool.push_back(pr.second);
+  }
+  c->ef_pending.clear();
+  return FC_OK;
+}
+
+int finish_step(fc_ctx* c, fc_step_stats* st, uint64_t k, int sel, int coll, double hbm, double bus,
+                uint64_t launches0) {
+  if (!st) {
+    if (!(c->flags & FC_FLAG_ASYNC)) {
+      CUDA_TRY(cudaStreamSynchronize(c->stream));
+      TRY(drain_ef_events(c));
+    }
+    return FC_OK;
+  }
+  std::memset(st, 0, sizeof(*st));
+  st->selected_rank = sel;
+  st->collective = coll;
+  st->k = k;
+  st->hbm_bytes = hbm;
+  st->bus_bytes = bus;
+  st->launches = fcb::launches() - launches0;
+  if (c->flags & FC_FLAG_ASYNC) return FC_OK;
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  TRY(drain_ef_events(c));
+  if (c->timing) {
+    float a = 0, b = 0, d = 0, e = 0, t = 0;
+    cudaEventElapsedTime(&a, c->ev[0], c->ev[1]);
+    cudaEventElapsedTime(&b, c->ev[1], c->ev[2]);
+    cudaEventElapsedTime(&d, c->ev[2], c->ev[3]);
+    cudaEventElapsedTime(&e, c->ev[3], c->ev[4]);
+    cudaEventElapsedTime(&t, c->ev[0], c->ev[4]);
+    st->ms_ef = a;
+    st->ms_select = b;
+    st->ms_exchange = d;
+    st->ms_decode = e;
+    st->ms_total = t;
+  }
+  for (int i = 0; i < c->n_local; ++i) {
+    unsigned fb = 0;
+    CUDA_TRY(cudaMemcpy(&fb, &c->w[i].ctl->fallback, sizeof(fb), cudaMemcpyDeviceToHost));
+    st->fallback |= fb ? 1 : 0;
+  }
+  return FC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fc_status_string(int status) {
+  switch (status) {
+    case FC_OK: return "ok";
+    case FC_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case FC_ERR_OUT_OF_RANGE: return "out of range";
+    case FC_ERR_RUNTIME: return "runtime error";
+    case FC_ERR_CUDA: return "CUDA error";
+    case FC_ERR_NCCL: return "NCCL error";
+    case FC_ERR_NO_DEVICE: return "no CUDA device";
+  }
+  return "unknown status";
+}
+
+const char* fc_last_error(void) { return g_err.c_str(); }
+int fc_abi_version(void) { return FC_ABI_VERSION; }
+uint64_t fc_launch_count(void) { return fcb::launches(); }
+
+int fc_k_of(double c, uint64_t grad_len, uint64_t* k_out) {
+  if (!cr_valid(c)) return fail(FC_ERR_INVALID_ARGUMENT, "compression ratio must be in (0, 1]");
+  if (grad_len == 0) return fail(FC_ERR_INVALID_ARGUMENT, "empty gradient (G == 0)");
+  if (!k_out) return fail(FC_ERR_INVALID_ARGUMENT, "null output");
+  *k_out = k_of_host(c, grad_len);
+  return FC_OK;
+}
+
+int fc_select_star(long step, int n, int* rank_out) {
+  if (n < 1) return fail(FC_ERR_INVALID_ARGUMENT, "worker count must be >= 1");
+  if (!rank_out) return fail(FC_ERR_INVALID_ARGUMENT, "null output");
+  *rank_out = static_cast<int>(step % n);
+  return FC_OK;
+}
+
+int fc_get_unique_id(unsigned char uid_out[FC_NCCL_UID_BYTES]) {
+  static_assert(sizeof(ncclUniqueId) == FC_NCCL_UID_BYTES, "nccl uid size");
+  ncclUniqueId id;
+  NCCL_TRY(ncclGetUniqueId(&id));
+  std::memcpy(uid_out, &id, sizeof(id));
+  return FC_OK;
+}
+
+static int create_impl(fc_ctx* c, const fc_opts* o) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(FC_ERR_NO_DEVICE, "no CUDA device visible (the B200 path has no CPU fallback)");
+  if (o->device < 0 || o->device >= ndev) return fail(FC_ERR_INVALID_ARGUMENT, "bad device ordinal");
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, o->device));
+  if (prop.major != 10) return fail(FC_ERR_NO_DEVICE, "device is not sm_100 (B200)");
+  if (o->grad_len == 0) return fail(FC_ERR_INVALID_ARGUMENT, "empty gradient (G == 0)");
+  if (o->grad_len >= (1ull << 31)) return fail(FC_ERR_INVALID_ARGUMENT, "G must be < 2^31");
+  if (o->n_local < 1) return fail(FC_ERR_INVALID_ARGUMENT, "worker count must be >= 1");
+  c->device = o->device;
+  c->G = o->grad_len;
+  c->flags = o->flags;
+  c->timing = !(o->flags & FC_FLAG_NO_TIMING);
+  c->nccl = o->nccl_uid != nullptr;
+  c->n_local = o->n_local;
+  if (c->nccl) {
+    if (o->n_local != 1) return fail(FC_ERR_INVALID_ARGUMENT, "NCCL contexts hold one worker");
+    if (o->world < 1 || o->rank < 0 || o->rank >= o->world)
+      return fail(FC_ERR_INVALID_ARGUMENT, "bad world/rank");
+    c->world = o->world;
+    c->rank = o->rank;
+  } else {
+    c->world = o->n_local;
+    c->rank = 0;
+  }
+  const double max_cr = o->max_cr > 0.0 ? o->max_cr : 1.0;
+  if (!cr_valid(max_cr)) return fail(FC_ERR_INVALID_ARGUMENT, "max_cr must be in (0, 1]");
+  c->kmax = k_of_host(max_cr, c->G);
+  c->ntd = (c->G + fcb::kDecTile - 1) >> fcb::kDecShift;
+
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
+
+  const uint64_t G = c->G, N = c->n_local;
+  c->gstride = (G + 63) & ~uint64_t(63);
+  const uint64_t GS = c->gstride;
+  const unsigned ntiles = (unsigned)((G + fcb::kTile - 1) >> fcb::kTileShift);
+  const unsigned ef_grid = (unsigned)fcb::ef_grid_size();
+  TRY(c->alloc(&c->g_o_all, N * GS));
+  TRY(c->alloc(&c->ge_all, N * GS));
+  TRY(c->alloc(&c->agg, G));
+  TRY(c->alloc(&c->pack_all, N * 2 * c->kmax));
+  TRY(c->alloc(&c->contrib_all, N * c->kmax));
+  const uint64_t nl = std::max<uint64_t>(N, (uint64_t)c->world);
+  TRY(c->alloc(&c->bounds, nl * (c->ntd + 1)));
+  if (c->nccl) {
+    TRY(c->alloc(&c->reduced, c->kmax));
+    TRY(c->alloc(&c->bidx, c->kmax));
+    TRY(c->alloc(&c->ag_recv, (uint64_t)c->world * 2 * c->kmax));
+    TRY(c->alloc(&c->dnorms, (uint64_t)c->world));
+  }
+  CUDA_TRY(cudaMallocHost(&c->h_norms, sizeof(double) * std::max(c->world, c->n_local)));
+  CUDA_TRY(cudaMemsetAsync(c->ge_all, 0, N * GS * sizeof(float), c->stream));
+  CUDA_TRY(cudaMemsetAsync(c->g_o_all, 0, N * GS * sizeof(float), c->stream));
+  CUDA_TRY(cudaMemsetAsync(c->agg, 0, G * sizeof(float), c->stream));
+  c->w.resize(N);
+  for (uint64_t i = 0; i < N; ++i) {
+    Worker& w = c->w[i];
+    w.g_o = c->g_o_all + i * GS;
+    w.ge = c->ge_all + i * GS;
+    w.pack = c->pack_all + i * 2 * c->kmax;
+    w.contrib = c->contrib_all + i * c->kmax;
+    TRY(c->alloc(&w.ctl, 1));
+    fcb::TileWs& s = w.ws;
+    s.ntiles = ntiles;
+    s.ef_grid = ef_grid;
+    TRY(c->alloc(&s.off, ntiles));
+    TRY(c->alloc(&s.cnt, ntiles));
+    TRY(c->alloc(&s.gt, ntiles));
+    TRY(c->alloc(&s.eq, ntiles));
+    TRY(c->alloc(&s.out, ntiles));
+    TRY(c->alloc(&s.take, ntiles));
+    TRY(c->alloc(&s.norm, ntiles));
+    TRY(c->alloc(&s.cand_idx, G));
+    TRY(c->alloc(&s.cand_val, G));
+    TRY(c->alloc(&s.ef_part, ef_grid));
+    TRY(c->alloc(&s.g_part, 4096));
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+
+  if (c->nccl) {
+    ncclUniqueId id;
+    std::memcpy(&id, o->nccl_uid, sizeof(id));
+    const bool force = std::getenv("FC_NCCL_NO_FORCE_ALGO") == nullptr;
+    const char* prev = std::getenv("NCCL_ALGO");
+    std::string saved = prev ? prev : "";
+    if (force) setenv("NCCL_ALGO", "Ring", 1);
+    ncclResult_t r = ncclCommInitRank(&c->comm_ring, c->world, id, c->rank);
+    if (r == ncclSuccess) {
+      if (force) setenv("NCCL_ALGO", "Tree", 1);
+      r = ncclCommSplit(c->comm_ring, 0, c->rank, &c->comm_tree, nullptr);
+    }
+    if (force) {
+      if (prev) setenv("NCCL_ALGO", saved.c_str(), 1);
+      else unsetenv("NCCL_ALGO");
+    }
+    NCCL_TRY(r);
+  }
+  return FC_OK;
+}
+
+int fc_create(fc_ctx** out, const fc_opts* opts) {
+  if (!out || !opts) return fail(FC_ERR_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  fc_ctx* c = new fc_ctx();
+  const int s = create_impl(c, opts);
+  if (s != FC_OK) {
+    std::string msg = g_err;
+    fc_destroy(c);
+    g_err = msg;
+    return s;
+  }
+  *out = c;
+  return FC_OK;
+}
+
+int fc_destroy(fc_ctx* c) {
+  if (!c) return FC_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->comm_tree) ncclCommDestroy(c->comm_tree);
+  if (c->comm_ring) ncclCommDestroy(c->comm_ring);
+  for (void* p : c->allocs) cudaFree(p);
+  for (auto& w : c->w)
+    if (w.snap) cudaFree(w.snap);
+  if (c->h_norms) cudaFreeHost(c->h_norms);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& pr : c->ef_pending) {
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return FC_OK;
+}
+
+int fc_num_workers(const fc_ctx* c, int* n_local, int* world, int* rank) {
+  if (!c) return fail(FC_ERR_INVALID_ARGUMENT, "null context");
+  if (n_local) *n_local = c->n_local;
+  if (world) *world = c->world;
+  if (rank) *rank = c->rank;
+  return FC_OK;
+}
+
+int fc_set_grad(fc_ctx* c, int worker, const float* src, int memkind) {
+  TRY(check_worker(c, worker));
+  CUDA_TRY(cudaSetDevice(c->device));
+  return copy_in(c, c->w[worker].g_o, src, memkind);
+}
+
+int fc_grad_ptr(fc_ctx* c, int worker, float** p) {
+  TRY(check_worker(c, worker));
+  if (!p) return fail(FC_ERR_INVALID_ARGUMENT, "null output");
+  *p = c->w[worker].g_o;
+  return FC_OK;
+}
+
+int fc_fill_synthetic(fc_ctx* c, int worker, uint64_t seed, uint32_t rank, uint64_t step, int dist) {
+  TRY(check_worker(c, worker));
+  if (dist < FC_DIST_NORMAL || dist > FC_DIST_LAYERED) return fail(FC_ERR_INVALID_ARGUMENT, "bad distribution");
+  CUDA_TRY(cudaSetDevice(c->device));
+  fcb::launch_fill_synth(c->w[worker].g_o, c->G, fc_stream_key(seed, rank, step), dist, c->stream);
+  LAUNCHED();
+  if (!(c->flags & FC_FLAG_ASYNC)) CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return FC_OK;
+}
+
+int fc_set_residual(fc_ctx* c, int worker, const float* src, int memkind) {
+  TRY(check_worker(c, worker));
+  CUDA_TRY(cudaSetDevice(c->device));
+  return copy_in(c, c->w[worker].ge, src, memkind);
+}
+
+int fc_get_residual(fc_ctx* c, int worker, float* dst, int memkind) {
+  TRY(check_worker(c, worker));
+  CUDA_TRY(cudaSetDevice(c->device));
+  return copy_out(c, dst, c->w[worker].ge, c->G, memkind);
+}
+
+int fc_residual_ptr(fc_ctx* c, int worker, float** p) {
+  TRY(check_worker(c, worker));
+  if (!p) return fail(FC_ERR_INVALID_ARGUMENT, "null output");
+  *p = c->w[worker].ge;
+  return FC_OK;
+}
+
+int fc_reset_residuals(fc_ctx* c) {
+  if (!c) return fail(FC_ERR_INVALID_ARGUMENT, "null context");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaMemsetAsync(c->ge_all, 0, (uint64_t)c->n_local * c->gstride * sizeof(float), c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return FC_OK;
+}
+
+int fc_get_aggregate(fc_ctx* c, float* dst, int memkind) {
+  if (!c) return fail(FC_ERR_INVALID_ARGUMENT, "null context");
+  CUDA_TRY(cudaSetDevice(c->device));
+  return copy_out(c, dst, c->agg, c->G, memkind);
+}
+
+int fc_aggregate_ptr(fc_ctx* c, float** p) {
+  if (!c || !p) return fail(FC_ERR_INVALID_ARGUMENT, "null argument");
+  *p = c->agg;
+  return FC_OK;
+}
+
+int fc_get_topk(fc_ctx* c, int worker, uint32_t* idx, float* val, uint64_t* k_out) {
+  TRY(check_worker(c, worker));
+  const Worker& w = c->w[worker];
+  if (!w.has_topk) return fail(FC_ERR_RUNTIME, "no top-k was computed for this worker in the last step");
+  if (k_out) *k_out = w.topk_k;
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (idx) CUDA_TRY(cudaMemcpy(idx, w.pack, w.topk_k * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  if (val) CUDA_TRY(cudaMemcpy(val, w.pack + w.topk_k, w.topk_k * sizeof(float), cudaMemcpyDeviceToHost));
+  return FC_OK;
+}
+
+int fc_get_worker_stats(fc_ctx* c, int worker, fc_worker_stats* out) {
+  TRY(check_worker(c, worker));
+  if (!out) return fail(FC_ERR_INVALID_ARGUMENT, "null output");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  fcb::Ctl h;
+  CUDA_TRY(cudaMemcpy(&h, c->w[worker].ctl, offsetof(fcb::Ctl, hist_s), cudaMemcpyDeviceToHost));
+  out->ge_norm2 = h.ge_norm2;
+  out->kept_norm2 = h.kept_norm2;
+  out->topk_norm2 = h.topk_norm2;
+  out->threshold_key = h.T;
+  out->candidates = h.cand_count;
+  out->count_above = h.count_gt;
+  out->fallback = h.fallback ? 1 : 0;
+  return FC_OK;
+}
+
+int fc_snapshot(fc_ctx* c) {
+  if (!c) return fail(FC_ERR_INVALID_ARGUMENT, "null context");
+  CUDA_TRY(cudaSetDevice(c->device));
+  for (auto& w : c->w) {
+    if (!w.snap) CUDA_TRY(cudaMalloc(&w.snap, c->G * sizeof(float)));
+    CUDA_TRY(cudaMemcpyAsync(w.snap, w.ge, c->G * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return FC_OK;
+}
+
+int fc_restore(fc_ctx* c) {
+  if (!c) return fail(FC_ERR_INVALID_ARGUMENT, "null context");
+  CUDA_TRY(cudaSetDevice(c->device));
+  for (auto& w : c->w) {
+    if (!w.snap) return fail(FC_ERR_RUNTIME, "restore without snapshot");
+    CUDA_TRY(cudaMemcpyAsync(w.ge, w.snap, c->G * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return FC_OK;
+}
+
+int fc_sync(fc_ctx* c) {
+  if (!c) return fail(FC_ERR_INVALID_ARGUMENT, "null context");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return FC_OK;
+}
+
+int fc_stream(fc_ctx* c, void** stream_out) {
+  if (!c || !stream_out) return fail(FC_ERR_INVALID_ARGUMENT, "null argument");
+  *stream_out = c->stream;
+  return FC_OK;
+}
+
+int fc_ef_kernel_timing(fc_ctx* c, double* mean_ms, uint64_t* launches, int reset) {
+  if (!c) return fail(FC_ERR_INVALID_ARGUMENT, "null context");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  TRY(drain_ef_events(c));
+  if (mean_ms) *mean_ms = c->ef_n ? c->ef_ms_sum / (double)c->ef_n : 0.0;
+  if (launches) *launches = c->ef_n;
+  if (reset) {
+    c->ef_ms_sum = 0.0;
+    c->ef_n = 0;
+  }
+  return FC_OK;
+}
+
+// ------------------------------------------------------------ hot path -----
+
+int fc_topk_exact(fc_ctx* c, int worker, double cr, fc_step_stats* st) {
+  TRY(check_worker(c, worker));
+  if (!cr_valid(cr)) return fail(FC_ERR_INVALID_ARGUMENT, "compression ratio must be in (0, 1]");
+  const uint64_t k = k_of_host(cr, c->G);
+  if (k > c->kmax) return fail(FC_ERR_INVALID_ARGUMENT, "compression ratio above the context's max_cr");
+  CUDA_TRY(cudaSetDevice(c->device));
+  const uint64_t l0 = fcb::launches();
+  Worker& w = c->w[worker];
+  const bool force_fb = std::getenv("FC_FORCE_FALLBACK") != nullptr;
+  record(c, 0);
+  CUDA_TRY(cudaMemsetAsync(w.ctl, 0, sizeof(fcb::Ctl), c->stream));
+  fcb::launch_sample(nullptr, w.g_o, c->G, k, w.ctl, 0, force_fb ? 1 : 0, c->stream);
+  fcb::launch_ef(nullptr, w.g_o, c->G, k, w.ctl, w.ws, 0, 1, c->stream);
+  fcb::launch_fallback(w.g_o, c->G, k, w.ctl, w.ws, c->stream);
+  LAUNCHED();
+  record(c, 1);
+  fcb::launch_refine(k, w.ctl, w.ws, c->stream);
+  fcb::launch_emit(w.ctl, w.ws, w.pack, reinterpret_cast<float*>(w.pack + k), nullptr, 0, c->stream);
+  LAUNCHED();
+  w.has_topk = true;
+  w.topk_k = k;
+  record(c, 2);
+  record(c, 3);
+  record(c, 4);
+  return finish_step(c, st, k, -1, -1, 4.0 * c->G + 16.0 * k, 0.0, l0);
+}
+
+int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, fc_step_stats* st) {
+  if (!c) return fail(FC_ERR_INVALID_ARGUMENT, "null context");
+  if (!cr_valid(cr)) return fail(FC_ERR_INVALID_ARGUMENT, "compression ratio must be in (0, 1]");
+  if (mode != FC_STAR && mode != FC_VAR) return fail(FC_ERR_INVALID_ARGUMENT, "unknown selection mode");
+  if (algo != FC_RING && algo != FC_TREE) return fail(FC_ERR_INVALID_ARGUMENT, "unknown reduce algo");
+  if (op != FC_SUM && op != FC_AVG) return fail(FC_ERR_INVALID_ARGUMENT, "unknown reduce op");
+  const uint64_t k = k_of_host(cr, c->G);
+  if (k > c->kmax) return fail(FC_ERR_INVALID_ARGUMENT, "compression ratio above the context's max_cr");
+  const int N = c->world;
+  int sel = -1;
+  if (mode == FC_STAR) {
+    sel = static_cast<int>(step % N);  // select_star, inc/artopk.hpp:27-30
+    if (sel < 0) return fail(FC_ERR_INVALID_ARGUMENT, "broadcast: bad source rank");
+  }
+  CUDA_TRY(cudaSetDevice(c->device));
+  const uint64_t l0 = fcb::launches();
+  for (auto& w : c->w) w.has_topk = false;
+
+  // (1) error feedback on every worker; Top-k where its result is consumed
+  record(c, 0);
+  for (int i = 0; i < c->n_local; ++i) {
+    const bool topk = mode == FC_VAR || (c->rank + i) == sel;
+    TRY(run_ef(c, i, k, topk));
+  }
+  record(c, 1);
+  for (int i = 0; i < c->n_local; ++i) {
+    const bool topk = mode == FC_VAR || (c->rank + i) == sel;
+    if (topk) TRY(run_select(c, i, k, false));
+  }
+  record(c, 2);
+
+  // (2) VAR: allgather of N ||top-k||^2, argmax, ties -> lowest rank
+  //     (select_var, inc/artopk.hpp:35-48)
+  if (mode == FC_VAR) {
+    if (c->nccl) {
+      NCCL_TRY(ncclAllGather(&c->w[0].ctl->topk_norm2, c->dnorms, 1, ncclFloat64, c->comm_ring,
+                             c->stream));
+      CUDA_TRY(cudaMemcpyAsync(c->h_norms, c->dnorms, sizeof(double) * N, cudaMemcpyDeviceToHost,
+                               c->stream));
+    } else {
+      for (int i = 0; i < N; ++i)
+        CUDA_TRY(cudaMemcpyAsync(c->h_norms + i, &c->w[i].ctl->topk_norm2, sizeof(double),
+                                 cudaMemcpyDeviceToHost, c->stream));
+    }
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    sel = 0;
+    for (int r = 1; r < N; ++r)
+      if (c->h_norms[r] > c->h_norms[sel]) sel = r;
+  }
+
+  // (3) broadcast of the selected index set, gather + residual zeroing,
+  //     allreduce of the k values (artopk.hpp:87-104)
+  const unsigned* bsrc = nullptr;
+  if (c->nccl) {
+    NCCL_TRY(ncclBroadcast(c->w[0].pack, c->bidx, k, ncclUint32, sel, c->comm_ring, c->stream));
+    bsrc = c->bidx;
+  } else {
+    bsrc = c->w[sel].pack;
+  }
+  for (int i = 0; i < c->n_local; ++i) {
+    Worker& w = c->w[i];
+    fcb::launch_gather_zero(bsrc, k, w.ge, w.contrib, w.ctl, w.ws.g_part, c->stream);
+    LAUNCHED();
+  }
+  if (c->nccl) {
+    NCCL_TRY(ncclAllReduce(c->w[0].contrib, c->reduced, k, ncclFloat32, ncclSum,
+                           algo == FC_TREE ? c->comm_tree : c->comm_ring, c->stream));
+  }
+  record(c, 3);
+
+  // (4) densify (core.hpp:72-81); /N for Avg (collectives.hpp:85-87)
+  fcb::launch_tile_bounds(bsrc, k, 0, 1, c->G, c->bounds, c->stream);
+  if (c->nccl)
+    fcb::launch_decode_ar(bsrc, c->bounds, c->reduced, 1, 0, op == FC_AVG, (float)N, c->agg, c->G,
+                          c->stream);
+  else
+    fcb::launch_decode_ar(bsrc, c->bounds, c->contrib_all, N, c->kmax, op == FC_AVG, (float)N,
+                          c->agg, c->G, c->stream);
+  LAUNCHED();
+  record(c, 4);
+  c->has_agg = true;
+
+  const double nl = c->n_local;
+  const double hbm = nl * 12.0 * c->G + 4.0 * c->G + 32.0 * k * (mode == FC_VAR ? nl : 1.0) +
+                     (mode == FC_VAR ? 8.0 * N : 0.0);
+  const double bus = N > 1 ? 4.0 * k + 2.0 * (N - 1) / N * 4.0 * k + (mode == FC_VAR ? 8.0 * (N - 1) : 0.0)
+                           : 0.0;
+  return finish_step(c, st, k, sel, algo == FC_TREE ? 2 : 1, hbm, bus, l0);
+}
+
+int fc_ag_step(fc_ctx* c, double cr, int compressor, fc_step_stats* st) {
+  if (!c) return fail(FC_ERR_INVALID_ARGUMENT, "null context");
+  if (!cr_valid(cr)) return fail(FC_ERR_INVALID_ARGUMENT, "compression ratio must be in (0, 1]");
+  if (compressor != FC_EXACT)
+    return fail(FC_ERR_INVALID_ARGUMENT, "only the Exact compressor is implemented on B200");
+  const uint64_t k = k_of_host(cr, c->G);
+  if (k > c->kmax) return fail(FC_ERR_INVALID_ARGUMENT, "compression ratio above the context's max_cr");
+  const int N = c->world;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const uint64_t l0 = fcb::launches();
+
+  record(c, 0);
+  for (int i = 0; i < c->n_local; ++i) TRY(run_ef(c, i, k, true));
+  record(c, 1);
+  // residual_update folded into the emission (exact zeros at own indices)
+  for (int i = 0; i < c->n_local; ++i) TRY(run_select(c, i, k, true));
+  record(c, 2);
+
+  const unsigned* packs;
+  uint64_t stride;
+  if (c->nccl) {
+    NCCL_TRY(ncclAllGather(c->w[0].pack, c->ag_recv, 2 * k, ncclUint32, c->comm_ring, c->stream));
+    packs = c->ag_recv;
+    stride = 2 * k;
+  } else {
+    packs = c->pack_all;
+    stride = 2 * c->kmax;
+  }
+  record(c, 3);
+  fcb::launch_tile_bounds(packs, k, stride, N, c->G, c->bounds, c->stream);
+  fcb::launch_decode_ag(packs, stride, k, N, c->bounds, (float)N, c->agg, c->G, c->stream);
+  LAUNCHED();
+  record(c, 4);
+  c->has_agg = true;
+
+  const double nl = c->n_local;
+  const double hbm = nl * (12.0 * c->G + 8.0 * k) + 4.0 * c->G + 12.0 * N * k;
+  const double bus = N > 1 ? (N - 1) * 8.0 * k : 0.0;
+  return finish_step(c, st, k, -1, 0, hbm, bus, l0);
+}
+
+int fc_dense_step(fc_ctx* c, int algo, int op, fc_step_stats* st) {
+  if (!c) return fail(FC_ERR_INVALID_ARGUMENT, "null context");
+  if (algo != FC_RING && algo != FC_TREE) return fail(FC_ERR_INVALID_ARGUMENT, "unknown reduce algo");
+  if (op != FC_SUM && op != FC_AVG) return fail(FC_ERR_INVALID_ARGUMENT, "unknown reduce op");
+  const int N = c->world;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const uint64_t l0 = fcb::launches();
+  record(c, 0);
+  record(c, 1);
+  record(c, 2);
+  if (c->nccl) {
+    NCCL_TRY(ncclAllReduce(c->w[0].g_o, c->agg, c->G, ncclFloat32, ncclSum,
+                           algo == FC_TREE ? c->comm_tree : c->comm_ring, c->stream));
+    record(c, 3);
+    if (op == FC_AVG) fcb::launch_dense_sum(c->agg, 1, 0, 1, (float)N, c->agg, c->G, c->stream);
+  } else {
+    record(c, 3);
+    fcb::launch_dense_sum(c->g_o_all, N, c->gstride, op == FC_AVG, (float)N, c->agg, c->G, c->stream);
+  }
+  LAUNCHED();
+  record(c, 4);
+  c->has_agg = true;
+  const double bus = N > 1 ? 2.0 * (N - 1) / N * 4.0 * c->G : 0.0;
+  return finish_step(c, st, c->G, -1, algo == FC_TREE ? 2 : 1, 12.0 * c->G, bus, l0);
+}
+
+}  // extern "C"
