@@ -267,11 +267,21 @@ def main():
     for s in range(a.warmup):
         step(s)
     barrier()
-    cl.ef_kernel_timing(reset=True)
-    l0 = fc.lib.fc_launch_count()
+    t_w = time.time()
+    for s in range(5):
+        step(a.warmup + s)
+    barrier()
+    per_step = max_over_ranks((time.time() - t_w) / 5)
     clocks = ClockSampler(local)
     clocks.start()
-    time.sleep(0.3)
+    # the timed region is short (K steps of well under a millisecond): keep
+    # the GPU busy with identical steps for ~1.5 s around it so nvidia-smi
+    # sees the clocks under this load (same count on every rank)
+    n_soak = int(min(20_000, max(50, 1.5 / max(per_step, 1e-5))))
+    for s in range(n_soak):
+        step(10_000 + s)
+    cl.ef_kernel_timing(reset=True)
+    l0 = fc.lib.fc_launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     ev0.record(stream)

@@ -217,6 +217,14 @@ int fc_stream(fc_ctx* ctx, void** stream_out);
  * for the roofline computation in bench.py.  Returns mean ms per launch
  * since the last reset and the number of launches timed. */
 int fc_ef_kernel_timing(fc_ctx* ctx, double* mean_ms, uint64_t* launches, int reset);
+/* Diagnostics (roofline calibration, not the hot path): mean device ms of one
+ * kernel on worker 0's buffers.  which: 0/1/2 reference triad b += a at
+ * 3/4/8 blocks per SM, 3 write-only fill, 4 EF, 5 EF + candidate emission,
+ * 6 EF + emission + owed zeros. */
+int fc_diag_kernel_ms(fc_ctx* ctx, int which, int iters, double* ms_out);
+/* Diagnostics: %globaltimer (ns) at the select kernel's phase boundaries of
+ * the last step (start, staged, digit 1/2/3 resolved, counted, emitted, end). */
+int fc_diag_select_phases(fc_ctx* ctx, int worker, uint64_t* out8);
 
 #ifdef __cplusplus
 }

@@ -10,6 +10,11 @@
 // collectives in HBM with the reference's rank-ascending order; NCCL contexts
 // hold one worker per process (one GPU each) and use a Ring-forced and a
 // Tree-forced communicator (ReduceAlgo, inc/collectives.hpp:36).
+//
+// Residual zeroing (artopk.hpp:99-101, compress.hpp:122-130) is recorded as a
+// pending-zero list per worker and applied by the next error-feedback pass;
+// every path that exposes the residual store materialises it first, so the
+// observable state is exactly the reference's.
 #include <nccl.h>
 
 #include <algorithm>
@@ -43,6 +48,11 @@ int fail(int code, const std::string& msg) {
     if (r_ != ncclSuccess) return fail(FC_ERR_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_)); \
   } while (0)
 #define LAUNCHED() CUDA_TRY(cudaGetLastError())
+#define TRY(x)                  \
+  do {                          \
+    int s_ = (x);               \
+    if (s_ != FC_OK) return s_; \
+  } while (0)
 
 uint64_t k_of_host(double c, uint64_t g) {
   // inc/compress.hpp:28-33 verbatim semantics: clamp(ceil(c*G - 1e-9), 1, G)
@@ -53,23 +63,30 @@ uint64_t k_of_host(double c, uint64_t g) {
 
 bool cr_valid(double c) { return c > 0.0 && c <= 1.0; }
 
+uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
 struct Worker {
   float* g_o = nullptr;
   float* ge = nullptr;  // the residual store; holds g_e between EF and gather
   float* snap = nullptr;
   fcb::Ctl* ctl = nullptr;
-  fcb::TileWs ws{};
+  size_t ctl_bytes = 0;     // zeroed per step
+  fcb::ChunkWs ws{};
   unsigned* pack = nullptr;  // [idx k | val k], capacity 2*kmax
   float* contrib = nullptr;  // capacity kmax
   bool has_topk = false;
   uint64_t topk_k = 0;
+  bool kept_is_topk = false;  // gather skipped: kept energy == ||top-k||^2
+  fcb::Pending pz{};          // zeros owed to `ge` (zero map, read by the next EF)
+  const unsigned* pz_idx = nullptr;  // the same zeros as a sorted index list
+  uint64_t pz_k = 0;
 };
 
 }  // namespace
 
 struct fc_ctx {
   int device = 0, n_local = 1, world = 1, rank = 0;
-  uint64_t G = 0, gstride = 0, kmax = 0, ntd = 0;  // gstride: per-worker stride (256 B aligned)
+  uint64_t G = 0, gstride = 0, kmax = 0, nch = 0;  // gstride: per-worker stride (256 B aligned)
   unsigned flags = 0;
   bool nccl = false;
   ncclComm_t comm_ring = nullptr, comm_tree = nullptr;
@@ -84,7 +101,8 @@ struct fc_ctx {
   float* reduced = nullptr;
   unsigned* bidx = nullptr;
   unsigned* ag_recv = nullptr;
-  unsigned* bounds = nullptr;
+  unsigned* bounds = nullptr;  // nlists x (nch + 1)
+  unsigned* zmaps = nullptr;   // n_local x (nch * 32) zero maps
   double* dnorms = nullptr;
   double* h_norms = nullptr;  // pinned
   bool has_agg = false;
@@ -119,12 +137,6 @@ struct fc_ctx {
 
 namespace {
 
-#define TRY(x)                 \
-  do {                         \
-    int s_ = (x);              \
-    if (s_ != FC_OK) return s_; \
-  } while (0)
-
 int check_worker(const fc_ctx* c, int worker) {
   if (!c) return fail(FC_ERR_INVALID_ARGUMENT, "null context");
   if (worker < 0 || worker >= c->n_local) return fail(FC_ERR_OUT_OF_RANGE, "worker index out of range");
@@ -153,14 +165,31 @@ void record(fc_ctx* c, int i) {
   if (c->timing) cudaEventRecord(c->ev[i], c->stream);
 }
 
+// Write the owed zeros now (the residual store is about to be observed).
+int materialize(fc_ctx* c, Worker& w) {
+  if (w.pz_idx && w.pz_k) {
+    fcb::launch_zero_at(w.pz_idx, w.pz_k, w.ge, c->stream);
+    LAUNCHED();
+  }
+  w.pz = fcb::Pending{};
+  w.pz_idx = nullptr;
+  w.pz_k = 0;
+  return FC_OK;
+}
+
+int materialize_all(fc_ctx* c) {
+  for (auto& w : c->w) TRY(materialize(c, w));
+  return FC_OK;
+}
+
 // EF + (optionally) candidate emission for worker i; times the EF kernel of
 // local worker 0 (the dominant kernel) for the roofline.
 int run_ef(fc_ctx* c, int i, uint64_t k, bool topk) {
   Worker& w = c->w[i];
   const bool force_fb = std::getenv("FC_FORCE_FALLBACK") != nullptr;
-  CUDA_TRY(cudaMemsetAsync(w.ctl, 0, sizeof(fcb::Ctl), c->stream));
+  CUDA_TRY(cudaMemsetAsync(w.ctl, 0, w.ctl_bytes, c->stream));
   if (topk) {
-    fcb::launch_sample(w.g_o, w.ge, c->G, k, w.ctl, 1, force_fb ? 1 : 0, c->stream);
+    fcb::launch_sample(w.g_o, w.ge, c->G, k, w.ctl, 1, w.pz, force_fb ? 1 : 0, c->stream);
     LAUNCHED();
   }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -169,8 +198,11 @@ int run_ef(fc_ctx* c, int i, uint64_t k, bool topk) {
     e1 = c->take_event();
     cudaEventRecord(e0, c->stream);
   }
-  fcb::launch_ef(w.g_o, w.ge, c->G, k, w.ctl, w.ws, 1, topk ? 1 : 0, c->stream);
+  fcb::launch_ef(w.g_o, w.ge, c->G, k, w.ctl, w.ws, w.pz, 1, topk ? 1 : 0, c->stream);
   LAUNCHED();
+  w.pz = fcb::Pending{};  // consumed
+  w.pz_idx = nullptr;
+  w.pz_k = 0;
   if (e0) {
     cudaEventRecord(e1, c->stream);
     c->ef_pending.emplace_back(e0, e1);
@@ -182,12 +214,12 @@ int run_ef(fc_ctx* c, int i, uint64_t k, bool topk) {
   return FC_OK;
 }
 
-int run_select(fc_ctx* c, int i, uint64_t k, bool zero_own) {
+int run_select(fc_ctx* c, int i, uint64_t k) {
   Worker& w = c->w[i];
-  fcb::launch_refine(k, w.ctl, w.ws, c->stream);
-  LAUNCHED();
-  fcb::launch_emit(w.ctl, w.ws, w.pack, reinterpret_cast<float*>(w.pack + k), w.ge, zero_own ? 1 : 0,
-                   c->stream);
+  const int e = fcb::launch_select(k, w.ctl, w.ws, w.pack, reinterpret_cast<float*>(w.pack + k),
+                                   c->stream);
+  if (e) return fail(FC_ERR_CUDA, std::string("k_select launch: ") +
+                                      cudaGetErrorString(static_cast<cudaError_t>(e)));
   LAUNCHED();
   w.has_topk = true;
   w.topk_k = k;
@@ -323,16 +355,16 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
   const double max_cr = o->max_cr > 0.0 ? o->max_cr : 1.0;
   if (!cr_valid(max_cr)) return fail(FC_ERR_INVALID_ARGUMENT, "max_cr must be in (0, 1]");
   c->kmax = k_of_host(max_cr, c->G);
-  c->ntd = (c->G + fcb::kDecTile - 1) >> fcb::kDecShift;
+  c->nch = fcb::nchunks_of(c->G);
 
   CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
 
   const uint64_t G = c->G, N = c->n_local;
-  c->gstride = (G + 63) & ~uint64_t(63);
+  c->gstride = align_up(G, 64);
   const uint64_t GS = c->gstride;
-  const unsigned ntiles = (unsigned)((G + fcb::kTile - 1) >> fcb::kTileShift);
+  const unsigned nch = (unsigned)c->nch;
   const unsigned ef_grid = (unsigned)fcb::ef_grid_size();
   TRY(c->alloc(&c->g_o_all, N * GS));
   TRY(c->alloc(&c->ge_all, N * GS));
@@ -340,7 +372,8 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
   TRY(c->alloc(&c->pack_all, N * 2 * c->kmax));
   TRY(c->alloc(&c->contrib_all, N * c->kmax));
   const uint64_t nl = std::max<uint64_t>(N, (uint64_t)c->world);
-  TRY(c->alloc(&c->bounds, nl * (c->ntd + 1)));
+  TRY(c->alloc(&c->bounds, nl * (c->nch + 1)));
+  TRY(c->alloc(&c->zmaps, N * c->nch * 32));
   if (c->nccl) {
     TRY(c->alloc(&c->reduced, c->kmax));
     TRY(c->alloc(&c->bidx, c->kmax));
@@ -358,19 +391,17 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
     w.ge = c->ge_all + i * GS;
     w.pack = c->pack_all + i * 2 * c->kmax;
     w.contrib = c->contrib_all + i * c->kmax;
+    w.ctl_bytes = sizeof(fcb::Ctl);
     TRY(c->alloc(&w.ctl, 1));
-    fcb::TileWs& s = w.ws;
-    s.ntiles = ntiles;
+    fcb::ChunkWs& s = w.ws;
+    s.nchunks = nch;
     s.ef_grid = ef_grid;
-    TRY(c->alloc(&s.off, ntiles));
-    TRY(c->alloc(&s.cnt, ntiles));
-    TRY(c->alloc(&s.gt, ntiles));
-    TRY(c->alloc(&s.eq, ntiles));
-    TRY(c->alloc(&s.out, ntiles));
-    TRY(c->alloc(&s.take, ntiles));
-    TRY(c->alloc(&s.norm, ntiles));
-    TRY(c->alloc(&s.cand_idx, G));
-    TRY(c->alloc(&s.cand_val, G));
+    TRY(c->alloc(&s.off, nch));
+    TRY(c->alloc(&s.cnt, nch));
+    TRY(c->alloc(&s.btot, 4096));
+    TRY(c->alloc(&s.bnorm, 4096));
+    TRY(c->alloc(&s.cand_idx, (uint64_t)nch << fcb::kChunkShift));
+    TRY(c->alloc(&s.cand_val, (uint64_t)nch << fcb::kChunkShift));
     TRY(c->alloc(&s.ef_part, ef_grid));
     TRY(c->alloc(&s.g_part, 4096));
   }
@@ -468,18 +499,26 @@ int fc_fill_synthetic(fc_ctx* c, int worker, uint64_t seed, uint32_t rank, uint6
 int fc_set_residual(fc_ctx* c, int worker, const float* src, int memkind) {
   TRY(check_worker(c, worker));
   CUDA_TRY(cudaSetDevice(c->device));
-  return copy_in(c, c->w[worker].ge, src, memkind);
+  Worker& w = c->w[worker];
+  w.pz = fcb::Pending{};  // overwritten wholesale: owed zeros are void
+  w.pz_idx = nullptr;
+  w.pz_k = 0;
+  return copy_in(c, w.ge, src, memkind);
 }
 
 int fc_get_residual(fc_ctx* c, int worker, float* dst, int memkind) {
   TRY(check_worker(c, worker));
   CUDA_TRY(cudaSetDevice(c->device));
+  TRY(materialize(c, c->w[worker]));
   return copy_out(c, dst, c->w[worker].ge, c->G, memkind);
 }
 
 int fc_residual_ptr(fc_ctx* c, int worker, float** p) {
   TRY(check_worker(c, worker));
   if (!p) return fail(FC_ERR_INVALID_ARGUMENT, "null output");
+  CUDA_TRY(cudaSetDevice(c->device));
+  TRY(materialize(c, c->w[worker]));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
   *p = c->w[worker].ge;
   return FC_OK;
 }
@@ -487,6 +526,11 @@ int fc_residual_ptr(fc_ctx* c, int worker, float** p) {
 int fc_reset_residuals(fc_ctx* c) {
   if (!c) return fail(FC_ERR_INVALID_ARGUMENT, "null context");
   CUDA_TRY(cudaSetDevice(c->device));
+  for (auto& w : c->w) {
+    w.pz = fcb::Pending{};
+    w.pz_idx = nullptr;
+    w.pz_k = 0;
+  }
   CUDA_TRY(cudaMemsetAsync(c->ge_all, 0, (uint64_t)c->n_local * c->gstride * sizeof(float), c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   return FC_OK;
@@ -524,7 +568,7 @@ int fc_get_worker_stats(fc_ctx* c, int worker, fc_worker_stats* out) {
   fcb::Ctl h;
   CUDA_TRY(cudaMemcpy(&h, c->w[worker].ctl, offsetof(fcb::Ctl, hist_s), cudaMemcpyDeviceToHost));
   out->ge_norm2 = h.ge_norm2;
-  out->kept_norm2 = h.kept_norm2;
+  out->kept_norm2 = c->w[worker].kept_is_topk ? h.topk_norm2 : h.kept_norm2;
   out->topk_norm2 = h.topk_norm2;
   out->threshold_key = h.T;
   out->candidates = h.cand_count;
@@ -536,6 +580,7 @@ int fc_get_worker_stats(fc_ctx* c, int worker, fc_worker_stats* out) {
 int fc_snapshot(fc_ctx* c) {
   if (!c) return fail(FC_ERR_INVALID_ARGUMENT, "null context");
   CUDA_TRY(cudaSetDevice(c->device));
+  TRY(materialize_all(c));
   for (auto& w : c->w) {
     if (!w.snap) CUDA_TRY(cudaMalloc(&w.snap, c->G * sizeof(float)));
     CUDA_TRY(cudaMemcpyAsync(w.snap, w.ge, c->G * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
@@ -549,6 +594,9 @@ int fc_restore(fc_ctx* c) {
   CUDA_TRY(cudaSetDevice(c->device));
   for (auto& w : c->w) {
     if (!w.snap) return fail(FC_ERR_RUNTIME, "restore without snapshot");
+    w.pz = fcb::Pending{};
+    w.pz_idx = nullptr;
+    w.pz_k = 0;
     CUDA_TRY(cudaMemcpyAsync(w.ge, w.snap, c->G * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
   }
   CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -582,6 +630,64 @@ int fc_ef_kernel_timing(fc_ctx* c, double* mean_ms, uint64_t* launches, int rese
   return FC_OK;
 }
 
+// Diagnostics: mean device time (CUDA events around each launch) of one
+// kernel of the path, or of a reference streaming kernel, on worker 0's
+// buffers.  Not on the hot path; used for roofline calibration.
+//   0/1/2  triad b += a over G floats, 3/4/8 blocks per SM (EF's access pattern)
+//   3      write-only zero fill of G floats (decode's access pattern)
+//   4      EF, no emission, no owed zeros        5  EF + candidate emission
+//   6      EF + emission + owed zeros (zero map of the last AR/AG step)
+int fc_diag_kernel_ms(fc_ctx* c, int which, int iters, double* ms_out) {
+  if (!c || !ms_out || iters < 1) return fail(FC_ERR_INVALID_ARGUMENT, "bad argument");
+  CUDA_TRY(cudaSetDevice(c->device));
+  TRY(materialize_all(c));
+  Worker& w = c->w[0];
+  const uint64_t k = std::max<uint64_t>(1, c->kmax / 10);
+  cudaEvent_t e0 = c->take_event(), e1 = c->take_event();
+  double sum = 0.0;
+  for (int it = 0; it < iters + 1; ++it) {
+    if (which >= 5) {
+      CUDA_TRY(cudaMemsetAsync(w.ctl, 0, w.ctl_bytes, c->stream));
+      fcb::launch_sample(w.g_o, w.ge, c->G, k, w.ctl, 1, fcb::Pending{}, 0, c->stream);
+    }
+    fcb::Pending pz{};
+    if (which == 6) pz.zmap = c->zmaps;
+    cudaEventRecord(e0, c->stream);
+    switch (which) {
+      case 0: fcb::launch_triad(w.g_o, w.ge, c->G & ~uint64_t(3), 3, c->stream); break;
+      case 1: fcb::launch_triad(w.g_o, w.ge, c->G & ~uint64_t(3), 4, c->stream); break;
+      case 2: fcb::launch_triad(w.g_o, w.ge, c->G & ~uint64_t(3), 8, c->stream); break;
+      case 3: fcb::launch_fill_zero(c->agg, c->G & ~uint64_t(3), 8, c->stream); break;
+      case 4: fcb::launch_ef(w.g_o, w.ge, c->G, k, w.ctl, w.ws, pz, 1, 0, c->stream); break;
+      case 5:
+      case 6: fcb::launch_ef(w.g_o, w.ge, c->G, k, w.ctl, w.ws, pz, 1, 1, c->stream); break;
+      default: return fail(FC_ERR_INVALID_ARGUMENT, "unknown diagnostic kernel");
+    }
+    LAUNCHED();
+    cudaEventRecord(e1, c->stream);
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (it > 0) sum += ms;  // first launch is a warm-up
+  }
+  c->ev_pool.push_back(e0);
+  c->ev_pool.push_back(e1);
+  *ms_out = sum / iters;
+  return FC_OK;
+}
+
+// Diagnostics: %globaltimer (ns) at k_select's phase boundaries in the last
+// step of `worker` (block 0): start, staged, digit 1/2/3, counted, emitted, end.
+int fc_diag_select_phases(fc_ctx* c, int worker, uint64_t* out8) {
+  TRY(check_worker(c, worker));
+  if (!out8) return fail(FC_ERR_INVALID_ARGUMENT, "null output");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  CUDA_TRY(cudaMemcpy(out8, &c->w[worker].ctl->tphase[0], 8 * sizeof(uint64_t),
+                      cudaMemcpyDeviceToHost));
+  return FC_OK;
+}
+
 // ------------------------------------------------------------ hot path -----
 
 int fc_topk_exact(fc_ctx* c, int worker, double cr, fc_step_stats* st) {
@@ -590,21 +696,19 @@ int fc_topk_exact(fc_ctx* c, int worker, double cr, fc_step_stats* st) {
   const uint64_t k = k_of_host(cr, c->G);
   if (k > c->kmax) return fail(FC_ERR_INVALID_ARGUMENT, "compression ratio above the context's max_cr");
   CUDA_TRY(cudaSetDevice(c->device));
+  // the packs are about to be rewritten: settle any zeros that reference them
+  TRY(materialize_all(c));
   const uint64_t l0 = fcb::launches();
   Worker& w = c->w[worker];
   const bool force_fb = std::getenv("FC_FORCE_FALLBACK") != nullptr;
   record(c, 0);
-  CUDA_TRY(cudaMemsetAsync(w.ctl, 0, sizeof(fcb::Ctl), c->stream));
-  fcb::launch_sample(nullptr, w.g_o, c->G, k, w.ctl, 0, force_fb ? 1 : 0, c->stream);
-  fcb::launch_ef(nullptr, w.g_o, c->G, k, w.ctl, w.ws, 0, 1, c->stream);
+  CUDA_TRY(cudaMemsetAsync(w.ctl, 0, w.ctl_bytes, c->stream));
+  fcb::launch_sample(nullptr, w.g_o, c->G, k, w.ctl, 0, fcb::Pending{}, force_fb ? 1 : 0, c->stream);
+  fcb::launch_ef(nullptr, w.g_o, c->G, k, w.ctl, w.ws, fcb::Pending{}, 0, 1, c->stream);
   fcb::launch_fallback(w.g_o, c->G, k, w.ctl, w.ws, c->stream);
   LAUNCHED();
   record(c, 1);
-  fcb::launch_refine(k, w.ctl, w.ws, c->stream);
-  fcb::launch_emit(w.ctl, w.ws, w.pack, reinterpret_cast<float*>(w.pack + k), nullptr, 0, c->stream);
-  LAUNCHED();
-  w.has_topk = true;
-  w.topk_k = k;
+  TRY(run_select(c, worker, k));
   record(c, 2);
   record(c, 3);
   record(c, 4);
@@ -627,7 +731,10 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
   }
   CUDA_TRY(cudaSetDevice(c->device));
   const uint64_t l0 = fcb::launches();
-  for (auto& w : c->w) w.has_topk = false;
+  for (auto& w : c->w) {
+    w.has_topk = false;
+    w.kept_is_topk = false;
+  }
 
   // (1) error feedback on every worker; Top-k where its result is consumed
   record(c, 0);
@@ -638,7 +745,7 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
   record(c, 1);
   for (int i = 0; i < c->n_local; ++i) {
     const bool topk = mode == FC_VAR || (c->rank + i) == sel;
-    if (topk) TRY(run_select(c, i, k, false));
+    if (topk) TRY(run_select(c, i, k));
   }
   record(c, 2);
 
@@ -661,37 +768,51 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
       if (c->h_norms[r] > c->h_norms[sel]) sel = r;
   }
 
-  // (3) broadcast of the selected index set, gather + residual zeroing,
-  //     allreduce of the k values (artopk.hpp:87-104)
+  // (3) broadcast of the selected index set, gather, allreduce of the k
+  //     values (artopk.hpp:87-104); the zeros at bidx become owed zeros
   const unsigned* bsrc = nullptr;
+  const float* contrib0 = nullptr;
   if (c->nccl) {
-    NCCL_TRY(ncclBroadcast(c->w[0].pack, c->bidx, k, ncclUint32, sel, c->comm_ring, c->stream));
+    Worker& w = c->w[0];
+    NCCL_TRY(ncclBroadcast(w.pack, c->bidx, k, ncclUint32, sel, c->comm_ring, c->stream));
     bsrc = c->bidx;
+    if (c->rank == sel) {
+      // the selected worker's contribution is its own top-k values
+      contrib0 = reinterpret_cast<const float*>(w.pack + k);
+      w.kept_is_topk = true;
+    } else {
+      fcb::launch_gather(bsrc, k, w.ge, w.contrib, w.ctl, w.ws.g_part, c->stream);
+      LAUNCHED();
+      contrib0 = w.contrib;
+    }
+    NCCL_TRY(ncclAllReduce(contrib0, c->reduced, k, ncclFloat32, ncclSum,
+                           algo == FC_TREE ? c->comm_tree : c->comm_ring, c->stream));
   } else {
     bsrc = c->w[sel].pack;
-  }
-  for (int i = 0; i < c->n_local; ++i) {
-    Worker& w = c->w[i];
-    fcb::launch_gather_zero(bsrc, k, w.ge, w.contrib, w.ctl, w.ws.g_part, c->stream);
-    LAUNCHED();
-  }
-  if (c->nccl) {
-    NCCL_TRY(ncclAllReduce(c->w[0].contrib, c->reduced, k, ncclFloat32, ncclSum,
-                           algo == FC_TREE ? c->comm_tree : c->comm_ring, c->stream));
+    for (int i = 0; i < c->n_local; ++i) {
+      Worker& w = c->w[i];
+      fcb::launch_gather(bsrc, k, w.ge, w.contrib, w.ctl, w.ws.g_part, c->stream);
+      LAUNCHED();
+    }
   }
   record(c, 3);
 
   // (4) densify (core.hpp:72-81); /N for Avg (collectives.hpp:85-87)
-  fcb::launch_tile_bounds(bsrc, k, 0, 1, c->G, c->bounds, c->stream);
+  fcb::launch_bounds(bsrc, k, 0, 1, c->G, c->bounds, c->stream);
   if (c->nccl)
     fcb::launch_decode_ar(bsrc, c->bounds, c->reduced, 1, 0, op == FC_AVG, (float)N, c->agg, c->G,
-                          c->stream);
+                          c->zmaps, c->stream);
   else
     fcb::launch_decode_ar(bsrc, c->bounds, c->contrib_all, N, c->kmax, op == FC_AVG, (float)N,
-                          c->agg, c->G, c->stream);
+                          c->agg, c->G, c->zmaps, c->stream);
   LAUNCHED();
   record(c, 4);
   c->has_agg = true;
+  for (auto& w : c->w) {  // every worker owes zeros at the broadcast indices
+    w.pz.zmap = c->zmaps;
+    w.pz_idx = bsrc;
+    w.pz_k = k;
+  }
 
   const double nl = c->n_local;
   const double hbm = nl * 12.0 * c->G + 4.0 * c->G + 32.0 * k * (mode == FC_VAR ? nl : 1.0) +
@@ -715,8 +836,10 @@ int fc_ag_step(fc_ctx* c, double cr, int compressor, fc_step_stats* st) {
   record(c, 0);
   for (int i = 0; i < c->n_local; ++i) TRY(run_ef(c, i, k, true));
   record(c, 1);
-  // residual_update folded into the emission (exact zeros at own indices)
-  for (int i = 0; i < c->n_local; ++i) TRY(run_select(c, i, k, true));
+  for (int i = 0; i < c->n_local; ++i) {
+    TRY(run_select(c, i, k));
+    c->w[i].kept_is_topk = true;
+  }
   record(c, 2);
 
   const unsigned* packs;
@@ -730,11 +853,20 @@ int fc_ag_step(fc_ctx* c, double cr, int compressor, fc_step_stats* st) {
     stride = 2 * c->kmax;
   }
   record(c, 3);
-  fcb::launch_tile_bounds(packs, k, stride, N, c->G, c->bounds, c->stream);
-  fcb::launch_decode_ag(packs, stride, k, N, c->bounds, (float)N, c->agg, c->G, c->stream);
+  fcb::launch_bounds(packs, k, stride, N, c->G, c->bounds, c->stream);
+  fcb::launch_decode_ag(packs, stride, k, N, c->bounds, (float)N, c->agg, c->G, c->zmaps,
+                        c->nccl ? c->rank : 0, c->n_local, c->stream);
   LAUNCHED();
   record(c, 4);
   c->has_agg = true;
+  // residual_update (compress.hpp:122-130): g_e - g_e = +0 at own indices
+  for (int i = 0; i < c->n_local; ++i) {
+    const int r = c->nccl ? c->rank : i;
+    Worker& w = c->w[i];
+    w.pz.zmap = c->zmaps + (uint64_t)i * c->nch * 32;
+    w.pz_idx = packs + (uint64_t)r * stride;
+    w.pz_k = k;
+  }
 
   const double nl = c->n_local;
   const double hbm = nl * (12.0 * c->G + 8.0 * k) + 4.0 * c->G + 12.0 * N * k;

@@ -1,20 +1,26 @@
 // fc_kernels.cu — sm_100a kernels of the Top-k gradient-sync hot path.
 //
 // Reference algorithm (all in /root/reference/proj/include/flexcomm):
-//   error_feedback        compress.hpp:114-120   -> k_ef (fused)
-//   select_topk_indices   compress.hpp:38-53     -> k_sample, k_ef (candidate
-//                                                   emission), k_refine{1,2},
-//                                                   k_tile_count, k_tile_scan,
-//                                                   k_emit
-//   artopk gather/residual artopk.hpp:92-102     -> k_gather_zero
-//   densify               core.hpp:72-81         -> k_tile_bounds + k_decode_ar
-//   ag_step scatter-add   artopk.hpp:151-159     -> k_tile_bounds + k_decode_ag
+//   error_feedback        compress.hpp:114-120   -> k_ef (fused with candidate
+//                                                   emission + the previous
+//                                                   step's residual zeroing)
+//   select_topk_indices   compress.hpp:38-53     -> k_sample, k_ef, k_refine1,
+//                                                   k_refine2, k_emit
+//   artopk gather         artopk.hpp:92-98       -> k_gather
+//   residual zeroing      artopk.hpp:99-101,
+//   residual_update       compress.hpp:122-130   -> Pending zeros, applied by
+//                                                   the next k_ef (k_zero_at
+//                                                   when materialised early)
+//   densify               core.hpp:72-81         -> k_bounds + k_decode_ar
+//   ag_step scatter-add   artopk.hpp:151-159     -> k_bounds + k_decode_ag
 //   allreduce (loopback)  collectives.hpp:82-87  -> summed inside k_decode_ar
 //
 // Everything is HBM-bound integer/fp32 streaming work: no tensor cores.
 // DESIGN.md §4 gives each kernel's algorithmic bytes and roofline.
 #include <atomic>
 #include <cstdio>
+
+#include <cooperative_groups.h>
 
 #include "fc_device.cuh"
 #include "fc_synth.h"
@@ -55,11 +61,16 @@ __device__ __forceinline__ unsigned long long warp_incl_scan(unsigned long long 
   return v;
 }
 
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 // Exclusive block scan; s_warp must hold B/32 + 1 entries.
 template <int B>
 __device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long v,
-                                                              unsigned long long* s_warp,
-                                                              unsigned long long* total) {
+                                                              unsigned long long* s_warp) {
   constexpr int W = B / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned long long inc = warp_incl_scan(v);
@@ -73,7 +84,6 @@ __device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long
   }
   __syncthreads();
   const unsigned long long r = inc - v + s_warp[warp];
-  if (total) *total = s_warp[W];
   __syncthreads();
   return r;
 }
@@ -92,6 +102,14 @@ __device__ __forceinline__ double block_sum(double v, double* s_red) {
   for (int w = 0; w < W; ++w) t += s_red[w];
   __syncthreads();
   return t;
+}
+
+// Fixed-order sum of n doubles written by other blocks (read through L2).
+template <int B>
+__device__ __forceinline__ double block_sum_array(const double* a, unsigned n, double* s_red) {
+  double acc = 0.0;
+  for (unsigned i = threadIdx.x; i < n; i += B) acc += __ldcg(a + i);
+  return block_sum<B>(acc, s_red);
 }
 
 // All blocks call this at their end; true in exactly one (the last) block.
@@ -123,7 +141,7 @@ __device__ bool block_select_top(const unsigned* hist, int nb, unsigned long lon
   unsigned long long sum = 0;
   for (int b = top - 1; b >= bot; --b) sum += __ldcg(hist + b);
   if (threadIdx.x == 0) s_found = 0;
-  const unsigned long long ex = block_excl_scan<B>(sum, s_scan, nullptr);
+  const unsigned long long ex = block_excl_scan<B>(sum, s_scan);
   if (top > bot && ex < target && target <= ex + sum) {
     unsigned long long acc = ex;
     for (int b = top - 1; b >= bot; --b) {
@@ -145,6 +163,11 @@ __device__ bool block_select_top(const unsigned* hist, int nb, unsigned long lon
   return f;
 }
 
+// Is element i owed a zero (bit of the zero map)?
+__device__ __forceinline__ bool pending_has(const Pending& pz, uint64_t i) {
+  return (__ldg(pz.zmap + zmap_word(i)) & zmap_bit(i)) != 0u;
+}
+
 // ------------------------------------------------------------- synthetic ---
 __global__ void k_fill_synth(float* __restrict__ dst, uint64_t G, uint64_t key, int dist) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < G;
@@ -164,13 +187,14 @@ void launch_fill_synth(float* dst, uint64_t G, uint64_t key, int dist, cudaStrea
 __global__ void __launch_bounds__(kThreads) k_sample(const float* __restrict__ g_o,
                                                      const float* __restrict__ ge, uint64_t G,
                                                      uint64_t k, Ctl* __restrict__ ctl, int add,
-                                                     int force_fb) {
+                                                     Pending pz, int force_fb) {
   __shared__ unsigned s_h[kBins1];
   for (int b = threadIdx.x; b < kBins1; b += kThreads) s_h[b] = 0;
   __syncthreads();
   const uint64_t s = blockIdx.x * (uint64_t)kThreads + threadIdx.x;
   const uint64_t i = ((2 * s + 1) * G) / (2ull * kSamples);
   float v = ge[i];
+  if (pz.zmap && pending_has(pz, i)) v = 0.0f;
   if (add) v = g_o[i] + v;
   atomicAdd(&s_h[key_of(v) >> kShift1], 1u);
   __syncthreads();
@@ -192,221 +216,270 @@ __global__ void __launch_bounds__(kThreads) k_sample(const float* __restrict__ g
 }
 
 void launch_sample(const float* g_o, const float* ge, uint64_t G, uint64_t k, Ctl* ctl, int add,
-                   int force_fallback, cudaStream_t s) {
-  k_sample<<<kSampleBlocks, kThreads, 0, s>>>(g_o, ge, G, k, ctl, add, force_fallback);
+                   Pending pz, int force_fallback, cudaStream_t s) {
+  k_sample<<<kSampleBlocks, kThreads, 0, s>>>(g_o, ge, G, k, ctl, add, pz, force_fallback);
   count_launch();
 }
 
 // ---------------------------------------------------------- error feedback ---
-// g_e = g_o + residual, written in place over the residual (12 B/elem), with
-//  - ||g_e||^2 (fp64, fixed block order),
+// g_e = g_o + residual, written in place over the residual (12 B/element):
+//  - kPend: the previous step's residual zeros are applied first (zero-map
+//    bits: residual := +0 there, exactly what the reference's residual holds),
+//  - ||g_e||^2 in fp64 (fixed block order),
 //  - kEmit: every element with key >= L (the sampled bound) is copied, in
-//    index order within its 8192-element tile, to the candidate arrays, and
+//    index order, to its chunk's fixed slot in the candidate arrays and
 //    counted in a 4096-bin histogram of its top 12 key bits.
-// Persistent grid with a static tile schedule (deterministic partials).
-template <bool kAdd, bool kEmit>
-__global__ void __launch_bounds__(kThreads) k_ef(const float* __restrict__ g_o,
-                                                 float* __restrict__ ge, uint64_t G, uint64_t k,
-                                                 Ctl* __restrict__ ctl, TileWs w, int gated) {
+// Loads are decoupled from the per-chunk work: every warp owns a 3-stage
+// ring in shared memory and one lane keeps the next chunks' residual / g_o /
+// zero-map bytes in flight with bulk async copies (cp.async.bulk ...
+// mbarrier::complete_tx, the TMA engine).  Lane l owns the contiguous 32
+// elements [32l, 32l+32) of a chunk (read with an XOR-swizzled LDS.128 order,
+// conflict-free), so lane order is index order: one 32-bit warp scan places
+// the candidates, and g_e goes back to HBM as one 4 KB bulk store from the
+// stage.  One 8-warp block per SM (the rings take ~195 KB).
+constexpr int kEfStages = 3;
+constexpr int kEfWarps = kThreads / 32;
+constexpr unsigned kStageBytes = 2 * kChunk * 4 + 128;  // residual/g_e | g_o | zero-map words
+constexpr unsigned kEfRingBytes = kEfWarps * kEfStages * kStageBytes;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n\t"
+               "cp.async.bulk.commit_group;" ::"l"(gdst),
+               "r"(smem_u32(ssrc)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <bool kAdd, bool kEmit, bool kPend>
+__global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_o,
+                                                    float* __restrict__ ge, uint64_t G, uint64_t k,
+                                                    Ctl* __restrict__ ctl, ChunkWs w, Pending pz,
+                                                    int gated) {
   if (gated && *(volatile unsigned*)&ctl->fallback == 0) return;
-  __shared__ unsigned s_h[kEmit ? kBins1 : 1];
-  __shared__ unsigned long long s_lo[2][kThreads / 32], s_hi[2][kThreads / 32];
-  __shared__ unsigned s_base[2];
+  extern __shared__ __align__(128) unsigned char s_ring[];
   __shared__ double s_red[kThreads / 32];
+  __shared__ __align__(8) unsigned long long s_bar[kEfWarps][kEfStages];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (kEmit)
-    for (int b = tid; b < kBins1; b += kThreads) s_h[b] = 0;
+  const unsigned sw = lane & 7;  // LDS.128 swizzle
+  unsigned char* ring = s_ring + warp * kEfStages * kStageBytes;
+  unsigned ncand = 0;  // candidates emitted by this warp (lane 0)
+  if (lane == 0) {
+    for (int s = 0; s < kEfStages; ++s) mbar_init(&s_bar[warp][s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   const unsigned Lkey = kEmit ? (*(volatile unsigned*)&ctl->L_digit) << kShift1 : 0u;
   __syncthreads();
 
+  const unsigned nchunks = w.nchunks;
+  const unsigned nfull = (unsigned)(G >> kChunkShift);  // chunks fed by TMA
+  const unsigned nw = gridDim.x * kEfWarps;
+  const unsigned cfirst = blockIdx.x * kEfWarps + warp;
+  constexpr unsigned kTx = kChunk * 4 * (kAdd ? 2 : 1) + (kPend ? 128 : 0);
+  auto issue = [&](unsigned it) {  // lane 0 only
+    const unsigned c = cfirst + it * nw;
+    if (c >= nfull) return;
+    const unsigned s = it % kEfStages;
+    unsigned long long* bar = &s_bar[warp][s];
+    unsigned char* st = ring + s * kStageBytes;
+    const uint64_t base = (uint64_t)c << kChunkShift;
+    mbar_expect_tx(bar, kTx);
+    bulk_g2s(st, ge + base, kChunk * 4, bar);
+    if (kAdd) bulk_g2s(st + kChunk * 4, g_o + base, kChunk * 4, bar);
+    if (kPend) bulk_g2s(st + 2 * kChunk * 4, pz.zmap + ((uint64_t)c << 5), 128, bar);
+  };
+  if (lane == 0)
+    for (int s = 0; s < kEfStages; ++s) issue(s);
+  __syncwarp();
+
   double nacc = 0.0;
-  const uint64_t ntiles = (G + kTile - 1) >> kTileShift;
-  int par = 0;
-  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x, par ^= 1) {
-    const uint64_t base = t << kTileShift;
-    float v[kVec * 4];
-    unsigned valid = 0xffffffffu;
-    if (base + kTile <= G) {
-      const float4* go4 = reinterpret_cast<const float4*>(g_o + base);
-      float4* ge4 = reinterpret_cast<float4*>(ge + base);
-      float4 A[kVec], Bv[kVec];
+  for (unsigned it = 0;; ++it) {
+    const unsigned c = cfirst + it * nw;
+    if (c >= nchunks) break;
+    const uint64_t base = (uint64_t)c << kChunkShift;
+    const unsigned s = it % kEfStages;
+    float* sge = reinterpret_cast<float*>(ring + s * kStageBytes);
+    unsigned mask = 0;  // bit p: element base + 32*lane + p is a candidate
+    if (c < nfull) {
+      mbar_wait(&s_bar[warp][s], (it / kEfStages) & 1u);
+      float4* r4 = reinterpret_cast<float4*>(sge) + lane * 8;
+      const float4* a4 = reinterpret_cast<const float4*>(sge + kChunk) + lane * 8;
+      const unsigned zm = kPend ? reinterpret_cast<const unsigned*>(sge + 2 * kChunk)[lane] : 0u;
 #pragma unroll
-      for (int j = 0; j < kVec; ++j) {
-        Bv[j] = __ldcs(ge4 + j * kThreads + tid);
-        if (kAdd) A[j] = __ldcs(go4 + j * kThreads + tid);
-      }
-#pragma unroll
-      for (int j = 0; j < kVec; ++j) {
-        float4 r = Bv[j];
-        if (kAdd) {
-          r.x = A[j].x + r.x;
-          r.y = A[j].y + r.y;
-          r.z = A[j].z + r.z;
-          r.w = A[j].w + r.w;
-          __stcs(ge4 + j * kThreads + tid, r);
+      for (int j = 0; j < 8; ++j) {
+        const unsigned q = (unsigned)j ^ sw;  // float4 q of the lane's run
+        float4 r = r4[q];
+        if (kPend) {
+          const unsigned zq = zm >> (q * 4);
+          if (zq & 1u) r.x = 0.0f;
+          if (zq & 2u) r.y = 0.0f;
+          if (zq & 4u) r.z = 0.0f;
+          if (zq & 8u) r.w = 0.0f;
         }
-        v[4 * j + 0] = r.x;
-        v[4 * j + 1] = r.y;
-        v[4 * j + 2] = r.z;
-        v[4 * j + 3] = r.w;
+        if (kAdd) {
+          const float4 a = a4[q];
+          r.x = __fadd_rn(a.x, r.x);
+          r.y = __fadd_rn(a.y, r.y);
+          r.z = __fadd_rn(a.z, r.z);
+          r.w = __fadd_rn(a.w, r.w);
+          r4[q] = r;  // g_e back into the stage, for the bulk store
+        }
+        float t = r.x * r.x;
+        t = fmaf(r.y, r.y, t);
+        t = fmaf(r.z, r.z, t);
+        t = fmaf(r.w, r.w, t);
+        nacc += (double)t;
+        if (kEmit) {
+          const unsigned m4 = (key_of(r.x) >= Lkey ? 1u : 0u) | (key_of(r.y) >= Lkey ? 2u : 0u) |
+                              (key_of(r.z) >= Lkey ? 4u : 0u) | (key_of(r.w) >= Lkey ? 8u : 0u);
+          mask |= m4 << (q * 4);
+        }
+      }
+      if (kAdd) {
+        fence_proxy_async();  // the stage's generic writes -> async-proxy reads
+        __syncwarp();
+        if (lane == 0) bulk_s2g(ge + base, sge, kChunk * 4);
       }
     } else {
-      valid = 0;
-#pragma unroll
-      for (int j = 0; j < kVec; ++j) {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const uint64_t i = base + (uint64_t)(j * kThreads + tid) * 4 + e;
-          float r = 0.f;
-          if (i < G) {
-            r = ge[i];
-            if (kAdd) {
-              r = g_o[i] + r;
-              ge[i] = r;
-            }
-            valid |= 1u << (j * 4 + e);
+      // the one partial chunk at the end of the gradient: plain loads/stores
+      const unsigned zm = kPend ? __ldg(pz.zmap + ((uint64_t)c << 5) + lane) : 0u;
+      for (int p = 0; p < 32; ++p) {
+        const uint64_t i = base + (uint64_t)lane * 32 + p;
+        float r = 0.f;
+        if (i < G) {
+          r = ge[i];
+          if (kPend && (zm & (1u << p))) r = 0.0f;
+          if (kAdd) {
+            r = __fadd_rn(g_o[i], r);
+            ge[i] = r;
           }
-          v[j * 4 + e] = r;
+          if (kEmit && key_of(r) >= Lkey) mask |= 1u << p;
         }
+        sge[lane * 32 + p] = r;
+        nacc += (double)(r * r);
       }
-    }
-#pragma unroll
-    for (int j = 0; j < kVec; ++j) {
-      float s = v[4 * j] * v[4 * j];
-      s = fmaf(v[4 * j + 1], v[4 * j + 1], s);
-      s = fmaf(v[4 * j + 2], v[4 * j + 2], s);
-      s = fmaf(v[4 * j + 3], v[4 * j + 3], s);
-      nacc += (double)s;
     }
     if (kEmit) {
-      unsigned mask = 0;
+      // lane order == index order: one warp scan places every candidate
+      const unsigned n = __popc(mask);
+      unsigned incl = n;
 #pragma unroll
-      for (int q = 0; q < kVec * 4; ++q) mask |= (key_of(v[q]) >= Lkey ? 1u : 0u) << q;
-      mask &= valid;
-      // Per-slot counts packed as 4 x 16-bit lanes: slots 0-3 in lo, 4-7 in hi.
-      unsigned long long lo = 0, hi = 0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        lo |= (unsigned long long)__popc((mask >> (4 * j)) & 0xFu) << (16 * j);
-        hi |= (unsigned long long)__popc((mask >> (4 * (j + 4))) & 0xFu) << (16 * j);
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned x = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += x;
       }
-      const unsigned long long ilo = warp_incl_scan(lo), ihi = warp_incl_scan(hi);
-      if (lane == 31) {
-        s_lo[par][warp] = ilo;
-        s_hi[par][warp] = ihi;
+      const unsigned run = __shfl_sync(0xffffffffu, incl, 31);
+      if (lane == 0) {
+        w.cnt[c] = run;
+        ncand += run;
       }
-      __syncthreads();
-      unsigned long long wlo = 0, whi = 0, tlo = 0, thi = 0;
-#pragma unroll
-      for (int q = 0; q < kThreads / 32; ++q) {
-        const unsigned long long a = s_lo[par][q], b = s_hi[par][q];
-        if (q < warp) {
-          wlo += a;
-          whi += b;
-        }
-        tlo += a;
-        thi += b;
+      unsigned pos = (c << kChunkShift) + incl - n;
+      const float* my = sge + lane * 32;
+      for (unsigned m = mask; m; m &= m - 1) {
+        const int p = __ffs(m) - 1;
+        const float x = my[p];
+        w.cand_idx[pos] = (unsigned)(base + (uint64_t)lane * 32 + p);
+        w.cand_val[pos] = x;
+        ++pos;
       }
-      const unsigned long long elo = ilo - lo + wlo, ehi = ihi - hi + whi;
-      unsigned sb[kVec];
-      unsigned run = 0;
-#pragma unroll
-      for (int j = 0; j < kVec; ++j) {
-        sb[j] = run;
-        run += (unsigned)(((j < 4 ? tlo : thi) >> (16 * (j & 3))) & 0xFFFFu);
-      }
-      if (tid == 0) {
-        const unsigned cb = run ? atomicAdd(&ctl->cand_count, run) : 0u;
-        s_base[par] = cb;
-        w.off[t] = cb;
-        w.cnt[t] = run;
-      }
-      __syncthreads();
-      if (mask) {
-        const unsigned cb = s_base[par];
-#pragma unroll
-        for (int j = 0; j < kVec; ++j) {
-          const unsigned m4 = (mask >> (4 * j)) & 0xFu;
-          if (!m4) continue;
-          unsigned pos = cb + sb[j] + (unsigned)(((j < 4 ? elo : ehi) >> (16 * (j & 3))) & 0xFFFFu);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            if (m4 & (1u << e)) {
-              const float x = v[4 * j + e];
-              w.cand_idx[pos] = (unsigned)(base + (uint64_t)(j * kThreads + tid) * 4 + e);
-              w.cand_val[pos] = x;
-              atomicAdd(&s_h[key_of(x) >> kShift1], 1u);
-              ++pos;
-            }
-          }
-        }
+    }
+    if (c < nfull) {
+      __syncwarp();  // all lanes done with stage s
+      if (lane == 0) {
+        if (kAdd) bulk_wait_read0();  // the g_e bulk store has read the stage
+        issue(it + kEfStages);
       }
     }
   }
+  if (lane == 0 && kAdd) bulk_wait0();
 
-  if (kEmit) {
-    __syncthreads();
-    for (int b = tid; b < kBins1; b += kThreads)
-      if (s_h[b]) atomicAdd(&ctl->hist1[b], s_h[b]);
-  }
+  if (kEmit && lane == 0 && ncand) atomicAdd(&ctl->cand_count, ncand);
   const double bsum = block_sum<kThreads>(nacc, s_red);
   if (tid == 0) w.ef_part[blockIdx.x] = bsum;
   if (!last_block_done(gated ? &ctl->done_fbe : &ctl->done_ef)) return;
 
-  // ---- last block: ||g_e||^2 and the first radix digit of the threshold ----
+  // ---- last block: ||g_e||^2; a candidate set smaller than k means the
+  // sampled bound missed and the fallback re-emission must run ----
   if (!gated) {
-    double acc = 0.0;
-    for (unsigned i = tid; i < gridDim.x; i += kThreads) acc += __ldcg(w.ef_part + i);
-    const double tot = block_sum<kThreads>(acc, s_red);
+    const double tot = block_sum_array<kThreads>(w.ef_part, gridDim.x, s_red);
     if (tid == 0) ctl->ge_norm2 = tot;
   }
-  if (kEmit) {
-    const unsigned M = __ldcg(&ctl->cand_count);
-    if ((unsigned long long)M < k) {
-      if (tid == 0) ctl->fallback = 1;
-      return;
-    }
-    unsigned bin;
-    unsigned long long above;
-    block_select_top<kThreads>(ctl->hist1, kBins1, k, bin, above);
-    if (tid == 0) {
-      ctl->b1 = bin;
-      ctl->need1 = k - above;
-    }
-  }
+  if (kEmit && tid == 0 && (unsigned long long)__ldcg(&ctl->cand_count) < k) ctl->fallback = 1;
 }
 
-static int g_ef_grid = 0;
-int ef_grid_size() {
-  if (!g_ef_grid) {
-    int occ = 0, o2 = 0, o3 = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ef<true, true>, kThreads, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_ef<true, false>, kThreads, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, k_ef<false, true>, kThreads, 0);
-    if (o2 < occ) occ = o2;
-    if (o3 < occ) occ = o3;
-    if (occ < 1) occ = 1;
-    g_ef_grid = num_sms() * occ;
+template <bool A, bool E, bool P>
+static void launch_ef_t(const float* g_o, float* ge, uint64_t G, uint64_t k, Ctl* ctl,
+                        const ChunkWs& w, Pending pz, int gated, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_ef<A, E, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kEfRingBytes);
+    attr = true;
   }
-  return g_ef_grid;
+  k_ef<A, E, P><<<w.ef_grid, kThreads, kEfRingBytes, s>>>(g_o, ge, G, k, ctl, w, pz, gated);
 }
 
-void launch_ef(const float* g_o, float* ge, uint64_t G, uint64_t k, Ctl* ctl, const TileWs& w,
-               int add, int emit, cudaStream_t s) {
-  const int grid = (int)w.ef_grid;
-  if (add && emit)
-    k_ef<true, true><<<grid, kThreads, 0, s>>>(g_o, ge, G, k, ctl, w, 0);
+int ef_grid_size() { return num_sms(); }
+
+static void launch_ef_any(const float* g_o, float* ge, uint64_t G, uint64_t k, Ctl* ctl,
+                          const ChunkWs& w, Pending pz, int add, int emit, int gated,
+                          cudaStream_t s) {
+  const bool pend = pz.zmap != nullptr;
+  if (add && emit && pend)
+    launch_ef_t<true, true, true>(g_o, ge, G, k, ctl, w, pz, gated, s);
+  else if (add && emit)
+    launch_ef_t<true, true, false>(g_o, ge, G, k, ctl, w, pz, gated, s);
+  else if (add && pend)
+    launch_ef_t<true, false, true>(g_o, ge, G, k, ctl, w, pz, gated, s);
   else if (add)
-    k_ef<true, false><<<grid, kThreads, 0, s>>>(g_o, ge, G, k, ctl, w, 0);
+    launch_ef_t<true, false, false>(g_o, ge, G, k, ctl, w, pz, gated, s);
   else
-    k_ef<false, true><<<grid, kThreads, 0, s>>>(g_o, ge, G, k, ctl, w, 0);
+    launch_ef_t<false, true, false>(g_o, ge, G, k, ctl, w, Pending{}, gated, s);
   count_launch();
 }
 
+void launch_ef(const float* g_o, float* ge, uint64_t G, uint64_t k, Ctl* ctl, const ChunkWs& w,
+               Pending pz, int add, int emit, cudaStream_t s) {
+  launch_ef_any(g_o, ge, G, k, ctl, w, pz, add, emit, 0, s);
+}
+
 // ---------------------------------------------------------------- fallback ---
-// Only runs when the sampled bound kept fewer than k elements: full digit-1
-// histogram of g_e, then an exact re-emission with L = the k-th element's
-// digit (so the candidate set provably contains the whole top-k).
+// Only does work when the sampled bound kept fewer than k elements: full
+// digit-1 histogram of g_e, then an exact re-emission with L = the k-th
+// element's digit (so the candidate set provably contains the whole top-k).
 __global__ void __launch_bounds__(kThreads) k_fb_hist(const float* __restrict__ ge, uint64_t G,
                                                       uint64_t k, Ctl* __restrict__ ctl) {
   if (*(volatile unsigned*)&ctl->fallback == 0) return;
@@ -440,192 +513,337 @@ __global__ void __launch_bounds__(kThreads) k_fb_hist(const float* __restrict__ 
   for (int b = threadIdx.x; b < kBins1; b += kThreads) ctl->hist1[b] = 0;
 }
 
-void launch_fallback(float* ge, uint64_t G, uint64_t k, Ctl* ctl, const TileWs& w, cudaStream_t s) {
-  k_fb_hist<<<num_sms() * 4, kThreads, 0, s>>>(ge, G, k, ctl);
+void launch_fallback(float* ge, uint64_t G, uint64_t k, Ctl* ctl, const ChunkWs& w, cudaStream_t s) {
+  k_fb_hist<<<num_sms() * 2, kThreads, 0, s>>>(ge, G, k, ctl);
   count_launch();
-  k_ef<false, true><<<(int)w.ef_grid, kThreads, 0, s>>>(nullptr, ge, G, k, ctl, w, 1);
-  count_launch();
+  launch_ef_any(nullptr, ge, G, k, ctl, w, Pending{}, 0, 1, 1, s);
 }
 
-// ------------------------------------------------------------------ refine ---
-// Digits 2 and 3 of the exact threshold, over the (small) candidate set only.
-__global__ void __launch_bounds__(kThreads) k_refine1(Ctl* __restrict__ ctl, TileWs w) {
-  __shared__ unsigned s_h[kBins2];
-  for (int b = threadIdx.x; b < kBins2; b += kThreads) s_h[b] = 0;
-  __syncthreads();
-  const unsigned M = *(volatile unsigned*)&ctl->cand_count;
-  const unsigned b1 = *(volatile unsigned*)&ctl->b1;
-  for (unsigned j = blockIdx.x * kThreads + threadIdx.x; j < M; j += gridDim.x * kThreads) {
-    const unsigned key = key_of(__ldcg(w.cand_val + j));
-    if ((key >> kShift1) == b1) atomicAdd(&s_h[(key >> kShift2) & (kBins2 - 1)], 1u);
-  }
-  __syncthreads();
-  for (int b = threadIdx.x; b < kBins2; b += kThreads)
-    if (s_h[b]) atomicAdd(&ctl->hist2[b], s_h[b]);
-  if (!last_block_done(&ctl->done_r1)) return;
-  const unsigned long long need1 = __ldcg(&ctl->need1);
-  unsigned bin;
-  unsigned long long above;
-  block_select_top<kThreads>(ctl->hist2, kBins2, need1, bin, above);
-  if (threadIdx.x == 0) {
-    ctl->b2 = bin;
-    ctl->need2 = need1 - above;
-  }
+// ------------------------------------------------------------------ select ---
+// One cooperative kernel (all blocks resident, grid barriers between phases)
+// turns the candidate runs into the exact, index-ordered top-k:
+//   A/B/C  radix digits 2..4 of the threshold T (key bits 18..11, 10..3,
+//          2..0) over the candidates of digit-1 bucket b1 (from the EF pass);
+//          every block derives the same digit from the global histogram
+//   D      per-chunk counts of candidates > T and == T, block totals
+//   E      each block's prefix over earlier blocks' totals, then every
+//          thread writes its chunks' selected (index, value) pairs in index
+//          order; ties at T are kept lowest index first
+//          (min(eq, max(0, needT - eq_before)) per chunk)
+// Block b owns a contiguous range of chunks, thread t a contiguous sub-range,
+// so all prefixes are plain scans (no look-back chains).
+namespace cg = cooperative_groups;
+constexpr int kSelBins = 4096;
+constexpr int kSelGridMax = 4096;
+
+__device__ __forceinline__ unsigned long long pack_ge(unsigned long long gt, unsigned long long eq) {
+  return (gt << 31) | eq;
 }
 
-__global__ void __launch_bounds__(kThreads) k_refine2(uint64_t k, Ctl* __restrict__ ctl, TileWs w) {
-  __shared__ unsigned s_h[kBins3];
-  for (int b = threadIdx.x; b < kBins3; b += kThreads) s_h[b] = 0;
+template <int B>
+__device__ __forceinline__ unsigned long long block_sum_u64(unsigned long long v,
+                                                            unsigned long long* s_red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum_u64(v);
+  if (lane == 0) s_red[warp] = v;
   __syncthreads();
-  const unsigned M = *(volatile unsigned*)&ctl->cand_count;
-  const unsigned hi = ((*(volatile unsigned*)&ctl->b1) << 12) | (*(volatile unsigned*)&ctl->b2);
-  for (unsigned j = blockIdx.x * kThreads + threadIdx.x; j < M; j += gridDim.x * kThreads) {
-    const unsigned key = key_of(__ldcg(w.cand_val + j));
-    if ((key >> kShift2) == hi) atomicAdd(&s_h[key & (kBins3 - 1)], 1u);
+  unsigned long long t = 0;
+#pragma unroll
+  for (int q = 0; q < B / 32; ++q) t += s_red[q];
+  __syncthreads();
+  return t;
+}
+
+__device__ __forceinline__ void flush_hist(unsigned* s_h, unsigned* g_h, int nb) {
+  __syncthreads();
+  for (int b = threadIdx.x; b < nb; b += blockDim.x)
+    if (s_h[b]) atomicAdd(g_h + b, s_h[b]);
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SEL_MARK(i) \
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctl->tphase[i] = gtimer()
+
+__device__ __forceinline__ float comp(const float4& v, int e) {
+  return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
+}
+__device__ __forceinline__ unsigned comp(const uint4& v, int e) {
+  return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
+}
+
+constexpr int kSelThreads = 1024;   // one block per SM: cheap grid barriers
+constexpr int kSelMaxCpb = 16384;   // chunks per block (G < 2^31 on 148 SMs)
+constexpr unsigned kSelSmemMax = 200 * 1024;
+constexpr int kSelQ = 8;            // float4 loads in flight per thread per round
+
+__host__ __device__ inline unsigned sel_cache_cap(unsigned cpb) {
+  const unsigned arrays = cpb * 12u;
+  return arrays >= kSelSmemMax ? 0u : ((kSelSmemMax - arrays) / 4u) & ~3u;
+}
+
+__global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __restrict__ ctl,
+                                                           ChunkWs w, unsigned* __restrict__ out_idx,
+                                                           float* __restrict__ out_val) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  __shared__ unsigned s_h[kSelBins];
+  __shared__ unsigned long long s_scan[kSelThreads / 32 + 1];
+  __shared__ unsigned long long s_red[kSelThreads / 32];
+  __shared__ double s_dred[kSelThreads / 32];
+  __shared__ int s_cached;
+  __shared__ unsigned s_used;  // cache values in use (padded)
+  const int tid = threadIdx.x;
+  SEL_MARK(0);
+  const unsigned nch = w.nchunks;
+  const unsigned cpb = (nch + gridDim.x - 1) / gridDim.x;
+  const unsigned c0 = min(nch, blockIdx.x * cpb), c1 = min(nch, c0 + cpb);
+  const unsigned cache_cap = sel_cache_cap(cpb);
+  float* s_val = reinterpret_cast<float*>(s_dyn);                 // cache_cap
+  unsigned* s_cnt = reinterpret_cast<unsigned*>(s_val + cache_cap);  // cpb
+  unsigned* s_off = s_cnt + cpb;                                  // cpb (16-B aligned offsets)
+  unsigned* s_ge = s_off + cpb;                                   // cpb: (gt << 16) | eq
+  const unsigned cpt = (cpb + kSelThreads - 1) / kSelThreads;
+  const unsigned t0 = min(c1, c0 + tid * cpt), t1 = min(c1, t0 + cpt);
+
+  // ---- stage: chunk counts, and the block's candidate values if they fit ----
+  unsigned mysum = 0;
+  for (unsigned c = t0; c < t1; ++c) {
+    const unsigned n = __ldcg(w.cnt + c);
+    s_cnt[c - c0] = n;
+    mysum += (n + 3u) & ~3u;
+  }
+  {
+    const unsigned long long ex = block_excl_scan<kSelThreads>(mysum, s_scan);
+    if (tid == 0) {
+      s_cached = s_scan[kSelThreads / 32] <= (unsigned long long)cache_cap;
+      s_used = (unsigned)s_scan[kSelThreads / 32];
+    }
+    unsigned o = (unsigned)ex;
+    for (unsigned c = t0; c < t1; ++c) {
+      s_off[c - c0] = o;
+      o += (s_cnt[c - c0] + 3u) & ~3u;
+    }
   }
   __syncthreads();
-  for (int b = threadIdx.x; b < kBins3; b += kThreads)
-    if (s_h[b]) atomicAdd(&ctl->hist3[b], s_h[b]);
-  if (!last_block_done(&ctl->done_r2)) return;
-  const unsigned long long need2 = __ldcg(&ctl->need2);
-  unsigned bin;
-  unsigned long long above;
-  block_select_top<kThreads>(ctl->hist3, kBins3, need2, bin, above);
-  if (threadIdx.x == 0) {
-    const unsigned long long needT = need2 - above;
-    ctl->T = (hi << kShift2) | bin;
+  const bool cached = s_cached != 0;
+  if (cached) {
+    // each thread stages its own runs: up to kSelQ 16-byte loads in flight
+    for (unsigned c = t0; c < t1; ++c) {
+      const unsigned n4 = (s_cnt[c - c0] + 3) >> 2;
+      const float4* v4 = reinterpret_cast<const float4*>(w.cand_val + ((uint64_t)c << kChunkShift));
+      float4* d4 = reinterpret_cast<float4*>(s_val + s_off[c - c0]);
+      for (unsigned q0 = 0; q0 < n4; q0 += kSelQ) {
+        float4 x[kSelQ];
+#pragma unroll
+        for (int u = 0; u < kSelQ; ++u)
+          if (q0 + u < n4) x[u] = __ldcg(v4 + q0 + u);
+#pragma unroll
+        for (int u = 0; u < kSelQ; ++u)
+          if (q0 + u < n4) d4[q0 + u] = x[u];
+      }
+    }
+    __syncthreads();
+  }
+  SEL_MARK(1);
+  // f(x) for every candidate value this thread owns, in index order
+  auto visit_chunk = [&](unsigned c, auto&& f) {
+    const unsigned cnt = s_cnt[c - c0];
+    if (cached) {
+      const float* sv = s_val + s_off[c - c0];
+      for (unsigned i = 0; i < cnt; ++i) f(sv[i]);
+      return;
+    }
+    const float4* v4 = reinterpret_cast<const float4*>(w.cand_val + ((uint64_t)c << kChunkShift));
+    const unsigned n4 = (cnt + 3) >> 2;
+    for (unsigned q0 = 0; q0 < n4; q0 += kSelQ) {
+      float4 x[kSelQ];
+#pragma unroll
+      for (int u = 0; u < kSelQ; ++u)
+        x[u] = q0 + u < n4 ? __ldcg(v4 + q0 + u) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < kSelQ; ++u)
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if ((q0 + u) * 4 + e < cnt) f(comp(x[u], e));
+    }
+  };
+
+  // ---- three radix digits of T: key bits 30..19 (all candidates), 18..11
+  // and 10..0 (only candidates whose higher digits match) ----
+  unsigned long long need = k;
+  unsigned prefix = 0;  // key bits above the digit being resolved
+  const int shifts[3] = {kShift1, 11, 0};
+  const int widths[3] = {12, 8, 11};
+  int above_shift = 31;
+  unsigned* ghs[3] = {ctl->hist1, ctl->hist2, ctl->hist3};
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const int nb = 1 << widths[d];
+    for (int b = tid; b < nb; b += kSelThreads) s_h[b] = 0;
+    __syncthreads();
+    const int sh = shifts[d], as = above_shift;
+    const unsigned pf = prefix, dm = (unsigned)nb - 1;
+    for (unsigned c = t0; c < t1; ++c)
+      visit_chunk(c, [&](float x) {
+        const unsigned key = key_of(x);
+        if ((key >> as) == pf) atomicAdd(&s_h[(key >> sh) & dm], 1u);
+      });
+    flush_hist(s_h, ghs[d], nb);
+    grid.sync();
+    SEL_MARK(2 + d);
+    unsigned bin;
+    unsigned long long above;
+    block_select_top<kSelThreads>(ghs[d], nb, need, bin, above);
+    need -= above;
+    prefix = (prefix << widths[d]) | bin;
+    above_shift = sh;
+    if (d == 0 && blockIdx.x == 0 && tid == 0) ctl->b1 = bin;
+  }
+  const unsigned T = prefix;
+  const unsigned long long needT = need;
+  if (blockIdx.x == 0 && tid == 0) {
+    ctl->T = T;
     ctl->needT = needT;
     ctl->count_gt = k - needT;
   }
-}
 
-void launch_refine(uint64_t k, Ctl* ctl, const TileWs& w, cudaStream_t s) {
-  const int grid = num_sms() * 2;
-  k_refine1<<<grid, kThreads, 0, s>>>(ctl, w);
-  count_launch();
-  k_refine2<<<grid, kThreads, 0, s>>>(k, ctl, w);
-  count_launch();
-}
-
-// --------------------------------------------------------- ordered emission ---
-// (1) per tile: candidates above / equal to T; (2) one-block scan giving each
-// tile its output offset and how many of its ties it keeps (lowest index
-// first: ties are taken in global index order); (3) per tile: ordered write
-// of the selected (index, value) pairs, optional residual zeroing (AG:
-// residual_update, compress.hpp:122-130) and the fp64 sum of squares.
-__global__ void __launch_bounds__(kThreads) k_tile_count(const Ctl* __restrict__ ctl, TileWs w) {
-  const unsigned T = *(volatile const unsigned*)&ctl->T;
-  const int lane = threadIdx.x & 31;
-  const unsigned nw = gridDim.x * (kThreads / 32);
-  for (unsigned t = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); t < w.ntiles; t += nw) {
-    const unsigned cnt = w.cnt[t], off = w.off[t];
+  // ---- D: per-chunk (gt, eq) and block totals ----
+  unsigned long long mine = 0;
+  for (unsigned c = t0; c < t1; ++c) {
     unsigned gt = 0, eq = 0;
-    for (unsigned c0 = 0; c0 < cnt; c0 += 32) {
-      const unsigned c = c0 + lane;
-      if (c < cnt) {
-        const unsigned key = key_of(__ldcg(w.cand_val + off + c));
-        gt += key > T;
-        eq += key == T;
-      }
-    }
-    gt = __reduce_add_sync(0xffffffffu, gt);
-    eq = __reduce_add_sync(0xffffffffu, eq);
-    if (lane == 0) {
-      w.gt[t] = gt;
-      w.eq[t] = eq;
-    }
+    visit_chunk(c, [&](float x) {
+      const unsigned key = key_of(x);
+      gt += key > T;
+      eq += key == T;
+    });
+    s_ge[c - c0] = (gt << 16) | eq;
+    mine += pack_ge(gt, eq);
   }
-}
+  const unsigned long long excl = block_excl_scan<kSelThreads>(mine, s_scan);
+  const unsigned long long blk_total = s_scan[kSelThreads / 32];
+  if (tid == 0) w.btot[blockIdx.x] = blk_total;
+  grid.sync();
+  SEL_MARK(5);
 
-constexpr int kScanThreads = 1024;
-__global__ void __launch_bounds__(kScanThreads) k_tile_scan(const Ctl* __restrict__ ctl, TileWs w) {
-  __shared__ unsigned long long s_scan[kScanThreads / 32 + 1];
-  const unsigned long long needT = *(volatile const unsigned long long*)&ctl->needT;
-  const unsigned n = w.ntiles;
-  const unsigned chunk = (n + kScanThreads - 1) / kScanThreads;
-  const unsigned t0 = min(n, threadIdx.x * chunk), t1 = min(n, t0 + chunk);
-  unsigned long long eqs = 0;
-  for (unsigned t = t0; t < t1; ++t) eqs += w.eq[t];
-  unsigned long long ep = block_excl_scan<kScanThreads>(eqs, s_scan, nullptr);
-  unsigned long long sels = 0;
-  for (unsigned t = t0; t < t1; ++t) {
-    const unsigned eq = w.eq[t];
-    const unsigned long long take = ep >= needT ? 0ull : min((unsigned long long)eq, needT - ep);
-    w.take[t] = (unsigned)take;
-    ep += eq;
-    sels += w.gt[t] + take;
-  }
-  unsigned long long sp = block_excl_scan<kScanThreads>(sels, s_scan, nullptr);
-  for (unsigned t = t0; t < t1; ++t) {
-    w.out[t] = (unsigned)sp;
-    sp += w.gt[t] + w.take[t];
-  }
-}
-
-__global__ void __launch_bounds__(kThreads) k_emit(Ctl* __restrict__ ctl, TileWs w,
-                                                   unsigned* __restrict__ out_idx,
-                                                   float* __restrict__ out_val,
-                                                   float* __restrict__ ge, int zero_own) {
-  __shared__ double s_red[kThreads / 32];
-  const unsigned T = *(volatile const unsigned*)&ctl->T;
-  const int lane = threadIdx.x & 31;
-  const unsigned lt = lanemask_lt();
-  const unsigned nw = gridDim.x * (kThreads / 32);
-  for (unsigned t = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); t < w.ntiles; t += nw) {
-    const unsigned cnt = w.cnt[t], off = w.off[t], out = w.out[t], take = w.take[t];
-    unsigned eq_seen = 0, written = 0;
-    double acc = 0.0;
-    for (unsigned c0 = 0; c0 < cnt; c0 += 32) {
-      const unsigned c = c0 + lane;
-      const bool in = c < cnt;
-      const float val = in ? __ldcg(w.cand_val + off + c) : 0.f;
-      const unsigned idx = in ? __ldcg(w.cand_idx + off + c) : 0u;
-      const unsigned key = key_of(val);
-      const bool is_eq = in && key == T;
-      const unsigned eqb = __ballot_sync(0xffffffffu, is_eq);
-      const bool sel = in && (key > T || (is_eq && eq_seen + __popc(eqb & lt) < take));
-      const unsigned sb = __ballot_sync(0xffffffffu, sel);
-      if (sel) {
-        const unsigned pos = out + written + __popc(sb & lt);
-        out_idx[pos] = idx;
-        out_val[pos] = val;
-        if (zero_own) ge[idx] = 0.f;
-        acc = fma((double)val, (double)val, acc);
-      }
-      written += __popc(sb);
-      eq_seen += __popc(eqb);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) w.norm[t] = acc;
-  }
-  if (!last_block_done(&ctl->done_emit)) return;
+  // ---- E: block prefix, ordered emission ----
+  unsigned long long bp = 0;
+  for (unsigned i = tid; i < blockIdx.x; i += kSelThreads) bp += __ldcg(w.btot + i);
+  bp = block_sum_u64<kSelThreads>(bp, s_red);
+  unsigned long long before = bp + excl;
+  // The block's selected pairs form one contiguous range of the output:
+  // assemble it in shared memory, then write it out coalesced.
+  const unsigned long long bgt_pre = bp >> 31, beq_pre = bp & 0x7fffffffull;
+  const unsigned long long obase = bgt_pre + (beq_pre < needT ? beq_pre : needT);
+  const unsigned long long blk_eq = blk_total & 0x7fffffffull;
+  const unsigned long long nsel =
+      (blk_total >> 31) + (beq_pre >= needT ? 0ull : min(blk_eq, needT - beq_pre));
+  const bool staged = cached && (unsigned long long)s_used + 2 * nsel <= cache_cap;
+  unsigned* s_oidx = reinterpret_cast<unsigned*>(s_val + s_used);
+  float* s_oval = reinterpret_cast<float*>(s_oidx + (staged ? nsel : 0));
   double acc = 0.0;
-  for (unsigned t = threadIdx.x; t < w.ntiles; t += kThreads) acc += __ldcg(w.norm + t);
-  const double tot = block_sum<kThreads>(acc, s_red);
-  if (threadIdx.x == 0) ctl->topk_norm2 = tot;
+  for (unsigned c = t0; c < t1; ++c) {
+    const unsigned pc = s_ge[c - c0];
+    const unsigned gt = pc >> 16, eq = pc & 0xFFFFu;
+    const unsigned long long gt_pre = before >> 31, eq_pre = before & 0x7fffffffull;
+    unsigned long long o = gt_pre + (eq_pre < needT ? eq_pre : needT);
+    const unsigned take = eq_pre >= needT ? 0u : (unsigned)min((unsigned long long)eq, needT - eq_pre);
+    before += pack_ge(gt, eq);
+    if (gt + take == 0) continue;
+    const unsigned cnt = s_cnt[c - c0];
+    const uint64_t slot = (uint64_t)c << kChunkShift;
+    const float4* v4 = reinterpret_cast<const float4*>(w.cand_val + slot);
+    const uint4* i4 = reinterpret_cast<const uint4*>(w.cand_idx + slot);
+    const float4* sv4 = reinterpret_cast<const float4*>(s_val + s_off[c - c0]);
+    const unsigned n4 = (cnt + 3) >> 2;
+    unsigned t = 0;
+    constexpr int QE = 4;
+    for (unsigned q0 = 0; q0 < n4; q0 += QE) {
+      float4 x[QE];
+      uint4 id[QE];
+#pragma unroll
+      for (int u = 0; u < QE; ++u) {
+        if (q0 + u < n4) {
+          x[u] = cached ? sv4[q0 + u] : __ldcg(v4 + q0 + u);
+          id[u] = __ldcg(i4 + q0 + u);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < QE; ++u) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if ((q0 + u) * 4 + e >= cnt) break;
+          const float xv = comp(x[u], e);
+          const unsigned key = key_of(xv);
+          bool sel = key > T;
+          if (key == T) {
+            sel = t < take;
+            ++t;
+          }
+          if (sel) {
+            if (staged) {
+              s_oidx[o - obase] = comp(id[u], e);
+              s_oval[o - obase] = xv;
+            } else {
+              out_idx[o] = comp(id[u], e);
+              out_val[o] = xv;
+            }
+            ++o;
+            acc = fma((double)xv, (double)xv, acc);
+          }
+        }
+      }
+    }
+  }
+  const double bsum = block_sum<kSelThreads>(acc, s_dred);  // (also a barrier)
+  if (staged)
+    for (unsigned i = tid; i < nsel; i += kSelThreads) {
+      out_idx[obase + i] = s_oidx[i];
+      out_val[obase + i] = s_oval[i];
+    }
+  if (tid == 0) w.bnorm[blockIdx.x] = bsum;
+  SEL_MARK(6);
+  grid.sync();
+  SEL_MARK(7);
+  if (blockIdx.x == 0) {
+    const double tot = block_sum_array<kSelThreads>(w.bnorm, gridDim.x, s_dred);
+    if (tid == 0) ctl->topk_norm2 = tot;
+  }
 }
 
-void launch_emit(Ctl* ctl, const TileWs& w, unsigned* out_idx, float* out_val, float* ge,
-                 int zero_own, cudaStream_t s) {
-  const int grid = num_sms() * 4;
-  k_tile_count<<<grid, kThreads, 0, s>>>(ctl, w);
+// Grid of the cooperative select: one resident 1024-thread block per SM.
+int launch_select(uint64_t k, Ctl* ctl, const ChunkWs& w, unsigned* out_idx, float* out_val,
+                  cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelSmemMax);
+    attr = true;
+  }
+  const int grid = num_sms();
+  const unsigned cpb = (w.nchunks + grid - 1) / grid;
+  if (cpb > (unsigned)kSelMaxCpb) return (int)cudaErrorInvalidValue;
+  const unsigned smem = cpb * 12u + sel_cache_cap(cpb) * 4u;
+  ChunkWs ws = w;
+  void* args[] = {&k, &ctl, &ws, &out_idx, &out_val};
+  const cudaError_t e = cudaLaunchCooperativeKernel((void*)k_select, dim3(grid), dim3(kSelThreads),
+                                                    args, smem, s);
   count_launch();
-  k_tile_scan<<<1, kScanThreads, 0, s>>>(ctl, w);
-  count_launch();
-  k_emit<<<grid, kThreads, 0, s>>>(ctl, w, out_idx, out_val, ge, zero_own);
-  count_launch();
+  return e == cudaSuccess ? 0 : (int)e;
 }
 
-// ------------------------------------------------------------ gather/zero ---
-// contrib[j] = g_e[bidx[j]]; residual[bidx[j]] = 0 (artopk.hpp:92-102), and
-// the kept energy sum_j g_e[bidx[j]]^2 for the gain (trainer.hpp:387-396).
+// ------------------------------------------------------------------ gather ---
+// contrib[j] = g_e[bidx[j]] (artopk.hpp:92-98) and the kept energy
+// sum_j g_e[bidx[j]]^2 for the gain (trainer.hpp:387-396).  The residual
+// zeros at bidx are owed, not written (Pending).
 constexpr int kGatherUnroll = 4;
-__global__ void __launch_bounds__(kThreads) k_gather_zero(const unsigned* __restrict__ bidx,
-                                                          uint64_t k, float* __restrict__ ge,
-                                                          float* __restrict__ contrib,
-                                                          Ctl* __restrict__ ctl,
-                                                          double* __restrict__ part) {
+__global__ void __launch_bounds__(kThreads) k_gather(const unsigned* __restrict__ bidx, uint64_t k,
+                                                     const float* __restrict__ ge,
+                                                     float* __restrict__ contrib,
+                                                     Ctl* __restrict__ ctl,
+                                                     double* __restrict__ part) {
   __shared__ double s_red[kThreads / 32];
   double acc = 0.0;
   const uint64_t step = (uint64_t)gridDim.x * kThreads;
@@ -639,12 +857,11 @@ __global__ void __launch_bounds__(kThreads) k_gather_zero(const unsigned* __rest
       ii[u] = j < k ? __ldcs(bidx + j) : 0xffffffffu;
     }
 #pragma unroll
-    for (int u = 0; u < kGatherUnroll; ++u) vv[u] = ii[u] != 0xffffffffu ? ge[ii[u]] : 0.f;
+    for (int u = 0; u < kGatherUnroll; ++u) vv[u] = ii[u] != 0xffffffffu ? __ldcs(ge + ii[u]) : 0.f;
 #pragma unroll
     for (int u = 0; u < kGatherUnroll; ++u) {
       if (ii[u] != 0xffffffffu) {
         contrib[j0 + u * step] = vv[u];
-        ge[ii[u]] = 0.f;
         acc = fma((double)vv[u], (double)vv[u], acc);
       }
     }
@@ -652,124 +869,191 @@ __global__ void __launch_bounds__(kThreads) k_gather_zero(const unsigned* __rest
   const double b = block_sum<kThreads>(acc, s_red);
   if (threadIdx.x == 0) part[blockIdx.x] = b;
   if (!last_block_done(&ctl->done_gather)) return;
-  double a2 = 0.0;
-  for (unsigned i = threadIdx.x; i < gridDim.x; i += kThreads) a2 += __ldcg(part + i);
-  const double tot = block_sum<kThreads>(a2, s_red);
+  const double tot = block_sum_array<kThreads>(part, gridDim.x, s_red);
   if (threadIdx.x == 0) ctl->kept_norm2 = tot;
 }
 
-void launch_gather_zero(const unsigned* bidx, uint64_t k, float* ge, float* contrib, Ctl* ctl,
-                        double* part, cudaStream_t s) {
-  k_gather_zero<<<num_sms() * 4, kThreads, 0, s>>>(bidx, k, ge, contrib, ctl, part);
+void launch_gather(const unsigned* bidx, uint64_t k, const float* ge, float* contrib, Ctl* ctl,
+                   double* part, cudaStream_t s) {
+  int grid = (int)std::min<uint64_t>((k + kThreads * kGatherUnroll - 1) / (kThreads * kGatherUnroll),
+                                     (uint64_t)num_sms() * 8);
+  if (grid < 1) grid = 1;
+  k_gather<<<grid, kThreads, 0, s>>>(bidx, k, ge, contrib, ctl, part);
   count_launch();
 }
 
-// ------------------------------------------------------------------ decode ---
-// bounds[t] = first j with idx[j] >= t * kDecTile (per list), so every decode
-// tile finds its slice of the sorted index list without a search.
-__global__ void k_tile_bounds(const unsigned* __restrict__ idx, uint64_t k, uint64_t list_stride,
-                              int nlists, uint64_t ntd, unsigned* __restrict__ bounds) {
+// Materialise owed zeros (before the residual store is read from outside).
+__global__ void k_zero_at(const unsigned* __restrict__ idx, uint64_t k, float* __restrict__ ge) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < k;
+       j += (uint64_t)gridDim.x * blockDim.x)
+    ge[idx[j]] = 0.0f;
+}
+
+void launch_zero_at(const unsigned* idx, uint64_t k, float* ge, cudaStream_t s) {
+  k_zero_at<<<num_sms() * 8, kThreads, 0, s>>>(idx, k, ge);
+  count_launch();
+}
+
+// ------------------------------------------------------------------ bounds ---
+// bounds[c] = first j with idx[j] >= c * kChunk (per list, nchunks+1 entries),
+// so the decode tiles and the next EF pass find their slice of a sorted index
+// list without a search.
+__global__ void k_bounds(const unsigned* __restrict__ idx, uint64_t k, uint64_t list_stride,
+                         int nlists, uint64_t nch, unsigned* __restrict__ bounds) {
   const uint64_t per = k + 1;
   for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < per * nlists;
        q += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t r = q / per, j = q - r * per;
     const unsigned* id = idx + r * list_stride;
-    unsigned* bd = bounds + r * (ntd + 1);
-    const uint64_t hi = j < k ? (uint64_t)(id[j] >> kDecShift) : ntd;
-    const uint64_t lo = j == 0 ? 0 : (uint64_t)(id[j - 1] >> kDecShift) + 1;
+    unsigned* bd = bounds + r * (nch + 1);
+    const uint64_t hi = j < k ? (uint64_t)(id[j] >> kChunkShift) : nch;
+    const uint64_t lo = j == 0 ? 0 : (uint64_t)(id[j - 1] >> kChunkShift) + 1;
     for (uint64_t t = lo; t <= hi; ++t) bd[t] = (unsigned)j;
   }
 }
 
-void launch_tile_bounds(const unsigned* idx, uint64_t k, uint64_t list_stride, int nlists,
-                        uint64_t G, unsigned* bounds, cudaStream_t s) {
-  const uint64_t ntd = (G + kDecTile - 1) >> kDecShift;
+void launch_bounds(const unsigned* idx, uint64_t k, uint64_t list_stride, int nlists, uint64_t G,
+                   unsigned* bounds, cudaStream_t s) {
+  const uint64_t nch = nchunks_of(G);
   const uint64_t work = (k + 1) * nlists;
-  int grid = (int)std::min<uint64_t>((work + kThreads - 1) / kThreads, (uint64_t)num_sms() * 8);
-  if (grid < 1) grid = 1;
-  k_tile_bounds<<<grid, kThreads, 0, s>>>(idx, k, list_stride, nlists, ntd, bounds);
+  uint64_t grid = (work + kThreads - 1) / kThreads;
+  if (grid > (1u << 30)) grid = 1u << 30;
+  k_bounds<<<(unsigned)grid, kThreads, 0, s>>>(idx, k, list_stride, nlists, nch, bounds);
   count_launch();
 }
 
-__device__ __forceinline__ void store_tile(const float* __restrict__ tile, float* __restrict__ agg,
-                                           uint64_t t0, uint64_t G) {
-  if (t0 + kDecTile <= G) {
-    const float4* s4 = reinterpret_cast<const float4*>(tile);
-    float4* d4 = reinterpret_cast<float4*>(agg + t0);
+// ------------------------------------------------------------------ decode ---
+// Dense 4096-float tiles built in shared memory and written with bulk async
+// copies (cp.async.bulk shared::cta -> global, TMA engine), double-buffered so
+// the next tile is assembled while the previous one drains to HBM.
+__device__ __forceinline__ void bulk_store(float* gdst, const float* ssrc, unsigned bytes) {
+  const unsigned saddr = (unsigned)__cvta_generic_to_shared(ssrc);
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst),
+               "r"(saddr), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_async_shared() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+// Writes tile[0..n) to agg[t0..t0+n): the 16-byte-multiple head by one bulk
+// copy issued by thread 0, the (< 4 element) tail by plain stores.
+__device__ __forceinline__ void emit_tile(float* __restrict__ agg, const float* tile, uint64_t t0,
+                                          uint64_t G) {
+  const unsigned n = (unsigned)min((uint64_t)kDecTile, G - t0);
+  const unsigned nb = (n & ~3u) * 4u;
+  fence_async_shared();
+  __syncthreads();
+  if (threadIdx.x == 0 && nb) bulk_store(agg + t0, tile, nb);
+  for (unsigned i = (n & ~3u) + threadIdx.x; i < n; i += kThreads) agg[t0 + i] = tile[i];
+}
+
+__device__ __forceinline__ void zero_tile(float* tile) {
+  float4* t4 = reinterpret_cast<float4*>(tile);
 #pragma unroll
-    for (int q = 0; q < kDecTile / 4 / kThreads; ++q) __stcs(d4 + q * kThreads + threadIdx.x, s4[q * kThreads + threadIdx.x]);
-  } else {
-    for (uint64_t i = threadIdx.x; t0 + i < G; i += kThreads) agg[t0 + i] = tile[i];
-  }
+  for (int q = 0; q < kDecTile / 4 / kThreads; ++q)
+    t4[q * kThreads + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 // AR decode (densify, core.hpp:72-81): zeros everywhere except the broadcast
 // indices, which get the allreduced value.  In loopback the allreduce itself
 // happens here, in the reference's order: v = c_0; v += c_r (r ascending);
-// v /= N for Avg (collectives.hpp:82-87).
+// v /= N for Avg (collectives.hpp:82-87).  The same pass writes the zero map
+// of the broadcast indices: the residual zeros every worker owes (Pending).
 __global__ void __launch_bounds__(kThreads) k_decode_ar(const unsigned* __restrict__ idx,
                                                         const unsigned* __restrict__ bounds,
                                                         const float* __restrict__ lists,
                                                         int nlists, uint64_t list_stride,
                                                         int divide, float divisor,
-                                                        float* __restrict__ agg, uint64_t G) {
-  __shared__ __align__(16) float tile[kDecTile];
+                                                        float* __restrict__ agg, uint64_t G,
+                                                        unsigned* __restrict__ zmap) {
+  __shared__ __align__(128) float tile[2][kDecTile];
+  __shared__ unsigned s_zm[kDecChunks * 32];
   const uint64_t ntd = (G + kDecTile - 1) >> kDecShift;
-  for (uint64_t t = blockIdx.x; t < ntd; t += gridDim.x) {
+  const uint64_t nch = nchunks_of(G);
+  int buf = 0, iter = 0;
+  for (uint64_t t = blockIdx.x; t < ntd; t += gridDim.x, buf ^= 1, ++iter) {
     const uint64_t t0 = t << kDecShift;
-    float4* t4 = reinterpret_cast<float4*>(tile);
-#pragma unroll
-    for (int q = 0; q < kDecTile / 4 / kThreads; ++q)
-      t4[q * kThreads + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
-    const unsigned lo = __ldg(bounds + t), hi = __ldg(bounds + t + 1);
+    if (iter >= 2 && threadIdx.x == 0) bulk_wait_read1();
+    __syncthreads();
+    float* tl = tile[buf];
+    zero_tile(tl);
+    if (threadIdx.x < kDecChunks * 32) s_zm[threadIdx.x] = 0u;
+    const uint64_t c0 = t * kDecChunks, c1 = min(c0 + kDecChunks, nch);
+    const unsigned lo = __ldg(bounds + c0), hi = __ldg(bounds + c1);
     __syncthreads();
     for (unsigned j = lo + threadIdx.x; j < hi; j += kThreads) {
       float v = lists[j];
       for (int l = 1; l < nlists; ++l) v += lists[(uint64_t)l * list_stride + j];
       if (divide) v = v / divisor;
-      tile[idx[j] - (unsigned)t0] = v;
+      const unsigned p = idx[j];
+      tl[p - (unsigned)t0] = v;
+      atomicOr(&s_zm[zmap_word(p) - (unsigned)(c0 << 5)], zmap_bit(p));
     }
-    __syncthreads();
-    store_tile(tile, agg, t0, G);
-    __syncthreads();
+    emit_tile(agg, tl, t0, G);
+    if (threadIdx.x < (c1 - c0) * 32) zmap[(c0 << 5) + threadIdx.x] = s_zm[threadIdx.x];
   }
+  if (threadIdx.x == 0) bulk_wait_all();
 }
 
 void launch_decode_ar(const unsigned* idx, const unsigned* bounds, const float* lists, int nlists,
                       uint64_t list_stride, int divide, float divisor, float* agg, uint64_t G,
-                      cudaStream_t s) {
-  k_decode_ar<<<num_sms() * 8, kThreads, 0, s>>>(idx, bounds, lists, nlists, list_stride, divide,
-                                                  divisor, agg, G);
+                      unsigned* zmap, cudaStream_t s) {
+  k_decode_ar<<<num_sms() * 6, kThreads, 0, s>>>(idx, bounds, lists, nlists, list_stride, divide,
+                                                  divisor, agg, G, zmap);
   count_launch();
 }
 
 // AG decode (ag_step, artopk.hpp:151-159): agg = 0; agg[idx_r] += val_r for
 // r ascending; every element /= N.  Indices are unique within a rank, so each
 // rank's scatter into the shared-memory tile is race-free; ranks are
-// separated by a barrier to keep the reference's summation order.
+// separated by a barrier to keep the reference's summation order.  Zero maps
+// of ranks [map_rank0, map_rank0 + nmaps) are written on the way (each
+// worker owes zeros at its own indices: residual_update, compress.hpp:122).
 __global__ void __launch_bounds__(kThreads) k_decode_ag(const unsigned* __restrict__ packs,
                                                         uint64_t pack_stride, uint64_t k,
                                                         int nranks,
                                                         const unsigned* __restrict__ bounds,
                                                         float divisor, float* __restrict__ agg,
-                                                        uint64_t G) {
-  __shared__ __align__(16) float tile[kDecTile];
+                                                        uint64_t G, unsigned* __restrict__ zmaps,
+                                                        int map_rank0, int nmaps) {
+  __shared__ __align__(128) float tile[2][kDecTile];
+  extern __shared__ unsigned s_zm[];  // nmaps x kDecChunks*32
   const uint64_t ntd = (G + kDecTile - 1) >> kDecShift;
-  for (uint64_t t = blockIdx.x; t < ntd; t += gridDim.x) {
+  const uint64_t nch = nchunks_of(G);
+  const int zw = kDecChunks * 32;
+  int buf = 0, iter = 0;
+  for (uint64_t t = blockIdx.x; t < ntd; t += gridDim.x, buf ^= 1, ++iter) {
     const uint64_t t0 = t << kDecShift;
-    float4* t4 = reinterpret_cast<float4*>(tile);
-#pragma unroll
-    for (int q = 0; q < kDecTile / 4 / kThreads; ++q)
-      t4[q * kThreads + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (iter >= 2 && threadIdx.x == 0) bulk_wait_read1();
     __syncthreads();
+    float* tl = tile[buf];
+    zero_tile(tl);
+    for (int q = threadIdx.x; q < nmaps * zw; q += kThreads) s_zm[q] = 0u;
+    __syncthreads();
+    const uint64_t c0 = t * kDecChunks, c1 = min(c0 + kDecChunks, nch);
     for (int r = 0; r < nranks; ++r) {
-      const unsigned* bd = bounds + (uint64_t)r * (ntd + 1);
-      const unsigned lo = __ldg(bd + t), hi = __ldg(bd + t + 1);
+      const unsigned* bd = bounds + (uint64_t)r * (nch + 1);
+      const unsigned lo = __ldg(bd + c0), hi = __ldg(bd + c1);
       const unsigned* id = packs + (uint64_t)r * pack_stride;
       const float* va = reinterpret_cast<const float*>(id + k);
-      for (unsigned j = lo + threadIdx.x; j < hi; j += kThreads) tile[id[j] - (unsigned)t0] += va[j];
+      const int m = r - map_rank0;
+      const bool mapped = m >= 0 && m < nmaps;
+      for (unsigned j = lo + threadIdx.x; j < hi; j += kThreads) {
+        const unsigned p = id[j];
+        tl[p - (unsigned)t0] += va[j];
+        if (mapped) atomicOr(&s_zm[m * zw + zmap_word(p) - (unsigned)(c0 << 5)], zmap_bit(p));
+      }
       __syncthreads();
     }
+    float4* t4 = reinterpret_cast<float4*>(tl);
 #pragma unroll
     for (int q = 0; q < kDecTile / 4 / kThreads; ++q) {
       float4 x = t4[q * kThreads + threadIdx.x];
@@ -779,17 +1063,24 @@ __global__ void __launch_bounds__(kThreads) k_decode_ag(const unsigned* __restri
       x.w = x.w / divisor;
       t4[q * kThreads + threadIdx.x] = x;
     }
-    __syncthreads();
-    store_tile(tile, agg, t0, G);
-    __syncthreads();
+    emit_tile(agg, tl, t0, G);
+    const unsigned nw = (unsigned)(c1 - c0) * 32;
+    for (int q = threadIdx.x; q < nmaps * zw; q += kThreads) {
+      const int m = q / zw, wq = q - m * zw;
+      if ((unsigned)wq < nw) zmaps[(uint64_t)m * (nch << 5) + (c0 << 5) + wq] = s_zm[q];
+    }
   }
+  if (threadIdx.x == 0) bulk_wait_all();
 }
 
 void launch_decode_ag(const unsigned* packs, uint64_t pack_stride, uint64_t k, int nranks,
                       const unsigned* bounds, float divisor, float* agg, uint64_t G,
-                      cudaStream_t s) {
-  k_decode_ag<<<num_sms() * 8, kThreads, 0, s>>>(packs, pack_stride, k, nranks, bounds, divisor,
-                                                  agg, G);
+                      unsigned* zmaps, int map_rank0, int nmaps, cudaStream_t s) {
+  const size_t smem = (size_t)nmaps * kDecChunks * 32 * sizeof(unsigned);
+  if (smem > 16 * 1024)
+    cudaFuncSetAttribute(k_decode_ag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_decode_ag<<<num_sms() * 6, kThreads, smem, s>>>(packs, pack_stride, k, nranks, bounds, divisor,
+                                                     agg, G, zmaps, map_rank0, nmaps);
   count_launch();
 }
 
@@ -812,4 +1103,51 @@ void launch_dense_sum(const float* lists, int nlists, uint64_t list_stride, int 
   count_launch();
 }
 
+}  // namespace fcb
+
+namespace fcb {
+// ------------------------------------------------------------- diagnostics ---
+// Reference streaming kernels for roofline calibration (not on the hot path):
+// the EF pass's access pattern without any of its work.
+__global__ void __launch_bounds__(kThreads) k_triad(const float4* __restrict__ a,
+                                                    float4* __restrict__ b, uint64_t n4) {
+  constexpr int U = 8;
+  const uint64_t stride = (uint64_t)gridDim.x * kThreads;
+  for (uint64_t i0 = blockIdx.x * (uint64_t)kThreads + threadIdx.x; i0 < n4; i0 += stride * U) {
+    float4 x[U], y[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = i0 + u * stride;
+      if (i < n4) {
+        x[u] = __ldcs(a + i);
+        y[u] = __ldcs(b + i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = i0 + u * stride;
+      if (i < n4) {
+        y[u].x += x[u].x;
+        y[u].y += x[u].y;
+        y[u].z += x[u].z;
+        y[u].w += x[u].w;
+        __stcs(b + i, y[u]);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_fill_zero(float4* __restrict__ b, uint64_t n4) {
+  for (uint64_t i = blockIdx.x * (uint64_t)kThreads + threadIdx.x; i < n4;
+       i += (uint64_t)gridDim.x * kThreads)
+    __stcs(b + i, make_float4(0.f, 0.f, 0.f, 0.f));
+}
+
+void launch_triad(const float* a, float* b, uint64_t n, int blocks_per_sm, cudaStream_t s) {
+  k_triad<<<num_sms() * blocks_per_sm, kThreads, 0, s>>>(reinterpret_cast<const float4*>(a),
+                                                          reinterpret_cast<float4*>(b), n / 4);
+}
+void launch_fill_zero(float* b, uint64_t n, int blocks_per_sm, cudaStream_t s) {
+  k_fill_zero<<<num_sms() * blocks_per_sm, kThreads, 0, s>>>(reinterpret_cast<float4*>(b), n / 4);
+}
 }  // namespace fcb

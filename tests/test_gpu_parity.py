@@ -325,3 +325,72 @@ def test_c3_size_properties(fc, f32, c):
     ties_in = np.nonzero(sel & (key == tmin))[0]
     if ties_out.size:
         assert ties_in.max() < ties_out.min()
+
+
+# ------------------------------------------- owed zeros / NCCL single rank --
+
+@pytest.mark.parametrize("kind", ["star", "var", "ag"])
+def test_owed_zeros_applied_by_next_pass(fc, f32, kind):
+    """Residuals are NOT read between steps, so every step's residual zeroing
+    travels as owed zeros into the next error-feedback pass; the aggregates of
+    every step and the final residuals must still be bit-exact."""
+    n, g = 3, 70_001
+    with fc.Cluster(n, g) as cl:
+        res = np.zeros((n, g), np.float32)
+        for s in range(6):
+            c = [0.01, 0.05, 0.002][s % 3]
+            g_o = np.stack([f32.synth(g, 77, r, s, s % 3) for r in range(n)])
+            for r in range(n):
+                cl.fill_synthetic(r, 77, r, s, s % 3)
+            if kind == "ag":
+                cl.ag_step(c)
+                agg = f32.ag_step(g_o, res, c)
+            else:
+                mode = fc.STAR if kind == "star" else fc.VAR
+                st = cl.artopk_step(c, mode, fc.RING, s, fc.AVG)
+                agg, sel, _, _ = f32.artopk_step(g_o, res, c, mode, s, 1)
+                assert st.selected_rank == sel
+            assert_bitwise(cl.aggregate(), agg, f"{kind} aggregate step {s}")
+        for r in range(n):
+            assert_bitwise(cl.residual(r), res[r], f"{kind} final residual r{r}")
+
+
+@pytest.mark.parametrize("kind", ["star", "var", "ag", "dense"])
+def test_nccl_single_rank_path(fc, f32, kind):
+    """The one-process-per-GPU (NCCL) code path at world size 1."""
+    g = 123_457
+    uid = fc.get_unique_id()
+    with fc.Cluster.nccl(1, 0, uid, g, device=0, max_cr=0.2) as cl:
+        res = np.zeros((1, g), np.float32)
+        for s in range(4):
+            c = [0.01, 0.1][s % 2]
+            g_o = f32.synth(g, 5, 0, s)[None, :]
+            cl.fill_synthetic(0, 5, 0, s)
+            if kind == "ag":
+                cl.ag_step(c)
+                agg = f32.ag_step(g_o, res, c)
+            elif kind == "dense":
+                cl.dense_step(fc.RING, fc.AVG)
+                agg = f32.dense(g_o, 1)
+            else:
+                mode = fc.STAR if kind == "star" else fc.VAR
+                st = cl.artopk_step(c, mode, fc.RING, s, fc.AVG)
+                agg, sel, _, _ = f32.artopk_step(g_o, res, c, mode, s, 1)
+                assert st.selected_rank == sel == 0
+            assert_bitwise(cl.aggregate(), agg, f"{kind} nccl aggregate step {s}")
+        if kind != "dense":
+            assert_bitwise(cl.residual(0), res[0], "nccl residual")
+
+
+def test_residual_pointer_and_snapshot_materialise(fc, f32):
+    n, g = 2, 40_000
+    with fc.Cluster(n, g) as cl:
+        for r in range(n):
+            cl.fill_synthetic(r, 8, r, 0)
+        cl.artopk_step(0.01, fc.STAR, fc.RING, 0)
+        cl.snapshot()  # must include the owed zeros
+        a1 = [cl.residual(r).copy() for r in range(n)]
+        cl.artopk_step(0.01, fc.STAR, fc.RING, 1)
+        cl.restore()
+        for r in range(n):
+            assert_bitwise(cl.residual(r), a1[r], "restored residual")

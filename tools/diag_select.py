@@ -1,0 +1,21 @@
+"""Phase timing of the cooperative select kernel (block 0, %globaltimer)."""
+import ctypes as C
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2312_02493_b200 import flexcomm as fc  # noqa: E402
+from paper_2312_02493_b200._abi import check, lib  # noqa: E402
+
+G = int(sys.argv[1]) if len(sys.argv) > 1 else 138_000_000
+cr = float(sys.argv[2]) if len(sys.argv) > 2 else 0.01
+names = ["staged", "digit1", "digit2", "digit3", "counted", "emitted", "end"]
+with fc.Cluster(1, G, max_cr=max(cr, 0.1)) as cl:
+    cl.fill_synthetic(0, 42, 0, 0)
+    for s in range(4):
+        st = cl.artopk_step(cr, fc.STAR, fc.RING, s)
+        t = (C.c_uint64 * 8)()
+        check(lib.fc_diag_select_phases(cl._ctx, 0, t))
+        ws = cl.worker_stats(0)
+        print(f"step {s}: total {st.ms_total * 1e3:.0f}us select {st.ms_select * 1e3:.0f}us cand {ws.candidates} "
+              + " ".join(f"{n}={(t[i + 1] - t[i]) / 1e3:.1f}us" for i, n in enumerate(names)))
