@@ -1,0 +1,103 @@
+"""Multi-GPU parity of the NCCL path (one process per GPU).
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 --master-port P tests/mp_check.py
+
+Every rank runs a trajectory of STAR/VAR AR-Top-k (Ring and Tree) and
+AG-Top-k steps on its own synthetic gradient; rank 0 regenerates all ranks'
+gradients (the generator is counter-based) and checks against the fp32
+oracle:
+  * selected rank, residuals and the AG aggregate: bit-exact;
+  * AR aggregates: NCCL's ring/tree summation order differs from the
+    reference's rank-ascending order, so |gpu - oracle| <= 1e-5 * mean_r |c_r|
+    (the north star's 1e-5 relative bar, cancellation-safe).
+Exit code 0 on success.
+"""
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import oracle  # noqa: E402
+from paper_2312_02493_b200 import dist  # noqa: E402
+from paper_2312_02493_b200 import flexcomm as fc  # noqa: E402
+
+
+def main() -> int:
+    env = dist.init_from_env("gloo")
+    import torch
+
+    torch.cuda.set_device(env.local_rank)
+    uid = dist.share_nccl_uid(env)
+    G = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_003
+    f32 = oracle.F32() if env.rank == 0 else None
+    plan = [("star", fc.RING, 0.01), ("star", fc.TREE, 0.05), ("var", fc.RING, 0.01),
+            ("var", fc.TREE, 0.002), ("ag", fc.RING, 0.01), ("ag", fc.RING, 0.1),
+            ("star", fc.RING, 0.001), ("dense", fc.TREE, 1.0)]
+    failures = []
+    with fc.Cluster.nccl(env.world, env.rank, uid, G, device=env.local_rank, max_cr=0.2) as cl:
+        res = np.zeros((env.world, G), np.float32) if env.rank == 0 else None
+        for s, (kind, algo, c) in enumerate(plan):
+            cl.fill_synthetic(0, 1234, env.rank, s)
+            sel = -1
+            if kind == "ag":
+                cl.ag_step(c)
+            elif kind == "dense":
+                cl.dense_step(algo, fc.AVG)
+            else:
+                st = cl.artopk_step(c, fc.STAR if kind == "star" else fc.VAR, algo, s, fc.AVG)
+                sel = st.selected_rank
+            agg = cl.aggregate()
+            mine = cl.residual(0)
+            aggs = env.gather_arrays(agg)
+            resid = env.gather_arrays(mine)
+            sels = env.gather_arrays(np.array([sel]))
+            if env.rank != 0:
+                continue
+            g_o = np.stack([f32.synth(G, 1234, r, s) for r in range(env.world)])
+            if kind == "ag":
+                ref = f32.ag_step(g_o, res, c)
+                exact = True
+            elif kind == "dense":
+                ref = f32.dense(g_o, 1)
+                exact = False
+            else:
+                ge = g_o + res  # the error-fed gradients (for the tolerance scale)
+                ref, rsel, _, _ = f32.artopk_step(g_o, res, c, 0 if kind == "star" else 1, s, 1)
+                if any(int(x[0]) != rsel for x in sels):
+                    failures.append(f"step {s} {kind}: selected {[int(x[0]) for x in sels]} != {rsel}")
+                exact = False
+            for r in range(env.world):
+                if kind != "dense" and not np.array_equal(resid[r].view(np.uint32), res[r].view(np.uint32)):
+                    failures.append(f"step {s} {kind}: residual of rank {r} differs")
+                if exact:
+                    if not np.array_equal(aggs[r].view(np.uint32), ref.view(np.uint32)):
+                        failures.append(f"step {s} {kind}: aggregate on rank {r} not bit-exact")
+                else:
+                    base = g_o if kind == "dense" else ge
+                    scale = np.abs(base).sum(axis=0) / env.world
+                    if (kind != "dense"):
+                        scale = np.where(ref != 0, scale, 0)
+                    err = np.abs(aggs[r].astype(np.float64) - ref)
+                    if not np.all(err <= 1e-5 * scale + 1e-30):
+                        failures.append(f"step {s} {kind}: aggregate on rank {r} off by {err.max():.3g}")
+                    if kind != "dense" and not np.array_equal(aggs[r] != 0, ref != 0):
+                        # support = the broadcast index set (zeros elsewhere)
+                        nz = np.nonzero((aggs[r] != 0) != (ref != 0))[0]
+                        if np.any(np.abs(ref[nz]) > 0):
+                            failures.append(f"step {s} {kind}: aggregate support differs")
+            print(f"[mp_check] step {s} {kind} algo={algo} c={c} ok={not failures}", flush=True)
+    if env.rank == 0:
+        print("MP_CHECK", "PASS" if not failures else "FAIL", env.world, flush=True)
+        for f in failures[:20]:
+            print("  ", f)
+    env.close()
+    return 0 if not failures else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())
