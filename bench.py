@@ -33,6 +33,9 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+# NCCL prints a version banner on stdout at INFO/VERSION level; the contract
+# is one JSON line on stdout
+os.environ.setdefault("NCCL_DEBUG", "WARN")
 
 MODES = {"star": 0, "var": 1, "ag": 2, "dense": 3}
 ALGOS = {"ring": 0, "tree": 1}
@@ -274,25 +277,26 @@ def main():
     per_step = max_over_ranks((time.time() - t_w) / 5)
     clocks = ClockSampler(local)
     clocks.start()
-    # the timed region is short (K steps of well under a millisecond): keep
-    # the GPU busy with identical steps for ~1.5 s around it so nvidia-smi
-    # sees the clocks under this load (same count on every rank)
-    n_soak = int(min(20_000, max(50, 1.5 / max(per_step, 1e-5))))
-    for s in range(n_soak):
-        step(10_000 + s)
     cl.ef_kernel_timing(reset=True)
     l0 = fc.lib.fc_launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     ev0.record(stream)
     for s in range(a.steps):
-        step(a.warmup + s)
+        step(a.warmup + 5 + s)
     ev1.record(stream)
     barrier()
     ms_local = ev0.elapsed_time(ev1) / a.steps
     launches = fc.lib.fc_launch_count() - l0
-    clk = clocks.stop()
     ef_ms, ef_n = cl.ef_kernel_timing()
+    # the timed region is short (K steps of well under a millisecond): keep the
+    # same load running ~1.5 s longer so nvidia-smi samples the clocks under it
+    # (same step count on every rank; not part of the timed number)
+    n_soak = int(min(20_000, max(50, 1.5 / max(per_step, 1e-5))))
+    for s in range(n_soak):
+        step(10_000 + s)
+    barrier()
+    clk = clocks.stop()
     ms = max_over_ranks(ms_local)
 
     # ---- end-to-end through the public API with host buffers --------------

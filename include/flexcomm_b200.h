@@ -71,6 +71,11 @@ typedef enum fc_memkind { FC_HOST = 0, FC_DEVICE = 1 } fc_memkind;
 /* creation flags */
 #define FC_FLAG_ASYNC 0x1u        /* do not synchronize at the end of a step      */
 #define FC_FLAG_NO_TIMING 0x2u    /* skip per-phase CUDA events                   */
+#define FC_FLAG_DENSE_DECODE 0x4u /* always rewrite the whole aggregate; otherwise
+                                     AR steps at k <= G/128 update it in place (zero
+                                     the previous support, write the new one), so
+                                     callers must treat fc_aggregate_ptr() memory
+                                     as read-only                                 */
 
 #define FC_NCCL_UID_BYTES 128
 

@@ -103,6 +103,9 @@ struct fc_ctx {
   unsigned* ag_recv = nullptr;
   unsigned* bounds = nullptr;  // nlists x (nch + 1)
   unsigned* zmaps = nullptr;   // n_local x (nch * 32) zero maps
+  unsigned* agg_support = nullptr;  // indices of agg's nonzero support (incremental decode)
+  uint64_t agg_support_k = 0;
+  bool agg_incr = false;            // agg == densify(agg_support) and zmap 0 == its bits
   double* dnorms = nullptr;
   double* h_norms = nullptr;  // pinned
   bool has_agg = false;
@@ -374,6 +377,10 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
   const uint64_t nl = std::max<uint64_t>(N, (uint64_t)c->world);
   TRY(c->alloc(&c->bounds, nl * (c->nch + 1)));
   TRY(c->alloc(&c->zmaps, N * c->nch * 32));
+  TRY(c->alloc(&c->agg_support, c->kmax));
+  CUDA_TRY(cudaMemsetAsync(c->zmaps, 0, N * c->nch * 32 * sizeof(unsigned), c->stream));
+  c->agg_incr = !(o->flags & FC_FLAG_DENSE_DECODE);  // zero agg == densify(empty support)
+  c->agg_support_k = 0;
   if (c->nccl) {
     TRY(c->alloc(&c->reduced, c->kmax));
     TRY(c->alloc(&c->bidx, c->kmax));
@@ -798,14 +805,26 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
   record(c, 3);
 
   // (4) densify (core.hpp:72-81); /N for Avg (collectives.hpp:85-87)
-  fcb::launch_bounds(bsrc, k, 0, 1, c->G, c->bounds, c->stream);
-  if (c->nccl)
-    fcb::launch_decode_ar(bsrc, c->bounds, c->reduced, 1, 0, op == FC_AVG, (float)N, c->agg, c->G,
-                          c->zmaps, c->stream);
-  else
-    fcb::launch_decode_ar(bsrc, c->bounds, c->contrib_all, N, c->kmax, op == FC_AVG, (float)N,
-                          c->agg, c->G, c->zmaps, c->stream);
+  const float* lists = c->nccl ? c->reduced : c->contrib_all;
+  const int nlists = c->nccl ? 1 : N;
+  const uint64_t lstride = c->nccl ? 0 : c->kmax;
+  // in-place update costs ~2k random sector RMWs: worth it below ~G/128
+  const bool incr_ok = !(c->flags & FC_FLAG_DENSE_DECODE) && k * 128 <= c->G;
+  if (incr_ok && c->agg_incr) {
+    // in place: zero the previous support, write this one (same dense content)
+    fcb::launch_agg_update(c->agg_support, c->agg_support_k, bsrc, k, lists, nlists, lstride,
+                           op == FC_AVG, (float)N, c->agg, c->zmaps, c->agg_support, c->stream);
+  } else {
+    fcb::launch_bounds(bsrc, k, 0, 1, c->G, c->bounds, c->stream);
+    fcb::launch_decode_ar(bsrc, c->bounds, lists, nlists, lstride, op == FC_AVG, (float)N, c->agg,
+                          c->G, c->zmaps, c->stream);
+    if (incr_ok)
+      CUDA_TRY(cudaMemcpyAsync(c->agg_support, bsrc, k * sizeof(unsigned), cudaMemcpyDeviceToDevice,
+                               c->stream));
+  }
   LAUNCHED();
+  c->agg_incr = incr_ok;
+  c->agg_support_k = incr_ok ? k : 0;
   record(c, 4);
   c->has_agg = true;
   for (auto& w : c->w) {  // every worker owes zeros at the broadcast indices
@@ -857,6 +876,7 @@ int fc_ag_step(fc_ctx* c, double cr, int compressor, fc_step_stats* st) {
   fcb::launch_decode_ag(packs, stride, k, N, c->bounds, (float)N, c->agg, c->G, c->zmaps,
                         c->nccl ? c->rank : 0, c->n_local, c->stream);
   LAUNCHED();
+  c->agg_incr = false;  // the aggregate's support is now a union of N lists
   record(c, 4);
   c->has_agg = true;
   // residual_update (compress.hpp:122-130): g_e - g_e = +0 at own indices
@@ -894,6 +914,7 @@ int fc_dense_step(fc_ctx* c, int algo, int op, fc_step_stats* st) {
     fcb::launch_dense_sum(c->g_o_all, N, c->gstride, op == FC_AVG, (float)N, c->agg, c->G, c->stream);
   }
   LAUNCHED();
+  c->agg_incr = false;
   record(c, 4);
   c->has_agg = true;
   const double bus = N > 1 ? 2.0 * (N - 1) / N * 4.0 * c->G : 0.0;

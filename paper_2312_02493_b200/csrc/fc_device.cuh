@@ -93,6 +93,12 @@ void launch_gather(const unsigned* bidx, uint64_t k, const float* ge, float* con
 void launch_bounds(const unsigned* idx, uint64_t k, uint64_t list_stride, int nlists, uint64_t G,
                    unsigned* bounds, cudaStream_t s);
 void launch_zero_at(const unsigned* idx, uint64_t k, float* ge, cudaStream_t s);
+// Incremental AR decode: zero the previous support `prev` (kp indices), write
+// this step's k values at idx (loopback: rank-ascending sum of nlists lists),
+// keep the new support in `keep` (may alias prev); owed-zero bits follow.
+void launch_agg_update(const unsigned* prev, uint64_t kp, const unsigned* idx, uint64_t k,
+                       const float* lists, int nlists, uint64_t list_stride, int divide,
+                       float divisor, float* agg, unsigned* zmap, unsigned* keep, cudaStream_t s);
 // Decodes also write the zero map(s) of the decoded index list(s).
 void launch_decode_ar(const unsigned* idx, const unsigned* bounds, const float* lists, int nlists,
                       uint64_t list_stride, int divide, float divisor, float* agg, uint64_t G,

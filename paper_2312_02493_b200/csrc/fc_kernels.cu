@@ -202,7 +202,8 @@ __global__ void __launch_bounds__(kThreads) k_sample(const float* __restrict__ g
     if (s_h[b]) atomicAdd(&ctl->hist_s[b], s_h[b]);
   if (!last_block_done(&ctl->done_sample)) return;
   const double mean = (double)k / (double)G * (double)kSamples;
-  const double target = 1.5 * mean + 6.0 * sqrt(mean) + 8.0;
+  // 6 sigma of sampling noise plus 15 %: a miss only costs the fallback
+  const double target = 1.15 * mean + 6.0 * sqrt(mean) + 8.0;
   unsigned Ld = 0;
   if (force_fb) {
     Ld = kBins1 - 1;
@@ -520,21 +521,29 @@ void launch_fallback(float* ge, uint64_t G, uint64_t k, Ctl* ctl, const ChunkWs&
 }
 
 // ------------------------------------------------------------------ select ---
-// One cooperative kernel (all blocks resident, grid barriers between phases)
-// turns the candidate runs into the exact, index-ordered top-k:
-//   A/B/C  radix digits 2..4 of the threshold T (key bits 18..11, 10..3,
-//          2..0) over the candidates of digit-1 bucket b1 (from the EF pass);
-//          every block derives the same digit from the global histogram
-//   D      per-chunk counts of candidates > T and == T, block totals
-//   E      each block's prefix over earlier blocks' totals, then every
-//          thread writes its chunks' selected (index, value) pairs in index
-//          order; ties at T are kept lowest index first
-//          (min(eq, max(0, needT - eq_before)) per chunk)
-// Block b owns a contiguous range of chunks, thread t a contiguous sub-range,
-// so all prefixes are plain scans (no look-back chains).
+// One cooperative kernel (one resident 1024-thread block per SM, grid
+// barriers between phases) turns the candidate runs into the exact,
+// index-ordered top-k:
+//   digits  three radix digits of the threshold key T (bits 30..19, 18..11,
+//           10..0) over the candidates (lower digits only over candidates
+//           whose higher digits match); after each grid barrier every block
+//           derives the same digit from the global histogram
+//   count   per-chunk counts of candidates > T and == T; block totals
+//   emit    each block's prefix over earlier blocks' totals, then the
+//           selected (index, value) pairs in index order; ties at T are kept
+//           lowest index first: a chunk keeps min(eq, max(0, needT - eq_before))
+// Block b owns a contiguous range of chunks.  Short runs (sparse candidates)
+// are walked one chunk per thread; long runs one chunk per warp with
+// coalesced 128-byte accesses, ballot compaction and match-aggregated
+// histogram atomics.  A block's runs are staged in shared memory when they fit.
 namespace cg = cooperative_groups;
+constexpr int kSelThreads = 1024;
+constexpr int kSelWarps = kSelThreads / 32;
 constexpr int kSelBins = 4096;
-constexpr int kSelGridMax = 4096;
+constexpr int kSelMaxCpb = 8192;             // chunks per block (G < 2^31 on 148 SMs)
+constexpr unsigned kSelSmemMax = 200 * 1024;  // dynamic shared memory per block
+constexpr int kSelQ = 8;                      // float4 loads in flight (thread mode)
+constexpr unsigned kSelDense = 48;            // mean run length for warp-per-chunk mode
 
 __device__ __forceinline__ unsigned long long pack_ge(unsigned long long gt, unsigned long long eq) {
   return (gt << 31) | eq;
@@ -575,14 +584,11 @@ __device__ __forceinline__ unsigned comp(const uint4& v, int e) {
   return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
 }
 
-constexpr int kSelThreads = 1024;   // one block per SM: cheap grid barriers
-constexpr int kSelMaxCpb = 16384;   // chunks per block (G < 2^31 on 148 SMs)
-constexpr unsigned kSelSmemMax = 200 * 1024;
-constexpr int kSelQ = 8;            // float4 loads in flight per thread per round
-
+// bytes of the per-chunk arrays: s_pre (u64) | s_cnt | s_off | s_ge (u32)
+__host__ __device__ inline unsigned sel_arrays_bytes(unsigned cpb) { return (cpb * 20u + 15u) & ~15u; }
 __host__ __device__ inline unsigned sel_cache_cap(unsigned cpb) {
-  const unsigned arrays = cpb * 12u;
-  return arrays >= kSelSmemMax ? 0u : ((kSelSmemMax - arrays) / 4u) & ~3u;
+  const unsigned a = sel_arrays_bytes(cpb);
+  return a >= kSelSmemMax ? 0u : ((kSelSmemMax - a) / 4u) & ~3u;
 }
 
 __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __restrict__ ctl,
@@ -591,89 +597,147 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char s_dyn[];
   __shared__ unsigned s_h[kSelBins];
-  __shared__ unsigned long long s_scan[kSelThreads / 32 + 1];
-  __shared__ unsigned long long s_red[kSelThreads / 32];
-  __shared__ double s_dred[kSelThreads / 32];
-  __shared__ int s_cached;
-  __shared__ unsigned s_used;  // cache values in use (padded)
-  const int tid = threadIdx.x;
+  __shared__ unsigned long long s_scan[kSelWarps + 1];
+  __shared__ unsigned long long s_red[kSelWarps];
+  __shared__ double s_dred[kSelWarps];
+  __shared__ unsigned s_used, s_cached, s_dense;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt = lanemask_lt();
   SEL_MARK(0);
   const unsigned nch = w.nchunks;
   const unsigned cpb = (nch + gridDim.x - 1) / gridDim.x;
-  const unsigned c0 = min(nch, blockIdx.x * cpb), c1 = min(nch, c0 + cpb);
+  const unsigned c0 = min(nch, blockIdx.x * cpb), c1 = min(nch, c0 + cpb), nc = c1 - c0;
+  unsigned long long* s_pre = reinterpret_cast<unsigned long long*>(s_dyn);  // per chunk
+  unsigned* s_cnt = reinterpret_cast<unsigned*>(s_pre + cpb);
+  unsigned* s_off = s_cnt + cpb;
+  unsigned* s_ge = s_off + cpb;
   const unsigned cache_cap = sel_cache_cap(cpb);
-  float* s_val = reinterpret_cast<float*>(s_dyn);                 // cache_cap
-  unsigned* s_cnt = reinterpret_cast<unsigned*>(s_val + cache_cap);  // cpb
-  unsigned* s_off = s_cnt + cpb;                                  // cpb (16-B aligned offsets)
-  unsigned* s_ge = s_off + cpb;                                   // cpb: (gt << 16) | eq
-  const unsigned cpt = (cpb + kSelThreads - 1) / kSelThreads;
-  const unsigned t0 = min(c1, c0 + tid * cpt), t1 = min(c1, t0 + cpt);
+  float* s_val = reinterpret_cast<float*>(s_dyn + sel_arrays_bytes(cpb));
 
-  // ---- stage: chunk counts, and the block's candidate values if they fit ----
-  unsigned mysum = 0;
-  for (unsigned c = t0; c < t1; ++c) {
-    const unsigned n = __ldcg(w.cnt + c);
-    s_cnt[c - c0] = n;
-    mysum += (n + 3u) & ~3u;
-  }
+  // ---- stage: counts, cache offsets, mode ----
+  for (unsigned i = tid; i < nc; i += kSelThreads) s_cnt[i] = __ldcg(w.cnt + c0 + i);
+  __syncthreads();
+  const unsigned cpt = (cpb + kSelThreads - 1) / kSelThreads;
+  const unsigned t0 = min(nc, tid * cpt), t1 = min(nc, t0 + cpt);  // local chunk range
   {
-    const unsigned long long ex = block_excl_scan<kSelThreads>(mysum, s_scan);
-    if (tid == 0) {
-      s_cached = s_scan[kSelThreads / 32] <= (unsigned long long)cache_cap;
-      s_used = (unsigned)s_scan[kSelThreads / 32];
+    unsigned padded = 0, raw = 0;
+    for (unsigned c = t0; c < t1; ++c) {
+      padded += (s_cnt[c] + 3u) & ~3u;
+      raw += s_cnt[c];
     }
+    const unsigned long long ex = block_excl_scan<kSelThreads>(padded, s_scan);
+    const unsigned long long tot = s_scan[kSelWarps];
     unsigned o = (unsigned)ex;
     for (unsigned c = t0; c < t1; ++c) {
-      s_off[c - c0] = o;
-      o += (s_cnt[c - c0] + 3u) & ~3u;
+      s_off[c] = o;
+      o += (s_cnt[c] + 3u) & ~3u;
+    }
+    const unsigned long long rawtot = block_sum_u64<kSelThreads>(raw, s_red);
+    if (tid == 0) {
+      s_used = (unsigned)tot;
+      s_cached = tot <= cache_cap;
+      s_dense = rawtot > (unsigned long long)kSelDense * nc;
     }
   }
   __syncthreads();
-  const bool cached = s_cached != 0;
+  const bool cached = s_cached != 0, dense = s_dense != 0;
+  const float* gval = w.cand_val + ((uint64_t)c0 << kChunkShift);
+  const unsigned* gidx = w.cand_idx + ((uint64_t)c0 << kChunkShift);
   if (cached) {
-    // each thread stages its own runs: up to kSelQ 16-byte loads in flight
-    for (unsigned c = t0; c < t1; ++c) {
-      const unsigned n4 = (s_cnt[c - c0] + 3) >> 2;
-      const float4* v4 = reinterpret_cast<const float4*>(w.cand_val + ((uint64_t)c << kChunkShift));
-      float4* d4 = reinterpret_cast<float4*>(s_val + s_off[c - c0]);
-      for (unsigned q0 = 0; q0 < n4; q0 += kSelQ) {
-        float4 x[kSelQ];
+    if (dense) {  // warp per chunk, 4 chunks per round
+      for (unsigned cb = warp; cb < nc; cb += kSelWarps * 4) {
 #pragma unroll
-        for (int u = 0; u < kSelQ; ++u)
-          if (q0 + u < n4) x[u] = __ldcg(v4 + q0 + u);
+        for (int u = 0; u < 4; ++u) {
+          const unsigned c = cb + u * kSelWarps;
+          if (c >= nc) break;
+          const unsigned n = s_cnt[c];
+          const float* src = gval + ((uint64_t)c << kChunkShift);
+          float* dst = s_val + s_off[c];
+          for (unsigned p = lane; p < n; p += 32) dst[p] = __ldcg(src + p);
+        }
+      }
+    } else {  // thread per chunk, up to kSelQ 16-byte loads in flight
+      for (unsigned c = t0; c < t1; ++c) {
+        const unsigned n4 = (s_cnt[c] + 3) >> 2;
+        const float4* v4 = reinterpret_cast<const float4*>(gval + ((uint64_t)c << kChunkShift));
+        float4* d4 = reinterpret_cast<float4*>(s_val + s_off[c]);
+        for (unsigned q0 = 0; q0 < n4; q0 += kSelQ) {
+          float4 x[kSelQ];
 #pragma unroll
-        for (int u = 0; u < kSelQ; ++u)
-          if (q0 + u < n4) d4[q0 + u] = x[u];
+          for (int u = 0; u < kSelQ; ++u)
+            if (q0 + u < n4) x[u] = __ldcg(v4 + q0 + u);
+#pragma unroll
+          for (int u = 0; u < kSelQ; ++u)
+            if (q0 + u < n4) d4[q0 + u] = x[u];
+        }
       }
     }
     __syncthreads();
   }
   SEL_MARK(1);
-  // f(x) for every candidate value this thread owns, in index order
-  auto visit_chunk = [&](unsigned c, auto&& f) {
-    const unsigned cnt = s_cnt[c - c0];
-    if (cached) {
-      const float* sv = s_val + s_off[c - c0];
-      for (unsigned i = 0; i < cnt; ++i) f(sv[i]);
-      return;
+
+  // value p of local chunk c
+  auto val_at = [&](unsigned c, unsigned p) -> float {
+    return cached ? s_val[s_off[c] + p] : __ldcg(gval + ((uint64_t)c << kChunkShift) + p);
+  };
+  // thread mode: f(x) for every value of the thread's chunks
+  auto visit_thread = [&](auto&& f) {
+    for (unsigned c = t0; c < t1; ++c) {
+      const unsigned cnt = s_cnt[c];
+      if (cached) {
+        const float* sv = s_val + s_off[c];
+        for (unsigned i = 0; i < cnt; ++i) f(sv[i]);
+        continue;
+      }
+      const float4* v4 = reinterpret_cast<const float4*>(gval + ((uint64_t)c << kChunkShift));
+      const unsigned n4 = (cnt + 3) >> 2;
+      for (unsigned q0 = 0; q0 < n4; q0 += kSelQ) {
+        float4 x[kSelQ];
+#pragma unroll
+        for (int u = 0; u < kSelQ; ++u)
+          x[u] = q0 + u < n4 ? __ldcg(v4 + q0 + u) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < kSelQ; ++u)
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if ((q0 + u) * 4 + e < cnt) f(comp(x[u], e));
+      }
     }
-    const float4* v4 = reinterpret_cast<const float4*>(w.cand_val + ((uint64_t)c << kChunkShift));
-    const unsigned n4 = (cnt + 3) >> 2;
-    for (unsigned q0 = 0; q0 < n4; q0 += kSelQ) {
-      float4 x[kSelQ];
+  };
+  // warp mode: f(x, valid, u) for 4 chunks x 2 rounds of 32 values at a time
+  // (all lanes call f: warp-synchronous helpers may be used inside)
+  auto visit_warp = [&](auto&& begin_chunk, auto&& f) {
+    for (unsigned cb = warp; cb < nc; cb += kSelWarps * 4) {
+      unsigned n[4];
+      unsigned maxn = 0;
 #pragma unroll
-      for (int u = 0; u < kSelQ; ++u)
-        x[u] = q0 + u < n4 ? __ldcg(v4 + q0 + u) : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int u = 0; u < 4; ++u) {
+        const unsigned c = cb + u * kSelWarps;
+        n[u] = c < nc ? s_cnt[c] : 0u;
+        maxn = max(maxn, n[u]);
+        if (c < nc) begin_chunk(u, c);
+      }
+      for (unsigned r0 = 0; r0 < maxn; r0 += 64) {
+        float x[4][2];
 #pragma unroll
-      for (int u = 0; u < kSelQ; ++u)
+        for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-          if ((q0 + u) * 4 + e < cnt) f(comp(x[u], e));
+          for (int rr = 0; rr < 2; ++rr) {
+            const unsigned p = r0 + rr * 32 + lane;
+            x[u][rr] = p < n[u] ? val_at(cb + u * kSelWarps, p) : 0.f;
+          }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int rr = 0; rr < 2; ++rr) {
+            const unsigned p = r0 + rr * 32 + lane;
+            if (r0 + rr * 32 < n[u]) f(x[u][rr], p < n[u], u, cb + u * kSelWarps, r0 + rr * 32);
+          }
+      }
     }
   };
 
-  // ---- three radix digits of T: key bits 30..19 (all candidates), 18..11
-  // and 10..0 (only candidates whose higher digits match) ----
+  // ---- digits of T ----
   unsigned long long need = k;
   unsigned prefix = 0;  // key bits above the digit being resolved
   const int shifts[3] = {kShift1, 11, 0};
@@ -687,11 +751,20 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
     __syncthreads();
     const int sh = shifts[d], as = above_shift;
     const unsigned pf = prefix, dm = (unsigned)nb - 1;
-    for (unsigned c = t0; c < t1; ++c)
-      visit_chunk(c, [&](float x) {
+    if (dense) {
+      visit_warp([](int, unsigned) {},
+                 [&](float x, bool valid, int, unsigned, unsigned) {
+                   const unsigned key = key_of(x);
+                   const unsigned bin = valid && (key >> as) == pf ? ((key >> sh) & dm) : 0xffffffffu;
+                   const unsigned m = __match_any_sync(0xffffffffu, bin);
+                   if (bin != 0xffffffffu && (m & lt) == 0) atomicAdd(&s_h[bin], __popc(m));
+                 });
+    } else {
+      visit_thread([&](float x) {
         const unsigned key = key_of(x);
         if ((key >> as) == pf) atomicAdd(&s_h[(key >> sh) & dm], 1u);
       });
+    }
     flush_hist(s_h, ghs[d], nb);
     grid.sync();
     SEL_MARK(2 + d);
@@ -711,99 +784,175 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
     ctl->count_gt = k - needT;
   }
 
-  // ---- D: per-chunk (gt, eq) and block totals ----
-  unsigned long long mine = 0;
-  for (unsigned c = t0; c < t1; ++c) {
-    unsigned gt = 0, eq = 0;
-    visit_chunk(c, [&](float x) {
-      const unsigned key = key_of(x);
-      gt += key > T;
-      eq += key == T;
-    });
-    s_ge[c - c0] = (gt << 16) | eq;
-    mine += pack_ge(gt, eq);
+  // ---- count: per-chunk (gt, eq), block-level chunk prefixes, block total ----
+  if (dense) {
+    unsigned gt[4], eq[4];
+    visit_warp(
+        [&](int u, unsigned) {
+          gt[u] = 0;
+          eq[u] = 0;
+        },
+        [&](float x, bool valid, int u, unsigned c, unsigned r) {
+          const unsigned key = key_of(x);
+          gt[u] += __popc(__ballot_sync(0xffffffffu, valid && key > T));
+          eq[u] += __popc(__ballot_sync(0xffffffffu, valid && key == T));
+          if (lane == 0 && r + 32 >= s_cnt[c]) s_ge[c] = (gt[u] << 16) | eq[u];
+        });
+    // chunks with no candidates were never visited
+    __syncthreads();
+    for (unsigned c = tid; c < nc; c += kSelThreads)
+      if (s_cnt[c] == 0) s_ge[c] = 0;
+  } else {
+    for (unsigned c = t0; c < t1; ++c) {
+      unsigned gt = 0, eq = 0;
+      const unsigned cnt = s_cnt[c];
+      if (cached) {
+        const float* sv = s_val + s_off[c];
+        for (unsigned i = 0; i < cnt; ++i) {
+          const unsigned key = key_of(sv[i]);
+          gt += key > T;
+          eq += key == T;
+        }
+      } else {
+        const float4* v4 = reinterpret_cast<const float4*>(gval + ((uint64_t)c << kChunkShift));
+        const unsigned n4 = (cnt + 3) >> 2;
+        for (unsigned q0 = 0; q0 < n4; q0 += kSelQ) {
+          float4 x[kSelQ];
+#pragma unroll
+          for (int u = 0; u < kSelQ; ++u)
+            x[u] = q0 + u < n4 ? __ldcg(v4 + q0 + u) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int u = 0; u < kSelQ; ++u)
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if ((q0 + u) * 4 + e < cnt) {
+                const unsigned key = key_of(comp(x[u], e));
+                gt += key > T;
+                eq += key == T;
+              }
+        }
+      }
+      s_ge[c] = (gt << 16) | eq;
+    }
   }
-  const unsigned long long excl = block_excl_scan<kSelThreads>(mine, s_scan);
-  const unsigned long long blk_total = s_scan[kSelThreads / 32];
-  if (tid == 0) w.btot[blockIdx.x] = blk_total;
+  __syncthreads();
+  {
+    unsigned long long mine = 0;
+    for (unsigned c = t0; c < t1; ++c) mine += pack_ge(s_ge[c] >> 16, s_ge[c] & 0xFFFFu);
+    unsigned long long run = block_excl_scan<kSelThreads>(mine, s_scan);
+    if (tid == 0) w.btot[blockIdx.x] = s_scan[kSelWarps];
+    for (unsigned c = t0; c < t1; ++c) {
+      s_pre[c] = run;
+      run += pack_ge(s_ge[c] >> 16, s_ge[c] & 0xFFFFu);
+    }
+  }
+  const unsigned long long blk_total = s_scan[kSelWarps];
   grid.sync();
   SEL_MARK(5);
 
-  // ---- E: block prefix, ordered emission ----
+  // ---- emit ----
   unsigned long long bp = 0;
   for (unsigned i = tid; i < blockIdx.x; i += kSelThreads) bp += __ldcg(w.btot + i);
-  bp = block_sum_u64<kSelThreads>(bp, s_red);
-  unsigned long long before = bp + excl;
-  // The block's selected pairs form one contiguous range of the output:
-  // assemble it in shared memory, then write it out coalesced.
-  const unsigned long long bgt_pre = bp >> 31, beq_pre = bp & 0x7fffffffull;
-  const unsigned long long obase = bgt_pre + (beq_pre < needT ? beq_pre : needT);
-  const unsigned long long blk_eq = blk_total & 0x7fffffffull;
-  const unsigned long long nsel =
-      (blk_total >> 31) + (beq_pre >= needT ? 0ull : min(blk_eq, needT - beq_pre));
-  const bool staged = cached && (unsigned long long)s_used + 2 * nsel <= cache_cap;
-  unsigned* s_oidx = reinterpret_cast<unsigned*>(s_val + s_used);
-  float* s_oval = reinterpret_cast<float*>(s_oidx + (staged ? nsel : 0));
+  bp = block_sum_u64<kSelThreads>(bp, s_red);  // (also a barrier: s_pre visible)
   double acc = 0.0;
-  for (unsigned c = t0; c < t1; ++c) {
-    const unsigned pc = s_ge[c - c0];
-    const unsigned gt = pc >> 16, eq = pc & 0xFFFFu;
-    const unsigned long long gt_pre = before >> 31, eq_pre = before & 0x7fffffffull;
-    unsigned long long o = gt_pre + (eq_pre < needT ? eq_pre : needT);
-    const unsigned take = eq_pre >= needT ? 0u : (unsigned)min((unsigned long long)eq, needT - eq_pre);
-    before += pack_ge(gt, eq);
-    if (gt + take == 0) continue;
-    const unsigned cnt = s_cnt[c - c0];
-    const uint64_t slot = (uint64_t)c << kChunkShift;
-    const float4* v4 = reinterpret_cast<const float4*>(w.cand_val + slot);
-    const uint4* i4 = reinterpret_cast<const uint4*>(w.cand_idx + slot);
-    const float4* sv4 = reinterpret_cast<const float4*>(s_val + s_off[c - c0]);
-    const unsigned n4 = (cnt + 3) >> 2;
-    unsigned t = 0;
-    constexpr int QE = 4;
-    for (unsigned q0 = 0; q0 < n4; q0 += QE) {
-      float4 x[QE];
-      uint4 id[QE];
-#pragma unroll
-      for (int u = 0; u < QE; ++u) {
-        if (q0 + u < n4) {
-          x[u] = cached ? sv4[q0 + u] : __ldcg(v4 + q0 + u);
-          id[u] = __ldcg(i4 + q0 + u);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < QE; ++u) {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          if ((q0 + u) * 4 + e >= cnt) break;
-          const float xv = comp(x[u], e);
-          const unsigned key = key_of(xv);
-          bool sel = key > T;
-          if (key == T) {
-            sel = t < take;
-            ++t;
-          }
+  if (dense) {
+    unsigned long long o[4];
+    unsigned take[4], tseen[4];
+    visit_warp(
+        [&](int u, unsigned c) {
+          const unsigned long long before = bp + s_pre[c];
+          const unsigned long long gt_pre = before >> 31, eq_pre = before & 0x7fffffffull;
+          o[u] = gt_pre + (eq_pre < needT ? eq_pre : needT);
+          take[u] = eq_pre >= needT ? 0u
+                                    : (unsigned)min((unsigned long long)(s_ge[c] & 0xFFFFu), needT - eq_pre);
+          tseen[u] = 0;
+        },
+        [&](float x, bool valid, int u, unsigned c, unsigned r) {
+          const unsigned key = key_of(x);
+          const bool is_eq = valid && key == T;
+          const unsigned eqb = __ballot_sync(0xffffffffu, is_eq);
+          const bool sel = valid && (key > T || (is_eq && tseen[u] + __popc(eqb & lt) < take[u]));
+          const unsigned sb = __ballot_sync(0xffffffffu, sel);
           if (sel) {
-            if (staged) {
-              s_oidx[o - obase] = comp(id[u], e);
-              s_oval[o - obase] = xv;
-            } else {
-              out_idx[o] = comp(id[u], e);
-              out_val[o] = xv;
+            const unsigned long long pos = o[u] + __popc(sb & lt);
+            out_idx[pos] = __ldcg(gidx + ((uint64_t)c << kChunkShift) + r + lane);
+            out_val[pos] = x;
+            acc = fma((double)x, (double)x, acc);
+          }
+          o[u] += __popc(sb);
+          tseen[u] += __popc(eqb);
+        });
+  } else {
+    // the block's selected pairs form one contiguous output range: assemble
+    // it in shared memory when it fits, then write it out coalesced
+    const unsigned long long bgt_pre = bp >> 31, beq_pre = bp & 0x7fffffffull;
+    const unsigned long long obase = bgt_pre + (beq_pre < needT ? beq_pre : needT);
+    const unsigned long long blk_eq = blk_total & 0x7fffffffull;
+    const unsigned long long nsel =
+        (blk_total >> 31) + (beq_pre >= needT ? 0ull : min(blk_eq, needT - beq_pre));
+    const bool staged = cached && (unsigned long long)s_used + 2 * nsel <= cache_cap;
+    unsigned* s_oidx = reinterpret_cast<unsigned*>(s_val + s_used);
+    float* s_oval = reinterpret_cast<float*>(s_oidx + (staged ? nsel : 0));
+    for (unsigned c = t0; c < t1; ++c) {
+      const unsigned pc = s_ge[c];
+      const unsigned gt = pc >> 16, eq = pc & 0xFFFFu;
+      const unsigned long long before = bp + s_pre[c];
+      const unsigned long long gt_pre = before >> 31, eq_pre = before & 0x7fffffffull;
+      unsigned long long o = gt_pre + (eq_pre < needT ? eq_pre : needT);
+      const unsigned take = eq_pre >= needT ? 0u : (unsigned)min((unsigned long long)eq, needT - eq_pre);
+      if (gt + take == 0) continue;
+      const unsigned cnt = s_cnt[c];
+      const float4* v4 = reinterpret_cast<const float4*>(gval + ((uint64_t)c << kChunkShift));
+      const uint4* i4 = reinterpret_cast<const uint4*>(gidx + ((uint64_t)c << kChunkShift));
+      const float4* sv4 = reinterpret_cast<const float4*>(s_val + s_off[c]);
+      const unsigned n4 = (cnt + 3) >> 2;
+      unsigned t = 0;
+      constexpr int QE = 4;
+      for (unsigned q0 = 0; q0 < n4; q0 += QE) {
+        float4 x[QE];
+        uint4 id[QE];
+#pragma unroll
+        for (int u = 0; u < QE; ++u) {
+          if (q0 + u < n4) {
+            x[u] = cached ? sv4[q0 + u] : __ldcg(v4 + q0 + u);
+            id[u] = __ldcg(i4 + q0 + u);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < QE; ++u) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if ((q0 + u) * 4 + e >= cnt) break;
+            const float xv = comp(x[u], e);
+            const unsigned key = key_of(xv);
+            bool sel = key > T;
+            if (key == T) {
+              sel = t < take;
+              ++t;
             }
-            ++o;
-            acc = fma((double)xv, (double)xv, acc);
+            if (sel) {
+              if (staged) {
+                s_oidx[o - obase] = comp(id[u], e);
+                s_oval[o - obase] = xv;
+              } else {
+                out_idx[o] = comp(id[u], e);
+                out_val[o] = xv;
+              }
+              ++o;
+              acc = fma((double)xv, (double)xv, acc);
+            }
           }
         }
       }
     }
+    __syncthreads();
+    if (staged)
+      for (unsigned i = tid; i < nsel; i += kSelThreads) {
+        out_idx[obase + i] = s_oidx[i];
+        out_val[obase + i] = s_oval[i];
+      }
   }
-  const double bsum = block_sum<kSelThreads>(acc, s_dred);  // (also a barrier)
-  if (staged)
-    for (unsigned i = tid; i < nsel; i += kSelThreads) {
-      out_idx[obase + i] = s_oidx[i];
-      out_val[obase + i] = s_oval[i];
-    }
+  const double bsum = block_sum<kSelThreads>(acc, s_dred);
   if (tid == 0) w.bnorm[blockIdx.x] = bsum;
   SEL_MARK(6);
   grid.sync();
@@ -825,7 +974,7 @@ int launch_select(uint64_t k, Ctl* ctl, const ChunkWs& w, unsigned* out_idx, flo
   const int grid = num_sms();
   const unsigned cpb = (w.nchunks + grid - 1) / grid;
   if (cpb > (unsigned)kSelMaxCpb) return (int)cudaErrorInvalidValue;
-  const unsigned smem = cpb * 12u + sel_cache_cap(cpb) * 4u;
+  const unsigned smem = sel_arrays_bytes(cpb) + sel_cache_cap(cpb) * 4u;
   ChunkWs ws = w;
   void* args[] = {&k, &ctl, &ws, &out_idx, &out_val};
   const cudaError_t e = cudaLaunchCooperativeKernel((void*)k_select, dim3(grid), dim3(kSelThreads),
@@ -879,6 +1028,53 @@ void launch_gather(const unsigned* bidx, uint64_t k, const float* ge, float* con
                                      (uint64_t)num_sms() * 8);
   if (grid < 1) grid = 1;
   k_gather<<<grid, kThreads, 0, s>>>(bidx, k, ge, contrib, ctl, part);
+  count_launch();
+}
+
+// ------------------------------------------------------ incremental decode ---
+// The dense aggregate buffer is library-owned, so after the first full decode
+// it can be kept equal to densify(this step) by touching only the supports:
+// (1) the previous step's indices are zeroed (and their owed-zero bits
+// cleared), (2) this step's values are written (and their bits set).  For
+// k << G this replaces a 4G-byte dense write with ~2k random 4-byte writes;
+// the buffer content is identical to a full decode.
+__global__ void k_agg_clear(const unsigned* __restrict__ prev, uint64_t kp, float* __restrict__ agg,
+                            unsigned* __restrict__ zmap) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < kp;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned i = __ldcs(prev + j);
+    agg[i] = 0.0f;
+    atomicAnd(zmap + zmap_word(i), ~zmap_bit(i));
+  }
+}
+
+__global__ void k_agg_write(const unsigned* __restrict__ idx, uint64_t k,
+                            const float* __restrict__ lists, int nlists, uint64_t list_stride,
+                            int divide, float divisor, float* __restrict__ agg,
+                            unsigned* __restrict__ zmap, unsigned* __restrict__ keep) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < k;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned i = __ldcs(idx + j);
+    float v = lists[j];  // v = c_0; v += c_r (r ascending), collectives.hpp:82-87
+    for (int l = 1; l < nlists; ++l) v += lists[(uint64_t)l * list_stride + j];
+    if (divide) v = v / divisor;
+    agg[i] = v;
+    atomicOr(zmap + zmap_word(i), zmap_bit(i));
+    keep[j] = i;  // the support the next step clears
+  }
+}
+
+void launch_agg_update(const unsigned* prev, uint64_t kp, const unsigned* idx, uint64_t k,
+                       const float* lists, int nlists, uint64_t list_stride, int divide,
+                       float divisor, float* agg, unsigned* zmap, unsigned* keep, cudaStream_t s) {
+  if (kp) {
+    const unsigned g = (unsigned)std::min<uint64_t>((kp + kThreads - 1) / kThreads, num_sms() * 16ull);
+    k_agg_clear<<<g, kThreads, 0, s>>>(prev, kp, agg, zmap);
+    count_launch();
+  }
+  const unsigned g = (unsigned)std::min<uint64_t>((k + kThreads - 1) / kThreads, num_sms() * 16ull);
+  k_agg_write<<<g, kThreads, 0, s>>>(idx, k, lists, nlists, list_stride, divide, divisor, agg, zmap,
+                                      keep);
   count_launch();
 }
 
@@ -1025,10 +1221,12 @@ __global__ void __launch_bounds__(kThreads) k_decode_ag(const unsigned* __restri
                                                         uint64_t G, unsigned* __restrict__ zmaps,
                                                         int map_rank0, int nmaps) {
   __shared__ __align__(128) float tile[2][kDecTile];
-  extern __shared__ unsigned s_zm[];  // nmaps x kDecChunks*32
+  __shared__ unsigned s_touch[kDecTile / 32];  // union of the ranks' indices in the tile
+  extern __shared__ unsigned s_zm[];           // nmaps x kDecChunks*32
   const uint64_t ntd = (G + kDecTile - 1) >> kDecShift;
   const uint64_t nch = nchunks_of(G);
   const int zw = kDecChunks * 32;
+  const bool divide = divisor != 1.0f;
   int buf = 0, iter = 0;
   for (uint64_t t = blockIdx.x; t < ntd; t += gridDim.x, buf ^= 1, ++iter) {
     const uint64_t t0 = t << kDecShift;
@@ -1037,6 +1235,7 @@ __global__ void __launch_bounds__(kThreads) k_decode_ag(const unsigned* __restri
     float* tl = tile[buf];
     zero_tile(tl);
     for (int q = threadIdx.x; q < nmaps * zw; q += kThreads) s_zm[q] = 0u;
+    if (threadIdx.x < kDecTile / 32) s_touch[threadIdx.x] = 0u;
     __syncthreads();
     const uint64_t c0 = t * kDecChunks, c1 = min(c0 + kDecChunks, nch);
     for (int r = 0; r < nranks; ++r) {
@@ -1048,20 +1247,20 @@ __global__ void __launch_bounds__(kThreads) k_decode_ag(const unsigned* __restri
       const bool mapped = m >= 0 && m < nmaps;
       for (unsigned j = lo + threadIdx.x; j < hi; j += kThreads) {
         const unsigned p = id[j];
-        tl[p - (unsigned)t0] += va[j];
+        const unsigned lp = p - (unsigned)t0;
+        tl[lp] += va[j];
+        if (divide) atomicOr(&s_touch[lp >> 5], 1u << (lp & 31));
         if (mapped) atomicOr(&s_zm[m * zw + zmap_word(p) - (unsigned)(c0 << 5)], zmap_bit(p));
       }
       __syncthreads();
     }
-    float4* t4 = reinterpret_cast<float4*>(tl);
-#pragma unroll
-    for (int q = 0; q < kDecTile / 4 / kThreads; ++q) {
-      float4 x = t4[q * kThreads + threadIdx.x];
-      x.x = x.x / divisor;
-      x.y = x.y / divisor;
-      x.z = x.z / divisor;
-      x.w = x.w / divisor;
-      t4[q * kThreads + threadIdx.x] = x;
+    // every element /= N: untouched elements are +0 and 0/N = +0, so only the
+    // touched ones need the (IEEE, correctly rounded) division
+    if (divide && threadIdx.x < kDecTile / 32) {
+      for (unsigned b = s_touch[threadIdx.x]; b; b &= b - 1) {
+        float& x = tl[threadIdx.x * 32 + __ffs(b) - 1];
+        x = x / divisor;
+      }
     }
     emit_tile(agg, tl, t0, G);
     const unsigned nw = (unsigned)(c1 - c0) * 32;
