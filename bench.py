@@ -35,7 +35,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 # NCCL prints a version banner on stdout at INFO/VERSION level; the contract
 # is one JSON line on stdout
-os.environ.setdefault("NCCL_DEBUG", "WARN")
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 MODES = {"star": 0, "var": 1, "ag": 2, "dense": 3}
 ALGOS = {"ring": 0, "tree": 1}
@@ -309,19 +309,26 @@ def main():
         host_g.copy_(_tensor_from_ptr(cl.grad_ptr(0), G, local))  # setup only
         torch.cuda.synchronize()
         e2e_steps = max(3, min(a.steps, 10))
+        # Each step: upload of the step's gradient from pinned host memory,
+        # the sync step, download of the dense aggregate (the reference returns
+        # it by value).  The copies are queued on the copy engines, so step
+        # s's download overlaps step s+1's upload (PCIe is full duplex).
         for s in range(2):
-            cl.set_grad(0, host_g)
+            cl.set_grad(0, host_g, async_=True)
             step(s)
-            cl.aggregate(host_agg)
+            cl.aggregate(host_agg, async_=True)
+        cl.sync()
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for s in range(e2e_steps):
-            cl.set_grad(0, host_g)      # H2D of the step's gradient (pinned)
+            cl.set_grad(0, host_g, async_=True)
             step(100 + s)
-            cl.aggregate(host_agg)      # D2H of the dense aggregate (the result)
+            cl.aggregate(host_agg, async_=True)
+        cl.join()
         e1.record(stream)
         barrier()
+        cl.sync()
         e2e_ms = max_over_ranks(e0.elapsed_time(e1) / e2e_steps)
         e2e = {"value": round(e2e_ms, 4), "unit": "ms/step",
                "h2d_bytes_per_step": 4 * G, "d2h_bytes_per_step": 4 * G, "steps": e2e_steps}

@@ -66,7 +66,13 @@ typedef enum fc_reduce_op { FC_SUM = 0, FC_AVG = 1 } fc_reduce_op;
 /* inc/artopk.hpp:113 (only Exact is on the path; the others are §8f "next") */
 typedef enum fc_compressor { FC_EXACT = 0, FC_LAYERWISE = 1, FC_THRESHOLD = 2 } fc_compressor;
 /* memory kind of a caller pointer */
-typedef enum fc_memkind { FC_HOST = 0, FC_DEVICE = 1 } fc_memkind;
+/* FC_HOST_ASYNC: pinned host memory, the copy is queued on a copy engine and
+ * the call returns at once.  Uploads (fc_set_grad) are ordered after the
+ * previous step's error-feedback pass and before the next one; downloads
+ * (fc_get_aggregate) after the step's decode and before the next decode, so
+ * a caller can overlap step s's aggregate download with step s+1's gradient
+ * upload (PCIe is full duplex).  Host data is valid after fc_sync(). */
+typedef enum fc_memkind { FC_HOST = 0, FC_DEVICE = 1, FC_HOST_ASYNC = 2 } fc_memkind;
 
 /* creation flags */
 #define FC_FLAG_ASYNC 0x1u        /* do not synchronize at the end of a step      */
@@ -212,8 +218,11 @@ int fc_crossover_cr(double alpha, double bandwidth, double m_bytes, int n, int p
 int fc_derive_m_from_ag(double alpha, double bandwidth, double c, int n, double seconds,
                         double* m_out);
 
-/* Synchronize the context stream (for FC_FLAG_ASYNC users). */
+/* Synchronize the context's streams (for FC_FLAG_ASYNC / FC_HOST_ASYNC users). */
 int fc_sync(fc_ctx* ctx);
+/* Order the compute stream after every queued FC_HOST_ASYNC copy (so an event
+ * recorded on fc_stream() afterwards covers them). */
+int fc_join(fc_ctx* ctx);
 /* The context's CUDA stream (cudaStream_t), so callers can record their own
  * CUDA events around steps on the stream the kernels run on. */
 int fc_stream(fc_ctx* ctx, void** stream_out);

@@ -23,9 +23,10 @@ FC_STAR, FC_VAR = 0, 1
 FC_RING, FC_TREE = 0, 1
 FC_SUM, FC_AVG = 0, 1
 FC_EXACT, FC_LAYERWISE, FC_THRESHOLD = 0, 1, 2
-FC_HOST, FC_DEVICE = 0, 1
+FC_HOST, FC_DEVICE, FC_HOST_ASYNC = 0, 1, 2
 FC_FLAG_ASYNC = 0x1
 FC_FLAG_NO_TIMING = 0x2
+FC_FLAG_DENSE_DECODE = 0x4
 FC_NCCL_UID_BYTES = 128
 FC_DIST_NORMAL, FC_DIST_TIES, FC_DIST_LAYERED = 0, 1, 2
 
@@ -110,6 +111,7 @@ def _load() -> C.CDLL:
         "fc_dense_step": ([P, i, i, C.POINTER(fc_step_stats)], i),
         "fc_topk_exact": ([P, i, d, C.POINTER(fc_step_stats)], i),
         "fc_sync": ([P], i),
+        "fc_join": ([P], i),
         "fc_stream": ([P, C.POINTER(P)], i),
         "fc_ef_kernel_timing": ([P, C.POINTER(d), C.POINTER(u64), i], i),
         "fc_diag_kernel_ms": ([P, i, i, C.POINTER(d)], i),
@@ -137,7 +139,7 @@ EXPORTS = [
     "fc_set_grad", "fc_grad_ptr", "fc_fill_synthetic", "fc_set_residual", "fc_get_residual",
     "fc_residual_ptr", "fc_reset_residuals", "fc_get_aggregate", "fc_aggregate_ptr",
     "fc_get_topk", "fc_get_worker_stats", "fc_snapshot", "fc_restore", "fc_artopk_step",
-    "fc_ag_step", "fc_dense_step", "fc_topk_exact", "fc_sync", "fc_stream", "fc_ef_kernel_timing",
+    "fc_ag_step", "fc_dense_step", "fc_topk_exact", "fc_sync", "fc_join", "fc_stream", "fc_ef_kernel_timing",
     "fc_diag_kernel_ms", "fc_diag_select_phases",
     "fc_cost_primitives", "fc_select_collective", "fc_prefer", "fc_crossover_cr",
     "fc_derive_m_from_ag",

@@ -91,6 +91,13 @@ struct fc_ctx {
   bool nccl = false;
   ncclComm_t comm_ring = nullptr, comm_tree = nullptr;
   cudaStream_t stream = nullptr;
+  // FC_HOST_ASYNC copies: an upload stream and a download stream, ordered
+  // against the compute stream with events
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  std::vector<cudaEvent_t> ev_go_ready, ev_go_free;  // per worker: upload done / EF read g_o
+  std::vector<char> go_pending, go_read;
+  cudaEvent_t ev_agg_ready = nullptr, ev_agg_free = nullptr;  // decode done / download done
+  bool agg_pending = false, agg_written = false;
   std::vector<Worker> w;
   std::vector<void*> allocs;
   float* g_o_all = nullptr;
@@ -146,8 +153,38 @@ int check_worker(const fc_ctx* c, int worker) {
   return FC_OK;
 }
 
+// The compute stream must not read worker i's gradient before its async
+// upload landed (called before any kernel that reads g_o).
+int wait_grad(fc_ctx* c, int i) {
+  if (c->go_pending[i]) {
+    CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_go_ready[i], 0));
+    c->go_pending[i] = 0;
+  }
+  return FC_OK;
+}
+// ... and an async upload must not overwrite g_o before the EF pass read it.
+int grad_consumed(fc_ctx* c, int i) {
+  CUDA_TRY(cudaEventRecord(c->ev_go_free[i], c->stream));
+  c->go_read[i] = 1;
+  return FC_OK;
+}
+// A decode must not overwrite the aggregate while an async download reads it.
+int wait_agg_free(fc_ctx* c) {
+  if (c->agg_pending) {
+    CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_agg_free, 0));
+    c->agg_pending = false;
+  }
+  return FC_OK;
+}
+int agg_written(fc_ctx* c) {
+  CUDA_TRY(cudaEventRecord(c->ev_agg_ready, c->stream));
+  c->agg_written = true;
+  return FC_OK;
+}
+
 int copy_in(fc_ctx* c, float* dst, const float* src, int memkind) {
   if (!src) return fail(FC_ERR_INVALID_ARGUMENT, "null source pointer");
+  if (memkind == FC_HOST_ASYNC) return fail(FC_ERR_INVALID_ARGUMENT, "async copies only for gradients");
   CUDA_TRY(cudaMemcpyAsync(dst, src, c->G * sizeof(float),
                            memkind == FC_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                            c->stream));
@@ -191,6 +228,7 @@ int run_ef(fc_ctx* c, int i, uint64_t k, bool topk) {
   Worker& w = c->w[i];
   const bool force_fb = std::getenv("FC_FORCE_FALLBACK") != nullptr;
   CUDA_TRY(cudaMemsetAsync(w.ctl, 0, w.ctl_bytes, c->stream));
+  TRY(wait_grad(c, i));
   if (topk) {
     fcb::launch_sample(w.g_o, w.ge, c->G, k, w.ctl, 1, w.pz, force_fb ? 1 : 0, c->stream);
     LAUNCHED();
@@ -203,6 +241,7 @@ int run_ef(fc_ctx* c, int i, uint64_t k, bool topk) {
   }
   fcb::launch_ef(w.g_o, w.ge, c->G, k, w.ctl, w.ws, w.pz, 1, topk ? 1 : 0, c->stream);
   LAUNCHED();
+  TRY(grad_consumed(c, i));
   w.pz = fcb::Pending{};  // consumed
   w.pz_idx = nullptr;
   w.pz_k = 0;
@@ -362,7 +401,19 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
 
   CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
   for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
+  CUDA_TRY(cudaEventCreateWithFlags(&c->ev_agg_ready, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&c->ev_agg_free, cudaEventDisableTiming));
+  c->ev_go_ready.assign(c->n_local, nullptr);
+  c->ev_go_free.assign(c->n_local, nullptr);
+  c->go_pending.assign(c->n_local, 0);
+  c->go_read.assign(c->n_local, 0);
+  for (int i = 0; i < c->n_local; ++i) {
+    CUDA_TRY(cudaEventCreateWithFlags(&c->ev_go_ready[i], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->ev_go_free[i], cudaEventDisableTiming));
+  }
 
   const uint64_t G = c->G, N = c->n_local;
   c->gstride = align_up(G, 64);
@@ -453,7 +504,9 @@ int fc_create(fc_ctx** out, const fc_opts* opts) {
 int fc_destroy(fc_ctx* c) {
   if (!c) return FC_OK;
   cudaSetDevice(c->device);
+  if (c->s_h2d) cudaStreamSynchronize(c->s_h2d);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->s_d2h) cudaStreamSynchronize(c->s_d2h);
   if (c->comm_tree) ncclCommDestroy(c->comm_tree);
   if (c->comm_ring) ncclCommDestroy(c->comm_ring);
   for (void* p : c->allocs) cudaFree(p);
@@ -468,6 +521,14 @@ int fc_destroy(fc_ctx* c) {
   }
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
+  if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
+  for (auto e : c->ev_go_ready)
+    if (e) cudaEventDestroy(e);
+  for (auto e : c->ev_go_free)
+    if (e) cudaEventDestroy(e);
+  if (c->ev_agg_ready) cudaEventDestroy(c->ev_agg_ready);
+  if (c->ev_agg_free) cudaEventDestroy(c->ev_agg_free);
   delete c;
   return FC_OK;
 }
@@ -483,6 +544,17 @@ int fc_num_workers(const fc_ctx* c, int* n_local, int* world, int* rank) {
 int fc_set_grad(fc_ctx* c, int worker, const float* src, int memkind) {
   TRY(check_worker(c, worker));
   CUDA_TRY(cudaSetDevice(c->device));
+  if (memkind == FC_HOST_ASYNC) {
+    if (!src) return fail(FC_ERR_INVALID_ARGUMENT, "null source pointer");
+    // after the last reader of g_o (previous EF pass), before the next one
+    if (c->go_read[worker]) CUDA_TRY(cudaStreamWaitEvent(c->s_h2d, c->ev_go_free[worker], 0));
+    CUDA_TRY(cudaMemcpyAsync(c->w[worker].g_o, src, c->G * sizeof(float), cudaMemcpyHostToDevice,
+                             c->s_h2d));
+    CUDA_TRY(cudaEventRecord(c->ev_go_ready[worker], c->s_h2d));
+    c->go_pending[worker] = 1;
+    return FC_OK;
+  }
+  TRY(wait_grad(c, worker));
   return copy_in(c, c->w[worker].g_o, src, memkind);
 }
 
@@ -497,8 +569,10 @@ int fc_fill_synthetic(fc_ctx* c, int worker, uint64_t seed, uint32_t rank, uint6
   TRY(check_worker(c, worker));
   if (dist < FC_DIST_NORMAL || dist > FC_DIST_LAYERED) return fail(FC_ERR_INVALID_ARGUMENT, "bad distribution");
   CUDA_TRY(cudaSetDevice(c->device));
+  TRY(wait_grad(c, worker));
   fcb::launch_fill_synth(c->w[worker].g_o, c->G, fc_stream_key(seed, rank, step), dist, c->stream);
   LAUNCHED();
+  TRY(grad_consumed(c, worker));  // a later async upload must follow the fill
   if (!(c->flags & FC_FLAG_ASYNC)) CUDA_TRY(cudaStreamSynchronize(c->stream));
   return FC_OK;
 }
@@ -546,6 +620,16 @@ int fc_reset_residuals(fc_ctx* c) {
 int fc_get_aggregate(fc_ctx* c, float* dst, int memkind) {
   if (!c) return fail(FC_ERR_INVALID_ARGUMENT, "null context");
   CUDA_TRY(cudaSetDevice(c->device));
+  if (memkind == FC_HOST_ASYNC) {
+    if (!dst) return fail(FC_ERR_INVALID_ARGUMENT, "null destination pointer");
+    // after this step's decode, before the next one (which waits on ev_agg_free)
+    if (c->agg_written) CUDA_TRY(cudaStreamWaitEvent(c->s_d2h, c->ev_agg_ready, 0));
+    CUDA_TRY(cudaMemcpyAsync(dst, c->agg, c->G * sizeof(float), cudaMemcpyDeviceToHost, c->s_d2h));
+    CUDA_TRY(cudaEventRecord(c->ev_agg_free, c->s_d2h));
+    c->agg_pending = true;
+    return FC_OK;
+  }
+  TRY(wait_agg_free(c));
   return copy_out(c, dst, c->agg, c->G, memkind);
 }
 
@@ -613,7 +697,22 @@ int fc_restore(fc_ctx* c) {
 int fc_sync(fc_ctx* c) {
   if (!c) return fail(FC_ERR_INVALID_ARGUMENT, "null context");
   CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaStreamSynchronize(c->s_h2d));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->s_d2h));
+  return FC_OK;
+}
+
+int fc_join(fc_ctx* c) {
+  if (!c) return fail(FC_ERR_INVALID_ARGUMENT, "null context");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaEvent_t a = c->take_event(), b = c->take_event();
+  CUDA_TRY(cudaEventRecord(a, c->s_h2d));
+  CUDA_TRY(cudaEventRecord(b, c->s_d2h));
+  CUDA_TRY(cudaStreamWaitEvent(c->stream, a, 0));
+  CUDA_TRY(cudaStreamWaitEvent(c->stream, b, 0));
+  c->ev_pool.push_back(a);  // safe: a recorded event may be re-recorded later
+  c->ev_pool.push_back(b);
   return FC_OK;
 }
 
@@ -710,9 +809,11 @@ int fc_topk_exact(fc_ctx* c, int worker, double cr, fc_step_stats* st) {
   const bool force_fb = std::getenv("FC_FORCE_FALLBACK") != nullptr;
   record(c, 0);
   CUDA_TRY(cudaMemsetAsync(w.ctl, 0, w.ctl_bytes, c->stream));
+  TRY(wait_grad(c, worker));
   fcb::launch_sample(nullptr, w.g_o, c->G, k, w.ctl, 0, fcb::Pending{}, force_fb ? 1 : 0, c->stream);
   fcb::launch_ef(nullptr, w.g_o, c->G, k, w.ctl, w.ws, fcb::Pending{}, 0, 1, c->stream);
   fcb::launch_fallback(w.g_o, c->G, k, w.ctl, w.ws, c->stream);
+  TRY(grad_consumed(c, worker));
   LAUNCHED();
   record(c, 1);
   TRY(run_select(c, worker, k));
@@ -810,6 +911,7 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
   const uint64_t lstride = c->nccl ? 0 : c->kmax;
   // in-place update costs ~2k random sector RMWs: worth it below ~G/128
   const bool incr_ok = !(c->flags & FC_FLAG_DENSE_DECODE) && k * 128 <= c->G;
+  TRY(wait_agg_free(c));
   if (incr_ok && c->agg_incr) {
     // in place: zero the previous support, write this one (same dense content)
     fcb::launch_agg_update(c->agg_support, c->agg_support_k, bsrc, k, lists, nlists, lstride,
@@ -827,6 +929,7 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
   c->agg_support_k = incr_ok ? k : 0;
   record(c, 4);
   c->has_agg = true;
+  TRY(agg_written(c));
   for (auto& w : c->w) {  // every worker owes zeros at the broadcast indices
     w.pz.zmap = c->zmaps;
     w.pz_idx = bsrc;
@@ -873,12 +976,14 @@ int fc_ag_step(fc_ctx* c, double cr, int compressor, fc_step_stats* st) {
   }
   record(c, 3);
   fcb::launch_bounds(packs, k, stride, N, c->G, c->bounds, c->stream);
+  TRY(wait_agg_free(c));
   fcb::launch_decode_ag(packs, stride, k, N, c->bounds, (float)N, c->agg, c->G, c->zmaps,
                         c->nccl ? c->rank : 0, c->n_local, c->stream);
   LAUNCHED();
   c->agg_incr = false;  // the aggregate's support is now a union of N lists
   record(c, 4);
   c->has_agg = true;
+  TRY(agg_written(c));
   // residual_update (compress.hpp:122-130): g_e - g_e = +0 at own indices
   for (int i = 0; i < c->n_local; ++i) {
     const int r = c->nccl ? c->rank : i;
@@ -904,6 +1009,8 @@ int fc_dense_step(fc_ctx* c, int algo, int op, fc_step_stats* st) {
   record(c, 0);
   record(c, 1);
   record(c, 2);
+  for (int i = 0; i < c->n_local; ++i) TRY(wait_grad(c, i));
+  TRY(wait_agg_free(c));
   if (c->nccl) {
     NCCL_TRY(ncclAllReduce(c->w[0].g_o, c->agg, c->G, ncclFloat32, ncclSum,
                            algo == FC_TREE ? c->comm_tree : c->comm_ring, c->stream));
@@ -917,6 +1024,7 @@ int fc_dense_step(fc_ctx* c, int algo, int op, fc_step_stats* st) {
   c->agg_incr = false;
   record(c, 4);
   c->has_agg = true;
+  TRY(agg_written(c));
   const double bus = N > 1 ? 2.0 * (N - 1) / N * 4.0 * c->G : 0.0;
   return finish_step(c, st, c->G, -1, algo == FC_TREE ? 2 : 1, 12.0 * c->G, bus, l0);
 }

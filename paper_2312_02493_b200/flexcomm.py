@@ -183,9 +183,13 @@ class Cluster:
         return self.world
 
     # ---- state I/O -----------------------------------------------------------
-    def set_grad(self, worker: int, g) -> None:
+    def set_grad(self, worker: int, g, async_: bool = False) -> None:
+        """Upload a worker's gradient.  async_=True (pinned host memory only)
+        queues the copy on the upload engine and returns at once."""
         a = self._f32(g)
         p, kind = _ptr(a)
+        if async_ and kind == _abi.FC_HOST:
+            kind = _abi.FC_HOST_ASYNC
         check(lib.fc_set_grad(self._ctx, worker, p, kind))
 
     def set_grads(self, grads) -> None:
@@ -226,12 +230,20 @@ class Cluster:
     def reset_residuals(self) -> None:
         check(lib.fc_reset_residuals(self._ctx))
 
-    def aggregate(self, out=None) -> np.ndarray:
+    def aggregate(self, out=None, async_: bool = False) -> np.ndarray:
+        """Dense aggregate of the last step.  async_=True (pinned host `out`)
+        queues the download; the data is valid after sync()."""
         if out is None:
             out = np.empty(self.grad_len, dtype=np.float32)
         p, kind = _ptr(out)
+        if async_ and kind == _abi.FC_HOST:
+            kind = _abi.FC_HOST_ASYNC
         check(lib.fc_get_aggregate(self._ctx, p, kind))
         return out
+
+    def join(self) -> None:
+        """Order the compute stream after all queued async host copies."""
+        check(lib.fc_join(self._ctx))
 
     def topk(self, worker: int):
         k = C.c_uint64()
