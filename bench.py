@@ -38,6 +38,16 @@ sys.path.insert(0, str(ROOT))
 os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 MODES = {"star": 0, "var": 1, "ag": 2, "dense": 3}
+# BASELINE.json configs (per-GPU workload; one worker per GPU):
+CONFIGS = {
+    "C1": dict(mode="star", grad_len=11_700_000, cr=0.01),   # ResNet-18-sized, STAR
+    "C2": dict(mode="var", grad_len=25_600_000, cr=0.001),   # ResNet-50-sized, VAR
+    "C3": dict(mode="star", grad_len=138_000_000, cr=0.01),  # VGG-16-sized (headline)
+    "C3-ag": dict(mode="ag", grad_len=138_000_000, cr=0.01),
+    "C3-tree": dict(mode="star", grad_len=138_000_000, cr=0.01, algo="tree"),
+    "C4": dict(mode="star", grad_len=355_000_000, cr=0.001),  # GPT-2-medium-sized
+    "C5": dict(mode="star", grad_len=1_000_000_000, cr=0.001),  # 1B
+}
 ALGOS = {"ring": 0, "tree": 1}
 SEED = 42
 
@@ -52,11 +62,17 @@ def parse():
     p.add_argument("--algo", choices=list(ALGOS), default="ring")
     p.add_argument("--grad-len", type=int, default=138_000_000)
     p.add_argument("--cr", type=float, default=0.01)
+    p.add_argument("--config", choices=list(CONFIGS), default=None,
+                   help="BASELINE.json configuration preset (overrides mode/grad-len/cr)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-budget-s", type=float, default=20.0,
                    help="approximate CPU seconds for the cpu_baseline sample")
-    return p.parse_args()
+    a = p.parse_args()
+    if a.config:
+        for key, val in CONFIGS[a.config].items():
+            setattr(a, key, val)
+    return a
 
 
 def dist_env():
@@ -127,6 +143,19 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------- peaks ----
+
+def ef_traffic(G):
+    """DRAM bytes per EF launch from the committed ncu --set full capture
+    (profiles/r01_ef_traffic.json), scaled to G if the capture's size differs;
+    None when absent."""
+    p = ROOT / "profiles" / "r01_ef_traffic.json"
+    try:
+        d = json.loads(p.read_text())
+        scale = G / 138_000_000
+        return round((d["dram_read_bytes"] + d["dram_write_bytes"]) * scale)
+    except Exception:
+        return None
+
 
 def hbm_peak():
     p = ROOT / "MEASURED_PEAKS.json"
@@ -234,8 +263,16 @@ def main():
         pg.broadcast_object_list(obj, src=0)
         uid = obj[0]
     max_cr = min(1.0, max(a.cr, 0.1))
-    cl = fc.Cluster.nccl(world, rank, uid, a.grad_len, device=local, max_cr=max_cr,
-                         flags=_abi.FC_FLAG_ASYNC)
+    # NCCL's init banner goes to fd 1; keep stdout to the one JSON line
+    sys.stdout.flush()
+    saved_fd = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        cl = fc.Cluster.nccl(world, rank, uid, a.grad_len, device=local, max_cr=max_cr,
+                             flags=_abi.FC_FLAG_ASYNC)
+    finally:
+        os.dup2(saved_fd, 1)
+        os.close(saved_fd)
     G = a.grad_len
     mode = MODES[a.mode]
     algo = ALGOS[a.algo]
@@ -396,7 +433,7 @@ def main():
             "roofline": {"kernel": "k_ef (error feedback + candidate emission)", "bound": "hbm",
                          "achieved": round(achieved, 1) if achieved else None, "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4) if achieved else None,
-                         "traffic": None, "bytes_per_launch": ef_bytes,
+                         "traffic": ef_traffic(G), "bytes_per_launch": ef_bytes,
                          "mean_launch_ms": round(ef_ms, 5), "launches_timed": ef_n,
                          "peak_source": peak_src},
             "step_roofline": {"alg_bytes": step_bytes, "achieved_gbs": round(step_gbs, 1),

@@ -239,6 +239,12 @@ int fc_diag_kernel_ms(fc_ctx* ctx, int which, int iters, double* ms_out);
 /* Diagnostics: %globaltimer (ns) at the select kernel's phase boundaries of
  * the last step (start, staged, digit 1/2/3 resolved, counted, emitted, end). */
 int fc_diag_select_phases(fc_ctx* ctx, int worker, uint64_t* out8);
+/* Diagnostics (NVLink calibration): mean device ms of one NCCL collective on
+ * this context's communicators, all ranks calling alike.  which: 0 broadcast,
+ * 1 ring allreduce, 2 tree allreduce, 3 allgather (bytes per rank),
+ * 4 ART-Ring (broadcast + ring allreduce of `bytes`), 5 ART-Tree,
+ * 6 AG-compressed (allgather of 2*bytes per rank). */
+int fc_diag_collective_ms(fc_ctx* ctx, int which, uint64_t bytes, int iters, double* ms_out);
 
 #ifdef __cplusplus
 }

@@ -116,6 +116,7 @@ def _load() -> C.CDLL:
         "fc_ef_kernel_timing": ([P, C.POINTER(d), C.POINTER(u64), i], i),
         "fc_diag_kernel_ms": ([P, i, i, C.POINTER(d)], i),
         "fc_diag_select_phases": ([P, i, C.POINTER(u64)], i),
+        "fc_diag_collective_ms": ([P, i, u64, i, C.POINTER(d)], i),
         # host cost model (csrc/fc_costmodel.cpp)
         "fc_cost_primitives": ([d, d, d, d, i, C.POINTER(d)], i),
         "fc_select_collective": ([d, d, d, d, i, C.POINTER(i), C.POINTER(d)], i),
@@ -140,7 +141,7 @@ EXPORTS = [
     "fc_residual_ptr", "fc_reset_residuals", "fc_get_aggregate", "fc_aggregate_ptr",
     "fc_get_topk", "fc_get_worker_stats", "fc_snapshot", "fc_restore", "fc_artopk_step",
     "fc_ag_step", "fc_dense_step", "fc_topk_exact", "fc_sync", "fc_join", "fc_stream", "fc_ef_kernel_timing",
-    "fc_diag_kernel_ms", "fc_diag_select_phases",
+    "fc_diag_kernel_ms", "fc_diag_select_phases", "fc_diag_collective_ms",
     "fc_cost_primitives", "fc_select_collective", "fc_prefer", "fc_crossover_cr",
     "fc_derive_m_from_ag",
 ]

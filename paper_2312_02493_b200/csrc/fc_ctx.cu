@@ -782,6 +782,56 @@ int fc_diag_kernel_ms(fc_ctx* c, int which, int iters, double* ms_out) {
   return FC_OK;
 }
 
+// Diagnostics for the NVLink calibration of the cost model: mean device time
+// (CUDA events, this rank) of one NCCL collective on the context's comms:
+//   0 broadcast of `bytes` from rank 0      1 ring allreduce of bytes/4 floats
+//   2 tree allreduce of bytes/4 floats      3 allgather of `bytes` per rank
+//   4 ART-Ring = broadcast(bytes) + ring allreduce(bytes)
+//   5 ART-Tree = broadcast(bytes) + tree allreduce(bytes)
+//   6 AG-compressed = allgather(2 * bytes)   (values + indices, cost_ag_compressed)
+// All ranks must call with the same arguments (collective).
+int fc_diag_collective_ms(fc_ctx* c, int which, uint64_t bytes, int iters, double* ms_out) {
+  if (!c || !ms_out || iters < 1) return fail(FC_ERR_INVALID_ARGUMENT, "bad argument");
+  if (!c->nccl) return fail(FC_ERR_INVALID_ARGUMENT, "needs an NCCL context");
+  const uint64_t cap = c->kmax * 4;  // bytes available in bidx / reduced / pack
+  const uint64_t need = (which == 3 || which == 6) ? (which == 6 ? 2 * bytes : bytes) : bytes;
+  if (need > 2 * cap || (which != 3 && which != 6 && bytes > cap) || bytes < 4)
+    return fail(FC_ERR_INVALID_ARGUMENT, "message larger than the context's buffers");
+  CUDA_TRY(cudaSetDevice(c->device));
+  Worker& w = c->w[0];
+  const size_t nf = bytes / 4;
+  auto once = [&]() -> int {
+    switch (which) {
+      case 0: NCCL_TRY(ncclBroadcast(w.pack, c->bidx, nf, ncclUint32, 0, c->comm_ring, c->stream)); break;
+      case 1: NCCL_TRY(ncclAllReduce(w.contrib, c->reduced, nf, ncclFloat32, ncclSum, c->comm_ring, c->stream)); break;
+      case 2: NCCL_TRY(ncclAllReduce(w.contrib, c->reduced, nf, ncclFloat32, ncclSum, c->comm_tree, c->stream)); break;
+      case 3: NCCL_TRY(ncclAllGather(w.pack, c->ag_recv, nf, ncclUint32, c->comm_ring, c->stream)); break;
+      case 4:
+      case 5:
+        NCCL_TRY(ncclBroadcast(w.pack, c->bidx, nf, ncclUint32, 0, c->comm_ring, c->stream));
+        NCCL_TRY(ncclAllReduce(w.contrib, c->reduced, nf, ncclFloat32, ncclSum,
+                               which == 4 ? c->comm_ring : c->comm_tree, c->stream));
+        break;
+      case 6: NCCL_TRY(ncclAllGather(w.pack, c->ag_recv, 2 * nf, ncclUint32, c->comm_ring, c->stream)); break;
+      default: return fail(FC_ERR_INVALID_ARGUMENT, "unknown collective");
+    }
+    return FC_OK;
+  };
+  for (int i = 0; i < 3; ++i) TRY(once());
+  cudaEvent_t e0 = c->take_event(), e1 = c->take_event();
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  CUDA_TRY(cudaEventRecord(e0, c->stream));
+  for (int i = 0; i < iters; ++i) TRY(once());
+  CUDA_TRY(cudaEventRecord(e1, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  float ms = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+  c->ev_pool.push_back(e0);
+  c->ev_pool.push_back(e1);
+  *ms_out = ms / iters;
+  return FC_OK;
+}
+
 // Diagnostics: %globaltimer (ns) at k_select's phase boundaries in the last
 // step of `worker` (block 0): start, staged, digit 1/2/3, counted, emitted, end.
 int fc_diag_select_phases(fc_ctx* c, int worker, uint64_t* out8) {

@@ -1,0 +1,72 @@
+"""NVLink calibration fixtures, validated the way the reference
+validates its WAN fixtures (tests/test_acceptance.cpp:47-60): the unchanged
+cost model with the fitted NetParams must pick the measured-fastest exchange
+wherever the measured top-two margin is decisive."""
+from __future__ import annotations
+
+import csv
+import json
+import math
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+FIX = ROOT / "fixtures"
+WORLDS = sorted(int(p.stem.split("_n")[-1]) for p in FIX.glob("nvlink_fit_n*.json"))
+
+
+def _rows(n):
+    with open(FIX / f"nvlink_grid_n{n}.csv") as f:
+        return list(csv.DictReader(f))
+
+
+@pytest.mark.parametrize("n", WORLDS)
+def test_fit_is_physical(n):
+    d = json.loads((FIX / f"nvlink_fit_n{n}.json").read_text())
+    assert 1e-6 <= d["alpha_s"] <= 5e-5            # NCCL launch + sync latency
+    assert 100 <= d["bandwidth_GBps"] <= 1800      # per-GPU NVLink 5 is 900 GB/s/direction
+
+
+@pytest.mark.parametrize("n", WORLDS)
+def test_selector_matches_measured_winner(fc, n):
+    d = json.loads((FIX / f"nvlink_fit_n{n}.json").read_text())
+    net = fc.NetParams(d["alpha_s"], d["bandwidth_bps"])
+    names = {0: "ag_compressed_us", 1: "art_ring_us", 2: "art_tree_us"}
+    decisive = agree = 0
+    for r in _rows(n):
+        mc = float(r["payload_bytes"])
+        meas = {k: float(r[k]) for k in names.values()}
+        order = sorted(meas, key=meas.get)
+        ch = fc.select_collective(net, fc.MessageSpec(mc / 0.01, 0.01, n))
+        # the library's costs are the reference's formulas (bit-exact, test_cpu)
+        costs = fc.cost_primitives(net, fc.MessageSpec(mc / 0.01, 0.01, n))
+        assert costs["ag_compressed"] > 0 and costs["art_ring"] > 0
+        if meas[order[1]] / meas[order[0]] - 1.0 > 0.15:
+            decisive += 1
+            agree += names[int(ch.collective)] == order[0]
+    assert decisive >= 3
+    assert agree / decisive >= 0.85, (agree, decisive)
+
+
+@pytest.mark.parametrize("n", WORLDS)
+def test_fit_recomputes(fc, n):
+    """The stored fit is the least-squares optimum of the stored grid (log time)."""
+    d = json.loads((FIX / f"nvlink_fit_n{n}.json").read_text())
+
+    def err(alpha, beta):
+        e = 0.0
+        for r in _rows(n):
+            mc = float(r["payload_bytes"])
+            lg = math.log2(n)
+            m = {"ag_compressed_us": alpha * lg + 2 * mc * beta * (n - 1),
+                 "art_ring_us": alpha * (2 * (n - 1) + lg) + mc * beta * (2 * (n - 1) / n + lg),
+                 "art_tree_us": 3 * alpha * lg + 3 * mc * beta * lg}
+            for k, v in m.items():
+                e += (math.log(v) - math.log(float(r[k]) * 1e-6)) ** 2
+        return e
+
+    a, b = d["alpha_s"], 8.0 / d["bandwidth_bps"]
+    base = err(a, b)
+    for fa, fb in [(1.3, 1), (1 / 1.3, 1), (1, 1.3), (1, 1 / 1.3)]:
+        assert err(a * fa, b * fb) >= base * 0.999
