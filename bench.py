@@ -256,23 +256,27 @@ def main():
 
         dist.init_process_group("gloo", rank=rank, world_size=world)
         pg = dist
-    # NCCL bootstrap: rank 0's unique id shipped over the gloo group
-    uid = fc.get_unique_id() if rank == 0 else None
-    if pg:
-        obj = [uid]
-        pg.broadcast_object_list(obj, src=0)
-        uid = obj[0]
     max_cr = min(1.0, max(a.cr, 0.1))
-    # NCCL's init banner goes to fd 1; keep stdout to the one JSON line
-    sys.stdout.flush()
-    saved_fd = os.dup(1)
-    os.dup2(2, 1)
-    try:
-        cl = fc.Cluster.nccl(world, rank, uid, a.grad_len, device=local, max_cr=max_cr,
-                             flags=_abi.FC_FLAG_ASYNC)
-    finally:
-        os.dup2(saved_fd, 1)
-        os.close(saved_fd)
+
+    def make_cluster(flags):
+        # NCCL bootstrap: rank 0's unique id shipped over the gloo group
+        uid = fc.get_unique_id() if rank == 0 else None
+        if pg:
+            obj = [uid]
+            pg.broadcast_object_list(obj, src=0)
+            uid = obj[0]
+        # NCCL's init banner goes to fd 1; keep stdout to the one JSON line
+        sys.stdout.flush()
+        saved_fd = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            return fc.Cluster.nccl(world, rank, uid, a.grad_len, device=local, max_cr=max_cr,
+                                   flags=flags)
+        finally:
+            os.dup2(saved_fd, 1)
+            os.close(saved_fd)
+
+    cl = make_cluster(_abi.FC_FLAG_ASYNC)
     G = a.grad_len
     mode = MODES[a.mode]
     algo = ALGOS[a.algo]
@@ -336,40 +340,6 @@ def main():
     clk = clocks.stop()
     ms = max_over_ranks(ms_local)
 
-    # ---- end-to-end through the public API with host buffers --------------
-    # Every step: H2D of the step's gradient from pinned host memory, the
-    # step, D2H of the dense aggregate (the reference returns it by value).
-    e2e = None
-    if not a.no_e2e:
-        host_g = torch.empty(G, dtype=torch.float32, pin_memory=True)
-        host_agg = torch.empty(G, dtype=torch.float32, pin_memory=True)
-        host_g.copy_(_tensor_from_ptr(cl.grad_ptr(0), G, local))  # setup only
-        torch.cuda.synchronize()
-        e2e_steps = max(3, min(a.steps, 10))
-        # Each step: upload of the step's gradient from pinned host memory,
-        # the sync step, download of the dense aggregate (the reference returns
-        # it by value).  The copies are queued on the copy engines, so step
-        # s's download overlaps step s+1's upload (PCIe is full duplex).
-        for s in range(2):
-            cl.set_grad(0, host_g, async_=True)
-            step(s)
-            cl.aggregate(host_agg, async_=True)
-        cl.sync()
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for s in range(e2e_steps):
-            cl.set_grad(0, host_g, async_=True)
-            step(100 + s)
-            cl.aggregate(host_agg, async_=True)
-        cl.join()
-        e1.record(stream)
-        barrier()
-        cl.sync()
-        e2e_ms = max_over_ranks(e0.elapsed_time(e1) / e2e_steps)
-        e2e = {"value": round(e2e_ms, 4), "unit": "ms/step",
-               "h2d_bytes_per_step": 4 * G, "d2h_bytes_per_step": 4 * G, "steps": e2e_steps}
-
     # ---- phase split from one synchronous step (diagnostic) ---------------
     phase = None
     try:
@@ -389,6 +359,44 @@ def main():
                      "launches_per_step": stt.launches}
     except Exception:
         pass
+
+    # ---- end-to-end through the public API with host buffers --------------
+    # A host-fed user creates the context with FC_FLAG_PIPELINE (two gradient
+    # and two aggregate buffers).  Every step: upload of the step's gradient
+    # from pinned host memory, the sync step, download of the dense aggregate
+    # (the reference returns it by value).  The copies run on the copy
+    # engines: step s+1's upload and step s's download overlap each other and
+    # the compute (PCIe is full duplex).
+    e2e = None
+    if not a.no_e2e:
+        host_g = torch.empty(G, dtype=torch.float32, pin_memory=True)
+        host_agg = torch.empty(G, dtype=torch.float32, pin_memory=True)
+        host_g.copy_(_tensor_from_ptr(cl.grad_ptr(0), G, local))  # setup only
+        torch.cuda.synchronize()
+        cl.close()
+        cl = make_cluster(_abi.FC_FLAG_ASYNC | _abi.FC_FLAG_PIPELINE)
+        stream = torch.cuda.ExternalStream(cl.stream_ptr(), device=local)
+        e2e_steps = max(3, a.steps)
+        for s in range(2):
+            cl.set_grad(0, host_g, async_=True)
+            step(s)
+            cl.aggregate(host_agg, async_=True)
+        cl.sync()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for s in range(e2e_steps):
+            cl.set_grad(0, host_g, async_=True)
+            step(100 + s)
+            cl.aggregate(host_agg, async_=True)
+        cl.join()
+        e1.record(stream)
+        barrier()
+        cl.sync()
+        e2e_ms = max_over_ranks(e0.elapsed_time(e1) / e2e_steps)
+        e2e = {"value": round(e2e_ms, 4), "unit": "ms/step",
+               "h2d_bytes_per_step": 4 * G, "d2h_bytes_per_step": 4 * G, "steps": e2e_steps,
+               "context": "FC_FLAG_ASYNC | FC_FLAG_PIPELINE, FC_HOST_ASYNC copies"}
 
     # ---- roofline of the dominant kernel (error feedback) -----------------
     peak, peak_src = hbm_peak()

@@ -82,6 +82,12 @@ typedef enum fc_memkind { FC_HOST = 0, FC_DEVICE = 1, FC_HOST_ASYNC = 2 } fc_mem
                                      the previous support, write the new one), so
                                      callers must treat fc_aggregate_ptr() memory
                                      as read-only                                 */
+#define FC_FLAG_PIPELINE 0x8u     /* host-fed pipelining: two gradient buffer sets
+                                     and two aggregate buffers, so FC_HOST_ASYNC
+                                     uploads for step s+1 and the download of step
+                                     s-1 overlap step s (fc_grad_ptr / the
+                                     aggregate pointer alternate between buffers;
+                                     implies FC_FLAG_DENSE_DECODE)                */
 
 #define FC_NCCL_UID_BYTES 128
 
@@ -217,6 +223,55 @@ int fc_crossover_cr(double alpha, double bandwidth, double m_bytes, int n, int p
 /* derive_m_from_ag, costmodel.hpp:171-175 */
 int fc_derive_m_from_ag(double alpha, double bandwidth, double c, int n, double seconds,
                         double* m_out);
+
+/* ---- adaptive-CR controller (inc/moo.hpp, kept unchanged) ------------------ */
+/* CandidateCR, inc/moo.hpp:20-25 */
+typedef struct fc_candidate {
+  double c;
+  double gain_avg;
+  double t_comp_avg;     /* seconds */
+  double t_sync_modeled; /* seconds */
+} fc_candidate;
+/* ControllerConfig, inc/moo.hpp:27-32 (defaults 0.001, 0.1, 3, 10, 0.10) */
+typedef struct fc_controller_config {
+  double c_low;
+  double c_high;
+  double factor;
+  int probe_iters;
+  double gain_threshold;
+} fc_controller_config;
+/* ControllerConfig::validate, inc/moo.hpp:34-41 */
+int fc_controller_config_validate(const fc_controller_config* cfg);
+/* round_3sig, inc/moo.hpp:44-48 */
+int fc_round_3sig(double v, double* out);
+/* candidate_ladder, inc/moo.hpp:52-65: writes min(cap, count) rungs */
+int fc_candidate_ladder(const fc_controller_config* cfg, double* out, int cap, int* count);
+/* trigger_gain, inc/moo.hpp:67-71, over the GainTracker window samples in
+ * push order (inc/compress.hpp:145-165) */
+int fc_trigger_gain(double gain_ref, const double* samples, uint64_t count, double threshold,
+                    int* fire);
+/* pareto_front, inc/moo.hpp:88-102: mask[i] = 1 iff candidate i is undominated */
+int fc_pareto_front(const fc_candidate* cands, int m, int* mask);
+/* choose_cr, inc/moo.hpp:111-146 over a front of m candidates: *chosen = index
+ * of the knee, *collective = select_collective at its c (may be NULL) */
+int fc_choose_cr(const fc_candidate* front, int m, double alpha, double bandwidth, double m_bytes,
+                 int n, int* chosen, int* collective);
+/* network_changed, inc/netsched.hpp:50-58 */
+int fc_network_changed(double alpha0, double bandwidth0, double alpha1, double bandwidth1,
+                       double rel_threshold, int* changed);
+/* Per-step controller inputs after fc_artopk_step / fc_ag_step (the Trainer's
+ * artopk_with_gain / ag_step_with_gain, inc/trainer.hpp:361-398, with the
+ * 0.5 ns/element compression model of :346-359 replaced by measurement):
+ *   gain   = mean over all N workers, in rank order, of
+ *            AR: clamp(kept_norm2 / ge_norm2, 0, 1);  AG (ag != 0): topk_norm2 / ge_norm2
+ *   t_comp = compression + decompression seconds of the step (ms_ef +
+ *            ms_select + ms_decode of `stats`), max over ranks.
+ * Under NCCL the per-rank values are allgathered so every rank returns the
+ * same numbers.  A worker with ge_norm2 == 0 is FC_ERR_RUNTIME ("degenerate
+ * gradient", inc/trainer.hpp:391-393, inc/compress.hpp:140).  Needs stats
+ * recorded by the step (not FC_FLAG_NO_TIMING). */
+int fc_moo_metrics(fc_ctx* ctx, int ag, const fc_step_stats* stats, double* gain,
+                   double* t_comp_s);
 
 /* Synchronize the context's streams (for FC_FLAG_ASYNC / FC_HOST_ASYNC users). */
 int fc_sync(fc_ctx* ctx);

@@ -42,12 +42,19 @@ namespace flexcomm {
 namespace b200 {
 
 // ---- status -> the reference's exception types ------------------------------
+// CUDA / NCCL failures are runtime_errors too, but never a property of the data.
+struct device_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
 inline void check(int s) {
   if (s == FC_OK) return;
   const std::string msg = std::string(fc_status_string(s)) + ": " + fc_last_error();
   switch (s) {
     case FC_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
     case FC_ERR_OUT_OF_RANGE: throw std::out_of_range(msg);
+    case FC_ERR_CUDA:
+    case FC_ERR_NCCL: throw device_error(msg);
     default: throw std::runtime_error(msg);
   }
 }

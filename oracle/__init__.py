@@ -136,6 +136,10 @@ class Ref:
         lib.ref_candidate_ladder.argtypes, lib.ref_candidate_ladder.restype = [d, d, d, P, i], i
         lib.ref_choose_cr.argtypes = [P, i, d, d, d, i, P, P, P]
         lib.ref_choose_cr.restype = i
+        lib.ref_round_3sig.argtypes, lib.ref_round_3sig.restype = [d], d
+        lib.ref_trigger_gain.argtypes, lib.ref_trigger_gain.restype = [d, P, u64, u64, d], i
+        lib.ref_network_changed.argtypes, lib.ref_network_changed.restype = [d, d, d, d, d], i
+        lib.ref_params_at.argtypes, lib.ref_params_at.restype = [P, i, L, P, P], i
         lib.ref_state_create.argtypes, lib.ref_state_create.restype = [i, u64], P
         lib.ref_state_destroy.argtypes, lib.ref_state_destroy.restype = [P], None
         lib.ref_state_fill_synth.argtypes = [P, i, u64, C.c_uint32, u64, i]
@@ -210,9 +214,12 @@ class Ref:
     def candidate_ladder(self, c_low=0.001, c_high=0.1, factor=3.0):
         out = np.empty(64, dtype=np.float64)
         m = self.lib.ref_candidate_ladder(c_low, c_high, factor, out.ctypes.data, 64)
+        if m > 64:
+            out = np.empty(m, dtype=np.float64)
+            m = self.lib.ref_candidate_ladder(c_low, c_high, factor, out.ctypes.data, m)
         if m < 0:
             raise ValueError("reference raised")
-        return list(out[:m])
+        return [float(x) for x in out[:m]]
 
     def choose_cr(self, rows, alpha, bandwidth, m_bytes, n):
         rows = np.ascontiguousarray(rows, dtype=np.float64)
@@ -224,6 +231,28 @@ class Ref:
         if rc:
             raise ValueError(f"reference raised (code {rc})")
         return mask.astype(bool), chosen.value, coll.value
+
+    def round_3sig(self, v):
+        return self.lib.ref_round_3sig(v)
+
+    def trigger_gain(self, gain_ref, samples, window, threshold):
+        s = np.ascontiguousarray(samples, dtype=np.float64)
+        r = self.lib.ref_trigger_gain(gain_ref, s.ctypes.data, s.size, window, threshold)
+        if r < 0:
+            raise ValueError(f"reference raised (code {-r})")
+        return bool(r)
+
+    def network_changed(self, a0, b0, a1, b1, rel):
+        return bool(self.lib.ref_network_changed(a0, b0, a1, b1, rel))
+
+    def params_at(self, segments, epoch):
+        segs = np.ascontiguousarray(segments, dtype=np.float64).reshape(-1, 3)
+        a, b = C.c_double(), C.c_double()
+        rc = self.lib.ref_params_at(segs.ctypes.data, segs.shape[0], epoch, C.addressof(a),
+                                    C.addressof(b))
+        if rc:
+            raise ValueError(f"reference raised (code {rc})")
+        return a.value, b.value
 
 
 class RefState:

@@ -22,6 +22,7 @@
 #include "flexcomm/core.hpp"
 #include "flexcomm/costmodel.hpp"
 #include "flexcomm/moo.hpp"
+#include "flexcomm/netsched.hpp"
 
 using namespace flexcomm;
 
@@ -201,6 +202,42 @@ int ref_choose_cr(const double* rows, int m, double alpha, double bandwidth, dou
     auto ch = choose_cr(front, NetParams(alpha, bandwidth), m_bytes, n);
     *chosen = ch.candidate.c;
     *collective = static_cast<int>(ch.collective);
+    return 0;
+  } catch (...) {
+    return code_of(std::current_exception());
+  }
+}
+
+// round_3sig (inc/moo.hpp:44-48)
+double ref_round_3sig(double v) { return round_3sig(v); }
+
+// trigger_gain (inc/moo.hpp:67-71) after pushing `count` samples into a
+// GainTracker of the given window (inc/compress.hpp:145-165); -code on error.
+int ref_trigger_gain(double gain_ref, const double* samples, uint64_t count, uint64_t window,
+                     double threshold) {
+  try {
+    GainTracker t(window);
+    for (uint64_t i = 0; i < count; ++i) t.push(samples[i]);
+    return trigger_gain(gain_ref, t, threshold) ? 1 : 0;
+  } catch (...) {
+    return -code_of(std::current_exception());
+  }
+}
+
+// network_changed (inc/netsched.hpp:50-58)
+int ref_network_changed(double a0, double b0, double a1, double b1, double rel) {
+  return network_changed(NetParams(a0, b0), NetParams(a1, b1), rel) ? 1 : 0;
+}
+
+// params_at (inc/netsched.hpp:38-46) over m segments (start_epoch, alpha, bandwidth)
+int ref_params_at(const double* segs, int m, long epoch, double* alpha, double* bandwidth) {
+  try {
+    NetworkSchedule s;
+    for (int i = 0; i < m; ++i)
+      s.segments.push_back({static_cast<long>(segs[3 * i]), NetParams(segs[3 * i + 1], segs[3 * i + 2])});
+    auto p = params_at(s, epoch);
+    *alpha = p.alpha;
+    *bandwidth = p.bandwidth;
     return 0;
   } catch (...) {
     return code_of(std::current_exception());

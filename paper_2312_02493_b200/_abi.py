@@ -27,6 +27,7 @@ FC_HOST, FC_DEVICE, FC_HOST_ASYNC = 0, 1, 2
 FC_FLAG_ASYNC = 0x1
 FC_FLAG_NO_TIMING = 0x2
 FC_FLAG_DENSE_DECODE = 0x4
+FC_FLAG_PIPELINE = 0x8
 FC_NCCL_UID_BYTES = 128
 FC_DIST_NORMAL, FC_DIST_TIES, FC_DIST_LAYERED = 0, 1, 2
 
@@ -70,6 +71,27 @@ class fc_worker_stats(C.Structure):
         ("candidates", C.c_uint64),
         ("count_above", C.c_uint64),
         ("fallback", C.c_int),
+    ]
+
+
+class fc_candidate(C.Structure):
+    """CandidateCR, inc/moo.hpp:20-25."""
+    _fields_ = [
+        ("c", C.c_double),
+        ("gain_avg", C.c_double),
+        ("t_comp_avg", C.c_double),
+        ("t_sync_modeled", C.c_double),
+    ]
+
+
+class fc_controller_config(C.Structure):
+    """ControllerConfig, inc/moo.hpp:27-32."""
+    _fields_ = [
+        ("c_low", C.c_double),
+        ("c_high", C.c_double),
+        ("factor", C.c_double),
+        ("probe_iters", C.c_int),
+        ("gain_threshold", C.c_double),
     ]
 
 
@@ -123,6 +145,15 @@ def _load() -> C.CDLL:
         "fc_prefer": ([d, d, d, d, i, i, C.POINTER(i)], i),
         "fc_crossover_cr": ([d, d, d, i, i, C.POINTER(d), C.POINTER(i)], i),
         "fc_derive_m_from_ag": ([d, d, d, i, d, C.POINTER(d)], i),
+        # adaptive-CR controller (csrc/fc_moo.cpp, fc_ctx.cu)
+        "fc_controller_config_validate": ([C.POINTER(fc_controller_config)], i),
+        "fc_round_3sig": ([d, C.POINTER(d)], i),
+        "fc_candidate_ladder": ([C.POINTER(fc_controller_config), C.POINTER(d), i, C.POINTER(i)], i),
+        "fc_trigger_gain": ([d, C.POINTER(d), u64, d, C.POINTER(i)], i),
+        "fc_pareto_front": ([C.POINTER(fc_candidate), i, C.POINTER(i)], i),
+        "fc_choose_cr": ([C.POINTER(fc_candidate), i, d, d, d, i, C.POINTER(i), C.POINTER(i)], i),
+        "fc_network_changed": ([d, d, d, d, d, C.POINTER(i)], i),
+        "fc_moo_metrics": ([P, i, C.POINTER(fc_step_stats), C.POINTER(d), C.POINTER(d)], i),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(lib, name)
@@ -144,6 +175,8 @@ EXPORTS = [
     "fc_diag_kernel_ms", "fc_diag_select_phases", "fc_diag_collective_ms",
     "fc_cost_primitives", "fc_select_collective", "fc_prefer", "fc_crossover_cr",
     "fc_derive_m_from_ag",
+    "fc_controller_config_validate", "fc_round_3sig", "fc_candidate_ladder", "fc_trigger_gain",
+    "fc_pareto_front", "fc_choose_cr", "fc_network_changed", "fc_moo_metrics",
 ]
 
 
@@ -163,6 +196,10 @@ class RuntimeFailure(FlexcommError):
     """std::runtime_error in the reference (and CUDA / NCCL failures)."""
 
 
+class DeviceFailure(RuntimeFailure):
+    """A CUDA or NCCL failure (never a property of the data)."""
+
+
 class NoDevice(FlexcommError):
     """No sm_100 device: the path never falls back to the CPU."""
 
@@ -171,8 +208,8 @@ _ERRS = {
     FC_ERR_INVALID_ARGUMENT: InvalidArgument,
     FC_ERR_OUT_OF_RANGE: OutOfRange,
     FC_ERR_RUNTIME: RuntimeFailure,
-    FC_ERR_CUDA: RuntimeFailure,
-    FC_ERR_NCCL: RuntimeFailure,
+    FC_ERR_CUDA: DeviceFailure,
+    FC_ERR_NCCL: DeviceFailure,
     FC_ERR_NO_DEVICE: NoDevice,
 }
 

@@ -18,7 +18,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libfc_b200.so"
-SOURCES = [CSRC / "fc_kernels.cu", CSRC / "fc_ctx.cu", CSRC / "fc_costmodel.cpp"]
+SOURCES = [CSRC / "fc_kernels.cu", CSRC / "fc_ctx.cu", CSRC / "fc_costmodel.cpp", CSRC / "fc_moo.cpp"]
 HEADERS = [CSRC / "fc_device.cuh", ROOT / "include" / "flexcomm_b200.h", ROOT / "include" / "fc_synth.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -94,10 +94,19 @@ struct fc_ctx {
   // FC_HOST_ASYNC copies: an upload stream and a download stream, ordered
   // against the compute stream with events
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
-  std::vector<cudaEvent_t> ev_go_ready, ev_go_free;  // per worker: upload done / EF read g_o
+  // per (gradient set, worker): upload done / last kernel reading it done
+  std::vector<cudaEvent_t> ev_go_ready, ev_go_free;
   std::vector<char> go_pending, go_read;
-  cudaEvent_t ev_agg_ready = nullptr, ev_agg_free = nullptr;  // decode done / download done
-  bool agg_pending = false, agg_written = false;
+  // per aggregate buffer: decode done / download done
+  cudaEvent_t ev_agg_ready[2] = {}, ev_agg_free[2] = {};
+  bool agg_pending[2] = {}, agg_written[2] = {};
+  // FC_FLAG_PIPELINE: two gradient sets (uploads of step s+1 overlap step s)
+  // and two aggregates (the download of step s overlaps the decode of s+1)
+  int nbuf = 1;
+  float* g_o_set[2] = {};
+  int in_set = 0;      // the gradient set the next step reads
+  float* agg_buf[2] = {};
+  int agg_cur = 0;     // the buffer holding the last decoded aggregate (== agg)
   std::vector<Worker> w;
   std::vector<void*> allocs;
   float* g_o_all = nullptr;
@@ -155,30 +164,48 @@ int check_worker(const fc_ctx* c, int worker) {
 
 // The compute stream must not read worker i's gradient before its async
 // upload landed (called before any kernel that reads g_o).
+int go_slot(const fc_ctx* c, int i) { return c->in_set * c->n_local + i; }
 int wait_grad(fc_ctx* c, int i) {
-  if (c->go_pending[i]) {
-    CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_go_ready[i], 0));
-    c->go_pending[i] = 0;
+  const int q = go_slot(c, i);
+  if (c->go_pending[q]) {
+    CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_go_ready[q], 0));
+    c->go_pending[q] = 0;
   }
   return FC_OK;
 }
 // ... and an async upload must not overwrite g_o before the EF pass read it.
 int grad_consumed(fc_ctx* c, int i) {
-  CUDA_TRY(cudaEventRecord(c->ev_go_free[i], c->stream));
-  c->go_read[i] = 1;
+  const int q = go_slot(c, i);
+  CUDA_TRY(cudaEventRecord(c->ev_go_free[q], c->stream));
+  c->go_read[q] = 1;
   return FC_OK;
 }
+// After a step read its gradients: the next uploads go to the other set.
+void advance_input(fc_ctx* c) {
+  if (c->nbuf < 2) return;
+  c->in_set ^= 1;
+  for (int i = 0; i < c->n_local; ++i) c->w[i].g_o = c->g_o_set[c->in_set] + (uint64_t)i * c->gstride;
+  c->g_o_all = c->g_o_set[c->in_set];
+}
 // A decode must not overwrite the aggregate while an async download reads it.
-int wait_agg_free(fc_ctx* c) {
-  if (c->agg_pending) {
-    CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_agg_free, 0));
-    c->agg_pending = false;
+int wait_agg_free(fc_ctx* c, int b) {
+  if (c->agg_pending[b]) {
+    CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_agg_free[b], 0));
+    c->agg_pending[b] = false;
   }
   return FC_OK;
 }
-int agg_written(fc_ctx* c) {
-  CUDA_TRY(cudaEventRecord(c->ev_agg_ready, c->stream));
-  c->agg_written = true;
+// The buffer a step decodes into (the other one when pipelined), once its
+// download (if any) has finished.
+int agg_target(fc_ctx* c, int* b) {
+  *b = c->nbuf == 2 ? c->agg_cur ^ 1 : 0;
+  return wait_agg_free(c, *b);
+}
+int agg_written(fc_ctx* c, int b) {
+  c->agg_cur = b;
+  c->agg = c->agg_buf[b];
+  CUDA_TRY(cudaEventRecord(c->ev_agg_ready[b], c->stream));
+  c->agg_written[b] = true;
   return FC_OK;
 }
 
@@ -256,10 +283,12 @@ int run_ef(fc_ctx* c, int i, uint64_t k, bool topk) {
   return FC_OK;
 }
 
+// Top-k of worker i into its pack; also writes the chunk bounds of the
+// selection into bounds slot i (so a decode of this list needs no k_bounds).
 int run_select(fc_ctx* c, int i, uint64_t k) {
   Worker& w = c->w[i];
   const int e = fcb::launch_select(k, w.ctl, w.ws, w.pack, reinterpret_cast<float*>(w.pack + k),
-                                   c->stream);
+                                   c->bounds + (uint64_t)i * (c->nch + 1), c->stream);
   if (e) return fail(FC_ERR_CUDA, std::string("k_select launch: ") +
                                       cudaGetErrorString(static_cast<cudaError_t>(e)));
   LAUNCHED();
@@ -404,13 +433,16 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
   CUDA_TRY(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
   CUDA_TRY(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
   for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
-  CUDA_TRY(cudaEventCreateWithFlags(&c->ev_agg_ready, cudaEventDisableTiming));
-  CUDA_TRY(cudaEventCreateWithFlags(&c->ev_agg_free, cudaEventDisableTiming));
-  c->ev_go_ready.assign(c->n_local, nullptr);
-  c->ev_go_free.assign(c->n_local, nullptr);
-  c->go_pending.assign(c->n_local, 0);
-  c->go_read.assign(c->n_local, 0);
-  for (int i = 0; i < c->n_local; ++i) {
+  for (int b = 0; b < 2; ++b) {
+    CUDA_TRY(cudaEventCreateWithFlags(&c->ev_agg_ready[b], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->ev_agg_free[b], cudaEventDisableTiming));
+  }
+  c->nbuf = (o->flags & FC_FLAG_PIPELINE) ? 2 : 1;
+  c->ev_go_ready.assign(2 * c->n_local, nullptr);
+  c->ev_go_free.assign(2 * c->n_local, nullptr);
+  c->go_pending.assign(2 * c->n_local, 0);
+  c->go_read.assign(2 * c->n_local, 0);
+  for (int i = 0; i < 2 * c->n_local; ++i) {
     CUDA_TRY(cudaEventCreateWithFlags(&c->ev_go_ready[i], cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&c->ev_go_free[i], cudaEventDisableTiming));
   }
@@ -420,9 +452,15 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
   const uint64_t GS = c->gstride;
   const unsigned nch = (unsigned)c->nch;
   const unsigned ef_grid = (unsigned)fcb::ef_grid_size();
-  TRY(c->alloc(&c->g_o_all, N * GS));
+  for (int b = 0; b < c->nbuf; ++b) {
+    TRY(c->alloc(&c->g_o_set[b], N * GS));
+    TRY(c->alloc(&c->agg_buf[b], G));
+    CUDA_TRY(cudaMemsetAsync(c->g_o_set[b], 0, N * GS * sizeof(float), c->stream));
+    CUDA_TRY(cudaMemsetAsync(c->agg_buf[b], 0, G * sizeof(float), c->stream));
+  }
+  c->g_o_all = c->g_o_set[0];
+  c->agg = c->agg_buf[0];
   TRY(c->alloc(&c->ge_all, N * GS));
-  TRY(c->alloc(&c->agg, G));
   TRY(c->alloc(&c->pack_all, N * 2 * c->kmax));
   TRY(c->alloc(&c->contrib_all, N * c->kmax));
   const uint64_t nl = std::max<uint64_t>(N, (uint64_t)c->world);
@@ -430,18 +468,18 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
   TRY(c->alloc(&c->zmaps, N * c->nch * 32));
   TRY(c->alloc(&c->agg_support, c->kmax));
   CUDA_TRY(cudaMemsetAsync(c->zmaps, 0, N * c->nch * 32 * sizeof(unsigned), c->stream));
-  c->agg_incr = !(o->flags & FC_FLAG_DENSE_DECODE);  // zero agg == densify(empty support)
+  // zero agg == densify(empty support); pipelined contexts always decode densely
+  c->agg_incr = !(o->flags & (FC_FLAG_DENSE_DECODE | FC_FLAG_PIPELINE));
   c->agg_support_k = 0;
   if (c->nccl) {
     TRY(c->alloc(&c->reduced, c->kmax));
     TRY(c->alloc(&c->bidx, c->kmax));
     TRY(c->alloc(&c->ag_recv, (uint64_t)c->world * 2 * c->kmax));
-    TRY(c->alloc(&c->dnorms, (uint64_t)c->world));
+    // [0, W): VAR scores; [W, W+2): this rank's MOO metrics; [W+2, 3W+2): gathered
+    TRY(c->alloc(&c->dnorms, 3 * (uint64_t)c->world + 2));
   }
-  CUDA_TRY(cudaMallocHost(&c->h_norms, sizeof(double) * std::max(c->world, c->n_local)));
+  CUDA_TRY(cudaMallocHost(&c->h_norms, 2 * sizeof(double) * std::max(c->world, c->n_local)));
   CUDA_TRY(cudaMemsetAsync(c->ge_all, 0, N * GS * sizeof(float), c->stream));
-  CUDA_TRY(cudaMemsetAsync(c->g_o_all, 0, N * GS * sizeof(float), c->stream));
-  CUDA_TRY(cudaMemsetAsync(c->agg, 0, G * sizeof(float), c->stream));
   c->w.resize(N);
   for (uint64_t i = 0; i < N; ++i) {
     Worker& w = c->w[i];
@@ -527,8 +565,10 @@ int fc_destroy(fc_ctx* c) {
     if (e) cudaEventDestroy(e);
   for (auto e : c->ev_go_free)
     if (e) cudaEventDestroy(e);
-  if (c->ev_agg_ready) cudaEventDestroy(c->ev_agg_ready);
-  if (c->ev_agg_free) cudaEventDestroy(c->ev_agg_free);
+  for (int b = 0; b < 2; ++b) {
+    if (c->ev_agg_ready[b]) cudaEventDestroy(c->ev_agg_ready[b]);
+    if (c->ev_agg_free[b]) cudaEventDestroy(c->ev_agg_free[b]);
+  }
   delete c;
   return FC_OK;
 }
@@ -547,11 +587,12 @@ int fc_set_grad(fc_ctx* c, int worker, const float* src, int memkind) {
   if (memkind == FC_HOST_ASYNC) {
     if (!src) return fail(FC_ERR_INVALID_ARGUMENT, "null source pointer");
     // after the last reader of g_o (previous EF pass), before the next one
-    if (c->go_read[worker]) CUDA_TRY(cudaStreamWaitEvent(c->s_h2d, c->ev_go_free[worker], 0));
+    const int q = go_slot(c, worker);
+    if (c->go_read[q]) CUDA_TRY(cudaStreamWaitEvent(c->s_h2d, c->ev_go_free[q], 0));
     CUDA_TRY(cudaMemcpyAsync(c->w[worker].g_o, src, c->G * sizeof(float), cudaMemcpyHostToDevice,
                              c->s_h2d));
-    CUDA_TRY(cudaEventRecord(c->ev_go_ready[worker], c->s_h2d));
-    c->go_pending[worker] = 1;
+    CUDA_TRY(cudaEventRecord(c->ev_go_ready[q], c->s_h2d));
+    c->go_pending[q] = 1;
     return FC_OK;
   }
   TRY(wait_grad(c, worker));
@@ -623,13 +664,14 @@ int fc_get_aggregate(fc_ctx* c, float* dst, int memkind) {
   if (memkind == FC_HOST_ASYNC) {
     if (!dst) return fail(FC_ERR_INVALID_ARGUMENT, "null destination pointer");
     // after this step's decode, before the next one (which waits on ev_agg_free)
-    if (c->agg_written) CUDA_TRY(cudaStreamWaitEvent(c->s_d2h, c->ev_agg_ready, 0));
+    const int b = c->agg_cur;
+    if (c->agg_written[b]) CUDA_TRY(cudaStreamWaitEvent(c->s_d2h, c->ev_agg_ready[b], 0));
     CUDA_TRY(cudaMemcpyAsync(dst, c->agg, c->G * sizeof(float), cudaMemcpyDeviceToHost, c->s_d2h));
-    CUDA_TRY(cudaEventRecord(c->ev_agg_free, c->s_d2h));
-    c->agg_pending = true;
+    CUDA_TRY(cudaEventRecord(c->ev_agg_free[b], c->s_d2h));
+    c->agg_pending[b] = true;
     return FC_OK;
   }
-  TRY(wait_agg_free(c));
+  TRY(wait_agg_free(c, c->agg_cur));
   return copy_out(c, dst, c->agg, c->G, memkind);
 }
 
@@ -691,6 +733,45 @@ int fc_restore(fc_ctx* c) {
     CUDA_TRY(cudaMemcpyAsync(w.ge, w.snap, c->G * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
   }
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return FC_OK;
+}
+
+int fc_moo_metrics(fc_ctx* c, int ag, const fc_step_stats* st, double* gain, double* t_comp_s) {
+  if (!c || !st || !gain || !t_comp_s) return fail(FC_ERR_INVALID_ARGUMENT, "null argument");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  // this process's workers: (gain_r, t_comp) pairs
+  const double tc = (st->ms_ef + st->ms_select + st->ms_decode) * 1e-3;
+  std::vector<double> mine(2 * (size_t)c->n_local);
+  for (int i = 0; i < c->n_local; ++i) {
+    fc_worker_stats ws{};
+    TRY(fc_get_worker_stats(c, i, &ws));
+    if (ws.ge_norm2 <= 0.0) return fail(FC_ERR_RUNTIME, "degenerate gradient");
+    double g = (ag ? ws.topk_norm2 : ws.kept_norm2) / ws.ge_norm2;
+    if (!ag) g = std::min(std::max(g, 0.0), 1.0);  // std::clamp(kept / ge, 0, 1)
+    mine[2 * i] = g;
+    mine[2 * i + 1] = tc;
+  }
+  const int N = c->world;
+  double* all = c->h_norms;  // 2N pinned doubles, rank order
+  if (c->nccl) {
+    double* send = c->dnorms + N;
+    double* recv = c->dnorms + N + 2;
+    CUDA_TRY(cudaMemcpyAsync(send, mine.data(), 2 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    NCCL_TRY(ncclAllGather(send, recv, 2, ncclFloat64, c->comm_ring, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(all, recv, 2 * sizeof(double) * N, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+  } else {
+    for (int i = 0; i < 2 * N; ++i) all[i] = mine[i];
+  }
+  // gain_sum / n in rank order (inc/trainer.hpp:364-369, 387-396)
+  double sum = 0.0, tmax = 0.0;
+  for (int r = 0; r < N; ++r) {
+    sum += all[2 * r];
+    tmax = std::max(tmax, all[2 * r + 1]);
+  }
+  *gain = sum / N;
+  *t_comp_s = tmax;
   return FC_OK;
 }
 
@@ -900,6 +981,7 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
     const bool topk = mode == FC_VAR || (c->rank + i) == sel;
     TRY(run_ef(c, i, k, topk));
   }
+  advance_input(c);
   record(c, 1);
   for (int i = 0; i < c->n_local; ++i) {
     const bool topk = mode == FC_VAR || (c->rank + i) == sel;
@@ -909,7 +991,8 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
 
   // (2) VAR: allgather of N ||top-k||^2, argmax, ties -> lowest rank
   //     (select_var, inc/artopk.hpp:35-48)
-  if (mode == FC_VAR) {
+  if (mode == FC_VAR && N == 1) sel = 0;  // argmax over one worker
+  if (mode == FC_VAR && N > 1) {
     if (c->nccl) {
       NCCL_TRY(ncclAllGather(&c->w[0].ctl->topk_norm2, c->dnorms, 1, ncclFloat64, c->comm_ring,
                              c->stream));
@@ -930,7 +1013,15 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
   //     values (artopk.hpp:87-104); the zeros at bidx become owed zeros
   const unsigned* bsrc = nullptr;
   const float* contrib0 = nullptr;
-  if (c->nccl) {
+  const unsigned* own_bounds = nullptr;  // chunk bounds of bsrc, when a local select wrote them
+  if (c->nccl && N == 1) {
+    // a single rank: broadcast and allreduce are identities
+    Worker& w = c->w[0];
+    bsrc = w.pack;
+    contrib0 = reinterpret_cast<const float*>(w.pack + k);
+    w.kept_is_topk = true;
+    own_bounds = c->bounds;
+  } else if (c->nccl) {
     Worker& w = c->w[0];
     NCCL_TRY(ncclBroadcast(w.pack, c->bidx, k, ncclUint32, sel, c->comm_ring, c->stream));
     bsrc = c->bidx;
@@ -938,6 +1029,7 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
       // the selected worker's contribution is its own top-k values
       contrib0 = reinterpret_cast<const float*>(w.pack + k);
       w.kept_is_topk = true;
+      own_bounds = c->bounds;
     } else {
       fcb::launch_gather(bsrc, k, w.ge, w.contrib, w.ctl, w.ws.g_part, c->stream);
       LAUNCHED();
@@ -947,8 +1039,18 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
                            algo == FC_TREE ? c->comm_tree : c->comm_ring, c->stream));
   } else {
     bsrc = c->w[sel].pack;
+    own_bounds = c->bounds + (uint64_t)sel * (c->nch + 1);
     for (int i = 0; i < c->n_local; ++i) {
       Worker& w = c->w[i];
+      if (i == sel) {
+        // g_e at its own top-k indices are its top-k values
+        contrib0 = reinterpret_cast<const float*>(w.pack + k);
+        w.kept_is_topk = true;
+        if (N > 1)
+          CUDA_TRY(cudaMemcpyAsync(w.contrib, contrib0, k * sizeof(float), cudaMemcpyDeviceToDevice,
+                                   c->stream));
+        continue;
+      }
       fcb::launch_gather(bsrc, k, w.ge, w.contrib, w.ctl, w.ws.g_part, c->stream);
       LAUNCHED();
     }
@@ -956,19 +1058,24 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
   record(c, 3);
 
   // (4) densify (core.hpp:72-81); /N for Avg (collectives.hpp:85-87)
-  const float* lists = c->nccl ? c->reduced : c->contrib_all;
+  const float* lists = (c->nccl || N == 1) ? (N == 1 ? contrib0 : c->reduced) : c->contrib_all;
   const int nlists = c->nccl ? 1 : N;
   const uint64_t lstride = c->nccl ? 0 : c->kmax;
   // in-place update costs ~2k random sector RMWs: worth it below ~G/128
-  const bool incr_ok = !(c->flags & FC_FLAG_DENSE_DECODE) && k * 128 <= c->G;
-  TRY(wait_agg_free(c));
+  const bool incr_ok = !(c->flags & FC_FLAG_DENSE_DECODE) && c->nbuf == 1 && k * 128 <= c->G;
+  int ob = 0;
+  TRY(agg_target(c, &ob));
+  float* aggw = c->agg_buf[ob];
   if (incr_ok && c->agg_incr) {
     // in place: zero the previous support, write this one (same dense content)
     fcb::launch_agg_update(c->agg_support, c->agg_support_k, bsrc, k, lists, nlists, lstride,
-                           op == FC_AVG, (float)N, c->agg, c->zmaps, c->agg_support, c->stream);
+                           op == FC_AVG, (float)N, aggw, c->zmaps, c->agg_support, c->stream);
   } else {
-    fcb::launch_bounds(bsrc, k, 0, 1, c->G, c->bounds, c->stream);
-    fcb::launch_decode_ar(bsrc, c->bounds, lists, nlists, lstride, op == FC_AVG, (float)N, c->agg,
+    if (!own_bounds) {
+      fcb::launch_bounds(bsrc, k, 0, 1, c->G, c->bounds, c->stream);
+      own_bounds = c->bounds;
+    }
+    fcb::launch_decode_ar(bsrc, own_bounds, lists, nlists, lstride, op == FC_AVG, (float)N, aggw,
                           c->G, c->zmaps, c->stream);
     if (incr_ok)
       CUDA_TRY(cudaMemcpyAsync(c->agg_support, bsrc, k * sizeof(unsigned), cudaMemcpyDeviceToDevice,
@@ -979,7 +1086,7 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
   c->agg_support_k = incr_ok ? k : 0;
   record(c, 4);
   c->has_agg = true;
-  TRY(agg_written(c));
+  TRY(agg_written(c, ob));
   for (auto& w : c->w) {  // every worker owes zeros at the broadcast indices
     w.pz.zmap = c->zmaps;
     w.pz_idx = bsrc;
@@ -1007,6 +1114,7 @@ int fc_ag_step(fc_ctx* c, double cr, int compressor, fc_step_stats* st) {
 
   record(c, 0);
   for (int i = 0; i < c->n_local; ++i) TRY(run_ef(c, i, k, true));
+  advance_input(c);
   record(c, 1);
   for (int i = 0; i < c->n_local; ++i) {
     TRY(run_select(c, i, k));
@@ -1016,24 +1124,30 @@ int fc_ag_step(fc_ctx* c, double cr, int compressor, fc_step_stats* st) {
 
   const unsigned* packs;
   uint64_t stride;
-  if (c->nccl) {
+  bool local_bounds = true;  // every list's bounds were written by a local select
+  if (c->nccl && N == 1) {
+    packs = c->w[0].pack;  // allgather over one rank: identity
+    stride = 2 * k;
+  } else if (c->nccl) {
     NCCL_TRY(ncclAllGather(c->w[0].pack, c->ag_recv, 2 * k, ncclUint32, c->comm_ring, c->stream));
     packs = c->ag_recv;
     stride = 2 * k;
+    local_bounds = false;
   } else {
     packs = c->pack_all;
     stride = 2 * c->kmax;
   }
   record(c, 3);
-  fcb::launch_bounds(packs, k, stride, N, c->G, c->bounds, c->stream);
-  TRY(wait_agg_free(c));
-  fcb::launch_decode_ag(packs, stride, k, N, c->bounds, (float)N, c->agg, c->G, c->zmaps,
+  if (!local_bounds) fcb::launch_bounds(packs, k, stride, N, c->G, c->bounds, c->stream);
+  int ob = 0;
+  TRY(agg_target(c, &ob));
+  fcb::launch_decode_ag(packs, stride, k, N, c->bounds, (float)N, c->agg_buf[ob], c->G, c->zmaps,
                         c->nccl ? c->rank : 0, c->n_local, c->stream);
   LAUNCHED();
   c->agg_incr = false;  // the aggregate's support is now a union of N lists
   record(c, 4);
   c->has_agg = true;
-  TRY(agg_written(c));
+  TRY(agg_written(c, ob));
   // residual_update (compress.hpp:122-130): g_e - g_e = +0 at own indices
   for (int i = 0; i < c->n_local; ++i) {
     const int r = c->nccl ? c->rank : i;
@@ -1060,21 +1174,26 @@ int fc_dense_step(fc_ctx* c, int algo, int op, fc_step_stats* st) {
   record(c, 1);
   record(c, 2);
   for (int i = 0; i < c->n_local; ++i) TRY(wait_grad(c, i));
-  TRY(wait_agg_free(c));
-  if (c->nccl) {
-    NCCL_TRY(ncclAllReduce(c->w[0].g_o, c->agg, c->G, ncclFloat32, ncclSum,
+  int ob = 0;
+  TRY(agg_target(c, &ob));
+  float* aggw = c->agg_buf[ob];
+  if (c->nccl && N > 1) {
+    NCCL_TRY(ncclAllReduce(c->w[0].g_o, aggw, c->G, ncclFloat32, ncclSum,
                            algo == FC_TREE ? c->comm_tree : c->comm_ring, c->stream));
     record(c, 3);
-    if (op == FC_AVG) fcb::launch_dense_sum(c->agg, 1, 0, 1, (float)N, c->agg, c->G, c->stream);
-  } else {
+    if (op == FC_AVG) fcb::launch_dense_sum(aggw, 1, 0, 1, (float)N, aggw, c->G, c->stream);
+  } else {  // loopback, or a single NCCL rank (allreduce = identity)
     record(c, 3);
-    fcb::launch_dense_sum(c->g_o_all, N, c->gstride, op == FC_AVG, (float)N, c->agg, c->G, c->stream);
+    fcb::launch_dense_sum(c->g_o_all, c->n_local, c->gstride, op == FC_AVG, (float)N, aggw, c->G,
+                          c->stream);
   }
+  for (int i = 0; i < c->n_local; ++i) TRY(grad_consumed(c, i));
+  advance_input(c);
   LAUNCHED();
   c->agg_incr = false;
   record(c, 4);
   c->has_agg = true;
-  TRY(agg_written(c));
+  TRY(agg_written(c, ob));
   const double bus = N > 1 ? 2.0 * (N - 1) / N * 4.0 * c->G : 0.0;
   return finish_step(c, st, c->G, -1, algo == FC_TREE ? 2 : 1, 12.0 * c->G, bus, l0);
 }

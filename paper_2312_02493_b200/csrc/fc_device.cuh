@@ -86,8 +86,10 @@ void launch_ef(const float* g_o, float* ge, uint64_t G, uint64_t k, Ctl* ctl, co
                Pending pz, int add, int emit, cudaStream_t s);
 void launch_fallback(float* ge, uint64_t G, uint64_t k, Ctl* ctl, const ChunkWs& w, cudaStream_t s);
 // cooperative launch; returns a cudaError_t value (0 = success)
+// bounds_out (nullable): nchunks+1 entries, bounds_out[c] = first output
+// position whose index is >= c * kChunk (what k_bounds computes from a list)
 int launch_select(uint64_t k, Ctl* ctl, const ChunkWs& w, unsigned* out_idx, float* out_val,
-                  cudaStream_t s);
+                  unsigned* bounds_out, cudaStream_t s);
 void launch_gather(const unsigned* bidx, uint64_t k, const float* ge, float* contrib, Ctl* ctl,
                    double* part, cudaStream_t s);
 void launch_bounds(const unsigned* idx, uint64_t k, uint64_t list_stride, int nlists, uint64_t G,

@@ -593,7 +593,8 @@ __host__ __device__ inline unsigned sel_cache_cap(unsigned cpb) {
 
 __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __restrict__ ctl,
                                                            ChunkWs w, unsigned* __restrict__ out_idx,
-                                                           float* __restrict__ out_val) {
+                                                           float* __restrict__ out_val,
+                                                           unsigned* __restrict__ bounds_out) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char s_dyn[];
   __shared__ unsigned s_h[kSelBins];
@@ -863,6 +864,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
           const unsigned long long before = bp + s_pre[c];
           const unsigned long long gt_pre = before >> 31, eq_pre = before & 0x7fffffffull;
           o[u] = gt_pre + (eq_pre < needT ? eq_pre : needT);
+          if (bounds_out && lane == 0) bounds_out[c0 + c] = (unsigned)o[u];
           take[u] = eq_pre >= needT ? 0u
                                     : (unsigned)min((unsigned long long)(s_ge[c] & 0xFFFFu), needT - eq_pre);
           tseen[u] = 0;
@@ -899,6 +901,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
       const unsigned long long before = bp + s_pre[c];
       const unsigned long long gt_pre = before >> 31, eq_pre = before & 0x7fffffffull;
       unsigned long long o = gt_pre + (eq_pre < needT ? eq_pre : needT);
+      if (bounds_out) bounds_out[c0 + c] = (unsigned)o;  // first output index of chunk c
       const unsigned take = eq_pre >= needT ? 0u : (unsigned)min((unsigned long long)eq, needT - eq_pre);
       if (gt + take == 0) continue;
       const unsigned cnt = s_cnt[c];
@@ -954,6 +957,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
   }
   const double bsum = block_sum<kSelThreads>(acc, s_dred);
   if (tid == 0) w.bnorm[blockIdx.x] = bsum;
+  if (bounds_out && blockIdx.x == 0 && tid == 0) bounds_out[nch] = (unsigned)k;
   SEL_MARK(6);
   grid.sync();
   SEL_MARK(7);
@@ -965,7 +969,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
 
 // Grid of the cooperative select: one resident 1024-thread block per SM.
 int launch_select(uint64_t k, Ctl* ctl, const ChunkWs& w, unsigned* out_idx, float* out_val,
-                  cudaStream_t s) {
+                  unsigned* bounds_out, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelSmemMax);
@@ -976,7 +980,7 @@ int launch_select(uint64_t k, Ctl* ctl, const ChunkWs& w, unsigned* out_idx, flo
   if (cpb > (unsigned)kSelMaxCpb) return (int)cudaErrorInvalidValue;
   const unsigned smem = sel_arrays_bytes(cpb) + sel_cache_cap(cpb) * 4u;
   ChunkWs ws = w;
-  void* args[] = {&k, &ctl, &ws, &out_idx, &out_val};
+  void* args[] = {&k, &ctl, &ws, &out_idx, &out_val, &bounds_out};
   const cudaError_t e = cudaLaunchCooperativeKernel((void*)k_select, dim3(grid), dim3(kSelThreads),
                                                     args, smem, s);
   count_launch();

@@ -267,6 +267,16 @@ class Cluster:
     def sync(self) -> None:
         check(lib.fc_sync(self._ctx))
 
+    def moo_metrics(self, st: "StepStats", ag: bool = False) -> tuple[float, float]:
+        """(gain, t_comp seconds) of the last step, identical on every rank
+        (the Trainer's *_with_gain, inc/trainer.hpp:361-398; t_comp measured)."""
+        s = _abi.fc_step_stats()
+        for n, _ in s._fields_:
+            setattr(s, n, getattr(st, n))
+        g, t = C.c_double(), C.c_double()
+        check(lib.fc_moo_metrics(self._ctx, int(bool(ag)), C.byref(s), C.byref(g), C.byref(t)))
+        return g.value, t.value
+
     def stream_ptr(self) -> int:
         """cudaStream_t of the context (wrap with torch.cuda.ExternalStream)."""
         p = C.c_void_p()

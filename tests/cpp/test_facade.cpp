@@ -9,6 +9,7 @@
 #include <set>
 
 #include "flexcomm_b200/flexcomm.hpp"
+#include "flexcomm_b200/moo.hpp"
 #include "mini_test.hpp"
 
 using namespace flexcomm::b200;
@@ -307,6 +308,85 @@ TEST(Errors, MapToReferenceExceptions) {
                std::invalid_argument);
   EXPECT_THROW(residuals.of(2), std::out_of_range);
   EXPECT_THROW(Cluster(0, NetParams(0.001, 1e9), &clk, ctx), std::invalid_argument);
+}
+
+// tests/test_moo.cpp:29-46
+TEST(Ladder, DefaultRungsAndFactorTen) {
+  ControllerConfig cfg;
+  EXPECT_TRUE(candidate_ladder(cfg) == (std::vector<double>{0.1, 0.0333, 0.0111, 0.0037, 0.001}));
+  cfg.factor = 10.0;
+  EXPECT_TRUE(candidate_ladder(cfg) == (std::vector<double>{0.1, 0.01, 0.001}));
+  cfg.c_low = cfg.c_high = 0.05;
+  EXPECT_TRUE(candidate_ladder(cfg) == (std::vector<double>{0.05}));
+  cfg.c_low = 0.2;
+  EXPECT_THROW(candidate_ladder(cfg), std::invalid_argument);
+  EXPECT_DOUBLE_EQ(round_3sig(123456.0), 123000.0);
+}
+
+// tests/test_moo.cpp:97-113
+TEST(Knee, PicksBalancedCandidateAndTiesGoToLargerRatio) {
+  auto cand = [](double c, double tc, double ts, double inv_gain) {
+    return CandidateCR{c, 1.0 / inv_gain, tc, ts};
+  };
+  std::vector<CandidateCR> front = {cand(0.1, 1.0, 9.0, 9.0), cand(0.01, 5.0, 5.0, 5.0),
+                                    cand(0.001, 9.0, 9.0, 1.0)};
+  auto ch = choose_cr(front, NetParams(0.001, 10e9), 4e7, 8);
+  EXPECT_EQ(ch.candidate.c, 0.01);
+  EXPECT_TRUE(ch.collective == select_collective(NetParams(0.001, 10e9), MessageSpec(4e7, 0.01, 8)).collective);
+  std::vector<CandidateCR> tie = {cand(0.01, 1.0, 2.0, 2.0), cand(0.1, 2.0, 1.0, 2.0)};
+  EXPECT_EQ(choose_cr(tie, NetParams(0.001, 10e9), 4e7, 8).candidate.c, 0.1);
+  EXPECT_THROW(choose_cr({}, NetParams(0.001, 10e9), 4e7, 8), std::invalid_argument);
+}
+
+// tests/test_moo.cpp:115-135 on device residuals
+TEST(Controller, ExploreRestoresTrajectory) {
+  auto ctx = make_ctx(2, 50000);
+  NetworkSchedule sched;
+  sched.segments = {{0, NetParams(0.001, 10e9)}};
+  SyncConfig cfg;
+  cfg.adaptive = true;
+  cfg.c = 0.01;
+  SyncTrainer trainer(ctx, cfg, sched);
+  trainer.step();
+  const auto r0 = ctx->residual(0), r1 = ctx->residual(1);
+  const long step_before = trainer.step_index();
+  ControllerConfig cc;
+  cc.probe_iters = 3;
+  Controller controller(cc);
+  controller.explore(trainer, sched.segments[0].net);
+  EXPECT_TRUE(ctx->residual(0) == r0);
+  EXPECT_TRUE(ctx->residual(1) == r1);
+  EXPECT_EQ(trainer.step_index(), step_before);
+  EXPECT_TRUE(!trainer.probe_mode());
+  EXPECT_TRUE(trainer.clock().of(Category::Exploration) > 0.0);
+  EXPECT_EQ(controller.candidates().size(), candidate_ladder(controller.config()).size());
+  for (const auto& c : controller.candidates()) {
+    EXPECT_TRUE(c.gain_avg > 0.0 && c.gain_avg <= 1.0);
+    EXPECT_TRUE(c.t_comp_avg > 0.0);
+  }
+}
+
+// tests/test_moo.cpp:137-169
+TEST(Controller, HookSelectsOnFirstStepAndOnNetworkChange) {
+  auto ctx = make_ctx(2, 40000);
+  NetworkSchedule sched;
+  sched.segments = {{0, NetParams(0.001, 25e9)}, {1, NetParams(0.001, 1e9)}};
+  SyncConfig cfg;
+  cfg.adaptive = true;
+  cfg.size_bytes_override = 4e7;
+  cfg.epochs = 2;
+  cfg.steps_per_epoch = 4;
+  SyncTrainer trainer(ctx, cfg, sched);
+  Controller controller{ControllerConfig()};
+  trainer.run(controller.hook());
+  std::vector<ControllerEvent> net_events;
+  for (const auto& e : controller.events())
+    if (e.trigger == "network") net_events.push_back(e);
+  ASSERT_EQ(net_events.size(), 1u);
+  EXPECT_EQ(net_events[0].step, cfg.steps_per_epoch);
+  EXPECT_TRUE(net_events[0].chosen_c >= 0.001 && net_events[0].chosen_c <= 0.1);
+  EXPECT_TRUE(net_events[0].front_size >= 1u);
+  EXPECT_EQ(trainer.metrics().size(), 8u);
 }
 
 int main() { return mt::run_all(); }

@@ -162,6 +162,62 @@ def costmodel_cases(ref):
     return {"select": sel, "crossover": cross, "ladder_default": ladder}
 
 
+def moo_cases(ref):
+    """MOO controller decision functions (inc/moo.hpp:44-146, netsched.hpp:50-58)."""
+    rng = np.random.default_rng(77)
+    ladders = []
+    for _ in range(120):
+        c_high = float(10 ** rng.uniform(-3, 0))
+        c_low = float(c_high * 10 ** -rng.uniform(0, 3))
+        factor = float(rng.choice([1.5, 2.0, 3.0, 3.3, 10.0]) if rng.random() < 0.5
+                       else rng.uniform(1.01, 12))
+        ladders.append({"c_low": c_low, "c_high": c_high, "factor": factor,
+                        "ladder": ref.candidate_ladder(c_low, c_high, factor)})
+    r3 = []
+    for v in list(10 ** rng.uniform(-9, 9, 200)) + [0.0333333, 0.0111111, 0.0037037, 123456.0,
+                                                      0.0, 0.00125, 0.0445, 2.5e-3]:
+        v = float(v) * (-1.0 if rng.random() < 0.2 else 1.0)
+        r3.append([v, ref.round_3sig(v)])
+    knee = []
+    for _ in range(300):
+        m = int(rng.integers(1, 9))
+        rows = []
+        for i in range(m):
+            if rows and rng.random() < 0.2:  # exact duplicates / ties
+                rows.append(list(rows[int(rng.integers(0, len(rows)))]))
+                rows[-1][0] = float(rng.choice([0.1, 0.0333, 0.0111, 0.0037, 0.001]))
+                continue
+            rows.append([float(rng.choice([0.1, 0.0333, 0.0111, 0.0037, 0.001])),
+                         float(rng.uniform(0.05, 1.0)), float(10 ** rng.uniform(-5, -1)),
+                         float(10 ** rng.uniform(-5, 0))])
+        alpha = float(rng.uniform(1e-6, 0.01))
+        bw = float(10 ** rng.uniform(9, 13))
+        mb = float(10 ** rng.uniform(5, 10))
+        n = int(rng.integers(2, 65))
+        mask, chosen, coll = ref.choose_cr(np.array(rows), alpha, bw, mb, n)
+        knee.append({"rows": rows, "alpha": alpha, "bw": bw, "m": mb, "n": n,
+                     "mask": [int(x) for x in mask], "chosen": chosen, "collective": coll})
+    trig = []
+    for _ in range(200):
+        cnt = int(rng.integers(0, 12))
+        samples = [float(x) for x in rng.uniform(0.2, 1.0, cnt)]
+        window = int(rng.integers(1, 10))
+        gref = float(rng.choice([-1.0, 0.0, float(rng.uniform(0.2, 1.0))]))
+        thr = float(rng.choice([0.0, 0.05, 0.1, 0.25]))
+        trig.append({"gain_ref": gref, "samples": samples, "window": window, "threshold": thr,
+                     "fire": ref.trigger_gain(gref, samples, window, thr)})
+    net = []
+    for _ in range(200):
+        a0 = float(rng.uniform(0, 0.01))
+        b0 = float(10 ** rng.uniform(8, 12))
+        a1 = a0 * float(rng.choice([1.0, 1.0 + rng.uniform(-0.2, 0.2)]))
+        b1 = b0 * float(rng.choice([1.0, 1.0 + rng.uniform(-0.2, 0.2)]))
+        rel = float(rng.choice([0.0, 0.05, 0.1]))
+        net.append({"a0": a0, "b0": b0, "a1": a1, "b1": b1, "rel": rel,
+                    "changed": ref.network_changed(a0, b0, a1, b1, rel)})
+    return {"ladder": ladders, "round_3sig": r3, "knee": knee, "trigger": trig, "network": net}
+
+
 def main():
     oracle.build()
     ref, f32 = oracle.Ref(), oracle.F32()
@@ -174,6 +230,7 @@ def main():
         "artopk": artopk_cases(ref),
         "ag": ag_cases(ref),
         "costmodel": costmodel_cases(ref),
+        "moo": moo_cases(ref),
     }
     OUT.write_text(json.dumps(data, separators=(",", ":")))
     print(f"wrote {OUT} ({OUT.stat().st_size / 1e6:.2f} MB)")

@@ -91,6 +91,30 @@ def main() -> int:
                         if np.any(np.abs(ref[nz]) > 0):
                             failures.append(f"step {s} {kind}: aggregate support differs")
             print(f"[mp_check] step {s} {kind} algo={algo} c={c} ok={not failures}", flush=True)
+
+        # MOO controller over the NCCL path: every rank must take the same
+        # decisions (gains and measured compression times are rank-identical)
+        from paper_2312_02493_b200 import moo
+
+        sched = moo.NetworkSchedule([moo.Segment(0, fc.NetParams(5e-6, 4.5e12)),
+                                     moo.Segment(1, fc.NetParams(5e-6, 4.5e10))])
+        tr = moo.SyncTrainer(cl, moo.SyncConfig(epochs=2, steps_per_epoch=3, adaptive=True,
+                                                seed=77), sched)
+        ctl = moo.Controller(moo.ControllerConfig(probe_iters=2))
+        tr.run(ctl.hook())
+        summary = np.array([x for cnd in ctl.candidates
+                            for x in (cnd.c, cnd.gain_avg, cnd.t_comp_avg, cnd.t_sync_modeled)]
+                           + [x for e in ctl.events
+                              for x in (e.step, e.chosen_c, int(e.collective), e.front_size)]
+                           + [m.gain for m in tr.metrics] + [m.cr_used for m in tr.metrics])
+        allsum = env.gather_arrays(summary)
+        if env.rank == 0:
+            if any(not np.array_equal(a, allsum[0]) for a in allsum):
+                failures.append("MOO: ranks took different decisions")
+            if len([e for e in ctl.events if e.trigger == "network"]) != 1:
+                failures.append(f"MOO: expected one network event, got {ctl.events}")
+            print(f"[mp_check] moo events={[(e.step, e.trigger, e.chosen_c) for e in ctl.events]} "
+                  f"ok={not failures}", flush=True)
     if env.rank == 0:
         print("MP_CHECK", "PASS" if not failures else "FAIL", env.world, flush=True)
         for f in failures[:20]:

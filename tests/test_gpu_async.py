@@ -8,8 +8,9 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("kind", ["star", "ag"])
-def test_async_pipeline_matches_oracle(fc, f32, kind):
+@pytest.mark.parametrize("pipeline", [False, True])
+@pytest.mark.parametrize("kind", ["star", "ag", "dense"])
+def test_async_pipeline_matches_oracle(fc, f32, kind, pipeline):
     import torch
 
     from paper_2312_02493_b200 import _abi
@@ -18,11 +19,14 @@ def test_async_pipeline_matches_oracle(fc, f32, kind):
     uid = fc.get_unique_id()
     hosts = [torch.from_numpy(f32.synth(g, 31, 0, s)).pin_memory() for s in range(steps)]
     outs = [torch.empty(g, dtype=torch.float32).pin_memory() for _ in range(steps)]
-    with fc.Cluster.nccl(1, 0, uid, g, device=0, max_cr=0.1, flags=_abi.FC_FLAG_ASYNC) as cl:
+    flags = _abi.FC_FLAG_ASYNC | (_abi.FC_FLAG_PIPELINE if pipeline else 0)
+    with fc.Cluster.nccl(1, 0, uid, g, device=0, max_cr=0.1, flags=flags) as cl:
         for s in range(steps):
             cl.set_grad(0, hosts[s], async_=True)
             if kind == "ag":
                 cl.ag_step(c, stats=False)
+            elif kind == "dense":
+                cl.dense_step(fc.RING, fc.AVG, stats=False)
             else:
                 cl.artopk_step(c, fc.STAR, fc.RING, s, fc.AVG, stats=False)
             cl.aggregate(outs[s], async_=True)
@@ -31,7 +35,12 @@ def test_async_pipeline_matches_oracle(fc, f32, kind):
     res = np.zeros((1, g), np.float32)
     for s in range(steps):
         g_o = hosts[s].numpy()[None, :]
-        ref = f32.ag_step(g_o, res, c) if kind == "ag" else f32.artopk_step(g_o, res, c, 0, s, 1)[0]
+        if kind == "dense":
+            ref = f32.dense(g_o, 1)
+        elif kind == "ag":
+            ref = f32.ag_step(g_o, res, c)
+        else:
+            ref = f32.artopk_step(g_o, res, c, 0, s, 1)[0]
         assert np.array_equal(outs[s].numpy().view(np.uint32), ref.view(np.uint32)), f"step {s}"
     assert np.array_equal(res_gpu.view(np.uint32), res[0].view(np.uint32))
 

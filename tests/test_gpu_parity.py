@@ -91,8 +91,8 @@ def test_topk_adversarial_ties(fc, f32):
 
 # ------------------------------------------------------------ full protocol --
 
-def trajectory(fc, f32, n, g, steps, mode, op, crs, dist, seed, algo=0):
-    with fc.Cluster(n, g) as cl:
+def trajectory(fc, f32, n, g, steps, mode, op, crs, dist, seed, algo=0, flags=0):
+    with fc.Cluster(n, g, flags=flags) as cl:
         res = np.zeros((n, g), np.float32)
         for s in range(steps):
             c = crs[s % len(crs)]
@@ -117,6 +117,16 @@ def trajectory(fc, f32, n, g, steps, mode, op, crs, dist, seed, algo=0):
 @pytest.mark.parametrize("mode", [0, 1])
 def test_artopk_trajectory_bit_exact(fc, f32, n, mode):
     trajectory(fc, f32, n, 40_000 + 17 * n, 5, mode, 1, [0.01, 0.1, 0.003], n % 3, 100 + n)
+
+
+def test_artopk_dense_decode_flag(fc, f32):
+    """FC_FLAG_DENSE_DECODE: the tile decode at every k (no in-place support
+    update), bit-exact like the default path."""
+    from paper_2312_02493_b200 import _abi
+
+    for n, mode in ((1, 0), (3, 0), (2, 1)):
+        trajectory(fc, f32, n, 70_001, 6, mode, 1, [0.01, 0.001, 0.2, 0.003], 0, 31 + n,
+                   flags=_abi.FC_FLAG_DENSE_DECODE)
 
 
 @pytest.mark.parametrize("op", [0, 1])

@@ -5,17 +5,19 @@ from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2312_02493_b200 import flexcomm as fc  # noqa: E402
-from paper_2312_02493_b200._abi import check, lib  # noqa: E402
+from paper_2312_02493_b200._abi import FC_FLAG_DENSE_DECODE, check, lib  # noqa: E402
 
 G = int(sys.argv[1]) if len(sys.argv) > 1 else 138_000_000
 cr = float(sys.argv[2]) if len(sys.argv) > 2 else 0.01
+flags = FC_FLAG_DENSE_DECODE if "dense" in sys.argv[3:] else 0
 names = ["staged", "digit1", "digit2", "digit3", "counted", "emitted", "end"]
-with fc.Cluster(1, G, max_cr=max(cr, 0.1)) as cl:
+with fc.Cluster(1, G, max_cr=max(cr, 0.1), flags=flags) as cl:
     cl.fill_synthetic(0, 42, 0, 0)
     for s in range(4):
         st = cl.artopk_step(cr, fc.STAR, fc.RING, s)
         t = (C.c_uint64 * 8)()
         check(lib.fc_diag_select_phases(cl._ctx, 0, t))
         ws = cl.worker_stats(0)
-        print(f"step {s}: total {st.ms_total * 1e3:.0f}us select {st.ms_select * 1e3:.0f}us cand {ws.candidates} "
+        print(f"step {s}: total {st.ms_total * 1e3:.0f}us ef {st.ms_ef * 1e3:.0f}us select {st.ms_select * 1e3:.0f}us "
+              f"exch {st.ms_exchange * 1e3:.0f}us decode {st.ms_decode * 1e3:.0f}us cand {ws.candidates} "
               + " ".join(f"{n}={(t[i + 1] - t[i]) / 1e3:.1f}us" for i, n in enumerate(names)))

@@ -1,12 +1,15 @@
 """Per-phase device time (CUDA events on the library stream) of single steps
 for the BASELINE configurations, one GPU (loopback workers).
-Usage: python tools/diag_step.py"""
+Usage: python tools/diag_step.py [dense]   (dense: FC_FLAG_DENSE_DECODE)"""
 import json
 import sys
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2312_02493_b200 import _abi  # noqa: E402
 from paper_2312_02493_b200 import flexcomm as fc  # noqa: E402
+
+FLAGS = _abi.FC_FLAG_DENSE_DECODE if "dense" in sys.argv[1:] else 0
 
 CONFIGS = [
     ("C1 STAR 11.7M CR.01 N=2", 11_700_000, 2, "star", 0.01),
@@ -18,7 +21,7 @@ CONFIGS = [
 ]
 out = []
 for name, G, n, mode, cr in CONFIGS:
-    with fc.Cluster(n, G, max_cr=max(cr, 0.1)) as cl:
+    with fc.Cluster(n, G, max_cr=max(cr, 0.1), flags=FLAGS) as cl:
         for r in range(n):
             cl.fill_synthetic(r, 42, r, 0)
         rows = []
