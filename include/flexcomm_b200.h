@@ -292,8 +292,13 @@ int fc_ef_kernel_timing(fc_ctx* ctx, double* mean_ms, uint64_t* launches, int re
  * 6 EF + emission + owed zeros. */
 int fc_diag_kernel_ms(fc_ctx* ctx, int which, int iters, double* ms_out);
 /* Diagnostics: %globaltimer (ns) at the select kernel's phase boundaries of
- * the last step (start, staged, digit 1/2/3 resolved, counted, emitted, end). */
-int fc_diag_select_phases(fc_ctx* ctx, int worker, uint64_t* out8);
+ * the last step (start, staged, digit 1/2/3 resolved, counted, emitted, end),
+ * then the EF kernel's (start, sample barrier passed, bound derived, end of
+ * block 0's stream): out12 holds 12 values. */
+int fc_diag_select_phases(fc_ctx* ctx, int worker, uint64_t* out12);
+/* Diagnostics: %globaltimer (ns) at the start and end of every EF block of the
+ * last step (2 x grid values, grid = number of SMs). */
+int fc_diag_ef_blocks(fc_ctx* ctx, int worker, uint64_t* out, int n);
 /* Diagnostics (NVLink calibration): mean device ms of one NCCL collective on
  * this context's communicators, all ranks calling alike.  which: 0 broadcast,
  * 1 ring allreduce, 2 tree allreduce, 3 allgather (bytes per rank),

@@ -139,6 +139,7 @@ def _load() -> C.CDLL:
         "fc_diag_kernel_ms": ([P, i, i, C.POINTER(d)], i),
         "fc_diag_select_phases": ([P, i, C.POINTER(u64)], i),
         "fc_diag_collective_ms": ([P, i, u64, i, C.POINTER(d)], i),
+        "fc_diag_ef_blocks": ([P, i, C.POINTER(u64), i], i),
         # host cost model (csrc/fc_costmodel.cpp)
         "fc_cost_primitives": ([d, d, d, d, i, C.POINTER(d)], i),
         "fc_select_collective": ([d, d, d, d, i, C.POINTER(i), C.POINTER(d)], i),
@@ -172,7 +173,7 @@ EXPORTS = [
     "fc_residual_ptr", "fc_reset_residuals", "fc_get_aggregate", "fc_aggregate_ptr",
     "fc_get_topk", "fc_get_worker_stats", "fc_snapshot", "fc_restore", "fc_artopk_step",
     "fc_ag_step", "fc_dense_step", "fc_topk_exact", "fc_sync", "fc_join", "fc_stream", "fc_ef_kernel_timing",
-    "fc_diag_kernel_ms", "fc_diag_select_phases", "fc_diag_collective_ms",
+    "fc_diag_kernel_ms", "fc_diag_select_phases", "fc_diag_collective_ms", "fc_diag_ef_blocks",
     "fc_cost_primitives", "fc_select_collective", "fc_prefer", "fc_crossover_cr",
     "fc_derive_m_from_ag",
     "fc_controller_config_validate", "fc_round_3sig", "fc_candidate_ladder", "fc_trigger_gain",

@@ -69,8 +69,10 @@ struct Worker {
   float* g_o = nullptr;
   float* ge = nullptr;  // the residual store; holds g_e between EF and gather
   float* snap = nullptr;
-  fcb::Ctl* ctl = nullptr;
-  size_t ctl_bytes = 0;     // zeroed per step
+  fcb::Ctl* ctl = nullptr;      // this step's control block
+  fcb::Ctl* ctl_buf[2] = {};    // alternate steps; each EF zeroes the other one
+  int ctl_next = 0;             // the clean one the next EF pass uses
+  size_t ctl_bytes = 0;
   fcb::ChunkWs ws{};
   unsigned* pack = nullptr;  // [idx k | val k], capacity 2*kmax
   float* contrib = nullptr;  // capacity kmax
@@ -251,22 +253,29 @@ int materialize_all(fc_ctx* c) {
 
 // EF + (optionally) candidate emission for worker i; times the EF kernel of
 // local worker 0 (the dominant kernel) for the roofline.
+// Switch worker w to its clean control block; returns the other one (which
+// the EF pass about to run zeroes for the next step).
+fcb::Ctl* take_ctl(Worker& w) {
+  w.ctl = w.ctl_buf[w.ctl_next];
+  w.ctl_next ^= 1;
+  return w.ctl_buf[w.ctl_next];
+}
+
 int run_ef(fc_ctx* c, int i, uint64_t k, bool topk) {
   Worker& w = c->w[i];
-  const bool force_fb = std::getenv("FC_FORCE_FALLBACK") != nullptr;
-  CUDA_TRY(cudaMemsetAsync(w.ctl, 0, w.ctl_bytes, c->stream));
+  const int force_fb = std::getenv("FC_FORCE_FALLBACK") != nullptr ? 2 : 0;
+  fcb::Ctl* next = take_ctl(w);
   TRY(wait_grad(c, i));
-  if (topk) {
-    fcb::launch_sample(w.g_o, w.ge, c->G, k, w.ctl, 1, w.pz, force_fb ? 1 : 0, c->stream);
-    LAUNCHED();
-  }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (i == 0 && c->timing) {
     e0 = c->take_event();
     e1 = c->take_event();
     cudaEventRecord(e0, c->stream);
   }
-  fcb::launch_ef(w.g_o, w.ge, c->G, k, w.ctl, w.ws, w.pz, 1, topk ? 1 : 0, c->stream);
+  // EF, with the candidate bound sampled in the same kernel when Top-k follows
+  const int e = fcb::launch_ef(w.g_o, w.ge, c->G, k, w.ctl, w.ws, w.pz, 1, topk ? 1 : 0,
+                               topk ? (1 | force_fb) : 0, next, c->stream);
+  if (e) return fail(FC_ERR_CUDA, std::string("k_ef launch: ") + cudaGetErrorString(static_cast<cudaError_t>(e)));
   LAUNCHED();
   TRY(grad_consumed(c, i));
   w.pz = fcb::Pending{};  // consumed
@@ -276,18 +285,15 @@ int run_ef(fc_ctx* c, int i, uint64_t k, bool topk) {
     cudaEventRecord(e1, c->stream);
     c->ef_pending.emplace_back(e0, e1);
   }
-  if (topk) {
-    fcb::launch_fallback(w.ge, c->G, k, w.ctl, w.ws, c->stream);
-    LAUNCHED();
-  }
   return FC_OK;
 }
 
 // Top-k of worker i into its pack; also writes the chunk bounds of the
 // selection into bounds slot i (so a decode of this list needs no k_bounds).
-int run_select(fc_ctx* c, int i, uint64_t k) {
+int run_select(fc_ctx* c, int i, uint64_t k, const float* ef_out = nullptr) {
   Worker& w = c->w[i];
-  const int e = fcb::launch_select(k, w.ctl, w.ws, w.pack, reinterpret_cast<float*>(w.pack + k),
+  const int e = fcb::launch_select(k, w.ctl, w.ws, ef_out ? ef_out : w.ge, c->G, w.pack,
+                                   reinterpret_cast<float*>(w.pack + k),
                                    c->bounds + (uint64_t)i * (c->nch + 1), c->stream);
   if (e) return fail(FC_ERR_CUDA, std::string("k_select launch: ") +
                                       cudaGetErrorString(static_cast<cudaError_t>(e)));
@@ -488,7 +494,11 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
     w.pack = c->pack_all + i * 2 * c->kmax;
     w.contrib = c->contrib_all + i * c->kmax;
     w.ctl_bytes = sizeof(fcb::Ctl);
-    TRY(c->alloc(&w.ctl, 1));
+    for (auto& cb : w.ctl_buf) {
+      TRY(c->alloc(&cb, 1));
+      CUDA_TRY(cudaMemsetAsync(cb, 0, w.ctl_bytes, c->stream));
+    }
+    w.ctl = w.ctl_buf[0];
     fcb::ChunkWs& s = w.ws;
     s.nchunks = nch;
     s.ef_grid = ef_grid;
@@ -499,7 +509,9 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
     TRY(c->alloc(&s.cand_idx, (uint64_t)nch << fcb::kChunkShift));
     TRY(c->alloc(&s.cand_val, (uint64_t)nch << fcb::kChunkShift));
     TRY(c->alloc(&s.ef_part, ef_grid));
+    TRY(c->alloc(&s.cnorm, nch));
     TRY(c->alloc(&s.g_part, 4096));
+    TRY(c->alloc(&s.tblk, 2 * (uint64_t)ef_grid));
   }
   CUDA_TRY(cudaStreamSynchronize(c->stream));
 
@@ -697,9 +709,12 @@ int fc_get_worker_stats(fc_ctx* c, int worker, fc_worker_stats* out) {
   TRY(check_worker(c, worker));
   if (!out) return fail(FC_ERR_INVALID_ARGUMENT, "null output");
   CUDA_TRY(cudaSetDevice(c->device));
+  Worker& wk = c->w[worker];
+  // ||g_e||^2 of the last EF pass, summed over its per-chunk partials in chunk order
+  fcb::launch_sum_fixed(wk.ws.cnorm, c->nch, &wk.ctl->ge_norm2, c->stream);
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   fcb::Ctl h;
-  CUDA_TRY(cudaMemcpy(&h, c->w[worker].ctl, offsetof(fcb::Ctl, hist_s), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(&h, wk.ctl, offsetof(fcb::Ctl, hist_s), cudaMemcpyDeviceToHost));
   out->ge_norm2 = h.ge_norm2;
   out->kept_norm2 = c->w[worker].kept_is_topk ? h.topk_norm2 : h.kept_norm2;
   out->topk_norm2 = h.topk_norm2;
@@ -833,10 +848,7 @@ int fc_diag_kernel_ms(fc_ctx* c, int which, int iters, double* ms_out) {
   cudaEvent_t e0 = c->take_event(), e1 = c->take_event();
   double sum = 0.0;
   for (int it = 0; it < iters + 1; ++it) {
-    if (which >= 5) {
-      CUDA_TRY(cudaMemsetAsync(w.ctl, 0, w.ctl_bytes, c->stream));
-      fcb::launch_sample(w.g_o, w.ge, c->G, k, w.ctl, 1, fcb::Pending{}, 0, c->stream);
-    }
+    if (which >= 4) CUDA_TRY(cudaMemsetAsync(w.ctl, 0, w.ctl_bytes, c->stream));  // work queue, bound
     fcb::Pending pz{};
     if (which == 6) pz.zmap = c->zmaps;
     cudaEventRecord(e0, c->stream);
@@ -845,9 +857,9 @@ int fc_diag_kernel_ms(fc_ctx* c, int which, int iters, double* ms_out) {
       case 1: fcb::launch_triad(w.g_o, w.ge, c->G & ~uint64_t(3), 4, c->stream); break;
       case 2: fcb::launch_triad(w.g_o, w.ge, c->G & ~uint64_t(3), 8, c->stream); break;
       case 3: fcb::launch_fill_zero(c->agg, c->G & ~uint64_t(3), 8, c->stream); break;
-      case 4: fcb::launch_ef(w.g_o, w.ge, c->G, k, w.ctl, w.ws, pz, 1, 0, c->stream); break;
+      case 4: fcb::launch_ef(w.g_o, w.ge, c->G, k, w.ctl, w.ws, pz, 1, 0, 0, nullptr, c->stream); break;
       case 5:
-      case 6: fcb::launch_ef(w.g_o, w.ge, c->G, k, w.ctl, w.ws, pz, 1, 1, c->stream); break;
+      case 6: fcb::launch_ef(w.g_o, w.ge, c->G, k, w.ctl, w.ws, pz, 1, 1, 1, nullptr, c->stream); break;
       default: return fail(FC_ERR_INVALID_ARGUMENT, "unknown diagnostic kernel");
     }
     LAUNCHED();
@@ -915,13 +927,23 @@ int fc_diag_collective_ms(fc_ctx* c, int which, uint64_t bytes, int iters, doubl
 
 // Diagnostics: %globaltimer (ns) at k_select's phase boundaries in the last
 // step of `worker` (block 0): start, staged, digit 1/2/3, counted, emitted, end.
-int fc_diag_select_phases(fc_ctx* c, int worker, uint64_t* out8) {
+int fc_diag_select_phases(fc_ctx* c, int worker, uint64_t* out12) {
   TRY(check_worker(c, worker));
-  if (!out8) return fail(FC_ERR_INVALID_ARGUMENT, "null output");
+  if (!out12) return fail(FC_ERR_INVALID_ARGUMENT, "null output");
   CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
-  CUDA_TRY(cudaMemcpy(out8, &c->w[worker].ctl->tphase[0], 8 * sizeof(uint64_t),
+  CUDA_TRY(cudaMemcpy(out12, &c->w[worker].ctl->tphase[0], 12 * sizeof(uint64_t),
                       cudaMemcpyDeviceToHost));
+  return FC_OK;
+}
+
+int fc_diag_ef_blocks(fc_ctx* c, int worker, uint64_t* out, int n) {
+  TRY(check_worker(c, worker));
+  if (!out || n < 0) return fail(FC_ERR_INVALID_ARGUMENT, "bad output");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  const int m = std::min<int>(n, 2 * (int)c->w[worker].ws.ef_grid);
+  CUDA_TRY(cudaMemcpy(out, c->w[worker].ws.tblk, m * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   return FC_OK;
 }
 
@@ -937,17 +959,18 @@ int fc_topk_exact(fc_ctx* c, int worker, double cr, fc_step_stats* st) {
   TRY(materialize_all(c));
   const uint64_t l0 = fcb::launches();
   Worker& w = c->w[worker];
-  const bool force_fb = std::getenv("FC_FORCE_FALLBACK") != nullptr;
+  const int force_fb = std::getenv("FC_FORCE_FALLBACK") != nullptr ? 2 : 0;
   record(c, 0);
-  CUDA_TRY(cudaMemsetAsync(w.ctl, 0, w.ctl_bytes, c->stream));
+  fcb::Ctl* next = take_ctl(w);
   TRY(wait_grad(c, worker));
-  fcb::launch_sample(nullptr, w.g_o, c->G, k, w.ctl, 0, fcb::Pending{}, force_fb ? 1 : 0, c->stream);
-  fcb::launch_ef(nullptr, w.g_o, c->G, k, w.ctl, w.ws, fcb::Pending{}, 0, 1, c->stream);
-  fcb::launch_fallback(w.g_o, c->G, k, w.ctl, w.ws, c->stream);
+  // the "error-fed" vector is the gradient itself (no residual added)
+  const int e = fcb::launch_ef(nullptr, w.g_o, c->G, k, w.ctl, w.ws, fcb::Pending{}, 0, 1,
+                               1 | force_fb, next, c->stream);
+  if (e) return fail(FC_ERR_CUDA, std::string("k_ef launch: ") + cudaGetErrorString(static_cast<cudaError_t>(e)));
   TRY(grad_consumed(c, worker));
   LAUNCHED();
   record(c, 1);
-  TRY(run_select(c, worker, k));
+  TRY(run_select(c, worker, k, w.g_o));
   record(c, 2);
   record(c, 3);
   record(c, 4);

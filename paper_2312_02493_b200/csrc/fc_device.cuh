@@ -30,20 +30,22 @@ static_assert((1 << kDecShift) == kDecTile, "decode tile must be a power of two"
 // k_select over the candidates the error-feedback pass emits.
 constexpr int kShift1 = 19, kBins1 = 4096;    // bits 30..19 (exponent + 3 mantissa)
 
-constexpr int kSampleBlocks = 128;            // 128 x 256 = 32768 samples
-constexpr int kSamples = kSampleBlocks * kThreads;
+constexpr int kSamples = 32768;                // candidate-bound sample size
 
-// Per-worker control block, zeroed at the start of every step (one memset).
+// Per-worker control block.  Each worker has two, used by alternate steps; the
+// EF pass of one step zeroes the other for the next step.
 struct Ctl {
   unsigned L_digit;       // candidate bound: key >= L_digit << kShift1
   unsigned fallback;      // 1 => sampled bound missed, full re-emission ran
   unsigned cand_count;    // M: candidates emitted
   unsigned done_sample, done_ef, done_fbh, done_fbe, done_gather;
+  unsigned ef_next;       // EF work queue: next chunk to hand out
   unsigned b1, b2, T;     // radix digits and the final threshold key
   unsigned pad0;
   unsigned long long need1, needT, count_gt;
   double ge_norm2, topk_norm2, kept_norm2;
   unsigned long long tphase[8];  // %globaltimer at k_select phase boundaries (diagnostics)
+  unsigned long long tphase_ef[4];  // ... and at k_ef's (start, sampled, bound, end)
   unsigned hist_s[kBins1];   // sample histogram (digit 1)
   unsigned hist1[kBins1];    // candidate histogram, key bits 30..19 (k_select)
   unsigned hist_fb[kBins1];  // full histogram (fallback only)
@@ -60,8 +62,10 @@ struct ChunkWs {
   double* bnorm;              // k_select: per-block sum of squares of selected values
   unsigned* cand_idx;
   float* cand_val;
-  double* ef_part;            // one per EF block (fixed grid => deterministic)
+  double* ef_part;            // (unused)
+  double* cnorm;              // per chunk: sum of g_e^2 (fp64), reduced in chunk order on demand
   double* g_part;             // one per gather block
+  unsigned long long* tblk;   // diagnostics: %globaltimer at each EF block's start and end
   unsigned nchunks;
   unsigned ef_grid;
 };
@@ -80,16 +84,21 @@ __host__ __device__ inline unsigned zmap_bit(uint64_t i) { return 1u << ((unsign
 
 // Kernel launchers (fc_kernels.cu).  All take the context stream.
 void launch_fill_synth(float* dst, uint64_t G, uint64_t key, int dist, cudaStream_t s);
-void launch_sample(const float* g_o, const float* ge, uint64_t G, uint64_t k, Ctl* ctl, int add,
-                   Pending pz, int force_fallback, cudaStream_t s);
-void launch_ef(const float* g_o, float* ge, uint64_t G, uint64_t k, Ctl* ctl, const ChunkWs& w,
-               Pending pz, int add, int emit, cudaStream_t s);
-void launch_fallback(float* ge, uint64_t G, uint64_t k, Ctl* ctl, const ChunkWs& w, cudaStream_t s);
+// EF pass (+ candidate emission when emit).  opts bit 0: fused sample of the
+// candidate bound (cooperative launch), bit 1: force the fallback.  ctl_next:
+// the worker's other control block, zeroed for the next step (nullable).
+// Returns a cudaError_t.
+int launch_ef(const float* g_o, float* ge, uint64_t G, uint64_t k, Ctl* ctl, const ChunkWs& w,
+              Pending pz, int add, int emit, int opts, Ctl* ctl_next, cudaStream_t s);
 // cooperative launch; returns a cudaError_t value (0 = success)
 // bounds_out (nullable): nchunks+1 entries, bounds_out[c] = first output
 // position whose index is >= c * kChunk (what k_bounds computes from a list)
-int launch_select(uint64_t k, Ctl* ctl, const ChunkWs& w, unsigned* out_idx, float* out_val,
-                  unsigned* bounds_out, cudaStream_t s);
+// ef_out: the array the EF pass wrote g_e to (read only by the fallback).
+int launch_select(uint64_t k, Ctl* ctl, const ChunkWs& w, const float* ef_out, uint64_t G,
+                  unsigned* out_idx, float* out_val, unsigned* bounds_out, cudaStream_t s);
+// out = sum of parts[0..n) in a fixed order (one block), e.g. ||g_e||^2 from
+// the per-chunk partials of the last EF pass.
+void launch_sum_fixed(const double* parts, uint64_t n, double* out, cudaStream_t s);
 void launch_gather(const unsigned* bidx, uint64_t k, const float* ge, float* contrib, Ctl* ctl,
                    double* part, cudaStream_t s);
 void launch_bounds(const unsigned* idx, uint64_t k, uint64_t list_stride, int nlists, uint64_t G,

@@ -26,6 +26,7 @@
 #include "fc_synth.h"
 
 namespace fcb {
+namespace cg = cooperative_groups;
 
 static std::atomic<uint64_t> g_launches{0};
 uint64_t launches() { return g_launches.load(std::memory_order_relaxed); }
@@ -127,25 +128,29 @@ __device__ __forceinline__ bool last_block_done(unsigned* counter) {
 //   above(b) < target <= above(b) + hist[b]
 // where above(b) = sum of bins > b.  Block-uniform result; false if the whole
 // histogram holds fewer than `target` entries.  hist lives in global memory
-// (read through L2: it was filled by other blocks' atomics).
+// (filled by other blocks' atomics): it is first copied to s_stage (nb words
+// of shared memory) with independent L2 loads, then scanned there.
 template <int B>
 __device__ bool block_select_top(const unsigned* hist, int nb, unsigned long long target,
-                                 unsigned& bin, unsigned long long& above) {
+                                 unsigned& bin, unsigned long long& above, unsigned* s_stage) {
   __shared__ unsigned long long s_scan[B / 32 + 1];
   __shared__ unsigned s_bin;
   __shared__ unsigned long long s_above;
   __shared__ int s_found;
+#pragma unroll 16
+  for (int b = threadIdx.x; b < nb; b += B) s_stage[b] = __ldcg(hist + b);
+  __syncthreads();
   const int per = (nb + B - 1) / B;
   const int top = nb - per * (int)threadIdx.x;
   const int bot = top - per < 0 ? 0 : top - per;
   unsigned long long sum = 0;
-  for (int b = top - 1; b >= bot; --b) sum += __ldcg(hist + b);
+  for (int b = top - 1; b >= bot; --b) sum += s_stage[b];
   if (threadIdx.x == 0) s_found = 0;
   const unsigned long long ex = block_excl_scan<B>(sum, s_scan);
   if (top > bot && ex < target && target <= ex + sum) {
     unsigned long long acc = ex;
     for (int b = top - 1; b >= bot; --b) {
-      const unsigned h = __ldcg(hist + b);
+      const unsigned h = s_stage[b];
       if (target <= acc + h) {
         s_bin = (unsigned)b;
         s_above = acc;
@@ -181,46 +186,35 @@ void launch_fill_synth(float* dst, uint64_t G, uint64_t key, int dist, cudaStrea
 }
 
 // ------------------------------------------------------------------ sample ---
-// Strided sample of 32768 error-fed magnitudes -> the candidate bound digit.
-// The bound only decides how many elements the EF pass copies out; exactness
-// never depends on it (a miss triggers the full fallback).
-__global__ void __launch_bounds__(kThreads) k_sample(const float* __restrict__ g_o,
-                                                     const float* __restrict__ ge, uint64_t G,
-                                                     uint64_t k, Ctl* __restrict__ ctl, int add,
-                                                     Pending pz, int force_fb) {
-  __shared__ unsigned s_h[kBins1];
-  for (int b = threadIdx.x; b < kBins1; b += kThreads) s_h[b] = 0;
-  __syncthreads();
-  const uint64_t s = blockIdx.x * (uint64_t)kThreads + threadIdx.x;
-  const uint64_t i = ((2 * s + 1) * G) / (2ull * kSamples);
-  float v = ge[i];
-  if (pz.zmap && pending_has(pz, i)) v = 0.0f;
-  if (add) v = g_o[i] + v;
-  atomicAdd(&s_h[key_of(v) >> kShift1], 1u);
-  __syncthreads();
-  for (int b = threadIdx.x; b < kBins1; b += kThreads)
-    if (s_h[b]) atomicAdd(&ctl->hist_s[b], s_h[b]);
-  if (!last_block_done(&ctl->done_sample)) return;
+// Candidate bound from a strided sample of 32768 error-fed magnitudes (fused
+// into the EF kernel, before it streams): the largest 12-bit key bucket L such
+// that the sample holds at least 1.15*mean + 6*sqrt(mean) + 8 values >= L,
+// mean = k/G * 32768.  The bound only decides how many elements EF copies
+// out; exactness never depends on it (a miss triggers the fallback in k_select).
+__device__ __forceinline__ uint64_t sample_pos(uint64_t s, uint64_t G) {
+  return ((2 * s + 1) * G) / (2ull * kSamples);
+}
+
+template <int B>
+__device__ unsigned sample_bound(const unsigned* hist_s, uint64_t G, uint64_t k, bool force_fb,
+                                 unsigned* s_stage) {
+  if (force_fb) return kBins1 - 1;
   const double mean = (double)k / (double)G * (double)kSamples;
   // 6 sigma of sampling noise plus 15 %: a miss only costs the fallback
   const double target = 1.15 * mean + 6.0 * sqrt(mean) + 8.0;
-  unsigned Ld = 0;
-  if (force_fb) {
-    Ld = kBins1 - 1;
-  } else if (target < (double)kSamples) {
-    unsigned bin;
-    unsigned long long above;
-    if (block_select_top<kThreads>(ctl->hist_s, kBins1, (unsigned long long)target, bin, above))
-      Ld = bin;
-  }
-  if (threadIdx.x == 0) ctl->L_digit = Ld;
+  if (!(target < (double)kSamples)) return 0;
+  unsigned bin;
+  unsigned long long above;
+  return block_select_top<B>(hist_s, kBins1, (unsigned long long)target, bin, above, s_stage) ? bin : 0u;
 }
 
-void launch_sample(const float* g_o, const float* ge, uint64_t G, uint64_t k, Ctl* ctl, int add,
-                   Pending pz, int force_fallback, cudaStream_t s) {
-  k_sample<<<kSampleBlocks, kThreads, 0, s>>>(g_o, ge, G, k, ctl, add, pz, force_fallback);
-  count_launch();
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
+#define EF_MARK(i) \
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctl->tphase_ef[i] = gtimer()
 
 // ---------------------------------------------------------- error feedback ---
 // g_e = g_o + residual, written in place over the residual (12 B/element):
@@ -285,15 +279,22 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// opts bit 0: derive the candidate bound from a fused sample (cooperative
+// launch: one grid barrier between sampling and streaming); bit 1: force the
+// fallback (tests).  ctl_next (nullable): the worker's other control block,
+// zeroed here for the next step.
 template <bool kAdd, bool kEmit, bool kPend>
 __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_o,
                                                     float* __restrict__ ge, uint64_t G, uint64_t k,
                                                     Ctl* __restrict__ ctl, ChunkWs w, Pending pz,
-                                                    int gated) {
-  if (gated && *(volatile unsigned*)&ctl->fallback == 0) return;
+                                                    int opts, Ctl* __restrict__ ctl_next) {
   extern __shared__ __align__(128) unsigned char s_ring[];
+  EF_MARK(0);
+  if (threadIdx.x == 0) w.tblk[2 * blockIdx.x] = gtimer();
   __shared__ double s_red[kThreads / 32];
+  __shared__ unsigned s_hist[kEmit ? kBins1 : 1];  // sample histogram, then the bound's staging
   __shared__ __align__(8) unsigned long long s_bar[kEfWarps][kEfStages];
+  __shared__ unsigned s_chunk[kEfWarps][kEfStages];  // chunk held by each stage
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned sw = lane & 7;  // LDS.128 swizzle
   unsigned char* ring = s_ring + warp * kEfStages * kStageBytes;
@@ -302,18 +303,50 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
     for (int s = 0; s < kEfStages; ++s) mbar_init(&s_bar[warp][s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  const unsigned Lkey = kEmit ? (*(volatile unsigned*)&ctl->L_digit) << kShift1 : 0u;
+  if (ctl_next) {
+    unsigned* z = reinterpret_cast<unsigned*>(ctl_next);
+    for (unsigned q = blockIdx.x * kThreads + tid; q < sizeof(Ctl) / 4; q += gridDim.x * kThreads) z[q] = 0u;
+  }
+  const bool sampling = kEmit && (opts & 1);
+  if (sampling)
+    for (int b = tid; b < kBins1; b += kThreads) s_hist[b] = 0u;
   __syncthreads();
 
+  // the sample's loads go out first, ahead of the stream's first stages
+  auto sample_at = [&](unsigned q) -> float {
+    const uint64_t i = sample_pos(q, G);
+    float v = ge[i];
+    if (kPend && pending_has(pz, i)) v = 0.0f;
+    if (kAdd) v = __fadd_rn(g_o[i], v);
+    return v;
+  };
+  const unsigned q0 = blockIdx.x * kThreads + tid, qstride = gridDim.x * kThreads;
+  float sv = 0.f;
+  if (sampling && q0 < (unsigned)kSamples) sv = sample_at(q0);
+
+  // Chunks are handed out dynamically (one atomic per chunk): SMs do not
+  // stream at equal rates, and a static split leaves a long tail.
   const unsigned nchunks = w.nchunks;
   const unsigned nfull = (unsigned)(G >> kChunkShift);  // chunks fed by TMA
-  const unsigned nw = gridDim.x * kEfWarps;
-  const unsigned cfirst = blockIdx.x * kEfWarps + warp;
   constexpr unsigned kTx = kChunk * 4 * (kAdd ? 2 : 1) + (kPend ? 128 : 0);
-  auto issue = [&](unsigned it) {  // lane 0 only
-    const unsigned c = cfirst + it * nw;
-    if (c >= nfull) return;
+  // lane 0 takes chunks in batches of 4 (one shared counter caps the atomic
+  // rate) until the last ~10 %, then one at a time (short tail)
+  unsigned q_next = 0, q_left = 0;
+  const unsigned big_until = nchunks - nchunks / 10;
+  auto take = [&]() -> unsigned {
+    if (q_left == 0) {
+      const unsigned n = q_next < big_until ? 4u : 1u;
+      q_next = atomicAdd(&ctl->ef_next, n);
+      q_left = n;
+    }
+    --q_left;
+    return q_next++;
+  };
+  auto issue = [&](unsigned it) {  // lane 0 only: take the next chunk into stage it % kEfStages
     const unsigned s = it % kEfStages;
+    const unsigned c = take();
+    s_chunk[warp][s] = c;
+    if (c >= nfull) return;  // past the end, or the partial last chunk (plain loads)
     unsigned long long* bar = &s_bar[warp][s];
     unsigned char* st = ring + s * kStageBytes;
     const uint64_t base = (uint64_t)c << kChunkShift;
@@ -326,10 +359,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
     for (int s = 0; s < kEfStages; ++s) issue(s);
   __syncwarp();
 
-  double nacc = 0.0;
+  // candidate bound: derived while the first stages are in flight, before any
+  // block writes g_e back over the residual
+  unsigned Lkey = 0u;
+  if (kEmit) {
+    if (opts & 1) {
+      if (q0 < (unsigned)kSamples) atomicAdd(&s_hist[key_of(sv) >> kShift1], 1u);
+      for (unsigned q = q0 + qstride; q < (unsigned)kSamples; q += qstride)  // small grids only
+        atomicAdd(&s_hist[key_of(sample_at(q)) >> kShift1], 1u);
+      __syncthreads();
+      for (int b = tid; b < kBins1; b += kThreads)
+        if (s_hist[b]) atomicAdd(&ctl->hist_s[b], s_hist[b]);
+      cg::this_grid().sync();
+      EF_MARK(1);
+      const unsigned Ld = sample_bound<kThreads>(ctl->hist_s, G, k, (opts & 2) != 0, s_hist);
+      EF_MARK(2);
+      if (blockIdx.x == 0 && tid == 0) ctl->L_digit = Ld;
+      Lkey = Ld << kShift1;
+    } else {
+      Lkey = (*(volatile unsigned*)&ctl->L_digit) << kShift1;
+    }
+  }
+
   for (unsigned it = 0;; ++it) {
-    const unsigned c = cfirst + it * nw;
+    const unsigned c = s_chunk[warp][it % kEfStages];
     if (c >= nchunks) break;
+    double nacc = 0.0;
     const uint64_t base = (uint64_t)c << kChunkShift;
     const unsigned s = it % kEfStages;
     float* sge = reinterpret_cast<float*>(ring + s * kStageBytes);
@@ -393,6 +448,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
         nacc += (double)(r * r);
       }
     }
+    {  // this chunk's sum of squares (fixed lane tree: reproducible per chunk)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) nacc += __shfl_xor_sync(0xffffffffu, nacc, o);
+      if (lane == 0) w.cnorm[c] = nacc;
+    }
     if (kEmit) {
       // lane order == index order: one warp scan places every candidate
       const unsigned n = __popc(mask);
@@ -428,96 +488,49 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
   if (lane == 0 && kAdd) bulk_wait0();
 
   if (kEmit && lane == 0 && ncand) atomicAdd(&ctl->cand_count, ncand);
-  const double bsum = block_sum<kThreads>(nacc, s_red);
-  if (tid == 0) w.ef_part[blockIdx.x] = bsum;
-  if (!last_block_done(gated ? &ctl->done_fbe : &ctl->done_ef)) return;
-
-  // ---- last block: ||g_e||^2; a candidate set smaller than k means the
-  // sampled bound missed and the fallback re-emission must run ----
-  if (!gated) {
-    const double tot = block_sum_array<kThreads>(w.ef_part, gridDim.x, s_red);
-    if (tid == 0) ctl->ge_norm2 = tot;
-  }
-  if (kEmit && tid == 0 && (unsigned long long)__ldcg(&ctl->cand_count) < k) ctl->fallback = 1;
+  EF_MARK(3);
+  if (threadIdx.x == 0) w.tblk[2 * blockIdx.x + 1] = gtimer();
+  // ||g_e||^2 is reduced from w.cnorm when asked for (launch_sum_fixed); a
+  // candidate set smaller than k (sampled bound missed) is detected by k_select
 }
 
 template <bool A, bool E, bool P>
-static void launch_ef_t(const float* g_o, float* ge, uint64_t G, uint64_t k, Ctl* ctl,
-                        const ChunkWs& w, Pending pz, int gated, cudaStream_t s) {
+static int launch_ef_t(const float* g_o, float* ge, uint64_t G, uint64_t k, Ctl* ctl,
+                       const ChunkWs& w, Pending pz, int opts, Ctl* ctl_next, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_ef<A, E, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kEfRingBytes);
     attr = true;
   }
-  k_ef<A, E, P><<<w.ef_grid, kThreads, kEfRingBytes, s>>>(g_o, ge, G, k, ctl, w, pz, gated);
+  if (E && (opts & 1)) {  // grid barrier inside: all blocks co-resident (one per SM)
+    ChunkWs ws = w;
+    void* args[] = {&g_o, &ge, &G, &k, &ctl, &ws, &pz, &opts, &ctl_next};
+    return (int)cudaLaunchCooperativeKernel((void*)k_ef<A, E, P>, dim3(w.ef_grid), dim3(kThreads), args,
+                                            kEfRingBytes, s);
+  }
+  k_ef<A, E, P><<<w.ef_grid, kThreads, kEfRingBytes, s>>>(g_o, ge, G, k, ctl, w, pz, opts, ctl_next);
+  return (int)cudaGetLastError();
 }
 
 int ef_grid_size() { return num_sms(); }
 
-static void launch_ef_any(const float* g_o, float* ge, uint64_t G, uint64_t k, Ctl* ctl,
-                          const ChunkWs& w, Pending pz, int add, int emit, int gated,
-                          cudaStream_t s) {
+int launch_ef(const float* g_o, float* ge, uint64_t G, uint64_t k, Ctl* ctl, const ChunkWs& w,
+              Pending pz, int add, int emit, int opts, Ctl* ctl_next, cudaStream_t s) {
   const bool pend = pz.zmap != nullptr;
+  int e;
   if (add && emit && pend)
-    launch_ef_t<true, true, true>(g_o, ge, G, k, ctl, w, pz, gated, s);
+    e = launch_ef_t<true, true, true>(g_o, ge, G, k, ctl, w, pz, opts, ctl_next, s);
   else if (add && emit)
-    launch_ef_t<true, true, false>(g_o, ge, G, k, ctl, w, pz, gated, s);
+    e = launch_ef_t<true, true, false>(g_o, ge, G, k, ctl, w, pz, opts, ctl_next, s);
   else if (add && pend)
-    launch_ef_t<true, false, true>(g_o, ge, G, k, ctl, w, pz, gated, s);
+    e = launch_ef_t<true, false, true>(g_o, ge, G, k, ctl, w, pz, opts, ctl_next, s);
   else if (add)
-    launch_ef_t<true, false, false>(g_o, ge, G, k, ctl, w, pz, gated, s);
+    e = launch_ef_t<true, false, false>(g_o, ge, G, k, ctl, w, pz, opts, ctl_next, s);
   else
-    launch_ef_t<false, true, false>(g_o, ge, G, k, ctl, w, Pending{}, gated, s);
+    e = launch_ef_t<false, true, false>(g_o, ge, G, k, ctl, w, Pending{}, opts, ctl_next, s);
   count_launch();
-}
-
-void launch_ef(const float* g_o, float* ge, uint64_t G, uint64_t k, Ctl* ctl, const ChunkWs& w,
-               Pending pz, int add, int emit, cudaStream_t s) {
-  launch_ef_any(g_o, ge, G, k, ctl, w, pz, add, emit, 0, s);
-}
-
-// ---------------------------------------------------------------- fallback ---
-// Only does work when the sampled bound kept fewer than k elements: full
-// digit-1 histogram of g_e, then an exact re-emission with L = the k-th
-// element's digit (so the candidate set provably contains the whole top-k).
-__global__ void __launch_bounds__(kThreads) k_fb_hist(const float* __restrict__ ge, uint64_t G,
-                                                      uint64_t k, Ctl* __restrict__ ctl) {
-  if (*(volatile unsigned*)&ctl->fallback == 0) return;
-  __shared__ unsigned s_h[kBins1];
-  for (int b = threadIdx.x; b < kBins1; b += kThreads) s_h[b] = 0;
-  __syncthreads();
-  const uint64_t n4 = G / 4;
-  const float4* ge4 = reinterpret_cast<const float4*>(ge);
-  for (uint64_t i = blockIdx.x * (uint64_t)kThreads + threadIdx.x; i < n4;
-       i += (uint64_t)gridDim.x * kThreads) {
-    const float4 x = __ldcs(ge4 + i);
-    atomicAdd(&s_h[key_of(x.x) >> kShift1], 1u);
-    atomicAdd(&s_h[key_of(x.y) >> kShift1], 1u);
-    atomicAdd(&s_h[key_of(x.z) >> kShift1], 1u);
-    atomicAdd(&s_h[key_of(x.w) >> kShift1], 1u);
-  }
-  if (blockIdx.x == 0)
-    for (uint64_t i = n4 * 4 + threadIdx.x; i < G; i += kThreads)
-      atomicAdd(&s_h[key_of(ge[i]) >> kShift1], 1u);
-  __syncthreads();
-  for (int b = threadIdx.x; b < kBins1; b += kThreads)
-    if (s_h[b]) atomicAdd(&ctl->hist_fb[b], s_h[b]);
-  if (!last_block_done(&ctl->done_fbh)) return;
-  unsigned bin;
-  unsigned long long above;
-  block_select_top<kThreads>(ctl->hist_fb, kBins1, k, bin, above);
-  if (threadIdx.x == 0) {
-    ctl->L_digit = bin;
-    ctl->cand_count = 0;
-  }
-  for (int b = threadIdx.x; b < kBins1; b += kThreads) ctl->hist1[b] = 0;
-}
-
-void launch_fallback(float* ge, uint64_t G, uint64_t k, Ctl* ctl, const ChunkWs& w, cudaStream_t s) {
-  k_fb_hist<<<num_sms() * 2, kThreads, 0, s>>>(ge, G, k, ctl);
-  count_launch();
-  launch_ef_any(nullptr, ge, G, k, ctl, w, Pending{}, 0, 1, 1, s);
+  return e;
 }
 
 // ------------------------------------------------------------------ select ---
@@ -536,7 +549,6 @@ void launch_fallback(float* ge, uint64_t G, uint64_t k, Ctl* ctl, const ChunkWs&
 // are walked one chunk per thread; long runs one chunk per warp with
 // coalesced 128-byte accesses, ballot compaction and match-aggregated
 // histogram atomics.  A block's runs are staged in shared memory when they fit.
-namespace cg = cooperative_groups;
 constexpr int kSelThreads = 1024;
 constexpr int kSelWarps = kSelThreads / 32;
 constexpr int kSelBins = 4096;
@@ -569,11 +581,6 @@ __device__ __forceinline__ void flush_hist(unsigned* s_h, unsigned* g_h, int nb)
     if (s_h[b]) atomicAdd(g_h + b, s_h[b]);
 }
 
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 #define SEL_MARK(i) \
   if (blockIdx.x == 0 && threadIdx.x == 0) ctl->tphase[i] = gtimer()
 
@@ -592,7 +599,8 @@ __host__ __device__ inline unsigned sel_cache_cap(unsigned cpb) {
 }
 
 __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __restrict__ ctl,
-                                                           ChunkWs w, unsigned* __restrict__ out_idx,
+                                                           ChunkWs w, const float* __restrict__ ef_out,
+                                                           uint64_t G, unsigned* __restrict__ out_idx,
                                                            float* __restrict__ out_val,
                                                            unsigned* __restrict__ bounds_out) {
   cg::grid_group grid = cg::this_grid();
@@ -614,6 +622,54 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
   unsigned* s_ge = s_off + cpb;
   const unsigned cache_cap = sel_cache_cap(cpb);
   float* s_val = reinterpret_cast<float*>(s_dyn + sel_arrays_bytes(cpb));
+
+  // ---- fallback (the sampled bound kept fewer than k elements): exact
+  // digit-1 histogram of every |g_e|, then this block's chunks re-emitted
+  // with L = the k-th element's digit, so the candidates hold the whole top-k
+  const bool fb = (unsigned long long)__ldcg(&ctl->cand_count) < k;
+  if (fb && blockIdx.x == 0 && tid == 0) ctl->fallback = 1;
+  if (fb) {
+    for (int b = tid; b < kBins1; b += kSelThreads) s_h[b] = 0;
+    __syncthreads();
+    const uint64_t n4 = G / 4;
+    const float4* src4 = reinterpret_cast<const float4*>(ef_out);
+    for (uint64_t i = blockIdx.x * (uint64_t)kSelThreads + tid; i < n4; i += (uint64_t)gridDim.x * kSelThreads) {
+      const float4 x = __ldcg(src4 + i);
+      atomicAdd(&s_h[key_of(x.x) >> kShift1], 1u);
+      atomicAdd(&s_h[key_of(x.y) >> kShift1], 1u);
+      atomicAdd(&s_h[key_of(x.z) >> kShift1], 1u);
+      atomicAdd(&s_h[key_of(x.w) >> kShift1], 1u);
+    }
+    if (blockIdx.x == 0)
+      for (uint64_t i = n4 * 4 + tid; i < G; i += kSelThreads) atomicAdd(&s_h[key_of(ef_out[i]) >> kShift1], 1u);
+    flush_hist(s_h, ctl->hist_fb, kBins1);
+    grid.sync();
+    unsigned bin;
+    unsigned long long above;
+    block_select_top<kSelThreads>(ctl->hist_fb, kBins1, k, bin, above, s_h);
+    if (blockIdx.x == 0 && tid == 0) ctl->L_digit = bin;
+    const unsigned Lk = bin << kShift1;
+    for (unsigned c = c0 + warp; c < c1; c += kSelWarps) {  // warp per chunk, rows of 32
+      const uint64_t base = (uint64_t)c << kChunkShift;
+      unsigned pos = 0;
+      for (int r = 0; r < kChunk / 32; ++r) {
+        const uint64_t i = base + (uint64_t)r * 32 + lane;
+        float x = 0.f;
+        if (i < G) x = __ldcg(ef_out + i);
+        const bool on = i < G && key_of(x) >= Lk;
+        const unsigned bal = __ballot_sync(0xffffffffu, on);
+        if (on) {
+          const unsigned p = pos + __popc(bal & lt);
+          w.cand_idx[base + p] = (unsigned)i;
+          w.cand_val[base + p] = x;
+        }
+        pos += __popc(bal);
+      }
+      if (lane == 0) w.cnt[c] = pos;
+    }
+    __threadfence();
+    __syncthreads();
+  }
 
   // ---- stage: counts, cache offsets, mode ----
   for (unsigned i = tid; i < nc; i += kSelThreads) s_cnt[i] = __ldcg(w.cnt + c0 + i);
@@ -771,7 +827,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
     SEL_MARK(2 + d);
     unsigned bin;
     unsigned long long above;
-    block_select_top<kSelThreads>(ghs[d], nb, need, bin, above);
+    block_select_top<kSelThreads>(ghs[d], nb, need, bin, above, s_h);
     need -= above;
     prefix = (prefix << widths[d]) | bin;
     above_shift = sh;
@@ -968,8 +1024,8 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
 }
 
 // Grid of the cooperative select: one resident 1024-thread block per SM.
-int launch_select(uint64_t k, Ctl* ctl, const ChunkWs& w, unsigned* out_idx, float* out_val,
-                  unsigned* bounds_out, cudaStream_t s) {
+int launch_select(uint64_t k, Ctl* ctl, const ChunkWs& w, const float* ef_out, uint64_t G,
+                  unsigned* out_idx, float* out_val, unsigned* bounds_out, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelSmemMax);
@@ -980,11 +1036,27 @@ int launch_select(uint64_t k, Ctl* ctl, const ChunkWs& w, unsigned* out_idx, flo
   if (cpb > (unsigned)kSelMaxCpb) return (int)cudaErrorInvalidValue;
   const unsigned smem = sel_arrays_bytes(cpb) + sel_cache_cap(cpb) * 4u;
   ChunkWs ws = w;
-  void* args[] = {&k, &ctl, &ws, &out_idx, &out_val, &bounds_out};
+  void* args[] = {&k, &ctl, &ws, &ef_out, &G, &out_idx, &out_val, &bounds_out};
   const cudaError_t e = cudaLaunchCooperativeKernel((void*)k_select, dim3(grid), dim3(kSelThreads),
                                                     args, smem, s);
   count_launch();
   return e == cudaSuccess ? 0 : (int)e;
+}
+
+// Fixed-order sum of per-chunk partials (one block): reproducible regardless
+// of which warp streamed which chunk.
+__global__ void __launch_bounds__(1024) k_sum_fixed(const double* __restrict__ parts, uint64_t n,
+                                                     double* __restrict__ out) {
+  __shared__ double s_red[32];
+  double acc = 0.0;
+  for (uint64_t i = threadIdx.x; i < n; i += 1024) acc += parts[i];
+  const double t = block_sum<1024>(acc, s_red);
+  if (threadIdx.x == 0) *out = t;
+}
+
+void launch_sum_fixed(const double* parts, uint64_t n, double* out, cudaStream_t s) {
+  k_sum_fixed<<<1, 1024, 0, s>>>(parts, n, out);
+  count_launch();
 }
 
 // ------------------------------------------------------------------ gather ---
