@@ -127,9 +127,10 @@ struct fc_ctx {
   double* dnorms = nullptr;
   double* h_norms = nullptr;  // pinned
   bool has_agg = false;
-  // phase events
+  // phase events (recorded only for calls that asked for step statistics)
   cudaEvent_t ev[5] = {};
   bool timing = false;
+  bool phase_stats = false;
   // EF-kernel timing (dominant kernel, for the roofline)
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ef_pending;
   std::vector<cudaEvent_t> ev_pool;
@@ -231,7 +232,7 @@ int copy_out(fc_ctx* c, float* dst, const float* src, uint64_t n, int memkind) {
 }
 
 void record(fc_ctx* c, int i) {
-  if (c->timing) cudaEventRecord(c->ev[i], c->stream);
+  if (c->timing && c->phase_stats) cudaEventRecord(c->ev[i], c->stream);
 }
 
 // Write the owed zeros now (the residual store is about to be observed).
@@ -318,12 +319,24 @@ int drain_ef_events(fc_ctx* c) {
   return FC_OK;
 }
 
+// The EF / select kernels' grid barriers assume one resident block per SM;
+// a timeout there means the result cannot be trusted.
+int check_barriers(fc_ctx* c) {
+  for (auto& w : c->w) {
+    unsigned e = 0;
+    CUDA_TRY(cudaMemcpy(&e, &w.ctl->bar_err, sizeof(e), cudaMemcpyDeviceToHost));
+    if (e) return fail(FC_ERR_RUNTIME, "grid barrier timed out (kernel blocks not co-resident)");
+  }
+  return FC_OK;
+}
+
 int finish_step(fc_ctx* c, fc_step_stats* st, uint64_t k, int sel, int coll, double hbm, double bus,
                 uint64_t launches0) {
   if (!st) {
     if (!(c->flags & FC_FLAG_ASYNC)) {
       CUDA_TRY(cudaStreamSynchronize(c->stream));
       TRY(drain_ef_events(c));
+      return check_barriers(c);
     }
     return FC_OK;
   }
@@ -337,7 +350,7 @@ int finish_step(fc_ctx* c, fc_step_stats* st, uint64_t k, int sel, int coll, dou
   if (c->flags & FC_FLAG_ASYNC) return FC_OK;
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   TRY(drain_ef_events(c));
-  if (c->timing) {
+  if (c->timing && c->phase_stats) {
     float a = 0, b = 0, d = 0, e = 0, t = 0;
     cudaEventElapsedTime(&a, c->ev[0], c->ev[1]);
     cudaEventElapsedTime(&b, c->ev[1], c->ev[2]);
@@ -355,7 +368,7 @@ int finish_step(fc_ctx* c, fc_step_stats* st, uint64_t k, int sel, int coll, dou
     CUDA_TRY(cudaMemcpy(&fb, &c->w[i].ctl->fallback, sizeof(fb), cudaMemcpyDeviceToHost));
     st->fallback |= fb ? 1 : 0;
   }
-  return FC_OK;
+  return check_barriers(c);
 }
 
 }  // namespace
@@ -796,7 +809,7 @@ int fc_sync(fc_ctx* c) {
   CUDA_TRY(cudaStreamSynchronize(c->s_h2d));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->s_d2h));
-  return FC_OK;
+  return check_barriers(c);
 }
 
 int fc_join(fc_ctx* c) {
@@ -944,6 +957,13 @@ int fc_diag_ef_blocks(fc_ctx* c, int worker, uint64_t* out, int n) {
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   const int m = std::min<int>(n, 2 * (int)c->w[worker].ws.ef_grid);
   CUDA_TRY(cudaMemcpy(out, c->w[worker].ws.tblk, m * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  // followed by the last AR decode's start and end marks
+  if (n >= m + 2) {
+    unsigned long long t[8];
+    fcb::read_tdiag(t);
+    out[m] = t[0];
+    out[m + 1] = t[1];
+  }
   return FC_OK;
 }
 
@@ -958,6 +978,7 @@ int fc_topk_exact(fc_ctx* c, int worker, double cr, fc_step_stats* st) {
   // the packs are about to be rewritten: settle any zeros that reference them
   TRY(materialize_all(c));
   const uint64_t l0 = fcb::launches();
+  c->phase_stats = st != nullptr;
   Worker& w = c->w[worker];
   const int force_fb = std::getenv("FC_FORCE_FALLBACK") != nullptr ? 2 : 0;
   record(c, 0);
@@ -993,6 +1014,7 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
   }
   CUDA_TRY(cudaSetDevice(c->device));
   const uint64_t l0 = fcb::launches();
+  c->phase_stats = st != nullptr;
   for (auto& w : c->w) {
     w.has_topk = false;
     w.kept_is_topk = false;
@@ -1134,6 +1156,7 @@ int fc_ag_step(fc_ctx* c, double cr, int compressor, fc_step_stats* st) {
   const int N = c->world;
   CUDA_TRY(cudaSetDevice(c->device));
   const uint64_t l0 = fcb::launches();
+  c->phase_stats = st != nullptr;
 
   record(c, 0);
   for (int i = 0; i < c->n_local; ++i) TRY(run_ef(c, i, k, true));
@@ -1193,6 +1216,7 @@ int fc_dense_step(fc_ctx* c, int algo, int op, fc_step_stats* st) {
   const int N = c->world;
   CUDA_TRY(cudaSetDevice(c->device));
   const uint64_t l0 = fcb::launches();
+  c->phase_stats = st != nullptr;
   record(c, 0);
   record(c, 1);
   record(c, 2);

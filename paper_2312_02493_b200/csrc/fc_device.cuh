@@ -40,6 +40,8 @@ struct Ctl {
   unsigned cand_count;    // M: candidates emitted
   unsigned done_sample, done_ef, done_fbh, done_fbe, done_gather;
   unsigned ef_next;       // EF work queue: next chunk to hand out
+  unsigned bar_ef, bar_sel;  // software grid barriers of the EF / select kernels
+  unsigned bar_err;       // a grid barrier timed out (blocks not co-resident)
   unsigned b1, b2, T;     // radix digits and the final threshold key
   unsigned pad0;
   unsigned long long need1, needT, count_gt;
@@ -85,12 +87,12 @@ __host__ __device__ inline unsigned zmap_bit(uint64_t i) { return 1u << ((unsign
 // Kernel launchers (fc_kernels.cu).  All take the context stream.
 void launch_fill_synth(float* dst, uint64_t G, uint64_t key, int dist, cudaStream_t s);
 // EF pass (+ candidate emission when emit).  opts bit 0: fused sample of the
-// candidate bound (cooperative launch), bit 1: force the fallback.  ctl_next:
+// candidate bound (one grid barrier inside), bit 1: force the fallback.  ctl_next:
 // the worker's other control block, zeroed for the next step (nullable).
 // Returns a cudaError_t.
 int launch_ef(const float* g_o, float* ge, uint64_t G, uint64_t k, Ctl* ctl, const ChunkWs& w,
               Pending pz, int add, int emit, int opts, Ctl* ctl_next, cudaStream_t s);
-// cooperative launch; returns a cudaError_t value (0 = success)
+// Returns a cudaError_t value (0 = success).
 // bounds_out (nullable): nchunks+1 entries, bounds_out[c] = first output
 // position whose index is >= c * kChunk (what k_bounds computes from a list)
 // ef_out: the array the EF pass wrote g_e to (read only by the fallback).
@@ -99,6 +101,8 @@ int launch_select(uint64_t k, Ctl* ctl, const ChunkWs& w, const float* ef_out, u
 // out = sum of parts[0..n) in a fixed order (one block), e.g. ||g_e||^2 from
 // the per-chunk partials of the last EF pass.
 void launch_sum_fixed(const double* parts, uint64_t n, double* out, cudaStream_t s);
+// diagnostics: %globaltimer marks of the last decode (start, end)
+void read_tdiag(unsigned long long* out8);
 void launch_gather(const unsigned* bidx, uint64_t k, const float* ge, float* contrib, Ctl* ctl,
                    double* part, cudaStream_t s);
 void launch_bounds(const unsigned* idx, uint64_t k, uint64_t list_stride, int nlists, uint64_t G,

@@ -29,16 +29,46 @@ namespace fcb {
 namespace cg = cooperative_groups;
 
 static std::atomic<uint64_t> g_launches{0};
+// diagnostics: %globaltimer marks of the last step's kernels
+// [0] decode block-0 start, [1] latest decode block end
+__device__ unsigned long long g_tdiag[8];
 uint64_t launches() { return g_launches.load(std::memory_order_relaxed); }
 static inline void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+// Programmatic dependent launch: the step's kernels are launched with
+// programmatic stream serialization, so a kernel's launch and block
+// scheduling overlap the previous kernel's tail.  Each such kernel waits
+// (griddepcontrol.wait: the previous grid complete, its writes visible)
+// before touching memory, and lets the next one launch once its own blocks
+// are done with their main work (griddepcontrol.launch_dependents).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 static int g_num_sms = 0;
+static void prefer_max_smem();
 static int num_sms() {
   if (!g_num_sms) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_num_sms <= 0) g_num_sms = 148;
+    prefer_max_smem();
   }
   return g_num_sms;
 }
@@ -168,6 +198,36 @@ __device__ bool block_select_top(const unsigned* hist, int nb, unsigned long lon
   return f;
 }
 
+// Grid barrier for the kernels that run exactly one block per SM (grid = SM
+// count, shared memory sized so that no second block fits), launched as plain
+// kernels: a cooperative launch costs ~8 us more per kernel here.  `ctr` is a
+// per-step counter (zeroed with the control block); every barrier raises the
+// target by gridDim.x.  The wait is bounded: if the blocks were not all
+// resident, *err is set and the kernel proceeds (the host reports it).
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned& target, unsigned* err) {
+  __syncthreads();
+  target += gridDim.x;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    unsigned spins = 0;
+    while (ld_acquire(ctr) < target) {
+      __nanosleep(64);
+      if (++spins > (1u << 25)) {  // ~ seconds: not co-resident
+        atomicExch(err, 1u);
+        break;
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 // Is element i owed a zero (bit of the zero map)?
 __device__ __forceinline__ bool pending_has(const Pending& pz, uint64_t i) {
   return (__ldg(pz.zmap + zmap_word(i)) & zmap_bit(i)) != 0u;
@@ -175,13 +235,14 @@ __device__ __forceinline__ bool pending_has(const Pending& pz, uint64_t i) {
 
 // ------------------------------------------------------------- synthetic ---
 __global__ void k_fill_synth(float* __restrict__ dst, uint64_t G, uint64_t key, int dist) {
+  pdl_wait();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < G;
        i += (uint64_t)gridDim.x * blockDim.x)
     dst[i] = fc_synth_value(key, i, dist);
 }
 
 void launch_fill_synth(float* dst, uint64_t G, uint64_t key, int dist, cudaStream_t s) {
-  k_fill_synth<<<num_sms() * 8, kThreads, 0, s>>>(dst, G, key, dist);
+  launch_pdl(k_fill_synth, num_sms() * 8, kThreads, 0, s, dst, G, key, dist);
   count_launch();
 }
 
@@ -279,8 +340,8 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// opts bit 0: derive the candidate bound from a fused sample (cooperative
-// launch: one grid barrier between sampling and streaming); bit 1: force the
+// opts bit 0: derive the candidate bound from a fused sample (one grid
+// barrier between sampling and streaming); bit 1: force the
 // fallback (tests).  ctl_next (nullable): the worker's other control block,
 // zeroed here for the next step.
 template <bool kAdd, bool kEmit, bool kPend>
@@ -288,6 +349,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
                                                     float* __restrict__ ge, uint64_t G, uint64_t k,
                                                     Ctl* __restrict__ ctl, ChunkWs w, Pending pz,
                                                     int opts, Ctl* __restrict__ ctl_next) {
+  pdl_wait();
   extern __shared__ __align__(128) unsigned char s_ring[];
   EF_MARK(0);
   if (threadIdx.x == 0) w.tblk[2 * blockIdx.x] = gtimer();
@@ -370,7 +432,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
       __syncthreads();
       for (int b = tid; b < kBins1; b += kThreads)
         if (s_hist[b]) atomicAdd(&ctl->hist_s[b], s_hist[b]);
-      cg::this_grid().sync();
+      unsigned bar = 0;
+      grid_barrier(&ctl->bar_ef, bar, &ctl->bar_err);
       EF_MARK(1);
       const unsigned Ld = sample_bound<kThreads>(ctl->hist_s, G, k, (opts & 2) != 0, s_hist);
       EF_MARK(2);
@@ -485,6 +548,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
       }
     }
   }
+  pdl_trigger();
   if (lane == 0 && kAdd) bulk_wait0();
 
   if (kEmit && lane == 0 && ncand) atomicAdd(&ctl->cand_count, ncand);
@@ -503,14 +567,8 @@ static int launch_ef_t(const float* g_o, float* ge, uint64_t G, uint64_t k, Ctl*
                          (int)kEfRingBytes);
     attr = true;
   }
-  if (E && (opts & 1)) {  // grid barrier inside: all blocks co-resident (one per SM)
-    ChunkWs ws = w;
-    void* args[] = {&g_o, &ge, &G, &k, &ctl, &ws, &pz, &opts, &ctl_next};
-    return (int)cudaLaunchCooperativeKernel((void*)k_ef<A, E, P>, dim3(w.ef_grid), dim3(kThreads), args,
-                                            kEfRingBytes, s);
-  }
-  k_ef<A, E, P><<<w.ef_grid, kThreads, kEfRingBytes, s>>>(g_o, ge, G, k, ctl, w, pz, opts, ctl_next);
-  return (int)cudaGetLastError();
+  return (int)launch_pdl(k_ef<A, E, P>, w.ef_grid, kThreads, kEfRingBytes, s, g_o, ge, G, k, ctl, w, pz,
+                        opts, ctl_next);
 }
 
 int ef_grid_size() { return num_sms(); }
@@ -534,7 +592,7 @@ int launch_ef(const float* g_o, float* ge, uint64_t G, uint64_t k, Ctl* ctl, con
 }
 
 // ------------------------------------------------------------------ select ---
-// One cooperative kernel (one resident 1024-thread block per SM, grid
+// One kernel (one resident 1024-thread block per SM, software grid
 // barriers between phases) turns the candidate runs into the exact,
 // index-ordered top-k:
 //   digits  three radix digits of the threshold key T (bits 30..19, 18..11,
@@ -603,7 +661,8 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
                                                            uint64_t G, unsigned* __restrict__ out_idx,
                                                            float* __restrict__ out_val,
                                                            unsigned* __restrict__ bounds_out) {
-  cg::grid_group grid = cg::this_grid();
+  pdl_wait();
+  unsigned bar = 0;  // grid barrier target (ctl->bar_sel)
   extern __shared__ __align__(16) unsigned char s_dyn[];
   __shared__ unsigned s_h[kSelBins];
   __shared__ unsigned long long s_scan[kSelWarps + 1];
@@ -643,7 +702,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
     if (blockIdx.x == 0)
       for (uint64_t i = n4 * 4 + tid; i < G; i += kSelThreads) atomicAdd(&s_h[key_of(ef_out[i]) >> kShift1], 1u);
     flush_hist(s_h, ctl->hist_fb, kBins1);
-    grid.sync();
+    grid_barrier(&ctl->bar_sel, bar, &ctl->bar_err);
     unsigned bin;
     unsigned long long above;
     block_select_top<kSelThreads>(ctl->hist_fb, kBins1, k, bin, above, s_h);
@@ -823,7 +882,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
       });
     }
     flush_hist(s_h, ghs[d], nb);
-    grid.sync();
+    grid_barrier(&ctl->bar_sel, bar, &ctl->bar_err);
     SEL_MARK(2 + d);
     unsigned bin;
     unsigned long long above;
@@ -904,7 +963,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
     }
   }
   const unsigned long long blk_total = s_scan[kSelWarps];
-  grid.sync();
+  grid_barrier(&ctl->bar_sel, bar, &ctl->bar_err);
   SEL_MARK(5);
 
   // ---- emit ----
@@ -1015,7 +1074,8 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
   if (tid == 0) w.bnorm[blockIdx.x] = bsum;
   if (bounds_out && blockIdx.x == 0 && tid == 0) bounds_out[nch] = (unsigned)k;
   SEL_MARK(6);
-  grid.sync();
+  grid_barrier(&ctl->bar_sel, bar, &ctl->bar_err);
+  pdl_trigger();
   SEL_MARK(7);
   if (blockIdx.x == 0) {
     const double tot = block_sum_array<kSelThreads>(w.bnorm, gridDim.x, s_dred);
@@ -1023,7 +1083,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
   }
 }
 
-// Grid of the cooperative select: one resident 1024-thread block per SM.
+// Grid of the select: one resident 1024-thread block per SM.
 int launch_select(uint64_t k, Ctl* ctl, const ChunkWs& w, const float* ef_out, uint64_t G,
                   unsigned* out_idx, float* out_val, unsigned* bounds_out, cudaStream_t s) {
   static bool attr = false;
@@ -1037,8 +1097,19 @@ int launch_select(uint64_t k, Ctl* ctl, const ChunkWs& w, const float* ef_out, u
   const unsigned smem = sel_arrays_bytes(cpb) + sel_cache_cap(cpb) * 4u;
   ChunkWs ws = w;
   void* args[] = {&k, &ctl, &ws, &ef_out, &G, &out_idx, &out_val, &bounds_out};
-  const cudaError_t e = cudaLaunchCooperativeKernel((void*)k_select, dim3(grid), dim3(kSelThreads),
-                                                    args, smem, s);
+  // one resident block per SM (1024 threads, ~217 KB shared): plain launch,
+  // software grid barriers (grid_barrier)
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kSelThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelExC(&cfg, (const void*)k_select, args);
   count_launch();
   return e == cudaSuccess ? 0 : (int)e;
 }
@@ -1047,6 +1118,7 @@ int launch_select(uint64_t k, Ctl* ctl, const ChunkWs& w, const float* ef_out, u
 // of which warp streamed which chunk.
 __global__ void __launch_bounds__(1024) k_sum_fixed(const double* __restrict__ parts, uint64_t n,
                                                      double* __restrict__ out) {
+  pdl_wait();
   __shared__ double s_red[32];
   double acc = 0.0;
   for (uint64_t i = threadIdx.x; i < n; i += 1024) acc += parts[i];
@@ -1055,7 +1127,7 @@ __global__ void __launch_bounds__(1024) k_sum_fixed(const double* __restrict__ p
 }
 
 void launch_sum_fixed(const double* parts, uint64_t n, double* out, cudaStream_t s) {
-  k_sum_fixed<<<1, 1024, 0, s>>>(parts, n, out);
+  launch_pdl(k_sum_fixed, 1, 1024, 0, s, parts, n, out);
   count_launch();
 }
 
@@ -1069,6 +1141,7 @@ __global__ void __launch_bounds__(kThreads) k_gather(const unsigned* __restrict_
                                                      float* __restrict__ contrib,
                                                      Ctl* __restrict__ ctl,
                                                      double* __restrict__ part) {
+  pdl_wait();
   __shared__ double s_red[kThreads / 32];
   double acc = 0.0;
   const uint64_t step = (uint64_t)gridDim.x * kThreads;
@@ -1103,7 +1176,7 @@ void launch_gather(const unsigned* bidx, uint64_t k, const float* ge, float* con
   int grid = (int)std::min<uint64_t>((k + kThreads * kGatherUnroll - 1) / (kThreads * kGatherUnroll),
                                      (uint64_t)num_sms() * 8);
   if (grid < 1) grid = 1;
-  k_gather<<<grid, kThreads, 0, s>>>(bidx, k, ge, contrib, ctl, part);
+  launch_pdl(k_gather, grid, kThreads, 0, s, bidx, k, ge, contrib, ctl, part);
   count_launch();
 }
 
@@ -1116,6 +1189,7 @@ void launch_gather(const unsigned* bidx, uint64_t k, const float* ge, float* con
 // the buffer content is identical to a full decode.
 __global__ void k_agg_clear(const unsigned* __restrict__ prev, uint64_t kp, float* __restrict__ agg,
                             unsigned* __restrict__ zmap) {
+  pdl_wait();
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < kp;
        j += (uint64_t)gridDim.x * blockDim.x) {
     const unsigned i = __ldcs(prev + j);
@@ -1128,6 +1202,7 @@ __global__ void k_agg_write(const unsigned* __restrict__ idx, uint64_t k,
                             const float* __restrict__ lists, int nlists, uint64_t list_stride,
                             int divide, float divisor, float* __restrict__ agg,
                             unsigned* __restrict__ zmap, unsigned* __restrict__ keep) {
+  pdl_wait();
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < k;
        j += (uint64_t)gridDim.x * blockDim.x) {
     const unsigned i = __ldcs(idx + j);
@@ -1145,24 +1220,25 @@ void launch_agg_update(const unsigned* prev, uint64_t kp, const unsigned* idx, u
                        float divisor, float* agg, unsigned* zmap, unsigned* keep, cudaStream_t s) {
   if (kp) {
     const unsigned g = (unsigned)std::min<uint64_t>((kp + kThreads - 1) / kThreads, num_sms() * 16ull);
-    k_agg_clear<<<g, kThreads, 0, s>>>(prev, kp, agg, zmap);
+    launch_pdl(k_agg_clear, g, kThreads, 0, s, prev, kp, agg, zmap);
     count_launch();
   }
   const unsigned g = (unsigned)std::min<uint64_t>((k + kThreads - 1) / kThreads, num_sms() * 16ull);
-  k_agg_write<<<g, kThreads, 0, s>>>(idx, k, lists, nlists, list_stride, divide, divisor, agg, zmap,
+  launch_pdl(k_agg_write, g, kThreads, 0, s, idx, k, lists, nlists, list_stride, divide, divisor, agg, zmap,
                                       keep);
   count_launch();
 }
 
 // Materialise owed zeros (before the residual store is read from outside).
 __global__ void k_zero_at(const unsigned* __restrict__ idx, uint64_t k, float* __restrict__ ge) {
+  pdl_wait();
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < k;
        j += (uint64_t)gridDim.x * blockDim.x)
     ge[idx[j]] = 0.0f;
 }
 
 void launch_zero_at(const unsigned* idx, uint64_t k, float* ge, cudaStream_t s) {
-  k_zero_at<<<num_sms() * 8, kThreads, 0, s>>>(idx, k, ge);
+  launch_pdl(k_zero_at, num_sms() * 8, kThreads, 0, s, idx, k, ge);
   count_launch();
 }
 
@@ -1172,6 +1248,7 @@ void launch_zero_at(const unsigned* idx, uint64_t k, float* ge, cudaStream_t s) 
 // list without a search.
 __global__ void k_bounds(const unsigned* __restrict__ idx, uint64_t k, uint64_t list_stride,
                          int nlists, uint64_t nch, unsigned* __restrict__ bounds) {
+  pdl_wait();
   const uint64_t per = k + 1;
   for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < per * nlists;
        q += (uint64_t)gridDim.x * blockDim.x) {
@@ -1190,7 +1267,7 @@ void launch_bounds(const unsigned* idx, uint64_t k, uint64_t list_stride, int nl
   const uint64_t work = (k + 1) * nlists;
   uint64_t grid = (work + kThreads - 1) / kThreads;
   if (grid > (1u << 30)) grid = 1u << 30;
-  k_bounds<<<(unsigned)grid, kThreads, 0, s>>>(idx, k, list_stride, nlists, nch, bounds);
+  launch_pdl(k_bounds, (unsigned)grid, kThreads, 0, s, idx, k, list_stride, nlists, nch, bounds);
   count_launch();
 }
 
@@ -1246,8 +1323,10 @@ __global__ void __launch_bounds__(kThreads) k_decode_ar(const unsigned* __restri
                                                         int divide, float divisor,
                                                         float* __restrict__ agg, uint64_t G,
                                                         unsigned* __restrict__ zmap) {
+  pdl_wait();
   __shared__ __align__(128) float tile[2][kDecTile];
   __shared__ unsigned s_zm[kDecChunks * 32];
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_tdiag[0] = gtimer();
   const uint64_t ntd = (G + kDecTile - 1) >> kDecShift;
   const uint64_t nch = nchunks_of(G);
   int buf = 0, iter = 0;
@@ -1272,13 +1351,17 @@ __global__ void __launch_bounds__(kThreads) k_decode_ar(const unsigned* __restri
     emit_tile(agg, tl, t0, G);
     if (threadIdx.x < (c1 - c0) * 32) zmap[(c0 << 5) + threadIdx.x] = s_zm[threadIdx.x];
   }
-  if (threadIdx.x == 0) bulk_wait_all();
+  pdl_trigger();
+  if (threadIdx.x == 0) {
+    bulk_wait_all();
+    atomicMax(&g_tdiag[1], gtimer());
+  }
 }
 
 void launch_decode_ar(const unsigned* idx, const unsigned* bounds, const float* lists, int nlists,
                       uint64_t list_stride, int divide, float divisor, float* agg, uint64_t G,
                       unsigned* zmap, cudaStream_t s) {
-  k_decode_ar<<<num_sms() * 6, kThreads, 0, s>>>(idx, bounds, lists, nlists, list_stride, divide,
+  launch_pdl(k_decode_ar, num_sms() * 6, kThreads, 0, s, idx, bounds, lists, nlists, list_stride, divide,
                                                   divisor, agg, G, zmap);
   count_launch();
 }
@@ -1296,6 +1379,7 @@ __global__ void __launch_bounds__(kThreads) k_decode_ag(const unsigned* __restri
                                                         float divisor, float* __restrict__ agg,
                                                         uint64_t G, unsigned* __restrict__ zmaps,
                                                         int map_rank0, int nmaps) {
+  pdl_wait();
   __shared__ __align__(128) float tile[2][kDecTile];
   __shared__ unsigned s_touch[kDecTile / 32];  // union of the ranks' indices in the tile
   extern __shared__ unsigned s_zm[];           // nmaps x kDecChunks*32
@@ -1345,6 +1429,7 @@ __global__ void __launch_bounds__(kThreads) k_decode_ag(const unsigned* __restri
       if ((unsigned)wq < nw) zmaps[(uint64_t)m * (nch << 5) + (c0 << 5) + wq] = s_zm[q];
     }
   }
+  pdl_trigger();
   if (threadIdx.x == 0) bulk_wait_all();
 }
 
@@ -1354,7 +1439,7 @@ void launch_decode_ag(const unsigned* packs, uint64_t pack_stride, uint64_t k, i
   const size_t smem = (size_t)nmaps * kDecChunks * 32 * sizeof(unsigned);
   if (smem > 16 * 1024)
     cudaFuncSetAttribute(k_decode_ag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_decode_ag<<<num_sms() * 6, kThreads, smem, s>>>(packs, pack_stride, k, nranks, bounds, divisor,
+  launch_pdl(k_decode_ag, num_sms() * 6, kThreads, smem, s, packs, pack_stride, k, nranks, bounds, divisor,
                                                      agg, G, zmaps, map_rank0, nmaps);
   count_launch();
 }
@@ -1362,6 +1447,7 @@ void launch_decode_ag(const unsigned* packs, uint64_t pack_stride, uint64_t k, i
 // Dense baseline (trainer.hpp:240-244): out = sum_r lists[r] (r ascending), /N.
 __global__ void k_dense_sum(const float* __restrict__ lists, int nlists, uint64_t list_stride,
                             int divide, float divisor, float* __restrict__ out, uint64_t G) {
+  pdl_wait();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < G;
        i += (uint64_t)gridDim.x * blockDim.x) {
     float v = lists[i];
@@ -1373,9 +1459,25 @@ __global__ void k_dense_sum(const float* __restrict__ lists, int nlists, uint64_
 
 void launch_dense_sum(const float* lists, int nlists, uint64_t list_stride, int divide,
                       float divisor, float* out, uint64_t G, cudaStream_t s) {
-  k_dense_sum<<<num_sms() * 8, kThreads, 0, s>>>(lists, nlists, list_stride, divide, divisor, out,
+  launch_pdl(k_dense_sum, num_sms() * 8, kThreads, 0, s, lists, nlists, list_stride, divide, divisor, out,
                                                   G);
   count_launch();
+}
+
+// Every kernel of the step runs with the maximum shared-memory carveout: the
+// EF and select kernels need it, and switching the L1/shared split between
+// consecutive kernels costs an SM drain at each boundary.
+static void prefer_max_smem() {
+  const void* fs[] = {(const void*)k_fill_synth, (const void*)k_gather, (const void*)k_agg_clear,
+                      (const void*)k_agg_write, (const void*)k_zero_at, (const void*)k_bounds,
+                      (const void*)k_decode_ar, (const void*)k_decode_ag, (const void*)k_dense_sum,
+                      (const void*)k_sum_fixed};
+  for (const void* f : fs)
+    cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+}
+
+void read_tdiag(unsigned long long* out8) {
+  cudaMemcpyFromSymbol(out8, g_tdiag, sizeof(unsigned long long) * 8);
 }
 
 }  // namespace fcb
