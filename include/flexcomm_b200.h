@@ -194,10 +194,24 @@ int fc_restore(fc_ctx* ctx);
  * decoded.  selected rank in stats->selected_rank (stats may be NULL). */
 int fc_artopk_step(fc_ctx* ctx, double cr, int mode, int algo, long step, int op,
                    fc_step_stats* stats);
-/* AG-Top-k step.  Replaces flexcomm::ag_step, inc/artopk.hpp:128 (Exact
- * compressor).  Per worker EF + top-k + residual_update; allgather of the
- * (index,value) pairs; rank-ordered scatter-add; every element divided by N. */
+/* AG-Top-k step.  Replaces flexcomm::ag_step, inc/artopk.hpp:128-161.
+ * Per worker EF + compression (run_compressor, artopk.hpp:115-123) +
+ * residual_update; allgather of the (index,value) pairs; rank-ordered
+ * scatter-add; every element divided by N.  compressor:
+ *   FC_EXACT      topk_exact (compress.hpp:57-65)
+ *   FC_LAYERWISE  topk_layerwise (compress.hpp:67-79): exact Top-k_of(c, len)
+ *                 per layer of the map set by fc_set_layer_map (none: exact)
+ *   FC_THRESHOLD  topk_threshold (compress.hpp:81-112): bisection of a
+ *                 magnitude threshold (fc_set_threshold_rounds rounds, 25 by
+ *                 default); the selection size may differ from k and per
+ *                 worker (stats->k = this context's first worker's). */
 int fc_ag_step(fc_ctx* ctx, double cr, int compressor, fc_step_stats* stats);
+/* DenseGrad::layer_map (inc/core.hpp:11-23) of the gradients, for
+ * FC_LAYERWISE: nlayers (offset, length) pairs, sorted and disjoint, length
+ * >= 1 (nlayers = 0 clears it). */
+int fc_set_layer_map(fc_ctx* ctx, const uint64_t* offsets, const uint64_t* lengths, int nlayers);
+/* ag_step's threshold_rounds (inc/artopk.hpp:131; >= 1, at most 64 here). */
+int fc_set_threshold_rounds(fc_ctx* ctx, int rounds);
 /* Dense baseline: allreduce of g_o, inc/trainer.hpp:240-244 */
 int fc_dense_step(fc_ctx* ctx, int algo, int op, fc_step_stats* stats);
 /* Stand-alone exact top-k of a worker's gradient buffer (no error feedback);

@@ -87,8 +87,15 @@ inline int select_star(long step, int n) {
   return r;
 }
 
+struct LayerSpan {  // inc/core.hpp:11-15
+  std::string name;
+  std::size_t offset = 0;
+  std::size_t length = 0;
+};
+
 struct DenseGrad {
   std::vector<double> values;
+  std::vector<LayerSpan> layer_map;  // used by the Layerwise compressor
   std::size_t size() const { return values.size(); }
 };
 
@@ -363,16 +370,27 @@ inline ArtopkResult artopk_step(const Cluster& cluster, const std::vector<DenseG
   return out;
 }
 
-// inc/artopk.hpp:128-161 (Exact compressor on the device).
+// inc/artopk.hpp:128-161, every compressor on the device (Layerwise uses
+// g_o's layer map, like error_feedback's copy of it in the reference).
 inline DenseGrad ag_step(const Cluster& cluster, const std::vector<DenseGrad>& g_o,
                          ResidualStore& /*device-resident*/, CompressionRatio c,
                          CompressorKind compressor = CompressorKind::Exact,
-                         double payload_scale = 1.0, int /*threshold_rounds*/ = 25) {
-  if (compressor != CompressorKind::Exact)
-    throw std::invalid_argument("only the Exact compressor is implemented on B200");
+                         double payload_scale = 1.0, int threshold_rounds = 25) {
   detail::upload(cluster, g_o);
+  if (compressor == CompressorKind::Layerwise) {
+    std::vector<uint64_t> off, len;
+    for (const auto& l : g_o.front().layer_map) {
+      off.push_back(l.offset);
+      len.push_back(l.length);
+    }
+    check(fc_set_layer_map(cluster.ctx->get(), off.data(), len.data(), static_cast<int>(off.size())));
+  }
+  if (compressor == CompressorKind::Threshold) check(fc_set_threshold_rounds(cluster.ctx->get(), threshold_rounds));
+  const int kind = compressor == CompressorKind::Exact ? FC_EXACT
+                   : compressor == CompressorKind::Layerwise ? FC_LAYERWISE
+                                                             : FC_THRESHOLD;
   fc_step_stats st{};
-  check(fc_ag_step(cluster.ctx->get(), c.c, FC_EXACT, &st));
+  check(fc_ag_step(cluster.ctx->get(), c.c, kind, &st));
   if (cluster.n > 1)
     cluster.charge(cost_allgather_dense(
         cluster.net, cluster.msg(2.0 * 4.0 * static_cast<double>(st.k) * payload_scale)));

@@ -58,6 +58,10 @@ class F32:
         lib.orc_ag_step.argtypes, lib.orc_ag_step.restype = [i, u64, P, P, d, P], u64
         lib.orc_dense.argtypes, lib.orc_dense.restype = [i, u64, P, i, P], None
         lib.orc_fill_synth.argtypes, lib.orc_fill_synth.restype = [P, u64, u64, C.c_uint32, u64, i], None
+        lib.orc_topk_kind.argtypes = [P, u64, d, i, i, P, P, i, P, P]
+        lib.orc_topk_kind.restype = u64
+        lib.orc_ag_step_kind.argtypes = [i, u64, P, P, d, i, i, P, P, i, P, P]
+        lib.orc_ag_step_kind.restype = u64
         self.lib = lib
 
     def k_of(self, c, g):
@@ -105,6 +109,36 @@ class F32:
             raise ValueError("oracle rejected arguments")
         return agg
 
+    @staticmethod
+    def _layers(layers):
+        if not layers:
+            return 0, None, None, None
+        off = np.ascontiguousarray([o for o, _ in layers], dtype=np.uint64)
+        ln = np.ascontiguousarray([n for _, n in layers], dtype=np.uint64)
+        return len(layers), off, ln, (off, ln)
+
+    def topk_kind(self, v, c, kind, layers=None, rounds=25):
+        """kind 0 exact, 1 layerwise (layers = [(offset, length)]), 2 threshold."""
+        v = np.ascontiguousarray(v, dtype=np.float32)
+        nl, off, ln, _keep = self._layers(layers)
+        idx = np.empty(v.size, dtype=np.uint32)
+        val = np.empty(v.size, dtype=np.float32)
+        m = self.lib.orc_topk_kind(v.ctypes.data, v.size, c, kind, nl,
+                                   off.ctypes.data if nl else None, ln.ctypes.data if nl else None,
+                                   rounds, idx.ctypes.data, val.ctypes.data)
+        return idx[:m].copy(), val[:m].copy()
+
+    def ag_step_kind(self, g_o, res, c, kind, layers=None, rounds=25):
+        n, g = g_o.shape
+        g_o = np.ascontiguousarray(g_o, dtype=np.float32)
+        nl, off, ln, _keep = self._layers(layers)
+        agg = np.empty(g, dtype=np.float32)
+        counts = np.empty(n, dtype=np.uint64)
+        self.lib.orc_ag_step_kind(n, g, g_o.ctypes.data, res.ctypes.data, c, kind, nl,
+                                  off.ctypes.data if nl else None, ln.ctypes.data if nl else None,
+                                  rounds, agg.ctypes.data, counts.ctypes.data)
+        return agg, counts
+
     def dense(self, g_o, op=1):
         n, g = g_o.shape
         g_o = np.ascontiguousarray(g_o, dtype=np.float32)
@@ -140,6 +174,10 @@ class Ref:
         lib.ref_trigger_gain.argtypes, lib.ref_trigger_gain.restype = [d, P, u64, u64, d], i
         lib.ref_network_changed.argtypes, lib.ref_network_changed.restype = [d, d, d, d, d], i
         lib.ref_params_at.argtypes, lib.ref_params_at.restype = [P, i, L, P, P], i
+        lib.ref_topk_kind.argtypes = [P, u64, d, i, i, P, P, i, P, P]
+        lib.ref_topk_kind.restype = L
+        lib.ref_ag_step_kind.argtypes = [i, u64, P, P, d, i, i, P, P, i, P]
+        lib.ref_ag_step_kind.restype = i
         lib.ref_state_create.argtypes, lib.ref_state_create.restype = [i, u64], P
         lib.ref_state_destroy.argtypes, lib.ref_state_destroy.restype = [P], None
         lib.ref_state_fill_synth.argtypes = [P, i, u64, C.c_uint32, u64, i]
@@ -253,6 +291,44 @@ class Ref:
         if rc:
             raise ValueError(f"reference raised (code {rc})")
         return a.value, b.value
+
+
+def _ref_layers(layers):
+    if not layers:
+        return 0, None, None
+    off = np.ascontiguousarray([o for o, _ in layers], dtype=np.uint64)
+    ln = np.ascontiguousarray([n for _, n in layers], dtype=np.uint64)
+    return len(layers), off, ln
+
+
+def _ref_topk_kind(self, v, c, kind, layers=None, rounds=25):
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    nl, off, ln = _ref_layers(layers)
+    idx = np.empty(max(1, v.size), dtype=np.uint64)
+    val = np.empty(max(1, v.size), dtype=np.float64)
+    m = self.lib.ref_topk_kind(v.ctypes.data, v.size, c, kind, nl,
+                               off.ctypes.data if nl else None, ln.ctypes.data if nl else None,
+                               rounds, idx.ctypes.data, val.ctypes.data)
+    if m < 0:
+        raise ValueError(f"reference raised (code {-m})")
+    return idx[:m].copy(), val[:m].copy()
+
+
+def _ref_ag_step_kind(self, g_o, res, c, kind, layers=None, rounds=25):
+    n, g = g_o.shape
+    g_o = np.ascontiguousarray(g_o, dtype=np.float64)
+    nl, off, ln = _ref_layers(layers)
+    agg = np.empty(g, dtype=np.float64)
+    rc = self.lib.ref_ag_step_kind(n, g, g_o.ctypes.data, res.ctypes.data, c, kind, nl,
+                                   off.ctypes.data if nl else None, ln.ctypes.data if nl else None,
+                                   rounds, agg.ctypes.data)
+    if rc:
+        raise ValueError(f"reference raised (code {rc})")
+    return agg
+
+
+Ref.topk_kind = _ref_topk_kind
+Ref.ag_step_kind = _ref_ag_step_kind
 
 
 class RefState:

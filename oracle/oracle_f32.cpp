@@ -55,6 +55,52 @@ double squared_norm(const float* v, uint64_t n) {
   return s;
 }
 
+// inc/compress.hpp:67-79 topk_layerwise: per layer (offset, length) the exact
+// top-k_of(c, length) of that slice; layers in map order.  No map -> exact.
+void select_layerwise(const float* v, uint64_t g, double c, int nl, const uint64_t* off,
+                      const uint64_t* len, std::vector<uint32_t>& out) {
+  out.clear();
+  if (nl <= 0) {
+    select_topk_indices(v, g, k_of(c, g), out);
+    return;
+  }
+  for (int l = 0; l < nl; ++l) {
+    std::vector<uint32_t> part;
+    select_topk_indices(v + off[l], len[l], k_of(c, len[l]), part);
+    for (uint32_t i : part) out.push_back(static_cast<uint32_t>(i + off[l]));
+  }
+}
+
+// inc/compress.hpp:81-112 topk_threshold: bisect t in [0, max|v|] (doubles)
+// for `rounds` rounds, stopping when exactly k elements have |v| >= t; keep
+// every element with |v| >= t (count may differ from k).
+void select_threshold(const float* v, uint64_t g, double c, int rounds, std::vector<uint32_t>& out) {
+  const uint64_t k = k_of(c, g);
+  double hi = 0.0;
+  for (uint64_t i = 0; i < g; ++i) hi = std::max(hi, static_cast<double>(std::fabs(v[i])));
+  double lo = 0.0, t = 0.0;
+  for (int r = 0; r < rounds; ++r) {
+    t = (lo + hi) / 2.0;
+    uint64_t count = 0;
+    for (uint64_t i = 0; i < g; ++i)
+      if (static_cast<double>(std::fabs(v[i])) >= t) ++count;
+    if (count == k) break;
+    if (count > k) lo = t;
+    else hi = t;
+  }
+  out.clear();
+  for (uint64_t i = 0; i < g; ++i)
+    if (static_cast<double>(std::fabs(v[i])) >= t) out.push_back(static_cast<uint32_t>(i));
+}
+
+// inc/artopk.hpp:115-123 run_compressor (kind 0 exact, 1 layerwise, 2 threshold)
+void compress(int kind, const float* v, uint64_t g, double c, int nl, const uint64_t* off,
+              const uint64_t* len, int rounds, std::vector<uint32_t>& out) {
+  if (kind == 1) select_layerwise(v, g, c, nl, off, len, out);
+  else if (kind == 2) select_threshold(v, g, c, rounds, out);
+  else select_topk_indices(v, g, k_of(c, g), out);
+}
+
 }  // namespace
 
 extern "C" {
@@ -153,6 +199,47 @@ uint64_t orc_ag_step(int n, uint64_t g, const float* g_o, float* res, double c, 
     for (uint64_t j = 0; j < k; ++j) agg_out[idx[r][j]] += val[r][j];
   for (uint64_t i = 0; i < g; ++i) agg_out[i] /= static_cast<float>(n);
   return k;
+}
+
+// Layerwise / threshold Top-k of one vector (no error feedback).  Writes
+// the selection (count returned; idx/val must hold g entries).
+uint64_t orc_topk_kind(const float* v, uint64_t g, double c, int kind, int nl, const uint64_t* off,
+                       const uint64_t* len, int rounds, uint32_t* idx_out, float* val_out) {
+  if (!(c > 0.0 && c <= 1.0) || g == 0) return 0;
+  std::vector<uint32_t> idx;
+  compress(kind, v, g, c, nl, off, len, rounds, idx);
+  for (size_t j = 0; j < idx.size(); ++j) {
+    if (idx_out) idx_out[j] = idx[j];
+    if (val_out) val_out[j] = v[idx[j]];
+  }
+  return idx.size();
+}
+
+// inc/artopk.hpp:128-161 ag_step with any compressor, fp32.  counts_out[r]
+// (may be NULL) gets each worker's selection size.  Returns max count.
+uint64_t orc_ag_step_kind(int n, uint64_t g, const float* g_o, float* res, double c, int kind, int nl,
+                          const uint64_t* off, const uint64_t* len, int rounds, float* agg_out,
+                          uint64_t* counts_out) {
+  if (n < 1 || g == 0 || !(c > 0.0 && c <= 1.0)) return 0;
+  std::vector<std::vector<uint32_t>> idx(n);
+  std::vector<std::vector<float>> val(n);
+  std::vector<float> ge(g);
+  uint64_t maxk = 0;
+  for (int r = 0; r < n; ++r) {
+    for (uint64_t i = 0; i < g; ++i) ge[i] = g_o[r * g + i] + res[r * g + i];
+    compress(kind, ge.data(), g, c, nl, off, len, rounds, idx[r]);
+    val[r].resize(idx[r].size());
+    for (size_t j = 0; j < idx[r].size(); ++j) val[r][j] = ge[idx[r][j]];
+    for (uint64_t i = 0; i < g; ++i) res[r * g + i] = ge[i];
+    for (size_t j = 0; j < idx[r].size(); ++j) res[r * g + idx[r][j]] -= val[r][j];
+    maxk = std::max<uint64_t>(maxk, idx[r].size());
+    if (counts_out) counts_out[r] = idx[r].size();
+  }
+  for (uint64_t i = 0; i < g; ++i) agg_out[i] = 0.0f;
+  for (int r = 0; r < n; ++r)
+    for (size_t j = 0; j < idx[r].size(); ++j) agg_out[idx[r][j]] += val[r][j];
+  for (uint64_t i = 0; i < g; ++i) agg_out[i] /= static_cast<float>(n);
+  return maxk;
 }
 
 // Dense sync, inc/trainer.hpp:240-244 -> allreduce(g_o), collectives.hpp:82-87

@@ -13,6 +13,7 @@
 #include <exception>
 #include <memory>
 #include <stdexcept>
+#include <string>
 #include <vector>
 
 #include "fc_synth.h"
@@ -128,6 +129,51 @@ int ref_ag_step(int n, uint64_t g, const double* g_o, double* res, double c, dou
     for (int r = 0; r < n; ++r) std::memcpy(res + r * g, store.of(r).data(), g * sizeof(double));
     std::memcpy(agg, out.values.data(), g * sizeof(double));
     if (sync_charge) *sync_charge = clk.of(Category::Sync);
+    return 0;
+  } catch (...) {
+    return code_of(std::current_exception());
+  }
+}
+
+// topk_layerwise / topk_threshold (inc/compress.hpp:67-112) on one vector;
+// kind 1 layerwise (nl layers, offsets/lengths), kind 2 threshold.  Writes
+// the selection; returns its size or -code.
+long ref_topk_kind(const double* v, uint64_t g, double c, int kind, int nl, const uint64_t* off,
+                   const uint64_t* len, int rounds, uint64_t* idx_out, double* val_out) {
+  try {
+    DenseGrad d;
+    d.values.assign(v, v + g);
+    for (int l = 0; l < nl; ++l) d.layer_map.push_back({"L" + std::to_string(l), off[l], len[l]});
+    SparseGrad s = kind == 1 ? topk_layerwise(d, CompressionRatio(c))
+                             : topk_threshold(d, CompressionRatio(c), rounds);
+    for (std::size_t j = 0; j < s.indices.size(); ++j) {
+      idx_out[j] = s.indices[j];
+      val_out[j] = s.values[j];
+    }
+    return static_cast<long>(s.indices.size());
+  } catch (...) {
+    return -code_of(std::current_exception());
+  }
+}
+
+// ag_step with a compressor kind (inc/artopk.hpp:128-161); the gradients carry
+// the layer map (error_feedback copies it into g_e).
+int ref_ag_step_kind(int n, uint64_t g, const double* g_o, double* res, double c, int kind, int nl,
+                     const uint64_t* off, const uint64_t* len, int rounds, double* agg) {
+  try {
+    SimClock clk;
+    Cluster cluster(n, NetParams(0.001, 1e9), &clk);
+    std::vector<DenseGrad> grads(static_cast<std::size_t>(n));
+    ResidualStore store(n, g);
+    for (int r = 0; r < n; ++r) {
+      grads[r].values.assign(g_o + r * g, g_o + (r + 1) * g);
+      for (int l = 0; l < nl; ++l) grads[r].layer_map.push_back({"L" + std::to_string(l), off[l], len[l]});
+      store.of(r).assign(res + r * g, res + (r + 1) * g);
+    }
+    auto out = ag_step(cluster, grads, store, CompressionRatio(c), static_cast<CompressorKind>(kind), 1.0,
+                       rounds);
+    for (int r = 0; r < n; ++r) std::memcpy(res + r * g, store.of(r).data(), g * sizeof(double));
+    std::memcpy(agg, out.values.data(), g * sizeof(double));
     return 0;
   } catch (...) {
     return code_of(std::current_exception());

@@ -130,6 +130,8 @@ def _load() -> C.CDLL:
         "fc_restore": ([P], i),
         "fc_artopk_step": ([P, d, i, i, C.c_long, i, C.POINTER(fc_step_stats)], i),
         "fc_ag_step": ([P, d, i, C.POINTER(fc_step_stats)], i),
+        "fc_set_layer_map": ([P, C.POINTER(u64), C.POINTER(u64), i], i),
+        "fc_set_threshold_rounds": ([P, i], i),
         "fc_dense_step": ([P, i, i, C.POINTER(fc_step_stats)], i),
         "fc_topk_exact": ([P, i, d, C.POINTER(fc_step_stats)], i),
         "fc_sync": ([P], i),
@@ -172,7 +174,7 @@ EXPORTS = [
     "fc_set_grad", "fc_grad_ptr", "fc_fill_synthetic", "fc_set_residual", "fc_get_residual",
     "fc_residual_ptr", "fc_reset_residuals", "fc_get_aggregate", "fc_aggregate_ptr",
     "fc_get_topk", "fc_get_worker_stats", "fc_snapshot", "fc_restore", "fc_artopk_step",
-    "fc_ag_step", "fc_dense_step", "fc_topk_exact", "fc_sync", "fc_join", "fc_stream", "fc_ef_kernel_timing",
+    "fc_ag_step", "fc_set_layer_map", "fc_set_threshold_rounds", "fc_dense_step", "fc_topk_exact", "fc_sync", "fc_join", "fc_stream", "fc_ef_kernel_timing",
     "fc_diag_kernel_ms", "fc_diag_select_phases", "fc_diag_collective_ms", "fc_diag_ef_blocks",
     "fc_cost_primitives", "fc_select_collective", "fc_prefer", "fc_crossover_cr",
     "fc_derive_m_from_ag",

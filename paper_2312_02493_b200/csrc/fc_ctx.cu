@@ -124,6 +124,10 @@ struct fc_ctx {
   unsigned* agg_support = nullptr;  // indices of agg's nonzero support (incremental decode)
   uint64_t agg_support_k = 0;
   bool agg_incr = false;            // agg == densify(agg_support) and zmap 0 == its bits
+  // compressors of the AG path (inc/artopk.hpp:113-123)
+  std::vector<uint64_t> layer_off, layer_len;  // layer map (Layerwise), sorted, disjoint
+  int thresh_rounds = 25;                      // Threshold bisection rounds
+  float* scratch = nullptr;                    // G floats, for layer slices not 16-byte aligned
   double* dnorms = nullptr;
   double* h_norms = nullptr;  // pinned
   bool has_agg = false;
@@ -291,16 +295,92 @@ int run_ef(fc_ctx* c, int i, uint64_t k, bool topk) {
 
 // Top-k of worker i into its pack; also writes the chunk bounds of the
 // selection into bounds slot i (so a decode of this list needs no k_bounds).
-int run_select(fc_ctx* c, int i, uint64_t k, const float* ef_out = nullptr) {
+int run_select(fc_ctx* c, int i, uint64_t k, const float* ef_out = nullptr,
+               const fcb::SelectMode& mode = fcb::SelectMode{}) {
   Worker& w = c->w[i];
+  // exact: [idx k | val k]; threshold (count unknown): [idx kmax | val kmax]
+  const uint64_t voff = mode.rounds > 0 ? c->kmax : k;
   const int e = fcb::launch_select(k, w.ctl, w.ws, ef_out ? ef_out : w.ge, c->G, w.pack,
-                                   reinterpret_cast<float*>(w.pack + k),
-                                   c->bounds + (uint64_t)i * (c->nch + 1), c->stream);
+                                   reinterpret_cast<float*>(w.pack + voff),
+                                   c->bounds + (uint64_t)i * (c->nch + 1), mode, c->stream);
   if (e) return fail(FC_ERR_CUDA, std::string("k_select launch: ") +
                                       cudaGetErrorString(static_cast<cudaError_t>(e)));
   LAUNCHED();
   w.has_topk = true;
   w.topk_k = k;
+  return FC_OK;
+}
+
+// Layerwise Top-k (inc/compress.hpp:67-79) of worker i's error-fed gradient
+// into its pack [idx ktot | val ktot]: for every layer an exact
+// Top-k_of(c, length) over the layer's slice (EF kernel with emission on the
+// slice + k_select, layer offset added to the indices), layers in map order.
+int run_layerwise(fc_ctx* c, int i, double cr, uint64_t ktot) {
+  Worker& w = c->w[i];
+  const int force_fb = std::getenv("FC_FORCE_FALLBACK") != nullptr ? 2 : 0;
+  fcb::ChunkWs ws = w.ws;
+  ws.cnorm = w.ws.cnorm + c->nch;  // keep the full pass's per-chunk norms
+  float* vals = reinterpret_cast<float*>(w.pack + ktot);
+  uint64_t acc = 0;
+  for (size_t l = 0; l < c->layer_off.size(); ++l) {
+    const uint64_t off = c->layer_off[l], len = c->layer_len[l], kl = k_of_host(cr, len);
+    float* src = w.ge + off;
+    if (off % 4) {  // the EF kernel's bulk copies need 16-byte aligned rows
+      if (!c->scratch) TRY(c->alloc(&c->scratch, c->G));
+      CUDA_TRY(cudaMemcpyAsync(c->scratch, src, len * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+      src = c->scratch;
+    }
+    fcb::Ctl* next = take_ctl(w);
+    ws.nchunks = (unsigned)fcb::nchunks_of(len);
+    int e = fcb::launch_ef(nullptr, src, len, kl, w.ctl, ws, fcb::Pending{}, 0, 1, 1 | force_fb, next,
+                           c->stream);
+    if (e) return fail(FC_ERR_CUDA, std::string("k_ef launch: ") + cudaGetErrorString(static_cast<cudaError_t>(e)));
+    LAUNCHED();
+    fcb::SelectMode m;
+    m.idx_base = (unsigned)off;
+    e = fcb::launch_select(kl, w.ctl, ws, src, len, w.pack + acc, vals + acc, nullptr, m, c->stream);
+    if (e) return fail(FC_ERR_CUDA, std::string("k_select launch: ") + cudaGetErrorString(static_cast<cudaError_t>(e)));
+    LAUNCHED();
+    acc += kl;
+  }
+  // ||g_c||^2 of the whole selection (gain input) into this step's control block
+  fcb::launch_sumsq_fixed(vals, ktot, &w.ctl->topk_norm2, c->stream);
+  LAUNCHED();
+  w.has_topk = true;
+  w.topk_k = ktot;
+  w.kept_is_topk = true;
+  return FC_OK;
+}
+
+// Threshold compressor (inc/compress.hpp:81-112) of worker i: bisection in
+// k_select over the EF pass's candidates; the selection size is read back.
+int run_threshold(fc_ctx* c, int i, uint64_t k, uint64_t* kout) {
+  Worker& w = c->w[i];
+  fcb::SelectMode m;
+  m.rounds = c->thresh_rounds;
+  m.kcap = c->kmax;
+  TRY(run_select(c, i, k, nullptr, m));
+  unsigned tfail = 0;
+  CUDA_TRY(cudaMemcpyAsync(&tfail, &w.ctl->tfail, sizeof(tfail), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (tfail == 1) {
+    // the final t fell below the candidate bound: every element a candidate
+    fcb::Ctl* next = take_ctl(w);
+    const int e = fcb::launch_ef(nullptr, w.ge, c->G, k, w.ctl, w.ws, fcb::Pending{}, 0, 1, 4, next,
+                                 c->stream);
+    if (e) return fail(FC_ERR_CUDA, std::string("k_ef launch: ") + cudaGetErrorString(static_cast<cudaError_t>(e)));
+    LAUNCHED();
+    TRY(run_select(c, i, k, nullptr, m));
+    CUDA_TRY(cudaMemcpyAsync(&tfail, &w.ctl->tfail, sizeof(tfail), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+  }
+  if (tfail == 2)
+    return fail(FC_ERR_INVALID_ARGUMENT, "threshold selection larger than the context's max_cr capacity");
+  if (tfail) return fail(FC_ERR_RUNTIME, "threshold selection failed");
+  unsigned long long ko = 0;
+  CUDA_TRY(cudaMemcpy(&ko, &w.ctl->kout, sizeof(ko), cudaMemcpyDeviceToHost));
+  *kout = ko;
+  w.kept_is_topk = true;
   return FC_OK;
 }
 
@@ -522,7 +602,7 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
     TRY(c->alloc(&s.cand_idx, (uint64_t)nch << fcb::kChunkShift));
     TRY(c->alloc(&s.cand_val, (uint64_t)nch << fcb::kChunkShift));
     TRY(c->alloc(&s.ef_part, ef_grid));
-    TRY(c->alloc(&s.cnorm, nch));
+    TRY(c->alloc(&s.cnorm, 2 * (uint64_t)nch));  // [full EF pass | layer passes]
     TRY(c->alloc(&s.g_part, 4096));
     TRY(c->alloc(&s.tblk, 2 * (uint64_t)ef_grid));
   }
@@ -1149,45 +1229,102 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
 int fc_ag_step(fc_ctx* c, double cr, int compressor, fc_step_stats* st) {
   if (!c) return fail(FC_ERR_INVALID_ARGUMENT, "null context");
   if (!cr_valid(cr)) return fail(FC_ERR_INVALID_ARGUMENT, "compression ratio must be in (0, 1]");
-  if (compressor != FC_EXACT)
-    return fail(FC_ERR_INVALID_ARGUMENT, "only the Exact compressor is implemented on B200");
+  if (compressor != FC_EXACT && compressor != FC_LAYERWISE && compressor != FC_THRESHOLD)
+    return fail(FC_ERR_INVALID_ARGUMENT, "unknown compressor");
+  // topk_layerwise without a layer map is topk_exact (compress.hpp:68)
+  if (compressor == FC_LAYERWISE && c->layer_off.empty()) compressor = FC_EXACT;
   const uint64_t k = k_of_host(cr, c->G);
-  if (k > c->kmax) return fail(FC_ERR_INVALID_ARGUMENT, "compression ratio above the context's max_cr");
+  uint64_t kk = k;  // per-worker selection size when it is the same on every worker
+  if (compressor == FC_LAYERWISE) {
+    kk = 0;
+    for (uint64_t len : c->layer_len) kk += k_of_host(cr, len);
+  }
+  if (kk > c->kmax) return fail(FC_ERR_INVALID_ARGUMENT, "compression ratio above the context's max_cr");
   const int N = c->world;
   CUDA_TRY(cudaSetDevice(c->device));
   const uint64_t l0 = fcb::launches();
   c->phase_stats = st != nullptr;
 
+  // (1) error feedback + compression per worker (compress.hpp:114-130)
   record(c, 0);
-  for (int i = 0; i < c->n_local; ++i) TRY(run_ef(c, i, k, true));
+  std::vector<uint64_t> kr(N, kk);  // selection size of every rank
+  std::vector<uint64_t> mine(c->n_local, kk);
+  for (int i = 0; i < c->n_local; ++i) TRY(run_ef(c, i, k, compressor != FC_LAYERWISE));
   advance_input(c);
   record(c, 1);
   for (int i = 0; i < c->n_local; ++i) {
-    TRY(run_select(c, i, k));
-    c->w[i].kept_is_topk = true;
+    if (compressor == FC_EXACT) {
+      TRY(run_select(c, i, k));
+      c->w[i].kept_is_topk = true;
+    } else if (compressor == FC_LAYERWISE) {
+      TRY(run_layerwise(c, i, cr, kk));
+    } else {
+      TRY(run_threshold(c, i, k, &mine[i]));
+    }
   }
   record(c, 2);
 
+  // (2) allgather of the (index, value) pairs (collectives.hpp:39-56)
   const unsigned* packs;
-  uint64_t stride;
-  bool local_bounds = true;  // every list's bounds were written by a local select
+  uint64_t stride, voff;  // between ranks' lists; from a list's indices to its values
+  bool local_bounds = compressor == FC_EXACT;  // bounds written by the local selects
+  if (compressor == FC_THRESHOLD) {
+    if (!c->nccl) {
+      for (int r = 0; r < N; ++r) kr[r] = mine[r];
+    } else if (N == 1) {
+      kr[0] = mine[0];
+    } else {
+      // sizes differ per rank: exchange them, then allgather padded lists
+      double* dk = c->dnorms + N;
+      double* dks = c->dnorms + N + 2;
+      const double mk = (double)mine[0];
+      CUDA_TRY(cudaMemcpyAsync(dk, &mk, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+      NCCL_TRY(ncclAllGather(dk, dks, 1, ncclFloat64, c->comm_ring, c->stream));
+      CUDA_TRY(cudaMemcpyAsync(c->h_norms, dks, N * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CUDA_TRY(cudaStreamSynchronize(c->stream));
+      for (int r = 0; r < N; ++r) kr[r] = (uint64_t)c->h_norms[r];
+    }
+    kk = *std::max_element(kr.begin(), kr.end());
+  }
   if (c->nccl && N == 1) {
     packs = c->w[0].pack;  // allgather over one rank: identity
-    stride = 2 * k;
+    stride = 2 * c->kmax;
+    voff = compressor == FC_THRESHOLD ? c->kmax : kk;
   } else if (c->nccl) {
-    NCCL_TRY(ncclAllGather(c->w[0].pack, c->ag_recv, 2 * k, ncclUint32, c->comm_ring, c->stream));
+    Worker& w = c->w[0];
+    if (compressor == FC_THRESHOLD) {
+      // [idx kmax | val kmax] -> [idx kk | val kk] (padding is never read:
+      // the decode only visits each list's first kr[r] entries)
+      CUDA_TRY(cudaMemcpyAsync(w.contrib, w.pack + c->kmax, mine[0] * sizeof(float),
+                               cudaMemcpyDeviceToDevice, c->stream));
+      CUDA_TRY(cudaMemcpyAsync(w.pack + kk, w.contrib, mine[0] * sizeof(float), cudaMemcpyDeviceToDevice,
+                               c->stream));
+    }
+    NCCL_TRY(ncclAllGather(w.pack, c->ag_recv, 2 * kk, ncclUint32, c->comm_ring, c->stream));
     packs = c->ag_recv;
-    stride = 2 * k;
+    stride = 2 * kk;
+    voff = kk;
     local_bounds = false;
   } else {
     packs = c->pack_all;
     stride = 2 * c->kmax;
+    voff = compressor == FC_THRESHOLD ? c->kmax : kk;
   }
   record(c, 3);
-  if (!local_bounds) fcb::launch_bounds(packs, k, stride, N, c->G, c->bounds, c->stream);
+
+  // (3) rank-ordered scatter-add, every element / N (artopk.hpp:151-159)
+  if (!local_bounds) {
+    if (compressor == FC_THRESHOLD) {
+      for (int r = 0; r < N; ++r)
+        fcb::launch_bounds(packs + (uint64_t)r * stride, kr[r], 0, 1, c->G,
+                           c->bounds + (uint64_t)r * (c->nch + 1), c->stream);
+    } else {
+      fcb::launch_bounds(packs, kk, stride, N, c->G, c->bounds, c->stream);
+    }
+  }
   int ob = 0;
   TRY(agg_target(c, &ob));
-  fcb::launch_decode_ag(packs, stride, k, N, c->bounds, (float)N, c->agg_buf[ob], c->G, c->zmaps,
+  fcb::launch_decode_ag(packs, stride, voff, N, c->bounds, (float)N, c->agg_buf[ob], c->G, c->zmaps,
                         c->nccl ? c->rank : 0, c->n_local, c->stream);
   LAUNCHED();
   c->agg_incr = false;  // the aggregate's support is now a union of N lists
@@ -1200,13 +1337,37 @@ int fc_ag_step(fc_ctx* c, double cr, int compressor, fc_step_stats* st) {
     Worker& w = c->w[i];
     w.pz.zmap = c->zmaps + (uint64_t)i * c->nch * 32;
     w.pz_idx = packs + (uint64_t)r * stride;
-    w.pz_k = k;
+    w.pz_k = kr[r];
   }
 
   const double nl = c->n_local;
-  const double hbm = nl * (12.0 * c->G + 8.0 * k) + 4.0 * c->G + 12.0 * N * k;
-  const double bus = N > 1 ? (N - 1) * 8.0 * k : 0.0;
-  return finish_step(c, st, k, -1, 0, hbm, bus, l0);
+  const double hbm = nl * (12.0 * c->G + 8.0 * kk) + 4.0 * c->G + 12.0 * N * kk;
+  const double bus = N > 1 ? (N - 1) * 8.0 * kk : 0.0;
+  return finish_step(c, st, compressor == FC_THRESHOLD ? mine[0] : kk, -1, 0, hbm, bus, l0);
+}
+
+int fc_set_layer_map(fc_ctx* c, const uint64_t* offsets, const uint64_t* lengths, int nlayers) {
+  if (!c) return fail(FC_ERR_INVALID_ARGUMENT, "null context");
+  if (nlayers < 0 || (nlayers > 0 && (!offsets || !lengths)))
+    return fail(FC_ERR_INVALID_ARGUMENT, "bad layer map");
+  std::vector<uint64_t> off(offsets, offsets + nlayers), len(lengths, lengths + nlayers);
+  for (int l = 0; l < nlayers; ++l) {
+    if (len[l] == 0) return fail(FC_ERR_INVALID_ARGUMENT, "layer of length 0 (k_of needs G > 0)");
+    if (off[l] + len[l] > c->G) return fail(FC_ERR_OUT_OF_RANGE, "layer beyond the gradient");
+    if (l > 0 && off[l] < off[l - 1] + len[l - 1])
+      return fail(FC_ERR_INVALID_ARGUMENT, "layers must be sorted and disjoint");
+  }
+  c->layer_off = std::move(off);
+  c->layer_len = std::move(len);
+  return FC_OK;
+}
+
+int fc_set_threshold_rounds(fc_ctx* c, int rounds) {
+  if (!c) return fail(FC_ERR_INVALID_ARGUMENT, "null context");
+  if (rounds < 1) return fail(FC_ERR_INVALID_ARGUMENT, "rounds must be >= 1");  // compress.hpp:84
+  if (rounds > 64) return fail(FC_ERR_INVALID_ARGUMENT, "at most 64 bisection rounds on B200");
+  c->thresh_rounds = rounds;
+  return FC_OK;
 }
 
 int fc_dense_step(fc_ctx* c, int algo, int op, fc_step_stats* st) {

@@ -42,6 +42,10 @@ struct Ctl {
   unsigned ef_next;       // EF work queue: next chunk to hand out
   unsigned bar_ef, bar_sel;  // software grid barriers of the EF / select kernels
   unsigned bar_err;       // a grid barrier timed out (blocks not co-resident)
+  unsigned maxkey;        // threshold compressor: max |g_e| key
+  unsigned tfail;         // threshold: 1 final t below the candidate bound, 2 output > capacity
+  unsigned long long kout;      // threshold: elements selected
+  unsigned long long tcnt[64];  // threshold: per-round counts
   unsigned b1, b2, T;     // radix digits and the final threshold key
   unsigned pad0;
   unsigned long long need1, needT, count_gt;
@@ -87,7 +91,8 @@ __host__ __device__ inline unsigned zmap_bit(uint64_t i) { return 1u << ((unsign
 // Kernel launchers (fc_kernels.cu).  All take the context stream.
 void launch_fill_synth(float* dst, uint64_t G, uint64_t key, int dist, cudaStream_t s);
 // EF pass (+ candidate emission when emit).  opts bit 0: fused sample of the
-// candidate bound (one grid barrier inside), bit 1: force the fallback.  ctl_next:
+// candidate bound (one grid barrier inside), bit 1: force the fallback, bit 2:
+// every element is a candidate (bound 0).  ctl_next:
 // the worker's other control block, zeroed for the next step (nullable).
 // Returns a cudaError_t.
 int launch_ef(const float* g_o, float* ge, uint64_t G, uint64_t k, Ctl* ctl, const ChunkWs& w,
@@ -96,11 +101,22 @@ int launch_ef(const float* g_o, float* ge, uint64_t G, uint64_t k, Ctl* ctl, con
 // bounds_out (nullable): nchunks+1 entries, bounds_out[c] = first output
 // position whose index is >= c * kChunk (what k_bounds computes from a list)
 // ef_out: the array the EF pass wrote g_e to (read only by the fallback).
+// Exact Top-k (SelectMode{} default) or, with rounds > 0, the reference's
+// threshold compressor (inc/compress.hpp:81-112): bisection over the
+// candidates, then every element with |g_e| >= t (count in ctl->kout, at
+// most kcap).  idx_base is added to the emitted indices.
+struct SelectMode {
+  int rounds = 0;
+  uint64_t kcap = 0;
+  unsigned idx_base = 0;
+};
 int launch_select(uint64_t k, Ctl* ctl, const ChunkWs& w, const float* ef_out, uint64_t G,
-                  unsigned* out_idx, float* out_val, unsigned* bounds_out, cudaStream_t s);
+                  unsigned* out_idx, float* out_val, unsigned* bounds_out, const SelectMode& m,
+                  cudaStream_t s);
 // out = sum of parts[0..n) in a fixed order (one block), e.g. ||g_e||^2 from
 // the per-chunk partials of the last EF pass.
 void launch_sum_fixed(const double* parts, uint64_t n, double* out, cudaStream_t s);
+void launch_sumsq_fixed(const float* v, uint64_t n, double* out, cudaStream_t s);
 // diagnostics: %globaltimer marks of the last decode (start, end)
 void read_tdiag(unsigned long long* out8);
 void launch_gather(const unsigned* bidx, uint64_t k, const float* ge, float* contrib, Ctl* ctl,

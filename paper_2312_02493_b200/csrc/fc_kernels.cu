@@ -439,6 +439,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
       EF_MARK(2);
       if (blockIdx.x == 0 && tid == 0) ctl->L_digit = Ld;
       Lkey = Ld << kShift1;
+    } else if (opts & 4) {  // every element is a candidate
+      if (blockIdx.x == 0 && tid == 0) ctl->L_digit = 0;
+      Lkey = 0u;
     } else {
       Lkey = (*(volatile unsigned*)&ctl->L_digit) << kShift1;
     }
@@ -633,6 +636,21 @@ __device__ __forceinline__ unsigned long long block_sum_u64(unsigned long long v
   return t;
 }
 
+template <int B>
+__device__ __forceinline__ unsigned long long block_max_u64(unsigned long long v,
+                                                            unsigned long long* s_red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if (lane == 0) s_red[warp] = v;
+  __syncthreads();
+  unsigned long long t = 0;
+#pragma unroll
+  for (int q = 0; q < B / 32; ++q) t = max(t, s_red[q]);
+  __syncthreads();
+  return t;
+}
+
 __device__ __forceinline__ void flush_hist(unsigned* s_h, unsigned* g_h, int nb) {
   __syncthreads();
   for (int b = threadIdx.x; b < nb; b += blockDim.x)
@@ -660,9 +678,11 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
                                                            ChunkWs w, const float* __restrict__ ef_out,
                                                            uint64_t G, unsigned* __restrict__ out_idx,
                                                            float* __restrict__ out_val,
-                                                           unsigned* __restrict__ bounds_out) {
+                                                           unsigned* __restrict__ bounds_out,
+                                                           SelectMode mode) {
   pdl_wait();
   unsigned bar = 0;  // grid barrier target (ctl->bar_sel)
+  const bool thresh = mode.rounds > 0;
   extern __shared__ __align__(16) unsigned char s_dyn[];
   __shared__ unsigned s_h[kSelBins];
   __shared__ unsigned long long s_scan[kSelWarps + 1];
@@ -685,7 +705,11 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
   // ---- fallback (the sampled bound kept fewer than k elements): exact
   // digit-1 histogram of every |g_e|, then this block's chunks re-emitted
   // with L = the k-th element's digit, so the candidates hold the whole top-k
-  const bool fb = (unsigned long long)__ldcg(&ctl->cand_count) < k;
+  // (threshold mode needs more than k candidates when they are a strict
+  // subset: bisection probes below the bound are then decided without counting)
+  const unsigned long long M = __ldcg(&ctl->cand_count);
+  const bool fb = thresh ? (M <= k && M < G) : M < k;
+  const unsigned long long fb_target = thresh && k < G ? k + 1 : k;
   if (fb && blockIdx.x == 0 && tid == 0) ctl->fallback = 1;
   if (fb) {
     for (int b = tid; b < kBins1; b += kSelThreads) s_h[b] = 0;
@@ -705,7 +729,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
     grid_barrier(&ctl->bar_sel, bar, &ctl->bar_err);
     unsigned bin;
     unsigned long long above;
-    block_select_top<kSelThreads>(ctl->hist_fb, kBins1, k, bin, above, s_h);
+    block_select_top<kSelThreads>(ctl->hist_fb, kBins1, fb_target, bin, above, s_h);
     if (blockIdx.x == 0 && tid == 0) ctl->L_digit = bin;
     const unsigned Lk = bin << kShift1;
     for (unsigned c = c0 + warp; c < c1; c += kSelWarps) {  // warp per chunk, rows of 32
@@ -853,6 +877,61 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
     }
   };
 
+  unsigned T = 0;
+  unsigned long long needT = 0;
+  if (thresh) {
+    // ---- threshold compressor: bisection of t in [0, max|g_e|] (doubles,
+    // inc/compress.hpp:84-101).  A probe t is counted over the candidates
+    // (|x| >= t <=> key(x) >= key(t rounded up to float)); a probe below the
+    // candidate bound has count >= M > k, so it moves lo without counting.
+    const unsigned Lkey = __ldcg(&ctl->L_digit) << kShift1;
+    unsigned long long mk = 0;
+    if (dense)
+      visit_warp([](int, unsigned) {}, [&](float x, bool valid, int, unsigned, unsigned) {
+        if (valid) mk = max(mk, (unsigned long long)key_of(x));
+      });
+    else
+      visit_thread([&](float x) { mk = max(mk, (unsigned long long)key_of(x)); });
+    mk = block_max_u64<kSelThreads>(mk, s_red);
+    if (tid == 0 && mk) atomicMax(&ctl->maxkey, (unsigned)mk);
+    grid_barrier(&ctl->bar_sel, bar, &ctl->bar_err);
+    double hi = (double)__uint_as_float(__ldcg(&ctl->maxkey)), lo = 0.0, t = 0.0;
+    unsigned tk = 0;
+    const int rounds = min(mode.rounds, 64);
+    for (int r = 0; r < rounds; ++r) {
+      t = (lo + hi) / 2.0;
+      tk = key_of(__double2float_ru(t));
+      if (tk < Lkey) {  // count >= M > k
+        lo = t;
+        continue;
+      }
+      unsigned long long cnt = 0;
+      if (dense)
+        visit_warp([](int, unsigned) {}, [&](float x, bool valid, int, unsigned, unsigned) {
+          cnt += __popc(__ballot_sync(0xffffffffu, valid && key_of(x) >= tk)) * (lane == 0);
+        });
+      else
+        visit_thread([&](float x) { cnt += key_of(x) >= tk; });
+      cnt = block_sum_u64<kSelThreads>(cnt, s_red);
+      if (tid == 0 && cnt) atomicAdd(&ctl->tcnt[r], cnt);
+      grid_barrier(&ctl->bar_sel, bar, &ctl->bar_err);
+      const unsigned long long c_r = __ldcg(&ctl->tcnt[r]);
+      if (c_r == k) break;
+      if (c_r > k) lo = t;
+      else hi = t;
+    }
+    // every element with |x| >= t: key > T, plus all of key == T
+    T = key_of(__double2float_ru(t));
+    needT = ~0ull >> 2;
+    if (T < Lkey) {  // not all selected elements are candidates (host retries)
+      if (blockIdx.x == 0 && tid == 0) ctl->tfail = 1;
+      return;
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+      ctl->T = T;
+      ctl->needT = 0;
+    }
+  } else {
   // ---- digits of T ----
   unsigned long long need = k;
   unsigned prefix = 0;  // key bits above the digit being resolved
@@ -892,13 +971,14 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
     above_shift = sh;
     if (d == 0 && blockIdx.x == 0 && tid == 0) ctl->b1 = bin;
   }
-  const unsigned T = prefix;
-  const unsigned long long needT = need;
+  T = prefix;
+  needT = need;
   if (blockIdx.x == 0 && tid == 0) {
     ctl->T = T;
     ctl->needT = needT;
     ctl->count_gt = k - needT;
   }
+  }  // exact mode
 
   // ---- count: per-chunk (gt, eq), block-level chunk prefixes, block total ----
   if (dense) {
@@ -963,8 +1043,17 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
     }
   }
   const unsigned long long blk_total = s_scan[kSelWarps];
+  if (thresh && tid == 0) {  // threshold: every candidate > T or == T is kept
+    const unsigned long long bk = (blk_total >> 31) + (blk_total & 0x7fffffffull);
+    if (bk) atomicAdd(&ctl->kout, bk);
+  }
   grid_barrier(&ctl->bar_sel, bar, &ctl->bar_err);
   SEL_MARK(5);
+  const unsigned long long kout = thresh ? __ldcg(&ctl->kout) : k;
+  if (thresh && kout > mode.kcap) {  // output does not fit: report, emit nothing
+    if (blockIdx.x == 0 && tid == 0) ctl->tfail = 2;
+    return;
+  }
 
   // ---- emit ----
   unsigned long long bp = 0;
@@ -992,7 +1081,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
           const unsigned sb = __ballot_sync(0xffffffffu, sel);
           if (sel) {
             const unsigned long long pos = o[u] + __popc(sb & lt);
-            out_idx[pos] = __ldcg(gidx + ((uint64_t)c << kChunkShift) + r + lane);
+            out_idx[pos] = __ldcg(gidx + ((uint64_t)c << kChunkShift) + r + lane) + mode.idx_base;
             out_val[pos] = x;
             acc = fma((double)x, (double)x, acc);
           }
@@ -1050,10 +1139,10 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
             }
             if (sel) {
               if (staged) {
-                s_oidx[o - obase] = comp(id[u], e);
+                s_oidx[o - obase] = comp(id[u], e) + mode.idx_base;
                 s_oval[o - obase] = xv;
               } else {
-                out_idx[o] = comp(id[u], e);
+                out_idx[o] = comp(id[u], e) + mode.idx_base;
                 out_val[o] = xv;
               }
               ++o;
@@ -1072,7 +1161,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
   }
   const double bsum = block_sum<kSelThreads>(acc, s_dred);
   if (tid == 0) w.bnorm[blockIdx.x] = bsum;
-  if (bounds_out && blockIdx.x == 0 && tid == 0) bounds_out[nch] = (unsigned)k;
+  if (bounds_out && blockIdx.x == 0 && tid == 0) bounds_out[nch] = (unsigned)kout;
   SEL_MARK(6);
   grid_barrier(&ctl->bar_sel, bar, &ctl->bar_err);
   pdl_trigger();
@@ -1085,7 +1174,8 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
 
 // Grid of the select: one resident 1024-thread block per SM.
 int launch_select(uint64_t k, Ctl* ctl, const ChunkWs& w, const float* ef_out, uint64_t G,
-                  unsigned* out_idx, float* out_val, unsigned* bounds_out, cudaStream_t s) {
+                  unsigned* out_idx, float* out_val, unsigned* bounds_out, const SelectMode& m,
+                  cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelSmemMax);
@@ -1096,7 +1186,8 @@ int launch_select(uint64_t k, Ctl* ctl, const ChunkWs& w, const float* ef_out, u
   if (cpb > (unsigned)kSelMaxCpb) return (int)cudaErrorInvalidValue;
   const unsigned smem = sel_arrays_bytes(cpb) + sel_cache_cap(cpb) * 4u;
   ChunkWs ws = w;
-  void* args[] = {&k, &ctl, &ws, &ef_out, &G, &out_idx, &out_val, &bounds_out};
+  SelectMode mode = m;
+  void* args[] = {&k, &ctl, &ws, &ef_out, &G, &out_idx, &out_val, &bounds_out, &mode};
   // one resident block per SM (1024 threads, ~217 KB shared): plain launch,
   // software grid barriers (grid_barrier)
   cudaLaunchConfig_t cfg{};
@@ -1124,6 +1215,22 @@ __global__ void __launch_bounds__(1024) k_sum_fixed(const double* __restrict__ p
   for (uint64_t i = threadIdx.x; i < n; i += 1024) acc += parts[i];
   const double t = block_sum<1024>(acc, s_red);
   if (threadIdx.x == 0) *out = t;
+}
+
+// out = sum of v[i]^2 (fp64) in a fixed order (one block).
+__global__ void __launch_bounds__(1024) k_sumsq_fixed(const float* __restrict__ v, uint64_t n,
+                                                       double* __restrict__ out) {
+  pdl_wait();
+  __shared__ double s_red[32];
+  double acc = 0.0;
+  for (uint64_t i = threadIdx.x; i < n; i += 1024) acc = fma((double)v[i], (double)v[i], acc);
+  const double t = block_sum<1024>(acc, s_red);
+  if (threadIdx.x == 0) *out = t;
+}
+
+void launch_sumsq_fixed(const float* v, uint64_t n, double* out, cudaStream_t s) {
+  launch_pdl(k_sumsq_fixed, 1, 1024, 0, s, v, n, out);
+  count_launch();
 }
 
 void launch_sum_fixed(const double* parts, uint64_t n, double* out, cudaStream_t s) {

@@ -40,6 +40,7 @@ STAR, VAR = _abi.FC_STAR, _abi.FC_VAR
 RING, TREE = _abi.FC_RING, _abi.FC_TREE
 SUM, AVG = _abi.FC_SUM, _abi.FC_AVG
 DIST_NORMAL, DIST_TIES, DIST_LAYERED = _abi.FC_DIST_NORMAL, _abi.FC_DIST_TIES, _abi.FC_DIST_LAYERED
+EXACT, LAYERWISE, THRESHOLD = _abi.FC_EXACT, _abi.FC_LAYERWISE, _abi.FC_THRESHOLD  # inc/artopk.hpp:113
 
 InvalidArgument = _abi.InvalidArgument
 OutOfRange = _abi.OutOfRange
@@ -305,6 +306,18 @@ class Cluster:
                              C.byref(st) if st is not None else None))
         return StepStats.of(st) if st is not None else None
 
+    def set_layer_map(self, layers) -> None:
+        """DenseGrad::layer_map (inc/core.hpp:11-23) as [(offset, length), ...]
+        for the Layerwise compressor; [] clears it."""
+        n = len(layers)
+        off = (C.c_uint64 * max(1, n))(*[o for o, _ in layers])
+        ln = (C.c_uint64 * max(1, n))(*[m for _, m in layers])
+        check(lib.fc_set_layer_map(self._ctx, off, ln, n))
+
+    def set_threshold_rounds(self, rounds: int) -> None:
+        """ag_step's threshold_rounds (inc/artopk.hpp:131)."""
+        check(lib.fc_set_threshold_rounds(self._ctx, int(rounds)))
+
     def dense_step(self, algo: int = RING, op: int = AVG, stats: bool = True) -> StepStats | None:
         """Dense allreduce baseline, inc/trainer.hpp:240-244."""
         st = _abi.fc_step_stats() if stats else None
@@ -416,5 +429,5 @@ __all__ = [
     "WorkerStats", "k_of", "select_star", "check_cr", "get_unique_id", "NetParams",
     "MessageSpec", "cost_primitives", "select_collective", "prefer", "crossover_cr",
     "derive_m_from_ag", "InvalidArgument", "OutOfRange", "RuntimeFailure", "NoDevice",
-    "DIST_NORMAL", "DIST_TIES", "DIST_LAYERED",
+    "DIST_NORMAL", "DIST_TIES", "DIST_LAYERED", "EXACT", "LAYERWISE", "THRESHOLD",
 ]

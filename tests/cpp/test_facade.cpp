@@ -389,4 +389,31 @@ TEST(Controller, HookSelectsOnFirstStepAndOnNetworkChange) {
   EXPECT_EQ(trainer.metrics().size(), 8u);
 }
 
+// tests/test_compress.cpp:73-78 through ag_step at N=1 (the aggregate is the selection)
+TEST(TopkLayerwise, AppliesRatioPerLayer) {
+  auto ctx = make_ctx(1, 8);
+  SimClock clk;
+  auto cluster = make_cluster(1, &clk, ctx);
+  ResidualStore residuals(ctx);
+  std::vector<DenseGrad> g(1);
+  g[0].values = {5.0, 0.1, 0.2, 0.3, 0.01, 9.0, 0.02, 0.03};
+  g[0].layer_map = {{"L0", 0, 4}, {"L1", 4, 4}};
+  auto agg = ag_step(cluster, g, residuals, CompressionRatio(0.25), CompressorKind::Layerwise);
+  EXPECT_TRUE(agg.values == (std::vector<double>{5.0, 0, 0, 0, 0, 9.0, 0, 0}));
+}
+
+// tests/test_compress.cpp:93-98 through ag_step at N=1
+TEST(TopkThreshold, FullRatioKeepsEverything) {
+  std::mt19937_64 rng(3);
+  auto ctx = make_ctx(1, 97);
+  SimClock clk;
+  auto cluster = make_cluster(1, &clk, ctx);
+  ResidualStore residuals(ctx);
+  auto g = random_grads(rng, 1, 97);
+  auto agg = ag_step(cluster, g, residuals, CompressionRatio(1.0), CompressorKind::Threshold, 1.0, 25);
+  EXPECT_TRUE(agg.values == g[0].values);
+  EXPECT_THROW(ag_step(cluster, g, residuals, CompressionRatio(1.0), CompressorKind::Threshold, 1.0, 0),
+               std::invalid_argument);
+}
+
 int main() { return mt::run_all(); }

@@ -37,15 +37,24 @@ def main() -> int:
     f32 = oracle.F32() if env.rank == 0 else None
     plan = [("star", fc.RING, 0.01), ("star", fc.TREE, 0.05), ("var", fc.RING, 0.01),
             ("var", fc.TREE, 0.002), ("ag", fc.RING, 0.01), ("ag", fc.RING, 0.1),
-            ("star", fc.RING, 0.001), ("dense", fc.TREE, 1.0)]
+            ("star", fc.RING, 0.001), ("dense", fc.TREE, 1.0),
+            # AG with the layerwise / threshold compressors (threshold sizes
+            # differ per rank: padded allgather)
+            ("ag-lw", fc.RING, 0.05), ("ag-thr", fc.RING, 0.01), ("ag-thr", fc.RING, 0.1)]
+    layers = [(0, 3), (3, 1000), (1005, G // 2 - 1005), (G // 2, G - G // 2)]
     failures = []
     with fc.Cluster.nccl(env.world, env.rank, uid, G, device=env.local_rank, max_cr=0.2) as cl:
+        cl.set_layer_map(layers)
         res = np.zeros((env.world, G), np.float32) if env.rank == 0 else None
         for s, (kind, algo, c) in enumerate(plan):
             cl.fill_synthetic(0, 1234, env.rank, s)
             sel = -1
             if kind == "ag":
                 cl.ag_step(c)
+            elif kind == "ag-lw":
+                cl.ag_step(c, fc.LAYERWISE)
+            elif kind == "ag-thr":
+                cl.ag_step(c, fc.THRESHOLD)
             elif kind == "dense":
                 cl.dense_step(algo, fc.AVG)
             else:
@@ -61,6 +70,10 @@ def main() -> int:
             g_o = np.stack([f32.synth(G, 1234, r, s) for r in range(env.world)])
             if kind == "ag":
                 ref = f32.ag_step(g_o, res, c)
+                exact = True
+            elif kind in ("ag-lw", "ag-thr"):
+                ref, _ = f32.ag_step_kind(g_o, res, c, 1 if kind == "ag-lw" else 2,
+                                          layers if kind == "ag-lw" else None, 25)
                 exact = True
             elif kind == "dense":
                 ref = f32.dense(g_o, 1)

@@ -212,3 +212,71 @@ def test_costmodel_errors(fc):
         fc.MessageSpec(2.0, 0.1, 2)
     with pytest.raises(fc.InvalidArgument):
         fc.crossover_cr(fc.NetParams(0.001, 1e9), 1e6, 1, 0)
+
+
+# ---- layerwise / threshold compressors ----------------------------
+
+def _random_layers(rng, g):
+    cuts = sorted(set(int(x) for x in rng.integers(1, g, int(rng.integers(0, 6))))) if g > 2 else []
+    b = [0] + cuts + [g]
+    return [(a, e - a) for a, e in zip(b, b[1:]) if e > a]
+
+
+def test_oracle_compressors_vs_live_reference(ref, f32):
+    """topk_layerwise / topk_threshold (inc/compress.hpp:67-112): the fp32
+    restatement selects exactly what the reference selects."""
+    rng = np.random.default_rng(21)
+    for _ in range(400):
+        g = int(rng.integers(1, 600))
+        c = float(rng.uniform(0.005, 1.0))
+        kind = int(rng.integers(1, 3))
+        dist = rng.integers(0, 3)
+        v = rng.standard_normal(g).astype(np.float32)
+        if dist == 1:
+            v = np.round(v * 4) / 4  # ties
+        elif dist == 2:
+            v = v * np.float32(10.0) ** rng.integers(-3, 3, g).astype(np.float32)
+        layers = _random_layers(rng, g) if kind == 1 else None
+        rounds = int(rng.integers(1, 40))
+        i1, v1 = f32.topk_kind(v, c, kind, layers, rounds)
+        i2, v2 = ref.topk_kind(v.astype(np.float64), c, kind, layers, rounds)
+        np.testing.assert_array_equal(i1.astype(np.uint64), i2)
+        np.testing.assert_array_equal(v1.astype(np.float64), v2)
+
+
+def test_oracle_ag_step_kinds_vs_live_reference(ref, f32):
+    """ag_step with Layerwise / Threshold (inc/artopk.hpp:128-161) on dyadic
+    inputs (sums exact in fp32 and fp64): aggregates and residuals equal."""
+    rng = np.random.default_rng(22)
+    for _ in range(60):
+        n = int(rng.choice([1, 2, 4]))  # /N exact in both precisions
+        g = int(rng.integers(4, 300))
+        kind = int(rng.integers(1, 3))
+        layers = _random_layers(rng, g) if kind == 1 else None
+        rounds = int(rng.integers(1, 30))
+        res32 = np.zeros((n, g), np.float32)
+        res64 = np.zeros((n, g), np.float64)
+        for s in range(3):
+            c = float(rng.choice([0.05, 0.1, 0.25, 0.5]))
+            g_o = (rng.integers(-64, 65, (n, g)) / 16.0).astype(np.float32)
+            a32, _ = f32.ag_step_kind(g_o, res32, c, kind, layers, rounds)
+            a64 = ref.ag_step_kind(g_o.astype(np.float64), res64, c, kind, layers, rounds)
+            np.testing.assert_array_equal(a32.astype(np.float64), a64)
+            np.testing.assert_array_equal(res32.astype(np.float64), res64)
+
+
+def test_oracle_compressor_reference_cases(f32):
+    # tests/test_compress.cpp:73-78
+    v = np.array([5.0, 0.1, 0.2, 0.3, 0.01, 9.0, 0.02, 0.03], np.float32)
+    idx, val = f32.topk_kind(v, 0.25, 1, [(0, 4), (4, 4)])
+    assert list(idx) == [0, 5] and list(val) == [5.0, 9.0]
+    # tests/test_compress.cpp:80-91: distinct magnitudes -> threshold == exact
+    rng = np.random.default_rng(11)
+    for _ in range(50):
+        g = int(rng.integers(2, 400))
+        v = rng.standard_normal(g).astype(np.float32)
+        c = float(rng.uniform(0.01, 1.0))
+        np.testing.assert_array_equal(f32.topk_kind(v, c, 2)[0], f32.topk_exact(v, c)[0])
+    # tests/test_compress.cpp:93-98
+    v = rng.standard_normal(97).astype(np.float32)
+    assert f32.topk_kind(v, 1.0, 2)[0].size == 97
