@@ -45,10 +45,31 @@ CONFIGS = {
     "C3": dict(mode="star", grad_len=138_000_000, cr=0.01),  # VGG-16-sized (headline)
     "C3-ag": dict(mode="ag", grad_len=138_000_000, cr=0.01),
     "C3-tree": dict(mode="star", grad_len=138_000_000, cr=0.01, algo="tree"),
+    "C3-lw": dict(mode="ag", grad_len=138_000_000, cr=0.01, compressor="layerwise"),
+    "C3-thr": dict(mode="ag", grad_len=138_000_000, cr=0.01, compressor="threshold"),
     "C4": dict(mode="star", grad_len=355_000_000, cr=0.001),  # GPT-2-medium-sized
     "C5": dict(mode="star", grad_len=1_000_000_000, cr=0.001),  # 1B
 }
 ALGOS = {"ring": 0, "tree": 1}
+COMPRESSORS = {"exact": 0, "layerwise": 1, "threshold": 2}
+
+
+def vgg16_layers(G):
+    """VGG-16's parameter layout (13 conv + 3 FC layers, weight then bias),
+    the last layer trimmed or padded so the map covers G elements."""
+    convs = [(3, 64), (64, 64), (64, 128), (128, 128), (128, 256), (256, 256), (256, 256),
+             (256, 512), (512, 512), (512, 512), (512, 512), (512, 512), (512, 512)]
+    sizes = []
+    for cin, cout in convs:
+        sizes += [cin * cout * 9, cout]
+    for fin, fout in [(25088, 4096), (4096, 4096), (4096, 1000)]:
+        sizes += [fin * fout, fout]
+    sizes[-2] += G - sum(sizes)
+    layers, off = [], 0
+    for n in sizes:
+        layers.append((off, n))
+        off += n
+    return layers
 SEED = 42
 
 
@@ -62,6 +83,8 @@ def parse():
     p.add_argument("--algo", choices=list(ALGOS), default="ring")
     p.add_argument("--grad-len", type=int, default=138_000_000)
     p.add_argument("--cr", type=float, default=0.01)
+    p.add_argument("--compressor", choices=list(COMPRESSORS), default="exact",
+                   help="AG-path compressor (inc/artopk.hpp:113); layerwise uses VGG-16's layer map")
     p.add_argument("--config", choices=list(CONFIGS), default=None,
                    help="BASELINE.json configuration preset (overrides mode/grad-len/cr)")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -86,7 +109,9 @@ def workload_name(a, world):
     mode = {"star": "STAR AR-Topk", "var": "VAR AR-Topk", "ag": "AG-Topk",
             "dense": "Dense allreduce"}[a.mode]
     algo = "" if a.mode in ("ag", "dense") and a.mode != "dense" else f" ({a.algo})"
-    return f"{mode}{algo}, {a.grad_len / 1e6:g}M fp32 gradient per GPU, CR {a.cr:g}, {world} worker(s)"
+    comp = "" if getattr(a, "compressor", "exact") == "exact" else f" [{a.compressor} compressor]"
+    return (f"{mode}{algo}{comp}, {a.grad_len / 1e6:g}M fp32 gradient per GPU, CR {a.cr:g}, "
+            f"{world} worker(s)")
 
 
 # ------------------------------------------------------------------ clocks ---
@@ -276,14 +301,20 @@ def main():
             os.dup2(saved_fd, 1)
             os.close(saved_fd)
 
-    cl = make_cluster(_abi.FC_FLAG_ASYNC)
+    def make_ready(flags):
+        c_ = make_cluster(flags)
+        if a.compressor == "layerwise":
+            c_.set_layer_map(vgg16_layers(a.grad_len))
+        return c_
+
+    cl = make_ready(_abi.FC_FLAG_ASYNC)
     G = a.grad_len
     mode = MODES[a.mode]
     algo = ALGOS[a.algo]
 
     def step(s):
         if mode == 2:
-            cl.ag_step(a.cr, stats=False)
+            cl.ag_step(a.cr, COMPRESSORS[a.compressor], stats=False)
         elif mode == 3:
             cl.dense_step(algo, fc.AVG, stats=False)
         else:
@@ -348,7 +379,7 @@ def main():
         import ctypes as C
 
         if mode == 2:
-            rc = fc.lib.fc_ag_step(cl._ctx, a.cr, 0, C.byref(stt))
+            rc = fc.lib.fc_ag_step(cl._ctx, a.cr, COMPRESSORS[a.compressor], C.byref(stt))
         elif mode == 3:
             rc = fc.lib.fc_dense_step(cl._ctx, algo, fc.AVG, C.byref(stt))
         else:
@@ -374,7 +405,7 @@ def main():
         host_g.copy_(_tensor_from_ptr(cl.grad_ptr(0), G, local))  # setup only
         torch.cuda.synchronize()
         cl.close()
-        cl = make_cluster(_abi.FC_FLAG_ASYNC | _abi.FC_FLAG_PIPELINE)
+        cl = make_ready(_abi.FC_FLAG_ASYNC | _abi.FC_FLAG_PIPELINE)
         stream = torch.cuda.ExternalStream(cl.stream_ptr(), device=local)
         e2e_steps = max(3, a.steps)
         for s in range(2):
@@ -416,7 +447,7 @@ def main():
 
     # ---- CPU baseline (rank 0, N=1 only): the reference itself -------------
     cpu = None
-    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+    if rank == 0 and world == 1 and not a.no_cpu_baseline and a.compressor == "exact":
         try:
             ms_cpu, sample, _ = run_reference_cpu(a.mode if a.mode != "dense" else "star", a.algo,
                                                   G, a.cr, 1, 2, a.cpu_budget_s)
@@ -434,6 +465,7 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": workload_name(a, world), "grad_len": G, "cr": a.cr, "k": k,
                        "mode": a.mode, "algo": a.algo, "workers": world, "parallelism": f"dp{world}",
+                       "compressor": a.compressor,
                        "l2": "inputs (2 x %.0f MB) larger than the 126 MB L2" % (4 * G / 1e6)},
             "hbm_gbs_step": round(step_gbs, 1),
             "bus_gbs": round(bus / (ms * 1e-3) / 1e9, 2) if bus else 0.0,
