@@ -287,6 +287,13 @@ int fc_network_changed(double alpha0, double bandwidth0, double alpha1, double b
 int fc_moo_metrics(fc_ctx* ctx, int ag, const fc_step_stats* stats, double* gain,
                    double* t_comp_s);
 
+/* NCCL contexts with 1 < world <= 8: 1 if every rank's exchange buffer is
+ * mapped into every other (CUDA IPC over NVLink) and STAR steps exchange
+ * through peer memory (broadcast + allreduce fused into a fetch-gather and
+ * the decode; rank-ordered sums, bit-exact with the reference), 0 if they use
+ * NCCL collectives (FC_NO_P2P=1 in the environment forces that). */
+int fc_peer_exchange(fc_ctx* ctx, int* enabled);
+
 /* Synchronize the context's streams (for FC_FLAG_ASYNC / FC_HOST_ASYNC users). */
 int fc_sync(fc_ctx* ctx);
 /* Order the compute stream after every queued FC_HOST_ASYNC copy (so an event

@@ -157,6 +157,7 @@ def _load() -> C.CDLL:
         "fc_choose_cr": ([C.POINTER(fc_candidate), i, d, d, d, i, C.POINTER(i), C.POINTER(i)], i),
         "fc_network_changed": ([d, d, d, d, d, C.POINTER(i)], i),
         "fc_moo_metrics": ([P, i, C.POINTER(fc_step_stats), C.POINTER(d), C.POINTER(d)], i),
+        "fc_peer_exchange": ([P, C.POINTER(i)], i),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(lib, name)
@@ -179,7 +180,7 @@ EXPORTS = [
     "fc_cost_primitives", "fc_select_collective", "fc_prefer", "fc_crossover_cr",
     "fc_derive_m_from_ag",
     "fc_controller_config_validate", "fc_round_3sig", "fc_candidate_ladder", "fc_trigger_gain",
-    "fc_pareto_front", "fc_choose_cr", "fc_network_changed", "fc_moo_metrics",
+    "fc_pareto_front", "fc_choose_cr", "fc_network_changed", "fc_moo_metrics", "fc_peer_exchange",
 ]
 
 

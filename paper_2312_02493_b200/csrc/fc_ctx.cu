@@ -78,6 +78,8 @@ struct Worker {
   float* contrib = nullptr;  // capacity kmax
   bool has_topk = false;
   uint64_t topk_k = 0;
+  const unsigned* topk_idx = nullptr;  // where the last select wrote its output
+  const float* topk_val = nullptr;
   bool kept_is_topk = false;  // gather skipped: kept energy == ||top-k||^2
   fcb::Pending pz{};          // zeros owed to `ge` (zero map, read by the next EF)
   const unsigned* pz_idx = nullptr;  // the same zeros as a sorted index list
@@ -130,6 +132,15 @@ struct fc_ctx {
   float* scratch = nullptr;                    // G floats, for layer slices not 16-byte aligned
   double* dnorms = nullptr;
   double* h_norms = nullptr;  // pinned
+  int* dsel = nullptr;        // VAR winner chosen on the device (NCCL)
+  // peer-memory exchange (NCCL contexts, 1 < world <= 8, every rank's
+  // exchange buffer mapped into every other with CUDA IPC over NVLink)
+  bool p2p = false;
+  fcb::PeerBufs pb{};
+  void* xbuf = nullptr;
+  std::vector<void*> peer_maps;
+  unsigned long long epoch = 0;
+  bool sel_on_device = false; // the last step's selected rank is in *dsel
   bool has_agg = false;
   // phase events (recorded only for calls that asked for step statistics)
   cudaEvent_t ev[5] = {};
@@ -296,12 +307,18 @@ int run_ef(fc_ctx* c, int i, uint64_t k, bool topk) {
 // Top-k of worker i into its pack; also writes the chunk bounds of the
 // selection into bounds slot i (so a decode of this list needs no k_bounds).
 int run_select(fc_ctx* c, int i, uint64_t k, const float* ef_out = nullptr,
-               const fcb::SelectMode& mode = fcb::SelectMode{}) {
+               const fcb::SelectMode& mode = fcb::SelectMode{}, unsigned* out_idx = nullptr,
+               float* out_val = nullptr) {
   Worker& w = c->w[i];
   // exact: [idx k | val k]; threshold (count unknown): [idx kmax | val kmax]
   const uint64_t voff = mode.rounds > 0 ? c->kmax : k;
-  const int e = fcb::launch_select(k, w.ctl, w.ws, ef_out ? ef_out : w.ge, c->G, w.pack,
-                                   reinterpret_cast<float*>(w.pack + voff),
+  if (!out_idx) {
+    out_idx = w.pack;
+    out_val = reinterpret_cast<float*>(w.pack + voff);
+  }
+  w.topk_idx = out_idx;
+  w.topk_val = out_val;
+  const int e = fcb::launch_select(k, w.ctl, w.ws, ef_out ? ef_out : w.ge, c->G, out_idx, out_val,
                                    c->bounds + (uint64_t)i * (c->nch + 1), mode, c->stream);
   if (e) return fail(FC_ERR_CUDA, std::string("k_select launch: ") +
                                       cudaGetErrorString(static_cast<cudaError_t>(e)));
@@ -422,6 +439,10 @@ int finish_step(fc_ctx* c, fc_step_stats* st, uint64_t k, int sel, int coll, dou
   }
   std::memset(st, 0, sizeof(*st));
   st->selected_rank = sel;
+  if (sel < 0 && c->sel_on_device && !(c->flags & FC_FLAG_ASYNC)) {
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    CUDA_TRY(cudaMemcpy(&st->selected_rank, c->dsel, sizeof(int), cudaMemcpyDeviceToHost));
+  }
   st->collective = coll;
   st->k = k;
   st->hbm_bytes = hbm;
@@ -576,6 +597,7 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
     TRY(c->alloc(&c->ag_recv, (uint64_t)c->world * 2 * c->kmax));
     // [0, W): VAR scores; [W, W+2): this rank's MOO metrics; [W+2, 3W+2): gathered
     TRY(c->alloc(&c->dnorms, 3 * (uint64_t)c->world + 2));
+    TRY(c->alloc(&c->dsel, 1));
   }
   CUDA_TRY(cudaMallocHost(&c->h_norms, 2 * sizeof(double) * std::max(c->world, c->n_local)));
   CUDA_TRY(cudaMemsetAsync(c->ge_all, 0, N * GS * sizeof(float), c->stream));
@@ -629,11 +651,74 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
   return FC_OK;
 }
 
+// Map every rank's exchange buffer into every other rank (CUDA IPC handles
+// allgathered over NCCL); used only if every rank succeeds.  FC_NO_P2P=1
+// keeps the NCCL collectives.
+int setup_p2p(fc_ctx* c) {
+  const int N = c->world;
+  if (!c->nccl || N < 2 || N > fcb::kMaxPeers || std::getenv("FC_NO_P2P")) return FC_OK;
+  const uint64_t list_b = align_up(2 * c->kmax * sizeof(unsigned), 256);
+  const uint64_t contrib_b = align_up(2 * c->kmax * sizeof(float), 256);
+  const uint64_t total = list_b + contrib_b + 256;
+  CUDA_TRY(cudaMalloc(&c->xbuf, total));
+  CUDA_TRY(cudaMemset(c->xbuf, 0, total));
+  int ok = 1;
+  cudaIpcMemHandle_t mine{};
+  if (cudaIpcGetMemHandle(&mine, c->xbuf) != cudaSuccess) ok = 0;
+  cudaGetLastError();
+  unsigned char* dh = nullptr;
+  int* dok = nullptr;
+  CUDA_TRY(cudaMalloc(&dh, (N + 1) * sizeof(cudaIpcMemHandle_t)));
+  CUDA_TRY(cudaMalloc(&dok, sizeof(int)));
+  CUDA_TRY(cudaMemcpy(dh + N * sizeof(cudaIpcMemHandle_t), &mine, sizeof(mine), cudaMemcpyHostToDevice));
+  NCCL_TRY(ncclAllGather(dh + N * sizeof(cudaIpcMemHandle_t), dh, sizeof(cudaIpcMemHandle_t), ncclUint8,
+                         c->comm_ring, c->stream));
+  std::vector<cudaIpcMemHandle_t> hs(N);
+  CUDA_TRY(cudaMemcpyAsync(hs.data(), dh, N * sizeof(cudaIpcMemHandle_t), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  std::vector<unsigned char*> base(N, nullptr);
+  base[c->rank] = static_cast<unsigned char*>(c->xbuf);
+  for (int r = 0; r < N && ok; ++r) {
+    if (r == c->rank) continue;
+    void* p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, hs[r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      ok = 0;
+      break;
+    }
+    c->peer_maps.push_back(p);
+    base[r] = static_cast<unsigned char*>(p);
+  }
+  // every rank must take the same path
+  CUDA_TRY(cudaMemcpy(dok, &ok, sizeof(int), cudaMemcpyHostToDevice));
+  NCCL_TRY(ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, c->comm_ring, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  cudaFree(dh);
+  cudaFree(dok);
+  if (!ok) {
+    for (void* p : c->peer_maps) cudaIpcCloseMemHandle(p);
+    c->peer_maps.clear();
+    return FC_OK;
+  }
+  c->pb.n = N;
+  c->pb.rank = c->rank;
+  c->pb.kmax = c->kmax;
+  for (int r = 0; r < N; ++r) {
+    c->pb.list[r] = reinterpret_cast<unsigned*>(base[r]);
+    c->pb.contrib[r] = reinterpret_cast<float*>(base[r] + list_b);
+    c->pb.flags[r] = reinterpret_cast<unsigned long long*>(base[r] + list_b + contrib_b);
+  }
+  c->p2p = true;
+  return FC_OK;
+}
+
 int fc_create(fc_ctx** out, const fc_opts* opts) {
   if (!out || !opts) return fail(FC_ERR_INVALID_ARGUMENT, "null argument");
   *out = nullptr;
   fc_ctx* c = new fc_ctx();
-  const int s = create_impl(c, opts);
+  int s = create_impl(c, opts);
+  if (s == FC_OK) s = setup_p2p(c);
   if (s != FC_OK) {
     std::string msg = g_err;
     fc_destroy(c);
@@ -650,6 +735,8 @@ int fc_destroy(fc_ctx* c) {
   if (c->s_h2d) cudaStreamSynchronize(c->s_h2d);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->s_d2h) cudaStreamSynchronize(c->s_d2h);
+  for (void* p : c->peer_maps) cudaIpcCloseMemHandle(p);
+  if (c->xbuf) cudaFree(c->xbuf);
   if (c->comm_tree) ncclCommDestroy(c->comm_tree);
   if (c->comm_ring) ncclCommDestroy(c->comm_ring);
   for (void* p : c->allocs) cudaFree(p);
@@ -793,8 +880,10 @@ int fc_get_topk(fc_ctx* c, int worker, uint32_t* idx, float* val, uint64_t* k_ou
   if (k_out) *k_out = w.topk_k;
   CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
-  if (idx) CUDA_TRY(cudaMemcpy(idx, w.pack, w.topk_k * sizeof(uint32_t), cudaMemcpyDeviceToHost));
-  if (val) CUDA_TRY(cudaMemcpy(val, w.pack + w.topk_k, w.topk_k * sizeof(float), cudaMemcpyDeviceToHost));
+  const unsigned* ti = w.topk_idx ? w.topk_idx : w.pack;
+  const float* tv = w.topk_val ? w.topk_val : reinterpret_cast<const float*>(w.pack + w.topk_k);
+  if (idx) CUDA_TRY(cudaMemcpy(idx, ti, w.topk_k * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  if (val) CUDA_TRY(cudaMemcpy(val, tv, w.topk_k * sizeof(float), cudaMemcpyDeviceToHost));
   return FC_OK;
 }
 
@@ -841,6 +930,12 @@ int fc_restore(fc_ctx* c) {
     CUDA_TRY(cudaMemcpyAsync(w.ge, w.snap, c->G * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
   }
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return FC_OK;
+}
+
+int fc_peer_exchange(fc_ctx* c, int* enabled) {
+  if (!c || !enabled) return fail(FC_ERR_INVALID_ARGUMENT, "null argument");
+  *enabled = c->p2p ? 1 : 0;
   return FC_OK;
 }
 
@@ -1099,6 +1194,13 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
     w.has_topk = false;
     w.kept_is_topk = false;
   }
+  // STAR over peer memory: the selected rank's select publishes its list and
+  // values in its exchange buffer (parity of this step's epoch), the other
+  // ranks fetch the list and gather, and every rank's decode sums the
+  // contributions in rank order straight from peer memory
+  const bool p2p_star = c->p2p && mode == FC_STAR && N > 1;
+  const unsigned long long epoch = p2p_star ? ++c->epoch : 0;
+  const int par = (int)(epoch & 1);
 
   // (1) error feedback on every worker; Top-k where its result is consumed
   record(c, 0);
@@ -1110,24 +1212,29 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
   record(c, 1);
   for (int i = 0; i < c->n_local; ++i) {
     const bool topk = mode == FC_VAR || (c->rank + i) == sel;
-    if (topk) TRY(run_select(c, i, k));
+    if (!topk) continue;
+    if (p2p_star) {
+      fcb::SelectMode m;
+      m.publish = c->pb.flags[c->rank];
+      m.epoch = epoch;
+      m.err = &c->w[i].ctl->bar_err;
+      TRY(run_select(c, i, k, nullptr, m, c->pb.list[c->rank] + par * c->kmax,
+                     c->pb.contrib[c->rank] + par * c->kmax));
+    } else {
+      TRY(run_select(c, i, k));
+    }
   }
   record(c, 2);
 
   // (2) VAR: allgather of N ||top-k||^2, argmax, ties -> lowest rank
   //     (select_var, inc/artopk.hpp:35-48)
   if (mode == FC_VAR && N == 1) sel = 0;  // argmax over one worker
-  if (mode == FC_VAR && N > 1) {
-    if (c->nccl) {
-      NCCL_TRY(ncclAllGather(&c->w[0].ctl->topk_norm2, c->dnorms, 1, ncclFloat64, c->comm_ring,
-                             c->stream));
-      CUDA_TRY(cudaMemcpyAsync(c->h_norms, c->dnorms, sizeof(double) * N, cudaMemcpyDeviceToHost,
-                               c->stream));
-    } else {
-      for (int i = 0; i < N; ++i)
-        CUDA_TRY(cudaMemcpyAsync(c->h_norms + i, &c->w[i].ctl->topk_norm2, sizeof(double),
-                                 cudaMemcpyDeviceToHost, c->stream));
-    }
+  const bool var_device = mode == FC_VAR && N > 1 && c->nccl;  // winner found on the device
+  c->sel_on_device = var_device;
+  if (mode == FC_VAR && N > 1 && !c->nccl) {
+    for (int i = 0; i < N; ++i)
+      CUDA_TRY(cudaMemcpyAsync(c->h_norms + i, &c->w[i].ctl->topk_norm2, sizeof(double),
+                               cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     sel = 0;
     for (int r = 1; r < N; ++r)
@@ -1139,13 +1246,40 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
   const unsigned* bsrc = nullptr;
   const float* contrib0 = nullptr;
   const unsigned* own_bounds = nullptr;  // chunk bounds of bsrc, when a local select wrote them
-  if (c->nccl && N == 1) {
+  if (p2p_star) {
+    Worker& w = c->w[0];
+    if (c->rank != sel)
+      fcb::launch_fetch_gather(c->pb, sel, par, epoch, w.ge, k, c->bounds, c->nch, w.ctl, w.ws.g_part,
+                               c->stream);
+    else
+      w.kept_is_topk = true;
+    LAUNCHED();
+    bsrc = c->pb.list[c->rank] + par * c->kmax;  // local copy of the selected list
+    own_bounds = c->bounds;
+  } else if (c->nccl && N == 1) {
     // a single rank: broadcast and allreduce are identities
     Worker& w = c->w[0];
     bsrc = w.pack;
     contrib0 = reinterpret_cast<const float*>(w.pack + k);
     w.kept_is_topk = true;
     own_bounds = c->bounds;
+  } else if (var_device) {
+    // VAR: allgather of the N scores, winner on the device, its list
+    // broadcast as a sum-allreduce of (winner ? list : 0); every rank
+    // gathers g_e at the list (the winner's gather returns its own values)
+    Worker& w = c->w[0];
+    NCCL_TRY(ncclAllGather(&w.ctl->topk_norm2, c->dnorms, 1, ncclFloat64, c->comm_ring, c->stream));
+    unsigned* masked = reinterpret_cast<unsigned*>(w.contrib);
+    fcb::launch_var_mask(c->dnorms, N, c->rank, w.pack, k, masked, c->dsel, c->stream);
+    LAUNCHED();
+    NCCL_TRY(ncclAllReduce(masked, c->bidx, k, ncclUint32, ncclSum, c->comm_ring, c->stream));
+    bsrc = c->bidx;
+    fcb::launch_gather(bsrc, k, w.ge, w.contrib, w.ctl, w.ws.g_part, c->bounds, c->nch, c->stream);
+    LAUNCHED();
+    contrib0 = w.contrib;
+    own_bounds = c->bounds;
+    NCCL_TRY(ncclAllReduce(contrib0, c->reduced, k, ncclFloat32, ncclSum,
+                           algo == FC_TREE ? c->comm_tree : c->comm_ring, c->stream));
   } else if (c->nccl) {
     Worker& w = c->w[0];
     NCCL_TRY(ncclBroadcast(w.pack, c->bidx, k, ncclUint32, sel, c->comm_ring, c->stream));
@@ -1156,9 +1290,11 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
       w.kept_is_topk = true;
       own_bounds = c->bounds;
     } else {
-      fcb::launch_gather(bsrc, k, w.ge, w.contrib, w.ctl, w.ws.g_part, c->stream);
+      // the gather also writes the decode's chunk bounds of the broadcast list
+      fcb::launch_gather(bsrc, k, w.ge, w.contrib, w.ctl, w.ws.g_part, c->bounds, c->nch, c->stream);
       LAUNCHED();
       contrib0 = w.contrib;
+      own_bounds = c->bounds;
     }
     NCCL_TRY(ncclAllReduce(contrib0, c->reduced, k, ncclFloat32, ncclSum,
                            algo == FC_TREE ? c->comm_tree : c->comm_ring, c->stream));
@@ -1176,7 +1312,7 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
                                    c->stream));
         continue;
       }
-      fcb::launch_gather(bsrc, k, w.ge, w.contrib, w.ctl, w.ws.g_part, c->stream);
+      fcb::launch_gather(bsrc, k, w.ge, w.contrib, w.ctl, w.ws.g_part, nullptr, 0, c->stream);
       LAUNCHED();
     }
   }
@@ -1187,11 +1323,14 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
   const int nlists = c->nccl ? 1 : N;
   const uint64_t lstride = c->nccl ? 0 : c->kmax;
   // in-place update costs ~2k random sector RMWs: worth it below ~G/128
-  const bool incr_ok = !(c->flags & FC_FLAG_DENSE_DECODE) && c->nbuf == 1 && k * 128 <= c->G;
+  const bool incr_ok = !(c->flags & FC_FLAG_DENSE_DECODE) && c->nbuf == 1 && !p2p_star && k * 128 <= c->G;
   int ob = 0;
   TRY(agg_target(c, &ob));
   float* aggw = c->agg_buf[ob];
-  if (incr_ok && c->agg_incr) {
+  if (p2p_star) {
+    fcb::launch_decode_ar_peers(c->pb, par, epoch, bsrc, own_bounds, op == FC_AVG, (float)N, aggw, c->G,
+                                c->zmaps, &c->w[0].ctl->bar_err, c->stream);
+  } else if (incr_ok && c->agg_incr) {
     // in place: zero the previous support, write this one (same dense content)
     fcb::launch_agg_update(c->agg_support, c->agg_support_k, bsrc, k, lists, nlists, lstride,
                            op == FC_AVG, (float)N, aggw, c->zmaps, c->agg_support, c->stream);

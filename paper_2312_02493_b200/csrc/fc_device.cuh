@@ -98,6 +98,18 @@ void launch_fill_synth(float* dst, uint64_t G, uint64_t key, int dist, cudaStrea
 int launch_ef(const float* g_o, float* ge, uint64_t G, uint64_t k, Ctl* ctl, const ChunkWs& w,
               Pending pz, int add, int emit, int opts, Ctl* ctl_next, cudaStream_t s);
 // Returns a cudaError_t value (0 = success).
+// ---- peer-memory exchange over NVLink (one process per GPU) ----------------
+// Every rank owns an exchange buffer: two parities (alternate steps) of an
+// index list and a contribution list (kmax entries each) and two epoch flags
+// (list ready, contribution ready), mapped into every peer with CUDA IPC.
+constexpr int kMaxPeers = 8;
+struct PeerBufs {
+  unsigned* list[kMaxPeers];
+  float* contrib[kMaxPeers];
+  unsigned long long* flags[kMaxPeers];  // [0] list epoch, [1] contribution epoch
+  int n = 0, rank = 0;
+  uint64_t kmax = 0;
+};
 // bounds_out (nullable): nchunks+1 entries, bounds_out[c] = first output
 // position whose index is >= c * kChunk (what k_bounds computes from a list)
 // ef_out: the array the EF pass wrote g_e to (read only by the fallback).
@@ -109,6 +121,11 @@ struct SelectMode {
   int rounds = 0;
   uint64_t kcap = 0;
   unsigned idx_base = 0;
+  // peer exchange: after the selection, publish it (flags[0] = flags[1] =
+  // epoch, system-scope release) for the peers that read it over NVLink
+  unsigned long long* publish = nullptr;
+  unsigned long long epoch = 0;
+  unsigned* err = nullptr;  // (wait timeouts)
 };
 int launch_select(uint64_t k, Ctl* ctl, const ChunkWs& w, const float* ef_out, uint64_t G,
                   unsigned* out_idx, float* out_val, unsigned* bounds_out, const SelectMode& m,
@@ -119,8 +136,24 @@ void launch_sum_fixed(const double* parts, uint64_t n, double* out, cudaStream_t
 void launch_sumsq_fixed(const float* v, uint64_t n, double* out, cudaStream_t s);
 // diagnostics: %globaltimer marks of the last decode (start, end)
 void read_tdiag(unsigned long long* out8);
+// STAR over peer memory, non-selected ranks: wait for the selected rank's list
+// (epoch), copy it (own list, parity par), gather this rank's g_e at it into
+// its contribution list, write the decode's chunk bounds, publish the
+// contribution (flags[1] = epoch).  err: set on a wait timeout.
+void launch_fetch_gather(const PeerBufs& pb, int sel, int par, unsigned long long epoch, const float* ge,
+                         uint64_t k, unsigned* bounds, uint64_t nch, Ctl* ctl, double* part, cudaStream_t s);
+// Dense decode whose values are the rank-ordered sum of every rank's
+// contribution list (read from peer memory once each rank published `epoch`).
+void launch_decode_ar_peers(const PeerBufs& pb, int par, unsigned long long epoch, const unsigned* idx,
+                            const unsigned* bounds, int divide, float divisor, float* agg, uint64_t G,
+                            unsigned* zmap, unsigned* err, cudaStream_t s);
+// select_var on the device: winner of the N scores into *sel_out, this rank's
+// list (or zeros) into masked; a sum-allreduce of masked broadcasts the list.
+void launch_var_mask(const double* scores, int n, int rank, const unsigned* idx, uint64_t k, unsigned* masked,
+                     int* sel_out, cudaStream_t s);
+// bounds (nullable): also write the decode's chunk bounds of bidx (nch+1)
 void launch_gather(const unsigned* bidx, uint64_t k, const float* ge, float* contrib, Ctl* ctl,
-                   double* part, cudaStream_t s);
+                   double* part, unsigned* bounds, uint64_t nch, cudaStream_t s);
 void launch_bounds(const unsigned* idx, uint64_t k, uint64_t list_stride, int nlists, uint64_t G,
                    unsigned* bounds, cudaStream_t s);
 void launch_zero_at(const unsigned* idx, uint64_t k, float* ge, cudaStream_t s);

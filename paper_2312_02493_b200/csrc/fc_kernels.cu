@@ -228,6 +228,28 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned& target, un
   __syncthreads();
 }
 
+// System-scope epoch flags of the peer exchange (written by one GPU, polled
+// over NVLink by the others).  Waits are bounded like the grid barrier.
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void wait_epoch(const unsigned long long* flag, unsigned long long epoch,
+                                           unsigned* err) {
+  unsigned spins = 0;
+  while (ld_acquire_sys(flag) < epoch) {
+    __nanosleep(128);
+    if (++spins > (1u << 26)) {  // ~ 10 s: a peer is gone
+      if (err) atomicExch(err, 1u);
+      return;
+    }
+  }
+}
+
 // Is element i owed a zero (bit of the zero map)?
 __device__ __forceinline__ bool pending_has(const Pending& pz, uint64_t i) {
   return (__ldg(pz.zmap + zmap_word(i)) & zmap_bit(i)) != 0u;
@@ -1164,6 +1186,11 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
   if (bounds_out && blockIdx.x == 0 && tid == 0) bounds_out[nch] = (unsigned)kout;
   SEL_MARK(6);
   grid_barrier(&ctl->bar_sel, bar, &ctl->bar_err);
+  if (mode.publish && blockIdx.x == 0 && tid == 0) {  // every block's output is in (barrier)
+    __threadfence_system();
+    st_release_sys(mode.publish, mode.epoch);
+    st_release_sys(mode.publish + 1, mode.epoch);
+  }
   pdl_trigger();
   SEL_MARK(7);
   if (blockIdx.x == 0) {
@@ -1247,7 +1274,8 @@ __global__ void __launch_bounds__(kThreads) k_gather(const unsigned* __restrict_
                                                      const float* __restrict__ ge,
                                                      float* __restrict__ contrib,
                                                      Ctl* __restrict__ ctl,
-                                                     double* __restrict__ part) {
+                                                     double* __restrict__ part,
+                                                     unsigned* __restrict__ bounds, uint64_t nch) {
   pdl_wait();
   __shared__ double s_red[kThreads / 32];
   double acc = 0.0;
@@ -1266,8 +1294,16 @@ __global__ void __launch_bounds__(kThreads) k_gather(const unsigned* __restrict_
 #pragma unroll
     for (int u = 0; u < kGatherUnroll; ++u) {
       if (ii[u] != 0xffffffffu) {
-        contrib[j0 + u * step] = vv[u];
+        const uint64_t j = j0 + u * step;
+        contrib[j] = vv[u];
         acc = fma((double)vv[u], (double)vv[u], acc);
+        if (bounds) {  // the decode's chunk bounds of the (sorted) list, as k_bounds
+          const uint64_t hi = ii[u] >> kChunkShift;
+          const uint64_t lo = j == 0 ? 0 : (uint64_t)(__ldg(bidx + j - 1) >> kChunkShift) + 1;
+          for (uint64_t t = lo; t <= hi; ++t) bounds[t] = (unsigned)j;
+          if (j == k - 1)
+            for (uint64_t t = hi + 1; t <= nch; ++t) bounds[t] = (unsigned)k;
+        }
       }
     }
   }
@@ -1278,12 +1314,97 @@ __global__ void __launch_bounds__(kThreads) k_gather(const unsigned* __restrict_
   if (threadIdx.x == 0) ctl->kept_norm2 = tot;
 }
 
-void launch_gather(const unsigned* bidx, uint64_t k, const float* ge, float* contrib, Ctl* ctl,
-                   double* part, cudaStream_t s) {
+// select_var on the device (inc/artopk.hpp:35-48: argmax of the allgathered
+// ||top-k||^2, strict >, ties to the lowest rank): every block derives the
+// winner from the N scores; this rank's index list is copied to `masked`
+// if it won and zeros otherwise, so a sum-allreduce of `masked` is the
+// broadcast of the winner's list -- no host round trip for the root.
+__global__ void __launch_bounds__(kThreads) k_var_mask(const double* __restrict__ scores, int n, int rank,
+                                                       const unsigned* __restrict__ idx, uint64_t k,
+                                                       unsigned* __restrict__ masked, int* __restrict__ sel_out) {
+  pdl_wait();
+  int sel = 0;
+  for (int r = 1; r < n; ++r)
+    if (scores[r] > scores[sel]) sel = r;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *sel_out = sel;
+  const bool mine = sel == rank;
+  for (uint64_t j = blockIdx.x * (uint64_t)kThreads + threadIdx.x; j < k; j += (uint64_t)gridDim.x * kThreads)
+    masked[j] = mine ? idx[j] : 0u;
+}
+
+void launch_var_mask(const double* scores, int n, int rank, const unsigned* idx, uint64_t k, unsigned* masked,
+                     int* sel_out, cudaStream_t s) {
+  const unsigned g = (unsigned)std::min<uint64_t>(std::max<uint64_t>((k + kThreads - 1) / kThreads, 1),
+                                                  num_sms() * 8ull);
+  launch_pdl(k_var_mask, g, kThreads, 0, s, scores, n, rank, idx, k, masked, sel_out);
+  count_launch();
+}
+
+__global__ void __launch_bounds__(kThreads) k_fetch_gather(PeerBufs pb, int sel, int par,
+                                                           unsigned long long epoch,
+                                                           const float* __restrict__ ge, uint64_t k,
+                                                           unsigned* __restrict__ bounds, uint64_t nch,
+                                                           Ctl* __restrict__ ctl, double* __restrict__ part) {
+  pdl_wait();
+  __shared__ double s_red[kThreads / 32];
+  if (threadIdx.x == 0) wait_epoch(pb.flags[sel], epoch, &ctl->bar_err);
+  __syncthreads();
+  const unsigned* src = pb.list[sel] + (uint64_t)par * pb.kmax;  // the selected rank's list (NVLink)
+  unsigned* mine = pb.list[pb.rank] + (uint64_t)par * pb.kmax;
+  float* contrib = pb.contrib[pb.rank] + (uint64_t)par * pb.kmax;
+  double acc = 0.0;
+  const uint64_t step = (uint64_t)gridDim.x * kThreads;
+  for (uint64_t j0 = blockIdx.x * (uint64_t)kThreads + threadIdx.x; j0 < k; j0 += step * kGatherUnroll) {
+    unsigned ii[kGatherUnroll];
+    float vv[kGatherUnroll];
+#pragma unroll
+    for (int u = 0; u < kGatherUnroll; ++u) {
+      const uint64_t j = j0 + u * step;
+      ii[u] = j < k ? __ldcv(src + j) : 0xffffffffu;
+    }
+#pragma unroll
+    for (int u = 0; u < kGatherUnroll; ++u) vv[u] = ii[u] != 0xffffffffu ? __ldcs(ge + ii[u]) : 0.f;
+#pragma unroll
+    for (int u = 0; u < kGatherUnroll; ++u) {
+      if (ii[u] == 0xffffffffu) continue;
+      const uint64_t j = j0 + u * step;
+      mine[j] = ii[u];
+      contrib[j] = vv[u];
+      acc = fma((double)vv[u], (double)vv[u], acc);
+      const uint64_t hi = ii[u] >> kChunkShift;
+      const uint64_t lo = j == 0 ? 0 : (uint64_t)(__ldcv(src + j - 1) >> kChunkShift) + 1;
+      for (uint64_t t = lo; t <= hi; ++t) bounds[t] = (unsigned)j;
+      if (j == k - 1)
+        for (uint64_t t = hi + 1; t <= nch; ++t) bounds[t] = (unsigned)k;
+    }
+  }
+  const double b = block_sum<kThreads>(acc, s_red);
+  if (threadIdx.x == 0) part[blockIdx.x] = b;
+  pdl_trigger();
+  if (!last_block_done(&ctl->done_gather)) return;
+  const double tot = block_sum_array<kThreads>(part, gridDim.x, s_red);
+  if (threadIdx.x == 0) {
+    ctl->kept_norm2 = tot;
+    __threadfence_system();
+    st_release_sys(pb.flags[pb.rank] + 1, epoch);  // this rank's contribution is in
+  }
+}
+
+void launch_fetch_gather(const PeerBufs& pb, int sel, int par, unsigned long long epoch, const float* ge,
+                         uint64_t k, unsigned* bounds, uint64_t nch, Ctl* ctl, double* part, cudaStream_t s) {
   int grid = (int)std::min<uint64_t>((k + kThreads * kGatherUnroll - 1) / (kThreads * kGatherUnroll),
                                      (uint64_t)num_sms() * 8);
   if (grid < 1) grid = 1;
-  launch_pdl(k_gather, grid, kThreads, 0, s, bidx, k, ge, contrib, ctl, part);
+  launch_pdl(k_fetch_gather, grid, kThreads, 0, s, pb, sel, par, epoch, ge, k, bounds, nch, ctl, part);
+  count_launch();
+}
+
+void launch_gather(const unsigned* bidx, uint64_t k, const float* ge, float* contrib, Ctl* ctl,
+                   double* part, unsigned* bounds, uint64_t nch, cudaStream_t s) {
+  int grid = (int)std::min<uint64_t>((k + kThreads * kGatherUnroll - 1) / (kThreads * kGatherUnroll),
+                                     (uint64_t)num_sms() * 8);
+  if (grid < 1) grid = 1;
+  launch_pdl(k_gather, grid, kThreads, 0, s, bidx, k, ge, contrib, ctl, part, bounds, nch);
   count_launch();
 }
 
@@ -1423,16 +1544,27 @@ __device__ __forceinline__ void zero_tile(float* tile) {
 // happens here, in the reference's order: v = c_0; v += c_r (r ascending);
 // v /= N for Avg (collectives.hpp:82-87).  The same pass writes the zero map
 // of the broadcast indices: the residual zeros every worker owes (Pending).
+// kPeers: the values are the rank-ordered sum of every rank's contribution
+// list in peer memory (allreduce fused into the decode, bit-exact with the
+// reference's rank-ascending order); each block first waits for every
+// rank's "contribution ready" epoch.
+template <bool kPeers>
 __global__ void __launch_bounds__(kThreads) k_decode_ar(const unsigned* __restrict__ idx,
                                                         const unsigned* __restrict__ bounds,
                                                         const float* __restrict__ lists,
                                                         int nlists, uint64_t list_stride,
                                                         int divide, float divisor,
                                                         float* __restrict__ agg, uint64_t G,
-                                                        unsigned* __restrict__ zmap) {
+                                                        unsigned* __restrict__ zmap, PeerBufs pb,
+                                                        int par, unsigned long long epoch,
+                                                        unsigned* err) {
   pdl_wait();
   __shared__ __align__(128) float tile[2][kDecTile];
   __shared__ unsigned s_zm[kDecChunks * 32];
+  if (kPeers) {
+    if (threadIdx.x < (unsigned)pb.n) wait_epoch(pb.flags[threadIdx.x] + 1, epoch, err);
+    __syncthreads();
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) g_tdiag[0] = gtimer();
   const uint64_t ntd = (G + kDecTile - 1) >> kDecShift;
   const uint64_t nch = nchunks_of(G);
@@ -1448,8 +1580,14 @@ __global__ void __launch_bounds__(kThreads) k_decode_ar(const unsigned* __restri
     const unsigned lo = __ldg(bounds + c0), hi = __ldg(bounds + c1);
     __syncthreads();
     for (unsigned j = lo + threadIdx.x; j < hi; j += kThreads) {
-      float v = lists[j];
-      for (int l = 1; l < nlists; ++l) v += lists[(uint64_t)l * list_stride + j];
+      float v;
+      if (kPeers) {  // v = c_0; v += c_r, r ascending (collectives.hpp:82-87)
+        v = __ldcv(pb.contrib[0] + (uint64_t)par * pb.kmax + j);
+        for (int r = 1; r < pb.n; ++r) v += __ldcv(pb.contrib[r] + (uint64_t)par * pb.kmax + j);
+      } else {
+        v = lists[j];
+        for (int l = 1; l < nlists; ++l) v += lists[(uint64_t)l * list_stride + j];
+      }
       if (divide) v = v / divisor;
       const unsigned p = idx[j];
       tl[p - (unsigned)t0] = v;
@@ -1468,8 +1606,16 @@ __global__ void __launch_bounds__(kThreads) k_decode_ar(const unsigned* __restri
 void launch_decode_ar(const unsigned* idx, const unsigned* bounds, const float* lists, int nlists,
                       uint64_t list_stride, int divide, float divisor, float* agg, uint64_t G,
                       unsigned* zmap, cudaStream_t s) {
-  launch_pdl(k_decode_ar, num_sms() * 6, kThreads, 0, s, idx, bounds, lists, nlists, list_stride, divide,
-                                                  divisor, agg, G, zmap);
+  launch_pdl(k_decode_ar<false>, num_sms() * 6, kThreads, 0, s, idx, bounds, lists, nlists, list_stride, divide,
+             divisor, agg, G, zmap, PeerBufs{}, 0, 0ull, (unsigned*)nullptr);
+  count_launch();
+}
+
+void launch_decode_ar_peers(const PeerBufs& pb, int par, unsigned long long epoch, const unsigned* idx,
+                            const unsigned* bounds, int divide, float divisor, float* agg, uint64_t G,
+                            unsigned* zmap, unsigned* err, cudaStream_t s) {
+  launch_pdl(k_decode_ar<true>, num_sms() * 6, kThreads, 0, s, idx, bounds, (const float*)nullptr, pb.n,
+             (uint64_t)0, divide, divisor, agg, G, zmap, pb, par, epoch, err);
   count_launch();
 }
 
@@ -1577,7 +1723,7 @@ void launch_dense_sum(const float* lists, int nlists, uint64_t list_stride, int 
 static void prefer_max_smem() {
   const void* fs[] = {(const void*)k_fill_synth, (const void*)k_gather, (const void*)k_agg_clear,
                       (const void*)k_agg_write, (const void*)k_zero_at, (const void*)k_bounds,
-                      (const void*)k_decode_ar, (const void*)k_decode_ag, (const void*)k_dense_sum,
+                      (const void*)k_decode_ar<false>, (const void*)k_decode_ar<true>, (const void*)k_decode_ag, (const void*)k_dense_sum,
                       (const void*)k_sum_fixed};
   for (const void* f : fs)
     cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);

@@ -268,6 +268,13 @@ class Cluster:
     def sync(self) -> None:
         check(lib.fc_sync(self._ctx))
 
+    @property
+    def peer_exchange(self) -> bool:
+        """STAR steps exchange through NVLink peer memory (else NCCL)."""
+        e = C.c_int()
+        check(lib.fc_peer_exchange(self._ctx, C.byref(e)))
+        return bool(e.value)
+
     def moo_metrics(self, st: "StepStats", ag: bool = False) -> tuple[float, float]:
         """(gain, t_comp seconds) of the last step, identical on every rank
         (the Trainer's *_with_gain, inc/trainer.hpp:361-398; t_comp measured)."""

@@ -45,6 +45,9 @@ def main() -> int:
     failures = []
     with fc.Cluster.nccl(env.world, env.rank, uid, G, device=env.local_rank, max_cr=0.2) as cl:
         cl.set_layer_map(layers)
+        p2p = cl.peer_exchange
+        if env.rank == 0:
+            print(f"[mp_check] peer exchange: {p2p}", flush=True)
         res = np.zeros((env.world, G), np.float32) if env.rank == 0 else None
         for s, (kind, algo, c) in enumerate(plan):
             cl.fill_synthetic(0, 1234, env.rank, s)
@@ -95,6 +98,10 @@ def main() -> int:
                     scale = np.abs(base).sum(axis=0) / env.world
                     if (kind != "dense"):
                         scale = np.where(ref != 0, scale, 0)
+                    if kind == "star" and p2p and not np.array_equal(aggs[r].view(np.uint32),
+                                                                       ref.view(np.uint32)):
+                        # rank-ordered sums over peer memory: bit-exact
+                        failures.append(f"step {s} star: peer-exchange aggregate on rank {r} not bit-exact")
                     err = np.abs(aggs[r].astype(np.float64) - ref)
                     if not np.all(err <= 1e-5 * scale + 1e-30):
                         failures.append(f"step {s} {kind}: aggregate on rank {r} off by {err.max():.3g}")
