@@ -659,7 +659,7 @@ int setup_p2p(fc_ctx* c) {
   if (!c->nccl || N < 2 || N > fcb::kMaxPeers || std::getenv("FC_NO_P2P")) return FC_OK;
   const uint64_t list_b = align_up(2 * c->kmax * sizeof(unsigned), 256);
   const uint64_t contrib_b = align_up(2 * c->kmax * sizeof(float), 256);
-  const uint64_t total = list_b + contrib_b + 256;
+  const uint64_t total = list_b + 2 * contrib_b + 256;
   CUDA_TRY(cudaMalloc(&c->xbuf, total));
   CUDA_TRY(cudaMemset(c->xbuf, 0, total));
   int ok = 1;
@@ -707,7 +707,8 @@ int setup_p2p(fc_ctx* c) {
   for (int r = 0; r < N; ++r) {
     c->pb.list[r] = reinterpret_cast<unsigned*>(base[r]);
     c->pb.contrib[r] = reinterpret_cast<float*>(base[r] + list_b);
-    c->pb.flags[r] = reinterpret_cast<unsigned long long*>(base[r] + list_b + contrib_b);
+    c->pb.reduced[r] = reinterpret_cast<float*>(base[r] + list_b + contrib_b);
+    c->pb.flags[r] = reinterpret_cast<unsigned long long*>(base[r] + list_b + 2 * contrib_b);
   }
   c->p2p = true;
   return FC_OK;
@@ -1328,8 +1329,14 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
   TRY(agg_target(c, &ob));
   float* aggw = c->agg_buf[ob];
   if (p2p_star) {
-    fcb::launch_decode_ar_peers(c->pb, par, epoch, bsrc, own_bounds, op == FC_AVG, (float)N, aggw, c->G,
-                                c->zmaps, &c->w[0].ctl->bar_err, c->stream);
+    // N > 2: reduce-scatter (each rank sums its slice of the list from every
+    // rank's contribution, rank order), then the decode reads each value from
+    // the slice's owner: ring-like NVLink traffic, rank-ordered sums
+    // (two ranks: the decode sums both contributions directly, one fewer launch)
+    const bool rs = N > 2;
+    if (rs) fcb::launch_reduce_slice(c->pb, par, epoch, k, op == FC_AVG, (float)N, c->w[0].ctl, c->stream);
+    fcb::launch_decode_ar_peers(c->pb, par, epoch, bsrc, own_bounds, k, op == FC_AVG, (float)N, rs, aggw,
+                                c->G, c->zmaps, &c->w[0].ctl->bar_err, c->stream);
   } else if (incr_ok && c->agg_incr) {
     // in place: zero the previous support, write this one (same dense content)
     fcb::launch_agg_update(c->agg_support, c->agg_support_k, bsrc, k, lists, nlists, lstride,

@@ -38,7 +38,7 @@ struct Ctl {
   unsigned L_digit;       // candidate bound: key >= L_digit << kShift1
   unsigned fallback;      // 1 => sampled bound missed, full re-emission ran
   unsigned cand_count;    // M: candidates emitted
-  unsigned done_sample, done_ef, done_fbh, done_fbe, done_gather;
+  unsigned done_sample, done_ef, done_fbh, done_fbe, done_gather, done_red;
   unsigned ef_next;       // EF work queue: next chunk to hand out
   unsigned bar_ef, bar_sel;  // software grid barriers of the EF / select kernels
   unsigned bar_err;       // a grid barrier timed out (blocks not co-resident)
@@ -106,7 +106,8 @@ constexpr int kMaxPeers = 8;
 struct PeerBufs {
   unsigned* list[kMaxPeers];
   float* contrib[kMaxPeers];
-  unsigned long long* flags[kMaxPeers];  // [0] list epoch, [1] contribution epoch
+  float* reduced[kMaxPeers];             // rank r: the reduced values of its slice of the list
+  unsigned long long* flags[kMaxPeers];  // [0] list, [1] contribution, [2] reduced slice epochs
   int n = 0, rank = 0;
   uint64_t kmax = 0;
 };
@@ -142,11 +143,18 @@ void read_tdiag(unsigned long long* out8);
 // contribution (flags[1] = epoch).  err: set on a wait timeout.
 void launch_fetch_gather(const PeerBufs& pb, int sel, int par, unsigned long long epoch, const float* ge,
                          uint64_t k, unsigned* bounds, uint64_t nch, Ctl* ctl, double* part, cudaStream_t s);
-// Dense decode whose values are the rank-ordered sum of every rank's
-// contribution list (read from peer memory once each rank published `epoch`).
+// Reduce-scatter over peer memory: once every rank published its
+// contribution (`epoch`), rank r sums slice r of the list in rank order
+// (collectives.hpp:82-87, /divisor when divide) from all ranks' lists into
+// its reduced area and publishes it (flags[2]).
+void launch_reduce_slice(const PeerBufs& pb, int par, unsigned long long epoch, uint64_t k, int divide,
+                         float divisor, Ctl* ctl, cudaStream_t s);
+// Dense decode over peer memory once every rank published `epoch`: value j
+// is the rank-ordered sum of every rank's contribution (/divisor when divide)
+// or, with `reduced`, read from the reduced area of the rank owning slice j.
 void launch_decode_ar_peers(const PeerBufs& pb, int par, unsigned long long epoch, const unsigned* idx,
-                            const unsigned* bounds, int divide, float divisor, float* agg, uint64_t G,
-                            unsigned* zmap, unsigned* err, cudaStream_t s);
+                            const unsigned* bounds, uint64_t k, int divide, float divisor, bool reduced,
+                            float* agg, uint64_t G, unsigned* zmap, unsigned* err, cudaStream_t s);
 // select_var on the device: winner of the N scores into *sel_out, this rank's
 // list (or zeros) into masked; a sum-allreduce of masked broadcasts the list.
 void launch_var_mask(const double* scores, int n, int rank, const unsigned* idx, uint64_t k, unsigned* masked,

@@ -1548,7 +1548,9 @@ __device__ __forceinline__ void zero_tile(float* tile) {
 // list in peer memory (allreduce fused into the decode, bit-exact with the
 // reference's rank-ascending order); each block first waits for every
 // rank's "contribution ready" epoch.
-template <bool kPeers>
+// kPeers 0: local lists; 1: v = sum over every rank's contribution (peer
+// memory, rank order; 2 ranks); 2: v from the reduced slice's owner (N > 2).
+template <int kPeers>
 __global__ void __launch_bounds__(kThreads) k_decode_ar(const unsigned* __restrict__ idx,
                                                         const unsigned* __restrict__ bounds,
                                                         const float* __restrict__ lists,
@@ -1561,8 +1563,8 @@ __global__ void __launch_bounds__(kThreads) k_decode_ar(const unsigned* __restri
   pdl_wait();
   __shared__ __align__(128) float tile[2][kDecTile];
   __shared__ unsigned s_zm[kDecChunks * 32];
-  if (kPeers) {
-    if (threadIdx.x < (unsigned)pb.n) wait_epoch(pb.flags[threadIdx.x] + 1, epoch, err);
+  if (kPeers) {  // every rank's contribution (1) / reduced slice (2) is in
+    if (threadIdx.x < (unsigned)pb.n) wait_epoch(pb.flags[threadIdx.x] + kPeers, epoch, err);
     __syncthreads();
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) g_tdiag[0] = gtimer();
@@ -1581,9 +1583,14 @@ __global__ void __launch_bounds__(kThreads) k_decode_ar(const unsigned* __restri
     __syncthreads();
     for (unsigned j = lo + threadIdx.x; j < hi; j += kThreads) {
       float v;
-      if (kPeers) {  // v = c_0; v += c_r, r ascending (collectives.hpp:82-87)
+      if (kPeers == 1) {  // v = c_0; v += c_r, r ascending (collectives.hpp:82-87)
         v = __ldcv(pb.contrib[0] + (uint64_t)par * pb.kmax + j);
         for (int r = 1; r < pb.n; ++r) v += __ldcv(pb.contrib[r] + (uint64_t)par * pb.kmax + j);
+      } else if (kPeers == 2) {  // from the owner of slice j (list_stride = k here)
+        int r = (int)(((uint64_t)j * pb.n) / list_stride);
+        while (r + 1 < pb.n && ((uint64_t)(r + 1) * list_stride) / pb.n <= j) ++r;
+        while (r > 0 && ((uint64_t)r * list_stride) / pb.n > j) --r;
+        v = __ldcv(pb.reduced[r] + (uint64_t)par * pb.kmax + j);
       } else {
         v = lists[j];
         for (int l = 1; l < nlists; ++l) v += lists[(uint64_t)l * list_stride + j];
@@ -1606,16 +1613,53 @@ __global__ void __launch_bounds__(kThreads) k_decode_ar(const unsigned* __restri
 void launch_decode_ar(const unsigned* idx, const unsigned* bounds, const float* lists, int nlists,
                       uint64_t list_stride, int divide, float divisor, float* agg, uint64_t G,
                       unsigned* zmap, cudaStream_t s) {
-  launch_pdl(k_decode_ar<false>, num_sms() * 6, kThreads, 0, s, idx, bounds, lists, nlists, list_stride, divide,
+  launch_pdl(k_decode_ar<0>, num_sms() * 6, kThreads, 0, s, idx, bounds, lists, nlists, list_stride, divide,
              divisor, agg, G, zmap, PeerBufs{}, 0, 0ull, (unsigned*)nullptr);
   count_launch();
 }
 
 void launch_decode_ar_peers(const PeerBufs& pb, int par, unsigned long long epoch, const unsigned* idx,
-                            const unsigned* bounds, int divide, float divisor, float* agg, uint64_t G,
-                            unsigned* zmap, unsigned* err, cudaStream_t s) {
-  launch_pdl(k_decode_ar<true>, num_sms() * 6, kThreads, 0, s, idx, bounds, (const float*)nullptr, pb.n,
-             (uint64_t)0, divide, divisor, agg, G, zmap, pb, par, epoch, err);
+                            const unsigned* bounds, uint64_t k, int divide, float divisor, bool reduced,
+                            float* agg, uint64_t G, unsigned* zmap, unsigned* err, cudaStream_t s) {
+  if (reduced)
+    launch_pdl(k_decode_ar<2>, num_sms() * 6, kThreads, 0, s, idx, bounds, (const float*)nullptr, pb.n, k, 0,
+               1.0f, agg, G, zmap, pb, par, epoch, err);
+  else
+    launch_pdl(k_decode_ar<1>, num_sms() * 6, kThreads, 0, s, idx, bounds, (const float*)nullptr, pb.n, k,
+               divide, divisor, agg, G, zmap, pb, par, epoch, err);
+  count_launch();
+}
+
+// Reduce-scatter step of the peer exchange (see launch_reduce_slice).
+__global__ void __launch_bounds__(kThreads) k_reduce_slice(PeerBufs pb, int par, unsigned long long epoch,
+                                                           uint64_t k, int divide, float divisor,
+                                                           Ctl* __restrict__ ctl) {
+  pdl_wait();
+  if (threadIdx.x < (unsigned)pb.n) wait_epoch(pb.flags[threadIdx.x] + 1, epoch, &ctl->bar_err);
+  __syncthreads();
+  const uint64_t s0 = (k * pb.rank) / pb.n, s1 = (k * (pb.rank + 1)) / pb.n;
+  const uint64_t off = (uint64_t)par * pb.kmax;
+  float* out = pb.reduced[pb.rank] + off;
+  for (uint64_t j = s0 + blockIdx.x * (uint64_t)kThreads + threadIdx.x; j < s1; j += (uint64_t)gridDim.x * kThreads) {
+    float v = __ldcv(pb.contrib[0] + off + j);  // v = c_0; v += c_r, r ascending
+    for (int r = 1; r < pb.n; ++r) v += __ldcv(pb.contrib[r] + off + j);
+    if (divide) v = v / divisor;
+    out[j] = v;
+  }
+  pdl_trigger();
+  if (!last_block_done(&ctl->done_red)) return;
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    st_release_sys(pb.flags[pb.rank] + 2, epoch);  // this rank's slice is reduced
+  }
+}
+
+void launch_reduce_slice(const PeerBufs& pb, int par, unsigned long long epoch, uint64_t k, int divide,
+                         float divisor, Ctl* ctl, cudaStream_t s) {
+  const uint64_t slice = k / pb.n + 1;
+  const unsigned g = (unsigned)std::min<uint64_t>(std::max<uint64_t>((slice + kThreads - 1) / kThreads, 1),
+                                                  num_sms() * 4ull);
+  launch_pdl(k_reduce_slice, g, kThreads, 0, s, pb, par, epoch, k, divide, divisor, ctl);
   count_launch();
 }
 
@@ -1723,7 +1767,7 @@ void launch_dense_sum(const float* lists, int nlists, uint64_t list_stride, int 
 static void prefer_max_smem() {
   const void* fs[] = {(const void*)k_fill_synth, (const void*)k_gather, (const void*)k_agg_clear,
                       (const void*)k_agg_write, (const void*)k_zero_at, (const void*)k_bounds,
-                      (const void*)k_decode_ar<false>, (const void*)k_decode_ar<true>, (const void*)k_decode_ag, (const void*)k_dense_sum,
+                      (const void*)k_decode_ar<0>, (const void*)k_decode_ar<1>, (const void*)k_decode_ar<2>, (const void*)k_decode_ag, (const void*)k_dense_sum,
                       (const void*)k_sum_fixed};
   for (const void* f : fs)
     cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
