@@ -308,7 +308,7 @@ int run_ef(fc_ctx* c, int i, uint64_t k, bool topk) {
 // selection into bounds slot i (so a decode of this list needs no k_bounds).
 int run_select(fc_ctx* c, int i, uint64_t k, const float* ef_out = nullptr,
                const fcb::SelectMode& mode = fcb::SelectMode{}, unsigned* out_idx = nullptr,
-               float* out_val = nullptr) {
+               float* out_val = nullptr, unsigned* out_bounds = nullptr) {
   Worker& w = c->w[i];
   // exact: [idx k | val k]; threshold (count unknown): [idx kmax | val kmax]
   const uint64_t voff = mode.rounds > 0 ? c->kmax : k;
@@ -319,7 +319,8 @@ int run_select(fc_ctx* c, int i, uint64_t k, const float* ef_out = nullptr,
   w.topk_idx = out_idx;
   w.topk_val = out_val;
   const int e = fcb::launch_select(k, w.ctl, w.ws, ef_out ? ef_out : w.ge, c->G, out_idx, out_val,
-                                   c->bounds + (uint64_t)i * (c->nch + 1), mode, c->stream);
+                                   out_bounds ? out_bounds : c->bounds + (uint64_t)i * (c->nch + 1), mode,
+                                   c->stream);
   if (e) return fail(FC_ERR_CUDA, std::string("k_select launch: ") +
                                       cudaGetErrorString(static_cast<cudaError_t>(e)));
   LAUNCHED();
@@ -657,9 +658,12 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
 int setup_p2p(fc_ctx* c) {
   const int N = c->world;
   if (!c->nccl || N < 2 || N > fcb::kMaxPeers || std::getenv("FC_NO_P2P")) return FC_OK;
-  const uint64_t list_b = align_up(2 * c->kmax * sizeof(unsigned), 256);
-  const uint64_t contrib_b = align_up(2 * c->kmax * sizeof(float), 256);
-  const uint64_t total = list_b + 2 * contrib_b + 256;
+  // parity strides are multiples of 4 elements (16-byte rows for vector pulls)
+  const uint64_t kst = align_up(c->kmax, 4), nbs = align_up(c->nch + 1, 4);
+  const uint64_t list_b = align_up(2 * kst * sizeof(unsigned), 256);
+  const uint64_t contrib_b = align_up(2 * kst * sizeof(float), 256);
+  const uint64_t bounds_b = align_up(2 * nbs * sizeof(unsigned), 256);
+  const uint64_t total = list_b + 2 * contrib_b + bounds_b + 256;
   CUDA_TRY(cudaMalloc(&c->xbuf, total));
   CUDA_TRY(cudaMemset(c->xbuf, 0, total));
   int ok = 1;
@@ -703,12 +707,15 @@ int setup_p2p(fc_ctx* c) {
   }
   c->pb.n = N;
   c->pb.rank = c->rank;
-  c->pb.kmax = c->kmax;
+  c->pb.kmax = kst;
+  c->pb.nb = c->nch + 1;
+  c->pb.nbs = nbs;
   for (int r = 0; r < N; ++r) {
     c->pb.list[r] = reinterpret_cast<unsigned*>(base[r]);
     c->pb.contrib[r] = reinterpret_cast<float*>(base[r] + list_b);
     c->pb.reduced[r] = reinterpret_cast<float*>(base[r] + list_b + contrib_b);
-    c->pb.flags[r] = reinterpret_cast<unsigned long long*>(base[r] + list_b + 2 * contrib_b);
+    c->pb.bounds[r] = reinterpret_cast<unsigned*>(base[r] + list_b + 2 * contrib_b);
+    c->pb.flags[r] = reinterpret_cast<unsigned long long*>(base[r] + list_b + 2 * contrib_b + bounds_b);
   }
   c->p2p = true;
   return FC_OK;
@@ -1219,8 +1226,8 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
       m.publish = c->pb.flags[c->rank];
       m.epoch = epoch;
       m.err = &c->w[i].ctl->bar_err;
-      TRY(run_select(c, i, k, nullptr, m, c->pb.list[c->rank] + par * c->kmax,
-                     c->pb.contrib[c->rank] + par * c->kmax));
+      TRY(run_select(c, i, k, nullptr, m, c->pb.list[c->rank] + par * c->pb.kmax,
+                     c->pb.contrib[c->rank] + par * c->pb.kmax));
     } else {
       TRY(run_select(c, i, k));
     }
@@ -1255,7 +1262,7 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
     else
       w.kept_is_topk = true;
     LAUNCHED();
-    bsrc = c->pb.list[c->rank] + par * c->kmax;  // local copy of the selected list
+    bsrc = c->pb.list[c->rank] + par * c->pb.kmax;  // local copy of the selected list
     own_bounds = c->bounds;
   } else if (c->nccl && N == 1) {
     // a single rank: broadcast and allreduce are identities
@@ -1398,8 +1405,21 @@ int fc_ag_step(fc_ctx* c, double cr, int compressor, fc_step_stats* st) {
   for (int i = 0; i < c->n_local; ++i) TRY(run_ef(c, i, k, compressor != FC_LAYERWISE));
   advance_input(c);
   record(c, 1);
+  // Exact AG over peer memory: each rank's select publishes its list, values
+  // and chunk bounds in its exchange buffer; one pull kernel replaces the
+  // allgather and k_bounds
+  const bool p2p_ag = c->p2p && compressor == FC_EXACT && N > 1;
+  const unsigned long long epoch = p2p_ag ? ++c->epoch : 0;
+  const int par = (int)(epoch & 1);
   for (int i = 0; i < c->n_local; ++i) {
-    if (compressor == FC_EXACT) {
+    if (compressor == FC_EXACT && p2p_ag) {
+      fcb::SelectMode m;
+      m.publish = c->pb.flags[c->rank];
+      m.epoch = epoch;
+      TRY(run_select(c, i, k, nullptr, m, c->pb.list[c->rank] + par * c->pb.kmax,
+                     c->pb.contrib[c->rank] + par * c->pb.kmax, c->pb.bounds[c->rank] + par * c->pb.nbs));
+      c->w[i].kept_is_topk = true;
+    } else if (compressor == FC_EXACT) {
       TRY(run_select(c, i, k));
       c->w[i].kept_is_topk = true;
     } else if (compressor == FC_LAYERWISE) {
@@ -1432,7 +1452,14 @@ int fc_ag_step(fc_ctx* c, double cr, int compressor, fc_step_stats* st) {
     }
     kk = *std::max_element(kr.begin(), kr.end());
   }
-  if (c->nccl && N == 1) {
+  if (p2p_ag) {
+    fcb::launch_collect_packs(c->pb, par, epoch, kk, c->ag_recv, c->bounds, &c->w[0].ctl->bar_err, c->stream);
+    LAUNCHED();
+    packs = c->ag_recv;
+    stride = 2 * kk;
+    voff = kk;
+    local_bounds = true;  // collected with the lists
+  } else if (c->nccl && N == 1) {
     packs = c->w[0].pack;  // allgather over one rank: identity
     stride = 2 * c->kmax;
     voff = compressor == FC_THRESHOLD ? c->kmax : kk;

@@ -107,10 +107,17 @@ struct PeerBufs {
   unsigned* list[kMaxPeers];
   float* contrib[kMaxPeers];
   float* reduced[kMaxPeers];             // rank r: the reduced values of its slice of the list
+  unsigned* bounds[kMaxPeers];           // AG: the chunk bounds of rank r's list (2 parities)
   unsigned long long* flags[kMaxPeers];  // [0] list, [1] contribution, [2] reduced slice epochs
   int n = 0, rank = 0;
-  uint64_t kmax = 0;
+  uint64_t kmax = 0;                     // parity stride of list/contrib/reduced (multiple of 4)
+  uint64_t nb = 0, nbs = 0;              // bounds entries (nchunks + 1), parity stride (multiple of 4)
 };
+// AG over peer memory: once every rank published `epoch`, copy every rank's
+// list (indices, values) and chunk bounds into local arrays laid out as the
+// NCCL allgather + k_bounds would have produced them.
+void launch_collect_packs(const PeerBufs& pb, int par, unsigned long long epoch, uint64_t k, unsigned* packs,
+                          unsigned* bounds, unsigned* err, cudaStream_t s);
 // bounds_out (nullable): nchunks+1 entries, bounds_out[c] = first output
 // position whose index is >= c * kChunk (what k_bounds computes from a list)
 // ef_out: the array the EF pass wrote g_e to (read only by the fallback).

@@ -1630,6 +1630,54 @@ void launch_decode_ar_peers(const PeerBufs& pb, int par, unsigned long long epoc
   count_launch();
 }
 
+// AG over peer memory: the allgather (and k_bounds) as one pull kernel.
+// Remote rows are read 16 bytes at a time (parity strides are multiples of 4
+// elements), written to the local layout with 4-byte stores.
+__device__ __forceinline__ void pull_row(const unsigned* __restrict__ src, unsigned* __restrict__ dst,
+                                         uint64_t n, uint64_t t, uint64_t nt) {
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+  const uint64_t n4 = n / 4;
+  for (uint64_t q = t; q < n4; q += nt) {
+    const uint4 v = __ldcv(s4 + q);
+    dst[4 * q] = v.x;
+    dst[4 * q + 1] = v.y;
+    dst[4 * q + 2] = v.z;
+    dst[4 * q + 3] = v.w;
+  }
+  for (uint64_t q = 4 * n4 + t; q < n; q += nt) dst[q] = __ldcv(src + q);
+}
+
+__global__ void __launch_bounds__(kThreads) k_collect_packs(PeerBufs pb, int par, unsigned long long epoch,
+                                                            uint64_t k, unsigned* __restrict__ packs,
+                                                            unsigned* __restrict__ bounds, unsigned* err) {
+  pdl_wait();
+  if (threadIdx.x < (unsigned)pb.n) wait_epoch(pb.flags[threadIdx.x], epoch, err);
+  __syncthreads();
+  // blocks split over (rank, row): idx k | val k | bounds nb
+  const int rows = 3 * pb.n;
+  const unsigned per = gridDim.x / rows > 0 ? gridDim.x / rows : 1;
+  for (unsigned b = blockIdx.x; b < per * rows; b += gridDim.x) {
+    const int row = (int)(b / per);
+    const uint64_t t = (uint64_t)(b % per) * kThreads + threadIdx.x, nt = (uint64_t)per * kThreads;
+    const int r = row / 3, part = row % 3;
+    if (part == 0)
+      pull_row(pb.list[r] + (uint64_t)par * pb.kmax, packs + (uint64_t)r * 2 * k, k, t, nt);
+    else if (part == 1)
+      pull_row(reinterpret_cast<const unsigned*>(pb.contrib[r] + (uint64_t)par * pb.kmax),
+               packs + (uint64_t)r * 2 * k + k, k, t, nt);
+    else
+      pull_row(pb.bounds[r] + (uint64_t)par * pb.nbs, bounds + (uint64_t)r * pb.nb, pb.nb, t, nt);
+  }
+  pdl_trigger();
+}
+
+void launch_collect_packs(const PeerBufs& pb, int par, unsigned long long epoch, uint64_t k, unsigned* packs,
+                          unsigned* bounds, unsigned* err, cudaStream_t s) {
+  const unsigned g = (unsigned)(3 * pb.n * std::max<int>(1, num_sms() * 8 / (3 * pb.n)));
+  launch_pdl(k_collect_packs, g, kThreads, 0, s, pb, par, epoch, k, packs, bounds, err);
+  count_launch();
+}
+
 // Reduce-scatter step of the peer exchange (see launch_reduce_slice).
 __global__ void __launch_bounds__(kThreads) k_reduce_slice(PeerBufs pb, int par, unsigned long long epoch,
                                                            uint64_t k, int divide, float divisor,
