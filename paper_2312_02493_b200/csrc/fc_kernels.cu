@@ -711,6 +711,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
   __shared__ unsigned long long s_red[kSelWarps];
   __shared__ double s_dred[kSelWarps];
   __shared__ unsigned s_used, s_cached, s_dense;
+  __shared__ __align__(8) unsigned long long s_mbar;  // candidate staging (TMA)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned lt = lanemask_lt();
   SEL_MARK(0);
@@ -806,34 +807,20 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
   const float* gval = w.cand_val + ((uint64_t)c0 << kChunkShift);
   const unsigned* gidx = w.cand_idx + ((uint64_t)c0 << kChunkShift);
   if (cached) {
-    if (dense) {  // warp per chunk, 4 chunks per round
-      for (unsigned cb = warp; cb < nc; cb += kSelWarps * 4) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const unsigned c = cb + u * kSelWarps;
-          if (c >= nc) break;
-          const unsigned n = s_cnt[c];
-          const float* src = gval + ((uint64_t)c << kChunkShift);
-          float* dst = s_val + s_off[c];
-          for (unsigned p = lane; p < n; p += 32) dst[p] = __ldcg(src + p);
-        }
-      }
-    } else {  // thread per chunk, up to kSelQ 16-byte loads in flight
-      for (unsigned c = t0; c < t1; ++c) {
-        const unsigned n4 = (s_cnt[c] + 3) >> 2;
-        const float4* v4 = reinterpret_cast<const float4*>(gval + ((uint64_t)c << kChunkShift));
-        float4* d4 = reinterpret_cast<float4*>(s_val + s_off[c]);
-        for (unsigned q0 = 0; q0 < n4; q0 += kSelQ) {
-          float4 x[kSelQ];
-#pragma unroll
-          for (int u = 0; u < kSelQ; ++u)
-            if (q0 + u < n4) x[u] = __ldcg(v4 + q0 + u);
-#pragma unroll
-          for (int u = 0; u < kSelQ; ++u)
-            if (q0 + u < n4) d4[q0 + u] = x[u];
-        }
-      }
+    // every chunk's candidate run by one TMA bulk copy (rounded up to 16 bytes:
+    // the slots are 4 KB apart, so the over-read stays inside the slot), all
+    // completing on one mbarrier that expects the block's total bytes
+    if (tid == 0) {
+      mbar_init(&s_mbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_expect_tx(&s_mbar, s_used * 4u);
     }
+    __syncthreads();
+    for (unsigned c = t0; c < t1; ++c) {
+      const unsigned bytes = ((s_cnt[c] + 3u) & ~3u) * 4u;
+      if (bytes) bulk_g2s(s_val + s_off[c], gval + ((uint64_t)c << kChunkShift), bytes, &s_mbar);
+    }
+    mbar_wait(&s_mbar, 0);
     __syncthreads();
   }
   SEL_MARK(1);
