@@ -1,32 +1,34 @@
 // fc_kernels.cu — sm_100a kernels of the Top-k gradient-sync hot path.
 //
 // Reference algorithm (all in /root/reference/proj/include/flexcomm):
-//   error_feedback        compress.hpp:114-120   -> k_ef (fused with candidate
-//                                                   emission + the previous
-//                                                   step's residual zeroing)
-//   select_topk_indices   compress.hpp:38-53     -> k_sample, k_ef, k_refine1,
-//                                                   k_refine2, k_emit
-//   artopk gather         artopk.hpp:92-98       -> k_gather
+//   error_feedback        compress.hpp:114-120   -> k_ef (fused: candidate-bound
+//                                                   sample, candidate emission,
+//                                                   the previous step's residual
+//                                                   zeros)
+//   select_topk_indices   compress.hpp:38-53     -> k_ef (candidates) + k_select
+//   topk_layerwise        compress.hpp:67-79     -> k_ef + k_select per layer
+//   topk_threshold        compress.hpp:81-112    -> k_select (bisection mode)
+//   select_var            artopk.hpp:35-48       -> k_var_mask (NCCL path)
+//   artopk gather         artopk.hpp:92-98       -> k_gather / k_fetch_gather
 //   residual zeroing      artopk.hpp:99-101,
-//   residual_update       compress.hpp:122-130   -> Pending zeros, applied by
+//   residual_update       compress.hpp:122-130   -> owed zeros, applied by
 //                                                   the next k_ef (k_zero_at
 //                                                   when materialised early)
-//   densify               core.hpp:72-81         -> k_bounds + k_decode_ar
-//   ag_step scatter-add   artopk.hpp:151-159     -> k_bounds + k_decode_ag
-//   allreduce (loopback)  collectives.hpp:82-87  -> summed inside k_decode_ar
+//   allreduce             collectives.hpp:82-87  -> rank-ordered sums inside
+//                                                   k_decode_ar (loopback, 2
+//                                                   peers) / k_reduce_slice
+//   densify               core.hpp:72-81         -> k_decode_ar
+//   ag_step scatter-add   artopk.hpp:151-159     -> k_collect_packs + k_decode_ag
 //
 // Everything is HBM-bound integer/fp32 streaming work: no tensor cores.
 // DESIGN.md §4 gives each kernel's algorithmic bytes and roofline.
 #include <atomic>
 #include <cstdio>
 
-#include <cooperative_groups.h>
-
 #include "fc_device.cuh"
 #include "fc_synth.h"
 
 namespace fcb {
-namespace cg = cooperative_groups;
 
 static std::atomic<uint64_t> g_launches{0};
 // diagnostics: %globaltimer marks of the last step's kernels
@@ -200,7 +202,8 @@ __device__ bool block_select_top(const unsigned* hist, int nb, unsigned long lon
 
 // Grid barrier for the kernels that run exactly one block per SM (grid = SM
 // count, shared memory sized so that no second block fits), launched as plain
-// kernels: a cooperative launch costs ~8 us more per kernel here.  `ctr` is a
+// kernels so they can use programmatic dependent launch and cost no
+// cooperative-group bookkeeping (a barrier is ~2 us).  `ctr` is a
 // per-step counter (zeroed with the control block); every barrier raises the
 // target by gridDim.x.  The wait is bounded: if the blocks were not all
 // resident, *err is set and the kernel proceeds (the host reports it).

@@ -1,4 +1,5 @@
-"""Phase timing of the cooperative select kernel (block 0, %globaltimer)."""
+"""Phase timing of the select kernel and the EF kernel (block 0, %globaltimer),
+plus the EF blocks' start/end spread."""
 import ctypes as C
 import sys
 from pathlib import Path
