@@ -35,7 +35,7 @@ constexpr int kSamples = 32768;                // candidate-bound sample size
 // Per-worker control block.  Each worker has two, used by alternate steps; the
 // EF pass of one step zeroes the other for the next step.
 struct Ctl {
-  unsigned L_digit;       // candidate bound: key >= L_digit << kShift1
+  unsigned Lkey;          // candidate bound: every element with key >= Lkey
   unsigned fallback;      // 1 => sampled bound missed, full re-emission ran
   unsigned cand_count;    // M: candidates emitted
   unsigned done_sample, done_ef, done_fbh, done_fbe, done_gather, done_red;
@@ -53,6 +53,7 @@ struct Ctl {
   unsigned long long tphase[8];  // %globaltimer at k_select phase boundaries (diagnostics)
   unsigned long long tphase_ef[4];  // ... and at k_ef's (start, sampled, bound, end)
   unsigned hist_s[kBins1];   // sample histogram (digit 1)
+  unsigned hist_s2[256];     // sample histogram of bits 18..11 inside the bound's bucket
   unsigned hist1[kBins1];    // candidate histogram, key bits 30..19 (k_select)
   unsigned hist_fb[kBins1];  // full histogram (fallback only)
   unsigned hist2[256];       // bits 18..11 of bucket-b1 candidates

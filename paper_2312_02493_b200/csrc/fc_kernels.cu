@@ -281,17 +281,12 @@ __device__ __forceinline__ uint64_t sample_pos(uint64_t s, uint64_t G) {
   return ((2 * s + 1) * G) / (2ull * kSamples);
 }
 
-template <int B>
-__device__ unsigned sample_bound(const unsigned* hist_s, uint64_t G, uint64_t k, bool force_fb,
-                                 unsigned* s_stage) {
-  if (force_fb) return kBins1 - 1;
+// The bound's sample count: mean + 4 sigma of sampling noise + 5 % + 8 (a
+// bound above the true threshold -- probability ~1e-5 -- only costs the
+// fallback in k_select).
+__device__ __forceinline__ double sample_target(uint64_t G, uint64_t k) {
   const double mean = (double)k / (double)G * (double)kSamples;
-  // 6 sigma of sampling noise plus 15 %: a miss only costs the fallback
-  const double target = 1.15 * mean + 6.0 * sqrt(mean) + 8.0;
-  if (!(target < (double)kSamples)) return 0;
-  unsigned bin;
-  unsigned long long above;
-  return block_select_top<B>(hist_s, kBins1, (unsigned long long)target, bin, above, s_stage) ? bin : 0u;
+  return 1.05 * mean + 4.0 * sqrt(mean) + 8.0;
 }
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -460,15 +455,45 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
       unsigned bar = 0;
       grid_barrier(&ctl->bar_ef, bar, &ctl->bar_err);
       EF_MARK(1);
-      const unsigned Ld = sample_bound<kThreads>(ctl->hist_s, G, k, (opts & 2) != 0, s_hist);
+      // the bound: the sample's 12-bit bucket holding the target-th largest
+      // value, then (second level) the 8 bits below inside that bucket, so
+      // candidates overshoot the target by < 0.3 % of a value instead of up
+      // to one 1/16-octave bucket
+      const double target = sample_target(G, k);
+      if (opts & 2) {
+        Lkey = (unsigned)(kBins1 - 1) << kShift1;  // forced miss (tests)
+      } else if (target < (double)kSamples) {
+        unsigned b1, b2;
+        unsigned long long above1, above2;
+        const unsigned long long tgt = (unsigned long long)target;
+        if (block_select_top<kThreads>(ctl->hist_s, kBins1, tgt, b1, above1, s_hist)) {
+          for (int b = tid; b < 256; b += kThreads) s_hist[b] = 0u;
+          __syncthreads();
+          auto level2 = [&](float v) {
+            const unsigned key = key_of(v);
+            if ((key >> kShift1) == b1) atomicAdd(&s_hist[(key >> 11) & 255u], 1u);
+          };
+          if (q0 < (unsigned)kSamples) level2(sv);
+          for (unsigned q = q0 + qstride; q < (unsigned)kSamples; q += qstride) level2(sample_at(q));
+          __syncthreads();
+          for (int b = tid; b < 256; b += kThreads)
+            if (s_hist[b]) atomicAdd(&ctl->hist_s2[b], s_hist[b]);
+          grid_barrier(&ctl->bar_ef, bar, &ctl->bar_err);
+          const bool f2 = block_select_top<kThreads>(ctl->hist_s2, 256, tgt - above1, b2, above2, s_hist);
+          Lkey = (b1 << kShift1) | ((f2 ? b2 : 0u) << 11);
+        } else {
+          Lkey = 0u;
+        }
+      } else {
+        Lkey = 0u;
+      }
       EF_MARK(2);
-      if (blockIdx.x == 0 && tid == 0) ctl->L_digit = Ld;
-      Lkey = Ld << kShift1;
+      if (blockIdx.x == 0 && tid == 0) ctl->Lkey = Lkey;
     } else if (opts & 4) {  // every element is a candidate
-      if (blockIdx.x == 0 && tid == 0) ctl->L_digit = 0;
+      if (blockIdx.x == 0 && tid == 0) ctl->Lkey = 0;
       Lkey = 0u;
     } else {
-      Lkey = (*(volatile unsigned*)&ctl->L_digit) << kShift1;
+      Lkey = *(volatile unsigned*)&ctl->Lkey;
     }
   }
 
@@ -756,7 +781,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
     unsigned bin;
     unsigned long long above;
     block_select_top<kSelThreads>(ctl->hist_fb, kBins1, fb_target, bin, above, s_h);
-    if (blockIdx.x == 0 && tid == 0) ctl->L_digit = bin;
+    if (blockIdx.x == 0 && tid == 0) ctl->Lkey = bin << kShift1;
     const unsigned Lk = bin << kShift1;
     for (unsigned c = c0 + warp; c < c1; c += kSelWarps) {  // warp per chunk, rows of 32
       const uint64_t base = (uint64_t)c << kChunkShift;
@@ -896,7 +921,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
     // inc/compress.hpp:84-101).  A probe t is counted over the candidates
     // (|x| >= t <=> key(x) >= key(t rounded up to float)); a probe below the
     // candidate bound has count >= M > k, so it moves lo without counting.
-    const unsigned Lkey = __ldcg(&ctl->L_digit) << kShift1;
+    const unsigned Lkey = __ldcg(&ctl->Lkey);
     unsigned long long mk = 0;
     if (dense)
       visit_warp([](int, unsigned) {}, [&](float x, bool valid, int, unsigned, unsigned) {
