@@ -883,7 +883,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
   };
   // warp mode: f(x, valid, u) for 4 chunks x 2 rounds of 32 values at a time
   // (all lanes call f: warp-synchronous helpers may be used inside)
-  auto visit_warp = [&](auto&& begin_chunk, auto&& f) {
+  auto visit_warp = [&](auto&& begin_chunk, auto&& f, bool with_idx = false) {
     for (unsigned cb = warp; cb < nc; cb += kSelWarps * 4) {
       unsigned n[4];
       unsigned maxn = 0;
@@ -896,19 +896,22 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
       }
       for (unsigned r0 = 0; r0 < maxn; r0 += 64) {
         float x[4][2];
+        unsigned id[4][2];  // candidate indices (emission), loaded with the values
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
           for (int rr = 0; rr < 2; ++rr) {
             const unsigned p = r0 + rr * 32 + lane;
-            x[u][rr] = p < n[u] ? val_at(cb + u * kSelWarps, p) : 0.f;
+            const unsigned c = cb + u * kSelWarps;
+            x[u][rr] = p < n[u] ? val_at(c, p) : 0.f;
+            id[u][rr] = with_idx && p < n[u] ? __ldcg(gidx + ((uint64_t)c << kChunkShift) + p) : 0u;
           }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
           for (int rr = 0; rr < 2; ++rr) {
             const unsigned p = r0 + rr * 32 + lane;
-            if (r0 + rr * 32 < n[u]) f(x[u][rr], p < n[u], u, cb + u * kSelWarps, r0 + rr * 32);
+            if (r0 + rr * 32 < n[u]) f(x[u][rr], p < n[u], u, cb + u * kSelWarps, r0 + rr * 32, id[u][rr]);
           }
       }
     }
@@ -924,7 +927,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
     const unsigned Lkey = __ldcg(&ctl->Lkey);
     unsigned long long mk = 0;
     if (dense)
-      visit_warp([](int, unsigned) {}, [&](float x, bool valid, int, unsigned, unsigned) {
+      visit_warp([](int, unsigned) {}, [&](float x, bool valid, int, unsigned, unsigned, unsigned) {
         if (valid) mk = max(mk, (unsigned long long)key_of(x));
       });
     else
@@ -944,7 +947,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
       }
       unsigned long long cnt = 0;
       if (dense)
-        visit_warp([](int, unsigned) {}, [&](float x, bool valid, int, unsigned, unsigned) {
+        visit_warp([](int, unsigned) {}, [&](float x, bool valid, int, unsigned, unsigned, unsigned) {
           cnt += __popc(__ballot_sync(0xffffffffu, valid && key_of(x) >= tk)) * (lane == 0);
         });
       else
@@ -985,11 +988,9 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
     const unsigned pf = prefix, dm = (unsigned)nb - 1;
     if (dense) {
       visit_warp([](int, unsigned) {},
-                 [&](float x, bool valid, int, unsigned, unsigned) {
+                 [&](float x, bool valid, int, unsigned, unsigned, unsigned) {
                    const unsigned key = key_of(x);
-                   const unsigned bin = valid && (key >> as) == pf ? ((key >> sh) & dm) : 0xffffffffu;
-                   const unsigned m = __match_any_sync(0xffffffffu, bin);
-                   if (bin != 0xffffffffu && (m & lt) == 0) atomicAdd(&s_h[bin], __popc(m));
+                   if (valid && (key >> as) == pf) atomicAdd(&s_h[(key >> sh) & dm], 1u);
                  });
     } else {
       visit_thread([&](float x) {
@@ -1025,7 +1026,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
           gt[u] = 0;
           eq[u] = 0;
         },
-        [&](float x, bool valid, int u, unsigned c, unsigned r) {
+        [&](float x, bool valid, int u, unsigned c, unsigned r, unsigned) {
           const unsigned key = key_of(x);
           gt[u] += __popc(__ballot_sync(0xffffffffu, valid && key > T));
           eq[u] += __popc(__ballot_sync(0xffffffffu, valid && key == T));
@@ -1110,7 +1111,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
                                     : (unsigned)min((unsigned long long)(s_ge[c] & 0xFFFFu), needT - eq_pre);
           tseen[u] = 0;
         },
-        [&](float x, bool valid, int u, unsigned c, unsigned r) {
+        [&](float x, bool valid, int u, unsigned c, unsigned r, unsigned id) {
           const unsigned key = key_of(x);
           const bool is_eq = valid && key == T;
           const unsigned eqb = __ballot_sync(0xffffffffu, is_eq);
@@ -1118,13 +1119,14 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
           const unsigned sb = __ballot_sync(0xffffffffu, sel);
           if (sel) {
             const unsigned long long pos = o[u] + __popc(sb & lt);
-            out_idx[pos] = __ldcg(gidx + ((uint64_t)c << kChunkShift) + r + lane) + mode.idx_base;
+            out_idx[pos] = id + mode.idx_base;
             out_val[pos] = x;
             acc = fma((double)x, (double)x, acc);
           }
           o[u] += __popc(sb);
           tseen[u] += __popc(eqb);
-        });
+        },
+        true);
   } else {
     // the block's selected pairs form one contiguous output range: assemble
     // it in shared memory when it fits, then write it out coalesced
