@@ -307,6 +307,10 @@ int fc_stream(fc_ctx* ctx, void** stream_out);
  * for the roofline computation in bench.py.  Returns mean ms per launch
  * since the last reset and the number of launches timed. */
 int fc_ef_kernel_timing(fc_ctx* ctx, double* mean_ms, uint64_t* launches, int reset);
+/* Time only every period-th EF launch (default 1).  The event pair around
+ * the kernel keeps it from overlapping its neighbours' launch (programmatic
+ * dependent launch), so sampling keeps the measurement off most steps. */
+int fc_set_ef_timing_period(fc_ctx* ctx, int period);
 /* Diagnostics (roofline calibration, not the hot path): mean device ms of one
  * kernel on worker 0's buffers.  which: 0/1/2 reference triad b += a at
  * 3/4/8 blocks per SM, 3 write-only fill, 4 EF, 5 EF + candidate emission,

@@ -138,6 +138,7 @@ def _load() -> C.CDLL:
         "fc_join": ([P], i),
         "fc_stream": ([P, C.POINTER(P)], i),
         "fc_ef_kernel_timing": ([P, C.POINTER(d), C.POINTER(u64), i], i),
+        "fc_set_ef_timing_period": ([P, i], i),
         "fc_diag_kernel_ms": ([P, i, i, C.POINTER(d)], i),
         "fc_diag_select_phases": ([P, i, C.POINTER(u64)], i),
         "fc_diag_collective_ms": ([P, i, u64, i, C.POINTER(d)], i),
@@ -175,7 +176,7 @@ EXPORTS = [
     "fc_set_grad", "fc_grad_ptr", "fc_fill_synthetic", "fc_set_residual", "fc_get_residual",
     "fc_residual_ptr", "fc_reset_residuals", "fc_get_aggregate", "fc_aggregate_ptr",
     "fc_get_topk", "fc_get_worker_stats", "fc_snapshot", "fc_restore", "fc_artopk_step",
-    "fc_ag_step", "fc_set_layer_map", "fc_set_threshold_rounds", "fc_dense_step", "fc_topk_exact", "fc_sync", "fc_join", "fc_stream", "fc_ef_kernel_timing",
+    "fc_ag_step", "fc_set_layer_map", "fc_set_threshold_rounds", "fc_dense_step", "fc_topk_exact", "fc_sync", "fc_join", "fc_stream", "fc_ef_kernel_timing", "fc_set_ef_timing_period",
     "fc_diag_kernel_ms", "fc_diag_select_phases", "fc_diag_collective_ms", "fc_diag_ef_blocks",
     "fc_cost_primitives", "fc_select_collective", "fc_prefer", "fc_crossover_cr",
     "fc_derive_m_from_ag",

@@ -151,6 +151,7 @@ struct fc_ctx {
   std::vector<cudaEvent_t> ev_pool;
   double ef_ms_sum = 0.0;
   uint64_t ef_n = 0;
+  unsigned ef_period = 1, ef_calls = 0;  // time every ef_period-th EF launch
 
   template <typename T>
   int alloc(T** p, uint64_t count) {
@@ -283,7 +284,7 @@ int run_ef(fc_ctx* c, int i, uint64_t k, bool topk) {
   fcb::Ctl* next = take_ctl(w);
   TRY(wait_grad(c, i));
   cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (i == 0 && c->timing) {
+  if (i == 0 && c->timing && (c->ef_calls++ % c->ef_period) == 0) {
     e0 = c->take_event();
     e1 = c->take_event();
     cudaEventRecord(e0, c->stream);
@@ -1011,6 +1012,13 @@ int fc_join(fc_ctx* c) {
 int fc_stream(fc_ctx* c, void** stream_out) {
   if (!c || !stream_out) return fail(FC_ERR_INVALID_ARGUMENT, "null argument");
   *stream_out = c->stream;
+  return FC_OK;
+}
+
+int fc_set_ef_timing_period(fc_ctx* c, int period) {
+  if (!c || period < 1) return fail(FC_ERR_INVALID_ARGUMENT, "period must be >= 1");
+  c->ef_period = (unsigned)period;
+  c->ef_calls = 0;
   return FC_OK;
 }
 

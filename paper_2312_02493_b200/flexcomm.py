@@ -291,6 +291,10 @@ class Cluster:
         check(lib.fc_stream(self._ctx, C.byref(p)))
         return p.value or 0
 
+    def set_ef_timing_period(self, period: int) -> None:
+        """Time every period-th EF launch only (fc_set_ef_timing_period)."""
+        check(lib.fc_set_ef_timing_period(self._ctx, int(period)))
+
     def ef_kernel_timing(self, reset: bool = False):
         ms, n = C.c_double(), C.c_uint64()
         check(lib.fc_ef_kernel_timing(self._ctx, C.byref(ms), C.byref(n), int(reset)))
