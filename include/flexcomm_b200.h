@@ -319,7 +319,8 @@ int fc_diag_kernel_ms(fc_ctx* ctx, int which, int iters, double* ms_out);
 /* Diagnostics: %globaltimer (ns) at the select kernel's phase boundaries of
  * the last step (start, staged, digit 1/2/3 resolved, counted, emitted, end),
  * then the EF kernel's (start, sample barrier passed, bound derived, end of
- * block 0's stream): out12 holds 12 values. */
+ * block 0's stream), then two EF marks (sample histogrammed, flushed): out12
+ * holds 14 values. */
 int fc_diag_select_phases(fc_ctx* ctx, int worker, uint64_t* out12);
 /* Diagnostics: %globaltimer (ns) at the start and end of every EF block of the
  * last step (2 x grid values, grid = number of SMs). */

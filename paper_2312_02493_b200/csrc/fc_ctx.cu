@@ -1136,7 +1136,7 @@ int fc_diag_select_phases(fc_ctx* c, int worker, uint64_t* out12) {
   if (!out12) return fail(FC_ERR_INVALID_ARGUMENT, "null output");
   CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
-  CUDA_TRY(cudaMemcpy(out12, &c->w[worker].ctl->tphase[0], 12 * sizeof(uint64_t),
+  CUDA_TRY(cudaMemcpy(out12, &c->w[worker].ctl->tphase[0], 14 * sizeof(uint64_t),
                       cudaMemcpyDeviceToHost));
   return FC_OK;
 }

@@ -52,6 +52,7 @@ struct Ctl {
   double ge_norm2, topk_norm2, kept_norm2;
   unsigned long long tphase[8];  // %globaltimer at k_select phase boundaries (diagnostics)
   unsigned long long tphase_ef[4];  // ... and at k_ef's (start, sampled, bound, end)
+  unsigned long long tphase_ef2[4];  // k_ef: sample loaded, local histogram flushed, (spare)
   unsigned hist_s[kBins1];   // sample histogram (digit 1)
   unsigned hist_s2[256];     // sample histogram of bits 18..11 inside the bound's bucket
   unsigned hist1[kBins1];    // candidate histogram, key bits 30..19 (k_select)

@@ -450,8 +450,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
       for (unsigned q = q0 + qstride; q < (unsigned)kSamples; q += qstride)  // small grids only
         atomicAdd(&s_hist[key_of(sample_at(q)) >> kShift1], 1u);
       __syncthreads();
+      if (blockIdx.x == 0 && threadIdx.x == 0) ctl->tphase_ef2[0] = gtimer();
       for (int b = tid; b < kBins1; b += kThreads)
         if (s_hist[b]) atomicAdd(&ctl->hist_s[b], s_hist[b]);
+      if (blockIdx.x == 0 && threadIdx.x == 0) ctl->tphase_ef2[1] = gtimer();
       unsigned bar = 0;
       grid_barrier(&ctl->bar_ef, bar, &ctl->bar_err);
       EF_MARK(1);
