@@ -1214,7 +1214,7 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
   // values in its exchange buffer (parity of this step's epoch), the other
   // ranks fetch the list and gather, and every rank's decode sums the
   // contributions in rank order straight from peer memory
-  const bool p2p_star = c->p2p && mode == FC_STAR && N > 1;
+  const bool p2p_star = c->p2p && N > 1;  // STAR and VAR
   const unsigned long long epoch = p2p_star ? ++c->epoch : 0;
   const int par = (int)(epoch & 1);
 
@@ -1233,6 +1233,7 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
       fcb::SelectMode m;
       m.publish = c->pb.flags[c->rank];
       m.epoch = epoch;
+      m.publish_contrib = mode == FC_STAR;  // VAR: contributions come from the gather
       m.err = &c->w[i].ctl->bar_err;
       TRY(run_select(c, i, k, nullptr, m, c->pb.list[c->rank] + par * c->pb.kmax,
                      c->pb.contrib[c->rank] + par * c->pb.kmax));
@@ -1246,6 +1247,7 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
   //     (select_var, inc/artopk.hpp:35-48)
   if (mode == FC_VAR && N == 1) sel = 0;  // argmax over one worker
   const bool var_device = mode == FC_VAR && N > 1 && c->nccl;  // winner found on the device
+  const bool p2p_var = p2p_star && mode == FC_VAR;
   c->sel_on_device = var_device;
   if (mode == FC_VAR && N > 1 && !c->nccl) {
     for (int i = 0; i < N; ++i)
@@ -1264,9 +1266,12 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
   const unsigned* own_bounds = nullptr;  // chunk bounds of bsrc, when a local select wrote them
   if (p2p_star) {
     Worker& w = c->w[0];
-    if (c->rank != sel)
+    if (p2p_var)  // every rank: winner on the device, its list fetched, own g_e gathered
+      fcb::launch_fetch_gather(c->pb, -1, par, epoch, w.ge, k, c->bounds, c->nch, w.ctl, w.ws.g_part,
+                               c->dsel, c->stream);
+    else if (c->rank != sel)
       fcb::launch_fetch_gather(c->pb, sel, par, epoch, w.ge, k, c->bounds, c->nch, w.ctl, w.ws.g_part,
-                               c->stream);
+                               nullptr, c->stream);
     else
       w.kept_is_topk = true;
     LAUNCHED();

@@ -135,6 +135,7 @@ struct SelectMode {
   // epoch, system-scope release) for the peers that read it over NVLink
   unsigned long long* publish = nullptr;
   unsigned long long epoch = 0;
+  bool publish_contrib = true;  // the values are this rank's contribution (STAR's selected rank)
   unsigned* err = nullptr;  // (wait timeouts)
 };
 int launch_select(uint64_t k, Ctl* ctl, const ChunkWs& w, const float* ef_out, uint64_t G,
@@ -146,12 +147,14 @@ void launch_sum_fixed(const double* parts, uint64_t n, double* out, cudaStream_t
 void launch_sumsq_fixed(const float* v, uint64_t n, double* out, cudaStream_t s);
 // diagnostics: %globaltimer marks of the last decode (start, end)
 void read_tdiag(unsigned long long* out8);
-// STAR over peer memory, non-selected ranks: wait for the selected rank's list
-// (epoch), copy it (own list, parity par), gather this rank's g_e at it into
-// its contribution list, write the decode's chunk bounds, publish the
-// contribution (flags[1] = epoch).  err: set on a wait timeout.
+// Peer memory, STAR non-selected ranks (sel >= 0) or every rank in VAR (sel <
+// 0: the winner is the argmax of the published ||top-k||^2, written to
+// *sel_out): wait for the selected list (epoch), copy it (own list, parity
+// par), gather this rank's g_e at it into its contribution list, write the
+// decode's chunk bounds, publish the contribution (flags[1] = epoch).
 void launch_fetch_gather(const PeerBufs& pb, int sel, int par, unsigned long long epoch, const float* ge,
-                         uint64_t k, unsigned* bounds, uint64_t nch, Ctl* ctl, double* part, cudaStream_t s);
+                         uint64_t k, unsigned* bounds, uint64_t nch, Ctl* ctl, double* part, int* sel_out,
+                         cudaStream_t s);
 // Reduce-scatter over peer memory: once every rank published its
 // contribution (`epoch`), rank r sums slice r of the list in rank order
 // (collectives.hpp:82-87, /divisor when divide) from all ranks' lists into

@@ -1205,16 +1205,19 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
   if (bounds_out && blockIdx.x == 0 && tid == 0) bounds_out[nch] = (unsigned)kout;
   SEL_MARK(6);
   grid_barrier(&ctl->bar_sel, bar, &ctl->bar_err);
-  if (mode.publish && blockIdx.x == 0 && tid == 0) {  // every block's output is in (barrier)
-    __threadfence_system();
-    st_release_sys(mode.publish, mode.epoch);
-    st_release_sys(mode.publish + 1, mode.epoch);
-  }
   pdl_trigger();
   SEL_MARK(7);
   if (blockIdx.x == 0) {
     const double tot = block_sum_array<kSelThreads>(w.bnorm, gridDim.x, s_dred);
-    if (tid == 0) ctl->topk_norm2 = tot;
+    if (tid == 0) {
+      ctl->topk_norm2 = tot;
+      if (mode.publish) {  // every block's output is in (barrier); ||top-k||^2 with it (VAR)
+        reinterpret_cast<double*>(mode.publish)[4] = tot;
+        __threadfence_system();
+        st_release_sys(mode.publish, mode.epoch);
+        if (mode.publish_contrib) st_release_sys(mode.publish + 1, mode.epoch);
+      }
+    }
   }
 }
 
@@ -1363,11 +1366,35 @@ __global__ void __launch_bounds__(kThreads) k_fetch_gather(PeerBufs pb, int sel,
                                                            unsigned long long epoch,
                                                            const float* __restrict__ ge, uint64_t k,
                                                            unsigned* __restrict__ bounds, uint64_t nch,
-                                                           Ctl* __restrict__ ctl, double* __restrict__ part) {
+                                                           Ctl* __restrict__ ctl, double* __restrict__ part,
+                                                           int* __restrict__ sel_out) {
   pdl_wait();
   __shared__ double s_red[kThreads / 32];
-  if (threadIdx.x == 0) wait_epoch(pb.flags[sel], epoch, &ctl->bar_err);
-  __syncthreads();
+  __shared__ int s_sel;
+  if (sel < 0) {
+    // VAR (select_var, artopk.hpp:35-48): every rank published its list and
+    // ||top-k||^2; the winner is the argmax (strict >, ties to the lowest rank)
+    if (threadIdx.x < (unsigned)pb.n) wait_epoch(pb.flags[threadIdx.x], epoch, &ctl->bar_err);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int best = 0;
+      double bs = __ldcv(reinterpret_cast<const double*>(pb.flags[0]) + 4);
+      for (int r = 1; r < pb.n; ++r) {
+        const double x = __ldcv(reinterpret_cast<const double*>(pb.flags[r]) + 4);
+        if (x > bs) {
+          bs = x;
+          best = r;
+        }
+      }
+      s_sel = best;
+      if (blockIdx.x == 0 && sel_out) *sel_out = best;
+    }
+    __syncthreads();
+    sel = s_sel;
+  } else {
+    if (threadIdx.x == 0) wait_epoch(pb.flags[sel], epoch, &ctl->bar_err);
+    __syncthreads();
+  }
   const unsigned* src = pb.list[sel] + (uint64_t)par * pb.kmax;  // the selected rank's list (NVLink)
   unsigned* mine = pb.list[pb.rank] + (uint64_t)par * pb.kmax;
   float* contrib = pb.contrib[pb.rank] + (uint64_t)par * pb.kmax;
@@ -1410,11 +1437,12 @@ __global__ void __launch_bounds__(kThreads) k_fetch_gather(PeerBufs pb, int sel,
 }
 
 void launch_fetch_gather(const PeerBufs& pb, int sel, int par, unsigned long long epoch, const float* ge,
-                         uint64_t k, unsigned* bounds, uint64_t nch, Ctl* ctl, double* part, cudaStream_t s) {
+                         uint64_t k, unsigned* bounds, uint64_t nch, Ctl* ctl, double* part, int* sel_out,
+                         cudaStream_t s) {
   int grid = (int)std::min<uint64_t>((k + kThreads * kGatherUnroll - 1) / (kThreads * kGatherUnroll),
                                      (uint64_t)num_sms() * 8);
   if (grid < 1) grid = 1;
-  launch_pdl(k_fetch_gather, grid, kThreads, 0, s, pb, sel, par, epoch, ge, k, bounds, nch, ctl, part);
+  launch_pdl(k_fetch_gather, grid, kThreads, 0, s, pb, sel, par, epoch, ge, k, bounds, nch, ctl, part, sel_out);
   count_launch();
 }
 

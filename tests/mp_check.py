@@ -98,10 +98,10 @@ def main() -> int:
                     scale = np.abs(base).sum(axis=0) / env.world
                     if (kind != "dense"):
                         scale = np.where(ref != 0, scale, 0)
-                    if kind == "star" and p2p and not np.array_equal(aggs[r].view(np.uint32),
+                    if kind in ("star", "var") and p2p and not np.array_equal(aggs[r].view(np.uint32),
                                                                        ref.view(np.uint32)):
                         # rank-ordered sums over peer memory: bit-exact
-                        failures.append(f"step {s} star: peer-exchange aggregate on rank {r} not bit-exact")
+                        failures.append(f"step {s} {kind}: peer-exchange aggregate on rank {r} not bit-exact")
                     err = np.abs(aggs[r].astype(np.float64) - ref)
                     if not np.all(err <= 1e-5 * scale + 1e-30):
                         failures.append(f"step {s} {kind}: aggregate on rank {r} off by {err.max():.3g}")
