@@ -625,7 +625,6 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
     TRY(c->alloc(&s.bnorm, 4096));
     TRY(c->alloc(&s.cand_idx, (uint64_t)nch << fcb::kChunkShift));
     TRY(c->alloc(&s.cand_val, (uint64_t)nch << fcb::kChunkShift));
-    TRY(c->alloc(&s.ef_part, ef_grid));
     TRY(c->alloc(&s.cnorm, 2 * (uint64_t)nch));  // [full EF pass | layer passes]
     TRY(c->alloc(&s.g_part, 4096));
     TRY(c->alloc(&s.tblk, 2 * (uint64_t)ef_grid));

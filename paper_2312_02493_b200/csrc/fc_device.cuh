@@ -38,7 +38,7 @@ struct Ctl {
   unsigned Lkey;          // candidate bound: every element with key >= Lkey
   unsigned fallback;      // 1 => sampled bound missed, full re-emission ran
   unsigned cand_count;    // M: candidates emitted
-  unsigned done_sample, done_ef, done_fbh, done_fbe, done_gather, done_red;
+  unsigned done_gather, done_red;  // last-block counters
   unsigned ef_next;       // EF work queue: next chunk to hand out
   unsigned bar_ef, bar_sel;  // software grid barriers of the EF / select kernels
   unsigned bar_err;       // a grid barrier timed out (blocks not co-resident)
@@ -70,7 +70,6 @@ struct ChunkWs {
   double* bnorm;              // k_select: per-block sum of squares of selected values
   unsigned* cand_idx;
   float* cand_val;
-  double* ef_part;            // (unused)
   double* cnorm;              // per chunk: sum of g_e^2 (fp64), reduced in chunk order on demand
   double* g_part;             // one per gather block
   unsigned long long* tblk;   // diagnostics: %globaltimer at each EF block's start and end
