@@ -319,11 +319,16 @@ int fc_diag_kernel_ms(fc_ctx* ctx, int which, int iters, double* ms_out);
 /* Diagnostics: %globaltimer (ns) at the select kernel's phase boundaries of
  * the last step (start, staged, digit 1/2/3 resolved, counted, emitted, end),
  * then the EF kernel's (start, sample barrier passed, bound derived, end of
- * block 0's stream), then two EF marks (sample histogrammed, flushed): out12
- * holds 14 values. */
+ * block 0's stream), then two EF marks (sample histogrammed, flushed), then two
+ * select emission marks (output base known, pairs assembled): out12 holds 16
+ * values. */
 int fc_diag_select_phases(fc_ctx* ctx, int worker, uint64_t* out12);
 /* Diagnostics: %globaltimer (ns) at the start and end of every EF block of the
- * last step (2 x grid values, grid = number of SMs). */
+ * last step (2 x grid values, grid = number of SMs), followed (as n allows) by
+ * the last decode's start and end and the peer exchange's marks: fetch-gather
+ * wait start, gather start, contribution published; decode wait start;
+ * reduce-slice start, slice published (8 more values, stale for kernels the
+ * last step did not run), then the peer gather's per-block (start, end). */
 int fc_diag_ef_blocks(fc_ctx* ctx, int worker, uint64_t* out, int n);
 /* Diagnostics (NVLink calibration): mean device ms of one NCCL collective on
  * this context's communicators, all ranks calling alike.  which: 0 broadcast,

@@ -6,10 +6,12 @@ is missing or cannot be loaded, importing this module raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libfc_b200.so"
+# FC_LIB_PATH: an experimental build of the same library (tools/variants.py)
+LIB_PATH = Path(os.environ["FC_LIB_PATH"]) if os.environ.get("FC_LIB_PATH") else _PKG / "libfc_b200.so"
 
 FC_OK = 0
 FC_ERR_INVALID_ARGUMENT = 1

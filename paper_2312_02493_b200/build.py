@@ -47,25 +47,28 @@ def needs_build() -> bool:
     return any(s.stat().st_mtime > t for s in SOURCES + HEADERS)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: Path | None = None,
+          defines: tuple[str, ...] = ()) -> Path:
+    if out is None and not force and not needs_build():
         return LIB
+    out = out or LIB
     nr = nccl_root()
     libdir = nr / "lib"
     cmd = [
         nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off", "-shared",
         "-Xptxas", "-v" if verbose else "-O3",
+        *[f"-D{d}" for d in defines],
         f"-I{ROOT / 'include'}", f"-I{nr / 'include'}",
         *[str(s) for s in SOURCES],
         f"-L{libdir}", "-l:libnccl.so.2", f"-Xlinker", f"-rpath={libdir}",
-        "-o", str(LIB),
+        "-o", str(out),
     ]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + res.stdout + res.stderr)
     if verbose:
         sys.stderr.write(res.stdout + res.stderr)
-    return LIB
+    return out
 
 
 if __name__ == "__main__":

@@ -77,6 +77,8 @@ struct Worker {
   unsigned* pack = nullptr;  // [idx k | val k], capacity 2*kmax
   float* contrib = nullptr;  // capacity kmax
   bool has_topk = false;
+  const float* kept_vals = nullptr;  // peer gather: the contribution whose ||.||^2 is the kept mass
+  uint64_t kept_k = 0;
   uint64_t topk_k = 0;
   const unsigned* topk_idx = nullptr;  // where the last select wrote its output
   const float* topk_val = nullptr;
@@ -586,7 +588,7 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
   TRY(c->alloc(&c->pack_all, N * 2 * c->kmax));
   TRY(c->alloc(&c->contrib_all, N * c->kmax));
   const uint64_t nl = std::max<uint64_t>(N, (uint64_t)c->world);
-  TRY(c->alloc(&c->bounds, nl * (c->nch + 1)));
+  TRY(c->alloc(&c->bounds, nl * (c->nch + 1) + 4));  // (+4: vector pulls of a padded row)
   TRY(c->alloc(&c->zmaps, N * c->nch * 32));
   TRY(c->alloc(&c->agg_support, c->kmax));
   CUDA_TRY(cudaMemsetAsync(c->zmaps, 0, N * c->nch * 32 * sizeof(unsigned), c->stream));
@@ -663,7 +665,9 @@ int setup_p2p(fc_ctx* c) {
   const uint64_t list_b = align_up(2 * kst * sizeof(unsigned), 256);
   const uint64_t contrib_b = align_up(2 * kst * sizeof(float), 256);
   const uint64_t bounds_b = align_up(2 * nbs * sizeof(unsigned), 256);
-  const uint64_t total = list_b + 2 * contrib_b + bounds_b + 256;
+  const uint64_t inbox_b = align_up(N * 2 * kst * sizeof(float), 256);
+  const uint64_t box_b = align_up(N * 8 * sizeof(unsigned long long), 256);
+  const uint64_t total = list_b + 2 * contrib_b + inbox_b + bounds_b + box_b;
   CUDA_TRY(cudaMalloc(&c->xbuf, total));
   CUDA_TRY(cudaMemset(c->xbuf, 0, total));
   int ok = 1;
@@ -711,11 +715,13 @@ int setup_p2p(fc_ctx* c) {
   c->pb.nb = c->nch + 1;
   c->pb.nbs = nbs;
   for (int r = 0; r < N; ++r) {
-    c->pb.list[r] = reinterpret_cast<unsigned*>(base[r]);
-    c->pb.contrib[r] = reinterpret_cast<float*>(base[r] + list_b);
-    c->pb.reduced[r] = reinterpret_cast<float*>(base[r] + list_b + contrib_b);
-    c->pb.bounds[r] = reinterpret_cast<unsigned*>(base[r] + list_b + 2 * contrib_b);
-    c->pb.flags[r] = reinterpret_cast<unsigned long long*>(base[r] + list_b + 2 * contrib_b + bounds_b);
+    unsigned char* x = base[r];
+    c->pb.list[r] = reinterpret_cast<unsigned*>(x);
+    c->pb.contrib[r] = reinterpret_cast<float*>(x + list_b);
+    c->pb.reduced[r] = reinterpret_cast<float*>(x + list_b + contrib_b);
+    c->pb.inbox[r] = reinterpret_cast<float*>(x + list_b + 2 * contrib_b);
+    c->pb.bounds[r] = reinterpret_cast<unsigned*>(x + list_b + 2 * contrib_b + inbox_b);
+    c->pb.box[r] = reinterpret_cast<unsigned long long*>(x + list_b + 2 * contrib_b + inbox_b + bounds_b);
   }
   c->p2p = true;
   return FC_OK;
@@ -902,6 +908,8 @@ int fc_get_worker_stats(fc_ctx* c, int worker, fc_worker_stats* out) {
   Worker& wk = c->w[worker];
   // ||g_e||^2 of the last EF pass, summed over its per-chunk partials in chunk order
   fcb::launch_sum_fixed(wk.ws.cnorm, c->nch, &wk.ctl->ge_norm2, c->stream);
+  // ||kept||^2 of a peer gather: over its contribution list, in list order
+  if (wk.kept_vals) fcb::launch_sumsq_fixed(wk.kept_vals, wk.kept_k, &wk.ctl->kept_norm2, c->stream);
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   fcb::Ctl h;
   CUDA_TRY(cudaMemcpy(&h, wk.ctl, offsetof(fcb::Ctl, hist_s), cudaMemcpyDeviceToHost));
@@ -1135,7 +1143,7 @@ int fc_diag_select_phases(fc_ctx* c, int worker, uint64_t* out12) {
   if (!out12) return fail(FC_ERR_INVALID_ARGUMENT, "null output");
   CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
-  CUDA_TRY(cudaMemcpy(out12, &c->w[worker].ctl->tphase[0], 14 * sizeof(uint64_t),
+  CUDA_TRY(cudaMemcpy(out12, &c->w[worker].ctl->tphase[0], 16 * sizeof(uint64_t),
                       cudaMemcpyDeviceToHost));
   return FC_OK;
 }
@@ -1147,13 +1155,18 @@ int fc_diag_ef_blocks(fc_ctx* c, int worker, uint64_t* out, int n) {
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   const int m = std::min<int>(n, 2 * (int)c->w[worker].ws.ef_grid);
   CUDA_TRY(cudaMemcpy(out, c->w[worker].ws.tblk, m * sizeof(uint64_t), cudaMemcpyDeviceToHost));
-  // followed by the last AR decode's start and end marks
+  // followed by the last AR decode's start and end marks, then (n >= m + 8)
+  // the peer exchange's: fetch-gather wait start / start / flag published,
+  // decode wait start, reduce-slice start / flag published
   if (n >= m + 2) {
     unsigned long long t[8];
     fcb::read_tdiag(t);
-    out[m] = t[0];
-    out[m + 1] = t[1];
+    for (int i = 0; i < 8 && m + i < n; ++i) out[m + i] = t[i];
   }
+  // then the peer gather's per-block (start, end) marks
+  if (n > m + 8)
+    CUDA_TRY(cudaMemcpy(out + m + 8, c->w[worker].ws.g_part, std::min<int>(n - m - 8, 4096) * sizeof(uint64_t),
+                        cudaMemcpyDeviceToHost));
   return FC_OK;
 }
 
@@ -1208,6 +1221,7 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
   for (auto& w : c->w) {
     w.has_topk = false;
     w.kept_is_topk = false;
+    w.kept_vals = nullptr;
   }
   // STAR over peer memory: the selected rank's select publishes its list and
   // values in its exchange buffer (parity of this step's epoch), the other
@@ -1230,12 +1244,13 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
     if (!topk) continue;
     if (p2p_star) {
       fcb::SelectMode m;
-      m.publish = c->pb.flags[c->rank];
+      m.publish = true;
+      m.pb = c->pb;
       m.epoch = epoch;
       m.publish_contrib = mode == FC_STAR;  // VAR: contributions come from the gather
       m.err = &c->w[i].ctl->bar_err;
       TRY(run_select(c, i, k, nullptr, m, c->pb.list[c->rank] + par * c->pb.kmax,
-                     c->pb.contrib[c->rank] + par * c->pb.kmax));
+                     c->pb.contrib[c->rank] + par * c->pb.kmax, c->pb.bounds[c->rank] + par * c->pb.nbs));
     } else {
       TRY(run_select(c, i, k));
     }
@@ -1265,17 +1280,19 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
   const unsigned* own_bounds = nullptr;  // chunk bounds of bsrc, when a local select wrote them
   if (p2p_star) {
     Worker& w = c->w[0];
-    if (p2p_var)  // every rank: winner on the device, its list fetched, own g_e gathered
-      fcb::launch_fetch_gather(c->pb, -1, par, epoch, w.ge, k, c->bounds, c->nch, w.ctl, w.ws.g_part,
-                               c->dsel, c->stream);
-    else if (c->rank != sel)
-      fcb::launch_fetch_gather(c->pb, sel, par, epoch, w.ge, k, c->bounds, c->nch, w.ctl, w.ws.g_part,
-                               nullptr, c->stream);
-    else
+    if (p2p_var || c->rank != sel) {  // VAR: every rank (winner found on the device)
+      fcb::launch_fetch_gather(c->pb, p2p_var ? -1 : sel, par, epoch, w.ge, k, c->bounds, c->nch, w.ctl,
+                               p2p_var ? c->dsel : nullptr, reinterpret_cast<unsigned long long*>(w.ws.g_part),
+                               c->stream);
+      w.kept_vals = c->pb.contrib[c->rank] + par * c->pb.kmax;  // ||kept||^2 on demand
+      w.kept_k = k;
+      own_bounds = c->bounds;  // the selected list's bounds, pulled
+    } else {
       w.kept_is_topk = true;
+      own_bounds = c->pb.bounds[c->rank] + par * c->pb.nbs;  // written by the local select
+    }
     LAUNCHED();
     bsrc = c->pb.list[c->rank] + par * c->pb.kmax;  // local copy of the selected list
-    own_bounds = c->bounds;
   } else if (c->nccl && N == 1) {
     // a single rank: broadcast and allreduce are identities
     Worker& w = c->w[0];
@@ -1353,7 +1370,9 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
     // the slice's owner: ring-like NVLink traffic, rank-ordered sums
     // (two ranks: the decode sums both contributions directly, one fewer launch)
     const bool rs = N > 2;
-    if (rs) fcb::launch_reduce_slice(c->pb, par, epoch, k, op == FC_AVG, (float)N, c->w[0].ctl, c->stream);
+    if (rs)
+      fcb::launch_reduce_slice(c->pb, par, epoch, k, op == FC_AVG, (float)N, mode == FC_STAR ? sel : -1,
+                               c->w[0].ctl, c->stream);
     fcb::launch_decode_ar_peers(c->pb, par, epoch, bsrc, own_bounds, k, op == FC_AVG, (float)N, rs, aggw,
                                 c->G, c->zmaps, &c->w[0].ctl->bar_err, c->stream);
   } else if (incr_ok && c->agg_incr) {
@@ -1426,7 +1445,8 @@ int fc_ag_step(fc_ctx* c, double cr, int compressor, fc_step_stats* st) {
   for (int i = 0; i < c->n_local; ++i) {
     if (compressor == FC_EXACT && p2p_ag) {
       fcb::SelectMode m;
-      m.publish = c->pb.flags[c->rank];
+      m.publish = true;
+      m.pb = c->pb;
       m.epoch = epoch;
       TRY(run_select(c, i, k, nullptr, m, c->pb.list[c->rank] + par * c->pb.kmax,
                      c->pb.contrib[c->rank] + par * c->pb.kmax, c->pb.bounds[c->rank] + par * c->pb.nbs));

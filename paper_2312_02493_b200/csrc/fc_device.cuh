@@ -52,13 +52,14 @@ struct Ctl {
   double ge_norm2, topk_norm2, kept_norm2;
   unsigned long long tphase[8];  // %globaltimer at k_select phase boundaries (diagnostics)
   unsigned long long tphase_ef[4];  // ... and at k_ef's (start, sampled, bound, end)
-  unsigned long long tphase_ef2[4];  // k_ef: sample loaded, local histogram flushed, (spare)
+  unsigned long long tphase_ef2[4];  // k_ef: sample loaded, local histogram flushed; k_select: emission sub-phases
   unsigned hist_s[kBins1];   // sample histogram (digit 1)
   unsigned hist_s2[256];     // sample histogram of bits 18..11 inside the bound's bucket
   unsigned hist1[kBins1];    // candidate histogram, key bits 30..19 (k_select)
   unsigned hist_fb[kBins1];  // full histogram (fallback only)
   unsigned hist2[256];       // bits 18..11 of bucket-b1 candidates
   unsigned hist3[2048];      // bits 10..0
+  unsigned hist_w[4096];     // window histogram: key bits 30..11 relative to Lkey (k_select)
 };
 
 // Per-worker chunk workspace.  Chunk c's candidates occupy the fixed slot
@@ -107,11 +108,16 @@ constexpr int kMaxPeers = 8;
 struct PeerBufs {
   unsigned* list[kMaxPeers];
   float* contrib[kMaxPeers];
-  float* reduced[kMaxPeers];             // rank r: the reduced values of its slice of the list
+  float* reduced[kMaxPeers];             // rank r: the reduced values (every slice, pushed by its owner)
+  float* inbox[kMaxPeers];               // rank r: N x 2 parities of contributions pushed to it
   unsigned* bounds[kMaxPeers];           // AG: the chunk bounds of rank r's list (2 parities)
-  unsigned long long* flags[kMaxPeers];  // [0] list, [1] contribution, [2] reduced slice epochs
+  // rank r's mailbox, N x 8 words: box[r][src * 8 + slot] = the epoch src
+  // published for slot 0 (list), 1 (contribution), 2 (reduced slice); slot 4
+  // holds src's ||top-k||^2 (double).  Producers store into every rank's box,
+  // consumers poll their own (local) box.
+  unsigned long long* box[kMaxPeers];
   int n = 0, rank = 0;
-  uint64_t kmax = 0;                     // parity stride of list/contrib/reduced (multiple of 4)
+  uint64_t kmax = 0;                     // parity stride of list/contrib/reduced/inbox (multiple of 4)
   uint64_t nb = 0, nbs = 0;              // bounds entries (nchunks + 1), parity stride (multiple of 4)
 };
 // AG over peer memory: once every rank published `epoch`, copy every rank's
@@ -130,9 +136,11 @@ struct SelectMode {
   int rounds = 0;
   uint64_t kcap = 0;
   unsigned idx_base = 0;
-  // peer exchange: after the selection, publish it (flags[0] = flags[1] =
-  // epoch, system-scope release) for the peers that read it over NVLink
-  unsigned long long* publish = nullptr;
+  // peer exchange: after the selection, publish it (slot 0 -- and slot 1 --
+  // = epoch in every rank's mailbox, system-scope release) for the peers
+  // that read it over NVLink
+  bool publish = false;
+  PeerBufs pb;
   unsigned long long epoch = 0;
   bool publish_contrib = true;  // the values are this rank's contribution (STAR's selected rank)
   unsigned* err = nullptr;  // (wait timeouts)
@@ -150,19 +158,38 @@ void read_tdiag(unsigned long long* out8);
 // 0: the winner is the argmax of the published ||top-k||^2, written to
 // *sel_out): wait for the selected list (epoch), copy it (own list, parity
 // par), gather this rank's g_e at it into its contribution list, write the
-// decode's chunk bounds, publish the contribution (flags[1] = epoch).
+// decode's chunk bounds, and push the contribution to where it is summed
+// (two ranks: the peer's inbox, plus -- STAR -- the selected rank's values
+// pulled into this rank's inbox; N > 2: each slice into its owner's inbox),
+// then publish it (slot 1 = epoch).  Every later read is local.
+__device__ __host__ inline float* inbox_of(const PeerBufs& pb, int dst, int src, int par) {
+  return pb.inbox[dst] + ((uint64_t)src * 2 + (uint64_t)par) * pb.kmax;
+}
+// Owner of list position j when k positions are cut into n slices
+// [k r / n, k (r+1) / n).
+__device__ __host__ inline int slice_owner(uint64_t j, uint64_t k, int n) {
+  int r = (int)((j * (uint64_t)n) / k);
+  while (r + 1 < n && (k * (uint64_t)(r + 1)) / (uint64_t)n <= j) ++r;
+  while (r > 0 && (k * (uint64_t)r) / (uint64_t)n > j) --r;
+  return r;
+}
+// The selected list's chunk bounds are pulled from its exchange buffer
+// (pb.bounds, written by its select) into `bounds`.  ||kept||^2 is not
+// formed here (launch_sumsq_fixed over the contribution, on demand).
 void launch_fetch_gather(const PeerBufs& pb, int sel, int par, unsigned long long epoch, const float* ge,
-                         uint64_t k, unsigned* bounds, uint64_t nch, Ctl* ctl, double* part, int* sel_out,
-                         cudaStream_t s);
-// Reduce-scatter over peer memory: once every rank published its
+                         uint64_t k, unsigned* bounds, uint64_t nch, Ctl* ctl, int* sel_out,
+                         unsigned long long* tblk, cudaStream_t s);  // tblk: per-block marks (diagnostics)
+// Reduce-scatter over peer memory (N > 2): once every rank published its
 // contribution (`epoch`), rank r sums slice r of the list in rank order
-// (collectives.hpp:82-87, /divisor when divide) from all ranks' lists into
-// its reduced area and publishes it (flags[2]).
+// (collectives.hpp:82-87, /divisor when divide) from its inbox (the STAR
+// selected rank `star_sel`, which runs no gather, is read from its own
+// values), pushes the slice into every rank's reduced area and publishes it
+// (slot 2).
 void launch_reduce_slice(const PeerBufs& pb, int par, unsigned long long epoch, uint64_t k, int divide,
-                         float divisor, Ctl* ctl, cudaStream_t s);
-// Dense decode over peer memory once every rank published `epoch`: value j
-// is the rank-ordered sum of every rank's contribution (/divisor when divide)
-// or, with `reduced`, read from the reduced area of the rank owning slice j.
+                         float divisor, int star_sel, Ctl* ctl, cudaStream_t s);
+// Dense decode once every rank published `epoch`: value j is the sum of this
+// rank's contribution and its inbox copy of the peer's (two ranks; /divisor
+// when divide) or, with `reduced`, this rank's reduced area.  Local reads only.
 void launch_decode_ar_peers(const PeerBufs& pb, int par, unsigned long long epoch, const unsigned* idx,
                             const unsigned* bounds, uint64_t k, int divide, float divisor, bool reduced,
                             float* agg, uint64_t G, unsigned* zmap, unsigned* err, cudaStream_t s);

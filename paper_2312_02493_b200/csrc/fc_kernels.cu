@@ -231,8 +231,9 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned& target, un
   __syncthreads();
 }
 
-// System-scope epoch flags of the peer exchange (written by one GPU, polled
-// over NVLink by the others).  Waits are bounded like the grid barrier.
+// System-scope epoch flags of the peer exchange (written over NVLink by the
+// producer, polled locally by the consumer).  Waits are bounded like the grid
+// barrier.
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -251,6 +252,16 @@ __device__ __forceinline__ void wait_epoch(const unsigned long long* flag, unsig
       return;
     }
   }
+}
+
+// Mailbox protocol (PeerBufs::box): a producer stores its epoch into every
+// rank's box; a consumer polls only its own box (no polling over NVLink).
+__device__ __forceinline__ void publish_all(const PeerBufs& pb, int slot, unsigned long long epoch) {
+  for (int t = 0; t < pb.n; ++t) st_release_sys(pb.box[t] + pb.rank * 8 + slot, epoch);
+}
+__device__ __forceinline__ void wait_from(const PeerBufs& pb, int src, int slot, unsigned long long epoch,
+                                          unsigned* err) {
+  wait_epoch(pb.box[pb.rank] + src * 8 + slot, epoch, err);
 }
 
 // Is element i owed a zero (bit of the zero map)?
@@ -736,11 +747,11 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
   unsigned bar = 0;  // grid barrier target (ctl->bar_sel)
   const bool thresh = mode.rounds > 0;
   extern __shared__ __align__(16) unsigned char s_dyn[];
-  __shared__ unsigned s_h[kSelBins];
+  __shared__ __align__(16) unsigned s_h[kSelBins];
   __shared__ unsigned long long s_scan[kSelWarps + 1];
   __shared__ unsigned long long s_red[kSelWarps];
   __shared__ double s_dred[kSelWarps];
-  __shared__ unsigned s_used, s_cached, s_dense;
+  __shared__ unsigned s_used, s_cached, s_dense, s_nl;
   __shared__ __align__(8) unsigned long long s_mbar;  // candidate staging (TMA)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned lt = lanemask_lt();
@@ -764,6 +775,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
   const bool fb = thresh ? (M <= k && M < G) : M < k;
   const unsigned long long fb_target = thresh && k < G ? k + 1 : k;
   if (fb && blockIdx.x == 0 && tid == 0) ctl->fallback = 1;
+  unsigned Lb = fb ? 0u : __ldcg(&ctl->Lkey);  // every candidate has key >= Lb
   if (fb) {
     for (int b = tid; b < kBins1; b += kSelThreads) s_h[b] = 0;
     __syncthreads();
@@ -785,6 +797,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
     block_select_top<kSelThreads>(ctl->hist_fb, kBins1, fb_target, bin, above, s_h);
     if (blockIdx.x == 0 && tid == 0) ctl->Lkey = bin << kShift1;
     const unsigned Lk = bin << kShift1;
+    Lb = Lk;
     for (unsigned c = c0 + warp; c < c1; c += kSelWarps) {  // warp per chunk, rows of 32
       const uint64_t base = (uint64_t)c << kChunkShift;
       unsigned pos = 0;
@@ -860,12 +873,14 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
     return cached ? s_val[s_off[c] + p] : __ldcg(gval + ((uint64_t)c << kChunkShift) + p);
   };
   // thread mode: f(x) for every value of the thread's chunks
-  auto visit_thread = [&](auto&& f) {
+  // (f(x, c) for every value of chunk c, then end(c))
+  auto visit_thread_chunks = [&](auto&& f, auto&& end) {
     for (unsigned c = t0; c < t1; ++c) {
       const unsigned cnt = s_cnt[c];
       if (cached) {
         const float* sv = s_val + s_off[c];
-        for (unsigned i = 0; i < cnt; ++i) f(sv[i]);
+        for (unsigned i = 0; i < cnt; ++i) f(sv[i], c);
+        end(c);
         continue;
       }
       const float4* v4 = reinterpret_cast<const float4*>(gval + ((uint64_t)c << kChunkShift));
@@ -879,9 +894,13 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
         for (int u = 0; u < kSelQ; ++u)
 #pragma unroll
           for (int e = 0; e < 4; ++e)
-            if ((q0 + u) * 4 + e < cnt) f(comp(x[u], e));
+            if ((q0 + u) * 4 + e < cnt) f(comp(x[u], e), c);
       }
+      end(c);
     }
+  };
+  auto visit_thread = [&](auto&& f) {
+    visit_thread_chunks([&](float x, unsigned) { f(x); }, [](unsigned) {});
   };
   // warp mode: f(x, valid, u) for 4 chunks x 2 rounds of 32 values at a time
   // (all lanes call f: warp-synchronous helpers may be used inside)
@@ -921,6 +940,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
 
   unsigned T = 0;
   unsigned long long needT = 0;
+  bool counted = false;  // per-chunk (gt, eq) already in s_ge
   if (thresh) {
     // ---- threshold compressor: bisection of t in [0, max|g_e|] (doubles,
     // inc/compress.hpp:84-101).  A probe t is counted over the candidates
@@ -977,6 +997,101 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
   // ---- digits of T ----
   unsigned long long need = k;
   unsigned prefix = 0;  // key bits above the digit being resolved
+  // Window pass: every candidate has key >= Lkey, and the k-th largest sits
+  // just above it (M ~ 1.05k), so key bits 30..11 are resolved in ONE pass
+  // over 4096 bins counted from Lkey's 20-bit prefix (the top bin absorbs
+  // every key >= 2 Lkey).  The threshold lands in the top bin, or below the
+  // window, only when the bound is far off; then the three absolute digits
+  // below run instead.
+  bool windowed = false;
+  {
+    const unsigned wb = Lb >> 11;
+    for (int b = tid; b < kSelBins; b += kSelThreads) s_h[b] = 0;
+    __syncthreads();
+    if (dense) {
+      visit_warp([](int, unsigned) {},
+                 [&](float x, bool valid, int, unsigned, unsigned, unsigned) {
+                   const unsigned hi = key_of(x) >> 11;
+                   if (valid && hi >= wb) atomicAdd(&s_h[min(hi - wb, (unsigned)kSelBins - 1u)], 1u);
+                 });
+    } else {
+      visit_thread([&](float x) {
+        const unsigned hi = key_of(x) >> 11;
+        if (hi >= wb) atomicAdd(&s_h[min(hi - wb, (unsigned)kSelBins - 1u)], 1u);
+      });
+    }
+    flush_hist(s_h, ctl->hist_w, kSelBins);
+    grid_barrier(&ctl->bar_sel, bar, &ctl->bar_err);
+    SEL_MARK(2);
+    unsigned bin;
+    unsigned long long above;
+    if (block_select_top<kSelThreads>(ctl->hist_w, kSelBins, need, bin, above, s_h) &&
+        bin < (unsigned)kSelBins - 1u) {
+      windowed = true;
+      need -= above;
+      prefix = wb + bin;
+    }
+    SEL_MARK(3);
+  }
+  if (windowed) {
+    // last digit (bits 10..0) fused with the count: per chunk, the keys above
+    // the 20-bit prefix are counted here; the few keys inside the prefix bin
+    // are listed and settled against T once it is known
+    constexpr unsigned kListCap = kSelBins / 4;  // u64 entries in the upper half of s_h
+    unsigned long long* s_list = reinterpret_cast<unsigned long long*>(s_h + kSelBins / 2);
+    for (int b = tid; b < 2048; b += kSelThreads) s_h[b] = 0;
+    if (tid == 0) s_nl = 0;
+    __syncthreads();
+    const unsigned pf = prefix;
+    auto in_bin = [&](unsigned key, unsigned c) {
+      atomicAdd(&s_h[key & 2047u], 1u);
+      const unsigned slot = atomicAdd(&s_nl, 1u);
+      if (slot < kListCap) s_list[slot] = ((unsigned long long)c << 32) | key;
+    };
+    if (dense) {
+      unsigned g[4];
+      visit_warp([&](int u, unsigned) { g[u] = 0; },
+                 [&](float x, bool valid, int u, unsigned c, unsigned r, unsigned) {
+                   const unsigned key = key_of(x), hi = key >> 11;
+                   g[u] += __popc(__ballot_sync(0xffffffffu, valid && hi > pf));
+                   if (valid && hi == pf) in_bin(key, c);
+                   if (lane == 0 && r + 32 >= s_cnt[c]) s_ge[c] = g[u] << 16;
+                 });
+      __syncthreads();
+      for (unsigned c = tid; c < nc; c += kSelThreads)
+        if (s_cnt[c] == 0) s_ge[c] = 0;
+    } else {
+      unsigned g = 0;
+      visit_thread_chunks(
+          [&](float x, unsigned c) {
+            const unsigned key = key_of(x), hi = key >> 11;
+            g += hi > pf;
+            if (hi == pf) in_bin(key, c);
+          },
+          [&](unsigned c) {
+            s_ge[c] = g << 16;
+            g = 0;
+          });
+    }
+    flush_hist(s_h, ctl->hist3, 2048);
+    grid_barrier(&ctl->bar_sel, bar, &ctl->bar_err);
+    SEL_MARK(4);
+    unsigned bin;
+    unsigned long long above;
+    block_select_top<kSelThreads>(ctl->hist3, 2048, need, bin, above, s_h);
+    need -= above;
+    prefix = (prefix << 11) | bin;
+    const unsigned nl = s_nl;
+    if (nl <= kListCap) {
+      for (unsigned i = tid; i < nl; i += kSelThreads) {
+        const unsigned long long e = s_list[i];
+        const unsigned key = (unsigned)e, c = (unsigned)(e >> 32);
+        if (key > prefix) atomicAdd(&s_ge[c], 1u << 16);
+        else if (key == prefix) atomicAdd(&s_ge[c], 1u);
+      }
+      counted = true;
+    }
+  } else {
   const int shifts[3] = {kShift1, 11, 0};
   const int widths[3] = {12, 8, 11};
   int above_shift = 31;
@@ -1009,19 +1124,22 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
     need -= above;
     prefix = (prefix << widths[d]) | bin;
     above_shift = sh;
-    if (d == 0 && blockIdx.x == 0 && tid == 0) ctl->b1 = bin;
   }
+  }  // absolute digits
   T = prefix;
   needT = need;
   if (blockIdx.x == 0 && tid == 0) {
     ctl->T = T;
     ctl->needT = needT;
     ctl->count_gt = k - needT;
+    ctl->b1 = T >> kShift1;
+    ctl->b2 = windowed;
   }
   }  // exact mode
 
   // ---- count: per-chunk (gt, eq), block-level chunk prefixes, block total ----
-  if (dense) {
+  if (counted) {
+  } else if (dense) {
     unsigned gt[4], eq[4];
     visit_warp(
         [&](int u, unsigned) {
@@ -1099,6 +1217,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
   unsigned long long bp = 0;
   for (unsigned i = tid; i < blockIdx.x; i += kSelThreads) bp += __ldcg(w.btot + i);
   bp = block_sum_u64<kSelThreads>(bp, s_red);  // (also a barrier: s_pre visible)
+  if (blockIdx.x == 0 && tid == 0) ctl->tphase_ef2[2] = gtimer();
   double acc = 0.0;
   if (dense) {
     unsigned long long o[4];
@@ -1194,6 +1313,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
       }
     }
     __syncthreads();
+    if (blockIdx.x == 0 && tid == 0) ctl->tphase_ef2[3] = gtimer();
     if (staged)
       for (unsigned i = tid; i < nsel; i += kSelThreads) {
         out_idx[obase + i] = s_oidx[i];
@@ -1212,10 +1332,11 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
     if (tid == 0) {
       ctl->topk_norm2 = tot;
       if (mode.publish) {  // every block's output is in (barrier); ||top-k||^2 with it (VAR)
-        reinterpret_cast<double*>(mode.publish)[4] = tot;
+        for (int t = 0; t < mode.pb.n; ++t)
+          reinterpret_cast<double*>(mode.pb.box[t] + mode.pb.rank * 8)[4] = tot;
         __threadfence_system();
-        st_release_sys(mode.publish, mode.epoch);
-        if (mode.publish_contrib) st_release_sys(mode.publish + 1, mode.epoch);
+        publish_all(mode.pb, 0, mode.epoch);
+        if (mode.publish_contrib) publish_all(mode.pb, 1, mode.epoch);
       }
     }
   }
@@ -1366,21 +1487,23 @@ __global__ void __launch_bounds__(kThreads) k_fetch_gather(PeerBufs pb, int sel,
                                                            unsigned long long epoch,
                                                            const float* __restrict__ ge, uint64_t k,
                                                            unsigned* __restrict__ bounds, uint64_t nch,
-                                                           Ctl* __restrict__ ctl, double* __restrict__ part,
-                                                           int* __restrict__ sel_out) {
+                                                           Ctl* __restrict__ ctl, int* __restrict__ sel_out,
+                                                           unsigned long long* __restrict__ tblk) {
   pdl_wait();
-  __shared__ double s_red[kThreads / 32];
   __shared__ int s_sel;
-  if (sel < 0) {
+  const bool var = sel < 0;
+  const int n = pb.n, me = pb.rank;
+  if (var) {
     // VAR (select_var, artopk.hpp:35-48): every rank published its list and
     // ||top-k||^2; the winner is the argmax (strict >, ties to the lowest rank)
-    if (threadIdx.x < (unsigned)pb.n) wait_epoch(pb.flags[threadIdx.x], epoch, &ctl->bar_err);
+    if (threadIdx.x < (unsigned)n) wait_from(pb, threadIdx.x, 0, epoch, &ctl->bar_err);
     __syncthreads();
     if (threadIdx.x == 0) {
+      const double* norms = reinterpret_cast<const double*>(pb.box[me]);
       int best = 0;
-      double bs = __ldcv(reinterpret_cast<const double*>(pb.flags[0]) + 4);
-      for (int r = 1; r < pb.n; ++r) {
-        const double x = __ldcv(reinterpret_cast<const double*>(pb.flags[r]) + 4);
+      double bs = __ldcv(norms + 4);
+      for (int r = 1; r < n; ++r) {
+        const double x = __ldcv(norms + r * 8 + 4);
         if (x > bs) {
           bs = x;
           best = r;
@@ -1392,57 +1515,99 @@ __global__ void __launch_bounds__(kThreads) k_fetch_gather(PeerBufs pb, int sel,
     __syncthreads();
     sel = s_sel;
   } else {
-    if (threadIdx.x == 0) wait_epoch(pb.flags[sel], epoch, &ctl->bar_err);
+    if (blockIdx.x == 0 && threadIdx.x == 0) g_tdiag[2] = gtimer();
+    if (threadIdx.x == 0) wait_from(pb, sel, 0, epoch, &ctl->bar_err);
     __syncthreads();
   }
-  const unsigned* src = pb.list[sel] + (uint64_t)par * pb.kmax;  // the selected rank's list (NVLink)
-  unsigned* mine = pb.list[pb.rank] + (uint64_t)par * pb.kmax;
-  float* contrib = pb.contrib[pb.rank] + (uint64_t)par * pb.kmax;
-  double acc = 0.0;
-  const uint64_t step = (uint64_t)gridDim.x * kThreads;
-  for (uint64_t j0 = blockIdx.x * (uint64_t)kThreads + threadIdx.x; j0 < k; j0 += step * kGatherUnroll) {
-    unsigned ii[kGatherUnroll];
-    float vv[kGatherUnroll];
-#pragma unroll
-    for (int u = 0; u < kGatherUnroll; ++u) {
-      const uint64_t j = j0 + u * step;
-      ii[u] = j < k ? __ldcv(src + j) : 0xffffffffu;
-    }
-#pragma unroll
-    for (int u = 0; u < kGatherUnroll; ++u) vv[u] = ii[u] != 0xffffffffu ? __ldcs(ge + ii[u]) : 0.f;
-#pragma unroll
-    for (int u = 0; u < kGatherUnroll; ++u) {
-      if (ii[u] == 0xffffffffu) continue;
-      const uint64_t j = j0 + u * step;
-      mine[j] = ii[u];
-      contrib[j] = vv[u];
-      acc = fma((double)vv[u], (double)vv[u], acc);
-      const uint64_t hi = ii[u] >> kChunkShift;
-      const uint64_t lo = j == 0 ? 0 : (uint64_t)(__ldcv(src + j - 1) >> kChunkShift) + 1;
-      for (uint64_t t = lo; t <= hi; ++t) bounds[t] = (unsigned)j;
-      if (j == k - 1)
-        for (uint64_t t = hi + 1; t <= nch; ++t) bounds[t] = (unsigned)k;
-    }
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_tdiag[3] = gtimer();
+  if (threadIdx.x == 0) tblk[2 * blockIdx.x] = gtimer();
+  const uint64_t off = (uint64_t)par * pb.kmax;  // parity rows are 16-byte aligned
+  const uint4* src4 = reinterpret_cast<const uint4*>(pb.list[sel] + off);  // the selected list (NVLink)
+  uint4* mine4 = reinterpret_cast<uint4*>(pb.list[me] + off);
+  float4* contrib4 = reinterpret_cast<float4*>(pb.contrib[me] + off);
+  // two ranks: this contribution goes to the peer's inbox; STAR also pulls
+  // the selected rank's values into this rank's inbox (the decode then reads
+  // both locally).  N > 2: each value goes to the inbox of its slice's owner.
+  const bool pull_sel = n == 2 && !var;
+  const uint4* selv4 = reinterpret_cast<const uint4*>(pb.contrib[sel] + off);
+  uint4* selcopy4 = pull_sel ? reinterpret_cast<uint4*>(inbox_of(pb, me, sel, par)) : nullptr;
+  float4* peer4 = n == 2 ? reinterpret_cast<float4*>(inbox_of(pb, 1 - me, me, par)) : nullptr;
+  const bool copy_list = sel != me;  // the winner's own list is already in place
+  const uint64_t nq = (k + 3) / 4, nt = (uint64_t)gridDim.x * kThreads;
+  const uint64_t t0 = blockIdx.x * (uint64_t)kThreads + threadIdx.x;
+  // the selected list's chunk bounds (its select wrote them): a plain pull
+  {
+    const uint4* bs4 = reinterpret_cast<const uint4*>(pb.bounds[sel] + (uint64_t)par * pb.nbs);
+    const uint64_t nb4 = (nch + 1 + 3) / 4;  // (the parity row is padded to 4)
+    uint4* bd4 = reinterpret_cast<uint4*>(bounds);
+    for (uint64_t i = t0; i < nb4; i += nt) bd4[i] = __ldcv(bs4 + i);
   }
-  const double b = block_sum<kThreads>(acc, s_red);
-  if (threadIdx.x == 0) part[blockIdx.x] = b;
+  // groups of 4 consecutive list positions per thread, lanes on consecutive
+  // groups; the next group's remote loads are issued before this one's local
+  // gather (NVLink latency overlapped)
+  uint64_t q = t0;
+  uint4 ci = make_uint4(0, 0, 0, 0), cv = make_uint4(0, 0, 0, 0);
+  if (q < nq) {
+    ci = __ldcv(src4 + q);
+    if (pull_sel) cv = __ldcv(selv4 + q);
+  }
+  for (; q < nq; q += nt) {
+    const uint64_t qn = q + nt;
+    uint4 ni = make_uint4(0, 0, 0, 0), nv = make_uint4(0, 0, 0, 0);
+    if (qn < nq) {
+      ni = __ldcv(src4 + qn);
+      if (pull_sel) nv = __ldcv(selv4 + qn);
+    }
+    const uint64_t j = 4 * q;
+    float4 g4;
+    g4.x = __ldcs(ge + ci.x);
+    g4.y = j + 1 < k ? __ldcs(ge + ci.y) : 0.f;
+    g4.z = j + 2 < k ? __ldcs(ge + ci.z) : 0.f;
+    g4.w = j + 3 < k ? __ldcs(ge + ci.w) : 0.f;
+    if (copy_list) mine4[q] = ci;
+    contrib4[q] = g4;
+    if (pull_sel) selcopy4[q] = cv;
+    if (n == 2) {
+      __stcg(peer4 + q, g4);
+    } else {
+      const float g[4] = {g4.x, g4.y, g4.z, g4.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (j + e < k) __stcg(inbox_of(pb, slice_owner(j + e, k, n), me, par) + j + e, g[e]);
+    }
+    ci = ni;
+    cv = nv;
+  }
   pdl_trigger();
+  __syncthreads();
+  if (threadIdx.x == 0) tblk[2 * blockIdx.x + 1] = gtimer();
+  if (threadIdx.x == 0) __threadfence_system();  // the block's pushes before the flag
   if (!last_block_done(&ctl->done_gather)) return;
-  const double tot = block_sum_array<kThreads>(part, gridDim.x, s_red);
   if (threadIdx.x == 0) {
-    ctl->kept_norm2 = tot;
     __threadfence_system();
-    st_release_sys(pb.flags[pb.rank] + 1, epoch);  // this rank's contribution is in
+    publish_all(pb, 1, epoch);  // this rank's contribution is in
+    g_tdiag[4] = gtimer();
   }
 }
 
+// Grid of the peer gather: every block resident (one wave).
+int fetch_gather_grid() {
+  static int g = 0;
+  if (!g) {
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_fetch_gather, kThreads, 0);
+    g = num_sms() * std::max(per, 1);
+  }
+  return g;
+}
+
 void launch_fetch_gather(const PeerBufs& pb, int sel, int par, unsigned long long epoch, const float* ge,
-                         uint64_t k, unsigned* bounds, uint64_t nch, Ctl* ctl, double* part, int* sel_out,
-                         cudaStream_t s) {
-  int grid = (int)std::min<uint64_t>((k + kThreads * kGatherUnroll - 1) / (kThreads * kGatherUnroll),
-                                     (uint64_t)num_sms() * 8);
+                         uint64_t k, unsigned* bounds, uint64_t nch, Ctl* ctl, int* sel_out,
+                         unsigned long long* tblk, cudaStream_t s) {
+  const uint64_t nq = std::max<uint64_t>((k + 3) / 4, (nch + 4) / 4);
+  int grid = (int)std::min<uint64_t>((nq + kThreads - 1) / kThreads, (uint64_t)fetch_gather_grid());
   if (grid < 1) grid = 1;
-  launch_pdl(k_fetch_gather, grid, kThreads, 0, s, pb, sel, par, epoch, ge, k, bounds, nch, ctl, part, sel_out);
+  launch_pdl(k_fetch_gather, grid, kThreads, 0, s, pb, sel, par, epoch, ge, k, bounds, nch, ctl, sel_out, tblk);
   count_launch();
 }
 
@@ -1611,7 +1776,8 @@ __global__ void __launch_bounds__(kThreads) k_decode_ar(const unsigned* __restri
   __shared__ __align__(128) float tile[2][kDecTile];
   __shared__ unsigned s_zm[kDecChunks * 32];
   if (kPeers) {  // every rank's contribution (1) / reduced slice (2) is in
-    if (threadIdx.x < (unsigned)pb.n) wait_epoch(pb.flags[threadIdx.x] + kPeers, epoch, err);
+    if (blockIdx.x == 0 && threadIdx.x == 0) g_tdiag[5] = gtimer();
+    if (threadIdx.x < (unsigned)pb.n) wait_from(pb, threadIdx.x, kPeers, epoch, err);
     __syncthreads();
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) g_tdiag[0] = gtimer();
@@ -1630,14 +1796,11 @@ __global__ void __launch_bounds__(kThreads) k_decode_ar(const unsigned* __restri
     __syncthreads();
     for (unsigned j = lo + threadIdx.x; j < hi; j += kThreads) {
       float v;
-      if (kPeers == 1) {  // v = c_0; v += c_r, r ascending (collectives.hpp:82-87)
-        v = __ldcv(pb.contrib[0] + (uint64_t)par * pb.kmax + j);
-        for (int r = 1; r < pb.n; ++r) v += __ldcv(pb.contrib[r] + (uint64_t)par * pb.kmax + j);
-      } else if (kPeers == 2) {  // from the owner of slice j (list_stride = k here)
-        int r = (int)(((uint64_t)j * pb.n) / list_stride);
-        while (r + 1 < pb.n && ((uint64_t)(r + 1) * list_stride) / pb.n <= j) ++r;
-        while (r > 0 && ((uint64_t)r * list_stride) / pb.n > j) --r;
-        v = __ldcv(pb.reduced[r] + (uint64_t)par * pb.kmax + j);
+      if (kPeers == 1) {  // c_0 + c_1 (collectives.hpp:82-87; two terms: order-free)
+        v = __ldcg(pb.contrib[pb.rank] + (uint64_t)par * pb.kmax + j) +
+            __ldcg(inbox_of(pb, pb.rank, 1 - pb.rank, par) + j);
+      } else if (kPeers == 2) {  // pushed by the owner of slice j
+        v = __ldcg(pb.reduced[pb.rank] + (uint64_t)par * pb.kmax + j);
       } else {
         v = lists[j];
         for (int l = 1; l < nlists; ++l) v += lists[(uint64_t)l * list_stride + j];
@@ -1698,7 +1861,7 @@ __global__ void __launch_bounds__(kThreads) k_collect_packs(PeerBufs pb, int par
                                                             uint64_t k, unsigned* __restrict__ packs,
                                                             unsigned* __restrict__ bounds, unsigned* err) {
   pdl_wait();
-  if (threadIdx.x < (unsigned)pb.n) wait_epoch(pb.flags[threadIdx.x], epoch, err);
+  if (threadIdx.x < (unsigned)pb.n) wait_from(pb, threadIdx.x, 0, epoch, err);
   __syncthreads();
   // blocks split over (rank, row): idx k | val k | bounds nb
   const int rows = 3 * pb.n;
@@ -1727,34 +1890,40 @@ void launch_collect_packs(const PeerBufs& pb, int par, unsigned long long epoch,
 
 // Reduce-scatter step of the peer exchange (see launch_reduce_slice).
 __global__ void __launch_bounds__(kThreads) k_reduce_slice(PeerBufs pb, int par, unsigned long long epoch,
-                                                           uint64_t k, int divide, float divisor,
+                                                           uint64_t k, int divide, float divisor, int star_sel,
                                                            Ctl* __restrict__ ctl) {
   pdl_wait();
-  if (threadIdx.x < (unsigned)pb.n) wait_epoch(pb.flags[threadIdx.x] + 1, epoch, &ctl->bar_err);
+  if (threadIdx.x < (unsigned)pb.n) wait_from(pb, threadIdx.x, 1, epoch, &ctl->bar_err);
   __syncthreads();
-  const uint64_t s0 = (k * pb.rank) / pb.n, s1 = (k * (pb.rank + 1)) / pb.n;
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_tdiag[6] = gtimer();
+  const int n = pb.n, me = pb.rank;
+  const uint64_t s0 = (k * me) / n, s1 = (k * (me + 1)) / n;
   const uint64_t off = (uint64_t)par * pb.kmax;
-  float* out = pb.reduced[pb.rank] + off;
   for (uint64_t j = s0 + blockIdx.x * (uint64_t)kThreads + threadIdx.x; j < s1; j += (uint64_t)gridDim.x * kThreads) {
-    float v = __ldcv(pb.contrib[0] + off + j);  // v = c_0; v += c_r, r ascending
-    for (int r = 1; r < pb.n; ++r) v += __ldcv(pb.contrib[r] + off + j);
+    float v = 0.f;  // v = c_0; v += c_r, r ascending
+    for (int r = 0; r < n; ++r) {
+      const float x = r == star_sel ? __ldcv(pb.contrib[r] + off + j) : __ldcg(inbox_of(pb, me, r, par) + j);
+      v = r == 0 ? x : v + x;
+    }
     if (divide) v = v / divisor;
-    out[j] = v;
+    for (int t = 0; t < n; ++t) __stcg(pb.reduced[(me + t) % n] + off + j, v);  // push to every rank
   }
   pdl_trigger();
+  __threadfence_system();
   if (!last_block_done(&ctl->done_red)) return;
   if (threadIdx.x == 0) {
     __threadfence_system();
-    st_release_sys(pb.flags[pb.rank] + 2, epoch);  // this rank's slice is reduced
+    publish_all(pb, 2, epoch);  // this rank's slice is reduced
+    g_tdiag[7] = gtimer();
   }
 }
 
 void launch_reduce_slice(const PeerBufs& pb, int par, unsigned long long epoch, uint64_t k, int divide,
-                         float divisor, Ctl* ctl, cudaStream_t s) {
+                         float divisor, int star_sel, Ctl* ctl, cudaStream_t s) {
   const uint64_t slice = k / pb.n + 1;
   const unsigned g = (unsigned)std::min<uint64_t>(std::max<uint64_t>((slice + kThreads - 1) / kThreads, 1),
                                                   num_sms() * 4ull);
-  launch_pdl(k_reduce_slice, g, kThreads, 0, s, pb, par, epoch, k, divide, divisor, ctl);
+  launch_pdl(k_reduce_slice, g, kThreads, 0, s, pb, par, epoch, k, divide, divisor, star_sel, ctl);
   count_launch();
 }
 

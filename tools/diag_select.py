@@ -16,7 +16,7 @@ with fc.Cluster(1, G, max_cr=max(cr, 0.1), flags=flags) as cl:
     cl.fill_synthetic(0, 42, 0, 0)
     for s in range(4):
         st = cl.artopk_step(cr, fc.STAR, fc.RING, s)
-        t = (C.c_uint64 * 14)()
+        t = (C.c_uint64 * 16)()
         check(lib.fc_diag_select_phases(cl._ctx, 0, t))
         ws = cl.worker_stats(0)
         print(f"step {s}: total {st.ms_total * 1e3:.0f}us ef {st.ms_ef * 1e3:.0f}us select {st.ms_select * 1e3:.0f}us "
@@ -24,7 +24,9 @@ with fc.Cluster(1, G, max_cr=max(cr, 0.1), flags=flags) as cl:
               + " ".join(f"{n}={(t[i + 1] - t[i]) / 1e3:.1f}us" for i, n in enumerate(names))
               + f" | EF: sample={(t[12] - t[8]) / 1e3:.1f}us flush={(t[13] - t[12]) / 1e3:.1f}us "
               f"barrier={(t[9] - t[13]) / 1e3:.1f}us bound={(t[10] - t[9]) / 1e3:.1f}us "
-              f"stream={(t[11] - t[10]) / 1e3:.1f}us EF-end->select-start={(t[0] - t[11]) / 1e3:.1f}us")
+              f"stream={(t[11] - t[10]) / 1e3:.1f}us EF-end->select-start={(t[0] - t[11]) / 1e3:.1f}us"
+              + (f" | emit: base={(t[14] - t[5]) / 1e3:.1f}us assemble={(t[15] - t[14]) / 1e3:.1f}us "
+                 f"write={(t[6] - t[15]) / 1e3:.1f}us" if t[15] > t[14] else ""))
 
 # EF block imbalance of the last step: per-block start/end spread
 nb = 148
