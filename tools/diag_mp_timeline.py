@@ -6,6 +6,7 @@ enough for a microsecond view).  Run under torchrun:
         tools/diag_mp_timeline.py [star|var] [G] [cr]
 """
 import ctypes as C
+import os
 import sys
 from pathlib import Path
 
@@ -62,6 +63,9 @@ with fc.Cluster.nccl(env.world, env.rank, uid, G, device=env.local_rank, max_cr=
             en_ = sorted(e for _, e in gb)
             gstat = (f" | gather blocks {len(gb)}: start {rel(st_[0]):.1f}/{rel(st_[-1]):.1f} "
                      f"end {rel(en_[0]):.1f}/{rel(en_[len(en_) // 2]):.1f}/{rel(en_[-1]):.1f}")
+            if os.environ.get("DUMP_BLOCKS"):
+                gstat += "\n  block durations (us, block order): " + " ".join(
+                    f"{(e - a) / 1e3:.0f}" for a, e in gb)
         rows.append(
             f"rank {env.rank} step {28 + s}: EF 0..{rel(ef1):.1f} | select {rel(ts[0]):.1f}..{rel(ts[7]):.1f} | "
             f"gather wait {rel(d[2]):.1f} start {rel(d[3]):.1f} published {rel(d[4]):.1f} | "
