@@ -1409,6 +1409,15 @@ void launch_sum_fixed(const double* parts, uint64_t n, double* out, cudaStream_t
 }
 
 // ------------------------------------------------------------------ gather ---
+// One scattered 4-byte read of g_e (read-only for the kernel).  A plain miss
+// fills a whole 128-byte line from DRAM; the L2::64B size hint halves the
+// DRAM bytes of a random gather (tools/micro/gather_ld.cu: 157 -> 88 MB for
+// C3's 1.38M reads, 34.8 -> 29.5 us).
+__device__ __forceinline__ float ld_scattered(const float* p) {
+  float v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::64B.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
 // contrib[j] = g_e[bidx[j]] (artopk.hpp:92-98) and the kept energy
 // sum_j g_e[bidx[j]]^2 for the gain (trainer.hpp:387-396).  The residual
 // zeros at bidx are owed, not written (Pending).
@@ -1433,7 +1442,7 @@ __global__ void __launch_bounds__(kThreads) k_gather(const unsigned* __restrict_
       ii[u] = j < k ? __ldcs(bidx + j) : 0xffffffffu;
     }
 #pragma unroll
-    for (int u = 0; u < kGatherUnroll; ++u) vv[u] = ii[u] != 0xffffffffu ? __ldcs(ge + ii[u]) : 0.f;
+    for (int u = 0; u < kGatherUnroll; ++u) vv[u] = ii[u] != 0xffffffffu ? ld_scattered(ge + ii[u]) : 0.f;
 #pragma unroll
     for (int u = 0; u < kGatherUnroll; ++u) {
       if (ii[u] != 0xffffffffu) {
@@ -1560,10 +1569,10 @@ __global__ void __launch_bounds__(kThreads) k_fetch_gather(PeerBufs pb, int sel,
     }
     const uint64_t j = 4 * q;
     float4 g4;
-    g4.x = __ldcs(ge + ci.x);
-    g4.y = j + 1 < k ? __ldcs(ge + ci.y) : 0.f;
-    g4.z = j + 2 < k ? __ldcs(ge + ci.z) : 0.f;
-    g4.w = j + 3 < k ? __ldcs(ge + ci.w) : 0.f;
+    g4.x = ld_scattered(ge + ci.x);
+    g4.y = j + 1 < k ? ld_scattered(ge + ci.y) : 0.f;
+    g4.z = j + 2 < k ? ld_scattered(ge + ci.z) : 0.f;
+    g4.w = j + 3 < k ? ld_scattered(ge + ci.w) : 0.f;
     if (copy_list) mine4[q] = ci;
     contrib4[q] = g4;
     if (pull_sel) selcopy4[q] = cv;

@@ -6,6 +6,7 @@
 #include <vector>
 #include <algorithm>
 #include <random>
+#include <cstdlib>
 
 template <bool kRemoteIdx, bool kPullVals, bool kGather, bool kPush>
 __global__ void k_g(const uint4* __restrict__ idx_remote, const uint4* __restrict__ idx_local,
@@ -33,7 +34,7 @@ __global__ void k_g(const uint4* __restrict__ idx_remote, const uint4* __restric
   }
 }
 
-int main() {
+int main(int argc, char** argv) {
   int n = 0;
   cudaGetDeviceCount(&n);
   if (n < 2) { printf("need 2 GPUs\n"); return 0; }
@@ -72,6 +73,16 @@ int main() {
   cudaMalloc(&flush, 256ull << 20);
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  if (argc > 1) {  // L2 fetch granularity hint (bytes)
+    cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(argv[1]));
+    size_t v = 0;
+    cudaDeviceGetLimit(&v, cudaLimitMaxL2FetchGranularity);
+    printf("L2 fetch granularity limit: %zu\n", v);
+  } else {
+    size_t v = 0;
+    cudaDeviceGetLimit(&v, cudaLimitMaxL2FetchGranularity);
+    printf("L2 fetch granularity limit (default): %zu\n", v);
+  }
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -90,7 +101,7 @@ int main() {
     }
     printf("%-48s grid %5d: %7.1f us\n", name, grid, best * 1e3);
   };
-  for (int grid : {sms * 4, sms * 8, (int)((nq + 255) / 256)}) {
+  for (int grid : {sms * 8}) {
     run("local idx only (writes)", k_g<false, false, false, false>, grid);
     run("local idx + gather", k_g<false, false, true, false>, grid);
     run("remote idx", k_g<true, false, false, false>, grid);
