@@ -288,10 +288,13 @@ int fc_moo_metrics(fc_ctx* ctx, int ag, const fc_step_stats* stats, double* gain
                    double* t_comp_s);
 
 /* NCCL contexts with 1 < world <= 8: 1 if every rank's exchange buffer is
- * mapped into every other (CUDA IPC over NVLink) and STAR steps exchange
- * through peer memory (broadcast + allreduce fused into a fetch-gather and
- * the decode; rank-ordered sums, bit-exact with the reference), 0 if they use
- * NCCL collectives (FC_NO_P2P=1 in the environment forces that). */
+ * mapped into every other (CUDA IPC over NVLink) and STAR / VAR / exact-AG
+ * steps exchange through peer memory (broadcast + allreduce as a
+ * fetch-gather that pushes contributions into the consumers' inboxes, an
+ * NVLink reduce-scatter for N > 2, and a decode that reads local memory;
+ * epochs in per-rank mailboxes; rank-ordered sums, bit-exact with the
+ * reference), 0 if they use NCCL collectives (FC_NO_P2P=1 in the environment
+ * forces that). */
 int fc_peer_exchange(fc_ctx* ctx, int* enabled);
 
 /* Synchronize the context's streams (for FC_FLAG_ASYNC / FC_HOST_ASYNC users). */
