@@ -1918,7 +1918,8 @@ __global__ void __launch_bounds__(kThreads) k_reduce_slice(PeerBufs pb, int par,
     for (int t = 0; t < n; ++t) __stcg(pb.reduced[(me + t) % n] + off + j, v);  // push to every rank
   }
   pdl_trigger();
-  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) __threadfence_system();  // the block's pushes before the flag
   if (!last_block_done(&ctl->done_red)) return;
   if (threadIdx.x == 0) {
     __threadfence_system();
