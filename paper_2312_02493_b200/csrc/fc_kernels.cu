@@ -1792,6 +1792,32 @@ __global__ void __launch_bounds__(kThreads) k_decode_ar(const unsigned* __restri
   if (blockIdx.x == 0 && threadIdx.x == 0) g_tdiag[0] = gtimer();
   const uint64_t ntd = (G + kDecTile - 1) >> kDecShift;
   const uint64_t nch = nchunks_of(G);
+  auto value_at = [&](unsigned j) -> float {
+    float v;
+    if (kPeers == 1) {  // c_0 + c_1 (collectives.hpp:82-87; two terms: order-free)
+      v = __ldcg(pb.contrib[pb.rank] + (uint64_t)par * pb.kmax + j) +
+          __ldcg(inbox_of(pb, pb.rank, 1 - pb.rank, par) + j);
+    } else if (kPeers == 2) {  // pushed by the owner of slice j
+      v = __ldcg(pb.reduced[pb.rank] + (uint64_t)par * pb.kmax + j);
+    } else {
+      v = lists[j];
+      for (int l = 1; l < nlists; ++l) v += lists[(uint64_t)l * list_stride + j];
+    }
+    return divide ? v / divisor : v;
+  };
+  // the next tile's chunk bounds and first list entry per thread are loaded
+  // one tile ahead (the small dependent loads leave the per-tile chain)
+  unsigned lo = 0, hi = 0, pi = 0;
+  float pv = 0.f;
+  if (blockIdx.x < ntd) {
+    const uint64_t c0 = blockIdx.x * (uint64_t)kDecChunks;
+    lo = __ldg(bounds + c0);
+    hi = __ldg(bounds + min(c0 + kDecChunks, nch));
+    if (lo + threadIdx.x < hi) {
+      pi = idx[lo + threadIdx.x];
+      pv = value_at(lo + threadIdx.x);
+    }
+  }
   int buf = 0, iter = 0;
   for (uint64_t t = blockIdx.x; t < ntd; t += gridDim.x, buf ^= 1, ++iter) {
     const uint64_t t0 = t << kDecShift;
@@ -1801,21 +1827,23 @@ __global__ void __launch_bounds__(kThreads) k_decode_ar(const unsigned* __restri
     zero_tile(tl);
     if (threadIdx.x < kDecChunks * 32) s_zm[threadIdx.x] = 0u;
     const uint64_t c0 = t * kDecChunks, c1 = min(c0 + kDecChunks, nch);
-    const unsigned lo = __ldg(bounds + c0), hi = __ldg(bounds + c1);
-    __syncthreads();
-    for (unsigned j = lo + threadIdx.x; j < hi; j += kThreads) {
-      float v;
-      if (kPeers == 1) {  // c_0 + c_1 (collectives.hpp:82-87; two terms: order-free)
-        v = __ldcg(pb.contrib[pb.rank] + (uint64_t)par * pb.kmax + j) +
-            __ldcg(inbox_of(pb, pb.rank, 1 - pb.rank, par) + j);
-      } else if (kPeers == 2) {  // pushed by the owner of slice j
-        v = __ldcg(pb.reduced[pb.rank] + (uint64_t)par * pb.kmax + j);
-      } else {
-        v = lists[j];
-        for (int l = 1; l < nlists; ++l) v += lists[(uint64_t)l * list_stride + j];
+    const unsigned clo = lo, chi = hi, cpi = pi;
+    const float cpv = pv;
+    const uint64_t tn = t + gridDim.x;
+    if (tn < ntd) {
+      const uint64_t n0 = tn * kDecChunks;
+      lo = __ldg(bounds + n0);
+      hi = __ldg(bounds + min(n0 + kDecChunks, nch));
+      if (lo + threadIdx.x < hi) {
+        pi = idx[lo + threadIdx.x];
+        pv = value_at(lo + threadIdx.x);
       }
-      if (divide) v = v / divisor;
-      const unsigned p = idx[j];
+    }
+    __syncthreads();
+    for (unsigned j = clo + threadIdx.x; j < chi; j += kThreads) {
+      const bool pre = j == clo + threadIdx.x;
+      const float v = pre ? cpv : value_at(j);
+      const unsigned p = pre ? cpi : idx[j];
       tl[p - (unsigned)t0] = v;
       atomicOr(&s_zm[zmap_word(p) - (unsigned)(c0 << 5)], zmap_bit(p));
     }
