@@ -46,7 +46,7 @@ def _grad(f32, rank, step, same):
     return f32.synth(G, SEED, 0 if same else rank, step)
 
 
-def _worker(rank, world, port, mode, same, q):
+def _worker(rank, world, port, mode, same, c, q):
     sys.path.insert(0, str(ROOT))
     os.environ.update(WORLD_SIZE=str(world), RANK=str(rank), LOCAL_RANK=str(rank),
                       MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -62,7 +62,7 @@ def _worker(rank, world, port, mode, same, q):
     out = []
     for step in range(STEPS):
         ge = _grad(f32, rank, step, same) + res
-        idx, val = f32.topk_exact(ge, C)
+        idx, val = f32.topk_exact(ge, c)
         k = idx.size
         if mode == "ag":
             idxs = [torch.empty(k, dtype=torch.int64) for _ in range(world)]
@@ -108,11 +108,11 @@ def _worker(rank, world, port, mode, same, q):
     q.put((rank, out))
 
 
-def _run(world, mode, same=False):
+def _run(world, mode, same=False, c=C):
     port = _port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, same, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, same, c, q))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -123,22 +123,24 @@ def _run(world, mode, same=False):
     return got
 
 
-@pytest.mark.parametrize("world,mode,same", [
-    (2, "star", False), (3, "star", False),
-    (2, "var", False), (3, "var", False),
-    (3, "var", True),  # equal scores on every rank -> rank 0 (strict >)
-    (2, "ag", False), (3, "ag", False),
+@pytest.mark.parametrize("world,mode,same,c", [
+    (2, "star", False, C), (3, "star", False, C),
+    (2, "var", False, C), (3, "var", False, C),
+    (3, "var", True, C),  # equal scores on every rank -> rank 0 (strict >)
+    (2, "ag", False, C), (3, "ag", False, C),
+    (2, "star", False, 1.0), (2, "ag", False, 1.0),  # k = G: every index sent
+    (3, "var", False, 1e-4),  # k = 1
 ])
-def test_gloo_protocol_matches_oracle(f32, world, mode, same):
-    got = _run(world, mode, same)
+def test_gloo_protocol_matches_oracle(f32, world, mode, same, c):
+    got = _run(world, mode, same, c)
     res = np.zeros((world, G), np.float32)
     for step in range(STEPS):
         g_o = np.stack([_grad(f32, r, step, same) for r in range(world)])
         if mode == "ag":
-            agg = f32.ag_step(g_o, res, C)
+            agg = f32.ag_step(g_o, res, c)
             sel = -1
         else:
-            agg, sel, _, _ = f32.artopk_step(g_o, res, C, 0 if mode == "star" else 1, step)
+            agg, sel, _, _ = f32.artopk_step(g_o, res, c, 0 if mode == "star" else 1, step)
         if same and mode == "var":
             assert sel == 0
         for r in range(world):
