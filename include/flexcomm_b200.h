@@ -88,6 +88,13 @@ typedef enum fc_memkind { FC_HOST = 0, FC_DEVICE = 1, FC_HOST_ASYNC = 2 } fc_mem
                                      s-1 overlap step s (fc_grad_ptr / the
                                      aggregate pointer alternate between buffers;
                                      implies FC_FLAG_DENSE_DECODE)                */
+#define FC_FLAG_NO_COOPERATIVE 0x10u /* launch the two grid-barrier kernels (error
+                                     feedback, select) without the cooperative
+                                     attribute: co-residency is then only checked
+                                     against the static occupancy, and blocks kept
+                                     off the GPU by other streams' kernels make the
+                                     bounded barriers time out (reported as
+                                     FC_ERR_RUNTIME) instead of the launch waiting */
 
 #define FC_NCCL_UID_BYTES 128
 
@@ -297,7 +304,17 @@ int fc_moo_metrics(fc_ctx* ctx, int ag, const fc_step_stats* stats, double* gain
  * forces that). */
 int fc_peer_exchange(fc_ctx* ctx, int* enabled);
 
-/* Synchronize the context's streams (for FC_FLAG_ASYNC / FC_HOST_ASYNC users). */
+/* Peer-exchange epoch waits give up after `seconds` (default 120): the
+ * waiting kernel skips its remaining reads and the timeout is reported as
+ * FC_ERR_RUNTIME by the next step call, fc_sync or fc_join (the report is
+ * sticky across steps until returned once).  Every rank should use the same
+ * value.  seconds > 0. */
+int fc_set_peer_timeout(fc_ctx* ctx, double seconds);
+
+/* Synchronize the context's streams (for FC_FLAG_ASYNC / FC_HOST_ASYNC users).
+ * Returns FC_ERR_RUNTIME if a kernel of an earlier step reported a timeout
+ * (grid barrier or peer wait); every step call (also under FC_FLAG_ASYNC)
+ * and fc_join report timeouts of steps that have already finished. */
 int fc_sync(fc_ctx* ctx);
 /* Order the compute stream after every queued FC_HOST_ASYNC copy (so an event
  * recorded on fc_stream() afterwards covers them). */

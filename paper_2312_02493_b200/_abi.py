@@ -30,6 +30,7 @@ FC_FLAG_ASYNC = 0x1
 FC_FLAG_NO_TIMING = 0x2
 FC_FLAG_DENSE_DECODE = 0x4
 FC_FLAG_PIPELINE = 0x8
+FC_FLAG_NO_COOPERATIVE = 0x10
 FC_NCCL_UID_BYTES = 128
 FC_DIST_NORMAL, FC_DIST_TIES, FC_DIST_LAYERED = 0, 1, 2
 
@@ -161,6 +162,7 @@ def _load() -> C.CDLL:
         "fc_network_changed": ([d, d, d, d, d, C.POINTER(i)], i),
         "fc_moo_metrics": ([P, i, C.POINTER(fc_step_stats), C.POINTER(d), C.POINTER(d)], i),
         "fc_peer_exchange": ([P, C.POINTER(i)], i),
+        "fc_set_peer_timeout": ([P, d], i),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(lib, name)
@@ -184,6 +186,7 @@ EXPORTS = [
     "fc_derive_m_from_ag",
     "fc_controller_config_validate", "fc_round_3sig", "fc_candidate_ladder", "fc_trigger_gain",
     "fc_pareto_front", "fc_choose_cr", "fc_network_changed", "fc_moo_metrics", "fc_peer_exchange",
+    "fc_set_peer_timeout",
 ]
 
 

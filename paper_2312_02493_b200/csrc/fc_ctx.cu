@@ -134,6 +134,12 @@ struct fc_ctx {
   float* scratch = nullptr;                    // G floats, for layer slices not 16-byte aligned
   double* dnorms = nullptr;
   double* h_norms = nullptr;  // pinned
+  // sticky error words (pinned, mapped into the device): set by a kernel whose
+  // grid barrier or peer wait timed out, never reset by a step; checked by
+  // every step call (without synchronising), fc_sync and fc_join, cleared
+  // once reported
+  unsigned* h_err = nullptr;
+  unsigned* d_err = nullptr;  // the same words, device view
   int* dsel = nullptr;        // VAR winner chosen on the device (NCCL)
   // peer-memory exchange (NCCL contexts, 1 < world <= 8, every rank's
   // exchange buffer mapped into every other with CUDA IPC over NVLink)
@@ -420,15 +426,22 @@ int drain_ef_events(fc_ctx* c) {
   return FC_OK;
 }
 
-// The EF / select kernels' grid barriers assume one resident block per SM;
-// a timeout there means the result cannot be trusted.
-int check_barriers(fc_ctx* c) {
-  for (auto& w : c->w) {
-    unsigned e = 0;
-    CUDA_TRY(cudaMemcpy(&e, &w.ctl->bar_err, sizeof(e), cudaMemcpyDeviceToHost));
-    if (e) return fail(FC_ERR_RUNTIME, "grid barrier timed out (kernel blocks not co-resident)");
-  }
-  return FC_OK;
+// Timeouts recorded by the kernels (sticky words in mapped host memory, so
+// this needs no synchronisation: it sees every report of a kernel that has
+// finished).  A grid-barrier timeout means the EF / select blocks were not
+// co-resident; a peer-wait timeout that a peer was late or gone.  Either way
+// the step's results cannot be trusted.  A report is cleared once returned.
+int check_errors(fc_ctx* c) {
+  if (!c->h_err) return FC_OK;
+  volatile unsigned* e = c->h_err;
+  const unsigned bar = e[fcb::kErrBarrier], peer = e[fcb::kErrPeer];
+  if (!bar && !peer) return FC_OK;
+  e[fcb::kErrBarrier] = 0;
+  e[fcb::kErrPeer] = 0;
+  if (peer)
+    return fail(FC_ERR_RUNTIME, "peer exchange timed out waiting for another rank (late or gone); "
+                                "the step's results are invalid");
+  return fail(FC_ERR_RUNTIME, "grid barrier timed out (kernel blocks not co-resident)");
 }
 
 int finish_step(fc_ctx* c, fc_step_stats* st, uint64_t k, int sel, int coll, double hbm, double bus,
@@ -437,9 +450,8 @@ int finish_step(fc_ctx* c, fc_step_stats* st, uint64_t k, int sel, int coll, dou
     if (!(c->flags & FC_FLAG_ASYNC)) {
       CUDA_TRY(cudaStreamSynchronize(c->stream));
       TRY(drain_ef_events(c));
-      return check_barriers(c);
     }
-    return FC_OK;
+    return check_errors(c);  // async: reports of earlier steps that have finished
   }
   std::memset(st, 0, sizeof(*st));
   st->selected_rank = sel;
@@ -452,7 +464,7 @@ int finish_step(fc_ctx* c, fc_step_stats* st, uint64_t k, int sel, int coll, dou
   st->hbm_bytes = hbm;
   st->bus_bytes = bus;
   st->launches = fcb::launches() - launches0;
-  if (c->flags & FC_FLAG_ASYNC) return FC_OK;
+  if (c->flags & FC_FLAG_ASYNC) return check_errors(c);
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   TRY(drain_ef_events(c));
   if (c->timing && c->phase_stats) {
@@ -473,7 +485,7 @@ int finish_step(fc_ctx* c, fc_step_stats* st, uint64_t k, int sel, int coll, dou
     CUDA_TRY(cudaMemcpy(&fb, &c->w[i].ctl->fallback, sizeof(fb), cudaMemcpyDeviceToHost));
     st->fallback |= fb ? 1 : 0;
   }
-  return check_barriers(c);
+  return check_errors(c);
 }
 
 }  // namespace
@@ -599,11 +611,14 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
     TRY(c->alloc(&c->reduced, c->kmax));
     TRY(c->alloc(&c->bidx, c->kmax));
     TRY(c->alloc(&c->ag_recv, (uint64_t)c->world * 2 * c->kmax));
-    // [0, W): VAR scores; [W, W+2): this rank's MOO metrics; [W+2, 3W+2): gathered
-    TRY(c->alloc(&c->dnorms, 3 * (uint64_t)c->world + 2));
+    // [0, W): VAR scores; [W, W+3): this rank's MOO metrics; [W+3, 4W+3): gathered
+    TRY(c->alloc(&c->dnorms, 4 * (uint64_t)c->world + 3));
     TRY(c->alloc(&c->dsel, 1));
   }
-  CUDA_TRY(cudaMallocHost(&c->h_norms, 2 * sizeof(double) * std::max(c->world, c->n_local)));
+  CUDA_TRY(cudaMallocHost(&c->h_norms, 3 * sizeof(double) * std::max(c->world, c->n_local)));
+  CUDA_TRY(cudaHostAlloc(&c->h_err, 64, cudaHostAllocMapped));
+  std::memset(c->h_err, 0, 64);
+  CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->d_err), c->h_err, 0));
   CUDA_TRY(cudaMemsetAsync(c->ge_all, 0, N * GS * sizeof(float), c->stream));
   c->w.resize(N);
   for (uint64_t i = 0; i < N; ++i) {
@@ -621,6 +636,8 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
     fcb::ChunkWs& s = w.ws;
     s.nchunks = nch;
     s.ef_grid = ef_grid;
+    s.err = c->d_err;
+    s.coop = (o->flags & FC_FLAG_NO_COOPERATIVE) ? 0u : 1u;
     TRY(c->alloc(&s.off, nch));
     TRY(c->alloc(&s.cnt, nch));
     TRY(c->alloc(&s.btot, 4096));
@@ -711,6 +728,8 @@ int setup_p2p(fc_ctx* c) {
   }
   c->pb.n = N;
   c->pb.rank = c->rank;
+  c->pb.err = c->d_err;
+  c->pb.timeout_ns = 120ull * 1000000000ull;
   c->pb.kmax = kst;
   c->pb.nb = c->nch + 1;
   c->pb.nbs = nbs;
@@ -749,6 +768,14 @@ int fc_destroy(fc_ctx* c) {
   if (c->s_h2d) cudaStreamSynchronize(c->s_h2d);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->s_d2h) cudaStreamSynchronize(c->s_d2h);
+  // Peer memory: a peer may still be reading this rank's exchange buffer
+  // (AG's collect_packs waits only for the publish, not for the readers), so
+  // every rank first passes a barrier that is stream-ordered after all of its
+  // own kernels -- once it completes, no rank has an exchange kernel left.
+  if (c->p2p && c->comm_ring && c->dsel) {
+    if (ncclAllReduce(c->dsel, c->dsel, 1, ncclInt32, ncclMax, c->comm_ring, c->stream) == ncclSuccess)
+      cudaStreamSynchronize(c->stream);
+  }
   for (void* p : c->peer_maps) cudaIpcCloseMemHandle(p);
   if (c->xbuf) cudaFree(c->xbuf);
   if (c->comm_tree) ncclCommDestroy(c->comm_tree);
@@ -757,6 +784,7 @@ int fc_destroy(fc_ctx* c) {
   for (auto& w : c->w)
     if (w.snap) cudaFree(w.snap);
   if (c->h_norms) cudaFreeHost(c->h_norms);
+  if (c->h_err) cudaFreeHost(c->h_err);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   for (auto& pr : c->ef_pending) {
@@ -949,6 +977,13 @@ int fc_restore(fc_ctx* c) {
   return FC_OK;
 }
 
+int fc_set_peer_timeout(fc_ctx* c, double seconds) {
+  if (!c) return fail(FC_ERR_INVALID_ARGUMENT, "null context");
+  if (!(seconds > 0.0) || seconds > 1e7) return fail(FC_ERR_INVALID_ARGUMENT, "timeout must be in (0, 1e7] s");
+  c->pb.timeout_ns = (unsigned long long)(seconds * 1e9);
+  return FC_OK;
+}
+
 int fc_peer_exchange(fc_ctx* c, int* enabled) {
   if (!c || !enabled) return fail(FC_ERR_INVALID_ARGUMENT, "null argument");
   *enabled = c->p2p ? 1 : 0;
@@ -959,35 +994,40 @@ int fc_moo_metrics(fc_ctx* c, int ag, const fc_step_stats* st, double* gain, dou
   if (!c || !st || !gain || !t_comp_s) return fail(FC_ERR_INVALID_ARGUMENT, "null argument");
   CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
-  // this process's workers: (gain_r, t_comp) pairs
+  // this process's workers: (gain_r, t_comp, degenerate_r) triples.  A
+  // degenerate gradient (inc/trainer.hpp:391-393) is not returned early: the
+  // flag travels with the metrics so that every rank fails the same way and
+  // the ranks stay in lockstep (no rank left waiting in the allgather)
   const double tc = (st->ms_ef + st->ms_select + st->ms_decode) * 1e-3;
-  std::vector<double> mine(2 * (size_t)c->n_local);
+  std::vector<double> mine(3 * (size_t)c->n_local);
   for (int i = 0; i < c->n_local; ++i) {
     fc_worker_stats ws{};
     TRY(fc_get_worker_stats(c, i, &ws));
-    if (ws.ge_norm2 <= 0.0) return fail(FC_ERR_RUNTIME, "degenerate gradient");
-    double g = (ag ? ws.topk_norm2 : ws.kept_norm2) / ws.ge_norm2;
+    const bool degenerate = !(ws.ge_norm2 > 0.0);
+    double g = degenerate ? 0.0 : (ag ? ws.topk_norm2 : ws.kept_norm2) / ws.ge_norm2;
     if (!ag) g = std::min(std::max(g, 0.0), 1.0);  // std::clamp(kept / ge, 0, 1)
-    mine[2 * i] = g;
-    mine[2 * i + 1] = tc;
+    mine[3 * i] = g;
+    mine[3 * i + 1] = tc;
+    mine[3 * i + 2] = degenerate ? 1.0 : 0.0;
   }
   const int N = c->world;
-  double* all = c->h_norms;  // 2N pinned doubles, rank order
+  double* all = c->h_norms;  // 3N pinned doubles, rank order
   if (c->nccl) {
     double* send = c->dnorms + N;
-    double* recv = c->dnorms + N + 2;
-    CUDA_TRY(cudaMemcpyAsync(send, mine.data(), 2 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    NCCL_TRY(ncclAllGather(send, recv, 2, ncclFloat64, c->comm_ring, c->stream));
-    CUDA_TRY(cudaMemcpyAsync(all, recv, 2 * sizeof(double) * N, cudaMemcpyDeviceToHost, c->stream));
+    double* recv = c->dnorms + N + 3;
+    CUDA_TRY(cudaMemcpyAsync(send, mine.data(), 3 * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    NCCL_TRY(ncclAllGather(send, recv, 3, ncclFloat64, c->comm_ring, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(all, recv, 3 * sizeof(double) * N, cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
   } else {
-    for (int i = 0; i < 2 * N; ++i) all[i] = mine[i];
+    for (int i = 0; i < 3 * N; ++i) all[i] = mine[i];
   }
   // gain_sum / n in rank order (inc/trainer.hpp:364-369, 387-396)
   double sum = 0.0, tmax = 0.0;
   for (int r = 0; r < N; ++r) {
-    sum += all[2 * r];
-    tmax = std::max(tmax, all[2 * r + 1]);
+    if (all[3 * r + 2] != 0.0) return fail(FC_ERR_RUNTIME, "degenerate gradient");
+    sum += all[3 * r];
+    tmax = std::max(tmax, all[3 * r + 1]);
   }
   *gain = sum / N;
   *t_comp_s = tmax;
@@ -1000,7 +1040,7 @@ int fc_sync(fc_ctx* c) {
   CUDA_TRY(cudaStreamSynchronize(c->s_h2d));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->s_d2h));
-  return check_barriers(c);
+  return check_errors(c);
 }
 
 int fc_join(fc_ctx* c) {
@@ -1013,7 +1053,7 @@ int fc_join(fc_ctx* c) {
   CUDA_TRY(cudaStreamWaitEvent(c->stream, b, 0));
   c->ev_pool.push_back(a);  // safe: a recorded event may be re-recorded later
   c->ev_pool.push_back(b);
-  return FC_OK;
+  return check_errors(c);
 }
 
 int fc_stream(fc_ctx* c, void** stream_out) {
@@ -1248,7 +1288,6 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
       m.pb = c->pb;
       m.epoch = epoch;
       m.publish_contrib = mode == FC_STAR;  // VAR: contributions come from the gather
-      m.err = &c->w[i].ctl->bar_err;
       TRY(run_select(c, i, k, nullptr, m, c->pb.list[c->rank] + par * c->pb.kmax,
                      c->pb.contrib[c->rank] + par * c->pb.kmax, c->pb.bounds[c->rank] + par * c->pb.nbs));
     } else {
@@ -1374,7 +1413,7 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
       fcb::launch_reduce_slice(c->pb, par, epoch, k, op == FC_AVG, (float)N, mode == FC_STAR ? sel : -1,
                                c->w[0].ctl, c->stream);
     fcb::launch_decode_ar_peers(c->pb, par, epoch, bsrc, own_bounds, k, op == FC_AVG, (float)N, rs, aggw,
-                                c->G, c->zmaps, &c->w[0].ctl->bar_err, c->stream);
+                                c->G, c->zmaps, c->stream);
   } else if (incr_ok && c->agg_incr) {
     // in place: zero the previous support, write this one (same dense content)
     fcb::launch_agg_update(c->agg_support, c->agg_support_k, bsrc, k, lists, nlists, lstride,
@@ -1485,7 +1524,7 @@ int fc_ag_step(fc_ctx* c, double cr, int compressor, fc_step_stats* st) {
     kk = *std::max_element(kr.begin(), kr.end());
   }
   if (p2p_ag) {
-    fcb::launch_collect_packs(c->pb, par, epoch, kk, c->ag_recv, c->bounds, &c->w[0].ctl->bar_err, c->stream);
+    fcb::launch_collect_packs(c->pb, par, epoch, kk, c->ag_recv, c->bounds, c->stream);
     LAUNCHED();
     packs = c->ag_recv;
     stride = 2 * kk;

@@ -41,7 +41,7 @@ struct Ctl {
   unsigned done_gather, done_red;  // last-block counters
   unsigned ef_next;       // EF work queue: next chunk to hand out
   unsigned bar_ef, bar_sel;  // software grid barriers of the EF / select kernels
-  unsigned bar_err;       // a grid barrier timed out (blocks not co-resident)
+  unsigned pad_err;       // (timeouts go to the context's sticky error words, ChunkWs::err)
   unsigned maxkey;        // threshold compressor: max |g_e| key
   unsigned tfail;         // threshold: 1 final t below the candidate bound, 2 output > capacity
   unsigned long long kout;      // threshold: elements selected
@@ -74,9 +74,18 @@ struct ChunkWs {
   double* cnorm;              // per chunk: sum of g_e^2 (fp64), reduced in chunk order on demand
   double* g_part;             // one per gather block
   unsigned long long* tblk;   // diagnostics: %globaltimer at each EF block's start and end
+  unsigned* err;              // the context's sticky error words (host-mapped; see kErr*)
   unsigned nchunks;
   unsigned ef_grid;
+  unsigned coop;              // grid-barrier kernels launched cooperatively (default)
 };
+
+// Sticky error words of a context (pinned host memory mapped into the device,
+// never reset by a step: the host reads them without synchronising and clears
+// them only after reporting).  A kernel that times out stores 1 into its word.
+constexpr int kErrBarrier = 0;  // a software grid barrier timed out (blocks not co-resident)
+constexpr int kErrPeer = 1;     // a peer-exchange epoch wait timed out (a peer is late or gone)
+constexpr int kErrWords = 2;
 
 // Zeros owed to a residual store: the residual must be +0 at the set bits of
 // `zmap`.  Applied by the next error-feedback pass instead of k random
@@ -117,6 +126,8 @@ struct PeerBufs {
   // consumers poll their own (local) box.
   unsigned long long* box[kMaxPeers];
   int n = 0, rank = 0;
+  unsigned* err = nullptr;               // this rank's sticky error words (ChunkWs::err)
+  unsigned long long timeout_ns = 0;     // epoch waits give up (and report) after this long
   uint64_t kmax = 0;                     // parity stride of list/contrib/reduced/inbox (multiple of 4)
   uint64_t nb = 0, nbs = 0;              // bounds entries (nchunks + 1), parity stride (multiple of 4)
 };
@@ -124,7 +135,7 @@ struct PeerBufs {
 // list (indices, values) and chunk bounds into local arrays laid out as the
 // NCCL allgather + k_bounds would have produced them.
 void launch_collect_packs(const PeerBufs& pb, int par, unsigned long long epoch, uint64_t k, unsigned* packs,
-                          unsigned* bounds, unsigned* err, cudaStream_t s);
+                          unsigned* bounds, cudaStream_t s);
 // bounds_out (nullable): nchunks+1 entries, bounds_out[c] = first output
 // position whose index is >= c * kChunk (what k_bounds computes from a list)
 // ef_out: the array the EF pass wrote g_e to (read only by the fallback).
@@ -143,7 +154,6 @@ struct SelectMode {
   PeerBufs pb;
   unsigned long long epoch = 0;
   bool publish_contrib = true;  // the values are this rank's contribution (STAR's selected rank)
-  unsigned* err = nullptr;  // (wait timeouts)
 };
 int launch_select(uint64_t k, Ctl* ctl, const ChunkWs& w, const float* ef_out, uint64_t G,
                   unsigned* out_idx, float* out_val, unsigned* bounds_out, const SelectMode& m,
@@ -192,7 +202,7 @@ void launch_reduce_slice(const PeerBufs& pb, int par, unsigned long long epoch, 
 // when divide) or, with `reduced`, this rank's reduced area.  Local reads only.
 void launch_decode_ar_peers(const PeerBufs& pb, int par, unsigned long long epoch, const unsigned* idx,
                             const unsigned* bounds, uint64_t k, int divide, float divisor, bool reduced,
-                            float* agg, uint64_t G, unsigned* zmap, unsigned* err, cudaStream_t s);
+                            float* agg, uint64_t G, unsigned* zmap, cudaStream_t s);
 // select_var on the device: winner of the N scores into *sel_out, this rank's
 // list (or zeros) into masked; a sum-allreduce of masked broadcasts the list.
 void launch_var_mask(const double* scores, int n, int rank, const unsigned* idx, uint64_t k, unsigned* masked,

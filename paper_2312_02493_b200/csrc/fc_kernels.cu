@@ -62,6 +62,41 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+// Launch of a kernel with software grid barriers (one block per SM).  With
+// `coop` the launch carries the cooperative attribute: the driver then
+// guarantees that every block is resident at once (and rejects a grid larger
+// than the co-resident capacity), so the barriers cannot deadlock even when
+// other streams' kernels hold SMs -- the launch waits for room instead.
+// Without it (FC_FLAG_NO_COOPERATIVE) the co-resident capacity is checked
+// against the grid once per kernel; the bounded barriers then report, never
+// hang, if other work kept blocks off the GPU.
+static cudaError_t launch_grid_sync(const void* kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                                    void** args, bool coop) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeCooperative;
+  at[1].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = coop ? 2 : 1;
+  if (!coop) {
+    int per = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, (int)(block.x * block.y * block.z), smem) !=
+        cudaSuccess)
+      return cudaGetLastError();
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if ((long long)per * sms < (long long)grid.x * grid.y * grid.z) return cudaErrorCooperativeLaunchTooLarge;
+  }
+  return cudaLaunchKernelExC(&cfg, kern, args);
+}
+
 static int g_num_sms = 0;
 static void prefer_max_smem();
 static int num_sms() {
@@ -201,29 +236,45 @@ __device__ bool block_select_top(const unsigned* hist, int nb, unsigned long lon
 }
 
 // Grid barrier for the kernels that run exactly one block per SM (grid = SM
-// count, shared memory sized so that no second block fits), launched as plain
-// kernels so they can use programmatic dependent launch and cost no
-// cooperative-group bookkeeping (a barrier is ~2 us).  `ctr` is a
-// per-step counter (zeroed with the control block); every barrier raises the
-// target by gridDim.x.  The wait is bounded: if the blocks were not all
-// resident, *err is set and the kernel proceeds (the host reports it).
+// count, shared memory sized so that no second block fits).  They are
+// launched with the cooperative attribute by default (co-residency
+// guaranteed by the launch) together with programmatic dependent launch; a
+// barrier is ~2 us.  `ctr` is a per-step counter (zeroed with the control
+// block); every barrier raises the target by gridDim.x.  The wait is bounded
+// all the same: if the blocks were not all resident (a non-cooperative
+// launch beside other work), the context's sticky barrier-error word is set
+// and the kernel proceeds; the host reports it at the next call.
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// Sticky error report: a plain system-scope store of 1 (idempotent; the word
+// lives in mapped host memory, where device atomics are not guaranteed).
+__device__ __forceinline__ void report_error(unsigned* err, int which) {
+  if (!err) return;
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(err + which), "r"(1u) : "memory");
+}
+constexpr unsigned long long kBarrierTimeoutNs = 4000000000ull;  // 4 s: blocks are not co-resident
 __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned& target, unsigned* err) {
   __syncthreads();
   target += gridDim.x;
   if (threadIdx.x == 0) {
     __threadfence();
     atomicAdd(ctr, 1u);
-    unsigned spins = 0;
-    while (ld_acquire(ctr) < target) {
-      __nanosleep(64);
-      if (++spins > (1u << 25)) {  // ~ seconds: not co-resident
-        atomicExch(err, 1u);
-        break;
+    if (ld_acquire(ctr) < target) {
+      const unsigned long long t0 = gtimer();
+      while (ld_acquire(ctr) < target) {
+        __nanosleep(64);
+        if (gtimer() - t0 > kBarrierTimeoutNs) {
+          report_error(err, kErrBarrier);
+          break;
+        }
       }
     }
     __threadfence();
@@ -232,8 +283,10 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned& target, un
 }
 
 // System-scope epoch flags of the peer exchange (written over NVLink by the
-// producer, polled locally by the consumer).  Waits are bounded like the grid
-// barrier.
+// producer, polled locally by the consumer).  Waits are bounded by the
+// context's peer timeout (fc_set_peer_timeout, 120 s by default: long enough
+// for a peer delayed by host-side work); a timeout is fatal -- the waiting
+// kernel reports it in the sticky error word and skips its remaining reads.
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -242,16 +295,18 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void wait_epoch(const unsigned long long* flag, unsigned long long epoch,
-                                           unsigned* err) {
-  unsigned spins = 0;
+__device__ __forceinline__ bool wait_epoch(const unsigned long long* flag, unsigned long long epoch,
+                                           const PeerBufs& pb) {
+  if (ld_acquire_sys(flag) >= epoch) return true;
+  const unsigned long long t0 = gtimer();
   while (ld_acquire_sys(flag) < epoch) {
     __nanosleep(128);
-    if (++spins > (1u << 26)) {  // ~ 10 s: a peer is gone
-      if (err) atomicExch(err, 1u);
-      return;
+    if (gtimer() - t0 > pb.timeout_ns) {
+      report_error(pb.err, kErrPeer);
+      return false;
     }
   }
+  return true;
 }
 
 // Mailbox protocol (PeerBufs::box): a producer stores its epoch into every
@@ -259,9 +314,15 @@ __device__ __forceinline__ void wait_epoch(const unsigned long long* flag, unsig
 __device__ __forceinline__ void publish_all(const PeerBufs& pb, int slot, unsigned long long epoch) {
   for (int t = 0; t < pb.n; ++t) st_release_sys(pb.box[t] + pb.rank * 8 + slot, epoch);
 }
-__device__ __forceinline__ void wait_from(const PeerBufs& pb, int src, int slot, unsigned long long epoch,
-                                          unsigned* err) {
-  wait_epoch(pb.box[pb.rank] + src * 8 + slot, epoch, err);
+__device__ __forceinline__ bool wait_from(const PeerBufs& pb, int src, int slot, unsigned long long epoch) {
+  return wait_epoch(pb.box[pb.rank] + src * 8 + slot, epoch, pb);
+}
+// Block-wide wait for `slot` = epoch from every rank (thread r waits for rank
+// r); false in every thread if any wait timed out.
+__device__ __forceinline__ bool wait_all(const PeerBufs& pb, int slot, unsigned long long epoch) {
+  bool ok = true;
+  if (threadIdx.x < (unsigned)pb.n) ok = wait_from(pb, threadIdx.x, slot, epoch);
+  return __syncthreads_and(ok) != 0;
 }
 
 // Is element i owed a zero (bit of the zero map)?
@@ -284,9 +345,9 @@ void launch_fill_synth(float* dst, uint64_t G, uint64_t key, int dist, cudaStrea
 
 // ------------------------------------------------------------------ sample ---
 // Candidate bound from a strided sample of 32768 error-fed magnitudes (fused
-// into the EF kernel, before it streams): the largest 12-bit key bucket L such
-// that the sample holds at least 1.15*mean + 6*sqrt(mean) + 8 values >= L,
-// mean = k/G * 32768.  The bound only decides how many elements EF copies
+// into the EF kernel, before it streams): the largest key bound L (12-bit
+// bucket, then 8 more bits inside it) such that the sample holds at least
+// sample_target = 1.05*mean + 4*sqrt(mean) + 8 values >= L, mean = k/G * 32768.  The bound only decides how many elements EF copies
 // out; exactness never depends on it (a miss triggers the fallback in k_select).
 __device__ __forceinline__ uint64_t sample_pos(uint64_t s, uint64_t G) {
   return ((2 * s + 1) * G) / (2ull * kSamples);
@@ -300,11 +361,6 @@ __device__ __forceinline__ double sample_target(uint64_t G, uint64_t k) {
   return 1.05 * mean + 4.0 * sqrt(mean) + 8.0;
 }
 
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 #define EF_MARK(i) \
   if (blockIdx.x == 0 && threadIdx.x == 0) ctl->tphase_ef[i] = gtimer()
 
@@ -384,7 +440,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
   extern __shared__ __align__(128) unsigned char s_ring[];
   EF_MARK(0);
   if (threadIdx.x == 0) w.tblk[2 * blockIdx.x] = gtimer();
-  __shared__ double s_red[kThreads / 32];
   __shared__ unsigned s_hist[kEmit ? kBins1 : 1];  // sample histogram, then the bound's staging
   __shared__ __align__(8) unsigned long long s_bar[kEfWarps][kEfStages];
   __shared__ unsigned s_chunk[kEfWarps][kEfStages];  // chunk held by each stage
@@ -466,7 +521,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
         if (s_hist[b]) atomicAdd(&ctl->hist_s[b], s_hist[b]);
       if (blockIdx.x == 0 && threadIdx.x == 0) ctl->tphase_ef2[1] = gtimer();
       unsigned bar = 0;
-      grid_barrier(&ctl->bar_ef, bar, &ctl->bar_err);
+      grid_barrier(&ctl->bar_ef, bar, w.err);
       EF_MARK(1);
       // the bound: the sample's 12-bit bucket holding the target-th largest
       // value, then (second level) the 8 bits below inside that bucket, so
@@ -491,7 +546,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
           __syncthreads();
           for (int b = tid; b < 256; b += kThreads)
             if (s_hist[b]) atomicAdd(&ctl->hist_s2[b], s_hist[b]);
-          grid_barrier(&ctl->bar_ef, bar, &ctl->bar_err);
+          grid_barrier(&ctl->bar_ef, bar, w.err);
           const bool f2 = block_select_top<kThreads>(ctl->hist_s2, 256, tgt - above1, b2, above2, s_hist);
           Lkey = (b1 << kShift1) | ((f2 ? b2 : 0u) << 11);
         } else {
@@ -633,8 +688,10 @@ static int launch_ef_t(const float* g_o, float* ge, uint64_t G, uint64_t k, Ctl*
                          (int)kEfRingBytes);
     attr = true;
   }
-  return (int)launch_pdl(k_ef<A, E, P>, w.ef_grid, kThreads, kEfRingBytes, s, g_o, ge, G, k, ctl, w, pz,
-                        opts, ctl_next);
+  ChunkWs ws = w;
+  void* args[] = {&g_o, &ge, &G, &k, &ctl, &ws, &pz, &opts, &ctl_next};
+  return (int)launch_grid_sync((const void*)k_ef<A, E, P>, dim3(w.ef_grid), dim3(kThreads), kEfRingBytes, s,
+                               args, w.coop != 0);
 }
 
 int ef_grid_size() { return num_sms(); }
@@ -791,7 +848,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
     if (blockIdx.x == 0)
       for (uint64_t i = n4 * 4 + tid; i < G; i += kSelThreads) atomicAdd(&s_h[key_of(ef_out[i]) >> kShift1], 1u);
     flush_hist(s_h, ctl->hist_fb, kBins1);
-    grid_barrier(&ctl->bar_sel, bar, &ctl->bar_err);
+    grid_barrier(&ctl->bar_sel, bar, w.err);
     unsigned bin;
     unsigned long long above;
     block_select_top<kSelThreads>(ctl->hist_fb, kBins1, fb_target, bin, above, s_h);
@@ -956,7 +1013,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
       visit_thread([&](float x) { mk = max(mk, (unsigned long long)key_of(x)); });
     mk = block_max_u64<kSelThreads>(mk, s_red);
     if (tid == 0 && mk) atomicMax(&ctl->maxkey, (unsigned)mk);
-    grid_barrier(&ctl->bar_sel, bar, &ctl->bar_err);
+    grid_barrier(&ctl->bar_sel, bar, w.err);
     double hi = (double)__uint_as_float(__ldcg(&ctl->maxkey)), lo = 0.0, t = 0.0;
     unsigned tk = 0;
     const int rounds = min(mode.rounds, 64);
@@ -976,7 +1033,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
         visit_thread([&](float x) { cnt += key_of(x) >= tk; });
       cnt = block_sum_u64<kSelThreads>(cnt, s_red);
       if (tid == 0 && cnt) atomicAdd(&ctl->tcnt[r], cnt);
-      grid_barrier(&ctl->bar_sel, bar, &ctl->bar_err);
+      grid_barrier(&ctl->bar_sel, bar, w.err);
       const unsigned long long c_r = __ldcg(&ctl->tcnt[r]);
       if (c_r == k) break;
       if (c_r > k) lo = t;
@@ -1021,7 +1078,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
       });
     }
     flush_hist(s_h, ctl->hist_w, kSelBins);
-    grid_barrier(&ctl->bar_sel, bar, &ctl->bar_err);
+    grid_barrier(&ctl->bar_sel, bar, w.err);
     SEL_MARK(2);
     unsigned bin;
     unsigned long long above;
@@ -1074,7 +1131,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
           });
     }
     flush_hist(s_h, ctl->hist3, 2048);
-    grid_barrier(&ctl->bar_sel, bar, &ctl->bar_err);
+    grid_barrier(&ctl->bar_sel, bar, w.err);
     SEL_MARK(4);
     unsigned bin;
     unsigned long long above;
@@ -1116,7 +1173,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
       });
     }
     flush_hist(s_h, ghs[d], nb);
-    grid_barrier(&ctl->bar_sel, bar, &ctl->bar_err);
+    grid_barrier(&ctl->bar_sel, bar, w.err);
     SEL_MARK(2 + d);
     unsigned bin;
     unsigned long long above;
@@ -1205,7 +1262,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
     const unsigned long long bk = (blk_total >> 31) + (blk_total & 0x7fffffffull);
     if (bk) atomicAdd(&ctl->kout, bk);
   }
-  grid_barrier(&ctl->bar_sel, bar, &ctl->bar_err);
+  grid_barrier(&ctl->bar_sel, bar, w.err);
   SEL_MARK(5);
   const unsigned long long kout = thresh ? __ldcg(&ctl->kout) : k;
   if (thresh && kout > mode.kcap) {  // output does not fit: report, emit nothing
@@ -1324,7 +1381,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
   if (tid == 0) w.bnorm[blockIdx.x] = bsum;
   if (bounds_out && blockIdx.x == 0 && tid == 0) bounds_out[nch] = (unsigned)kout;
   SEL_MARK(6);
-  grid_barrier(&ctl->bar_sel, bar, &ctl->bar_err);
+  grid_barrier(&ctl->bar_sel, bar, w.err);
   pdl_trigger();
   SEL_MARK(7);
   if (blockIdx.x == 0) {
@@ -1358,19 +1415,10 @@ int launch_select(uint64_t k, Ctl* ctl, const ChunkWs& w, const float* ef_out, u
   ChunkWs ws = w;
   SelectMode mode = m;
   void* args[] = {&k, &ctl, &ws, &ef_out, &G, &out_idx, &out_val, &bounds_out, &mode};
-  // one resident block per SM (1024 threads, ~217 KB shared): plain launch,
-  // software grid barriers (grid_barrier)
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kSelThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelExC(&cfg, (const void*)k_select, args);
+  // one resident 1024-thread block per SM (~217 KB shared), software grid
+  // barriers (grid_barrier); cooperative unless the context opted out
+  const cudaError_t e =
+      launch_grid_sync((const void*)k_select, dim3(grid), dim3(kSelThreads), smem, s, args, w.coop != 0);
   count_launch();
   return e == cudaSuccess ? 0 : (int)e;
 }
@@ -1505,8 +1553,7 @@ __global__ void __launch_bounds__(kThreads) k_fetch_gather(PeerBufs pb, int sel,
   if (var) {
     // VAR (select_var, artopk.hpp:35-48): every rank published its list and
     // ||top-k||^2; the winner is the argmax (strict >, ties to the lowest rank)
-    if (threadIdx.x < (unsigned)n) wait_from(pb, threadIdx.x, 0, epoch, &ctl->bar_err);
-    __syncthreads();
+    if (!wait_all(pb, 0, epoch)) return;  // (timeout reported; no publish: peers fail too)
     if (threadIdx.x == 0) {
       const double* norms = reinterpret_cast<const double*>(pb.box[me]);
       int best = 0;
@@ -1525,8 +1572,9 @@ __global__ void __launch_bounds__(kThreads) k_fetch_gather(PeerBufs pb, int sel,
     sel = s_sel;
   } else {
     if (blockIdx.x == 0 && threadIdx.x == 0) g_tdiag[2] = gtimer();
-    if (threadIdx.x == 0) wait_from(pb, sel, 0, epoch, &ctl->bar_err);
-    __syncthreads();
+    bool ok = true;
+    if (threadIdx.x == 0) ok = wait_from(pb, sel, 0, epoch);
+    if (!__syncthreads_and(ok)) return;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) g_tdiag[3] = gtimer();
   if (threadIdx.x == 0) tblk[2 * blockIdx.x] = gtimer();
@@ -1779,15 +1827,13 @@ __global__ void __launch_bounds__(kThreads) k_decode_ar(const unsigned* __restri
                                                         int divide, float divisor,
                                                         float* __restrict__ agg, uint64_t G,
                                                         unsigned* __restrict__ zmap, PeerBufs pb,
-                                                        int par, unsigned long long epoch,
-                                                        unsigned* err) {
+                                                        int par, unsigned long long epoch) {
   pdl_wait();
   __shared__ __align__(128) float tile[2][kDecTile];
   __shared__ unsigned s_zm[kDecChunks * 32];
   if (kPeers) {  // every rank's contribution (1) / reduced slice (2) is in
     if (blockIdx.x == 0 && threadIdx.x == 0) g_tdiag[5] = gtimer();
-    if (threadIdx.x < (unsigned)pb.n) wait_from(pb, threadIdx.x, kPeers, epoch, err);
-    __syncthreads();
+    if (!wait_all(pb, kPeers, epoch)) return;  // timeout reported
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) g_tdiag[0] = gtimer();
   const uint64_t ntd = (G + kDecTile - 1) >> kDecShift;
@@ -1861,19 +1907,19 @@ void launch_decode_ar(const unsigned* idx, const unsigned* bounds, const float* 
                       uint64_t list_stride, int divide, float divisor, float* agg, uint64_t G,
                       unsigned* zmap, cudaStream_t s) {
   launch_pdl(k_decode_ar<0>, num_sms() * 6, kThreads, 0, s, idx, bounds, lists, nlists, list_stride, divide,
-             divisor, agg, G, zmap, PeerBufs{}, 0, 0ull, (unsigned*)nullptr);
+             divisor, agg, G, zmap, PeerBufs{}, 0, 0ull);
   count_launch();
 }
 
 void launch_decode_ar_peers(const PeerBufs& pb, int par, unsigned long long epoch, const unsigned* idx,
                             const unsigned* bounds, uint64_t k, int divide, float divisor, bool reduced,
-                            float* agg, uint64_t G, unsigned* zmap, unsigned* err, cudaStream_t s) {
+                            float* agg, uint64_t G, unsigned* zmap, cudaStream_t s) {
   if (reduced)
     launch_pdl(k_decode_ar<2>, num_sms() * 6, kThreads, 0, s, idx, bounds, (const float*)nullptr, pb.n, k, 0,
-               1.0f, agg, G, zmap, pb, par, epoch, err);
+               1.0f, agg, G, zmap, pb, par, epoch);
   else
     launch_pdl(k_decode_ar<1>, num_sms() * 6, kThreads, 0, s, idx, bounds, (const float*)nullptr, pb.n, k,
-               divide, divisor, agg, G, zmap, pb, par, epoch, err);
+               divide, divisor, agg, G, zmap, pb, par, epoch);
   count_launch();
 }
 
@@ -1896,10 +1942,9 @@ __device__ __forceinline__ void pull_row(const unsigned* __restrict__ src, unsig
 
 __global__ void __launch_bounds__(kThreads) k_collect_packs(PeerBufs pb, int par, unsigned long long epoch,
                                                             uint64_t k, unsigned* __restrict__ packs,
-                                                            unsigned* __restrict__ bounds, unsigned* err) {
+                                                            unsigned* __restrict__ bounds) {
   pdl_wait();
-  if (threadIdx.x < (unsigned)pb.n) wait_from(pb, threadIdx.x, 0, epoch, err);
-  __syncthreads();
+  if (!wait_all(pb, 0, epoch)) return;  // timeout reported
   // blocks split over (rank, row): idx k | val k | bounds nb
   const int rows = 3 * pb.n;
   const unsigned per = gridDim.x / rows > 0 ? gridDim.x / rows : 1;
@@ -1919,9 +1964,9 @@ __global__ void __launch_bounds__(kThreads) k_collect_packs(PeerBufs pb, int par
 }
 
 void launch_collect_packs(const PeerBufs& pb, int par, unsigned long long epoch, uint64_t k, unsigned* packs,
-                          unsigned* bounds, unsigned* err, cudaStream_t s) {
+                          unsigned* bounds, cudaStream_t s) {
   const unsigned g = (unsigned)(3 * pb.n * std::max<int>(1, num_sms() * 8 / (3 * pb.n)));
-  launch_pdl(k_collect_packs, g, kThreads, 0, s, pb, par, epoch, k, packs, bounds, err);
+  launch_pdl(k_collect_packs, g, kThreads, 0, s, pb, par, epoch, k, packs, bounds);
   count_launch();
 }
 
@@ -1930,8 +1975,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_slice(PeerBufs pb, int par,
                                                            uint64_t k, int divide, float divisor, int star_sel,
                                                            Ctl* __restrict__ ctl) {
   pdl_wait();
-  if (threadIdx.x < (unsigned)pb.n) wait_from(pb, threadIdx.x, 1, epoch, &ctl->bar_err);
-  __syncthreads();
+  if (!wait_all(pb, 1, epoch)) return;  // timeout reported (no publish: peers fail too)
   if (blockIdx.x == 0 && threadIdx.x == 0) g_tdiag[6] = gtimer();
   const int n = pb.n, me = pb.rank;
   const uint64_t s0 = (k * me) / n, s1 = (k * (me + 1)) / n;

@@ -268,6 +268,10 @@ class Cluster:
     def sync(self) -> None:
         check(lib.fc_sync(self._ctx))
 
+    def set_peer_timeout(self, seconds: float) -> None:
+        """Peer-exchange waits give up (and the next call raises) after this long."""
+        check(lib.fc_set_peer_timeout(self._ctx, float(seconds)))
+
     @property
     def peer_exchange(self) -> bool:
         """STAR steps exchange through NVLink peer memory (else NCCL)."""

@@ -129,6 +129,16 @@ def test_artopk_dense_decode_flag(fc, f32):
                    flags=_abi.FC_FLAG_DENSE_DECODE)
 
 
+def test_non_cooperative_launch_path(fc, f32):
+    """FC_FLAG_NO_COOPERATIVE: the grid-barrier kernels as plain launches
+    (occupancy-checked), bit-exact like the default cooperative launches."""
+    from paper_2312_02493_b200 import _abi
+
+    for n, mode in ((1, 0), (2, 1)):
+        trajectory(fc, f32, n, 90_001, 3, mode, 1, [0.01, 0.1], 0, 3 + n,
+                   flags=_abi.FC_FLAG_NO_COOPERATIVE)
+
+
 @pytest.mark.parametrize("op", [0, 1])
 @pytest.mark.parametrize("algo", [0, 1])
 def test_artopk_ops_algos(fc, f32, op, algo):
