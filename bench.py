@@ -89,8 +89,6 @@ def parse():
                    help="BASELINE.json configuration preset (overrides mode/grad-len/cr)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--cpu-budget-s", type=float, default=20.0,
-                   help="approximate CPU seconds for the cpu_baseline sample")
     a = p.parse_args()
     if a.config:
         for key, val in CONFIGS[a.config].items():
@@ -194,53 +192,65 @@ def hbm_peak():
 # ------------------------------------------------------ reference (CPU) ----
 
 def run_reference_cpu(mode: str, algo: str, grad_len: int, cr: float, n: int, steps: int,
-                      budget_s: float):
-    """Time the unmodified reference (oracle/_ref) on this host.
-
-    The reference loops over its N workers serially in one thread
-    (inc/artopk.hpp:75-102), so a step's cost is linear in N*G.  Each timed
-    call runs the reference on a G-slice sized for the budget; the per-step
-    time is scaled linearly back to the full G (said in `sample`).
-    """
+                      warmup: int = 0):
+    """Time the unmodified reference (oracle/_ref, the highest ISA level this
+    host supports) on this host: `warmup` untimed then `steps` timed calls of
+    flexcomm::artopk_step / ag_step on the FULL configuration (n workers x
+    grad_len fp64 elements, the reference's own in-process Cluster; it loops
+    over the workers serially in one thread, inc/artopk.hpp:75-102).
+    Returns (median ms per step, sample description, per-step seconds, isa)."""
     import oracle
 
-    ref = oracle.Ref()
+    ref = oracle.Ref("native")
     m = {"star": 0, "var": 1, "ag": 2}.get(mode, 0)
-    # ~41 ns per worker-element per step (SURVEY §6.3 probe); size the slice
-    per_step = budget_s / max(1, steps)
-    g_s = int(min(grad_len, max(1_000_000, per_step / (45e-9 * n))))
-    st = oracle.RefState(ref, n, g_s)
-    for r in range(n):
-        st.fill_synth(r, SEED, r, 0)
-    times = []
-    for s in range(steps):
-        times.append(st.step(cr, m, ALGOS[algo], s))
-    st.close()
-    scale = grad_len / g_s
-    ms = statistics.median(times) * 1e3 * scale
-    sample = (f"{n} worker(s) x {g_s / 1e6:.3g}M fp64 elements (reference artopk_step/ag_step), "
-              f"{steps} step(s), median, scaled x{scale:.3g} to {grad_len / 1e6:g}M")
-    return ms, sample, times
+    st = oracle.RefState(ref, n, grad_len)
+    try:
+        for r in range(n):
+            st.fill_synth(r, SEED, r, 0)
+        for s in range(warmup):
+            st.step(cr, m, ALGOS[algo], s)
+        times = [st.step(cr, m, ALGOS[algo], warmup + s) for s in range(steps)]
+    finally:
+        st.close()
+    ms = statistics.median(times) * 1e3
+    sample = (f"full configuration: {n} worker(s) x {grad_len / 1e6:g}M fp64 elements through the "
+              f"unmodified reference artopk_step/ag_step ({ref.isa} build), {warmup} untimed + "
+              f"{steps} timed step(s), median")
+    return ms, sample, times, ref.isa
+
+
+def bench_config(a, world: int) -> dict:
+    """The workload's config dict -- identical in both arms (ours / reference)."""
+    k = a.grad_len if a.mode == "dense" else k_of(a.cr, a.grad_len)
+    return {"workload": workload_name(a, world), "grad_len": a.grad_len, "cr": a.cr, "k": k,
+            "mode": a.mode, "algo": a.algo, "workers": world, "parallelism": f"dp{world}",
+            "compressor": a.compressor,
+            "l2": ("inputs (2 x %.0f MB per worker) larger than the 126 MB L2" % (4 * a.grad_len / 1e6))
+            if 8 * a.grad_len > 126e6 else "inputs smaller than the 126 MB L2 (not flushed)"}
+
+
+def k_of(c: float, g: int) -> int:
+    """inc/compress.hpp:28-33 (host arithmetic, as fc_k_of)."""
+    return int(min(max(math.ceil(c * g - 1e-9), 1), g))
 
 
 def reference_arm(a):
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
-    steps = a.steps + a.warmup
-    # bounded: about budget seconds of CPU work in total
-    budget = max(30.0, min(150.0, 6.0 * steps))
-    ms, sample, _ = run_reference_cpu(a.mode, a.algo, a.grad_len, a.cr, world, steps, budget)
+    mode = a.mode if a.mode != "dense" else "star"
+    ms, sample, _, isa = run_reference_cpu(mode, a.algo, a.grad_len, a.cr, world, a.steps, a.warmup)
     line = {
         "metric": "Topk sync ms/step (compress+collective+decode)",
         "value": round(ms, 3), "unit": "ms/step", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": workload_name(a, world), "grad_len": a.grad_len, "cr": a.cr,
-                   "mode": a.mode, "algo": a.algo, "workers": world},
+        "config": bench_config(a, world),
         "cpu_baseline": {"value": round(ms, 3), "unit": "ms/step", "cores": 1,
-                         "kind": "reference", "sample": sample,
+                         "kind": "reference", "sample": sample, "isa": isa,
+                         "threads_note": "the reference's sync path is single-threaded "
+                                         "(inc/artopk.hpp:75-102): 1 thread is every thread it can use",
                          "host": host_info()},
         "e2e": {"value": round(ms, 3), "unit": "ms/step", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -454,10 +464,11 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline and a.compressor == "exact":
         try:
-            ms_cpu, sample, _ = run_reference_cpu(a.mode if a.mode != "dense" else "star", a.algo,
-                                                  G, a.cr, 1, 2, a.cpu_budget_s)
+            # bounded: 2 timed steps of the full configuration (~6-10 s of CPU work)
+            ms_cpu, sample, _, isa = run_reference_cpu(a.mode if a.mode != "dense" else "star", a.algo,
+                                                       G, a.cr, 1, 2, 0)
             cpu = {"value": round(ms_cpu, 2), "unit": "ms/step", "cores": 1, "kind": "reference",
-                   "sample": sample, "host": host_info()}
+                   "sample": sample, "isa": isa, "host": host_info()}
         except Exception as e:  # the baseline is reported, never a dependency
             cpu = {"value": None, "unit": "ms/step", "cores": 1, "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -468,10 +479,7 @@ def main():
             "value": round(ms, 4), "unit": "ms/step", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": workload_name(a, world), "grad_len": G, "cr": a.cr, "k": k,
-                       "mode": a.mode, "algo": a.algo, "workers": world, "parallelism": f"dp{world}",
-                       "compressor": a.compressor,
-                       "l2": "inputs (2 x %.0f MB) larger than the 126 MB L2" % (4 * G / 1e6)},
+            "config": bench_config(a, world),
             "hbm_gbs_step": round(step_gbs, 1),
             "bus_gbs": round(bus / (ms * 1e-3) / 1e9, 2) if bus else 0.0,
             "bus_peak_gbs": 900.0,

@@ -62,10 +62,21 @@ class F32:
         lib.orc_topk_kind.restype = u64
         lib.orc_ag_step_kind.argtypes = [i, u64, P, P, d, i, i, P, P, i, P, P]
         lib.orc_ag_step_kind.restype = u64
+        lib.orc_topk_multi.argtypes, lib.orc_topk_multi.restype = [P, u64, P, i, P], i
         self.lib = lib
 
     def k_of(self, c, g):
         return int(self.lib.orc_k_of(c, g))
+
+    def topk_multi(self, v, crs):
+        """topk_exact index sets of one vector at several ratios (one key array)."""
+        v = np.ascontiguousarray(v, dtype=np.float32)
+        outs = [np.empty(self.k_of(c, v.size), dtype=np.uint32) for c in crs]
+        ptrs = (C.c_void_p * len(outs))(*[o.ctypes.data for o in outs])
+        cs = np.asarray(crs, dtype=np.float64)
+        if self.lib.orc_topk_multi(v.ctypes.data, v.size, cs.ctypes.data, len(outs), ptrs):
+            raise ValueError("bad topk_multi arguments")
+        return outs
 
     def synth(self, g, seed, rank, step, dist=0):
         out = np.empty(g, dtype=np.float32)
@@ -147,16 +158,47 @@ class F32:
         return agg
 
 
-class Ref:
-    """The unmodified reference (oracle/_ref/libflexcomm_ref.so), fp64."""
+def host_isa() -> str:
+    """Highest x86-64 micro-architecture level this host's CPU supports
+    ("x86-64-v4" AVX-512, "x86-64-v3" AVX2/FMA/BMI2, else "x86-64-v2")."""
+    try:
+        flags = set()
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("flags"):
+                flags = set(line.split(":", 1)[1].split())
+                break
+    except OSError:
+        return "x86-64-v2"
+    v3 = {"avx", "avx2", "bmi1", "bmi2", "f16c", "fma", "movbe", "xsave"} <= flags and (
+        "abm" in flags or "lzcnt" in flags)
+    v4 = v3 and {"avx512f", "avx512bw", "avx512cd", "avx512dq", "avx512vl"} <= flags
+    return "x86-64-v4" if v4 else "x86-64-v3" if v3 else "x86-64-v2"
 
-    def __init__(self):
+
+def ref_lib_for(isa: str) -> Path:
+    return {"x86-64-v4": HERE / "_ref" / "libflexcomm_ref_v4.so",
+            "x86-64-v3": HERE / "_ref" / "libflexcomm_ref_v3.so"}.get(isa, REF_LIB)
+
+
+class Ref:
+    """The unmodified reference (oracle/_ref/libflexcomm_ref*.so), fp64.
+
+    isa=None loads the portable x86-64-v2 build; isa="native" the highest
+    level this host supports (bench.py's reference arm)."""
+
+    def __init__(self, isa: str | None = None):
         if not REF_LIB.exists():
             if REF_INCLUDE.exists():
                 build()
             if not REF_LIB.exists():
                 raise FileNotFoundError(f"{REF_LIB} not built (needs /root/reference once)")
-        lib = C.CDLL(str(REF_LIB))
+        self.isa = "x86-64-v2"
+        path = REF_LIB
+        if isa == "native":
+            want = host_isa()
+            if ref_lib_for(want).exists():
+                self.isa, path = want, ref_lib_for(want)
+        lib = C.CDLL(str(path))
         u64, d, i, P, L = C.c_uint64, C.c_double, C.c_int, C.c_void_p, C.c_long
         lib.ref_k_of.argtypes, lib.ref_k_of.restype = [d, u64, P], i
         lib.ref_topk_exact.argtypes, lib.ref_topk_exact.restype = [P, u64, d, P, P, P], i

@@ -1630,10 +1630,12 @@ int fc_dense_step(fc_ctx* c, int algo, int op, fc_step_stats* st) {
   TRY(agg_target(c, &ob));
   float* aggw = c->agg_buf[ob];
   if (c->nccl && N > 1) {
-    NCCL_TRY(ncclAllReduce(c->w[0].g_o, aggw, c->G, ncclFloat32, ncclSum,
+    // Avg inside the collective (ncclAvg): no extra pass over the 4G-byte
+    // aggregate; NCCL's summation order makes this path 1e-5-relative, like
+    // every NCCL allreduce here
+    NCCL_TRY(ncclAllReduce(c->w[0].g_o, aggw, c->G, ncclFloat32, op == FC_AVG ? ncclAvg : ncclSum,
                            algo == FC_TREE ? c->comm_tree : c->comm_ring, c->stream));
     record(c, 3);
-    if (op == FC_AVG) fcb::launch_dense_sum(aggw, 1, 0, 1, (float)N, aggw, c->G, c->stream);
   } else {  // loopback, or a single NCCL rank (allreduce = identity)
     record(c, 3);
     fcb::launch_dense_sum(c->g_o_all, c->n_local, c->gstride, op == FC_AVG, (float)N, aggw, c->G,
@@ -1641,7 +1643,7 @@ int fc_dense_step(fc_ctx* c, int algo, int op, fc_step_stats* st) {
   }
   for (int i = 0; i < c->n_local; ++i) TRY(grad_consumed(c, i));
   advance_input(c);
-  LAUNCHED();
+  CUDA_TRY(cudaGetLastError());
   c->agg_incr = false;
   record(c, 4);
   c->has_agg = true;

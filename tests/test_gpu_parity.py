@@ -91,8 +91,8 @@ def test_topk_adversarial_ties(fc, f32):
 
 # ------------------------------------------------------------ full protocol --
 
-def trajectory(fc, f32, n, g, steps, mode, op, crs, dist, seed, algo=0, flags=0):
-    with fc.Cluster(n, g, flags=flags) as cl:
+def trajectory(fc, f32, n, g, steps, mode, op, crs, dist, seed, algo=0, flags=0, max_cr=1.0):
+    with fc.Cluster(n, g, max_cr=max_cr, flags=flags) as cl:
         res = np.zeros((n, g), np.float32)
         for s in range(steps):
             c = crs[s % len(crs)]
