@@ -356,6 +356,17 @@ int fc_diag_ef_blocks(fc_ctx* ctx, int worker, uint64_t* out, int n);
  * 4 ART-Ring (broadcast + ring allreduce of `bytes`), 5 ART-Tree,
  * 6 AG-compressed (allgather of 2*bytes per rank). */
 int fc_diag_collective_ms(fc_ctx* ctx, int which, uint64_t bytes, int iters, double* ms_out);
+/* Diagnostics (NVLink calibration on the product's own exchange): mean device
+ * ms of one exchange of k (index, value) pairs through the kernels the steps
+ * run -- which: 0 AG (list publish + k_collect_packs), 1 ART-Ring (list
+ * publish + fetch-gather + reduce-scatter/allgather by NVLink stores), 2
+ * ART-Tree (fetch-gather + reduce to the root + broadcast) -- up to the point
+ * where the decode could start (the decode itself is not timed).  The lists
+ * are spread index sets standing in for selections; afterwards the context
+ * holds no top-k / aggregate (run a step next).  Collective over the ranks.
+ * Without peer mappings the NCCL equivalents (fc_diag_collective_ms 6/4/5 at
+ * 4k bytes) are timed. */
+int fc_diag_exchange_ms(fc_ctx* ctx, int which, uint64_t k, int iters, double* ms_out);
 
 #ifdef __cplusplus
 }

@@ -1176,6 +1176,82 @@ int fc_diag_collective_ms(fc_ctx* c, int which, uint64_t bytes, int iters, doubl
   return FC_OK;
 }
 
+// Diagnostics for the NVLink calibration of the cost model on the exchange
+// the product actually runs (peer memory): mean device ms per exchange of
+// k (index, value) pairs, this rank, all ranks calling alike (collective):
+//   0 AG        every rank publishes its list; k_collect_packs pulls all N
+//   1 ART-Ring  the root (rotating as STAR does) publishes; the others'
+//               k_fetch_gather pulls the list, gathers g_e and pushes; N > 2
+//               k_reduce_slice (reduce-scatter + allgather by stores)
+//   2 ART-Tree  as 1, then k_reduce_root (reduce to the root + broadcast)
+// each followed by the wait the peer decode performs before reading (the
+// decode itself is compression-side work and is not timed).  The lists are
+// spread index sets (sorted, k over [0, G)); the selects are replaced by a
+// publish.  Without peer mappings the NCCL equivalents are timed
+// (fc_diag_collective_ms 6 / 4 / 5 with 4k-byte messages).
+int fc_diag_exchange_ms(fc_ctx* c, int which, uint64_t k, int iters, double* ms_out) {
+  if (!c || !ms_out || iters < 1 || which < 0 || which > 2) return fail(FC_ERR_INVALID_ARGUMENT, "bad argument");
+  if (!c->nccl || c->world < 2) return fail(FC_ERR_INVALID_ARGUMENT, "needs a multi-rank NCCL context");
+  if (k < 1 || k > c->kmax || k > c->G) return fail(FC_ERR_INVALID_ARGUMENT, "k outside [1, min(kmax, G)]");
+  if (!c->p2p) return fc_diag_collective_ms(c, which == 0 ? 6 : which == 1 ? 4 : 5, 4 * k, iters, ms_out);
+  CUDA_TRY(cudaSetDevice(c->device));
+  TRY(materialize_all(c));
+  Worker& w = c->w[0];
+  const int N = c->world;
+  // this rank's list in both parities (+ its chunk bounds, as a select writes them)
+  for (int q = 0; q < 2; ++q) {
+    unsigned* lst = c->pb.list[c->rank] + q * c->pb.kmax;
+    fcb::launch_spread_list(lst, k, c->G, (uint64_t)c->rank % std::max<uint64_t>(1, c->G / k), c->stream);
+    fcb::launch_bounds(lst, k, 0, 1, c->G, c->pb.bounds[c->rank] + q * c->pb.nbs, c->stream);
+  }
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  auto once = [&](int it) -> int {
+    const unsigned long long epoch = ++c->epoch;
+    const int par = (int)(epoch & 1);
+    const int sel = it % N;
+    // a fresh control block per exchange (its last-block counters)
+    fcb::Ctl* next = take_ctl(w);
+    CUDA_TRY(cudaMemsetAsync(next, 0, sizeof(fcb::Ctl), c->stream));
+    if (which == 0) {
+      fcb::launch_publish(c->pb, epoch, 1u, c->stream);
+      fcb::launch_collect_packs(c->pb, par, epoch, k, c->ag_recv, c->bounds, c->stream);
+    } else {
+      const bool tree = which == 2, rs = !tree && N > 2;
+      if (c->rank == sel) {
+        fcb::launch_publish(c->pb, epoch, 3u, c->stream);  // list + its values (the contribution)
+      } else {
+        fcb::launch_fetch_gather(c->pb, sel, par, tree, epoch, w.ge, k, c->bounds, c->nch, w.ctl, nullptr,
+                                 reinterpret_cast<unsigned long long*>(w.ws.g_part), c->stream);
+      }
+      if (rs) fcb::launch_reduce_slice(c->pb, par, epoch, k, 1, (float)N, sel, w.ctl, c->stream);
+      if (tree && c->rank == sel)
+        fcb::launch_reduce_root(c->pb, par, epoch, k, 1, (float)N, sel, c->dsel, w.ctl, c->stream);
+      fcb::launch_wait_slot(c->pb, rs || tree ? 2 : 1, epoch, tree ? sel : -1, c->stream);
+    }
+    CUDA_TRY(cudaGetLastError());
+    return FC_OK;
+  };
+  for (int i = 0; i < 3; ++i) TRY(once(i));
+  cudaEvent_t e0 = c->take_event(), e1 = c->take_event();
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  TRY(check_errors(c));
+  CUDA_TRY(cudaEventRecord(e0, c->stream));
+  for (int i = 0; i < iters; ++i) TRY(once(3 + i));
+  CUDA_TRY(cudaEventRecord(e1, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  TRY(check_errors(c));
+  float ms = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+  c->ev_pool.push_back(e0);
+  c->ev_pool.push_back(e1);
+  *ms_out = ms / iters;
+  // the lists are no longer a selection: nothing may treat them as one
+  for (auto& wk : c->w) wk.has_topk = false;
+  c->has_agg = false;
+  return FC_OK;
+}
+
 // Diagnostics: %globaltimer (ns) at k_select's phase boundaries in the last
 // step of `worker` (block 0): start, staged, digit 1/2/3, counted, emitted, end.
 int fc_diag_select_phases(fc_ctx* c, int worker, uint64_t* out12) {
@@ -1320,7 +1396,8 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
   if (p2p_star) {
     Worker& w = c->w[0];
     if (p2p_var || c->rank != sel) {  // VAR: every rank (winner found on the device)
-      fcb::launch_fetch_gather(c->pb, p2p_var ? -1 : sel, par, epoch, w.ge, k, c->bounds, c->nch, w.ctl,
+      fcb::launch_fetch_gather(c->pb, p2p_var ? -1 : sel, par, algo == FC_TREE, epoch, w.ge, k, c->bounds,
+                               c->nch, w.ctl,
                                p2p_var ? c->dsel : nullptr, reinterpret_cast<unsigned long long*>(w.ws.g_part),
                                c->stream);
       w.kept_vals = c->pb.contrib[c->rank] + par * c->pb.kmax;  // ||kept||^2 on demand
@@ -1404,16 +1481,23 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
   TRY(agg_target(c, &ob));
   float* aggw = c->agg_buf[ob];
   if (p2p_star) {
-    // N > 2: reduce-scatter (each rank sums its slice of the list from every
-    // rank's contribution, rank order), then the decode reads each value from
-    // the slice's owner: ring-like NVLink traffic, rank-ordered sums
-    // (two ranks: the decode sums both contributions directly, one fewer launch)
-    const bool rs = N > 2;
+    // ART-Ring, N > 2: reduce-scatter (each rank sums its slice of the list
+    // from every rank's contribution, rank order) and an allgather by NVLink
+    // stores into every rank's reduced area; two ranks: the decode sums both
+    // contributions directly (one fewer launch).  ART-Tree: reduce to the
+    // root (the selected rank), which broadcasts the reduced list.  Both sum
+    // in rank order, bit-exact with the reference (collectives.hpp:82-87).
+    const bool tree = algo == FC_TREE;
+    const bool rs = !tree && N > 2;
     if (rs)
       fcb::launch_reduce_slice(c->pb, par, epoch, k, op == FC_AVG, (float)N, mode == FC_STAR ? sel : -1,
                                c->w[0].ctl, c->stream);
-    fcb::launch_decode_ar_peers(c->pb, par, epoch, bsrc, own_bounds, k, op == FC_AVG, (float)N, rs, aggw,
-                                c->G, c->zmaps, c->stream);
+    if (tree && (mode == FC_VAR || c->rank == sel))  // (VAR: only the winner works; found on the device)
+      fcb::launch_reduce_root(c->pb, par, epoch, k, op == FC_AVG, (float)N, mode == FC_STAR ? sel : -1, c->dsel,
+                              c->w[0].ctl, c->stream);
+    fcb::launch_decode_ar_peers(c->pb, par, epoch, bsrc, own_bounds, k, op == FC_AVG, (float)N, rs || tree,
+                                aggw, c->G, c->zmaps, tree ? (mode == FC_STAR ? sel : -2) : -1, c->dsel,
+                                c->stream);
   } else if (incr_ok && c->agg_incr) {
     // in place: zero the previous support, write this one (same dense content)
     fcb::launch_agg_update(c->agg_support, c->agg_support_k, bsrc, k, lists, nlists, lstride,

@@ -186,9 +186,16 @@ __device__ __host__ inline int slice_owner(uint64_t j, uint64_t k, int n) {
 // The selected list's chunk bounds are pulled from its exchange buffer
 // (pb.bounds, written by its select) into `bounds`.  ||kept||^2 is not
 // formed here (launch_sumsq_fixed over the contribution, on demand).
-void launch_fetch_gather(const PeerBufs& pb, int sel, int par, unsigned long long epoch, const float* ge,
-                         uint64_t k, unsigned* bounds, uint64_t nch, Ctl* ctl, int* sel_out,
+// tree != 0 (ART-Tree): the whole contribution goes to the root's (sel's)
+// inbox instead (see launch_reduce_root).
+void launch_fetch_gather(const PeerBufs& pb, int sel, int par, int tree, unsigned long long epoch,
+                         const float* ge, uint64_t k, unsigned* bounds, uint64_t nch, Ctl* ctl, int* sel_out,
                          unsigned long long* tblk, cudaStream_t s);  // tblk: per-block marks (diagnostics)
+// ART-Tree allreduce over peer memory (see k_reduce_root): the root
+// (star_sel, or *dsel when star_sel < 0) sums every contribution in rank
+// order, pushes the result into every rank's reduced area, publishes slot 2.
+void launch_reduce_root(const PeerBufs& pb, int par, unsigned long long epoch, uint64_t k, int divide,
+                        float divisor, int star_sel, const int* dsel, Ctl* ctl, cudaStream_t s);
 // Reduce-scatter over peer memory (N > 2): once every rank published its
 // contribution (`epoch`), rank r sums slice r of the list in rank order
 // (collectives.hpp:82-87, /divisor when divide) from its inbox (the STAR
@@ -200,9 +207,18 @@ void launch_reduce_slice(const PeerBufs& pb, int par, unsigned long long epoch, 
 // Dense decode once every rank published `epoch`: value j is the sum of this
 // rank's contribution and its inbox copy of the peer's (two ranks; /divisor
 // when divide) or, with `reduced`, this rank's reduced area.  Local reads only.
+// wait_root: -1 waits for every rank's publish (ring), >= 0 for that rank's
+// (ART-Tree root), -2 for the rank in *dsel (ART-Tree, VAR winner).
 void launch_decode_ar_peers(const PeerBufs& pb, int par, unsigned long long epoch, const unsigned* idx,
                             const unsigned* bounds, uint64_t k, int divide, float divisor, bool reduced,
-                            float* agg, uint64_t G, unsigned* zmap, cudaStream_t s);
+                            float* agg, uint64_t G, unsigned* zmap, int wait_root, const int* dsel,
+                            cudaStream_t s);
+// Exchange diagnostics (fc_diag_exchange_ms): publish slots (mask bits) of
+// `epoch` without a select; wait like the peer decode (root < 0: every rank);
+// a sorted spread index list standing in for a selection.
+void launch_publish(const PeerBufs& pb, unsigned long long epoch, unsigned mask, cudaStream_t s);
+void launch_wait_slot(const PeerBufs& pb, int slot, unsigned long long epoch, int root, cudaStream_t s);
+void launch_spread_list(unsigned* out, uint64_t k, uint64_t G, uint64_t shift, cudaStream_t s);
 // select_var on the device: winner of the N scores into *sel_out, this rank's
 // list (or zeros) into masked; a sum-allreduce of masked broadcasts the list.
 void launch_var_mask(const double* scores, int n, int rank, const unsigned* idx, uint64_t k, unsigned* masked,

@@ -1540,7 +1540,7 @@ void launch_var_mask(const double* scores, int n, int rank, const unsigned* idx,
   count_launch();
 }
 
-__global__ void __launch_bounds__(kThreads) k_fetch_gather(PeerBufs pb, int sel, int par,
+__global__ void __launch_bounds__(kThreads) k_fetch_gather(PeerBufs pb, int sel, int par, int tree,
                                                            unsigned long long epoch,
                                                            const float* __restrict__ ge, uint64_t k,
                                                            unsigned* __restrict__ bounds, uint64_t nch,
@@ -1582,13 +1582,17 @@ __global__ void __launch_bounds__(kThreads) k_fetch_gather(PeerBufs pb, int sel,
   const uint4* src4 = reinterpret_cast<const uint4*>(pb.list[sel] + off);  // the selected list (NVLink)
   uint4* mine4 = reinterpret_cast<uint4*>(pb.list[me] + off);
   float4* contrib4 = reinterpret_cast<float4*>(pb.contrib[me] + off);
-  // two ranks: this contribution goes to the peer's inbox; STAR also pulls
-  // the selected rank's values into this rank's inbox (the decode then reads
-  // both locally).  N > 2: each value goes to the inbox of its slice's owner.
-  const bool pull_sel = n == 2 && !var;
+  // Where this contribution goes (ART-Ring): two ranks -- the peer's inbox,
+  // and STAR also pulls the selected rank's values into this rank's inbox
+  // (the decode then reads both locally); N > 2 -- each value to the inbox
+  // of its slice's owner (reduce-scatter).  ART-Tree: the whole list to the
+  // root's (= the selected rank's) inbox; the root sums and broadcasts.
+  const bool pull_sel = n == 2 && !var && !tree;
   const uint4* selv4 = reinterpret_cast<const uint4*>(pb.contrib[sel] + off);
   uint4* selcopy4 = pull_sel ? reinterpret_cast<uint4*>(inbox_of(pb, me, sel, par)) : nullptr;
-  float4* peer4 = n == 2 ? reinterpret_cast<float4*>(inbox_of(pb, 1 - me, me, par)) : nullptr;
+  float4* peer4 = tree ? (sel != me ? reinterpret_cast<float4*>(inbox_of(pb, sel, me, par)) : nullptr)
+                       : n == 2 ? reinterpret_cast<float4*>(inbox_of(pb, 1 - me, me, par)) : nullptr;
+  const bool slices = !tree && n > 2;
   const bool copy_list = sel != me;  // the winner's own list is already in place
   const uint64_t nq = (k + 3) / 4, nt = (uint64_t)gridDim.x * kThreads;
   const uint64_t t0 = blockIdx.x * (uint64_t)kThreads + threadIdx.x;
@@ -1624,9 +1628,9 @@ __global__ void __launch_bounds__(kThreads) k_fetch_gather(PeerBufs pb, int sel,
     if (copy_list) mine4[q] = ci;
     contrib4[q] = g4;
     if (pull_sel) selcopy4[q] = cv;
-    if (n == 2) {
+    if (peer4) {
       __stcg(peer4 + q, g4);
-    } else {
+    } else if (slices) {
       const float g[4] = {g4.x, g4.y, g4.z, g4.w};
 #pragma unroll
       for (int e = 0; e < 4; ++e)
@@ -1658,13 +1662,14 @@ int fetch_gather_grid() {
   return g;
 }
 
-void launch_fetch_gather(const PeerBufs& pb, int sel, int par, unsigned long long epoch, const float* ge,
-                         uint64_t k, unsigned* bounds, uint64_t nch, Ctl* ctl, int* sel_out,
+void launch_fetch_gather(const PeerBufs& pb, int sel, int par, int tree, unsigned long long epoch,
+                         const float* ge, uint64_t k, unsigned* bounds, uint64_t nch, Ctl* ctl, int* sel_out,
                          unsigned long long* tblk, cudaStream_t s) {
   const uint64_t nq = std::max<uint64_t>((k + 3) / 4, (nch + 4) / 4);
   int grid = (int)std::min<uint64_t>((nq + kThreads - 1) / kThreads, (uint64_t)fetch_gather_grid());
   if (grid < 1) grid = 1;
-  launch_pdl(k_fetch_gather, grid, kThreads, 0, s, pb, sel, par, epoch, ge, k, bounds, nch, ctl, sel_out, tblk);
+  launch_pdl(k_fetch_gather, grid, kThreads, 0, s, pb, sel, par, tree, epoch, ge, k, bounds, nch, ctl, sel_out,
+             tblk);
   count_launch();
 }
 
@@ -1827,13 +1832,20 @@ __global__ void __launch_bounds__(kThreads) k_decode_ar(const unsigned* __restri
                                                         int divide, float divisor,
                                                         float* __restrict__ agg, uint64_t G,
                                                         unsigned* __restrict__ zmap, PeerBufs pb,
-                                                        int par, unsigned long long epoch) {
+                                                        int par, unsigned long long epoch, int wait_root,
+                                                        const int* __restrict__ dsel) {
   pdl_wait();
   __shared__ __align__(128) float tile[2][kDecTile];
   __shared__ unsigned s_zm[kDecChunks * 32];
   if (kPeers) {  // every rank's contribution (1) / reduced slice (2) is in
     if (blockIdx.x == 0 && threadIdx.x == 0) g_tdiag[5] = gtimer();
-    if (!wait_all(pb, kPeers, epoch)) return;  // timeout reported
+    if (wait_root == -1) {
+      if (!wait_all(pb, kPeers, epoch)) return;  // timeout reported
+    } else {  // ART-Tree: the root's reduced list (root -2: VAR winner in *dsel)
+      bool ok = true;
+      if (threadIdx.x == 0) ok = wait_from(pb, wait_root >= 0 ? wait_root : *dsel, kPeers, epoch);
+      if (!__syncthreads_and(ok)) return;
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) g_tdiag[0] = gtimer();
   const uint64_t ntd = (G + kDecTile - 1) >> kDecShift;
@@ -1907,19 +1919,20 @@ void launch_decode_ar(const unsigned* idx, const unsigned* bounds, const float* 
                       uint64_t list_stride, int divide, float divisor, float* agg, uint64_t G,
                       unsigned* zmap, cudaStream_t s) {
   launch_pdl(k_decode_ar<0>, num_sms() * 6, kThreads, 0, s, idx, bounds, lists, nlists, list_stride, divide,
-             divisor, agg, G, zmap, PeerBufs{}, 0, 0ull);
+             divisor, agg, G, zmap, PeerBufs{}, 0, 0ull, -1, (const int*)nullptr);
   count_launch();
 }
 
 void launch_decode_ar_peers(const PeerBufs& pb, int par, unsigned long long epoch, const unsigned* idx,
                             const unsigned* bounds, uint64_t k, int divide, float divisor, bool reduced,
-                            float* agg, uint64_t G, unsigned* zmap, cudaStream_t s) {
+                            float* agg, uint64_t G, unsigned* zmap, int wait_root, const int* dsel,
+                            cudaStream_t s) {
   if (reduced)
     launch_pdl(k_decode_ar<2>, num_sms() * 6, kThreads, 0, s, idx, bounds, (const float*)nullptr, pb.n, k, 0,
-               1.0f, agg, G, zmap, pb, par, epoch);
+               1.0f, agg, G, zmap, pb, par, epoch, wait_root, dsel);
   else
     launch_pdl(k_decode_ar<1>, num_sms() * 6, kThreads, 0, s, idx, bounds, (const float*)nullptr, pb.n, k,
-               divide, divisor, agg, G, zmap, pb, par, epoch);
+               divide, divisor, agg, G, zmap, pb, par, epoch, -1, (const int*)nullptr);
   count_launch();
 }
 
@@ -2006,6 +2019,112 @@ void launch_reduce_slice(const PeerBufs& pb, int par, unsigned long long epoch, 
   const unsigned g = (unsigned)std::min<uint64_t>(std::max<uint64_t>((slice + kThreads - 1) / kThreads, 1),
                                                   num_sms() * 4ull);
   launch_pdl(k_reduce_slice, g, kThreads, 0, s, pb, par, epoch, k, divide, divisor, star_sel, ctl);
+  count_launch();
+}
+
+// ART-Tree over peer memory: the allreduce as reduce-to-root + broadcast (a
+// tree of depth one, which is what a tree is on a fully connected NVSwitch
+// fabric).  Every non-root rank pushed its whole contribution list into the
+// root's inbox (k_fetch_gather, tree mode); the root -- the STAR selected
+// rank `star_sel`, or for VAR the winner its own fetch-gather wrote to
+// *dsel -- waits for every contribution, sums them in rank order (v = c_0;
+// v += c_r, r ascending; /divisor for Avg: collectives.hpp:82-87, so the
+// result is bit-exact like the ring's), pushes the reduced list into every
+// rank's reduced area and publishes slot 2.  Other ranks return at once.
+// Traffic: the root receives (N-1)*4k bytes and sends (N-1)*4k, against
+// 2(N-1)/N*4k per rank for the ring's reduce-scatter + allgather.
+__global__ void __launch_bounds__(kThreads) k_reduce_root(PeerBufs pb, int par, unsigned long long epoch,
+                                                          uint64_t k, int divide, float divisor, int star_sel,
+                                                          const int* __restrict__ dsel, Ctl* __restrict__ ctl) {
+  pdl_wait();
+  const int n = pb.n, me = pb.rank;
+  const int root = star_sel >= 0 ? star_sel : *dsel;
+  if (me != root) return;
+  if (!wait_all(pb, 1, epoch)) return;  // timeout reported (no publish: peers fail too)
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_tdiag[6] = gtimer();
+  const uint64_t off = (uint64_t)par * pb.kmax;  // parity rows: 16-byte aligned
+  const uint64_t nq = (k + 3) / 4;
+  for (uint64_t q = blockIdx.x * (uint64_t)kThreads + threadIdx.x; q < nq; q += (uint64_t)gridDim.x * kThreads) {
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int r = 0; r < n; ++r) {  // v = c_0; v += c_r, r ascending
+      const float4* src = reinterpret_cast<const float4*>(r == me ? pb.contrib[me] + off : inbox_of(pb, me, r, par));
+      const float4 x = __ldcg(src + q);
+      if (r == 0) {
+        v = x;
+      } else {
+        v.x = v.x + x.x;
+        v.y = v.y + x.y;
+        v.z = v.z + x.z;
+        v.w = v.w + x.w;
+      }
+    }
+    if (divide) {
+      v.x = v.x / divisor;
+      v.y = v.y / divisor;
+      v.z = v.z / divisor;
+      v.w = v.w / divisor;
+    }
+    for (int t = 0; t < n; ++t)  // broadcast: push to every rank (own first)
+      __stcg(reinterpret_cast<float4*>(pb.reduced[(me + t) % n] + off) + q, v);
+  }
+  pdl_trigger();
+  __syncthreads();
+  if (threadIdx.x == 0) __threadfence_system();  // the block's pushes before the flag
+  if (!last_block_done(&ctl->done_red)) return;
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    publish_all(pb, 2, epoch);  // the reduced list is in every rank's buffer
+    g_tdiag[7] = gtimer();
+  }
+}
+
+void launch_reduce_root(const PeerBufs& pb, int par, unsigned long long epoch, uint64_t k, int divide,
+                        float divisor, int star_sel, const int* dsel, Ctl* ctl, cudaStream_t s) {
+  const uint64_t nq = (k + 3) / 4;
+  const unsigned g = (unsigned)std::min<uint64_t>(std::max<uint64_t>((nq + kThreads - 1) / kThreads, 1),
+                                                  num_sms() * 4ull);
+  launch_pdl(k_reduce_root, g, kThreads, 0, s, pb, par, epoch, k, divide, divisor, star_sel, dsel, ctl);
+  count_launch();
+}
+
+// ---- exchange diagnostics (NVLink calibration of the cost model) -----------
+// The selects' publish, without a select: stamp `epoch` into slots (bit s of
+// mask) of every rank's mailbox (the lists in the exchange buffer are left as
+// they are).
+__global__ void k_publish(PeerBufs pb, unsigned long long epoch, unsigned mask) {
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int sl = 0; sl < 3; ++sl)
+      if (mask & (1u << sl)) publish_all(pb, sl, epoch);
+  }
+}
+// What the peer decode waits for before it reads (slot from every rank, or
+// from `root`), without the decode.
+__global__ void k_wait_slot(PeerBufs pb, int slot, unsigned long long epoch, int root) {
+  pdl_wait();
+  if (root < 0) {
+    wait_all(pb, slot, epoch);
+  } else if (threadIdx.x == 0) {
+    wait_from(pb, root, slot, epoch);
+  }
+}
+void launch_publish(const PeerBufs& pb, unsigned long long epoch, unsigned mask, cudaStream_t s) {
+  launch_pdl(k_publish, 1, 32, 0, s, pb, epoch, mask);
+  count_launch();
+}
+void launch_wait_slot(const PeerBufs& pb, int slot, unsigned long long epoch, int root, cudaStream_t s) {
+  launch_pdl(k_wait_slot, 1, 32, 0, s, pb, slot, epoch, root);
+  count_launch();
+}
+// A sorted, duplicate-free index list of k positions spread over [0, G)
+// (j * G / k + shift, shift < G / k) -- the diagnostics' stand-in for a select.
+__global__ void k_spread_list(unsigned* __restrict__ out, uint64_t k, uint64_t G, uint64_t shift) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < k; j += (uint64_t)gridDim.x * blockDim.x)
+    out[j] = (unsigned)((j * G) / k + shift);
+}
+void launch_spread_list(unsigned* out, uint64_t k, uint64_t G, uint64_t shift, cudaStream_t s) {
+  k_spread_list<<<num_sms() * 4, kThreads, 0, s>>>(out, k, G, shift);
   count_launch();
 }
 
