@@ -1,0 +1,145 @@
+"""Fit the reference's NetParams to the product exchange's measured times.
+
+    python tools/fit_peer.py [fixtures_dir]
+
+Reads fixtures/peer_exchange_n{N}.csv and fixtures/peer_steps_n{N}.csv
+(tools/calibrate_peer.py, run on the GPUs) and fits ONE NetParams(alpha,
+bandwidth) per N -- the reference's API has a single one
+(inc/costmodel.hpp:12-27) -- by least squares on log time over the three
+exchanges of the exchange grid (the communication the selector models:
+cost_ag_compressed / cost_art_ring / cost_art_tree, inc/costmodel.hpp:79-96,
+with Mc = 4k bytes).  Then it checks the unchanged select_collective
+(inc/costmodel.hpp:153-167) the way the reference checks its fixtures
+(tests/test_acceptance.cpp:45-60): the predicted fastest collective must be
+the measured fastest wherever the measured top-two margin exceeds 15 %, on
+the exchange grid and on the whole-step grid of BASELINE configs 1-3 (sync
+time = step - the one-worker step of the same kind).  Writes
+fixtures/peer_fit_n{N}.json.
+"""
+from __future__ import annotations
+
+import csv
+import json
+import math
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+KINDS = ["ag", "art_ring", "art_tree"]
+
+
+def model(alpha: float, beta: float, n: int, mc: float) -> dict:
+    """cost_ag_compressed / cost_art_ring / cost_art_tree (inc/costmodel.hpp:79-96)."""
+    lg = math.log2(n)
+    nm1 = n - 1
+    return {"ag": alpha * lg + 2.0 * mc * beta * nm1,
+            "art_ring": alpha * (2 * nm1 + lg) + mc * beta * (2 * nm1 / n + lg),
+            "art_tree": 3 * alpha * lg + 3 * mc * beta * lg}
+
+
+def log_err(alpha: float, beta: float, n: int, pts) -> float:
+    e = 0.0
+    for mc, meas in pts:
+        m = model(alpha, beta, n, mc)
+        for kk in KINDS:
+            e += (math.log(m[kk]) - math.log(meas[kk])) ** 2
+    return e
+
+
+def fit(n: int, pts) -> tuple[float, float]:
+    """Grid search on log alpha / log beta, then local refinement."""
+    best = None
+    for i in range(121):
+        la = -7.5 + i * (5.0 / 120)          # alpha 30 ns .. 3 ms
+        for j in range(121):
+            lb = -13.5 + j * (5.0 / 120)     # beta: 1/(3e13) .. 1/(3e8) s/byte
+            e = log_err(10 ** la, 10 ** lb, n, pts)
+            if best is None or e < best[0]:
+                best = (e, la, lb)
+    _, la, lb = best
+    step = 5.0 / 120
+    for _ in range(60):
+        improved = False
+        for da, db in ((step, 0), (-step, 0), (0, step), (0, -step)):
+            e = log_err(10 ** (la + da), 10 ** (lb + db), n, pts)
+            if e < best[0]:
+                best, la, lb, improved = (e, la + da, lb + db), la + da, lb + db, True
+        if not improved:
+            step /= 2
+    return 10 ** la, 10 ** lb
+
+
+def choose(alpha: float, beta: float, n: int, mc: float) -> str:
+    """select_collective's argmin, ties to AG then ART_RING (costmodel.hpp:153-167)."""
+    m = model(alpha, beta, n, mc)
+    best, name = m["ag"], "ag"
+    if m["art_ring"] < best:
+        best, name = m["art_ring"], "art_ring"
+    if m["art_tree"] < best:
+        name = "art_tree"
+    return name
+
+
+def check(alpha, beta, n, pts, labels):
+    out = []
+    for (mc, meas), lab in zip(pts, labels):
+        order = sorted(KINDS, key=lambda kk: meas[kk])
+        margin = meas[order[1]] / meas[order[0]] - 1.0
+        pred = choose(alpha, beta, n, mc)
+        m = model(alpha, beta, n, mc)
+        out.append({"point": lab, "mc_bytes": mc, "measured_us": {kk: round(meas[kk] * 1e6, 2) for kk in KINDS},
+                    "measured_fastest": order[0], "margin": round(margin, 3), "predicted": pred,
+                    "agree": pred == order[0], "decisive": margin > 0.15,
+                    "rel_err": {kk: round(abs(m[kk] - meas[kk]) / meas[kk], 3) for kk in KINDS}})
+    return out
+
+
+def load(d: Path, n: int):
+    ex, st = [], []
+    with open(d / f"peer_exchange_n{n}.csv") as f:
+        for r in csv.DictReader(f):
+            ex.append((float(r["mc_bytes"]), {kk: float(r[kk + "_us"]) * 1e-6 for kk in KINDS}, f"k={r['k']}"))
+    p = d / f"peer_steps_n{n}.csv"
+    if p.exists():
+        with open(p) as f:
+            for r in csv.DictReader(f):
+                mc = 4.0 * float(r["grad_len"]) * float(r["cr"])
+                meas = {"ag": float(r["ag_step_us"]) - float(r["ag_one_worker_us"]),
+                        "art_ring": float(r["art_ring_step_us"]) - float(r["art_one_worker_us"]),
+                        "art_tree": float(r["art_tree_step_us"]) - float(r["art_one_worker_us"])}
+                meas = {kk: max(v, 0.05) * 1e-6 for kk, v in meas.items()}
+                st.append((mc, meas, r["config"]))
+    return ex, st
+
+
+def main() -> int:
+    d = Path(sys.argv[1]) if len(sys.argv) > 1 else ROOT / "fixtures"
+    worlds = sorted(int(p.stem.split("_n")[-1]) for p in d.glob("peer_exchange_n*.csv"))
+    for n in worlds:
+        ex, st = load(d, n)
+        pts = [(mc, meas) for mc, meas, _ in ex]
+        alpha, beta = fit(n, pts)
+        exc = check(alpha, beta, n, pts, [lab for *_, lab in ex])
+        stc = check(alpha, beta, n, [(mc, meas) for mc, meas, _ in st], [lab for *_, lab in st])
+        dec = [c for c in exc if c["decisive"]]
+        sdec = [c for c in stc if c["decisive"]]
+        res = {"n": n, "source": "product peer-memory exchange (fc_diag_exchange_ms), tools/calibrate_peer.py",
+               "alpha_s": alpha, "bandwidth_bps": 8.0 / beta, "bandwidth_GBps": 1.0 / beta / 1e9,
+               "fit": "least squares on log time, AG / ART-Ring / ART-Tree exchange grid",
+               "exchange_agreement_decisive": (sum(c["agree"] for c in dec) / len(dec)) if dec else None,
+               "exchange_decisive_points": len(dec),
+               "step_agreement_decisive": (sum(c["agree"] for c in sdec) / len(sdec)) if sdec else None,
+               "step_decisive_points": len(sdec),
+               "max_rel_err": max(max(c["rel_err"].values()) for c in exc),
+               "exchange_points": exc, "step_points": stc}
+        (d / f"peer_fit_n{n}.json").write_text(json.dumps(res, indent=1))
+        print(json.dumps({kk: v for kk, v in res.items() if not kk.endswith("_points")}))
+        for c in exc + stc:
+            print(f"  {c['point']:>12} fastest={c['measured_fastest']:9} margin={c['margin']:6.3f} "
+                  f"pred={c['predicted']:9} {'ok' if c['agree'] else ('MISS' if c['decisive'] else 'tie')} "
+                  f"{c['measured_us']}")
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
