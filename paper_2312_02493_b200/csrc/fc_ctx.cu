@@ -359,6 +359,7 @@ int run_layerwise(fc_ctx* c, int i, double cr, uint64_t ktot) {
     }
     fcb::Ctl* next = take_ctl(w);
     ws.nchunks = (unsigned)fcb::nchunks_of(len);
+    ws.batch = fcb::ef_batch(ws.nchunks, ws.ef_grid);
     int e = fcb::launch_ef(nullptr, src, len, kl, w.ctl, ws, fcb::Pending{}, 0, 1, 1 | force_fb, next,
                            c->stream);
     if (e) return fail(FC_ERR_CUDA, std::string("k_ef launch: ") + cudaGetErrorString(static_cast<cudaError_t>(e)));
@@ -638,6 +639,7 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
     s.ef_grid = ef_grid;
     s.err = c->d_err;
     s.coop = (o->flags & FC_FLAG_NO_COOPERATIVE) ? 0u : 1u;
+    s.batch = fcb::ef_batch(nch, ef_grid);  // packed candidate layout (EfLayout)
     TRY(c->alloc(&s.off, nch));
     TRY(c->alloc(&s.cnt, nch));
     TRY(c->alloc(&s.btot, 4096));
@@ -1553,6 +1555,8 @@ int fc_ag_step(fc_ctx* c, double cr, int compressor, fc_step_stats* st) {
   c->phase_stats = st != nullptr;
 
   // (1) error feedback + compression per worker (compress.hpp:114-130)
+  // (the threshold select reads per-chunk candidate slots: unpacked layout)
+  for (auto& w : c->w) w.ws.batch = compressor == FC_THRESHOLD ? 1u : fcb::ef_batch(c->nch, w.ws.ef_grid);
   record(c, 0);
   std::vector<uint64_t> kr(N, kk);  // selection size of every rank
   std::vector<uint64_t> mine(c->n_local, kk);

@@ -31,6 +31,7 @@ static_assert((1 << kDecShift) == kDecTile, "decode tile must be a power of two"
 constexpr int kShift1 = 19, kBins1 = 4096;    // bits 30..19 (exponent + 3 mantissa)
 
 constexpr int kSamples = 32768;                // candidate-bound sample size
+constexpr int kMaxGrid = 256;                  // grid of the one-block-per-SM kernels (>= SM count)
 
 // Per-worker control block.  Each worker has two, used by alternate steps; the
 // EF pass of one step zeroes the other for the next step.
@@ -60,6 +61,9 @@ struct Ctl {
   unsigned hist2[256];       // bits 18..11 of bucket-b1 candidates
   unsigned hist3[2048];      // bits 10..0
   unsigned hist_w[4096];     // window histogram: key bits 30..11 relative to Lkey (k_select)
+  unsigned done_sel;         // k_select_x: last-block counter (finalisation)
+  unsigned lb_flag[kMaxGrid];             // k_select_x look-back: block b's total is in
+  unsigned long long lb_tot[kMaxGrid];    // ... (gt << 32) | eq of block b
 };
 
 // Per-worker chunk workspace.  Chunk c's candidates occupy the fixed slot
@@ -78,7 +82,36 @@ struct ChunkWs {
   unsigned nchunks;
   unsigned ef_grid;
   unsigned coop;              // grid-barrier kernels launched cooperatively (default)
+  unsigned batch;             // EF work-queue batch (chunks per ticket) = candidate packing
 };
+
+// Candidate layout written by the EF pass and read by the select.  The EF
+// work queue hands out aligned batches of B consecutive chunks covering
+// [0, bnd) (bnd = the first multiple of B at or after 90 % of the chunks,
+// capped at nchunks), then single chunks; one warp processes a batch in chunk
+// order and writes the batch's candidate runs back to back from the batch's
+// first slot (B * 1024 slots, never overflowing).  A "segment" is a batch or
+// a single chunk: its candidates are contiguous from slot seg_base(c) << 10.
+// B = 1 is the plain per-chunk layout (the threshold select, the fallback).
+struct EfLayout {
+  unsigned B, bnd, nbat;
+  __host__ __device__ EfLayout(unsigned nchunks, unsigned b) {
+    B = b < 1 ? 1u : b;
+    const unsigned big = nchunks - nchunks / 10;
+    const unsigned long long up = ((unsigned long long)big + B - 1) / B * B;
+    bnd = B == 1 ? 0u : (unsigned)(up < nchunks ? up : nchunks);
+    nbat = (bnd + B - 1) / B;
+  }
+  __host__ __device__ bool seg_start(unsigned c) const { return c >= bnd || c % B == 0; }
+  __host__ __device__ unsigned seg_base(unsigned c) const { return c >= bnd ? c : c - c % B; }
+};
+// Batch size for a gradient of nchunks chunks on an EF grid of `blocks`
+// 8-warp blocks: 16 when every warp gets >= 4 such batches, 4 when it gets
+// >= 2 of 4, else 1 (small gradients: balance beats packing).
+__host__ __device__ inline unsigned ef_batch(uint64_t nchunks, unsigned blocks) {
+  const uint64_t warps = (uint64_t)blocks * 8;
+  return nchunks >= 64 * warps ? 16u : nchunks >= 8 * warps ? 4u : 1u;
+}
 
 // Sticky error words of a context (pinned host memory mapped into the device,
 // never reset by a step: the host reads them without synchronising and clears

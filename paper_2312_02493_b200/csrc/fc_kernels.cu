@@ -472,24 +472,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
   float sv = 0.f;
   if (sampling && q0 < (unsigned)kSamples) sv = sample_at(q0);
 
-  // Chunks are handed out dynamically (one atomic per chunk): SMs do not
-  // stream at equal rates, and a static split leaves a long tail.
+  // Chunks are handed out dynamically: SMs do not stream at equal rates, and
+  // a static split leaves a long tail.  Lane 0 takes a ticket (one atomic):
+  // tickets below nbat are the aligned batches of B chunks [tB, tB + B) that
+  // cover [0, bnd) (~90 % of the gradient), later tickets single chunks
+  // (short tail).  The mapping is fixed, so k_select_x knows which chunks
+  // one warp emitted back to back (EfLayout).
   const unsigned nchunks = w.nchunks;
   const unsigned nfull = (unsigned)(G >> kChunkShift);  // chunks fed by TMA
   constexpr unsigned kTx = kChunk * 4 * (kAdd ? 2 : 1) + (kPend ? 128 : 0);
-  // lane 0 takes chunks in batches of 4 (one shared counter caps the atomic
-  // rate) until the last ~10 %, then one at a time (short tail)
+  const EfLayout lay(nchunks, w.batch);
   unsigned q_next = 0, q_left = 0;
-  const unsigned big_until = nchunks - nchunks / 10;
   auto take = [&]() -> unsigned {
     if (q_left == 0) {
-      const unsigned n = q_next < big_until ? 4u : 1u;
-      q_next = atomicAdd(&ctl->ef_next, n);
-      q_left = n;
+      const unsigned t = atomicAdd(&ctl->ef_next, 1u);
+      if (t < lay.nbat) {
+        q_next = t * lay.B;
+        q_left = min(lay.B, lay.bnd - q_next);
+      } else {
+        q_next = lay.bnd + (t - lay.nbat);
+        q_left = 1;
+      }
     }
     --q_left;
     return q_next++;
   };
+  unsigned brun = 0;  // candidates this warp emitted so far in the current batch
   auto issue = [&](unsigned it) {  // lane 0 only: take the next chunk into stage it % kEfStages
     const unsigned s = it % kEfStages;
     const unsigned c = take();
@@ -651,7 +659,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
         w.cnt[c] = run;
         ncand += run;
       }
-      unsigned pos = (c << kChunkShift) + incl - n;
+      // packed candidate layout: the runs of one batch back to back from the
+      // batch's first slot (a single chunk: its own slot)
+      if (lay.seg_start(c)) brun = 0;
+      unsigned pos = (lay.seg_base(c) << kChunkShift) + brun + incl - n;
+      brun += run;
       const float* my = sge + lane * 32;
       for (unsigned m = mask; m; m &= m - 1) {
         const int p = __ffs(m) - 1;
@@ -1399,26 +1411,507 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
   }
 }
 
+// ---------------------------------------------------------------- select (x) ---
+// Exact Top-k of the EF pass's candidates (select_topk_indices,
+// inc/compress.hpp:38-53): the k largest |g_e|, ties to the lower index,
+// emitted in ascending index order.  One resident 1024-thread block per SM;
+// block b owns whole EF segments (EfLayout) of the chunk range
+// [b * cpb, (b + 1) * cpb).  The block's candidates form one "position
+// space": the segments' runs back to back, each padded to 4, and warp w
+// walks the contiguous position range [w R, (w + 1) R) 128 positions (one
+// float4 per lane) at a time -- coalesced reads, and position order is index
+// order, so ballots and warp scans place every selected pair.
+//   P1  load the block's candidates (values + indices into shared memory
+//       when they fit -- every later pass then reads shared memory), and
+//       histogram key bits 30..11 in a 4096-bin window from the sampled
+//       bound's prefix                                       -> grid barrier
+//   P2  the bin holding the k-th key (same in every block); count keys above
+//       it per warp, list the few keys inside it, histogram their low 11
+//       bits                                                  -> grid barrier
+//   P3  T and the ties to keep from the low-bit histogram; the listed keys
+//       settle the per-warp (> T, == T) counts; block totals are combined by
+//       a decoupled look-back over the earlier blocks (no grid barrier)
+//   P4  emission: per warp iteration one packed warp scan of (gt, eq) gives
+//       every selected pair its output position; ties are kept while the
+//       global tie rank is below needT (lowest index first); the block's
+//       contiguous output range is assembled in shared memory and written
+//       coalesced; the decode's chunk bounds come from the output list
+//   end the last block to finish sums the per-block ||top-k||^2 in block
+//       order (reproducible) and publishes to the peers
+// If the threshold lands outside the window (the sampled bound far off), the
+// three absolute radix digits (12 | 8 | 11 bits) run instead; if the
+// candidates hold fewer than k elements, the fallback builds the exact
+// digit-1 histogram of all of g_e and re-emits this block's segments first.
+constexpr int kSxThreads = 1024;
+constexpr int kSxWarps = kSxThreads / 32;
+constexpr unsigned kSxListCap = kSelBins / 2;  // u32 entries in the upper half of s_h
+
+__host__ __device__ inline unsigned sx_cpb(unsigned nch, unsigned grid, unsigned B) {
+  const unsigned c = (nch + grid - 1) / grid;
+  return (c + B - 1) / B * B;
+}
+
+__device__ __forceinline__ float f4c(const float4& v, int e) {
+  return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
+}
+__device__ __forceinline__ unsigned u4c(const uint4& v, int e) {
+  return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
+}
+
+__global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __restrict__ ctl, ChunkWs w,
+                                                            const float* __restrict__ ef_out, uint64_t G,
+                                                            unsigned* __restrict__ out_idx,
+                                                            float* __restrict__ out_val,
+                                                            unsigned* __restrict__ bounds_out, SelectMode mode) {
+  pdl_wait();
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  __shared__ __align__(16) unsigned s_h[kSelBins];
+  __shared__ unsigned long long s_red[kSxWarps];
+  __shared__ double s_dred[kSxWarps];
+  __shared__ unsigned s_wgt[kSxWarps], s_weq[kSxWarps];
+  __shared__ unsigned long long s_wpre[kSxWarps + 1];
+  __shared__ unsigned s_nl;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned lt = lanemask_lt();
+  unsigned bar = 0;  // grid barrier target (ctl->bar_sel)
+  SEL_MARK(0);
+  const unsigned nch = w.nchunks;
+  const EfLayout lay(nch, w.batch);
+  const unsigned cpb = sx_cpb(nch, gridDim.x, lay.B);
+  const unsigned c0 = min(nch, blockIdx.x * cpb), c1 = min(nch, c0 + cpb);
+  const unsigned al_end = min(c1, lay.bnd);
+  const unsigned nal = c0 < al_end ? (al_end - c0 + lay.B - 1) / lay.B : 0u;
+  const unsigned sg0 = max(c0, lay.bnd);
+  const unsigned S = nal + (c1 > sg0 ? c1 - sg0 : 0u);
+  auto seg_c0 = [&](unsigned j) -> unsigned { return j < nal ? c0 + j * lay.B : sg0 + (j - nal); };
+  auto seg_c1 = [&](unsigned j) -> unsigned { return j < nal ? min(c0 + (j + 1) * lay.B, al_end) : sg0 + (j - nal) + 1; };
+  unsigned* s_pos = reinterpret_cast<unsigned*>(s_dyn);  // S + 1 padded start positions
+  unsigned* s_sct = s_pos + S + 1;                         // S candidate counts
+  const unsigned tab_words = (2 * S + 1 + 3) & ~3u;
+  float* s_val = reinterpret_cast<float*>(s_dyn) + tab_words;
+  const unsigned cap = kSelSmemMax / 4 > tab_words ? kSelSmemMax / 4 - tab_words : 0u;
+
+  // ---- fallback (the sampled bound kept fewer than k elements) ----
+  const unsigned long long M = __ldcg(&ctl->cand_count);
+  const bool fb = M < k;
+  unsigned Lb = fb ? 0u : __ldcg(&ctl->Lkey);  // every candidate has key >= Lb
+  if (fb) {
+    if (blockIdx.x == 0 && tid == 0) ctl->fallback = 1;
+    for (int b = tid; b < kBins1; b += kSxThreads) s_h[b] = 0;
+    __syncthreads();
+    const uint64_t n4 = G / 4;
+    const float4* src4 = reinterpret_cast<const float4*>(ef_out);
+    for (uint64_t i = blockIdx.x * (uint64_t)kSxThreads + tid; i < n4; i += (uint64_t)gridDim.x * kSxThreads) {
+      const float4 x = __ldcg(src4 + i);
+      atomicAdd(&s_h[key_of(x.x) >> kShift1], 1u);
+      atomicAdd(&s_h[key_of(x.y) >> kShift1], 1u);
+      atomicAdd(&s_h[key_of(x.z) >> kShift1], 1u);
+      atomicAdd(&s_h[key_of(x.w) >> kShift1], 1u);
+    }
+    if (blockIdx.x == 0)
+      for (uint64_t i = n4 * 4 + tid; i < G; i += kSxThreads) atomicAdd(&s_h[key_of(ef_out[i]) >> kShift1], 1u);
+    flush_hist(s_h, ctl->hist_fb, kBins1);
+    grid_barrier(&ctl->bar_sel, bar, w.err);
+    unsigned bin;
+    unsigned long long above;
+    block_select_top<kSxThreads>(ctl->hist_fb, kBins1, k, bin, above, s_h);
+    const unsigned Lk = bin << kShift1;
+    if (blockIdx.x == 0 && tid == 0) ctl->Lkey = Lk;
+    // re-emit this block's segments in the packed layout (warp per segment)
+    for (unsigned j = warp; j < S; j += kSxWarps) {
+      const unsigned a = seg_c0(j), e = seg_c1(j);
+      const uint64_t sbase = (uint64_t)a << kChunkShift;  // a segment's first chunk is its base
+      unsigned pos = 0;
+      for (unsigned c = a; c < e; ++c) {
+        const uint64_t base = (uint64_t)c << kChunkShift;
+        unsigned cc = 0;
+        for (int r = 0; r < kChunk / 32; ++r) {
+          const uint64_t i = base + (uint64_t)r * 32 + lane;
+          const float x = i < G ? __ldcg(ef_out + i) : 0.f;
+          const bool on = i < G && key_of(x) >= Lk;
+          const unsigned bal = __ballot_sync(0xffffffffu, on);
+          if (on) {
+            const uint64_t q = sbase + pos + cc + __popc(bal & lt);
+            w.cand_idx[q] = (unsigned)i;
+            w.cand_val[q] = x;
+          }
+          cc += __popc(bal);
+        }
+        if (lane == 0) w.cnt[c] = cc;
+        pos += cc;
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    Lb = Lk;
+  }
+
+  // ---- the block's position space ----
+  for (unsigned j = tid; j < S; j += kSxThreads) {
+    unsigned n = 0;
+    for (unsigned c = seg_c0(j); c < seg_c1(j); ++c) n += __ldcg(w.cnt + c);
+    s_sct[j] = n;
+  }
+  __syncthreads();
+  {
+    const unsigned spt = (S + kSxThreads - 1) / kSxThreads;
+    const unsigned j0 = min(S, tid * spt), j1 = min(S, j0 + spt);
+    unsigned long long sum = 0;
+    for (unsigned j = j0; j < j1; ++j) sum += (s_sct[j] + 3u) & ~3u;
+    unsigned long long o = block_excl_scan<kSxThreads>(sum, s_red);
+    for (unsigned j = j0; j < j1; ++j) {
+      s_pos[j] = (unsigned)o;
+      o += (s_sct[j] + 3u) & ~3u;
+    }
+    if (j1 == S && j0 < j1) s_pos[S] = (unsigned)o;
+    if (S == 0 && tid == 0) s_pos[0] = 0;
+  }
+  __syncthreads();
+  const unsigned P = s_pos[S];
+  const bool cached = 2ull * P <= cap;
+  float4* s_val4 = reinterpret_cast<float4*>(s_val);
+  uint4* s_idx4 = reinterpret_cast<uint4*>(s_val + P);
+  // warp-contiguous ranges of 128-position steps
+  const unsigned R = (P + kSxWarps * 128 - 1) / (kSxWarps * 128) * 128;
+  const unsigned wlo = min(P, warp * R), whi = min(P, wlo + R);
+  const unsigned n_it = (whi - wlo + 127) / 128;
+  auto seg_of = [&](unsigned p) -> unsigned {  // last segment starting at or before p
+    unsigned lo = 0, hi = S;                   // s_pos[lo] <= p < s_pos[hi] (S >= 1 when P > 0)
+    while (hi - lo > 1) {
+      const unsigned mid = (lo + hi) >> 1;
+      if (s_pos[mid] <= p) lo = mid;
+      else hi = mid;
+    }
+    return lo;
+  };
+  // One pass over this warp's positions: f(v, id, nv) for every lane's float4
+  // group in position order (all lanes call f every iteration: warp-synchronous
+  // helpers may be used inside); nv = valid elements of the group (0..4).
+  // src 0: global candidates (+ store into shared memory when `stage`), 1:
+  // shared memory.
+  auto pass = [&](bool from_smem, bool with_idx, bool stage, auto&& f) {
+    if (n_it == 0) return;
+    unsigned sg = seg_of(min(wlo + lane * 4, P - 1));
+    constexpr int U = 2;
+    for (unsigned it0 = 0; it0 < n_it; it0 += U) {
+      float4 v[U];
+      uint4 id[U];
+      unsigned nv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const unsigned p = wlo + (it0 + u) * 128 + lane * 4;
+        nv[u] = 0;
+        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        id[u] = make_uint4(0, 0, 0, 0);
+        if (it0 + u < n_it && p < whi) {
+          while (s_pos[sg + 1] <= p) ++sg;
+          const unsigned off = p - s_pos[sg];
+          nv[u] = s_sct[sg] > off ? min(4u, s_sct[sg] - off) : 0u;
+          if (from_smem) {
+            v[u] = s_val4[p >> 2];
+            if (with_idx) id[u] = s_idx4[p >> 2];
+          } else if (nv[u]) {
+            const uint64_t g = ((uint64_t)seg_c0(sg) << kChunkShift) + off;
+            v[u] = __ldcg(reinterpret_cast<const float4*>(w.cand_val + g));
+            if (with_idx) id[u] = __ldcg(reinterpret_cast<const uint4*>(w.cand_idx + g));
+          }
+          if (stage) {
+            s_val4[p >> 2] = v[u];
+            s_idx4[p >> 2] = id[u];
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (it0 + u < n_it) f(v[u], id[u], nv[u]);
+    }
+  };
+
+  // ---- P1: window histogram (key bits 30..11 relative to Lb's prefix) ----
+  unsigned long long need = k;
+  unsigned prefix = 0;
+  bool windowed = false;
+  const unsigned wb = Lb >> 11;
+  for (int b = tid; b < kSelBins; b += kSxThreads) s_h[b] = 0;
+  __syncthreads();
+  pass(false, cached, cached, [&](const float4& v, const uint4&, unsigned nv) {
+    for (unsigned e = 0; e < nv; ++e) {
+      const unsigned hi = key_of(f4c(v, e)) >> 11;
+      if (hi >= wb) atomicAdd(&s_h[min(hi - wb, (unsigned)kSelBins - 1u)], 1u);
+    }
+  });
+  flush_hist(s_h, ctl->hist_w, kSelBins);
+  grid_barrier(&ctl->bar_sel, bar, w.err);
+  SEL_MARK(1);
+  {
+    unsigned bin;
+    unsigned long long above;
+    if (block_select_top<kSxThreads>(ctl->hist_w, kSelBins, need, bin, above, s_h) &&
+        bin < (unsigned)kSelBins - 1u) {
+      windowed = true;
+      need -= above;
+      prefix = wb + bin;
+    }
+  }
+  SEL_MARK(2);
+  unsigned T = 0;
+  unsigned long long needT = 0;
+  bool counted = false;  // per-warp (gt, eq) in s_wgt / s_weq
+  if (windowed) {
+    // ---- P2: keys above the prefix bin counted per warp; the keys inside
+    // it listed (warp, low 11 bits) and histogrammed ----
+    unsigned* s_list = s_h + kSelBins / 2;
+    for (int b = tid; b < kSelBins / 2; b += kSxThreads) s_h[b] = 0;
+    if (tid == 0) s_nl = 0;
+    __syncthreads();
+    const unsigned pf = prefix;
+    unsigned gt = 0;
+    pass(cached, false, false, [&](const float4& v, const uint4&, unsigned nv) {
+      for (unsigned e = 0; e < nv; ++e) {
+        const unsigned key = key_of(f4c(v, e)), hi = key >> 11;
+        gt += hi > pf;
+        if (hi == pf) {
+          atomicAdd(&s_h[key & 2047u], 1u);
+          const unsigned slot = atomicAdd(&s_nl, 1u);
+          if (slot < kSxListCap) s_list[slot] = ((unsigned)warp << 11) | (key & 2047u);
+        }
+      }
+    });
+    gt = (unsigned)warp_sum_u64(gt);
+    if (lane == 0) {
+      s_wgt[warp] = gt;
+      s_weq[warp] = 0;
+    }
+    flush_hist(s_h, ctl->hist3, 2048);
+    grid_barrier(&ctl->bar_sel, bar, w.err);
+    SEL_MARK(3);
+    unsigned bin;
+    unsigned long long above;
+    block_select_top<kSxThreads>(ctl->hist3, 2048, need, bin, above, s_h);
+    need -= above;
+    prefix = (prefix << 11) | bin;
+    const unsigned nl = s_nl;
+    if (nl <= kSxListCap) {
+      for (unsigned i = tid; i < nl; i += kSxThreads) {
+        const unsigned e = s_list[i], lo = e & 2047u, wq = e >> 11;
+        if (lo > bin) atomicAdd(&s_wgt[wq], 1u);
+        else if (lo == bin) atomicAdd(&s_weq[wq], 1u);
+      }
+      counted = true;
+    }
+  } else {
+    // ---- the three absolute digits (12 | 8 | 11 bits) ----
+    const int shifts[3] = {kShift1, 11, 0};
+    const int widths[3] = {12, 8, 11};
+    unsigned* ghs[3] = {ctl->hist1, ctl->hist2, ctl->hist3};
+    int as = 31;
+    for (int d = 0; d < 3; ++d) {
+      const int nb = 1 << widths[d], sh = shifts[d];
+      const unsigned pf = prefix, dm = (unsigned)nb - 1;
+      for (int b = tid; b < nb; b += kSxThreads) s_h[b] = 0;
+      __syncthreads();
+      pass(cached, false, false, [&](const float4& v, const uint4&, unsigned nv) {
+        for (unsigned e = 0; e < nv; ++e) {
+          const unsigned key = key_of(f4c(v, e));
+          if ((unsigned)((unsigned long long)key >> as) == pf) atomicAdd(&s_h[(key >> sh) & dm], 1u);
+        }
+      });
+      flush_hist(s_h, ghs[d], nb);
+      grid_barrier(&ctl->bar_sel, bar, w.err);
+      unsigned bin;
+      unsigned long long above;
+      block_select_top<kSxThreads>(ghs[d], nb, need, bin, above, s_h);
+      need -= above;
+      prefix = (prefix << widths[d]) | bin;
+      as = sh;
+    }
+    SEL_MARK(3);
+  }
+  T = prefix;
+  needT = need;
+  if (!counted) {
+    unsigned gt = 0, eq = 0;
+    pass(cached, false, false, [&](const float4& v, const uint4&, unsigned nv) {
+      for (unsigned e = 0; e < nv; ++e) {
+        const unsigned key = key_of(f4c(v, e));
+        gt += key > T;
+        eq += key == T;
+      }
+    });
+    gt = (unsigned)warp_sum_u64(gt);
+    eq = (unsigned)warp_sum_u64(eq);
+    if (lane == 0) {
+      s_wgt[warp] = gt;
+      s_weq[warp] = eq;
+    }
+  }
+  __syncthreads();
+
+  // ---- P3: per-warp prefixes, block total, look-back over earlier blocks ----
+  if (warp == 0) {
+    const unsigned long long x = ((unsigned long long)s_wgt[lane] << 32) | s_weq[lane];
+    const unsigned long long inc = warp_incl_scan(x);
+    s_wpre[lane] = inc - x;
+    if (lane == 31) s_wpre[kSxWarps] = inc;
+  }
+  __syncthreads();
+  const unsigned long long btot = s_wpre[kSxWarps];
+  if (tid == 0) {
+    ctl->lb_tot[blockIdx.x] = btot;
+    __threadfence();
+    atomicExch(&ctl->lb_flag[blockIdx.x], 1u);
+  }
+  unsigned long long mine = 0;
+  if (tid < (int)blockIdx.x) {
+    if (ld_acquire(&ctl->lb_flag[tid]) == 0u) {
+      const unsigned long long t0 = gtimer();
+      while (ld_acquire(&ctl->lb_flag[tid]) == 0u) {
+        __nanosleep(32);
+        if (gtimer() - t0 > kBarrierTimeoutNs) {
+          report_error(w.err, kErrBarrier);
+          break;
+        }
+      }
+    }
+    mine = __ldcg(&ctl->lb_tot[tid]);
+  }
+  const unsigned long long bp = block_sum_u64<kSxThreads>(mine, s_red);
+  SEL_MARK(4);
+  const unsigned long long bgt_pre = bp >> 32, beq_pre = bp & 0xffffffffull;
+  const unsigned long long avail = needT > beq_pre ? needT - beq_pre : 0ull;  // ties this block may keep
+  const unsigned long long obase = bgt_pre + min(beq_pre, needT);
+  const unsigned long long nsel = (btot >> 32) + min(btot & 0xffffffffull, avail);
+  const unsigned used = cached ? 2 * P : 0u;
+  const bool staged = (unsigned long long)used + 2 * nsel <= cap;
+  unsigned* s_oidx = reinterpret_cast<unsigned*>(s_val + used);
+  float* s_oval = reinterpret_cast<float*>(s_oidx + (staged ? nsel : 0));
+
+  // ---- P4: emission ----
+  double acc = 0.0;
+  {
+    unsigned long long grun = s_wpre[warp] >> 32, erun = s_wpre[warp] & 0xffffffffull;
+    const unsigned ibase = mode.idx_base;
+    pass(cached, true, false, [&](const float4& v, const uint4& id, unsigned nv) {
+      unsigned gm = 0, em = 0;
+      for (unsigned e = 0; e < nv; ++e) {
+        const unsigned key = key_of(f4c(v, e));
+        gm |= (key > T ? 1u : 0u) << e;
+        em |= (key == T ? 1u : 0u) << e;
+      }
+      const unsigned x = (__popc(gm) << 16) | __popc(em);
+      unsigned inc = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      const unsigned tot = __shfl_sync(0xffffffffu, inc, 31);
+      const unsigned ex = inc - x;
+      unsigned long long gb = grun + (ex >> 16), eb = erun + (ex & 0xffffu);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const bool g = (gm >> e) & 1u, q = (em >> e) & 1u;
+        if (g || (q && eb < avail)) {
+          const unsigned long long pos = gb + min(eb, avail);
+          const float xv = f4c(v, e);
+          const unsigned iv = u4c(id, e) + ibase;
+          if (staged) {
+            s_oidx[pos] = iv;
+            s_oval[pos] = xv;
+          } else {
+            out_idx[obase + pos] = iv;
+            out_val[obase + pos] = xv;
+          }
+          acc = fma((double)xv, (double)xv, acc);
+        }
+        gb += g;
+        eb += q;
+      }
+      grun += tot >> 16;
+      erun += tot & 0xffffu;
+    });
+  }
+  __syncthreads();
+  SEL_MARK(5);
+  if (staged)
+    for (unsigned i = tid; i < nsel; i += kSxThreads) {
+      out_idx[obase + i] = s_oidx[i];
+      out_val[obase + i] = s_oval[i];
+    }
+  // the decode's chunk bounds of [c0, c1): first output position >= chunk c
+  if (bounds_out) {
+    const unsigned* oi = staged ? s_oidx : out_idx + obase;
+    const unsigned ibase = mode.idx_base;
+    for (unsigned i = tid; i < nsel; i += kSxThreads) {
+      const long long ci = (long long)((oi[i] - ibase) >> kChunkShift);
+      const long long cp = i ? (long long)((oi[i - 1] - ibase) >> kChunkShift) : (long long)c0 - 1;
+      for (long long t = cp + 1; t <= ci; ++t) bounds_out[t] = (unsigned)(obase + i);
+    }
+    const long long cl = nsel ? (long long)((oi[nsel - 1] - ibase) >> kChunkShift) : (long long)c0 - 1;
+    for (long long t = cl + 1 + tid; t < (long long)c1; t += kSxThreads) bounds_out[t] = (unsigned)(obase + nsel);
+  }
+  const double bsum = block_sum<kSxThreads>(acc, s_dred);
+  if (tid == 0) {
+    w.bnorm[blockIdx.x] = bsum;
+    if (mode.publish) __threadfence_system();  // this block's output before the publish
+  }
+  pdl_trigger();
+  SEL_MARK(6);
+  if (!last_block_done(&ctl->done_sel)) return;
+  const double tot = block_sum_array<kSxThreads>(w.bnorm, gridDim.x, s_dred);
+  if (tid == 0) {
+    ctl->topk_norm2 = tot;
+    ctl->T = T;
+    ctl->needT = needT;
+    ctl->count_gt = k - needT;
+    ctl->b1 = T >> kShift1;
+    ctl->b2 = windowed;
+    if (bounds_out) bounds_out[nch] = (unsigned)k;
+    if (mode.publish) {  // every block's output is in; ||top-k||^2 with it (VAR)
+      for (int t = 0; t < mode.pb.n; ++t) reinterpret_cast<double*>(mode.pb.box[t] + mode.pb.rank * 8)[4] = tot;
+      __threadfence_system();
+      publish_all(mode.pb, 0, mode.epoch);
+      if (mode.publish_contrib) publish_all(mode.pb, 1, mode.epoch);
+    }
+  }
+  SEL_MARK(7);
+}
+
 // Grid of the select: one resident 1024-thread block per SM.
 int launch_select(uint64_t k, Ctl* ctl, const ChunkWs& w, const float* ef_out, uint64_t G,
                   unsigned* out_idx, float* out_val, unsigned* bounds_out, const SelectMode& m,
                   cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelSmemMax);
-    attr = true;
-  }
   const int grid = num_sms();
-  const unsigned cpb = (w.nchunks + grid - 1) / grid;
-  if (cpb > (unsigned)kSelMaxCpb) return (int)cudaErrorInvalidValue;
-  const unsigned smem = sel_arrays_bytes(cpb) + sel_cache_cap(cpb) * 4u;
+  if (grid > kMaxGrid) return (int)cudaErrorInvalidValue;
   ChunkWs ws = w;
   SelectMode mode = m;
   void* args[] = {&k, &ctl, &ws, &ef_out, &G, &out_idx, &out_val, &bounds_out, &mode};
-  // one resident 1024-thread block per SM (~217 KB shared), software grid
-  // barriers (grid_barrier); cooperative unless the context opted out
-  const cudaError_t e =
-      launch_grid_sync((const void*)k_select, dim3(grid), dim3(kSelThreads), smem, s, args, w.coop != 0);
+  cudaError_t e;
+  if (m.rounds == 0) {
+    // exact Top-k: k_select_x over the packed candidate layout
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_select_x, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelSmemMax);
+      attr = true;
+    }
+    const unsigned cpb = sx_cpb(w.nchunks, grid, EfLayout(w.nchunks, w.batch).B);
+    if (2ull * cpb + 8 > kSelSmemMax / 4) return (int)cudaErrorInvalidValue;
+    e = launch_grid_sync((const void*)k_select_x, dim3(grid), dim3(kSxThreads), kSelSmemMax, s, args, w.coop != 0);
+  } else {
+    // threshold compressor: k_select (bisection), per-chunk candidate slots
+    if (w.batch > 1) return (int)cudaErrorInvalidValue;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelSmemMax);
+      attr = true;
+    }
+    const unsigned cpb = (w.nchunks + grid - 1) / grid;
+    if (cpb > (unsigned)kSelMaxCpb) return (int)cudaErrorInvalidValue;
+    const unsigned smem = sel_arrays_bytes(cpb) + sel_cache_cap(cpb) * 4u;
+    // one resident 1024-thread block per SM (~217 KB shared), software grid
+    // barriers (grid_barrier); cooperative unless the context opted out
+    e = launch_grid_sync((const void*)k_select, dim3(grid), dim3(kSelThreads), smem, s, args, w.coop != 0);
+  }
   count_launch();
   return e == cudaSuccess ? 0 : (int)e;
 }
@@ -2195,14 +2688,116 @@ __global__ void __launch_bounds__(kThreads) k_decode_ag(const unsigned* __restri
   if (threadIdx.x == 0) bulk_wait_all();
 }
 
+// The same decode for at most NR ranks with the latency chain cut: every
+// rank's chunk bounds of the NEXT tile are loaded while this tile is built,
+// and the first list entry of every rank is loaded before the rank-ordered
+// scatter starts, so a tile costs one dependent load round instead of two
+// per rank (the per-rank passes keep their barriers: the reference's
+// rank-ascending summation order, artopk.hpp:154-158).
+template <int NR>
+__global__ void __launch_bounds__(kThreads) k_decode_ag_n(const unsigned* __restrict__ packs,
+                                                          uint64_t pack_stride, uint64_t k, int nranks,
+                                                          const unsigned* __restrict__ bounds,
+                                                          float divisor, float* __restrict__ agg, uint64_t G,
+                                                          unsigned* __restrict__ zmaps, int map_rank0, int nmaps) {
+  pdl_wait();
+  __shared__ __align__(128) float tile[2][kDecTile];
+  __shared__ unsigned s_touch[kDecTile / 32];
+  extern __shared__ unsigned s_zm[];  // nmaps x kDecChunks*32
+  const uint64_t ntd = (G + kDecTile - 1) >> kDecShift;
+  const uint64_t nch = nchunks_of(G);
+  const int zw = kDecChunks * 32;
+  const bool divide = divisor != 1.0f;
+  unsigned nlo[NR], nhi[NR];
+  auto load_bounds = [&](uint64_t t) {
+    const uint64_t c0 = t * kDecChunks, c1 = min(c0 + kDecChunks, nch);
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      nlo[r] = nhi[r] = 0;
+      if (r < nranks) {
+        const unsigned* bd = bounds + (uint64_t)r * (nch + 1);
+        nlo[r] = __ldg(bd + c0);
+        nhi[r] = __ldg(bd + c1);
+      }
+    }
+  };
+  if (blockIdx.x < ntd) load_bounds(blockIdx.x);
+  int buf = 0, iter = 0;
+  for (uint64_t t = blockIdx.x; t < ntd; t += gridDim.x, buf ^= 1, ++iter) {
+    const uint64_t t0 = t << kDecShift;
+    unsigned lo[NR], hi[NR], p0[NR];
+    float v0[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      lo[r] = nlo[r];
+      hi[r] = nhi[r];
+      p0[r] = 0;
+      v0[r] = 0.f;
+      const unsigned j = lo[r] + threadIdx.x;
+      if (r < nranks && j < hi[r]) {
+        const unsigned* id = packs + (uint64_t)r * pack_stride;
+        p0[r] = id[j];
+        v0[r] = reinterpret_cast<const float*>(id + k)[j];
+      }
+    }
+    if (t + gridDim.x < ntd) load_bounds(t + gridDim.x);
+    if (iter >= 2 && threadIdx.x == 0) bulk_wait_read1();
+    __syncthreads();
+    float* tl = tile[buf];
+    zero_tile(tl);
+    for (int q = threadIdx.x; q < nmaps * zw; q += kThreads) s_zm[q] = 0u;
+    if (threadIdx.x < kDecTile / 32) s_touch[threadIdx.x] = 0u;
+    __syncthreads();
+    const uint64_t c0 = t * kDecChunks, c1 = min(c0 + kDecChunks, nch);
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      if (r < nranks) {
+        const unsigned* id = packs + (uint64_t)r * pack_stride;
+        const float* va = reinterpret_cast<const float*>(id + k);
+        const int m = r - map_rank0;
+        const bool mapped = m >= 0 && m < nmaps;
+        for (unsigned j = lo[r] + threadIdx.x; j < hi[r]; j += kThreads) {
+          const bool first = j == lo[r] + threadIdx.x;
+          const unsigned p = first ? p0[r] : id[j];
+          const unsigned lp = p - (unsigned)t0;
+          tl[lp] += first ? v0[r] : va[j];
+          if (divide) atomicOr(&s_touch[lp >> 5], 1u << (lp & 31));
+          if (mapped) atomicOr(&s_zm[m * zw + zmap_word(p) - (unsigned)(c0 << 5)], zmap_bit(p));
+        }
+        __syncthreads();
+      }
+    }
+    if (divide && threadIdx.x < kDecTile / 32) {
+      for (unsigned b = s_touch[threadIdx.x]; b; b &= b - 1) {
+        float& x = tl[threadIdx.x * 32 + __ffs(b) - 1];
+        x = x / divisor;
+      }
+    }
+    emit_tile(agg, tl, t0, G);
+    const unsigned nw = (unsigned)(c1 - c0) * 32;
+    for (int q = threadIdx.x; q < nmaps * zw; q += kThreads) {
+      const int m = q / zw, wq = q - m * zw;
+      if ((unsigned)wq < nw) zmaps[(uint64_t)m * (nch << 5) + (c0 << 5) + wq] = s_zm[q];
+    }
+  }
+  pdl_trigger();
+  if (threadIdx.x == 0) bulk_wait_all();
+}
+
 void launch_decode_ag(const unsigned* packs, uint64_t pack_stride, uint64_t k, int nranks,
                       const unsigned* bounds, float divisor, float* agg, uint64_t G,
                       unsigned* zmaps, int map_rank0, int nmaps, cudaStream_t s) {
   const size_t smem = (size_t)nmaps * kDecChunks * 32 * sizeof(unsigned);
-  if (smem > 16 * 1024)
-    cudaFuncSetAttribute(k_decode_ag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  launch_pdl(k_decode_ag, num_sms() * 6, kThreads, smem, s, packs, pack_stride, k, nranks, bounds, divisor,
-                                                     agg, G, zmaps, map_rank0, nmaps);
+  auto go = [&](auto kern) {
+    if (smem > 16 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    launch_pdl(kern, num_sms() * 6, kThreads, smem, s, packs, pack_stride, k, nranks, bounds, divisor, agg, G,
+               zmaps, map_rank0, nmaps);
+  };
+  if (nranks <= 1) go(k_decode_ag_n<1>);
+  else if (nranks <= 2) go(k_decode_ag_n<2>);
+  else if (nranks <= 4) go(k_decode_ag_n<4>);
+  else if (nranks <= 8) go(k_decode_ag_n<8>);
+  else go(k_decode_ag);
   count_launch();
 }
 
@@ -2232,7 +2827,8 @@ void launch_dense_sum(const float* lists, int nlists, uint64_t list_stride, int 
 static void prefer_max_smem() {
   const void* fs[] = {(const void*)k_fill_synth, (const void*)k_gather, (const void*)k_agg_clear,
                       (const void*)k_agg_write, (const void*)k_zero_at, (const void*)k_bounds,
-                      (const void*)k_decode_ar<0>, (const void*)k_decode_ar<1>, (const void*)k_decode_ar<2>, (const void*)k_decode_ag, (const void*)k_dense_sum,
+                      (const void*)k_decode_ar<0>, (const void*)k_decode_ar<1>, (const void*)k_decode_ar<2>, (const void*)k_decode_ag, (const void*)k_decode_ag_n<1>, (const void*)k_decode_ag_n<2>,
+                      (const void*)k_decode_ag_n<4>, (const void*)k_decode_ag_n<8>, (const void*)k_dense_sum,
                       (const void*)k_sum_fixed};
   for (const void* f : fs)
     cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);

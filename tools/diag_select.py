@@ -11,7 +11,7 @@ from paper_2312_02493_b200._abi import FC_FLAG_DENSE_DECODE, check, lib  # noqa:
 G = int(sys.argv[1]) if len(sys.argv) > 1 else 138_000_000
 cr = float(sys.argv[2]) if len(sys.argv) > 2 else 0.01
 flags = FC_FLAG_DENSE_DECODE if "dense" in sys.argv[3:] else 0
-names = ["staged", "digit1", "digit2", "digit3", "counted", "emitted", "end"]
+names = ["load+window+bar", "windowbin", "inbin+bar", "T+lookback", "emit", "write+bounds", "final"]
 with fc.Cluster(1, G, max_cr=max(cr, 0.1), flags=flags) as cl:
     cl.fill_synthetic(0, 42, 0, 0)
     for s in range(4):
