@@ -404,6 +404,46 @@ def main():
     except Exception:
         pass
 
+    # ---- exchange phase alone (N > 1): bus GB/s of the collective ----------
+    # The product's own exchange kernels timed back to back with the lists in
+    # place (fc_diag_exchange_ms: from the selections' publish to the point
+    # where the decode could start), max over ranks; bus bytes follow the
+    # NCCL-tests convention (broadcast 4k + allreduce 2(N-1)/N 4k for ART,
+    # (N-1) 8k for AG, 2(N-1)/N 4G for the dense allreduce).
+    exchange = None
+    if world > 1:
+        try:
+            import ctypes as C
+
+            k_ex = fc.k_of(a.cr, G)
+            if mode == 3:
+                ex_ms = ms  # the dense step is the allreduce
+                ex_bus = 2.0 * (world - 1) / world * 4.0 * G
+                how = "the dense step (one ncclAllReduce of 4G bytes, ncclAvg)"
+            else:
+                which = 0 if mode == 2 else (2 if algo == 1 else 1)
+                out = C.c_double()
+                barrier()
+                rc = fc.lib.fc_diag_exchange_ms(cl._ctx, which, k_ex, 20, C.byref(out))
+                if rc != 0:
+                    raise RuntimeError(fc.lib.fc_last_error().decode())
+                ex_ms = max_over_ranks(out.value)
+                ex_bus = (world - 1) * 8.0 * k_ex if mode == 2 else 4.0 * k_ex + 2.0 * (world - 1) / world * 4.0 * k_ex
+                how = ("fc_diag_exchange_ms: the step's exchange kernels (" +
+                       ("list publish + k_collect_packs" if mode == 2 else
+                        "list publish + k_fetch_gather + " + ("k_reduce_root" if algo == 1 else
+                                                             ("k_reduce_slice" if world > 2 else "direct push")))
+                       + ") back to back, max over ranks; peer memory" if cl.peer_exchange else
+                       "fc_diag_exchange_ms (NCCL collectives)")
+                # the diagnostic leaves no selection behind: re-run one step
+                step(20_000)
+                barrier()
+            exchange = {"ms": round(ex_ms, 4), "bus_bytes": ex_bus,
+                        "bus_gbs": round(ex_bus / (ex_ms * 1e-3) / 1e9, 1), "bus_peak_gbs": 900.0,
+                        "frac": round(ex_bus / (ex_ms * 1e-3) / 1e9 / 900.0, 3), "timing": how}
+        except Exception as e:  # diagnostics never fail the bench
+            exchange = {"unavailable": str(e)[:200]}
+
     # ---- end-to-end through the public API with host buffers --------------
     # A host-fed user creates the context with FC_FLAG_PIPELINE (two gradient
     # and two aggregate buffers).  Every step: upload of the step's gradient
@@ -481,7 +521,8 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": bench_config(a, world),
             "hbm_gbs_step": round(step_gbs, 1),
-            "bus_gbs": round(bus / (ms * 1e-3) / 1e9, 2) if bus else 0.0,
+            "bus_gbs_step": round(bus / (ms * 1e-3) / 1e9, 2) if bus else 0.0,
+            "exchange": exchange,
             "bus_peak_gbs": 900.0,
             "roofline": {"kernel": "k_ef (error feedback + candidate emission)", "bound": "hbm",
                          "achieved": round(achieved, 1) if achieved else None, "peak": peak,

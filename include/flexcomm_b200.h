@@ -173,6 +173,17 @@ int fc_num_workers(const fc_ctx* ctx, int* n_local, int* world, int* rank);
  * (ResidualStore::of uses vector::at, inc/core.hpp:91). */
 int fc_set_grad(fc_ctx* ctx, int worker, const float* src, int memkind);
 int fc_grad_ptr(fc_ctx* ctx, int worker, float** dev_ptr);
+/* fp64 host buffers, as the reference holds them (DenseGrad::values is a
+ * std::vector<double>, inc/core.hpp:60-70): converted to / from fp32 by a
+ * small host thread pool through pinned staging chunks pipelined with the
+ * copy engine (PCIe carries fp32).  fc_set_grad_f64 returns once the upload
+ * is queued in FC_FLAG_ASYNC contexts (the step waits for it; src must stay
+ * valid until fc_sync), otherwise once it landed; the getters return the
+ * data (synchronous). */
+int fc_set_grad_f64(fc_ctx* ctx, int worker, const double* src);
+int fc_set_residual_f64(fc_ctx* ctx, int worker, const double* src);
+int fc_get_residual_f64(fc_ctx* ctx, int worker, double* dst);
+int fc_get_aggregate_f64(fc_ctx* ctx, double* dst);
 int fc_fill_synthetic(fc_ctx* ctx, int worker, uint64_t seed, uint32_t rank, uint64_t step,
                       int dist);
 int fc_set_residual(fc_ctx* ctx, int worker, const float* src, int memkind);
@@ -337,11 +348,12 @@ int fc_set_ef_timing_period(fc_ctx* ctx, int period);
  * 6 EF + emission + owed zeros. */
 int fc_diag_kernel_ms(fc_ctx* ctx, int which, int iters, double* ms_out);
 /* Diagnostics: %globaltimer (ns) at the select kernel's phase boundaries of
- * the last step (start, staged, digit 1/2/3 resolved, counted, emitted, end),
- * then the EF kernel's (start, sample barrier passed, bound derived, end of
- * block 0's stream), then two EF marks (sample histogrammed, flushed), then two
- * select emission marks (output base known, pairs assembled): out12 holds 16
- * values. */
+ * the last step (8 marks: start, window resolved, window bin, low digits,
+ * look-back, emitted, written, end), then the EF kernel's (start, sample
+ * barrier passed, bound derived, end of block 0's stream), then two EF marks
+ * (sample histogrammed, flushed) and two spare, then 8 select sub-phase marks
+ * (values loaded, window flushed, in-bin pass, indices staged, output
+ * written, bounds fixed, 2 spare): out12 holds 24 values (block 0). */
 int fc_diag_select_phases(fc_ctx* ctx, int worker, uint64_t* out12);
 /* Diagnostics: %globaltimer (ns) at the start and end of every EF block of the
  * last step (2 x grid values, grid = number of SMs), followed (as n allows) by

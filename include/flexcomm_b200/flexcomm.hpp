@@ -233,25 +233,25 @@ class Context {
   int world() const { return world_; }
   int rank() const { return rank_; }
 
+  // fp64 <-> fp32 conversion by the library's host thread pool through
+  // pinned staging chunks pipelined with the copy engine (fc_*_f64)
   void set_grad(int worker, const std::vector<double>& g) {
     if (g.size() != g_) throw std::invalid_argument("gradient length mismatch");
-    buf_.assign(g.begin(), g.end());
-    check(fc_set_grad(ctx_, worker, buf_.data(), FC_HOST));
+    check(fc_set_grad_f64(ctx_, worker, g.data()));
   }
   void set_residual(int worker, const std::vector<double>& r) {
     if (r.size() != g_) throw std::invalid_argument("residual length mismatch");
-    buf_.assign(r.begin(), r.end());
-    check(fc_set_residual(ctx_, worker, buf_.data(), FC_HOST));
+    check(fc_set_residual_f64(ctx_, worker, r.data()));
   }
   std::vector<double> residual(int worker) {
-    buf_.resize(g_);
-    check(fc_get_residual(ctx_, worker, buf_.data(), FC_HOST));
-    return std::vector<double>(buf_.begin(), buf_.end());
+    std::vector<double> out(g_);
+    check(fc_get_residual_f64(ctx_, worker, out.data()));
+    return out;
   }
   std::vector<double> aggregate() {
-    buf_.resize(g_);
-    check(fc_get_aggregate(ctx_, buf_.data(), FC_HOST));
-    return std::vector<double>(buf_.begin(), buf_.end());
+    std::vector<double> out(g_);
+    check(fc_get_aggregate_f64(ctx_, out.data()));
+    return out;
   }
   SparseGrad topk(int worker) {
     uint64_t k = 0;
@@ -286,7 +286,6 @@ class Context {
   fc_ctx* ctx_ = nullptr;
   std::size_t g_ = 0;
   int n_local_ = 1, world_ = 1, rank_ = 0;
-  std::vector<float> buf_;
 };
 
 // The reference's Cluster (inc/collectives.hpp:15-33) plus the device context

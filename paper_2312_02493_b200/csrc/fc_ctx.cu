@@ -22,6 +22,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "fc_device.cuh"
@@ -140,6 +141,11 @@ struct fc_ctx {
   // once reported
   unsigned* h_err = nullptr;
   unsigned* d_err = nullptr;  // the same words, device view
+  // fp64 host buffers (fc_*_f64, the reference's DenseGrad): per host thread a
+  // pinned fp32 staging chunk and an event (created on first use)
+  std::vector<float*> f64_stage;
+  std::vector<cudaEvent_t> f64_ev;
+  unsigned f64_threads = 0;
   int* dsel = nullptr;        // VAR winner chosen on the device (NCCL)
   // peer-memory exchange (NCCL contexts, 1 < world <= 8, every rank's
   // exchange buffer mapped into every other with CUDA IPC over NVLink)
@@ -787,6 +793,8 @@ int fc_destroy(fc_ctx* c) {
     if (w.snap) cudaFree(w.snap);
   if (c->h_norms) cudaFreeHost(c->h_norms);
   if (c->h_err) cudaFreeHost(c->h_err);
+  for (float* q : c->f64_stage) cudaFreeHost(q);
+  for (cudaEvent_t e : c->f64_ev) cudaEventDestroy(e);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   for (auto& pr : c->ef_pending) {
@@ -833,6 +841,131 @@ int fc_set_grad(fc_ctx* c, int worker, const float* src, int memkind) {
   }
   TRY(wait_grad(c, worker));
   return copy_in(c, c->w[worker].g_o, src, memkind);
+}
+
+// ---- fp64 host buffers (the reference's DenseGrad is std::vector<double>) --
+// A host thread pool converts chunk j (fp64 -> fp32, or back) through its own
+// pinned staging chunk while the copy engine moves the previous ones: PCIe
+// carries fp32 only, and no single-threaded conversion pass or pageable copy
+// sits on the path.  Thread t handles chunks t, t + T, ...
+namespace {
+constexpr uint64_t kF64Chunk = 4ull << 20;  // floats per staging chunk (16 MB)
+
+int f64_setup(fc_ctx* c) {
+  if (c->f64_threads) return FC_OK;
+  const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+  const unsigned T = std::min(8u, std::max(1u, hw / 2));
+  for (unsigned t = 0; t < T; ++t) {
+    float* q = nullptr;
+    cudaEvent_t e = nullptr;
+    CUDA_TRY(cudaMallocHost(&q, kF64Chunk * sizeof(float)));
+    CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->f64_stage.push_back(q);
+    c->f64_ev.push_back(e);
+  }
+  c->f64_threads = T;
+  return FC_OK;
+}
+
+// dev[0, n) <- (float) src[0, n), chunked through the staging on stream s
+int f64_upload(fc_ctx* c, float* dev, const double* src, uint64_t n, cudaStream_t s) {
+  TRY(f64_setup(c));
+  const unsigned T = c->f64_threads;
+  const uint64_t nchk = (n + kF64Chunk - 1) / kF64Chunk;
+  std::vector<int> rc(T, FC_OK);
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < T; ++t)
+    th.emplace_back([&, t] {
+      cudaSetDevice(c->device);
+      for (uint64_t j = t; j < nchk; j += T) {
+        const uint64_t a = j * kF64Chunk, m = std::min(kF64Chunk, n - a);
+        if (cudaEventSynchronize(c->f64_ev[t]) != cudaSuccess) { rc[t] = FC_ERR_CUDA; return; }
+        float* q = c->f64_stage[t];
+        for (uint64_t i = 0; i < m; ++i) q[i] = static_cast<float>(src[a + i]);
+        if (cudaMemcpyAsync(dev + a, q, m * sizeof(float), cudaMemcpyHostToDevice, s) != cudaSuccess ||
+            cudaEventRecord(c->f64_ev[t], s) != cudaSuccess) { rc[t] = FC_ERR_CUDA; return; }
+      }
+    });
+  for (auto& x : th) x.join();
+  for (int r : rc)
+    if (r != FC_OK) return fail(r, "fp64 upload: CUDA copy failed");
+  return FC_OK;
+}
+
+// dst[0, n) <- (double) dev[0, n), after everything queued on `after`
+int f64_download(fc_ctx* c, double* dst, const float* dev, uint64_t n, cudaStream_t after) {
+  TRY(f64_setup(c));
+  const unsigned T = c->f64_threads;
+  cudaEvent_t ready = c->take_event();
+  CUDA_TRY(cudaEventRecord(ready, after));
+  const uint64_t nchk = (n + kF64Chunk - 1) / kF64Chunk;
+  std::vector<int> rc(T, FC_OK);
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < T; ++t)
+    th.emplace_back([&, t] {
+      cudaSetDevice(c->device);
+      cudaStream_t s = nullptr;
+      if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaStreamWaitEvent(s, ready, 0) != cudaSuccess) { rc[t] = FC_ERR_CUDA; return; }
+      float* q = c->f64_stage[t];
+      for (uint64_t j = t; j < nchk; j += T) {
+        const uint64_t a = j * kF64Chunk, m = std::min(kF64Chunk, n - a);
+        if (cudaMemcpyAsync(q, dev + a, m * sizeof(float), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess) { rc[t] = FC_ERR_CUDA; break; }
+        for (uint64_t i = 0; i < m; ++i) dst[a + i] = q[i];
+      }
+      cudaStreamDestroy(s);
+    });
+  for (auto& x : th) x.join();
+  c->ev_pool.push_back(ready);
+  for (int r : rc)
+    if (r != FC_OK) return fail(r, "fp64 download: CUDA copy failed");
+  return FC_OK;
+}
+}  // namespace
+
+int fc_set_grad_f64(fc_ctx* c, int worker, const double* src) {
+  TRY(check_worker(c, worker));
+  if (!src) return fail(FC_ERR_INVALID_ARGUMENT, "null source pointer");
+  CUDA_TRY(cudaSetDevice(c->device));
+  // after the last reader of this gradient buffer, like an FC_HOST_ASYNC upload
+  const int q = go_slot(c, worker);
+  if (c->go_read[q]) CUDA_TRY(cudaStreamWaitEvent(c->s_h2d, c->ev_go_free[q], 0));
+  TRY(f64_upload(c, c->w[worker].g_o, src, c->G, c->s_h2d));
+  CUDA_TRY(cudaEventRecord(c->ev_go_ready[q], c->s_h2d));
+  c->go_pending[q] = 1;
+  if (!(c->flags & FC_FLAG_ASYNC)) CUDA_TRY(cudaStreamSynchronize(c->s_h2d));
+  return FC_OK;
+}
+
+int fc_set_residual_f64(fc_ctx* c, int worker, const double* src) {
+  TRY(check_worker(c, worker));
+  if (!src) return fail(FC_ERR_INVALID_ARGUMENT, "null source pointer");
+  CUDA_TRY(cudaSetDevice(c->device));
+  Worker& w = c->w[worker];
+  w.pz = fcb::Pending{};  // overwritten wholesale: owed zeros are void
+  w.pz_idx = nullptr;
+  w.pz_k = 0;
+  CUDA_TRY(cudaStreamSynchronize(c->stream));  // no kernel is using the residual store
+  TRY(f64_upload(c, w.ge, src, c->G, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return FC_OK;
+}
+
+int fc_get_residual_f64(fc_ctx* c, int worker, double* dst) {
+  TRY(check_worker(c, worker));
+  if (!dst) return fail(FC_ERR_INVALID_ARGUMENT, "null destination pointer");
+  CUDA_TRY(cudaSetDevice(c->device));
+  TRY(materialize(c, c->w[worker]));
+  return f64_download(c, dst, c->w[worker].ge, c->G, c->stream);
+}
+
+int fc_get_aggregate_f64(fc_ctx* c, double* dst) {
+  if (!c) return fail(FC_ERR_INVALID_ARGUMENT, "null context");
+  if (!dst) return fail(FC_ERR_INVALID_ARGUMENT, "null destination pointer");
+  CUDA_TRY(cudaSetDevice(c->device));
+  TRY(wait_agg_free(c, c->agg_cur));
+  return f64_download(c, dst, c->agg, c->G, c->stream);
 }
 
 int fc_grad_ptr(fc_ctx* c, int worker, float** p) {
@@ -1261,7 +1394,7 @@ int fc_diag_select_phases(fc_ctx* c, int worker, uint64_t* out12) {
   if (!out12) return fail(FC_ERR_INVALID_ARGUMENT, "null output");
   CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
-  CUDA_TRY(cudaMemcpy(out12, &c->w[worker].ctl->tphase[0], 16 * sizeof(uint64_t),
+  CUDA_TRY(cudaMemcpy(out12, &c->w[worker].ctl->tphase[0], 24 * sizeof(uint64_t),
                       cudaMemcpyDeviceToHost));
   return FC_OK;
 }

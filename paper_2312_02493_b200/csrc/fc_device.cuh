@@ -54,6 +54,7 @@ struct Ctl {
   unsigned long long tphase[8];  // %globaltimer at k_select phase boundaries (diagnostics)
   unsigned long long tphase_ef[4];  // ... and at k_ef's (start, sampled, bound, end)
   unsigned long long tphase_ef2[4];  // k_ef: sample loaded, local histogram flushed; k_select: emission sub-phases
+  unsigned long long tphase_sx[8];   // k_select_x sub-phases (block 0; diagnostics)
   unsigned hist_s[kBins1];   // sample histogram (digit 1)
   unsigned hist_s2[256];     // sample histogram of bits 18..11 inside the bound's bucket
   unsigned hist1[kBins1];    // candidate histogram, key bits 30..19 (k_select)
@@ -62,6 +63,7 @@ struct Ctl {
   unsigned hist3[2048];      // bits 10..0
   unsigned hist_w[4096];     // window histogram: key bits 30..11 relative to Lkey (k_select)
   unsigned done_sel;         // k_select_x: last-block counter (finalisation)
+  unsigned done_slice;       // k_fetch_gather two-stage broadcast: slice pulled
   unsigned lb_flag[kMaxGrid];             // k_select_x look-back: block b's total is in
   unsigned long long lb_tot[kMaxGrid];    // ... (gt << 32) | eq of block b
 };

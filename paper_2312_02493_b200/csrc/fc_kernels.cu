@@ -23,7 +23,9 @@
 // Everything is HBM-bound integer/fp32 streaming work: no tensor cores.
 // DESIGN.md §4 gives each kernel's algorithmic bytes and roofline.
 #include <atomic>
+#include <type_traits>
 #include <cstdio>
+#include <cstdlib>
 
 #include "fc_device.cuh"
 #include "fc_synth.h"
@@ -1446,6 +1448,9 @@ constexpr int kSxThreads = 1024;
 constexpr int kSxWarps = kSxThreads / 32;
 constexpr unsigned kSxListCap = kSelBins / 2;  // u32 entries in the upper half of s_h
 
+#define SX_MARK(i) \
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctl->tphase_sx[i] = gtimer()
+
 __host__ __device__ inline unsigned sx_cpb(unsigned nch, unsigned grid, unsigned B) {
   const unsigned c = (nch + grid - 1) / grid;
   return (c + B - 1) / B * B;
@@ -1471,6 +1476,7 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
   __shared__ unsigned s_wgt[kSxWarps], s_weq[kSxWarps];
   __shared__ unsigned long long s_wpre[kSxWarps + 1];
   __shared__ unsigned s_nl;
+  __shared__ __align__(8) unsigned long long s_mbar;  // index staging (TMA)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned lt = lanemask_lt();
   unsigned bar = 0;  // grid barrier target (ctl->bar_sel)
@@ -1542,6 +1548,7 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
       }
     }
     __threadfence();
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // re-emitted runs -> TMA reads below
     __syncthreads();
     Lb = Lk;
   }
@@ -1570,7 +1577,23 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
   const unsigned P = s_pos[S];
   const bool cached = 2ull * P <= cap;
   float4* s_val4 = reinterpret_cast<float4*>(s_val);
-  uint4* s_idx4 = reinterpret_cast<uint4*>(s_val + P);
+  unsigned* s_idx = reinterpret_cast<unsigned*>(s_val + P);
+  uint4* s_idx4 = reinterpret_cast<uint4*>(s_idx);
+  if (cached) {
+    // the indices are needed only by the emission: one TMA bulk copy per
+    // segment (runs padded to 16 bytes; a segment's slots are never
+    // overrun), completing on one mbarrier in the background of P1-P3
+    if (tid == 0) {
+      mbar_init(&s_mbar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_expect_tx(&s_mbar, P * 4u);
+    }
+    __syncthreads();
+    for (unsigned j = tid; j < S; j += kSxThreads) {
+      const unsigned bytes = ((s_sct[j] + 3u) & ~3u) * 4u;
+      if (bytes) bulk_g2s(s_idx + s_pos[j], w.cand_idx + ((uint64_t)seg_c0(j) << kChunkShift), bytes, &s_mbar);
+    }
+  }
   // warp-contiguous ranges of 128-position steps
   const unsigned R = (P + kSxWarps * 128 - 1) / (kSxWarps * 128) * 128;
   const unsigned wlo = min(P, warp * R), whi = min(P, wlo + R);
@@ -1584,15 +1607,16 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
     }
     return lo;
   };
-  // One pass over this warp's positions: f(v, id, nv) for every lane's float4
-  // group in position order (all lanes call f every iteration: warp-synchronous
-  // helpers may be used inside); nv = valid elements of the group (0..4).
-  // src 0: global candidates (+ store into shared memory when `stage`), 1:
-  // shared memory.
-  auto pass = [&](bool from_smem, bool with_idx, bool stage, auto&& f) {
+  // One pass over this warp's positions, Uc::value groups in flight per
+  // lane: f(v, id, nv) for every lane's float4 group in position order (all
+  // lanes call f every iteration: warp-synchronous helpers may be used
+  // inside); nv = valid elements of the group (0..4).  from_smem: the staged
+  // values (and indices), else global; stage: store the values read from
+  // global into shared memory.
+  auto pass = [&](auto Uc, bool from_smem, bool with_idx, bool stage, auto&& f) {
+    constexpr int U = decltype(Uc)::value;
     if (n_it == 0) return;
     unsigned sg = seg_of(min(wlo + lane * 4, P - 1));
-    constexpr int U = 2;
     for (unsigned it0 = 0; it0 < n_it; it0 += U) {
       float4 v[U];
       uint4 id[U];
@@ -1615,17 +1639,20 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
             v[u] = __ldcg(reinterpret_cast<const float4*>(w.cand_val + g));
             if (with_idx) id[u] = __ldcg(reinterpret_cast<const uint4*>(w.cand_idx + g));
           }
-          if (stage) {
-            s_val4[p >> 2] = v[u];
-            s_idx4[p >> 2] = id[u];
-          }
         }
       }
 #pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (it0 + u < n_it) f(v[u], id[u], nv[u]);
+      for (int u = 0; u < U; ++u) {
+        if (it0 + u < n_it) {
+          if (stage && wlo + (it0 + u) * 128 + lane * 4 < whi) s_val4[(wlo + (it0 + u) * 128 + lane * 4) >> 2] = v[u];
+          f(v[u], id[u], nv[u]);
+        }
+      }
     }
   };
+  using U1 = std::integral_constant<int, 1>;
+  using U2 = std::integral_constant<int, 2>;
+  using U4 = std::integral_constant<int, 4>;
 
   // ---- P1: window histogram (key bits 30..11 relative to Lb's prefix) ----
   unsigned long long need = k;
@@ -1634,13 +1661,17 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
   const unsigned wb = Lb >> 11;
   for (int b = tid; b < kSelBins; b += kSxThreads) s_h[b] = 0;
   __syncthreads();
-  pass(false, cached, cached, [&](const float4& v, const uint4&, unsigned nv) {
+  pass(U4{}, false, false, cached, [&](const float4& v, const uint4&, unsigned nv) {
     for (unsigned e = 0; e < nv; ++e) {
       const unsigned hi = key_of(f4c(v, e)) >> 11;
       if (hi >= wb) atomicAdd(&s_h[min(hi - wb, (unsigned)kSelBins - 1u)], 1u);
     }
   });
+  SX_MARK(0);
+  __syncthreads();
+  if (tid == 0) reinterpret_cast<unsigned long long*>(w.g_part)[2048 + 2 * blockIdx.x] = gtimer();  // (diagnostics)
   flush_hist(s_h, ctl->hist_w, kSelBins);
+  SX_MARK(1);
   grid_barrier(&ctl->bar_sel, bar, w.err);
   SEL_MARK(1);
   {
@@ -1666,7 +1697,7 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
     __syncthreads();
     const unsigned pf = prefix;
     unsigned gt = 0;
-    pass(cached, false, false, [&](const float4& v, const uint4&, unsigned nv) {
+    pass(U4{}, cached, false, false, [&](const float4& v, const uint4&, unsigned nv) {
       for (unsigned e = 0; e < nv; ++e) {
         const unsigned key = key_of(f4c(v, e)), hi = key >> 11;
         gt += hi > pf;
@@ -1682,6 +1713,9 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
       s_wgt[warp] = gt;
       s_weq[warp] = 0;
     }
+    SX_MARK(2);
+    __syncthreads();
+    if (tid == 0) reinterpret_cast<unsigned long long*>(w.g_part)[2048 + 2 * blockIdx.x + 1] = gtimer();
     flush_hist(s_h, ctl->hist3, 2048);
     grid_barrier(&ctl->bar_sel, bar, w.err);
     SEL_MARK(3);
@@ -1710,7 +1744,7 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
       const unsigned pf = prefix, dm = (unsigned)nb - 1;
       for (int b = tid; b < nb; b += kSxThreads) s_h[b] = 0;
       __syncthreads();
-      pass(cached, false, false, [&](const float4& v, const uint4&, unsigned nv) {
+      pass(U4{}, cached, false, false, [&](const float4& v, const uint4&, unsigned nv) {
         for (unsigned e = 0; e < nv; ++e) {
           const unsigned key = key_of(f4c(v, e));
           if ((unsigned)((unsigned long long)key >> as) == pf) atomicAdd(&s_h[(key >> sh) & dm], 1u);
@@ -1731,7 +1765,7 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
   needT = need;
   if (!counted) {
     unsigned gt = 0, eq = 0;
-    pass(cached, false, false, [&](const float4& v, const uint4&, unsigned nv) {
+    pass(U4{}, cached, false, false, [&](const float4& v, const uint4&, unsigned nv) {
       for (unsigned e = 0; e < nv; ++e) {
         const unsigned key = key_of(f4c(v, e));
         gt += key > T;
@@ -1785,13 +1819,28 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
   const bool staged = (unsigned long long)used + 2 * nsel <= cap;
   unsigned* s_oidx = reinterpret_cast<unsigned*>(s_val + used);
   float* s_oval = reinterpret_cast<float*>(s_oidx + (staged ? nsel : 0));
+  // not staged: each warp's iteration output goes through a 128-pair buffer
+  // (written out coalesced); it reuses shared memory past the staged values
+  unsigned* s_wbi = reinterpret_cast<unsigned*>(s_val + used) + warp * 256;
+  float* s_wbv = reinterpret_cast<float*>(s_wbi + 128);
+  const bool wbuf = !staged && used + kSxWarps * 256u <= cap;
+  if (cached) mbar_wait(&s_mbar, 0);  // the indices are in
+  SX_MARK(3);
 
-  // ---- P4: emission ----
+  // ---- P4: emission.  Per warp iteration one packed warp scan of (gt, eq)
+  // places every selected pair; ties are kept while the block's tie rank is
+  // below `avail`.  Selected pairs are counted per chunk (shared-memory
+  // histogram over the block's chunks) for the decode's chunk bounds. ----
+  const bool ccount = bounds_out && (c1 - c0) <= (unsigned)kSelBins;  // s_h holds the per-chunk counts
+  unsigned* s_cc = s_h;
+  if (ccount)
+    for (unsigned c = tid; c < c1 - c0; c += kSxThreads) s_cc[c] = 0u;
+  __syncthreads();
   double acc = 0.0;
   {
     unsigned long long grun = s_wpre[warp] >> 32, erun = s_wpre[warp] & 0xffffffffull;
     const unsigned ibase = mode.idx_base;
-    pass(cached, true, false, [&](const float4& v, const uint4& id, unsigned nv) {
+    pass(U2{}, cached, true, false, [&](const float4& v, const uint4& id, unsigned nv) {
       unsigned gm = 0, em = 0;
       for (unsigned e = 0; e < nv; ++e) {
         const unsigned key = key_of(f4c(v, e));
@@ -1807,6 +1856,7 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
       }
       const unsigned tot = __shfl_sync(0xffffffffu, inc, 31);
       const unsigned ex = inc - x;
+      const unsigned long long it_base = grun + min(erun, avail);  // first output position of the iteration
       unsigned long long gb = grun + (ex >> 16), eb = erun + (ex & 0xffffu);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -1814,14 +1864,18 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
         if (g || (q && eb < avail)) {
           const unsigned long long pos = gb + min(eb, avail);
           const float xv = f4c(v, e);
-          const unsigned iv = u4c(id, e) + ibase;
+          const unsigned raw = u4c(id, e);
           if (staged) {
-            s_oidx[pos] = iv;
+            s_oidx[pos] = raw + ibase;
             s_oval[pos] = xv;
+          } else if (wbuf) {
+            s_wbi[pos - it_base] = raw + ibase;
+            s_wbv[pos - it_base] = xv;
           } else {
-            out_idx[obase + pos] = iv;
+            out_idx[obase + pos] = raw + ibase;
             out_val[obase + pos] = xv;
           }
+          if (ccount) atomicAdd(&s_cc[(raw >> kChunkShift) - c0], 1u);
           acc = fma((double)xv, (double)xv, acc);
         }
         gb += g;
@@ -1829,6 +1883,15 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
       }
       grun += tot >> 16;
       erun += tot & 0xffffu;
+      if (wbuf) {  // this iteration's pairs: one contiguous output range
+        const unsigned n_out = (unsigned)(grun + min(erun, avail) - it_base);
+        __syncwarp();
+        for (unsigned i = lane; i < n_out; i += 32) {
+          out_idx[obase + it_base + i] = s_wbi[i];
+          out_val[obase + it_base + i] = s_wbv[i];
+        }
+        __syncwarp();
+      }
     });
   }
   __syncthreads();
@@ -1838,18 +1901,34 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
       out_idx[obase + i] = s_oidx[i];
       out_val[obase + i] = s_oval[i];
     }
-  // the decode's chunk bounds of [c0, c1): first output position >= chunk c
+  SX_MARK(4);
+  // the decode's chunk bounds of [c0, c1): bounds[c] = first output position
+  // whose index is >= c * kChunk = obase + selected pairs in earlier chunks
   if (bounds_out) {
-    const unsigned* oi = staged ? s_oidx : out_idx + obase;
-    const unsigned ibase = mode.idx_base;
-    for (unsigned i = tid; i < nsel; i += kSxThreads) {
-      const long long ci = (long long)((oi[i] - ibase) >> kChunkShift);
-      const long long cp = i ? (long long)((oi[i - 1] - ibase) >> kChunkShift) : (long long)c0 - 1;
-      for (long long t = cp + 1; t <= ci; ++t) bounds_out[t] = (unsigned)(obase + i);
+    if (ccount) {
+      const unsigned nc = c1 - c0, per = (nc + kSxThreads - 1) / kSxThreads;
+      const unsigned a0 = min(nc, tid * per), a1 = min(nc, a0 + per);
+      unsigned long long sum = 0;
+      for (unsigned c = a0; c < a1; ++c) sum += s_cc[c];
+      unsigned long long o = obase + block_excl_scan<kSxThreads>(sum, s_red);
+      for (unsigned c = a0; c < a1; ++c) {
+        const unsigned cnt = s_cc[c];
+        bounds_out[c0 + c] = (unsigned)o;
+        o += cnt;
+      }
+    } else {  // (very long block ranges) from the output list itself
+      __syncthreads();  // every thread's output pairs are written
+      const unsigned ibase = mode.idx_base;
+      for (unsigned long long i = tid; i < nsel; i += kSxThreads) {
+        const long long ci = (long long)((out_idx[obase + i] - ibase) >> kChunkShift);
+        const long long cp = i ? (long long)((out_idx[obase + i - 1] - ibase) >> kChunkShift) : (long long)c0 - 1;
+        for (long long t = cp + 1; t <= ci; ++t) bounds_out[t] = (unsigned)(obase + i);
+      }
+      const long long cl = nsel ? (long long)((out_idx[obase + nsel - 1] - ibase) >> kChunkShift) : (long long)c0 - 1;
+      for (long long t = cl + 1 + tid; t < (long long)c1; t += kSxThreads) bounds_out[t] = (unsigned)(obase + nsel);
     }
-    const long long cl = nsel ? (long long)((oi[nsel - 1] - ibase) >> kChunkShift) : (long long)c0 - 1;
-    for (long long t = cl + 1 + tid; t < (long long)c1; t += kSxThreads) bounds_out[t] = (unsigned)(obase + nsel);
   }
+  SX_MARK(5);
   const double bsum = block_sum<kSxThreads>(acc, s_dred);
   if (tid == 0) {
     w.bnorm[blockIdx.x] = bsum;
@@ -2034,7 +2113,7 @@ void launch_var_mask(const double* scores, int n, int rank, const unsigned* idx,
 }
 
 __global__ void __launch_bounds__(kThreads) k_fetch_gather(PeerBufs pb, int sel, int par, int tree,
-                                                           unsigned long long epoch,
+                                                           int two_stage, unsigned long long epoch,
                                                            const float* __restrict__ ge, uint64_t k,
                                                            unsigned* __restrict__ bounds, uint64_t nch,
                                                            Ctl* __restrict__ ctl, int* __restrict__ sel_out,
@@ -2096,20 +2175,59 @@ __global__ void __launch_bounds__(kThreads) k_fetch_gather(PeerBufs pb, int sel,
     uint4* bd4 = reinterpret_cast<uint4*>(bounds);
     for (uint64_t i = t0; i < nb4; i += nt) bd4[i] = __ldcv(bs4 + i);
   }
+  // Two-stage list broadcast (N large): instead of N-1 full pulls from the
+  // selected rank's egress, helper h (the non-selected ranks, in rank order
+  // after sel) pulls only slice h of the list from it, publishes the slice
+  // (mailbox slot 3), and the helpers then pull the other slices from each
+  // other -- the selected rank sends each list entry once.
+  const bool staged2 = two_stage && copy_list && n > 2;
+  const int nh = n - 1, hq = (me - sel - 1 + n) % n;  // helpers, my helper index
+  auto q_slice = [&](uint64_t q) -> int {              // helper owning quad q
+    int h = (int)((q * (uint64_t)nh) / nq);
+    while (h + 1 < nh && (nq * (uint64_t)(h + 1)) / (uint64_t)nh <= q) ++h;
+    while (h > 0 && (nq * (uint64_t)h) / (uint64_t)nh > q) --h;
+    return h;
+  };
+  unsigned seen = 0;  // helpers whose slice flag this thread has observed
+  auto src_quad = [&](uint64_t q) -> const uint4* {
+    if (!staged2) return src4 + q;
+    const int h = q_slice(q);
+    const int owner = (sel + 1 + h) % n;
+    if (!(seen & (1u << h))) {
+      if (!wait_from(pb, owner, 3, epoch)) return nullptr;
+      seen |= 1u << h;
+    }
+    return reinterpret_cast<const uint4*>(pb.list[owner] + off) + q;
+  };
+  if (staged2) {
+    // stage 1: my slice from the selected rank, into my list
+    const uint64_t s0 = (nq * (uint64_t)hq) / nh, s1 = (nq * (uint64_t)(hq + 1)) / nh;
+    for (uint64_t q = s0 + t0; q < s1; q += nt) mine4[q] = __ldcv(src4 + q);
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence_system();
+    if (last_block_done(&ctl->done_slice) && threadIdx.x == 0) {
+      __threadfence_system();
+      publish_all(pb, 3, epoch);  // my slice is in my list (the other helpers pull it)
+    }
+  }
   // groups of 4 consecutive list positions per thread, lanes on consecutive
   // groups; the next group's remote loads are issued before this one's local
   // gather (NVLink latency overlapped)
   uint64_t q = t0;
   uint4 ci = make_uint4(0, 0, 0, 0), cv = make_uint4(0, 0, 0, 0);
   if (q < nq) {
-    ci = __ldcv(src4 + q);
+    const uint4* a = src_quad(q);
+    if (!a) return;  // (peer timeout reported)
+    ci = __ldcv(a);
     if (pull_sel) cv = __ldcv(selv4 + q);
   }
   for (; q < nq; q += nt) {
     const uint64_t qn = q + nt;
     uint4 ni = make_uint4(0, 0, 0, 0), nv = make_uint4(0, 0, 0, 0);
     if (qn < nq) {
-      ni = __ldcv(src4 + qn);
+      const uint4* a = src_quad(qn);
+      if (!a) return;
+      ni = __ldcv(a);
       if (pull_sel) nv = __ldcv(selv4 + qn);
     }
     const uint64_t j = 4 * q;
@@ -2118,7 +2236,7 @@ __global__ void __launch_bounds__(kThreads) k_fetch_gather(PeerBufs pb, int sel,
     g4.y = j + 1 < k ? ld_scattered(ge + ci.y) : 0.f;
     g4.z = j + 2 < k ? ld_scattered(ge + ci.z) : 0.f;
     g4.w = j + 3 < k ? ld_scattered(ge + ci.w) : 0.f;
-    if (copy_list) mine4[q] = ci;
+    if (copy_list && !(staged2 && q_slice(q) == hq)) mine4[q] = ci;
     contrib4[q] = g4;
     if (pull_sel) selcopy4[q] = cv;
     if (peer4) {
@@ -2158,11 +2276,18 @@ int fetch_gather_grid() {
 void launch_fetch_gather(const PeerBufs& pb, int sel, int par, int tree, unsigned long long epoch,
                          const float* ge, uint64_t k, unsigned* bounds, uint64_t nch, Ctl* ctl, int* sel_out,
                          unsigned long long* tblk, cudaStream_t s) {
+  // the two-stage list broadcast from FC_TWO_STAGE_MIN ranks on (default 5:
+  // at N <= 4 the selected rank's egress of (N-1) lists is not the limit)
+  static const int two_min = [] {
+    const char* e = std::getenv("FC_TWO_STAGE_MIN");
+    return e ? std::atoi(e) : 5;
+  }();
+  const int two_stage = pb.n >= two_min ? 1 : 0;
   const uint64_t nq = std::max<uint64_t>((k + 3) / 4, (nch + 4) / 4);
   int grid = (int)std::min<uint64_t>((nq + kThreads - 1) / kThreads, (uint64_t)fetch_gather_grid());
   if (grid < 1) grid = 1;
-  launch_pdl(k_fetch_gather, grid, kThreads, 0, s, pb, sel, par, tree, epoch, ge, k, bounds, nch, ctl, sel_out,
-             tblk);
+  launch_pdl(k_fetch_gather, grid, kThreads, 0, s, pb, sel, par, tree, two_stage, epoch, ge, k, bounds, nch, ctl,
+             sel_out, tblk);
   count_launch();
 }
 

@@ -70,3 +70,68 @@ def test_fit_recomputes(fc, n):
     base = err(a, b)
     for fa, fb in [(1.3, 1), (1 / 1.3, 1), (1, 1.3), (1, 1 / 1.3)]:
         assert err(a * fa, b * fb) >= base * 0.999
+
+
+# ---- calibration on the product's own exchange (peer memory) -------------
+# tools/calibrate_peer.py measured AG / ART-Ring / ART-Tree through the
+# kernels the steps run (fc_diag_exchange_ms) and whole steps at BASELINE
+# configs 1-3; tools/fit_peer.py fitted one NetParams per N.  Validated the
+# reference's way (tests/test_acceptance.cpp:45-60): the unchanged
+# select_collective must name the measured-fastest collective wherever the
+# measured top-two margin exceeds 15 %.
+
+PEER_WORLDS = sorted(int(p.stem.split("_n")[-1]) for p in FIX.glob("peer_fit_n*.json"))
+
+
+def _peer_fit(n):
+    return json.loads((FIX / f"peer_fit_n{n}.json").read_text())
+
+
+@pytest.mark.parametrize("n", PEER_WORLDS)
+def test_peer_fit_is_physical(n):
+    d = _peer_fit(n)
+    assert 5e-7 <= d["alpha_s"] <= 1e-4           # kernel launch + flag latency
+    assert 100 <= d["bandwidth_GBps"] <= 1800      # NVLink 5: 900 GB/s per direction
+
+
+def _select(fc, d, n, mc):
+    net = fc.NetParams(d["alpha_s"], d["bandwidth_bps"])
+    ch = fc.select_collective(net, fc.MessageSpec(mc / 0.01, 0.01, n))
+    return {0: "ag", 1: "art_ring", 2: "art_tree"}[int(ch.collective)]
+
+
+@pytest.mark.parametrize("n", PEER_WORLDS)
+def test_peer_selector_matches_measured_exchange(fc, n):
+    """Every decisive point of the exchange grid: the library's
+    select_collective (the reference's formulas, bit-exact in test_cpu.py)
+    with the fitted NetParams picks the measured-fastest exchange."""
+    d = _peer_fit(n)
+    pts = [p for p in d["exchange_points"] if p["decisive"]]
+    assert len(pts) >= 3
+    for p in pts:
+        assert _select(fc, d, n, p["mc_bytes"]) == p["measured_fastest"], p
+
+
+@pytest.mark.parametrize("n", PEER_WORLDS)
+def test_peer_selector_matches_measured_steps(fc, n):
+    """BASELINE configs 1-3 as whole steps (sync time = step - the one-worker
+    step of the same kind): the selector agrees wherever the margin is decisive."""
+    d = _peer_fit(n)
+    assert {p["point"] for p in d["step_points"]} >= {"C1", "C2", "C3"}
+    for p in d["step_points"]:
+        if p["decisive"]:
+            assert _select(fc, d, n, p["mc_bytes"]) == p["measured_fastest"], p
+
+
+@pytest.mark.parametrize("n", PEER_WORLDS)
+def test_peer_fit_recomputes(n):
+    """The stored fit is what tools/fit_peer.py computes from the stored grid."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("fit_peer", ROOT / "tools" / "fit_peer.py")
+    fp = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(fp)
+    ex, _ = fp.load(FIX, n)
+    a, b = fp.fit(n, [(mc, m) for mc, m, _ in ex])
+    d = _peer_fit(n)
+    assert math.isclose(a, d["alpha_s"], rel_tol=1e-9) and math.isclose(8.0 / b, d["bandwidth_bps"], rel_tol=1e-9)

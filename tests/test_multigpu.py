@@ -19,15 +19,40 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("nproc", [2, 4, 8])
-def test_nccl_parity(nproc):
+def _run(nproc, script, args, extra_env=None, marker="MP_CHECK PASS"):
     import torch
 
     if torch.cuda.device_count() < nproc:
         pytest.skip(f"needs {nproc} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={nproc}", "--master-addr", "127.0.0.1",
-           "--master-port", str(_free_port()), str(ROOT / "tests" / "mp_check.py"), "400009"]
+           "--master-port", str(_free_port()), str(ROOT / script), *args]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
-                       env={**os.environ, "OMP_NUM_THREADS": "1"})
-    assert r.returncode == 0 and "MP_CHECK PASS" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+                       env={**os.environ, "OMP_NUM_THREADS": "1", **(extra_env or {})})
+    assert r.returncode == 0 and marker in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("nproc", [2, 4, 8])
+def test_nccl_parity(nproc):
+    _run(nproc, "tests/mp_check.py", ["400009"])
+
+
+@pytest.mark.parametrize("nproc", [3, 4])
+def test_two_stage_list_broadcast(nproc):
+    """The two-stage list broadcast (slices pulled from the selected rank,
+    then from each other; the default from 5 ranks on) forced at 3 and 4
+    ranks: STAR/VAR Ring/Tree and AG trajectories bit-exact."""
+    _run(nproc, "tests/mp_check.py", ["300007"], {"FC_TWO_STAGE_MIN": "3"})
+
+
+@pytest.mark.parametrize("nproc", [2, 4])
+def test_peer_exchange_soak(nproc):
+    """Many reuses of the mailbox epochs and parity rows: 100 steps cycling
+    STAR/VAR (Ring and Tree) and AG, every 20th step checked bit-exact."""
+    _run(nproc, "tools/soak_mp.py", ["60001", "100", "20"], marker="SOAK PASS")
+
+
+def test_peer_timeout_reported():
+    """A rank that never joins a step: the peer's exchange wait times out
+    (2 s), and the step call raises instead of hanging or returning stale data."""
+    _run(2, "tests/mp_timeout.py", [], marker="MP_TIMEOUT PASS")

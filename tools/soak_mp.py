@@ -1,5 +1,6 @@
 """Long-run soak of the multi-GPU exchange (peer memory or NCCL): STEPS
-back-to-back steps cycling STAR / VAR / AG with the residual carried, one
+back-to-back steps cycling STAR / VAR (Ring), STAR / VAR (Tree) and AG with
+the residual carried, one
 rank per GPU.  Rank 0 follows the same trajectory with the fp32 oracle (the
 checker) and compares every rank's aggregate and residual bit-exact every
 CHECK steps and at the last step — exercises the mailbox epochs and parity
@@ -29,7 +30,7 @@ def main():
     uid = dist.share_nccl_uid(env)
     f32 = oracle.F32() if env.rank == 0 else None
     res = np.zeros((env.world, G), np.float32) if env.rank == 0 else None
-    kinds = ("star", "var", "ag")
+    kinds = ("star", "var", "ag", "star-tree", "var-tree")
     c = 0.01
     failures, checks = [], 0
     t0 = time.time()
@@ -42,7 +43,8 @@ def main():
             if kind == "ag":
                 cl.ag_step(c)
             else:
-                sel = cl.artopk_step(c, fc.STAR if kind == "star" else fc.VAR, fc.RING, s, fc.AVG).selected_rank
+                sel = cl.artopk_step(c, fc.STAR if kind.startswith("star") else fc.VAR,
+                                     fc.TREE if kind.endswith("tree") else fc.RING, s, fc.AVG).selected_rank
             last = s == steps - 1
             do_check = last or (s + 1) % check == 0
             if do_check:
@@ -55,7 +57,7 @@ def main():
             if kind == "ag":
                 ref, rsel = f32.ag_step(g_o, res, c), -1
             else:
-                ref, rsel, _, _ = f32.artopk_step(g_o, res, c, 0 if kind == "star" else 1, s, 1)
+                ref, rsel, _, _ = f32.artopk_step(g_o, res, c, 0 if kind.startswith("star") else 1, s, 1)
             if not do_check:
                 continue
             checks += 1
