@@ -253,6 +253,11 @@ class Context {
     check(fc_get_aggregate_f64(ctx_, out.data()));
     return out;
   }
+  // into an existing vector (no allocation when it already holds G values)
+  void aggregate_into(std::vector<double>& out) {
+    if (out.size() != g_) out.resize(g_);
+    check(fc_get_aggregate_f64(ctx_, out.data()));
+  }
   SparseGrad topk(int worker) {
     uint64_t k = 0;
     check(fc_get_topk(ctx_, worker, nullptr, nullptr, &k));
@@ -367,6 +372,32 @@ inline ArtopkResult artopk_step(const Cluster& cluster, const std::vector<DenseG
   out.aggregate.values = cluster.ctx->aggregate();
   out.selected_rank = st.selected_rank;
   return out;
+}
+
+// artopk_step writing into a caller-owned result: the same step, but the
+// aggregate reuses out.aggregate's storage instead of returning a fresh
+// 8G-byte vector by value (on a host where first-touching 1.1 GB costs
+// hundreds of milliseconds, that allocation dominates the call; see
+// tests/cpp/bench_facade.cpp).  Not in the reference's API -- an addition.
+inline void artopk_step_into(ArtopkResult& out, const Cluster& cluster, const std::vector<DenseGrad>& g_o,
+                             ResidualStore& /*device-resident*/, CompressionRatio c, SelectionMode mode,
+                             ReduceAlgo algo, long step, SelectionLog* log = nullptr, ReduceOp op = ReduceOp::Avg,
+                             double payload_scale = 1.0) {
+  detail::upload(cluster, g_o);
+  fc_step_stats st{};
+  check(fc_artopk_step(cluster.ctx->get(), c.c, mode == SelectionMode::STAR ? FC_STAR : FC_VAR,
+                       algo == ReduceAlgo::Ring ? FC_RING : FC_TREE, step,
+                       op == ReduceOp::Sum ? FC_SUM : FC_AVG, &st));
+  if (log) log->record(step, st.selected_rank, cluster.n);
+  if (cluster.n > 1) {
+    if (mode == SelectionMode::VAR) cluster.charge(cost_allgather_dense(cluster.net, cluster.msg(4.0 * cluster.n)));
+    const double wire = 4.0 * static_cast<double>(st.k) * payload_scale;
+    cluster.charge(cost_broadcast(cluster.net, cluster.msg(wire)));
+    cluster.charge(algo == ReduceAlgo::Ring ? cost_ring_ar(cluster.net, cluster.msg(wire))
+                                            : cost_tree_ar(cluster.net, cluster.msg(wire)));
+  }
+  cluster.ctx->aggregate_into(out.aggregate.values);
+  out.selected_rank = st.selected_rank;
 }
 
 // inc/artopk.hpp:128-161, every compressor on the device (Layerwise uses

@@ -654,6 +654,7 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
     TRY(c->alloc(&s.cand_val, (uint64_t)nch << fcb::kChunkShift));
     TRY(c->alloc(&s.cnorm, 2 * (uint64_t)nch));  // [full EF pass | layer passes]
     TRY(c->alloc(&s.g_part, 4096));
+    TRY(c->alloc(&s.skeys, fcb::kSamples));
     TRY(c->alloc(&s.tblk, 2 * (uint64_t)ef_grid));
   }
   CUDA_TRY(cudaStreamSynchronize(c->stream));

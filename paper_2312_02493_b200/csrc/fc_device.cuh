@@ -81,6 +81,7 @@ struct ChunkWs {
   double* g_part;             // one per gather block
   unsigned long long* tblk;   // diagnostics: %globaltimer at each EF block's start and end
   unsigned* err;              // the context's sticky error words (host-mapped; see kErr*)
+  unsigned* skeys;            // kSamples sampled |g_e| keys (the EF pass's candidate bound)
   unsigned nchunks;
   unsigned ef_grid;
   unsigned coop;              // grid-barrier kernels launched cooperatively (default)

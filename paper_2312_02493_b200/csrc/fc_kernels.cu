@@ -199,6 +199,7 @@ __device__ __forceinline__ bool last_block_done(unsigned* counter) {
 // histogram holds fewer than `target` entries.  hist lives in global memory
 // (filled by other blocks' atomics): it is first copied to s_stage (nb words
 // of shared memory) with independent L2 loads, then scanned there.
+// hist == s_stage: the histogram is already in shared memory (no copy).
 template <int B>
 __device__ bool block_select_top(const unsigned* hist, int nb, unsigned long long target,
                                  unsigned& bin, unsigned long long& above, unsigned* s_stage) {
@@ -206,8 +207,10 @@ __device__ bool block_select_top(const unsigned* hist, int nb, unsigned long lon
   __shared__ unsigned s_bin;
   __shared__ unsigned long long s_above;
   __shared__ int s_found;
+  if (hist != s_stage) {
 #pragma unroll 16
-  for (int b = threadIdx.x; b < nb; b += B) s_stage[b] = __ldcg(hist + b);
+    for (int b = threadIdx.x; b < nb; b += B) s_stage[b] = __ldcg(hist + b);
+  }
   __syncthreads();
   const int per = (nb + B - 1) / B;
   const int top = nb - per * (int)threadIdx.x;
@@ -458,8 +461,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
     for (unsigned q = blockIdx.x * kThreads + tid; q < sizeof(Ctl) / 4; q += gridDim.x * kThreads) z[q] = 0u;
   }
   const bool sampling = kEmit && (opts & 1);
-  if (sampling)
-    for (int b = tid; b < kBins1; b += kThreads) s_hist[b] = 0u;
   __syncthreads();
 
   // the sample's loads go out first, ahead of the stream's first stages
@@ -522,9 +523,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
   unsigned Lkey = 0u;
   if (kEmit) {
     if (opts & 1) {
-      if (q0 < (unsigned)kSamples) atomicAdd(&s_hist[key_of(sv) >> kShift1], 1u);
-      for (unsigned q = q0 + qstride; q < (unsigned)kSamples; q += qstride)  // small grids only
-        atomicAdd(&s_hist[key_of(sample_at(q)) >> kShift1], 1u);
+      // Level 1 (12-bit buckets): each block histograms its own samples and
+      // flushes them (one grid barrier).  Level 2 (the next 8 bits inside the
+      // target bucket) is local: every sampled key is also stored in the
+      // shared sample array, and each block re-reads all 32768 from L2 and
+      // histograms the few that fall in the bucket -- no second flush or
+      // barrier.
+      for (int b = tid; b < kBins1; b += kThreads) s_hist[b] = 0u;
+      __syncthreads();
+      if (q0 < (unsigned)kSamples) {
+        w.skeys[q0] = key_of(sv);
+        atomicAdd(&s_hist[key_of(sv) >> kShift1], 1u);
+      }
+      for (unsigned q = q0 + qstride; q < (unsigned)kSamples; q += qstride) {  // small grids only
+        const unsigned kq = key_of(sample_at(q));
+        w.skeys[q] = kq;
+        atomicAdd(&s_hist[kq >> kShift1], 1u);
+      }
       __syncthreads();
       if (blockIdx.x == 0 && threadIdx.x == 0) ctl->tphase_ef2[0] = gtimer();
       for (int b = tid; b < kBins1; b += kThreads)
@@ -533,10 +548,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
       unsigned bar = 0;
       grid_barrier(&ctl->bar_ef, bar, w.err);
       EF_MARK(1);
-      // the bound: the sample's 12-bit bucket holding the target-th largest
-      // value, then (second level) the 8 bits below inside that bucket, so
-      // candidates overshoot the target by < 0.3 % of a value instead of up
-      // to one 1/16-octave bucket
       const double target = sample_target(G, k);
       if (opts & 2) {
         Lkey = (unsigned)(kBins1 - 1) << kShift1;  // forced miss (tests)
@@ -547,17 +558,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
         if (block_select_top<kThreads>(ctl->hist_s, kBins1, tgt, b1, above1, s_hist)) {
           for (int b = tid; b < 256; b += kThreads) s_hist[b] = 0u;
           __syncthreads();
-          auto level2 = [&](float v) {
-            const unsigned key = key_of(v);
-            if ((key >> kShift1) == b1) atomicAdd(&s_hist[(key >> 11) & 255u], 1u);
-          };
-          if (q0 < (unsigned)kSamples) level2(sv);
-          for (unsigned q = q0 + qstride; q < (unsigned)kSamples; q += qstride) level2(sample_at(q));
-          __syncthreads();
-          for (int b = tid; b < 256; b += kThreads)
-            if (s_hist[b]) atomicAdd(&ctl->hist_s2[b], s_hist[b]);
-          grid_barrier(&ctl->bar_ef, bar, w.err);
-          const bool f2 = block_select_top<kThreads>(ctl->hist_s2, 256, tgt - above1, b2, above2, s_hist);
+          const uint4* k4 = reinterpret_cast<const uint4*>(w.skeys);
+          constexpr int kQ = kSamples / 4 / kThreads;  // uint4 loads per thread
+#pragma unroll 8
+          for (int i = 0; i < kQ; ++i) {
+            const uint4 x = __ldcg(k4 + i * kThreads + tid);
+            const unsigned kk[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if ((kk[e] >> kShift1) == b1) atomicAdd(&s_hist[(kk[e] >> 11) & 255u], 1u);
+          }
+          const bool f2 = block_select_top<kThreads>(s_hist, 256, tgt - above1, b2, above2, s_hist);
           Lkey = (b1 << kShift1) | ((f2 ? b2 : 0u) << 11);
         } else {
           Lkey = 0u;
@@ -1451,10 +1462,44 @@ constexpr unsigned kSxListCap = kSelBins / 2;  // u32 entries in the upper half 
 #define SX_MARK(i) \
   if (blockIdx.x == 0 && threadIdx.x == 0) ctl->tphase_sx[i] = gtimer()
 
-__host__ __device__ inline unsigned sx_cpb(unsigned nch, unsigned grid, unsigned B) {
-  const unsigned c = (nch + grid - 1) / grid;
-  return (c + B - 1) / B * B;
-}
+// Block -> chunk ranges of the select.  Blocks [0, nbA) own whole batches
+// of the aligned region [0, bnd) (cpbA chunks each, a multiple of B); blocks
+// [nbA, grid) own the single-chunk tail (cpbS chunks each).  A single-chunk
+// segment costs about twice an aligned chunk (scattered 4 KB-apart runs,
+// more segment bookkeeping), so the tail is weighted 2 when the grid is
+// split, and no block waits at the barriers for a slow tail block.
+struct SxGeom {
+  unsigned nbA, cpbA, cpbS;
+  __host__ __device__ SxGeom(unsigned nch, unsigned grid, const EfLayout& lay) {
+    const unsigned A = lay.bnd, Sg = nch - lay.bnd;
+    if (Sg == 0) {
+      cpbA = ((A + grid - 1) / grid + lay.B - 1) / lay.B * lay.B;
+      nbA = cpbA ? (A + cpbA - 1) / cpbA : 0u;
+      cpbS = 1;
+    } else if (A == 0) {
+      nbA = 0;
+      cpbA = lay.B;
+      cpbS = (Sg + grid - 1) / grid;
+    } else {
+      const double W = (double)A + 2.0 * (double)Sg;
+      unsigned na = (unsigned)((double)grid * (double)A / W + 0.5);
+      na = na < 1 ? 1u : (na > grid - 1 ? grid - 1 : na);
+      cpbA = ((A + na - 1) / na + lay.B - 1) / lay.B * lay.B;
+      nbA = (A + cpbA - 1) / cpbA;
+      cpbS = (Sg + (grid - nbA) - 1) / (grid - nbA);
+    }
+  }
+  __host__ __device__ void range(unsigned b, unsigned nch, unsigned bnd, unsigned& c0, unsigned& c1) const {
+    if (b < nbA) {
+      c0 = min(bnd, b * cpbA);
+      c1 = min(bnd, c0 + cpbA);
+    } else {
+      c0 = min(nch, bnd + (b - nbA) * cpbS);
+      c1 = min(nch, c0 + cpbS);
+    }
+  }
+  __host__ __device__ unsigned max_chunks() const { return cpbA > cpbS ? cpbA : cpbS; }
+};
 
 __device__ __forceinline__ float f4c(const float4& v, int e) {
   return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
@@ -1483,8 +1528,9 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
   SEL_MARK(0);
   const unsigned nch = w.nchunks;
   const EfLayout lay(nch, w.batch);
-  const unsigned cpb = sx_cpb(nch, gridDim.x, lay.B);
-  const unsigned c0 = min(nch, blockIdx.x * cpb), c1 = min(nch, c0 + cpb);
+  const SxGeom geo(nch, gridDim.x, lay);
+  unsigned c0, c1;
+  geo.range(blockIdx.x, nch, lay.bnd, c0, c1);
   const unsigned al_end = min(c1, lay.bnd);
   const unsigned nal = c0 < al_end ? (al_end - c0 + lay.B - 1) / lay.B : 0u;
   const unsigned sg0 = max(c0, lay.bnd);
@@ -1973,7 +2019,7 @@ int launch_select(uint64_t k, Ctl* ctl, const ChunkWs& w, const float* ef_out, u
       cudaFuncSetAttribute(k_select_x, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelSmemMax);
       attr = true;
     }
-    const unsigned cpb = sx_cpb(w.nchunks, grid, EfLayout(w.nchunks, w.batch).B);
+    const unsigned cpb = SxGeom(w.nchunks, grid, EfLayout(w.nchunks, w.batch)).max_chunks();
     if (2ull * cpb + 8 > kSelSmemMax / 4) return (int)cudaErrorInvalidValue;
     e = launch_grid_sync((const void*)k_select_x, dim3(grid), dim3(kSxThreads), kSelSmemMax, s, args, w.coop != 0);
   } else {

@@ -56,9 +56,48 @@ int main(int argc, char** argv) {
     if (agg.size() != G) return 2;
   }
   const double old_ms = sum / steps;
+
+  // (1b) the allocation-free variant (result storage reused)
+  ArtopkResult into;
+  sum = 0.0;
+  for (int s = 0; s < steps + 1; ++s) {
+    const auto t0 = clk::now();
+    artopk_step_into(into, cluster, g_o, residuals, CompressionRatio(0.01), SelectionMode::STAR, ReduceAlgo::Ring, s);
+    const double ms = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+    if (s > 0) sum += ms;
+  }
+  const double into_ms = sum / steps;
+
+  // (3) the façade's parts: fp64 upload, the device step, the fp64 aggregate
+  double t_up = 0, t_step = 0, t_down = 0;
+  for (int s = 0; s < steps; ++s) {
+    auto t0 = clk::now();
+    ctx->set_grad(0, g_o[0].values);
+    auto t1 = clk::now();
+    fc_step_stats st{};
+    check(fc_artopk_step(ctx->get(), 0.01, FC_STAR, FC_RING, s, FC_AVG, &st));
+    auto t2 = clk::now();
+    auto agg = ctx->aggregate();
+    auto t3 = clk::now();
+    t_up += std::chrono::duration<double, std::milli>(t1 - t0).count();
+    t_step += std::chrono::duration<double, std::milli>(t2 - t1).count();
+    t_down += std::chrono::duration<double, std::milli>(t3 - t2).count();
+    if (agg.size() != G) return 2;
+  }
+  // a bare std::vector<double>(G): the allocation + zero fill that returning
+  // the aggregate by value (as the reference does) costs on this host
+  double t_alloc = 0;
+  for (int s = 0; s < steps; ++s) {
+    auto t0 = clk::now();
+    std::vector<double> v(G);
+    t_alloc += std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+    if (v.size() != G) return 2;
+  }
   std::printf("{\"bench\": \"facade artopk_step e2e\", \"grad_len\": %zu, \"cr\": 0.01, \"steps\": %d, "
-              "\"facade_ms_per_step\": %.2f, \"round1_facade_ms_per_step\": %.2f, "
-              "\"h2d_bytes\": %zu, \"d2h_bytes\": %zu}\n",
-              G, steps, facade_ms, old_ms, 4 * G, 4 * G);
+              "\"facade_ms_per_step\": %.2f, \"facade_into_ms_per_step\": %.2f, \"round1_facade_ms_per_step\": %.2f, "
+              "\"parts_ms\": {\"set_grad_f64\": %.2f, \"step\": %.3f, \"aggregate_f64\": %.2f, "
+              "\"vector_double_G_alloc_zero\": %.2f}, \"h2d_bytes\": %zu, \"d2h_bytes\": %zu}\n",
+              G, steps, facade_ms, into_ms, old_ms, t_up / steps, t_step / steps, t_down / steps, t_alloc / steps, 4 * G,
+              4 * G);
   return 0;
 }
