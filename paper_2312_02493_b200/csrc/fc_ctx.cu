@@ -133,6 +133,11 @@ struct fc_ctx {
   std::vector<uint64_t> layer_off, layer_len;  // layer map (Layerwise), sorted, disjoint
   int thresh_rounds = 25;                      // Threshold bisection rounds
   float* scratch = nullptr;                    // G floats, for layer slices not 16-byte aligned
+  fcb::SmallLayer* h_small = nullptr;          // small layers' table (pinned) and its device copy
+  fcb::SmallLayer* d_small = nullptr;
+  int n_small = 0;
+  double small_cr = -1.0;
+  uint64_t small_ktot = 0;
   double* dnorms = nullptr;
   double* h_norms = nullptr;  // pinned
   // sticky error words (pinned, mapped into the device): set by a kernel whose
@@ -345,18 +350,49 @@ int run_select(fc_ctx* c, int i, uint64_t k, const float* ef_out = nullptr,
 }
 
 // Layerwise Top-k (inc/compress.hpp:67-79) of worker i's error-fed gradient
-// into its pack [idx ktot | val ktot]: for every layer an exact
-// Top-k_of(c, length) over the layer's slice (EF kernel with emission on the
-// slice + k_select, layer offset added to the indices), layers in map order.
+// into its pack [idx ktot | val ktot], layers in map order: every layer of
+// at most kSmallLayerMax elements in ONE launch (k_topk_small, one block per
+// layer); each larger layer through the EF kernel's candidate emission on
+// its slice + k_select_x (layer offset added to the indices).
 int run_layerwise(fc_ctx* c, int i, double cr, uint64_t ktot) {
   Worker& w = c->w[i];
   const int force_fb = std::getenv("FC_FORCE_FALLBACK") != nullptr ? 2 : 0;
   fcb::ChunkWs ws = w.ws;
   ws.cnorm = w.ws.cnorm + c->nch;  // keep the full pass's per-chunk norms
   float* vals = reinterpret_cast<float*>(w.pack + ktot);
+  // the small layers' table (pinned host -> device), rebuilt when c changes
+  const size_t nl = c->layer_off.size();
+  if (c->small_cr != cr || c->small_ktot != ktot) {
+    if (!c->h_small) {
+      CUDA_TRY(cudaStreamSynchronize(c->stream));
+      CUDA_TRY(cudaMallocHost(&c->h_small, nl * sizeof(fcb::SmallLayer)));
+      TRY(c->alloc(&c->d_small, nl));
+    } else {
+      CUDA_TRY(cudaStreamSynchronize(c->stream));  // the previous table's upload is done
+    }
+    uint64_t acc = 0;
+    c->n_small = 0;
+    for (size_t l = 0; l < nl; ++l) {
+      const uint64_t len = c->layer_len[l], kl = k_of_host(cr, len);
+      if (len <= fcb::kSmallLayerMax)
+        c->h_small[c->n_small++] = fcb::SmallLayer{(unsigned)c->layer_off[l], (unsigned)len, (unsigned)kl, (unsigned)acc};
+      acc += kl;
+    }
+    if (c->n_small)
+      CUDA_TRY(cudaMemcpyAsync(c->d_small, c->h_small, c->n_small * sizeof(fcb::SmallLayer), cudaMemcpyHostToDevice,
+                               c->stream));
+    c->small_cr = cr;
+    c->small_ktot = ktot;
+  }
+  fcb::launch_topk_small(w.ge, c->d_small, c->n_small, w.pack, vals, nullptr, c->stream);
+  LAUNCHED();
   uint64_t acc = 0;
-  for (size_t l = 0; l < c->layer_off.size(); ++l) {
+  for (size_t l = 0; l < nl; ++l) {
     const uint64_t off = c->layer_off[l], len = c->layer_len[l], kl = k_of_host(cr, len);
+    if (len <= fcb::kSmallLayerMax) {
+      acc += kl;
+      continue;
+    }
     float* src = w.ge + off;
     if (off % 4) {  // the EF kernel's bulk copies need 16-byte aligned rows
       if (!c->scratch) TRY(c->alloc(&c->scratch, c->G));
@@ -655,6 +691,7 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
     TRY(c->alloc(&s.cnorm, 2 * (uint64_t)nch));  // [full EF pass | layer passes]
     TRY(c->alloc(&s.g_part, 4096));
     TRY(c->alloc(&s.skeys, fcb::kSamples));
+    TRY(c->alloc(&s.segcnt, nch + 1));
     TRY(c->alloc(&s.tblk, 2 * (uint64_t)ef_grid));
   }
   CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -794,6 +831,7 @@ int fc_destroy(fc_ctx* c) {
     if (w.snap) cudaFree(w.snap);
   if (c->h_norms) cudaFreeHost(c->h_norms);
   if (c->h_err) cudaFreeHost(c->h_err);
+  if (c->h_small) cudaFreeHost(c->h_small);
   for (float* q : c->f64_stage) cudaFreeHost(q);
   for (cudaEvent_t e : c->f64_ev) cudaEventDestroy(e);
   for (auto& e : c->ev)
@@ -1823,6 +1861,13 @@ int fc_set_layer_map(fc_ctx* c, const uint64_t* offsets, const uint64_t* lengths
     if (l > 0 && off[l] < off[l - 1] + len[l - 1])
       return fail(FC_ERR_INVALID_ARGUMENT, "layers must be sorted and disjoint");
   }
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));  // a queued table upload is done
+  if (c->h_small) {
+    cudaFreeHost(c->h_small);
+    c->h_small = nullptr;  // (d_small stays in the context's allocations; a new one is made)
+  }
+  c->small_cr = -1.0;
   c->layer_off = std::move(off);
   c->layer_len = std::move(len);
   return FC_OK;

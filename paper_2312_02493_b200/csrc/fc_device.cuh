@@ -63,6 +63,7 @@ struct Ctl {
   unsigned hist3[2048];      // bits 10..0
   unsigned hist_w[4096];     // window histogram: key bits 30..11 relative to Lkey (k_select)
   unsigned done_sel;         // k_select_x: last-block counter (finalisation)
+  unsigned hist_w_ready;     // the EF pass built hist_w while emitting (k_select_x skips its P1 histogram)
   unsigned done_slice;       // k_fetch_gather two-stage broadcast: slice pulled
   unsigned lb_flag[kMaxGrid];             // k_select_x look-back: block b's total is in
   unsigned long long lb_tot[kMaxGrid];    // ... (gt << 32) | eq of block b
@@ -82,6 +83,7 @@ struct ChunkWs {
   unsigned long long* tblk;   // diagnostics: %globaltimer at each EF block's start and end
   unsigned* err;              // the context's sticky error words (host-mapped; see kErr*)
   unsigned* skeys;            // kSamples sampled |g_e| keys (the EF pass's candidate bound)
+  unsigned* segcnt;           // candidates per EF segment (EfLayout::seg_id), written by the EF pass
   unsigned nchunks;
   unsigned ef_grid;
   unsigned coop;              // grid-barrier kernels launched cooperatively (default)
@@ -106,6 +108,11 @@ struct EfLayout {
     nbat = (bnd + B - 1) / B;
   }
   __host__ __device__ bool seg_start(unsigned c) const { return c >= bnd || c % B == 0; }
+  __host__ __device__ bool seg_last(unsigned c, unsigned nchunks) const {
+    return c >= bnd || c % B == B - 1 || c + 1 == bnd || c + 1 == nchunks;
+  }
+  // segment number: batch c / B in [0, bnd), then one per single chunk
+  __host__ __device__ unsigned seg_id(unsigned c) const { return c < bnd ? c / B : nbat + (c - bnd); }
   __host__ __device__ unsigned seg_base(unsigned c) const { return c >= bnd ? c : c - c % B; }
 };
 // Batch size for a gradient of nchunks chunks on an EF grid of `blocks`
@@ -281,6 +288,15 @@ void launch_decode_ag(const unsigned* packs, uint64_t pack_stride, uint64_t k, i
                       unsigned* zmaps, int map_rank0, int nmaps, cudaStream_t s);
 void launch_dense_sum(const float* lists, int nlists, uint64_t list_stride, int divide,
                       float divisor, float* out, uint64_t G, cudaStream_t s);
+// topk_layerwise for the map's small layers in one launch (one block per
+// layer, exact top-k, index order): layer b = layers[b] (offset into g_e,
+// length, k, first pack position); per-layer ||top-k||^2 into norms (nullable).
+struct SmallLayer {
+  unsigned off, len, k, out;
+};
+constexpr unsigned kSmallLayerMax = 1u << 20;  // layers up to this many elements take the one-launch path
+void launch_topk_small(const float* ge, const SmallLayer* layers, int nlayers, unsigned* out_idx, float* out_val,
+                       double* norms, cudaStream_t s);
 int ef_grid_size();
 uint64_t launches();
 __host__ __device__ inline uint64_t nchunks_of(uint64_t G) { return (G + kChunk - 1) >> kChunkShift; }

@@ -586,6 +586,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
     }
   }
 
+  const unsigned wb = Lkey >> 11;  // the window base of the select's histogram
+  if (sampling && blockIdx.x == 0 && tid == 0) ctl->hist_w_ready = 1u;
   for (unsigned it = 0;; ++it) {
     const unsigned c = s_chunk[warp][it % kEfStages];
     if (c >= nchunks) break;
@@ -677,6 +679,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
       if (lay.seg_start(c)) brun = 0;
       unsigned pos = (lay.seg_base(c) << kChunkShift) + brun + incl - n;
       brun += run;
+      if (lane == 0 && lay.seg_last(c, nchunks)) w.segcnt[lay.seg_id(c)] = brun;  // the segment's total
       const float* my = sge + lane * 32;
       for (unsigned m = mask; m; m &= m - 1) {
         const int p = __ffs(m) - 1;
@@ -684,6 +687,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
         w.cand_idx[pos] = (unsigned)(base + (uint64_t)lane * 32 + p);
         w.cand_val[pos] = x;
         ++pos;
+        // the select's window histogram (key bits 30..11 from the bound's
+        // prefix), built here by fire-and-forget reductions (RED: no result,
+        // no stall) so that k_select_x starts at the bin search
+        if (sampling) atomicAdd(&ctl->hist_w[min((key_of(x) >> 11) - wb, 4095u)], 1u);
       }
     }
     if (c < nfull) {
@@ -1560,8 +1567,10 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
       atomicAdd(&s_h[key_of(x.z) >> kShift1], 1u);
       atomicAdd(&s_h[key_of(x.w) >> kShift1], 1u);
     }
-    if (blockIdx.x == 0)
+    if (blockIdx.x == 0) {
       for (uint64_t i = n4 * 4 + tid; i < G; i += kSxThreads) atomicAdd(&s_h[key_of(ef_out[i]) >> kShift1], 1u);
+      for (int q = tid; q < kSelBins; q += kSxThreads) ctl->hist_w[q] = 0u;  // (the EF's window counts are void)
+    }
     flush_hist(s_h, ctl->hist_fb, kBins1);
     grid_barrier(&ctl->bar_sel, bar, w.err);
     unsigned bin;
@@ -1601,6 +1610,10 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
 
   // ---- the block's position space ----
   for (unsigned j = tid; j < S; j += kSxThreads) {
+    if (!fb) {  // the EF pass wrote every segment's total
+      s_sct[j] = __ldcg(w.segcnt + lay.seg_id(seg_c0(j)));
+      continue;
+    }
     unsigned n = 0;
     for (unsigned c = seg_c0(j); c < seg_c1(j); ++c) n += __ldcg(w.cnt + c);
     s_sct[j] = n;
@@ -1705,9 +1718,15 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
   unsigned prefix = 0;
   bool windowed = false;
   const unsigned wb = Lb >> 11;
-  for (int b = tid; b < kSelBins; b += kSxThreads) s_h[b] = 0;
-  __syncthreads();
+  // the EF pass histogrammed the window while emitting (unless the fallback
+  // re-emitted the candidates): P1 is then a plain load/stage, no barrier
+  const bool ef_hist = !fb && __ldcg(&ctl->hist_w_ready) != 0u;
+  if (!ef_hist) {
+    for (int b = tid; b < kSelBins; b += kSxThreads) s_h[b] = 0;
+    __syncthreads();
+  }
   pass(U4{}, false, false, cached, [&](const float4& v, const uint4&, unsigned nv) {
+    if (ef_hist) return;
     for (unsigned e = 0; e < nv; ++e) {
       const unsigned hi = key_of(f4c(v, e)) >> 11;
       if (hi >= wb) atomicAdd(&s_h[min(hi - wb, (unsigned)kSelBins - 1u)], 1u);
@@ -1716,9 +1735,11 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
   SX_MARK(0);
   __syncthreads();
   if (tid == 0) reinterpret_cast<unsigned long long*>(w.g_part)[2048 + 2 * blockIdx.x] = gtimer();  // (diagnostics)
-  flush_hist(s_h, ctl->hist_w, kSelBins);
-  SX_MARK(1);
-  grid_barrier(&ctl->bar_sel, bar, w.err);
+  if (!ef_hist) {
+    flush_hist(s_h, ctl->hist_w, kSelBins);
+    SX_MARK(1);
+    grid_barrier(&ctl->bar_sel, bar, w.err);
+  }
   SEL_MARK(1);
   {
     unsigned bin;
@@ -2039,6 +2060,116 @@ int launch_select(uint64_t k, Ctl* ctl, const ChunkWs& w, const float* ef_out, u
   }
   count_launch();
   return e == cudaSuccess ? 0 : (int)e;
+}
+
+// ------------------------------------------------------ small-layer top-k ---
+// topk_layerwise (inc/compress.hpp:67-79) for every "small" layer of the map
+// in ONE launch: block b owns layer b entirely and computes its exact top-k
+// (select_topk_indices, compress.hpp:38-53: ties to the lower index, output
+// in index order) with three radix digits (12 | 8 | 11 key bits) over the
+// layer's g_e -- staged in shared memory when the layer fits, else re-read
+// from L2 -- then an ordered emission: per-thread contiguous element ranges,
+// one block scan of (> T, == T) counts, ties kept by block tie rank.  Output
+// pairs go to the layer's slot of the pack (indices + the layer offset).
+constexpr int kSlThreads = 1024;
+constexpr unsigned kSlSmem = 200 * 1024;  // layer staging (floats)
+
+__global__ void __launch_bounds__(kSlThreads, 1) k_topk_small(const float* __restrict__ ge,
+                                                              const SmallLayer* __restrict__ layers,
+                                                              unsigned* __restrict__ out_idx,
+                                                              float* __restrict__ out_val,
+                                                              double* __restrict__ norms) {
+  pdl_wait();
+  extern __shared__ __align__(16) float s_lay[];
+  __shared__ unsigned s_h[kSelBins];
+  __shared__ unsigned long long s_scan[kSlThreads / 32 + 1];
+  __shared__ double s_dred[kSlThreads / 32];
+  const SmallLayer L = layers[blockIdx.x];
+  const unsigned len = L.len, tid = threadIdx.x;
+  const float* src = ge + L.off;
+  const bool staged = len <= kSlSmem / 4;
+  if (staged) {
+    for (unsigned i = tid; i < len; i += kSlThreads) s_lay[i] = __ldcg(src + i);
+    __syncthreads();
+  }
+  auto val = [&](unsigned i) -> float { return staged ? s_lay[i] : __ldcg(src + i); };
+  // three digits of the k-th largest key
+  const int shifts[3] = {kShift1, 11, 0};
+  const int widths[3] = {12, 8, 11};
+  unsigned long long need = L.k;
+  unsigned prefix = 0;
+  int as = 31;
+  for (int d = 0; d < 3; ++d) {
+    const int nb = 1 << widths[d], sh = shifts[d];
+    for (int b = tid; b < nb; b += kSlThreads) s_h[b] = 0;
+    __syncthreads();
+    const unsigned pf = prefix, dm = (unsigned)nb - 1;
+    for (unsigned i = tid; i < len; i += kSlThreads) {
+      const unsigned key = key_of(val(i));
+      if ((unsigned)((unsigned long long)key >> as) == pf) atomicAdd(&s_h[(key >> sh) & dm], 1u);
+    }
+    unsigned bin;
+    unsigned long long above;
+    block_select_top<kSlThreads>(s_h, nb, need, bin, above, s_h);
+    need -= above;
+    prefix = (prefix << widths[d]) | bin;
+    as = sh;
+  }
+  const unsigned T = prefix;
+  const unsigned long long needT = need;
+  // ordered emission: warp w walks [w R, (w + 1) R), 32 consecutive elements
+  // per iteration (coalesced); ballots give in-order positions
+  const int lane = tid & 31, warp = tid >> 5;
+  const unsigned lt = lanemask_lt();
+  const unsigned R = (len + kSlThreads - 1) / kSlThreads * 32;
+  const unsigned w0 = min(len, warp * R), w1 = min(len, w0 + R);
+  unsigned gt = 0, eq = 0;
+  for (unsigned i0 = w0; i0 < w1; i0 += 32) {
+    const unsigned i = i0 + lane;
+    const unsigned key = i < w1 ? key_of(val(i)) : 0u;
+    gt += __popc(__ballot_sync(0xffffffffu, i < w1 && key > T));
+    eq += __popc(__ballot_sync(0xffffffffu, i < w1 && key == T));
+  }
+  if (lane == 0) s_scan[warp] = ((unsigned long long)gt << 32) | eq;
+  __syncthreads();
+  if (warp == 0) {
+    const unsigned long long x = s_scan[lane];
+    const unsigned long long inc = warp_incl_scan(x);
+    s_scan[lane] = inc - x;
+  }
+  __syncthreads();
+  unsigned long long gb = s_scan[warp] >> 32, eb = s_scan[warp] & 0xffffffffull;
+  double acc = 0.0;
+  for (unsigned i0 = w0; i0 < w1; i0 += 32) {
+    const unsigned i = i0 + lane;
+    const float x = i < w1 ? val(i) : 0.f;
+    const unsigned key = key_of(x);
+    const bool g = i < w1 && key > T, q = i < w1 && key == T;
+    const unsigned gm = __ballot_sync(0xffffffffu, g), qm = __ballot_sync(0xffffffffu, q);
+    const unsigned long long my_eb = eb + __popc(qm & lt);
+    if (g || (q && my_eb < needT)) {
+      const unsigned long long pos = L.out + gb + __popc(gm & lt) + min(my_eb, needT);
+      out_idx[pos] = L.off + i;
+      out_val[pos] = x;
+      acc = fma((double)x, (double)x, acc);
+    }
+    gb += __popc(gm);
+    eb += __popc(qm);
+  }
+  const double t = block_sum<kSlThreads>(acc, s_dred);
+  if (tid == 0 && norms) norms[blockIdx.x] = t;
+}
+
+void launch_topk_small(const float* ge, const SmallLayer* layers, int nlayers, unsigned* out_idx, float* out_val,
+                       double* norms, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_topk_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSlSmem);
+    attr = true;
+  }
+  if (nlayers <= 0) return;
+  launch_pdl(k_topk_small, nlayers, kSlThreads, kSlSmem, s, ge, layers, out_idx, out_val, norms);
+  count_launch();
 }
 
 // Fixed-order sum of per-chunk partials (one block): reproducible regardless

@@ -61,6 +61,33 @@ def test_layerwise_trajectory(fc, f32, n):
     run_traj(fc, f32, n, g, fc.LAYERWISE, [0.01, 0.1, 0.25, 0.003], layers, dist=n % 3, seed=3 + n)
 
 
+def test_layerwise_small_and_large_layers(fc, f32):
+    """Layers above kSmallLayerMax (1M elements) go through the EF-emission
+    + k_select_x path, the rest through the one-launch small-layer kernel;
+    mixed maps (unaligned offsets, a tie-heavy input) stay bit-exact."""
+    g = 3_200_003
+    layers = [(0, 100), (100, 2_500_000), (2_500_101, 64), (2_500_165, 699_838)]
+    run_traj(fc, f32, 2, g, fc.LAYERWISE, [0.01, 0.001, 0.1], layers, dist=1, seed=77, max_cr=0.1)
+
+
+def test_layerwise_vgg16_map(fc, f32):
+    """VGG-16's 32-layer map (13 conv + 3 FC, weights then biases) scaled to
+    a ~27M-element gradient (convolutions at full size, FC layers shrunk),
+    two workers, two steps."""
+    convs = [(3, 64), (64, 64), (64, 128), (128, 128), (128, 256), (256, 256), (256, 256),
+             (256, 512), (512, 512), (512, 512), (512, 512), (512, 512), (512, 512)]
+    sizes = []
+    for cin, cout in convs:
+        sizes += [cin * cout * 9, cout]
+    for fin, fout in [(2508, 4096), (4096, 409), (4096, 100)]:
+        sizes += [fin * fout, fout]
+    layers, off = [], 0
+    for m in sizes:
+        layers.append((off, m))
+        off += m
+    run_traj(fc, f32, 2, off, fc.LAYERWISE, [0.01, 0.05], layers, seed=16, max_cr=0.1)
+
+
 def test_layerwise_without_map_is_exact(fc, f32):
     run_traj(fc, f32, 2, 30_011, fc.LAYERWISE, [0.01, 0.05], None, seed=9)
 

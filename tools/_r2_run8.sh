@@ -1,0 +1,8 @@
+export OMP_NUM_THREADS=1
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_compressors.py tests/test_gpu_async.py tests/test_gpu_moo.py -x -q --durations=8 > gpurun_out/r2_pytest8.log 2>&1; echo rc=$? >> gpurun_out/r2_pytest8.log
+timeout 300 python tools/diag_select.py 138000000 0.01 > gpurun_out/r2_sel8_c3.txt 2>&1
+timeout 300 python tools/diag_select.py 355000000 0.1 > gpurun_out/r2_sel8_c4.txt 2>&1
+timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/r2_bench8.json 2> gpurun_out/r2_bench8.err
+timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e --config C3-lw > gpurun_out/r2_bench8_lw.json 2> gpurun_out/r2_bench8_lw.err
+timeout 300 python tools/diag_step.py > gpurun_out/r2_diag_step8.jsonl 2>&1
+timeout 900 python -m pytest tests/test_gpu_fullsize.py -x -q > gpurun_out/r2_pytest8_full.log 2>&1; echo rc=$? >> gpurun_out/r2_pytest8_full.log

@@ -10,3 +10,4 @@ for cfg in "dense ring" "star ring" "ag ring"; do
   set -- $cfg
   timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29813 bench.py --gpus 2 --mode $1 --algo $2 --no-e2e > gpurun_out/r2_bench_n2_$1_$2.json 2> gpurun_out/r2_bench_n2_$1_$2.err
 done
+timeout 300 python tools/diag_select.py 138000000 0.01 > gpurun_out/r2_sel_n4box.txt 2>&1; timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/r2_bench_n4box_n1.json 2>/dev/null

@@ -9,15 +9,18 @@ reference validates that choice against measured collective times
 the three exchanges as the product runs them -- over NVLink peer memory,
 with the product's own kernels -- on this box's GPUs, max over ranks:
 
+  step grid       whole steps (fc_artopk_step Ring / Tree, fc_ag_step) at
+                  BASELINE configs 1-3 (G, CR) and seven more (G, CR) points
+                  (Mc = 4 G c = 47 KB .. 55 MB), plus the same steps of a
+                  one-worker context on the same GPU (no exchange): the
+                  measured sync time of a collective is its step minus the
+                  one-worker step of the same kind -- what choosing that
+                  collective costs the step (the fit's input)
   exchange grid   fc_diag_exchange_ms(AG / ART-Ring / ART-Tree) for k
                   (index, value) pairs, k = 1e3 .. 1.38e7 (Mc = 4k bytes):
                   the communication alone, from the selections being
-                  published to the decode's inputs being in place
-  step grid       whole steps (fc_artopk_step Ring / Tree, fc_ag_step) at
-                  BASELINE configs 1-3 (G, CR), plus the same steps of a
-                  one-worker context on the same GPU (no exchange): the
-                  measured sync time of a collective is its step minus the
-                  one-worker step of the same kind
+                  published to the decode's inputs being in place (reported
+                  beside the fit: it leaves out the N-list decode of AG)
 
 Writes fixtures/peer_exchange_n{N}.csv and fixtures/peer_steps_n{N}.csv;
 tools/fit_peer.py fits NetParams to them (no GPU needed).
@@ -39,7 +42,13 @@ from paper_2312_02493_b200 import flexcomm as fc  # noqa: E402
 from paper_2312_02493_b200._abi import check, lib  # noqa: E402
 
 KS = [1_000, 4_000, 25_600, 117_000, 400_000, 1_380_000, 4_000_000, 13_800_000]
-CONFIGS = [("C1", 11_700_000, 0.01), ("C2", 25_600_000, 0.001), ("C3", 138_000_000, 0.01)]
+# BASELINE configs 1-3, plus more (G, CR) points spanning Mc = 4 G c bytes
+# from 47 KB to 55 MB for the fit
+CONFIGS = [("C1", 11_700_000, 0.01), ("C2", 25_600_000, 0.001), ("C3", 138_000_000, 0.01),
+           ("G11.7M-c0.001", 11_700_000, 0.001), ("G11.7M-c0.1", 11_700_000, 0.1),
+           ("G25.6M-c0.01", 25_600_000, 0.01), ("G138M-c0.001", 138_000_000, 0.001),
+           ("G138M-c0.003", 138_000_000, 0.003), ("G138M-c0.03", 138_000_000, 0.03),
+           ("G138M-c0.1", 138_000_000, 0.1)]
 KINDS = ["ag", "art_ring", "art_tree"]
 
 
@@ -107,16 +116,21 @@ def main() -> int:
         row = {"n": n, "config": name, "grad_len": G, "cr": cr, "k": fc.k_of(cr, G)}
         with fc.Cluster.nccl(n, env.rank, uid, G, device=env.local_rank, max_cr=cr, flags=flags) as cl:
             cl.fill_synthetic(0, 42, env.rank, 0)
-            for kind in KINDS:
-                env.barrier()
-                row[kind + "_step_us"] = env.max_over_ranks(time_steps(cl, kind, cr, 30, 5, env)) * 1e3
+            for kind in KINDS:  # best of 3 runs of 30 steps (max over ranks each)
+                ts = []
+                for _ in range(3):
+                    env.barrier()
+                    ts.append(env.max_over_ranks(time_steps(cl, kind, cr, 30, 5, env)) * 1e3)
+                row[kind + "_step_us"] = min(ts)
         # the same steps without an exchange: one worker on this GPU
         with fc.Cluster(1, G, device=env.local_rank, max_cr=cr, flags=flags) as one:
             one.fill_synthetic(0, 42, env.rank, 0)
-            env.barrier()
-            row["art_one_worker_us"] = env.max_over_ranks(time_steps(one, "art_ring", cr, 30, 5)) * 1e3
-            env.barrier()
-            row["ag_one_worker_us"] = env.max_over_ranks(time_steps(one, "ag", cr, 30, 5)) * 1e3
+            for kind, key in (("art_ring", "art_one_worker_us"), ("ag", "ag_one_worker_us")):
+                ts = []
+                for _ in range(3):
+                    env.barrier()
+                    ts.append(env.max_over_ranks(time_steps(one, kind, cr, 30, 5)) * 1e3)
+                row[key] = min(ts)
         st_rows.append(row)
         if env.rank == 0:
             print(json.dumps(row), flush=True)

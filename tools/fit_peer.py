@@ -2,19 +2,23 @@
 
     python tools/fit_peer.py [fixtures_dir]
 
-Reads fixtures/peer_exchange_n{N}.csv and fixtures/peer_steps_n{N}.csv
+Reads fixtures/peer_steps_n{N}.csv and fixtures/peer_exchange_n{N}.csv
 (tools/calibrate_peer.py, run on the GPUs) and fits ONE NetParams(alpha,
 bandwidth) per N -- the reference's API has a single one
 (inc/costmodel.hpp:12-27) -- by least squares on log time over the three
-exchanges of the exchange grid (the communication the selector models:
-cost_ag_compressed / cost_art_ring / cost_art_tree, inc/costmodel.hpp:79-96,
-with Mc = 4k bytes).  Then it checks the unchanged select_collective
-(inc/costmodel.hpp:153-167) the way the reference checks its fixtures
-(tests/test_acceptance.cpp:45-60): the predicted fastest collective must be
-the measured fastest wherever the measured top-two margin exceeds 15 %, on
-the exchange grid and on the whole-step grid of BASELINE configs 1-3 (sync
-time = step - the one-worker step of the same kind).  Writes
-fixtures/peer_fit_n{N}.json.
+collectives' measured SYNC times of whole steps (step - the one-worker step
+of the same kind; ten (G, CR) points incl. BASELINE configs 1-3, Mc =
+4 G c), against cost_ag_compressed / cost_art_ring / cost_art_tree
+(inc/costmodel.hpp:79-96).  The sync time is what choosing a collective
+costs a step; it includes AG's N-list decode, which the formulas have no
+term for, so the fitted bandwidth is an effective one for the whole sync
+path rather than the link's.  Then it checks the unchanged
+select_collective (inc/costmodel.hpp:153-167) the way the reference checks
+its fixtures (tests/test_acceptance.cpp:45-60): the predicted fastest must
+be the measured fastest wherever the measured top-two margin exceeds 15 %,
+and (stricter) the predicted collective's measured time is within 15 % of
+the fastest at every point.  The exchange-only grid is checked against the
+same fit and reported, not fitted.  Writes fixtures/peer_fit_n{N}.json.
 """
 from __future__ import annotations
 
@@ -117,20 +121,24 @@ def main() -> int:
     worlds = sorted(int(p.stem.split("_n")[-1]) for p in d.glob("peer_exchange_n*.csv"))
     for n in worlds:
         ex, st = load(d, n)
-        pts = [(mc, meas) for mc, meas, _ in ex]
+        pts = [(mc, meas) for mc, meas, _ in st]
         alpha, beta = fit(n, pts)
-        exc = check(alpha, beta, n, pts, [lab for *_, lab in ex])
+        exc = check(alpha, beta, n, [(mc, meas) for mc, meas, _ in ex], [lab for *_, lab in ex])
         stc = check(alpha, beta, n, [(mc, meas) for mc, meas, _ in st], [lab for *_, lab in st])
         dec = [c for c in exc if c["decisive"]]
         sdec = [c for c in stc if c["decisive"]]
-        res = {"n": n, "source": "product peer-memory exchange (fc_diag_exchange_ms), tools/calibrate_peer.py",
+        regret = max((c["measured_us"][c["predicted"]] / c["measured_us"][c["measured_fastest"]] - 1.0)
+                     for c in stc) if stc else None
+        res = {"n": n, "source": "whole steps on the product's peer-memory exchange, tools/calibrate_peer.py",
                "alpha_s": alpha, "bandwidth_bps": 8.0 / beta, "bandwidth_GBps": 1.0 / beta / 1e9,
-               "fit": "least squares on log time, AG / ART-Ring / ART-Tree exchange grid",
+               "fit": "least squares on log time, AG / ART-Ring / ART-Tree step sync times "
+                      "(step - one-worker step), effective bandwidth of the whole sync path",
+               "step_max_regret": regret,
                "exchange_agreement_decisive": (sum(c["agree"] for c in dec) / len(dec)) if dec else None,
                "exchange_decisive_points": len(dec),
                "step_agreement_decisive": (sum(c["agree"] for c in sdec) / len(sdec)) if sdec else None,
                "step_decisive_points": len(sdec),
-               "max_rel_err": max(max(c["rel_err"].values()) for c in exc),
+               "max_rel_err": max(max(c["rel_err"].values()) for c in stc),
                "exchange_points": exc, "step_points": stc}
         (d / f"peer_fit_n{n}.json").write_text(json.dumps(res, indent=1))
         print(json.dumps({kk: v for kk, v in res.items() if not kk.endswith("_points")}))
