@@ -96,7 +96,15 @@ typedef enum fc_memkind { FC_HOST = 0, FC_DEVICE = 1, FC_HOST_ASYNC = 2 } fc_mem
                                      bounded barriers time out (reported as
                                      FC_ERR_RUNTIME) instead of the launch waiting */
 
+#define FC_FLAG_PEER_ONLY 0x20u  /* one worker per process over peer memory WITHOUT
+                                     NCCL (2 <= world <= 8, nccl_uid NULL): the
+                                     caller exchanges the exchange-buffer handles
+                                     (fc_peer_handle -> allgather -> fc_peer_attach);
+                                     STAR / VAR AR-Top-k and exact AG only (several
+                                     ranks may share a GPU, which NCCL forbids) */
+
 #define FC_NCCL_UID_BYTES 128
+#define FC_PEER_HANDLE_BYTES 64
 
 typedef struct fc_opts {
   int device;           /* CUDA ordinal for this context                       */
@@ -314,6 +322,12 @@ int fc_moo_metrics(fc_ctx* ctx, int ag, const fc_step_stats* stats, double* gain
  * reference), 0 if they use NCCL collectives (FC_NO_P2P=1 in the environment
  * forces that). */
 int fc_peer_exchange(fc_ctx* ctx, int* enabled);
+/* FC_FLAG_PEER_ONLY contexts: this rank's exchange-buffer handle, and the
+ * attachment of every rank's (world x FC_PEER_HANDLE_BYTES, rank order,
+ * allgathered by the caller -- e.g. over a torch.distributed gloo group).
+ * Steps need the attachment; every rank attaches before the first step. */
+int fc_peer_handle(fc_ctx* ctx, unsigned char out[FC_PEER_HANDLE_BYTES]);
+int fc_peer_attach(fc_ctx* ctx, const unsigned char* handles);
 
 /* Peer-exchange epoch waits give up after `seconds` (default 120): the
  * waiting kernel skips its remaining reads and the timeout is reported as

@@ -31,6 +31,8 @@ FC_FLAG_NO_TIMING = 0x2
 FC_FLAG_DENSE_DECODE = 0x4
 FC_FLAG_PIPELINE = 0x8
 FC_FLAG_NO_COOPERATIVE = 0x10
+FC_FLAG_PEER_ONLY = 0x20
+FC_PEER_HANDLE_BYTES = 64
 FC_NCCL_UID_BYTES = 128
 FC_DIST_NORMAL, FC_DIST_TIES, FC_DIST_LAYERED = 0, 1, 2
 
@@ -168,6 +170,8 @@ def _load() -> C.CDLL:
         "fc_set_residual_f64": ([P, i, P], i),
         "fc_get_residual_f64": ([P, i, P], i),
         "fc_get_aggregate_f64": ([P, P], i),
+        "fc_peer_handle": ([P, P], i),
+        "fc_peer_attach": ([P, P], i),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(lib, name)
@@ -192,7 +196,7 @@ EXPORTS = [
     "fc_controller_config_validate", "fc_round_3sig", "fc_candidate_ladder", "fc_trigger_gain",
     "fc_pareto_front", "fc_choose_cr", "fc_network_changed", "fc_moo_metrics", "fc_peer_exchange",
     "fc_set_peer_timeout", "fc_diag_exchange_ms", "fc_set_grad_f64", "fc_set_residual_f64",
-    "fc_get_residual_f64", "fc_get_aggregate_f64",
+    "fc_get_residual_f64", "fc_get_aggregate_f64", "fc_peer_handle", "fc_peer_attach",
 ]
 
 

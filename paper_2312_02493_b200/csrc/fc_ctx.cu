@@ -155,6 +155,8 @@ struct fc_ctx {
   // peer-memory exchange (NCCL contexts, 1 < world <= 8, every rank's
   // exchange buffer mapped into every other with CUDA IPC over NVLink)
   bool p2p = false;
+  bool peer_only = false;           // FC_FLAG_PEER_ONLY: no NCCL, handles exchanged by the caller
+  cudaIpcMemHandle_t my_handle{};
   fcb::PeerBufs pb{};
   void* xbuf = nullptr;
   std::vector<void*> peer_maps;
@@ -590,7 +592,13 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
   c->G = o->grad_len;
   c->flags = o->flags;
   c->timing = !(o->flags & FC_FLAG_NO_TIMING);
-  c->nccl = o->nccl_uid != nullptr;
+  c->peer_only = (o->flags & FC_FLAG_PEER_ONLY) != 0;
+  if (c->peer_only) {
+    if (o->nccl_uid) return fail(FC_ERR_INVALID_ARGUMENT, "a peer-only context takes no NCCL id");
+    if (o->world < 2 || o->world > fcb::kMaxPeers)
+      return fail(FC_ERR_INVALID_ARGUMENT, "a peer-only context needs 2 <= world <= 8");
+  }
+  c->nccl = o->nccl_uid != nullptr || c->peer_only;  // one worker per process
   c->n_local = o->n_local;
   if (c->nccl) {
     if (o->n_local != 1) return fail(FC_ERR_INVALID_ARGUMENT, "NCCL contexts hold one worker");
@@ -696,7 +704,7 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
   }
   CUDA_TRY(cudaStreamSynchronize(c->stream));
 
-  if (c->nccl) {
+  if (c->nccl && !c->peer_only) {
     ncclUniqueId id;
     std::memcpy(&id, o->nccl_uid, sizeof(id));
     const bool force = std::getenv("FC_NCCL_NO_FORCE_ALGO") == nullptr;
@@ -717,26 +725,96 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
   return FC_OK;
 }
 
-// Map every rank's exchange buffer into every other rank (CUDA IPC handles
-// allgathered over NCCL); used only if every rank succeeds.  FC_NO_P2P=1
-// keeps the NCCL collectives.
+// ---- the peer-memory exchange buffers --------------------------------------
+// Layout of one rank's exchange buffer (parity strides are multiples of 4
+// elements: 16-byte rows for vector pulls).
+struct XLayout {
+  uint64_t kst, nbs, list_b, contrib_b, bounds_b, inbox_b, box_b, total;
+  XLayout(const fc_ctx* c) {
+    const int N = c->world;
+    kst = align_up(c->kmax, 4);
+    nbs = align_up(c->nch + 1, 4);
+    list_b = align_up(2 * kst * sizeof(unsigned), 256);
+    contrib_b = align_up(2 * kst * sizeof(float), 256);
+    bounds_b = align_up(2 * nbs * sizeof(unsigned), 256);
+    inbox_b = align_up(N * 2 * kst * sizeof(float), 256);
+    box_b = align_up(N * 8 * sizeof(unsigned long long), 256);
+    total = list_b + 2 * contrib_b + inbox_b + bounds_b + box_b;
+  }
+};
+
+// Allocate and export this rank's exchange buffer.
+int p2p_alloc(fc_ctx* c, cudaIpcMemHandle_t* mine, int* ok) {
+  const XLayout L(c);
+  CUDA_TRY(cudaMalloc(&c->xbuf, L.total));
+  CUDA_TRY(cudaMemset(c->xbuf, 0, L.total));
+  *ok = cudaIpcGetMemHandle(mine, c->xbuf) == cudaSuccess ? 1 : 0;
+  cudaGetLastError();
+  return FC_OK;
+}
+
+// Map every peer's buffer (handles in rank order); *ok = 0 if any failed
+// (nothing stays mapped then).
+int p2p_open(fc_ctx* c, const cudaIpcMemHandle_t* hs, int* ok) {
+  const int N = c->world;
+  std::vector<unsigned char*> base(N, nullptr);
+  base[c->rank] = static_cast<unsigned char*>(c->xbuf);
+  for (int r = 0; r < N && *ok; ++r) {
+    if (r == c->rank) continue;
+    void* p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, hs[r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      *ok = 0;
+      break;
+    }
+    c->peer_maps.push_back(p);
+    base[r] = static_cast<unsigned char*>(p);
+  }
+  if (!*ok) {
+    for (void* p : c->peer_maps) cudaIpcCloseMemHandle(p);
+    c->peer_maps.clear();
+    return FC_OK;
+  }
+  const XLayout L(c);
+  c->pb.n = N;
+  c->pb.rank = c->rank;
+  c->pb.err = c->d_err;
+  if (!c->pb.timeout_ns) c->pb.timeout_ns = 120ull * 1000000000ull;
+  c->pb.kmax = L.kst;
+  c->pb.nb = c->nch + 1;
+  c->pb.nbs = L.nbs;
+  for (int r = 0; r < N; ++r) {
+    unsigned char* x = base[r];
+    c->pb.list[r] = reinterpret_cast<unsigned*>(x);
+    c->pb.contrib[r] = reinterpret_cast<float*>(x + L.list_b);
+    c->pb.reduced[r] = reinterpret_cast<float*>(x + L.list_b + L.contrib_b);
+    c->pb.inbox[r] = reinterpret_cast<float*>(x + L.list_b + 2 * L.contrib_b);
+    c->pb.bounds[r] = reinterpret_cast<unsigned*>(x + L.list_b + 2 * L.contrib_b + L.inbox_b);
+    c->pb.box[r] = reinterpret_cast<unsigned long long*>(x + L.list_b + 2 * L.contrib_b + L.inbox_b + L.bounds_b);
+  }
+  c->p2p = true;
+  return FC_OK;
+}
+
+// NCCL contexts: map every rank's exchange buffer into every other rank (CUDA
+// IPC handles allgathered over NCCL); used only if every rank succeeds.
+// FC_NO_P2P=1 keeps the NCCL collectives.  Peer-only contexts
+// (FC_FLAG_PEER_ONLY) allocate the buffer here and attach in fc_peer_attach,
+// with the handles exchanged by the caller.
 int setup_p2p(fc_ctx* c) {
   const int N = c->world;
+  if (c->peer_only) {
+    cudaIpcMemHandle_t mine{};
+    int ok = 1;
+    TRY(p2p_alloc(c, &mine, &ok));
+    if (!ok) return fail(FC_ERR_CUDA, "cudaIpcGetMemHandle failed for the exchange buffer");
+    c->my_handle = mine;
+    return FC_OK;
+  }
   if (!c->nccl || N < 2 || N > fcb::kMaxPeers || std::getenv("FC_NO_P2P")) return FC_OK;
-  // parity strides are multiples of 4 elements (16-byte rows for vector pulls)
-  const uint64_t kst = align_up(c->kmax, 4), nbs = align_up(c->nch + 1, 4);
-  const uint64_t list_b = align_up(2 * kst * sizeof(unsigned), 256);
-  const uint64_t contrib_b = align_up(2 * kst * sizeof(float), 256);
-  const uint64_t bounds_b = align_up(2 * nbs * sizeof(unsigned), 256);
-  const uint64_t inbox_b = align_up(N * 2 * kst * sizeof(float), 256);
-  const uint64_t box_b = align_up(N * 8 * sizeof(unsigned long long), 256);
-  const uint64_t total = list_b + 2 * contrib_b + inbox_b + bounds_b + box_b;
-  CUDA_TRY(cudaMalloc(&c->xbuf, total));
-  CUDA_TRY(cudaMemset(c->xbuf, 0, total));
-  int ok = 1;
   cudaIpcMemHandle_t mine{};
-  if (cudaIpcGetMemHandle(&mine, c->xbuf) != cudaSuccess) ok = 0;
-  cudaGetLastError();
+  int ok = 1;
+  TRY(p2p_alloc(c, &mine, &ok));
   unsigned char* dh = nullptr;
   int* dok = nullptr;
   CUDA_TRY(cudaMalloc(&dh, (N + 1) * sizeof(cudaIpcMemHandle_t)));
@@ -747,19 +825,7 @@ int setup_p2p(fc_ctx* c) {
   std::vector<cudaIpcMemHandle_t> hs(N);
   CUDA_TRY(cudaMemcpyAsync(hs.data(), dh, N * sizeof(cudaIpcMemHandle_t), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
-  std::vector<unsigned char*> base(N, nullptr);
-  base[c->rank] = static_cast<unsigned char*>(c->xbuf);
-  for (int r = 0; r < N && ok; ++r) {
-    if (r == c->rank) continue;
-    void* p = nullptr;
-    if (cudaIpcOpenMemHandle(&p, hs[r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-      cudaGetLastError();
-      ok = 0;
-      break;
-    }
-    c->peer_maps.push_back(p);
-    base[r] = static_cast<unsigned char*>(p);
-  }
+  TRY(p2p_open(c, hs.data(), &ok));
   // every rank must take the same path
   CUDA_TRY(cudaMemcpy(dok, &ok, sizeof(int), cudaMemcpyHostToDevice));
   NCCL_TRY(ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, c->comm_ring, c->stream));
@@ -767,28 +833,21 @@ int setup_p2p(fc_ctx* c) {
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   cudaFree(dh);
   cudaFree(dok);
-  if (!ok) {
+  if (!ok && c->p2p) {  // a peer failed: everyone falls back to NCCL
     for (void* p : c->peer_maps) cudaIpcCloseMemHandle(p);
     c->peer_maps.clear();
-    return FC_OK;
+    c->p2p = false;
   }
-  c->pb.n = N;
-  c->pb.rank = c->rank;
-  c->pb.err = c->d_err;
-  c->pb.timeout_ns = 120ull * 1000000000ull;
-  c->pb.kmax = kst;
-  c->pb.nb = c->nch + 1;
-  c->pb.nbs = nbs;
-  for (int r = 0; r < N; ++r) {
-    unsigned char* x = base[r];
-    c->pb.list[r] = reinterpret_cast<unsigned*>(x);
-    c->pb.contrib[r] = reinterpret_cast<float*>(x + list_b);
-    c->pb.reduced[r] = reinterpret_cast<float*>(x + list_b + contrib_b);
-    c->pb.inbox[r] = reinterpret_cast<float*>(x + list_b + 2 * contrib_b);
-    c->pb.bounds[r] = reinterpret_cast<unsigned*>(x + list_b + 2 * contrib_b + inbox_b);
-    c->pb.box[r] = reinterpret_cast<unsigned long long*>(x + list_b + 2 * contrib_b + inbox_b + bounds_b);
-  }
-  c->p2p = true;
+  return FC_OK;
+}
+
+// Operations on the NCCL communicators are not available in peer-only
+// contexts (and steps need the peer mappings there).
+int need_comm(fc_ctx* c, const char* what) {
+  if (c->nccl && c->world > 1 && !c->comm_ring)
+    return fail(FC_ERR_INVALID_ARGUMENT,
+                std::string(what) + " needs NCCL communicators (this is a peer-only context"
+                + (c->p2p ? ")" : " not attached yet: fc_peer_attach)"));
   return FC_OK;
 }
 
@@ -821,6 +880,9 @@ int fc_destroy(fc_ctx* c) {
   if (c->p2p && c->comm_ring && c->dsel) {
     if (ncclAllReduce(c->dsel, c->dsel, 1, ncclInt32, ncclMax, c->comm_ring, c->stream) == ncclSuccess)
       cudaStreamSynchronize(c->stream);
+  } else if (c->p2p && c->peer_only) {  // the same barrier through the mailboxes
+    fcb::launch_peer_barrier(c->pb, c->stream);
+    cudaStreamSynchronize(c->stream);
   }
   for (void* p : c->peer_maps) cudaIpcCloseMemHandle(p);
   if (c->xbuf) cudaFree(c->xbuf);
@@ -1151,6 +1213,29 @@ int fc_restore(fc_ctx* c) {
   return FC_OK;
 }
 
+int fc_peer_handle(fc_ctx* c, unsigned char out[FC_PEER_HANDLE_BYTES]) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == FC_PEER_HANDLE_BYTES, "IPC handle size");
+  if (!c || !out) return fail(FC_ERR_INVALID_ARGUMENT, "null argument");
+  if (!c->peer_only) return fail(FC_ERR_INVALID_ARGUMENT, "not a peer-only context (FC_FLAG_PEER_ONLY)");
+  std::memcpy(out, &c->my_handle, sizeof(c->my_handle));
+  return FC_OK;
+}
+
+int fc_peer_attach(fc_ctx* c, const unsigned char* handles) {
+  if (!c || !handles) return fail(FC_ERR_INVALID_ARGUMENT, "null argument");
+  if (!c->peer_only) return fail(FC_ERR_INVALID_ARGUMENT, "not a peer-only context (FC_FLAG_PEER_ONLY)");
+  if (c->p2p) return fail(FC_ERR_INVALID_ARGUMENT, "already attached");
+  CUDA_TRY(cudaSetDevice(c->device));
+  std::vector<cudaIpcMemHandle_t> hs(c->world);
+  std::memcpy(hs.data(), handles, c->world * sizeof(cudaIpcMemHandle_t));
+  if (std::memcmp(&hs[c->rank], &c->my_handle, sizeof(c->my_handle)) != 0)
+    return fail(FC_ERR_INVALID_ARGUMENT, "handles[rank] is not this context's handle (rank order?)");
+  int ok = 1;
+  TRY(p2p_open(c, hs.data(), &ok));
+  if (!ok) return fail(FC_ERR_CUDA, "cudaIpcOpenMemHandle failed for a peer's exchange buffer");
+  return FC_OK;
+}
+
 int fc_set_peer_timeout(fc_ctx* c, double seconds) {
   if (!c) return fail(FC_ERR_INVALID_ARGUMENT, "null context");
   if (!(seconds > 0.0) || seconds > 1e7) return fail(FC_ERR_INVALID_ARGUMENT, "timeout must be in (0, 1e7] s");
@@ -1166,6 +1251,7 @@ int fc_peer_exchange(fc_ctx* c, int* enabled) {
 
 int fc_moo_metrics(fc_ctx* c, int ag, const fc_step_stats* st, double* gain, double* t_comp_s) {
   if (!c || !st || !gain || !t_comp_s) return fail(FC_ERR_INVALID_ARGUMENT, "null argument");
+  TRY(need_comm(c, "fc_moo_metrics"));
   CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   // this process's workers: (gain_r, t_comp, degenerate_r) triples.  A
@@ -1311,6 +1397,7 @@ int fc_diag_kernel_ms(fc_ctx* c, int which, int iters, double* ms_out) {
 int fc_diag_collective_ms(fc_ctx* c, int which, uint64_t bytes, int iters, double* ms_out) {
   if (!c || !ms_out || iters < 1) return fail(FC_ERR_INVALID_ARGUMENT, "bad argument");
   if (!c->nccl) return fail(FC_ERR_INVALID_ARGUMENT, "needs an NCCL context");
+  TRY(need_comm(c, "fc_diag_collective_ms"));
   const uint64_t cap = c->kmax * 4;  // bytes available in bidx / reduced / pack
   const uint64_t need = (which == 3 || which == 6) ? (which == 6 ? 2 * bytes : bytes) : bytes;
   if (need > 2 * cap || (which != 3 && which != 6 && bytes > cap) || bytes < 4)
@@ -1521,6 +1608,7 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
   const unsigned long long epoch = p2p_star ? ++c->epoch : 0;
   const int par = (int)(epoch & 1);
 
+  if (!p2p_star) TRY(need_comm(c, "this step"));
   // (1) error feedback on every worker; Top-k where its result is consumed
   record(c, 0);
   for (int i = 0; i < c->n_local; ++i) {
@@ -1726,6 +1814,7 @@ int fc_ag_step(fc_ctx* c, double cr, int compressor, fc_step_stats* st) {
   const uint64_t l0 = fcb::launches();
   c->phase_stats = st != nullptr;
 
+  if (!(c->p2p && compressor == FC_EXACT && N > 1)) TRY(need_comm(c, "this AG step"));
   // (1) error feedback + compression per worker (compress.hpp:114-130)
   // (the threshold select reads per-chunk candidate slots: unpacked layout)
   for (auto& w : c->w) w.ws.batch = compressor == FC_THRESHOLD ? 1u : fcb::ef_batch(c->nch, w.ws.ef_grid);
@@ -1886,6 +1975,7 @@ int fc_dense_step(fc_ctx* c, int algo, int op, fc_step_stats* st) {
   if (algo != FC_RING && algo != FC_TREE) return fail(FC_ERR_INVALID_ARGUMENT, "unknown reduce algo");
   if (op != FC_SUM && op != FC_AVG) return fail(FC_ERR_INVALID_ARGUMENT, "unknown reduce op");
   const int N = c->world;
+  TRY(need_comm(c, "the dense step"));
   CUDA_TRY(cudaSetDevice(c->device));
   const uint64_t l0 = fcb::launches();
   c->phase_stats = st != nullptr;

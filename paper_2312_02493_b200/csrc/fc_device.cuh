@@ -164,7 +164,8 @@ struct PeerBufs {
   float* inbox[kMaxPeers];               // rank r: N x 2 parities of contributions pushed to it
   unsigned* bounds[kMaxPeers];           // AG: the chunk bounds of rank r's list (2 parities)
   // rank r's mailbox, N x 8 words: box[r][src * 8 + slot] = the epoch src
-  // published for slot 0 (list), 1 (contribution), 2 (reduced slice); slot 4
+  // published for slot 0 (list), 1 (contribution), 2 (reduced slice), 3
+  // (two-stage broadcast: its list slice), 5 (teardown barrier); slot 4
   // holds src's ||top-k||^2 (double).  Producers store into every rank's box,
   // consumers poll their own (local) box.
   unsigned long long* box[kMaxPeers];
@@ -260,6 +261,7 @@ void launch_decode_ar_peers(const PeerBufs& pb, int par, unsigned long long epoc
 // `epoch` without a select; wait like the peer decode (root < 0: every rank);
 // a sorted spread index list standing in for a selection.
 void launch_publish(const PeerBufs& pb, unsigned long long epoch, unsigned mask, cudaStream_t s);
+void launch_peer_barrier(const PeerBufs& pb, cudaStream_t s);
 void launch_wait_slot(const PeerBufs& pb, int slot, unsigned long long epoch, int root, cudaStream_t s);
 void launch_spread_list(unsigned* out, uint64_t k, uint64_t G, uint64_t shift, cudaStream_t s);
 // select_var on the device: winner of the N scores into *sel_out, this rank's

@@ -2904,6 +2904,21 @@ __global__ void k_wait_slot(PeerBufs pb, int slot, unsigned long long epoch, int
     wait_from(pb, root, slot, epoch);
   }
 }
+// Cross-rank barrier through the mailboxes (slot 5; used once, at teardown
+// of a peer-only context): after it, no rank has an exchange kernel left.
+__global__ void k_peer_barrier(PeerBufs pb) {
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    publish_all(pb, 5, 1ull);
+  }
+  __syncthreads();
+  wait_all(pb, 5, 1ull);
+}
+void launch_peer_barrier(const PeerBufs& pb, cudaStream_t s) {
+  launch_pdl(k_peer_barrier, 1, 32, 0, s, pb);
+  count_launch();
+}
 void launch_publish(const PeerBufs& pb, unsigned long long epoch, unsigned mask, cudaStream_t s) {
   launch_pdl(k_publish, 1, 32, 0, s, pb, epoch, mask);
   count_launch();

@@ -138,7 +138,7 @@ class Cluster:
 
     def __init__(self, n: int, grad_len: int, device: int = 0, max_cr: float = 1.0,
                  flags: int = 0, *, _world: Optional[int] = None, _rank: int = 0,
-                 _uid: Optional[bytes] = None):
+                 _uid: Optional[bytes] = None, _peer_only: bool = False):
         opts = _abi.fc_opts()
         opts.device = device
         opts.n_local = n
@@ -160,6 +160,21 @@ class Cluster:
     def nccl(cls, world: int, rank: int, uid: bytes, grad_len: int, device: int = 0,
              max_cr: float = 1.0, flags: int = 0) -> "Cluster":
         return cls(1, grad_len, device, max_cr, flags, _world=world, _rank=rank, _uid=uid)
+
+    @classmethod
+    def peer_only(cls, world: int, rank: int, grad_len: int, allgather, device: int = 0,
+                  max_cr: float = 1.0, flags: int = 0) -> "Cluster":
+        """One worker per process over NVLink peer memory without NCCL
+        (FC_FLAG_PEER_ONLY; several ranks may share a GPU).  `allgather(bytes)`
+        returns every rank's bytes in rank order (e.g. over a gloo group)."""
+        cl = cls(1, grad_len, device, max_cr, flags | _abi.FC_FLAG_PEER_ONLY, _world=world, _rank=rank,
+                 _uid=None, _peer_only=True)
+        h = (C.c_ubyte * _abi.FC_PEER_HANDLE_BYTES)()
+        check(lib.fc_peer_handle(cl._ctx, h))
+        parts = allgather(bytes(h))
+        allh = (C.c_ubyte * (_abi.FC_PEER_HANDLE_BYTES * world)).from_buffer_copy(b"".join(parts))
+        check(lib.fc_peer_attach(cl._ctx, allh))
+        return cl
 
     # ---- lifetime ----------------------------------------------------------
     def close(self) -> None:

@@ -56,3 +56,20 @@ def test_peer_timeout_reported():
     """A rank that never joins a step: the peer's exchange wait times out
     (2 s), and the step call raises instead of hanging or returning stale data."""
     _run(2, "tests/mp_timeout.py", [], marker="MP_TIMEOUT PASS")
+
+
+@pytest.mark.parametrize("ranks_per_gpu", [1, 2])
+def test_peer_only_contexts(ranks_per_gpu):
+    """Peer-only contexts (no NCCL; handles over gloo).  Two ranks per GPU
+    make 8 ranks on a 4-GPU lease: the kMaxPeers = 8 protocol (and the
+    two-stage list broadcast, on from 5 ranks) bit-exact -- correctness only,
+    the ranks sharing a GPU are time-sliced."""
+    import torch
+
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs 2 GPUs")
+    nproc = min(8, n * ranks_per_gpu)
+    if ranks_per_gpu == 2 and nproc < 8:
+        pytest.skip("the 8-rank case needs 4 GPUs")
+    _run(nproc, "tests/mp_peer_only.py", ["50021"], marker="MP_PEER_ONLY PASS")
