@@ -63,7 +63,6 @@ struct Ctl {
   unsigned hist3[2048];      // bits 10..0
   unsigned hist_w[4096];     // window histogram: key bits 30..11 relative to Lkey (k_select)
   unsigned done_sel;         // k_select_x: last-block counter (finalisation)
-  unsigned hist_w_ready;     // the EF pass built hist_w while emitting (k_select_x skips its P1 histogram)
   unsigned done_slice;       // k_fetch_gather two-stage broadcast: slice pulled
   unsigned lb_flag[kMaxGrid];             // k_select_x look-back: block b's total is in
   unsigned long long lb_tot[kMaxGrid];    // ... (gt << 32) | eq of block b

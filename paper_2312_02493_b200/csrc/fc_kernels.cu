@@ -586,8 +586,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
     }
   }
 
-  const unsigned wb = Lkey >> 11;  // the window base of the select's histogram
-  if (sampling && blockIdx.x == 0 && tid == 0) ctl->hist_w_ready = 1u;
   for (unsigned it = 0;; ++it) {
     const unsigned c = s_chunk[warp][it % kEfStages];
     if (c >= nchunks) break;
@@ -687,10 +685,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
         w.cand_idx[pos] = (unsigned)(base + (uint64_t)lane * 32 + p);
         w.cand_val[pos] = x;
         ++pos;
-        // the select's window histogram (key bits 30..11 from the bound's
-        // prefix), built here by fire-and-forget reductions (RED: no result,
-        // no stall) so that k_select_x starts at the bin search
-        if (sampling) atomicAdd(&ctl->hist_w[min((key_of(x) >> 11) - wb, 4095u)], 1u);
       }
     }
     if (c < nfull) {
@@ -1569,7 +1563,6 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
     }
     if (blockIdx.x == 0) {
       for (uint64_t i = n4 * 4 + tid; i < G; i += kSxThreads) atomicAdd(&s_h[key_of(ef_out[i]) >> kShift1], 1u);
-      for (int q = tid; q < kSelBins; q += kSxThreads) ctl->hist_w[q] = 0u;  // (the EF's window counts are void)
     }
     flush_hist(s_h, ctl->hist_fb, kBins1);
     grid_barrier(&ctl->bar_sel, bar, w.err);
@@ -1718,15 +1711,9 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
   unsigned prefix = 0;
   bool windowed = false;
   const unsigned wb = Lb >> 11;
-  // the EF pass histogrammed the window while emitting (unless the fallback
-  // re-emitted the candidates): P1 is then a plain load/stage, no barrier
-  const bool ef_hist = !fb && __ldcg(&ctl->hist_w_ready) != 0u;
-  if (!ef_hist) {
-    for (int b = tid; b < kSelBins; b += kSxThreads) s_h[b] = 0;
-    __syncthreads();
-  }
+  for (int b = tid; b < kSelBins; b += kSxThreads) s_h[b] = 0;
+  __syncthreads();
   pass(U4{}, false, false, cached, [&](const float4& v, const uint4&, unsigned nv) {
-    if (ef_hist) return;
     for (unsigned e = 0; e < nv; ++e) {
       const unsigned hi = key_of(f4c(v, e)) >> 11;
       if (hi >= wb) atomicAdd(&s_h[min(hi - wb, (unsigned)kSelBins - 1u)], 1u);
@@ -1735,11 +1722,9 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
   SX_MARK(0);
   __syncthreads();
   if (tid == 0) reinterpret_cast<unsigned long long*>(w.g_part)[2048 + 2 * blockIdx.x] = gtimer();  // (diagnostics)
-  if (!ef_hist) {
-    flush_hist(s_h, ctl->hist_w, kSelBins);
-    SX_MARK(1);
-    grid_barrier(&ctl->bar_sel, bar, w.err);
-  }
+  flush_hist(s_h, ctl->hist_w, kSelBins);
+  SX_MARK(1);
+  grid_barrier(&ctl->bar_sel, bar, w.err);
   SEL_MARK(1);
   {
     unsigned bin;
