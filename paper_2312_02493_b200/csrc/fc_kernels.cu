@@ -349,10 +349,11 @@ void launch_fill_synth(float* dst, uint64_t G, uint64_t key, int dist, cudaStrea
 }
 
 // ------------------------------------------------------------------ sample ---
-// Candidate bound from a strided sample of 32768 error-fed magnitudes (fused
-// into the EF kernel, before it streams): the largest key bound L (12-bit
+// Candidate bound from a strided sample of kSamples error-fed magnitudes
+// (fused into the EF kernel, before it streams; every block loads the same
+// sample and derives the same bound): the largest key bound L (12-bit
 // bucket, then 8 more bits inside it) such that the sample holds at least
-// sample_target = 1.05*mean + 4*sqrt(mean) + 8 values >= L, mean = k/G * 32768.  The bound only decides how many elements EF copies
+// sample_target = 1.05*mean + 4*sqrt(mean) + 8 values >= L, mean = k/G * kSamples.  The bound only decides how many elements EF copies
 // out; exactness never depends on it (a miss triggers the fallback in k_select).
 __device__ __forceinline__ uint64_t sample_pos(uint64_t s, uint64_t G) {
   return ((2 * s + 1) * G) / (2ull * kSamples);
@@ -471,9 +472,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
     if (kAdd) v = __fadd_rn(g_o[i], v);
     return v;
   };
-  const unsigned q0 = blockIdx.x * kThreads + tid, qstride = gridDim.x * kThreads;
-  float sv = 0.f;
-  if (sampling && q0 < (unsigned)kSamples) sv = sample_at(q0);
+  // every block loads the SAME kSamples positions (L2-shared after the first
+  // touch) and derives the same bound locally: no grid barrier, no global
+  // histogram.  Thread t holds samples t, t + 256, ... in registers.
+  constexpr int kPer = kSamples / kThreads;
+  unsigned skey[kPer];
+  if (sampling) {
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) skey[j] = key_of(sample_at((unsigned)(tid + j * kThreads)));
+  }
 
   // Chunks are handed out dynamically: SMs do not stream at equal rates, and
   // a static split leaves a long tail.  Lane 0 takes a ticket (one atomic):
@@ -523,30 +530,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
   unsigned Lkey = 0u;
   if (kEmit) {
     if (opts & 1) {
-      // Level 1 (12-bit buckets): each block histograms its own samples and
-      // flushes them (one grid barrier).  Level 2 (the next 8 bits inside the
-      // target bucket) is local: every sampled key is also stored in the
-      // shared sample array, and each block re-reads all 32768 from L2 and
-      // histograms the few that fall in the bucket -- no second flush or
-      // barrier.
+      // Level 1: the 12-bit buckets of the block's copy of the sample; level
+      // 2: the next 8 bits of the keys inside the target bucket (held in
+      // registers, no reload).  Every block computes the same bound.
       for (int b = tid; b < kBins1; b += kThreads) s_hist[b] = 0u;
       __syncthreads();
-      if (q0 < (unsigned)kSamples) {
-        w.skeys[q0] = key_of(sv);
-        atomicAdd(&s_hist[key_of(sv) >> kShift1], 1u);
-      }
-      for (unsigned q = q0 + qstride; q < (unsigned)kSamples; q += qstride) {  // small grids only
-        const unsigned kq = key_of(sample_at(q));
-        w.skeys[q] = kq;
-        atomicAdd(&s_hist[kq >> kShift1], 1u);
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        const unsigned bin = skey[j] >> kShift1;
+        const unsigned peers = __match_any_sync(0xffffffffu, bin);  // warp-aggregated (hot buckets)
+        if ((peers & lanemask_lt()) == 0u) atomicAdd(&s_hist[bin], (unsigned)__popc(peers));
       }
       __syncthreads();
       if (blockIdx.x == 0 && threadIdx.x == 0) ctl->tphase_ef2[0] = gtimer();
-      for (int b = tid; b < kBins1; b += kThreads)
-        if (s_hist[b]) atomicAdd(&ctl->hist_s[b], s_hist[b]);
-      if (blockIdx.x == 0 && threadIdx.x == 0) ctl->tphase_ef2[1] = gtimer();
-      unsigned bar = 0;
-      grid_barrier(&ctl->bar_ef, bar, w.err);
       EF_MARK(1);
       const double target = sample_target(G, k);
       if (opts & 2) {
@@ -555,19 +551,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
         unsigned b1, b2;
         unsigned long long above1, above2;
         const unsigned long long tgt = (unsigned long long)target;
-        if (block_select_top<kThreads>(ctl->hist_s, kBins1, tgt, b1, above1, s_hist)) {
+        if (block_select_top<kThreads>(s_hist, kBins1, tgt, b1, above1, s_hist)) {
           for (int b = tid; b < 256; b += kThreads) s_hist[b] = 0u;
           __syncthreads();
-          const uint4* k4 = reinterpret_cast<const uint4*>(w.skeys);
-          constexpr int kQ = kSamples / 4 / kThreads;  // uint4 loads per thread
-#pragma unroll 8
-          for (int i = 0; i < kQ; ++i) {
-            const uint4 x = __ldcg(k4 + i * kThreads + tid);
-            const unsigned kk[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-            for (int e = 0; e < 4; ++e)
-              if ((kk[e] >> kShift1) == b1) atomicAdd(&s_hist[(kk[e] >> 11) & 255u], 1u);
-          }
+          for (int j = 0; j < kPer; ++j)
+            if ((skey[j] >> kShift1) == b1) atomicAdd(&s_hist[(skey[j] >> 11) & 255u], 1u);
+          if (blockIdx.x == 0 && threadIdx.x == 0) ctl->tphase_ef2[1] = gtimer();
           const bool f2 = block_select_top<kThreads>(s_hist, 256, tgt - above1, b2, above2, s_hist);
           Lkey = (b1 << kShift1) | ((f2 ? b2 : 0u) << 11);
         } else {
@@ -1545,9 +1535,20 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
   const unsigned cap = kSelSmemMax / 4 > tab_words ? kSelSmemMax / 4 - tab_words : 0u;
 
   // ---- fallback (the sampled bound kept fewer than k elements) ----
+  // the candidate count, the bound and this thread's segment totals are
+  // loaded together (one memory round trip; the totals are void -- and
+  // recounted -- only in the rare fallback)
   const unsigned long long M = __ldcg(&ctl->cand_count);
+  const unsigned Lk0 = __ldcg(&ctl->Lkey);
+  constexpr int kSegPre = 2;  // segments per thread whose totals are loaded up front
+  unsigned segpre[kSegPre];
+#pragma unroll
+  for (int q = 0; q < kSegPre; ++q) {
+    const unsigned j = tid + q * kSxThreads;
+    segpre[q] = j < S ? __ldcg(w.segcnt + lay.seg_id(seg_c0(j))) : 0u;
+  }
   const bool fb = M < k;
-  unsigned Lb = fb ? 0u : __ldcg(&ctl->Lkey);  // every candidate has key >= Lb
+  unsigned Lb = fb ? 0u : Lk0;  // every candidate has key >= Lb
   if (fb) {
     if (blockIdx.x == 0 && tid == 0) ctl->fallback = 1;
     for (int b = tid; b < kBins1; b += kSxThreads) s_h[b] = 0;
@@ -1604,7 +1605,8 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
   // ---- the block's position space ----
   for (unsigned j = tid; j < S; j += kSxThreads) {
     if (!fb) {  // the EF pass wrote every segment's total
-      s_sct[j] = __ldcg(w.segcnt + lay.seg_id(seg_c0(j)));
+      const unsigned q = (j - tid) / kSxThreads;
+      s_sct[j] = q < (unsigned)kSegPre ? segpre[q] : __ldcg(w.segcnt + lay.seg_id(seg_c0(j)));
       continue;
     }
     unsigned n = 0;

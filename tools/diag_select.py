@@ -22,7 +22,7 @@ with fc.Cluster(1, G, max_cr=max(cr, 0.1), flags=flags) as cl:
         print(f"step {s}: total {st.ms_total * 1e3:.0f}us ef {st.ms_ef * 1e3:.0f}us select {st.ms_select * 1e3:.0f}us "
               f"exch {st.ms_exchange * 1e3:.0f}us decode {st.ms_decode * 1e3:.0f}us cand {ws.candidates} "
               + " ".join(f"{n}={(t[i + 1] - t[i]) / 1e3:.1f}us" for i, n in enumerate(names))
-              + f" | EF: sample={(t[12] - t[8]) / 1e3:.1f}us flush={(t[13] - t[12]) / 1e3:.1f}us "
+              + f" | EF: preamble={(t[10] - t[8]) / 1e3:.1f}us sample+hist1={(t[12] - t[8]) / 1e3:.1f}us flush={(t[13] - t[12]) / 1e3:.1f}us "
               f"barrier={(t[9] - t[13]) / 1e3:.1f}us bound={(t[10] - t[9]) / 1e3:.1f}us "
               f"stream={(t[11] - t[10]) / 1e3:.1f}us EF-end->select-start={(t[0] - t[11]) / 1e3:.1f}us"
               + (f" | sx: p1pass={(t[16] - t[0]) / 1e3:.1f} flush={(t[17] - t[16]) / 1e3:.1f} "
