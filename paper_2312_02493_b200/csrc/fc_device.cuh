@@ -30,7 +30,7 @@ static_assert((1 << kDecShift) == kDecTile, "decode tile must be a power of two"
 // k_select over the candidates the error-feedback pass emits.
 constexpr int kShift1 = 19, kBins1 = 4096;    // bits 30..19 (exponent + 3 mantissa)
 
-constexpr int kSamples = 8192;                 // candidate-bound sample size (every EF block loads it)
+constexpr int kSamples = 32768;                // candidate-bound sample size
 constexpr int kMaxGrid = 256;                  // grid of the one-block-per-SM kernels (>= SM count)
 
 // Per-worker control block.  Each worker has two, used by alternate steps; the

@@ -349,11 +349,10 @@ void launch_fill_synth(float* dst, uint64_t G, uint64_t key, int dist, cudaStrea
 }
 
 // ------------------------------------------------------------------ sample ---
-// Candidate bound from a strided sample of kSamples error-fed magnitudes
-// (fused into the EF kernel, before it streams; every block loads the same
-// sample and derives the same bound): the largest key bound L (12-bit
+// Candidate bound from a strided sample of 32768 error-fed magnitudes (fused
+// into the EF kernel, before it streams): the largest key bound L (12-bit
 // bucket, then 8 more bits inside it) such that the sample holds at least
-// sample_target = 1.05*mean + 4*sqrt(mean) + 8 values >= L, mean = k/G * kSamples.  The bound only decides how many elements EF copies
+// sample_target = 1.05*mean + 4*sqrt(mean) + 8 values >= L, mean = k/G * 32768.  The bound only decides how many elements EF copies
 // out; exactness never depends on it (a miss triggers the fallback in k_select).
 __device__ __forceinline__ uint64_t sample_pos(uint64_t s, uint64_t G) {
   return ((2 * s + 1) * G) / (2ull * kSamples);
@@ -472,15 +471,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
     if (kAdd) v = __fadd_rn(g_o[i], v);
     return v;
   };
-  // every block loads the SAME kSamples positions (L2-shared after the first
-  // touch) and derives the same bound locally: no grid barrier, no global
-  // histogram.  Thread t holds samples t, t + 256, ... in registers.
-  constexpr int kPer = kSamples / kThreads;
-  unsigned skey[kPer];
-  if (sampling) {
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) skey[j] = key_of(sample_at((unsigned)(tid + j * kThreads)));
-  }
+  const unsigned q0 = blockIdx.x * kThreads + tid, qstride = gridDim.x * kThreads;
+  float sv = 0.f;
+  if (sampling && q0 < (unsigned)kSamples) sv = sample_at(q0);
 
   // Chunks are handed out dynamically: SMs do not stream at equal rates, and
   // a static split leaves a long tail.  Lane 0 takes a ticket (one atomic):
@@ -530,19 +523,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
   unsigned Lkey = 0u;
   if (kEmit) {
     if (opts & 1) {
-      // Level 1: the 12-bit buckets of the block's copy of the sample; level
-      // 2: the next 8 bits of the keys inside the target bucket (held in
-      // registers, no reload).  Every block computes the same bound.
+      // Level 1 (12-bit buckets): each block histograms its own samples and
+      // flushes them (one grid barrier).  Level 2 (the next 8 bits inside the
+      // target bucket) is local: every sampled key is also stored in the
+      // shared sample array, and each block re-reads all 32768 from L2 and
+      // histograms the few that fall in the bucket -- no second flush or
+      // barrier.
       for (int b = tid; b < kBins1; b += kThreads) s_hist[b] = 0u;
       __syncthreads();
-#pragma unroll
-      for (int j = 0; j < kPer; ++j) {
-        const unsigned bin = skey[j] >> kShift1;
-        const unsigned peers = __match_any_sync(0xffffffffu, bin);  // warp-aggregated (hot buckets)
-        if ((peers & lanemask_lt()) == 0u) atomicAdd(&s_hist[bin], (unsigned)__popc(peers));
+      if (q0 < (unsigned)kSamples) {
+        w.skeys[q0] = key_of(sv);
+        atomicAdd(&s_hist[key_of(sv) >> kShift1], 1u);
+      }
+      for (unsigned q = q0 + qstride; q < (unsigned)kSamples; q += qstride) {  // small grids only
+        const unsigned kq = key_of(sample_at(q));
+        w.skeys[q] = kq;
+        atomicAdd(&s_hist[kq >> kShift1], 1u);
       }
       __syncthreads();
       if (blockIdx.x == 0 && threadIdx.x == 0) ctl->tphase_ef2[0] = gtimer();
+      for (int b = tid; b < kBins1; b += kThreads)
+        if (s_hist[b]) atomicAdd(&ctl->hist_s[b], s_hist[b]);
+      if (blockIdx.x == 0 && threadIdx.x == 0) ctl->tphase_ef2[1] = gtimer();
+      unsigned bar = 0;
+      grid_barrier(&ctl->bar_ef, bar, w.err);
       EF_MARK(1);
       const double target = sample_target(G, k);
       if (opts & 2) {
@@ -551,13 +555,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
         unsigned b1, b2;
         unsigned long long above1, above2;
         const unsigned long long tgt = (unsigned long long)target;
-        if (block_select_top<kThreads>(s_hist, kBins1, tgt, b1, above1, s_hist)) {
+        if (block_select_top<kThreads>(ctl->hist_s, kBins1, tgt, b1, above1, s_hist)) {
           for (int b = tid; b < 256; b += kThreads) s_hist[b] = 0u;
           __syncthreads();
+          const uint4* k4 = reinterpret_cast<const uint4*>(w.skeys);
+          constexpr int kQ = kSamples / 4 / kThreads;  // uint4 loads per thread
+#pragma unroll 8
+          for (int i = 0; i < kQ; ++i) {
+            const uint4 x = __ldcg(k4 + i * kThreads + tid);
+            const unsigned kk[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-          for (int j = 0; j < kPer; ++j)
-            if ((skey[j] >> kShift1) == b1) atomicAdd(&s_hist[(skey[j] >> 11) & 255u], 1u);
-          if (blockIdx.x == 0 && threadIdx.x == 0) ctl->tphase_ef2[1] = gtimer();
+            for (int e = 0; e < 4; ++e)
+              if ((kk[e] >> kShift1) == b1) atomicAdd(&s_hist[(kk[e] >> 11) & 255u], 1u);
+          }
           const bool f2 = block_select_top<kThreads>(s_hist, 256, tgt - above1, b2, above2, s_hist);
           Lkey = (b1 << kShift1) | ((f2 ? b2 : 0u) << 11);
         } else {
@@ -2775,14 +2785,50 @@ __global__ void __launch_bounds__(kThreads) k_reduce_slice(PeerBufs pb, int par,
   const int n = pb.n, me = pb.rank;
   const uint64_t s0 = (k * me) / n, s1 = (k * (me + 1)) / n;
   const uint64_t off = (uint64_t)par * pb.kmax;
-  for (uint64_t j = s0 + blockIdx.x * (uint64_t)kThreads + threadIdx.x; j < s1; j += (uint64_t)gridDim.x * kThreads) {
-    float v = 0.f;  // v = c_0; v += c_r, r ascending
+  const uint64_t tid0 = blockIdx.x * (uint64_t)kThreads + threadIdx.x, nt = (uint64_t)gridDim.x * kThreads;
+  // v = c_0; v += c_r, r ascending (collectives.hpp:82-87).  The slice's
+  // 16-byte-aligned body moves as float4 (rows are 16-byte aligned at index
+  // 0), its head and tail (< 4 each) as scalars.
+  const uint64_t b0 = (s0 + 3) & ~3ull, b1 = s1 & ~3ull;
+  if (b0 < b1) {
+    for (uint64_t q = b0 / 4 + tid0; q < b1 / 4; q += nt) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int r = 0; r < n; ++r) {
+        const float4* src = reinterpret_cast<const float4*>(r == star_sel ? pb.contrib[r] + off : inbox_of(pb, me, r, par));
+        const float4 x = r == star_sel ? __ldcv(src + q) : __ldcg(src + q);
+        if (r == 0) {
+          v = x;
+        } else {
+          v.x = v.x + x.x;
+          v.y = v.y + x.y;
+          v.z = v.z + x.z;
+          v.w = v.w + x.w;
+        }
+      }
+      if (divide) {
+        v.x = v.x / divisor;
+        v.y = v.y / divisor;
+        v.z = v.z / divisor;
+        v.w = v.w / divisor;
+      }
+      for (int t = 0; t < n; ++t)  // push to every rank (own first)
+        __stcg(reinterpret_cast<float4*>(pb.reduced[(me + t) % n] + off) + q, v);
+    }
+  }
+  auto scalar = [&](uint64_t j) {
+    float v = 0.f;
     for (int r = 0; r < n; ++r) {
       const float x = r == star_sel ? __ldcv(pb.contrib[r] + off + j) : __ldcg(inbox_of(pb, me, r, par) + j);
       v = r == 0 ? x : v + x;
     }
     if (divide) v = v / divisor;
-    for (int t = 0; t < n; ++t) __stcg(pb.reduced[(me + t) % n] + off + j, v);  // push to every rank
+    for (int t = 0; t < n; ++t) __stcg(pb.reduced[(me + t) % n] + off + j, v);
+  };
+  if (b0 >= b1) {  // a slice shorter than one aligned quad
+    for (uint64_t j = s0 + tid0; j < s1; j += nt) scalar(j);
+  } else {
+    if (tid0 < b0 - s0) scalar(s0 + tid0);
+    if (tid0 < s1 - b1) scalar(b1 + tid0);
   }
   pdl_trigger();
   __syncthreads();
@@ -2797,7 +2843,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_slice(PeerBufs pb, int par,
 
 void launch_reduce_slice(const PeerBufs& pb, int par, unsigned long long epoch, uint64_t k, int divide,
                          float divisor, int star_sel, Ctl* ctl, cudaStream_t s) {
-  const uint64_t slice = k / pb.n + 1;
+  const uint64_t slice = (k / pb.n + 4) / 4;  // quads
   const unsigned g = (unsigned)std::min<uint64_t>(std::max<uint64_t>((slice + kThreads - 1) / kThreads, 1),
                                                   num_sms() * 4ull);
   launch_pdl(k_reduce_slice, g, kThreads, 0, s, pb, par, epoch, k, divide, divisor, star_sel, ctl);
