@@ -700,6 +700,8 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
     TRY(c->alloc(&s.g_part, 4096));
     TRY(c->alloc(&s.skeys, fcb::kSamples));
     TRY(c->alloc(&s.segcnt, nch + 1));
+    TRY(c->alloc(&s.lastb1, 1));
+    CUDA_TRY(cudaMemsetAsync(s.lastb1, 0, sizeof(unsigned), c->stream));
     TRY(c->alloc(&s.tblk, 2 * (uint64_t)ef_grid));
   }
   CUDA_TRY(cudaStreamSynchronize(c->stream));

@@ -31,6 +31,7 @@ static_assert((1 << kDecShift) == kDecTile, "decode tile must be a power of two"
 constexpr int kShift1 = 19, kBins1 = 4096;    // bits 30..19 (exponent + 3 mantissa)
 
 constexpr int kSamples = 32768;                // candidate-bound sample size
+constexpr int kSpecBins = 5;                   // speculative level-2 buckets (previous target bucket +- 2)
 constexpr int kMaxGrid = 256;                  // grid of the one-block-per-SM kernels (>= SM count)
 
 // Per-worker control block.  Each worker has two, used by alternate steps; the
@@ -57,6 +58,7 @@ struct Ctl {
   unsigned long long tphase_sx[8];   // k_select_x sub-phases (block 0; diagnostics)
   unsigned hist_s[kBins1];   // sample histogram (digit 1)
   unsigned hist_s2[256];     // sample histogram of bits 18..11 inside the bound's bucket
+  unsigned hist_s2w[kSpecBins * 256];  // the same, speculatively, for the buckets around the previous step's
   unsigned hist1[kBins1];    // candidate histogram, key bits 30..19 (k_select)
   unsigned hist_fb[kBins1];  // full histogram (fallback only)
   unsigned hist2[256];       // bits 18..11 of bucket-b1 candidates
@@ -83,6 +85,7 @@ struct ChunkWs {
   unsigned* err;              // the context's sticky error words (host-mapped; see kErr*)
   unsigned* skeys;            // kSamples sampled |g_e| keys (the EF pass's candidate bound)
   unsigned* segcnt;           // candidates per EF segment (EfLayout::seg_id), written by the EF pass
+  unsigned* lastb1;           // the previous sampled EF pass's target bucket + 1 (0: none)
   unsigned nchunks;
   unsigned ef_grid;
   unsigned coop;              // grid-barrier kernels launched cooperatively (default)

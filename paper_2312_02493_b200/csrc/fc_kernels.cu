@@ -446,6 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
   EF_MARK(0);
   if (threadIdx.x == 0) w.tblk[2 * blockIdx.x] = gtimer();
   __shared__ unsigned s_hist[kEmit ? kBins1 : 1];  // sample histogram, then the bound's staging
+  __shared__ unsigned s_sub[kEmit ? kSpecBins * 256 : 1];  // speculative level-2 histograms
   __shared__ __align__(8) unsigned long long s_bar[kEfWarps][kEfStages];
   __shared__ unsigned s_chunk[kEfWarps][kEfStages];  // chunk held by each stage
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -461,6 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
     for (unsigned q = blockIdx.x * kThreads + tid; q < sizeof(Ctl) / 4; q += gridDim.x * kThreads) z[q] = 0u;
   }
   const bool sampling = kEmit && (opts & 1);
+  const unsigned lastb1 = sampling ? __ldcg(w.lastb1) : 0u;  // previous step's target bucket + 1 (0: none)
   __syncthreads();
 
   // the sample's loads go out first, ahead of the stream's first stages
@@ -525,25 +527,38 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
     if (opts & 1) {
       // Level 1 (12-bit buckets): each block histograms its own samples and
       // flushes them (one grid barrier).  Level 2 (the next 8 bits inside the
-      // target bucket) is local: every sampled key is also stored in the
-      // shared sample array, and each block re-reads all 32768 from L2 and
-      // histograms the few that fall in the bucket -- no second flush or
-      // barrier.
+      // target bucket) is speculative: the 8-bit histograms of the buckets
+      // around the previous step's target bucket travel with the level-1
+      // flush, and when the new target bucket is among them no second pass
+      // is needed.  Otherwise every sampled key is also in the shared sample
+      // array: each block re-reads all 32768 from L2 and histograms the few
+      // in the bucket (no second flush or barrier either way).
+      const unsigned pb1 = lastb1 ? lastb1 - 1u : 0u;
+      const unsigned slo = pb1 > kSpecBins / 2 ? pb1 - kSpecBins / 2 : 0u;  // speculative buckets [slo, slo + kSpecBins)
       for (int b = tid; b < kBins1; b += kThreads) s_hist[b] = 0u;
+      for (int b = tid; b < kSpecBins * 256; b += kThreads) s_sub[b] = 0u;
       __syncthreads();
+      auto add_sample = [&](unsigned kq) {
+        atomicAdd(&s_hist[kq >> kShift1], 1u);
+        const unsigned d = (kq >> kShift1) - slo;
+        if (lastb1 && d < (unsigned)kSpecBins) atomicAdd(&s_sub[d * 256 + ((kq >> 11) & 255u)], 1u);
+      };
       if (q0 < (unsigned)kSamples) {
         w.skeys[q0] = key_of(sv);
-        atomicAdd(&s_hist[key_of(sv) >> kShift1], 1u);
+        add_sample(key_of(sv));
       }
       for (unsigned q = q0 + qstride; q < (unsigned)kSamples; q += qstride) {  // small grids only
         const unsigned kq = key_of(sample_at(q));
         w.skeys[q] = kq;
-        atomicAdd(&s_hist[kq >> kShift1], 1u);
+        add_sample(kq);
       }
       __syncthreads();
       if (blockIdx.x == 0 && threadIdx.x == 0) ctl->tphase_ef2[0] = gtimer();
       for (int b = tid; b < kBins1; b += kThreads)
         if (s_hist[b]) atomicAdd(&ctl->hist_s[b], s_hist[b]);
+      if (lastb1)
+        for (int b = tid; b < kSpecBins * 256; b += kThreads)
+          if (s_sub[b]) atomicAdd(&ctl->hist_s2w[b], s_sub[b]);
       if (blockIdx.x == 0 && threadIdx.x == 0) ctl->tphase_ef2[1] = gtimer();
       unsigned bar = 0;
       grid_barrier(&ctl->bar_ef, bar, w.err);
@@ -556,20 +571,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
         unsigned long long above1, above2;
         const unsigned long long tgt = (unsigned long long)target;
         if (block_select_top<kThreads>(ctl->hist_s, kBins1, tgt, b1, above1, s_hist)) {
-          for (int b = tid; b < 256; b += kThreads) s_hist[b] = 0u;
-          __syncthreads();
-          const uint4* k4 = reinterpret_cast<const uint4*>(w.skeys);
-          constexpr int kQ = kSamples / 4 / kThreads;  // uint4 loads per thread
+          bool f2;
+          if (lastb1 && b1 - slo < (unsigned)kSpecBins) {  // speculation hit: level 2 is in
+            f2 = block_select_top<kThreads>(ctl->hist_s2w + (b1 - slo) * 256, 256, tgt - above1, b2, above2, s_hist);
+          } else {
+            for (int b = tid; b < 256; b += kThreads) s_hist[b] = 0u;
+            __syncthreads();
+            const uint4* k4 = reinterpret_cast<const uint4*>(w.skeys);
+            constexpr int kQ = kSamples / 4 / kThreads;  // uint4 loads per thread
 #pragma unroll 8
-          for (int i = 0; i < kQ; ++i) {
-            const uint4 x = __ldcg(k4 + i * kThreads + tid);
-            const unsigned kk[4] = {x.x, x.y, x.z, x.w};
+            for (int i = 0; i < kQ; ++i) {
+              const uint4 x = __ldcg(k4 + i * kThreads + tid);
+              const unsigned kk[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-            for (int e = 0; e < 4; ++e)
-              if ((kk[e] >> kShift1) == b1) atomicAdd(&s_hist[(kk[e] >> 11) & 255u], 1u);
+              for (int e = 0; e < 4; ++e)
+                if ((kk[e] >> kShift1) == b1) atomicAdd(&s_hist[(kk[e] >> 11) & 255u], 1u);
+            }
+            f2 = block_select_top<kThreads>(s_hist, 256, tgt - above1, b2, above2, s_hist);
           }
-          const bool f2 = block_select_top<kThreads>(s_hist, 256, tgt - above1, b2, above2, s_hist);
           Lkey = (b1 << kShift1) | ((f2 ? b2 : 0u) << 11);
+          if (blockIdx.x == 0 && tid == 0) *w.lastb1 = b1 + 1u;  // (every block read it before the barrier)
         } else {
           Lkey = 0u;
         }
