@@ -52,6 +52,7 @@ def build(force: bool = False, verbose: bool = False, out: Path | None = None,
     if out is None and not force and not needs_build():
         return LIB
     out = out or LIB
+    tmp = out.with_name(out.name + ".tmp")  # built aside, then renamed: readers never see a partial file
     nr = nccl_root()
     libdir = nr / "lib"
     cmd = [
@@ -61,13 +62,14 @@ def build(force: bool = False, verbose: bool = False, out: Path | None = None,
         f"-I{ROOT / 'include'}", f"-I{nr / 'include'}",
         *[str(s) for s in SOURCES],
         f"-L{libdir}", "-l:libnccl.so.2", f"-Xlinker", f"-rpath={libdir}",
-        "-o", str(out),
+        "-o", str(tmp),
     ]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + res.stdout + res.stderr)
     if verbose:
         sys.stderr.write(res.stdout + res.stderr)
+    os.replace(tmp, out)
     return out
 
 
