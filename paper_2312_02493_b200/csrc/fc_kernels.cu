@@ -23,7 +23,6 @@
 // Everything is HBM-bound integer/fp32 streaming work: no tensor cores.
 // DESIGN.md §4 gives each kernel's algorithmic bytes and roofline.
 #include <atomic>
-#include <string>
 #include <type_traits>
 #include <cstdio>
 #include <cstdlib>
@@ -2638,11 +2637,7 @@ __device__ __forceinline__ void zero_tile(float* tile) {
 // rank's "contribution ready" epoch.
 // kPeers 0: local lists; 1: v = sum over every rank's contribution (peer
 // memory, rank order; 2 ranks); 2: v from the reduced slice's owner (N > 2).
-// kDirect: the tile's zeros go out as plain 16-byte stores straight from
-// registers (the lines stay in L2, where the values' 4-byte stores -- after a
-// block barrier -- merge into them), instead of a shared-memory tile written
-// by a TMA bulk store.
-template <int kPeers, bool kDirect = false>
+template <int kPeers>
 __global__ void __launch_bounds__(kThreads) k_decode_ar(const unsigned* __restrict__ idx,
                                                         const unsigned* __restrict__ bounds,
                                                         const float* __restrict__ lists,
@@ -2697,20 +2692,10 @@ __global__ void __launch_bounds__(kThreads) k_decode_ar(const unsigned* __restri
   int buf = 0, iter = 0;
   for (uint64_t t = blockIdx.x; t < ntd; t += gridDim.x, buf ^= 1, ++iter) {
     const uint64_t t0 = t << kDecShift;
-    if (!kDirect && iter >= 2 && threadIdx.x == 0) bulk_wait_read1();
+    if (iter >= 2 && threadIdx.x == 0) bulk_wait_read1();
     __syncthreads();
     float* tl = tile[buf];
-    if (kDirect) {
-      if (t0 + kDecTile <= G) {
-        float4* a4 = reinterpret_cast<float4*>(agg + t0);
-#pragma unroll
-        for (int q = 0; q < kDecTile / 4 / kThreads; ++q) a4[q * kThreads + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
-      } else {
-        for (uint64_t i = t0 + threadIdx.x; i < G; i += kThreads) agg[i] = 0.f;
-      }
-    } else {
-      zero_tile(tl);
-    }
+    zero_tile(tl);
     if (threadIdx.x < kDecChunks * 32) s_zm[threadIdx.x] = 0u;
     const uint64_t c0 = t * kDecChunks, c1 = min(c0 + kDecChunks, nch);
     const unsigned clo = lo, chi = hi, cpi = pi;
@@ -2730,38 +2715,24 @@ __global__ void __launch_bounds__(kThreads) k_decode_ar(const unsigned* __restri
       const bool pre = j == clo + threadIdx.x;
       const float v = pre ? cpv : value_at(j);
       const unsigned p = pre ? cpi : idx[j];
-      if (kDirect) agg[p] = v;  // after the barrier above: ordered after the zeros
-      else tl[p - (unsigned)t0] = v;
+      tl[p - (unsigned)t0] = v;
       atomicOr(&s_zm[zmap_word(p) - (unsigned)(c0 << 5)], zmap_bit(p));
     }
-    if (kDirect) __syncthreads();  // s_zm complete
-    else emit_tile(agg, tl, t0, G);
+    emit_tile(agg, tl, t0, G);
     if (threadIdx.x < (c1 - c0) * 32) zmap[(c0 << 5) + threadIdx.x] = s_zm[threadIdx.x];
   }
   pdl_trigger();
   if (threadIdx.x == 0) {
-    if (!kDirect) bulk_wait_all();
+    bulk_wait_all();
     atomicMax(&g_tdiag[1], gtimer());
   }
-}
-
-static bool decode_direct() {
-  static const bool d = [] {
-    const char* e = std::getenv("FC_DECODE");
-    return e && std::string(e) == "direct";
-  }();
-  return d;
 }
 
 void launch_decode_ar(const unsigned* idx, const unsigned* bounds, const float* lists, int nlists,
                       uint64_t list_stride, int divide, float divisor, float* agg, uint64_t G,
                       unsigned* zmap, cudaStream_t s) {
-  if (decode_direct())
-    launch_pdl(k_decode_ar<0, true>, num_sms() * 6, kThreads, 0, s, idx, bounds, lists, nlists, list_stride, divide,
-               divisor, agg, G, zmap, PeerBufs{}, 0, 0ull, -1, (const int*)nullptr);
-  else
-    launch_pdl(k_decode_ar<0>, num_sms() * 6, kThreads, 0, s, idx, bounds, lists, nlists, list_stride, divide,
-               divisor, agg, G, zmap, PeerBufs{}, 0, 0ull, -1, (const int*)nullptr);
+  launch_pdl(k_decode_ar<0>, num_sms() * 6, kThreads, 0, s, idx, bounds, lists, nlists, list_stride, divide,
+             divisor, agg, G, zmap, PeerBufs{}, 0, 0ull, -1, (const int*)nullptr);
   count_launch();
 }
 
@@ -2769,16 +2740,9 @@ void launch_decode_ar_peers(const PeerBufs& pb, int par, unsigned long long epoc
                             const unsigned* bounds, uint64_t k, int divide, float divisor, bool reduced,
                             float* agg, uint64_t G, unsigned* zmap, int wait_root, const int* dsel,
                             cudaStream_t s) {
-  const bool d = decode_direct();
-  if (reduced && d)
-    launch_pdl(k_decode_ar<2, true>, num_sms() * 6, kThreads, 0, s, idx, bounds, (const float*)nullptr, pb.n, k, 0,
-               1.0f, agg, G, zmap, pb, par, epoch, wait_root, dsel);
-  else if (reduced)
+  if (reduced)
     launch_pdl(k_decode_ar<2>, num_sms() * 6, kThreads, 0, s, idx, bounds, (const float*)nullptr, pb.n, k, 0,
                1.0f, agg, G, zmap, pb, par, epoch, wait_root, dsel);
-  else if (d)
-    launch_pdl(k_decode_ar<1, true>, num_sms() * 6, kThreads, 0, s, idx, bounds, (const float*)nullptr, pb.n, k,
-               divide, divisor, agg, G, zmap, pb, par, epoch, -1, (const int*)nullptr);
   else
     launch_pdl(k_decode_ar<1>, num_sms() * 6, kThreads, 0, s, idx, bounds, (const float*)nullptr, pb.n, k,
                divide, divisor, agg, G, zmap, pb, par, epoch, -1, (const int*)nullptr);
@@ -3234,8 +3198,7 @@ void launch_dense_sum(const float* lists, int nlists, uint64_t list_stride, int 
 static void prefer_max_smem() {
   const void* fs[] = {(const void*)k_fill_synth, (const void*)k_gather, (const void*)k_agg_clear,
                       (const void*)k_agg_write, (const void*)k_zero_at, (const void*)k_bounds,
-                      (const void*)k_decode_ar<0>, (const void*)k_decode_ar<1>, (const void*)k_decode_ar<2>,
-                      (const void*)k_decode_ar<0, true>, (const void*)k_decode_ar<1, true>, (const void*)k_decode_ar<2, true>, (const void*)k_decode_ag, (const void*)k_decode_ag_n<1>, (const void*)k_decode_ag_n<2>,
+                      (const void*)k_decode_ar<0>, (const void*)k_decode_ar<1>, (const void*)k_decode_ar<2>, (const void*)k_decode_ag, (const void*)k_decode_ag_n<1>, (const void*)k_decode_ag_n<2>,
                       (const void*)k_decode_ag_n<4>, (const void*)k_decode_ag_n<8>, (const void*)k_dense_sum,
                       (const void*)k_sum_fixed};
   for (const void* f : fs)
