@@ -169,9 +169,11 @@ class ClockSampler:
 
 def ef_traffic(G):
     """DRAM bytes per EF launch from the committed ncu --set full capture
-    (profiles/r01_ef_traffic.json), scaled to G if the capture's size differs;
+    (profiles/r02_ef_traffic.json, else round 1's), scaled to G if the capture's size differs;
     None when absent."""
-    p = ROOT / "profiles" / "r01_ef_traffic.json"
+    p = ROOT / "profiles" / "r02_ef_traffic.json"
+    if not p.exists():
+        p = ROOT / "profiles" / "r01_ef_traffic.json"
     try:
         d = json.loads(p.read_text())
         scale = G / 138_000_000

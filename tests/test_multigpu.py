@@ -59,6 +59,15 @@ def test_peer_timeout_reported():
     _run(2, "tests/mp_timeout.py", [], marker="MP_TIMEOUT PASS")
 
 
+@pytest.mark.parametrize("nproc,extra", [(2, {}), (3, {"FC_TWO_STAGE_MIN": "3"})], ids=["2ranks", "3ranks-two-stage"])
+def test_peer_exchange_on_one_gpu(nproc, extra):
+    """The cross-rank kernels (fetch-gather, reduce-slice / reduce-root, the
+    two-stage broadcast, collect-packs, the peer decodes) on a single GPU:
+    peer-only contexts let 2 or 3 ranks share device 0 (time-sliced), so a
+    one-GPU box runs the multi-rank protocol bit-exact against the oracle."""
+    _run(nproc, "tests/mp_peer_only.py", ["30011"], extra, marker="MP_PEER_ONLY PASS", min_gpus=1)
+
+
 @pytest.mark.parametrize("ranks_per_gpu", [1, 2])
 def test_peer_only_contexts(ranks_per_gpu):
     """Peer-only contexts (no NCCL; handles over gloo).  Two ranks per GPU
