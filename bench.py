@@ -432,7 +432,7 @@ def main():
                 ex_ms = max_over_ranks(out.value)
                 ex_bus = (world - 1) * 8.0 * k_ex if mode == 2 else 4.0 * k_ex + 2.0 * (world - 1) / world * 4.0 * k_ex
                 how = ("fc_diag_exchange_ms: the step's exchange kernels (" +
-                       ("list publish + k_collect_packs" if mode == 2 else
+                       ("list publish + k_collect_packs, the allgather the step fuses into its decode" if mode == 2 else
                         "list publish + k_fetch_gather + " + ("k_reduce_root" if algo == 1 else
                                                              ("k_reduce_slice" if world > 2 else "direct push")))
                        + ") back to back, max over ranks; peer memory" if cl.peer_exchange else

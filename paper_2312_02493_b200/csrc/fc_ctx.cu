@@ -1875,12 +1875,12 @@ int fc_ag_step(fc_ctx* c, double cr, int compressor, fc_step_stats* st) {
     kk = *std::max_element(kr.begin(), kr.end());
   }
   if (p2p_ag) {
-    fcb::launch_collect_packs(c->pb, par, epoch, kk, c->ag_recv, c->bounds, c->stream);
-    LAUNCHED();
-    packs = c->ag_recv;
-    stride = 2 * kk;
-    voff = kk;
-    local_bounds = true;  // collected with the lists
+    // the allgather is fused into the decode: it reads every rank's list,
+    // values and bounds where the selects published them (peer memory)
+    packs = c->pb.list[c->rank] + par * c->pb.kmax;  // (this rank's own list, for the owed zeros)
+    stride = 0;
+    voff = 0;
+    local_bounds = true;
   } else if (c->nccl && N == 1) {
     packs = c->w[0].pack;  // allgather over one rank: identity
     stride = 2 * c->kmax;
@@ -1919,8 +1919,11 @@ int fc_ag_step(fc_ctx* c, double cr, int compressor, fc_step_stats* st) {
   }
   int ob = 0;
   TRY(agg_target(c, &ob));
-  fcb::launch_decode_ag(packs, stride, voff, N, c->bounds, (float)N, c->agg_buf[ob], c->G, c->zmaps,
-                        c->nccl ? c->rank : 0, c->n_local, c->stream);
+  if (p2p_ag)
+    fcb::launch_decode_ag_peers(c->pb, par, epoch, kk, (float)N, c->agg_buf[ob], c->G, c->zmaps, c->stream);
+  else
+    fcb::launch_decode_ag(packs, stride, voff, N, c->bounds, (float)N, c->agg_buf[ob], c->G, c->zmaps,
+                          c->nccl ? c->rank : 0, c->n_local, c->stream);
   LAUNCHED();
   c->agg_incr = false;  // the aggregate's support is now a union of N lists
   record(c, 4);
@@ -1931,7 +1934,7 @@ int fc_ag_step(fc_ctx* c, double cr, int compressor, fc_step_stats* st) {
     const int r = c->nccl ? c->rank : i;
     Worker& w = c->w[i];
     w.pz.zmap = c->zmaps + (uint64_t)i * c->nch * 32;
-    w.pz_idx = packs + (uint64_t)r * stride;
+    w.pz_idx = p2p_ag ? packs : packs + (uint64_t)r * stride;
     w.pz_k = kr[r];
   }
 

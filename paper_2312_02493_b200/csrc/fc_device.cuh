@@ -290,6 +290,11 @@ void launch_decode_ar(const unsigned* idx, const unsigned* bounds, const float* 
 void launch_decode_ag(const unsigned* packs, uint64_t pack_stride, uint64_t k, int nranks,
                       const unsigned* bounds, float divisor, float* agg, uint64_t G,
                       unsigned* zmaps, int map_rank0, int nmaps, cudaStream_t s);
+// AG decode straight from peer memory (every rank's list, values and chunk
+// bounds where its select published them, parity par; waits for `epoch`):
+// the allgather fused into the decode.
+void launch_decode_ag_peers(const PeerBufs& pb, int par, unsigned long long epoch, uint64_t k, float divisor,
+                            float* agg, uint64_t G, unsigned* zmap, cudaStream_t s);
 void launch_dense_sum(const float* lists, int nlists, uint64_t list_stride, int divide,
                       float divisor, float* out, uint64_t G, cudaStream_t s);
 // topk_layerwise for the map's small layers in one launch (one block per

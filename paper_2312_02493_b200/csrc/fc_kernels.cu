@@ -3065,20 +3065,39 @@ __global__ void __launch_bounds__(kThreads) k_decode_ag(const unsigned* __restri
 // scatter starts, so a tile costs one dependent load round instead of two
 // per rank (the per-rank passes keep their barriers: the reference's
 // rank-ascending summation order, artopk.hpp:154-158).
-template <int NR>
+// kPeer (AG over peer memory): rank r's list, values and chunk bounds are
+// read where its select published them (pb, parity par) -- the peers' over
+// NVLink, prefetched a tile ahead like the local ones -- after every rank's
+// publish; no separate allgather copy.
+template <int NR, bool kPeer = false>
 __global__ void __launch_bounds__(kThreads) k_decode_ag_n(const unsigned* __restrict__ packs,
                                                           uint64_t pack_stride, uint64_t k, int nranks,
                                                           const unsigned* __restrict__ bounds,
                                                           float divisor, float* __restrict__ agg, uint64_t G,
-                                                          unsigned* __restrict__ zmaps, int map_rank0, int nmaps) {
+                                                          unsigned* __restrict__ zmaps, int map_rank0, int nmaps,
+                                                          PeerBufs pb, int par, unsigned long long epoch) {
   pdl_wait();
   __shared__ __align__(128) float tile[2][kDecTile];
   __shared__ unsigned s_touch[kDecTile / 32];
   extern __shared__ unsigned s_zm[];  // nmaps x kDecChunks*32
+  if (kPeer && !wait_all(pb, 0, epoch)) return;  // timeout reported
   const uint64_t ntd = (G + kDecTile - 1) >> kDecShift;
   const uint64_t nch = nchunks_of(G);
   const int zw = kDecChunks * 32;
   const bool divide = divisor != 1.0f;
+  const uint64_t poff = kPeer ? (uint64_t)par * pb.kmax : 0;
+  auto idp = [&](int r) -> const unsigned* {
+    return kPeer ? pb.list[r] + poff : packs + (uint64_t)r * pack_stride;
+  };
+  auto vap = [&](int r) -> const float* {
+    return kPeer ? pb.contrib[r] + poff : reinterpret_cast<const float*>(packs + (uint64_t)r * pack_stride + k);
+  };
+  auto bdp = [&](int r) -> const unsigned* {
+    return kPeer ? pb.bounds[r] + (uint64_t)par * pb.nbs : bounds + (uint64_t)r * (nch + 1);
+  };
+  // remote rows: volatile loads over NVLink (after the acquire of the publish)
+  auto ldu = [&](const unsigned* q, int r) -> unsigned { return kPeer && r != pb.rank ? __ldcv(q) : __ldg(q); };
+  auto ldf = [&](const float* q, int r) -> float { return kPeer && r != pb.rank ? __ldcv(q) : __ldg(q); };
   unsigned nlo[NR], nhi[NR];
   auto load_bounds = [&](uint64_t t) {
     const uint64_t c0 = t * kDecChunks, c1 = min(c0 + kDecChunks, nch);
@@ -3086,9 +3105,9 @@ __global__ void __launch_bounds__(kThreads) k_decode_ag_n(const unsigned* __rest
     for (int r = 0; r < NR; ++r) {
       nlo[r] = nhi[r] = 0;
       if (r < nranks) {
-        const unsigned* bd = bounds + (uint64_t)r * (nch + 1);
-        nlo[r] = __ldg(bd + c0);
-        nhi[r] = __ldg(bd + c1);
+        const unsigned* bd = bdp(r);
+        nlo[r] = ldu(bd + c0, r);
+        nhi[r] = ldu(bd + c1, r);
       }
     }
   };
@@ -3106,9 +3125,8 @@ __global__ void __launch_bounds__(kThreads) k_decode_ag_n(const unsigned* __rest
       v0[r] = 0.f;
       const unsigned j = lo[r] + threadIdx.x;
       if (r < nranks && j < hi[r]) {
-        const unsigned* id = packs + (uint64_t)r * pack_stride;
-        p0[r] = id[j];
-        v0[r] = reinterpret_cast<const float*>(id + k)[j];
+        p0[r] = ldu(idp(r) + j, r);
+        v0[r] = ldf(vap(r) + j, r);
       }
     }
     if (t + gridDim.x < ntd) load_bounds(t + gridDim.x);
@@ -3123,15 +3141,15 @@ __global__ void __launch_bounds__(kThreads) k_decode_ag_n(const unsigned* __rest
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
       if (r < nranks) {
-        const unsigned* id = packs + (uint64_t)r * pack_stride;
-        const float* va = reinterpret_cast<const float*>(id + k);
+        const unsigned* id = idp(r);
+        const float* va = vap(r);
         const int m = r - map_rank0;
         const bool mapped = m >= 0 && m < nmaps;
         for (unsigned j = lo[r] + threadIdx.x; j < hi[r]; j += kThreads) {
           const bool first = j == lo[r] + threadIdx.x;
-          const unsigned p = first ? p0[r] : id[j];
+          const unsigned p = first ? p0[r] : ldu(id + j, r);
           const unsigned lp = p - (unsigned)t0;
-          tl[lp] += first ? v0[r] : va[j];
+          tl[lp] += first ? v0[r] : ldf(va + j, r);
           if (divide) atomicOr(&s_touch[lp >> 5], 1u << (lp & 31));
           if (mapped) atomicOr(&s_zm[m * zw + zmap_word(p) - (unsigned)(c0 << 5)], zmap_bit(p));
         }
@@ -3162,13 +3180,30 @@ void launch_decode_ag(const unsigned* packs, uint64_t pack_stride, uint64_t k, i
   auto go = [&](auto kern) {
     if (smem > 16 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     launch_pdl(kern, num_sms() * 6, kThreads, smem, s, packs, pack_stride, k, nranks, bounds, divisor, agg, G,
-               zmaps, map_rank0, nmaps);
+               zmaps, map_rank0, nmaps, PeerBufs{}, 0, 0ull);
   };
   if (nranks <= 1) go(k_decode_ag_n<1>);
   else if (nranks <= 2) go(k_decode_ag_n<2>);
   else if (nranks <= 4) go(k_decode_ag_n<4>);
   else if (nranks <= 8) go(k_decode_ag_n<8>);
-  else go(k_decode_ag);
+  else {
+    if (smem > 16 * 1024) cudaFuncSetAttribute(k_decode_ag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    launch_pdl(k_decode_ag, num_sms() * 6, kThreads, smem, s, packs, pack_stride, k, nranks, bounds, divisor, agg,
+               G, zmaps, map_rank0, nmaps);
+  }
+  count_launch();
+}
+
+void launch_decode_ag_peers(const PeerBufs& pb, int par, unsigned long long epoch, uint64_t k, float divisor,
+                            float* agg, uint64_t G, unsigned* zmap, cudaStream_t s) {
+  const size_t smem = (size_t)kDecChunks * 32 * sizeof(unsigned);
+  auto go = [&](auto kern) {
+    launch_pdl(kern, num_sms() * 6, kThreads, smem, s, (const unsigned*)nullptr, (uint64_t)0, k, pb.n,
+               (const unsigned*)nullptr, divisor, agg, G, zmap, pb.rank, 1, pb, par, epoch);
+  };
+  if (pb.n <= 2) go(k_decode_ag_n<2, true>);
+  else if (pb.n <= 4) go(k_decode_ag_n<4, true>);
+  else go(k_decode_ag_n<8, true>);
   count_launch();
 }
 
@@ -3199,7 +3234,8 @@ static void prefer_max_smem() {
   const void* fs[] = {(const void*)k_fill_synth, (const void*)k_gather, (const void*)k_agg_clear,
                       (const void*)k_agg_write, (const void*)k_zero_at, (const void*)k_bounds,
                       (const void*)k_decode_ar<0>, (const void*)k_decode_ar<1>, (const void*)k_decode_ar<2>, (const void*)k_decode_ag, (const void*)k_decode_ag_n<1>, (const void*)k_decode_ag_n<2>,
-                      (const void*)k_decode_ag_n<4>, (const void*)k_decode_ag_n<8>, (const void*)k_dense_sum,
+                      (const void*)k_decode_ag_n<4>, (const void*)k_decode_ag_n<8>, (const void*)k_decode_ag_n<2, true>,
+                      (const void*)k_decode_ag_n<4, true>, (const void*)k_decode_ag_n<8, true>, (const void*)k_dense_sum,
                       (const void*)k_sum_fixed};
   for (const void* f : fs)
     cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
