@@ -1,0 +1,20 @@
+export OMP_NUM_THREADS=1
+TR="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1"
+# bench lines at N=2 and N=4 (peer memory), and the NCCL-only path for comparison
+for N in 2 4; do
+  for cfg in "star ring" "star tree" "var ring" "ag ring" "dense ring"; do
+    set -- $cfg
+    timeout 300 $TR --nproc-per-node $N --master-port 2995$N bench.py --gpus $N --mode $1 --algo $2 --no-e2e \
+      > gpurun_out/r2f_bench_n${N}_$1_$2.json 2> gpurun_out/r2f_bench_n${N}_$1_$2.err
+  done
+  for cfg in "star ring" "ag ring"; do
+    set -- $cfg
+    FC_NO_P2P=1 timeout 300 $TR --nproc-per-node $N --master-port 2996$N bench.py --gpus $N --mode $1 --algo $2 --no-e2e \
+      > gpurun_out/r2f_bench_n${N}_$1_$2_nccl.json 2> gpurun_out/r2f_bench_n${N}_$1_$2_nccl.err
+  done
+done
+timeout 300 $TR --nproc-per-node 4 --master-port 29971 bench.py --gpus 4 --steps 20 --warmup 5 \
+  > gpurun_out/r2f_bench_n4_star_e2e.json 2> gpurun_out/r2f_bench_n4_star_e2e.err
+timeout 900 $TR --nproc-per-node 4 --master-port 29972 tools/c4_sweep.py gpurun_out/r2f_c4_sweep_n4.jsonl > gpurun_out/r2f_c4_sweep_n4.log 2>&1
+timeout 900 $TR --nproc-per-node 4 --master-port 29973 tools/moo_run.py --grad-len 1000000000 --steps 100 --out gpurun_out/r2f_moo_c5_n4_star.json > gpurun_out/r2f_moo_c5_n4.log 2>&1
+timeout 1500 python -m pytest tests/test_multigpu.py -x -q > gpurun_out/r2f_pytest_mg.log 2>&1; echo rc=$? >> gpurun_out/r2f_pytest_mg.log
