@@ -424,40 +424,6 @@ __device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, unsigned 
                "r"(smem_u32(ssrc)), "r"(bytes)
                : "memory");
 }
-// L2 eviction-priority policies (createpolicy): the EF pass streams 1.6 GB
-// through the 126 MB L2 with evict_first, and writes the candidate runs --
-// read by the select right after -- with evict_last, so they are still in
-// L2 when the select starts.
-__device__ __forceinline__ unsigned long long policy_evict_first() {
-  unsigned long long p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ unsigned long long policy_evict_last() {
-  unsigned long long p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
-                                              unsigned long long pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_s2g_hint(void* gdst, const void* ssrc, unsigned bytes, unsigned long long pol) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;\n\t"
-               "cp.async.bulk.commit_group;" ::"l"(gdst),
-               "r"(smem_u32(ssrc)), "r"(bytes), "l"(pol)
-               : "memory");
-}
-__device__ __forceinline__ void st_hint(unsigned* p, unsigned v, unsigned long long pol) {
-  asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void st_hint(float* p, float v, unsigned long long pol) {
-  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
-}
 __device__ __forceinline__ void bulk_wait_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
@@ -496,9 +462,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
     for (unsigned q = blockIdx.x * kThreads + tid; q < sizeof(Ctl) / 4; q += gridDim.x * kThreads) z[q] = 0u;
   }
   const bool sampling = kEmit && (opts & 1);
-  const bool l2hint = (opts & 8) != 0;  // L2 eviction policies (see policy_evict_first)
-  const unsigned long long pol_first = l2hint ? policy_evict_first() : 0ull;
-  const unsigned long long pol_last = l2hint ? policy_evict_last() : 0ull;
   const unsigned lastb1 = sampling ? __ldcg(w.lastb1) : 0u;  // previous step's target bucket + 1 (0: none)
   __syncthreads();
 
@@ -549,15 +512,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
     unsigned char* st = ring + s * kStageBytes;
     const uint64_t base = (uint64_t)c << kChunkShift;
     mbar_expect_tx(bar, kTx);
-    if (l2hint) {
-      bulk_g2s_hint(st, ge + base, kChunk * 4, bar, pol_first);
-      if (kAdd) bulk_g2s_hint(st + kChunk * 4, g_o + base, kChunk * 4, bar, pol_first);
-      if (kPend) bulk_g2s_hint(st + 2 * kChunk * 4, pz.zmap + ((uint64_t)c << 5), 128, bar, pol_first);
-    } else {
-      bulk_g2s(st, ge + base, kChunk * 4, bar);
-      if (kAdd) bulk_g2s(st + kChunk * 4, g_o + base, kChunk * 4, bar);
-      if (kPend) bulk_g2s(st + 2 * kChunk * 4, pz.zmap + ((uint64_t)c << 5), 128, bar);
-    }
+    bulk_g2s(st, ge + base, kChunk * 4, bar);
+    if (kAdd) bulk_g2s(st + kChunk * 4, g_o + base, kChunk * 4, bar);
+    if (kPend) bulk_g2s(st + 2 * kChunk * 4, pz.zmap + ((uint64_t)c << 5), 128, bar);
   };
   if (lane == 0)
     for (int s = 0; s < kEfStages; ++s) issue(s);
@@ -696,10 +653,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
       if (kAdd) {
         fence_proxy_async();  // the stage's generic writes -> async-proxy reads
         __syncwarp();
-        if (lane == 0) {
-          if (l2hint) bulk_s2g_hint(ge + base, sge, kChunk * 4, pol_first);
-          else bulk_s2g(ge + base, sge, kChunk * 4);
-        }
+        if (lane == 0) bulk_s2g(ge + base, sge, kChunk * 4);
       }
     } else {
       // the one partial chunk at the end of the gradient: plain loads/stores
@@ -749,13 +703,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
       for (unsigned m = mask; m; m &= m - 1) {
         const int p = __ffs(m) - 1;
         const float x = my[p];
-        if (l2hint) {
-          st_hint(w.cand_idx + pos, (unsigned)(base + (uint64_t)lane * 32 + p), pol_last);
-          st_hint(w.cand_val + pos, x, pol_last);
-        } else {
-          w.cand_idx[pos] = (unsigned)(base + (uint64_t)lane * 32 + p);
-          w.cand_val[pos] = x;
-        }
+        w.cand_idx[pos] = (unsigned)(base + (uint64_t)lane * 32 + p);
+        w.cand_val[pos] = x;
         ++pos;
       }
     }
@@ -796,11 +745,6 @@ int ef_grid_size() { return num_sms(); }
 
 int launch_ef(const float* g_o, float* ge, uint64_t G, uint64_t k, Ctl* ctl, const ChunkWs& w,
               Pending pz, int add, int emit, int opts, Ctl* ctl_next, cudaStream_t s) {
-  static const bool hint = [] {
-    const char* e = std::getenv("FC_L2HINT");
-    return !(e && e[0] == '0');
-  }();
-  if (hint) opts |= 8;
   const bool pend = pz.zmap != nullptr;
   int e;
   if (add && emit && pend)
