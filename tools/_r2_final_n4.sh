@@ -18,3 +18,5 @@ timeout 300 $TR --nproc-per-node 4 --master-port 29971 bench.py --gpus 4 --steps
 timeout 900 $TR --nproc-per-node 4 --master-port 29972 tools/c4_sweep.py gpurun_out/r2f_c4_sweep_n4.jsonl > gpurun_out/r2f_c4_sweep_n4.log 2>&1
 timeout 900 $TR --nproc-per-node 4 --master-port 29973 tools/moo_run.py --grad-len 1000000000 --steps 100 --out gpurun_out/r2f_moo_c5_n4_star.json > gpurun_out/r2f_moo_c5_n4.log 2>&1
 timeout 1500 python -m pytest tests/test_multigpu.py -x -q > gpurun_out/r2f_pytest_mg.log 2>&1; echo rc=$? >> gpurun_out/r2f_pytest_mg.log
+timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29981 tools/calibrate_peer.py gpurun_out/calf > gpurun_out/r2f_cal_n4.log 2>&1
+timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29982 tools/calibrate_peer.py gpurun_out/calf > gpurun_out/r2f_cal_n2.log 2>&1
