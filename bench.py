@@ -376,6 +376,7 @@ def main():
     ms_local = ev0.elapsed_time(ev1) / a.steps
     launches = fc.lib.fc_launch_count() - l0
     ef_ms, ef_n = cl.ef_kernel_timing()
+    in_place = mode in (0, 1) and cl.aggregate_in_place
     # the timed region is short (K steps of well under a millisecond): keep the
     # same load running ~1.5 s longer so nvidia-smi samples the clocks under it
     # (same step count on every rank; not part of the timed number)
@@ -432,7 +433,7 @@ def main():
                 ex_ms = max_over_ranks(out.value)
                 ex_bus = (world - 1) * 8.0 * k_ex if mode == 2 else 4.0 * k_ex + 2.0 * (world - 1) / world * 4.0 * k_ex
                 how = ("fc_diag_exchange_ms: the step's exchange kernels (" +
-                       ("list publish + k_collect_packs, the allgather the step fuses into its decode" if mode == 2 else
+                       ("list publish + k_collect_packs" if mode == 2 else
                         "list publish + k_fetch_gather + " + ("k_reduce_root" if algo == 1 else
                                                              ("k_reduce_slice" if world > 2 else "direct push")))
                        + ") back to back, max over ranks; peer memory" if cl.peer_exchange else
@@ -492,7 +493,10 @@ def main():
     achieved = ef_bytes / (ef_ms * 1e-3) / 1e9 if ef_ms > 0 else None
     k = fc.k_of(a.cr, G) if mode != 3 else G
     if mode in (0, 1):
-        step_bytes = 16.0 * G + 32.0 * k + (8.0 * world if mode == 1 else 0.0)
+        # dense aggregate: 4G written; in place: <= 2 x 32-byte sectors per
+        # index (the previous support cleared, this one written) + the lists
+        agg_bytes = 80.0 * k if in_place else 4.0 * G
+        step_bytes = 12.0 * G + agg_bytes + 32.0 * k + (8.0 * world if mode == 1 else 0.0)
         bus = 4.0 * k + 2.0 * (world - 1) / world * 4.0 * k if world > 1 else 0.0
     elif mode == 2:
         step_bytes = 16.0 * G + 8.0 * k + 12.0 * world * k
@@ -525,6 +529,9 @@ def main():
             "hbm_gbs_step": round(step_gbs, 1),
             "bus_gbs_step": round(bus / (ms * 1e-3) / 1e9, 2) if bus else 0.0,
             "exchange": exchange,
+            "aggregate": ("in place: the previous support's 32-byte sectors zeroed, this step's rewritten "
+                          "(same dense content; FC_FLAG_DENSE_DECODE / FC_INCR_DIV=0 rewrite it whole)"
+                          if in_place else "dense rewrite (4G bytes)") if mode in (0, 1) else None,
             "bus_peak_gbs": 900.0,
             "roofline": {"kernel": "k_ef (error feedback + candidate emission)", "bound": "hbm",
                          "achieved": round(achieved, 1) if achieved else None, "peak": peak,
@@ -535,7 +542,7 @@ def main():
                          "peak_source": peak_src},
             "step_roofline": {"alg_bytes": step_bytes, "achieved_gbs": round(step_gbs, 1),
                               "frac": round(step_gbs / peak, 4),
-                              "lower_bound_ms": round(16.0 * G / peak / 1e6, 4)},
+                              "lower_bound_ms": round(step_bytes / peak / 1e6, 4)},
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clk,

@@ -322,6 +322,13 @@ int fc_moo_metrics(fc_ctx* ctx, int ag, const fc_step_stats* stats, double* gain
  * reference), 0 if they use NCCL collectives (FC_NO_P2P=1 in the environment
  * forces that). */
 int fc_peer_exchange(fc_ctx* ctx, int* enabled);
+
+/* *in_place = 1 if the last AR-Top-k step left the aggregate as an in-place
+ * update (the previous support's sectors zeroed, this step's sectors
+ * rewritten: identical content, k <= G / 32 without FC_FLAG_DENSE_DECODE /
+ * FC_FLAG_PIPELINE, single-process or NCCL exchange), 0 if it was rewritten
+ * whole. */
+int fc_aggregate_in_place(fc_ctx* ctx, int* in_place);
 /* FC_FLAG_PEER_ONLY contexts: this rank's exchange-buffer handle, and the
  * attachment of every rank's (world x FC_PEER_HANDLE_BYTES, rank order,
  * allgathered by the caller -- e.g. over a torch.distributed gloo group).

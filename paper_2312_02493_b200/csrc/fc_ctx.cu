@@ -129,6 +129,7 @@ struct fc_ctx {
   unsigned* agg_support = nullptr;  // indices of agg's nonzero support (incremental decode)
   uint64_t agg_support_k = 0;
   bool agg_incr = false;            // agg == densify(agg_support) and zmap 0 == its bits
+  uint64_t incr_div = 32;           // in-place update when k <= G / incr_div (FC_INCR_DIV overrides)
   // compressors of the AG path (inc/artopk.hpp:113-123)
   std::vector<uint64_t> layer_off, layer_len;  // layer map (Layerwise), sorted, disjoint
   int thresh_rounds = 25;                      // Threshold bisection rounds
@@ -658,6 +659,7 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
   // zero agg == densify(empty support); pipelined contexts always decode densely
   c->agg_incr = !(o->flags & (FC_FLAG_DENSE_DECODE | FC_FLAG_PIPELINE));
   c->agg_support_k = 0;
+  if (const char* e = std::getenv("FC_INCR_DIV")) c->incr_div = std::strtoull(e, nullptr, 10);
   if (c->nccl) {
     TRY(c->alloc(&c->reduced, c->kmax));
     TRY(c->alloc(&c->bidx, c->kmax));
@@ -1251,6 +1253,12 @@ int fc_peer_exchange(fc_ctx* c, int* enabled) {
   return FC_OK;
 }
 
+int fc_aggregate_in_place(fc_ctx* c, int* in_place) {
+  if (!c || !in_place) return fail(FC_ERR_INVALID_ARGUMENT, "null argument");
+  *in_place = c->agg_incr ? 1 : 0;
+  return FC_OK;
+}
+
 int fc_moo_metrics(fc_ctx* c, int ag, const fc_step_stats* st, double* gain, double* t_comp_s) {
   if (!c || !st || !gain || !t_comp_s) return fail(FC_ERR_INVALID_ARGUMENT, "null argument");
   TRY(need_comm(c, "fc_moo_metrics"));
@@ -1739,8 +1747,10 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
   const float* lists = (c->nccl || N == 1) ? (N == 1 ? contrib0 : c->reduced) : c->contrib_all;
   const int nlists = c->nccl ? 1 : N;
   const uint64_t lstride = c->nccl ? 0 : c->kmax;
-  // in-place update costs ~2k random sector RMWs: worth it below ~G/128
-  const bool incr_ok = !(c->flags & FC_FLAG_DENSE_DECODE) && c->nbuf == 1 && !p2p_star && k * 128 <= c->G;
+  // in-place update: ~2k whole-sector writes (32 B each, scattered) against
+  // the 4G-byte dense write; measured break-even sets incr_div
+  const bool incr_ok = !(c->flags & FC_FLAG_DENSE_DECODE) && c->nbuf == 1 && !p2p_star && c->incr_div &&
+                       k * c->incr_div <= c->G;
   int ob = 0;
   TRY(agg_target(c, &ob));
   float* aggw = c->agg_buf[ob];
@@ -1765,7 +1775,7 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
   } else if (incr_ok && c->agg_incr) {
     // in place: zero the previous support, write this one (same dense content)
     fcb::launch_agg_update(c->agg_support, c->agg_support_k, bsrc, k, lists, nlists, lstride,
-                           op == FC_AVG, (float)N, aggw, c->zmaps, c->agg_support, c->stream);
+                           op == FC_AVG, (float)N, aggw, c->G, c->zmaps, c->agg_support, c->stream);
   } else {
     if (!own_bounds) {
       fcb::launch_bounds(bsrc, k, 0, 1, c->G, c->bounds, c->stream);
@@ -1875,12 +1885,12 @@ int fc_ag_step(fc_ctx* c, double cr, int compressor, fc_step_stats* st) {
     kk = *std::max_element(kr.begin(), kr.end());
   }
   if (p2p_ag) {
-    // the allgather is fused into the decode: it reads every rank's list,
-    // values and bounds where the selects published them (peer memory)
-    packs = c->pb.list[c->rank] + par * c->pb.kmax;  // (this rank's own list, for the owed zeros)
-    stride = 0;
-    voff = 0;
-    local_bounds = true;
+    fcb::launch_collect_packs(c->pb, par, epoch, kk, c->ag_recv, c->bounds, c->stream);
+    LAUNCHED();
+    packs = c->ag_recv;
+    stride = 2 * kk;
+    voff = kk;
+    local_bounds = true;  // collected with the lists
   } else if (c->nccl && N == 1) {
     packs = c->w[0].pack;  // allgather over one rank: identity
     stride = 2 * c->kmax;
@@ -1919,11 +1929,8 @@ int fc_ag_step(fc_ctx* c, double cr, int compressor, fc_step_stats* st) {
   }
   int ob = 0;
   TRY(agg_target(c, &ob));
-  if (p2p_ag)
-    fcb::launch_decode_ag_peers(c->pb, par, epoch, kk, (float)N, c->agg_buf[ob], c->G, c->zmaps, c->stream);
-  else
-    fcb::launch_decode_ag(packs, stride, voff, N, c->bounds, (float)N, c->agg_buf[ob], c->G, c->zmaps,
-                          c->nccl ? c->rank : 0, c->n_local, c->stream);
+  fcb::launch_decode_ag(packs, stride, voff, N, c->bounds, (float)N, c->agg_buf[ob], c->G, c->zmaps,
+                        c->nccl ? c->rank : 0, c->n_local, c->stream);
   LAUNCHED();
   c->agg_incr = false;  // the aggregate's support is now a union of N lists
   record(c, 4);
@@ -1934,7 +1941,7 @@ int fc_ag_step(fc_ctx* c, double cr, int compressor, fc_step_stats* st) {
     const int r = c->nccl ? c->rank : i;
     Worker& w = c->w[i];
     w.pz.zmap = c->zmaps + (uint64_t)i * c->nch * 32;
-    w.pz_idx = p2p_ag ? packs : packs + (uint64_t)r * stride;
+    w.pz_idx = packs + (uint64_t)r * stride;
     w.pz_k = kr[r];
   }
 

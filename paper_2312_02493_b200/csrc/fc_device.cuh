@@ -281,7 +281,8 @@ void launch_zero_at(const unsigned* idx, uint64_t k, float* ge, cudaStream_t s);
 // keep the new support in `keep` (may alias prev); owed-zero bits follow.
 void launch_agg_update(const unsigned* prev, uint64_t kp, const unsigned* idx, uint64_t k,
                        const float* lists, int nlists, uint64_t list_stride, int divide,
-                       float divisor, float* agg, unsigned* zmap, unsigned* keep, cudaStream_t s);
+                       float divisor, float* agg, uint64_t G, unsigned* zmap, unsigned* keep,
+                       cudaStream_t s);
 // Decodes also write the zero map(s) of the decoded index list(s).
 void launch_decode_ar(const unsigned* idx, const unsigned* bounds, const float* lists, int nlists,
                       uint64_t list_stride, int divide, float divisor, float* agg, uint64_t G,
@@ -290,11 +291,6 @@ void launch_decode_ar(const unsigned* idx, const unsigned* bounds, const float* 
 void launch_decode_ag(const unsigned* packs, uint64_t pack_stride, uint64_t k, int nranks,
                       const unsigned* bounds, float divisor, float* agg, uint64_t G,
                       unsigned* zmaps, int map_rank0, int nmaps, cudaStream_t s);
-// AG decode straight from peer memory (every rank's list, values and chunk
-// bounds where its select published them, parity par; waits for `epoch`):
-// the allgather fused into the decode.
-void launch_decode_ag_peers(const PeerBufs& pb, int par, unsigned long long epoch, uint64_t k, float divisor,
-                            float* agg, uint64_t G, unsigned* zmap, cudaStream_t s);
 void launch_dense_sum(const float* lists, int nlists, uint64_t list_stride, int divide,
                       float divisor, float* out, uint64_t G, cudaStream_t s);
 // topk_layerwise for the map's small layers in one launch (one block per

@@ -2498,49 +2498,97 @@ void launch_gather(const unsigned* bidx, uint64_t k, const float* ge, float* con
 // ------------------------------------------------------ incremental decode ---
 // The dense aggregate buffer is library-owned, so after the first full decode
 // it can be kept equal to densify(this step) by touching only the supports:
-// (1) the previous step's indices are zeroed (and their owed-zero bits
-// cleared), (2) this step's values are written (and their bits set).  For
-// k << G this replaces a 4G-byte dense write with ~2k random 4-byte writes;
-// the buffer content is identical to a full decode.
+// (1) every 32-byte sector holding a previous index is zeroed and every owed-
+// zero word holding one cleared, (2) every sector holding a new index is
+// rewritten whole (its new values, zeros elsewhere) and every owed-zero word
+// holding one rewritten.  Each sector / word is written by the thread of its
+// first list entry (the lists are sorted), so all writes are plain full-
+// sector stores -- no atomics, and no partial sectors for the memory system
+// to merge.  For k << G this replaces the 4G-byte dense write with ~2 x 32k
+// bytes; the buffer content is identical to a full decode.
+__device__ __forceinline__ void st_sector(float* __restrict__ agg, uint64_t b, const float (&v)[8],
+                                          uint64_t G) {
+  if (b + 8 <= G) {
+    float4* p = reinterpret_cast<float4*>(agg + b);
+    p[0] = make_float4(v[0], v[1], v[2], v[3]);
+    p[1] = make_float4(v[4], v[5], v[6], v[7]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      if (b + e < G) agg[b + e] = v[e];
+  }
+}
+
 __global__ void k_agg_clear(const unsigned* __restrict__ prev, uint64_t kp, float* __restrict__ agg,
-                            unsigned* __restrict__ zmap) {
+                            unsigned* __restrict__ zmap, uint64_t G) {
   pdl_wait();
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < kp;
        j += (uint64_t)gridDim.x * blockDim.x) {
     const unsigned i = __ldcs(prev + j);
-    agg[i] = 0.0f;
-    atomicAnd(zmap + zmap_word(i), ~zmap_bit(i));
+    const unsigned ip = j ? __ldcs(prev + j - 1) : 0u;
+    if (j == 0 || (ip >> 3) != (i >> 3)) {
+      const float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      st_sector(agg, (uint64_t)(i & ~7u), z, G);
+    }
+    if (j == 0 || zmap_word(ip) != zmap_word(i)) zmap[zmap_word(i)] = 0u;
   }
 }
 
 __global__ void k_agg_write(const unsigned* __restrict__ idx, uint64_t k,
                             const float* __restrict__ lists, int nlists, uint64_t list_stride,
                             int divide, float divisor, float* __restrict__ agg,
-                            unsigned* __restrict__ zmap, unsigned* __restrict__ keep) {
+                            unsigned* __restrict__ zmap, unsigned* __restrict__ keep, uint64_t G) {
   pdl_wait();
-  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < k;
-       j += (uint64_t)gridDim.x * blockDim.x) {
-    const unsigned i = __ldcs(idx + j);
+  auto value = [&](uint64_t j) {
     float v = lists[j];  // v = c_0; v += c_r (r ascending), collectives.hpp:82-87
     for (int l = 1; l < nlists; ++l) v += lists[(uint64_t)l * list_stride + j];
-    if (divide) v = v / divisor;
-    agg[i] = v;
-    atomicOr(zmap + zmap_word(i), zmap_bit(i));
+    return divide ? v / divisor : v;
+  };
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < k;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned i = idx[j];
+    const unsigned ip = j ? idx[j - 1] : 0u;
     keep[j] = i;  // the support the next step clears
+    if (j == 0 || (ip >> 3) != (i >> 3)) {
+      // this sector's entries are j, j+1, ... (at most 8)
+      float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      unsigned m = i;
+      for (uint64_t q = j; q < k && q < j + 8; ++q) {
+        if (q > j) {
+          m = idx[q];
+          if ((m >> 3) != (i >> 3)) break;
+        }
+        const float x = value(q);
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if ((m & 7u) == (unsigned)e) v[e] = x;
+      }
+      st_sector(agg, (uint64_t)(i & ~7u), v, G);
+    }
+    if (j == 0 || zmap_word(ip) != zmap_word(i)) {
+      unsigned bits = zmap_bit(i);
+      for (uint64_t q = j + 1; q < k && q < j + 32; ++q) {
+        const unsigned m = idx[q];
+        if (zmap_word(m) != zmap_word(i)) break;
+        bits |= zmap_bit(m);
+      }
+      zmap[zmap_word(i)] = bits;
+    }
   }
 }
 
 void launch_agg_update(const unsigned* prev, uint64_t kp, const unsigned* idx, uint64_t k,
                        const float* lists, int nlists, uint64_t list_stride, int divide,
-                       float divisor, float* agg, unsigned* zmap, unsigned* keep, cudaStream_t s) {
+                       float divisor, float* agg, uint64_t G, unsigned* zmap, unsigned* keep,
+                       cudaStream_t s) {
   if (kp) {
     const unsigned g = (unsigned)std::min<uint64_t>((kp + kThreads - 1) / kThreads, num_sms() * 16ull);
-    launch_pdl(k_agg_clear, g, kThreads, 0, s, prev, kp, agg, zmap);
+    launch_pdl(k_agg_clear, g, kThreads, 0, s, prev, kp, agg, zmap, G);
     count_launch();
   }
   const unsigned g = (unsigned)std::min<uint64_t>((k + kThreads - 1) / kThreads, num_sms() * 16ull);
   launch_pdl(k_agg_write, g, kThreads, 0, s, idx, k, lists, nlists, list_stride, divide, divisor, agg, zmap,
-                                      keep);
+             keep, G);
   count_launch();
 }
 
@@ -3065,39 +3113,20 @@ __global__ void __launch_bounds__(kThreads) k_decode_ag(const unsigned* __restri
 // scatter starts, so a tile costs one dependent load round instead of two
 // per rank (the per-rank passes keep their barriers: the reference's
 // rank-ascending summation order, artopk.hpp:154-158).
-// kPeer (AG over peer memory): rank r's list, values and chunk bounds are
-// read where its select published them (pb, parity par) -- the peers' over
-// NVLink, prefetched a tile ahead like the local ones -- after every rank's
-// publish; no separate allgather copy.
-template <int NR, bool kPeer = false>
+template <int NR>
 __global__ void __launch_bounds__(kThreads) k_decode_ag_n(const unsigned* __restrict__ packs,
                                                           uint64_t pack_stride, uint64_t k, int nranks,
                                                           const unsigned* __restrict__ bounds,
                                                           float divisor, float* __restrict__ agg, uint64_t G,
-                                                          unsigned* __restrict__ zmaps, int map_rank0, int nmaps,
-                                                          PeerBufs pb, int par, unsigned long long epoch) {
+                                                          unsigned* __restrict__ zmaps, int map_rank0, int nmaps) {
   pdl_wait();
   __shared__ __align__(128) float tile[2][kDecTile];
   __shared__ unsigned s_touch[kDecTile / 32];
   extern __shared__ unsigned s_zm[];  // nmaps x kDecChunks*32
-  if (kPeer && !wait_all(pb, 0, epoch)) return;  // timeout reported
   const uint64_t ntd = (G + kDecTile - 1) >> kDecShift;
   const uint64_t nch = nchunks_of(G);
   const int zw = kDecChunks * 32;
   const bool divide = divisor != 1.0f;
-  const uint64_t poff = kPeer ? (uint64_t)par * pb.kmax : 0;
-  auto idp = [&](int r) -> const unsigned* {
-    return kPeer ? pb.list[r] + poff : packs + (uint64_t)r * pack_stride;
-  };
-  auto vap = [&](int r) -> const float* {
-    return kPeer ? pb.contrib[r] + poff : reinterpret_cast<const float*>(packs + (uint64_t)r * pack_stride + k);
-  };
-  auto bdp = [&](int r) -> const unsigned* {
-    return kPeer ? pb.bounds[r] + (uint64_t)par * pb.nbs : bounds + (uint64_t)r * (nch + 1);
-  };
-  // remote rows: volatile loads over NVLink (after the acquire of the publish)
-  auto ldu = [&](const unsigned* q, int r) -> unsigned { return kPeer && r != pb.rank ? __ldcv(q) : __ldg(q); };
-  auto ldf = [&](const float* q, int r) -> float { return kPeer && r != pb.rank ? __ldcv(q) : __ldg(q); };
   unsigned nlo[NR], nhi[NR];
   auto load_bounds = [&](uint64_t t) {
     const uint64_t c0 = t * kDecChunks, c1 = min(c0 + kDecChunks, nch);
@@ -3105,9 +3134,9 @@ __global__ void __launch_bounds__(kThreads) k_decode_ag_n(const unsigned* __rest
     for (int r = 0; r < NR; ++r) {
       nlo[r] = nhi[r] = 0;
       if (r < nranks) {
-        const unsigned* bd = bdp(r);
-        nlo[r] = ldu(bd + c0, r);
-        nhi[r] = ldu(bd + c1, r);
+        const unsigned* bd = bounds + (uint64_t)r * (nch + 1);
+        nlo[r] = __ldg(bd + c0);
+        nhi[r] = __ldg(bd + c1);
       }
     }
   };
@@ -3125,8 +3154,9 @@ __global__ void __launch_bounds__(kThreads) k_decode_ag_n(const unsigned* __rest
       v0[r] = 0.f;
       const unsigned j = lo[r] + threadIdx.x;
       if (r < nranks && j < hi[r]) {
-        p0[r] = ldu(idp(r) + j, r);
-        v0[r] = ldf(vap(r) + j, r);
+        const unsigned* id = packs + (uint64_t)r * pack_stride;
+        p0[r] = id[j];
+        v0[r] = reinterpret_cast<const float*>(id + k)[j];
       }
     }
     if (t + gridDim.x < ntd) load_bounds(t + gridDim.x);
@@ -3141,15 +3171,15 @@ __global__ void __launch_bounds__(kThreads) k_decode_ag_n(const unsigned* __rest
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
       if (r < nranks) {
-        const unsigned* id = idp(r);
-        const float* va = vap(r);
+        const unsigned* id = packs + (uint64_t)r * pack_stride;
+        const float* va = reinterpret_cast<const float*>(id + k);
         const int m = r - map_rank0;
         const bool mapped = m >= 0 && m < nmaps;
         for (unsigned j = lo[r] + threadIdx.x; j < hi[r]; j += kThreads) {
           const bool first = j == lo[r] + threadIdx.x;
-          const unsigned p = first ? p0[r] : ldu(id + j, r);
+          const unsigned p = first ? p0[r] : id[j];
           const unsigned lp = p - (unsigned)t0;
-          tl[lp] += first ? v0[r] : ldf(va + j, r);
+          tl[lp] += first ? v0[r] : va[j];
           if (divide) atomicOr(&s_touch[lp >> 5], 1u << (lp & 31));
           if (mapped) atomicOr(&s_zm[m * zw + zmap_word(p) - (unsigned)(c0 << 5)], zmap_bit(p));
         }
@@ -3180,30 +3210,13 @@ void launch_decode_ag(const unsigned* packs, uint64_t pack_stride, uint64_t k, i
   auto go = [&](auto kern) {
     if (smem > 16 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     launch_pdl(kern, num_sms() * 6, kThreads, smem, s, packs, pack_stride, k, nranks, bounds, divisor, agg, G,
-               zmaps, map_rank0, nmaps, PeerBufs{}, 0, 0ull);
+               zmaps, map_rank0, nmaps);
   };
   if (nranks <= 1) go(k_decode_ag_n<1>);
   else if (nranks <= 2) go(k_decode_ag_n<2>);
   else if (nranks <= 4) go(k_decode_ag_n<4>);
   else if (nranks <= 8) go(k_decode_ag_n<8>);
-  else {
-    if (smem > 16 * 1024) cudaFuncSetAttribute(k_decode_ag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    launch_pdl(k_decode_ag, num_sms() * 6, kThreads, smem, s, packs, pack_stride, k, nranks, bounds, divisor, agg,
-               G, zmaps, map_rank0, nmaps);
-  }
-  count_launch();
-}
-
-void launch_decode_ag_peers(const PeerBufs& pb, int par, unsigned long long epoch, uint64_t k, float divisor,
-                            float* agg, uint64_t G, unsigned* zmap, cudaStream_t s) {
-  const size_t smem = (size_t)kDecChunks * 32 * sizeof(unsigned);
-  auto go = [&](auto kern) {
-    launch_pdl(kern, num_sms() * 6, kThreads, smem, s, (const unsigned*)nullptr, (uint64_t)0, k, pb.n,
-               (const unsigned*)nullptr, divisor, agg, G, zmap, pb.rank, 1, pb, par, epoch);
-  };
-  if (pb.n <= 2) go(k_decode_ag_n<2, true>);
-  else if (pb.n <= 4) go(k_decode_ag_n<4, true>);
-  else go(k_decode_ag_n<8, true>);
+  else go(k_decode_ag);
   count_launch();
 }
 
@@ -3234,8 +3247,7 @@ static void prefer_max_smem() {
   const void* fs[] = {(const void*)k_fill_synth, (const void*)k_gather, (const void*)k_agg_clear,
                       (const void*)k_agg_write, (const void*)k_zero_at, (const void*)k_bounds,
                       (const void*)k_decode_ar<0>, (const void*)k_decode_ar<1>, (const void*)k_decode_ar<2>, (const void*)k_decode_ag, (const void*)k_decode_ag_n<1>, (const void*)k_decode_ag_n<2>,
-                      (const void*)k_decode_ag_n<4>, (const void*)k_decode_ag_n<8>, (const void*)k_decode_ag_n<2, true>,
-                      (const void*)k_decode_ag_n<4, true>, (const void*)k_decode_ag_n<8, true>, (const void*)k_dense_sum,
+                      (const void*)k_decode_ag_n<4>, (const void*)k_decode_ag_n<8>, (const void*)k_dense_sum,
                       (const void*)k_sum_fixed};
   for (const void* f : fs)
     cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);

@@ -294,6 +294,14 @@ class Cluster:
         check(lib.fc_peer_exchange(self._ctx, C.byref(e)))
         return bool(e.value)
 
+    @property
+    def aggregate_in_place(self) -> bool:
+        """The last AR-Top-k step updated the aggregate in place (same content
+        as a full rewrite; FC_FLAG_DENSE_DECODE forces the rewrite)."""
+        e = C.c_int()
+        check(lib.fc_aggregate_in_place(self._ctx, C.byref(e)))
+        return bool(e.value)
+
     def moo_metrics(self, st: "StepStats", ag: bool = False) -> tuple[float, float]:
         """(gain, t_comp seconds) of the last step, identical on every rank
         (the Trainer's *_with_gain, inc/trainer.hpp:361-398; t_comp measured)."""
