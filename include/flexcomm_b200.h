@@ -78,7 +78,7 @@ typedef enum fc_memkind { FC_HOST = 0, FC_DEVICE = 1, FC_HOST_ASYNC = 2 } fc_mem
 #define FC_FLAG_ASYNC 0x1u        /* do not synchronize at the end of a step      */
 #define FC_FLAG_NO_TIMING 0x2u    /* skip per-phase CUDA events                   */
 #define FC_FLAG_DENSE_DECODE 0x4u /* always rewrite the whole aggregate; otherwise
-                                     AR steps at k <= G/128 update it in place (zero
+                                     AR steps at k <= G/80 update it in place (zero
                                      the previous support, write the new one), so
                                      callers must treat fc_aggregate_ptr() memory
                                      as read-only                                 */
@@ -325,7 +325,7 @@ int fc_peer_exchange(fc_ctx* ctx, int* enabled);
 
 /* *in_place = 1 if the last AR-Top-k step left the aggregate as an in-place
  * update (the previous support's sectors zeroed, this step's sectors
- * rewritten: identical content, k <= G / 32 without FC_FLAG_DENSE_DECODE /
+ * rewritten: identical content, k <= G / 80 without FC_FLAG_DENSE_DECODE /
  * FC_FLAG_PIPELINE, single-process or NCCL exchange), 0 if it was rewritten
  * whole. */
 int fc_aggregate_in_place(fc_ctx* ctx, int* in_place);

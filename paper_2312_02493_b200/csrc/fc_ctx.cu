@@ -129,7 +129,7 @@ struct fc_ctx {
   unsigned* agg_support = nullptr;  // indices of agg's nonzero support (incremental decode)
   uint64_t agg_support_k = 0;
   bool agg_incr = false;            // agg == densify(agg_support) and zmap 0 == its bits
-  uint64_t incr_div = 32;           // in-place update when k <= G / incr_div (FC_INCR_DIV overrides)
+  uint64_t incr_div = 80;           // in-place update when k <= G / incr_div (FC_INCR_DIV overrides)
   // compressors of the AG path (inc/artopk.hpp:113-123)
   std::vector<uint64_t> layer_off, layer_len;  // layer map (Layerwise), sorted, disjoint
   int thresh_rounds = 25;                      // Threshold bisection rounds
@@ -1749,7 +1749,7 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
   const uint64_t lstride = c->nccl ? 0 : c->kmax;
   // in-place update: ~2k whole-sector writes (32 B each, scattered) against
   // the 4G-byte dense write; measured break-even sets incr_div
-  const bool incr_ok = !(c->flags & FC_FLAG_DENSE_DECODE) && c->nbuf == 1 && !p2p_star && c->incr_div &&
+  const bool incr_ok = !(c->flags & FC_FLAG_DENSE_DECODE) && c->nbuf == 1 && c->incr_div &&
                        k * c->incr_div <= c->G;
   int ob = 0;
   TRY(agg_target(c, &ob));
@@ -1769,9 +1769,18 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
     if (tree && (mode == FC_VAR || c->rank == sel))  // (VAR: only the winner works; found on the device)
       fcb::launch_reduce_root(c->pb, par, epoch, k, op == FC_AVG, (float)N, mode == FC_STAR ? sel : -1, c->dsel,
                               c->w[0].ctl, c->stream);
-    fcb::launch_decode_ar_peers(c->pb, par, epoch, bsrc, own_bounds, k, op == FC_AVG, (float)N, rs || tree,
-                                aggw, c->G, c->zmaps, tree ? (mode == FC_STAR ? sel : -2) : -1, c->dsel,
-                                c->stream);
+    const int wait_root = tree ? (mode == FC_STAR ? sel : -2) : -1;
+    if (incr_ok && c->agg_incr) {
+      fcb::launch_agg_update_peers(c->pb, par, epoch, c->agg_support, c->agg_support_k, bsrc, k, op == FC_AVG,
+                                   (float)N, rs || tree, aggw, c->G, c->zmaps, c->agg_support, wait_root,
+                                   c->dsel, c->stream);
+    } else {
+      fcb::launch_decode_ar_peers(c->pb, par, epoch, bsrc, own_bounds, k, op == FC_AVG, (float)N, rs || tree,
+                                  aggw, c->G, c->zmaps, wait_root, c->dsel, c->stream);
+      if (incr_ok)
+        CUDA_TRY(cudaMemcpyAsync(c->agg_support, bsrc, k * sizeof(unsigned), cudaMemcpyDeviceToDevice,
+                                 c->stream));
+    }
   } else if (incr_ok && c->agg_incr) {
     // in place: zero the previous support, write this one (same dense content)
     fcb::launch_agg_update(c->agg_support, c->agg_support_k, bsrc, k, lists, nlists, lstride,

@@ -283,6 +283,12 @@ void launch_agg_update(const unsigned* prev, uint64_t kp, const unsigned* idx, u
                        const float* lists, int nlists, uint64_t list_stride, int divide,
                        float divisor, float* agg, uint64_t G, unsigned* zmap, unsigned* keep,
                        cudaStream_t s);
+// ... the same over the peer exchanges (values as launch_decode_ar_peers
+// reads them, after its publish waits)
+void launch_agg_update_peers(const PeerBufs& pb, int par, unsigned long long epoch, const unsigned* prev,
+                             uint64_t kp, const unsigned* idx, uint64_t k, int divide, float divisor,
+                             bool reduced, float* agg, uint64_t G, unsigned* zmap, unsigned* keep,
+                             int wait_root, const int* dsel, cudaStream_t s);
 // Decodes also write the zero map(s) of the decoded index list(s).
 void launch_decode_ar(const unsigned* idx, const unsigned* bounds, const float* lists, int nlists,
                       uint64_t list_stride, int divide, float divisor, float* agg, uint64_t G,

@@ -1659,6 +1659,7 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
     if (S == 0 && tid == 0) s_pos[0] = 0;
   }
   __syncthreads();
+  SX_MARK(6);
   const unsigned P = s_pos[S];
   const bool cached = 2ull * P <= cap;
   float4* s_val4 = reinterpret_cast<float4*>(s_val);
@@ -1679,6 +1680,7 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
       if (bytes) bulk_g2s(s_idx + s_pos[j], w.cand_idx + ((uint64_t)seg_c0(j) << kChunkShift), bytes, &s_mbar);
     }
   }
+  SX_MARK(7);
   // warp-contiguous ranges of 128-position steps
   const unsigned R = (P + kSxWarps * 128 - 1) / (kSxWarps * 128) * 128;
   const unsigned wlo = min(P, warp * R), whi = min(P, wlo + R);
@@ -1738,6 +1740,14 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
   using U1 = std::integral_constant<int, 1>;
   using U2 = std::integral_constant<int, 2>;
   using U4 = std::integral_constant<int, 4>;
+  // passes over the shared-memory-staged candidates run one 128-position
+  // group per loop iteration (a pass's instruction footprint is one f body:
+  // 1.5 us less per select than 4 unrolled copies); global-memory passes
+  // unroll for memory-level parallelism
+  auto run = [&](auto Uglobal, bool from_smem, bool with_idx, bool stage, auto&& f) {
+    if (from_smem) pass(U1{}, true, with_idx, stage, f);
+    else pass(Uglobal, false, with_idx, stage, f);
+  };
 
   // ---- P1: window histogram (key bits 30..11 relative to Lb's prefix) ----
   unsigned long long need = k;
@@ -1782,7 +1792,7 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
     __syncthreads();
     const unsigned pf = prefix;
     unsigned gt = 0;
-    pass(U4{}, cached, false, false, [&](const float4& v, const uint4&, unsigned nv) {
+    run(U4{}, cached, false, false, [&](const float4& v, const uint4&, unsigned nv) {
       for (unsigned e = 0; e < nv; ++e) {
         const unsigned key = key_of(f4c(v, e)), hi = key >> 11;
         gt += hi > pf;
@@ -1829,7 +1839,7 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
       const unsigned pf = prefix, dm = (unsigned)nb - 1;
       for (int b = tid; b < nb; b += kSxThreads) s_h[b] = 0;
       __syncthreads();
-      pass(U4{}, cached, false, false, [&](const float4& v, const uint4&, unsigned nv) {
+      run(U4{}, cached, false, false, [&](const float4& v, const uint4&, unsigned nv) {
         for (unsigned e = 0; e < nv; ++e) {
           const unsigned key = key_of(f4c(v, e));
           if ((unsigned)((unsigned long long)key >> as) == pf) atomicAdd(&s_h[(key >> sh) & dm], 1u);
@@ -1850,7 +1860,7 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
   needT = need;
   if (!counted) {
     unsigned gt = 0, eq = 0;
-    pass(U4{}, cached, false, false, [&](const float4& v, const uint4&, unsigned nv) {
+    run(U4{}, cached, false, false, [&](const float4& v, const uint4&, unsigned nv) {
       for (unsigned e = 0; e < nv; ++e) {
         const unsigned key = key_of(f4c(v, e));
         gt += key > T;
@@ -1925,7 +1935,7 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
   {
     unsigned long long grun = s_wpre[warp] >> 32, erun = s_wpre[warp] & 0xffffffffull;
     const unsigned ibase = mode.idx_base;
-    pass(U2{}, cached, true, false, [&](const float4& v, const uint4& id, unsigned nv) {
+    run(U2{}, cached, true, false, [&](const float4& v, const uint4& id, unsigned nv) {
       unsigned gm = 0, em = 0;
       for (unsigned e = 0; e < nv; ++e) {
         const unsigned key = key_of(f4c(v, e));
@@ -2060,7 +2070,8 @@ int launch_select(uint64_t k, Ctl* ctl, const ChunkWs& w, const float* ef_out, u
     }
     const unsigned cpb = SxGeom(w.nchunks, grid, EfLayout(w.nchunks, w.batch)).max_chunks();
     if (2ull * cpb + 8 > kSelSmemMax / 4) return (int)cudaErrorInvalidValue;
-    e = launch_grid_sync((const void*)k_select_x, dim3(grid), dim3(kSxThreads), kSelSmemMax, s, args, w.coop != 0);
+    e = launch_grid_sync((const void*)k_select_x, dim3(grid), dim3(kSxThreads), kSelSmemMax, s, args,
+                         w.coop != 0);
   } else {
     // threshold compressor: k_select (bisection), per-chunk candidate slots
     if (w.batch > 1) return (int)cudaErrorInvalidValue;
@@ -2506,42 +2517,70 @@ void launch_gather(const unsigned* bidx, uint64_t k, const float* ge, float* con
 // sector stores -- no atomics, and no partial sectors for the memory system
 // to merge.  For k << G this replaces the 4G-byte dense write with ~2 x 32k
 // bytes; the buffer content is identical to a full decode.
-__device__ __forceinline__ void st_sector(float* __restrict__ agg, uint64_t b, const float (&v)[8],
-                                          uint64_t G) {
-  if (b + 8 <= G) {
+template <int kA>
+__device__ __forceinline__ void st_atom(float* __restrict__ agg, uint64_t b, const float (&v)[kA], uint64_t G) {
+  if (b + kA <= G) {
     float4* p = reinterpret_cast<float4*>(agg + b);
-    p[0] = make_float4(v[0], v[1], v[2], v[3]);
-    p[1] = make_float4(v[4], v[5], v[6], v[7]);
+#pragma unroll
+    for (int q = 0; q < kA / 4; ++q) p[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
   } else {
 #pragma unroll
-    for (int e = 0; e < 8; ++e)
+    for (int e = 0; e < kA; ++e)
       if (b + e < G) agg[b + e] = v[e];
   }
 }
 
+template <int kA>
 __global__ void k_agg_clear(const unsigned* __restrict__ prev, uint64_t kp, float* __restrict__ agg,
                             unsigned* __restrict__ zmap, uint64_t G) {
   pdl_wait();
+  constexpr unsigned kSh = kA == 8 ? 3 : kA == 16 ? 4 : 5;
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < kp;
        j += (uint64_t)gridDim.x * blockDim.x) {
     const unsigned i = __ldcs(prev + j);
     const unsigned ip = j ? __ldcs(prev + j - 1) : 0u;
-    if (j == 0 || (ip >> 3) != (i >> 3)) {
-      const float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      st_sector(agg, (uint64_t)(i & ~7u), z, G);
+    if (j == 0 || (ip >> kSh) != (i >> kSh)) {
+      float z[kA];
+#pragma unroll
+      for (int e = 0; e < kA; ++e) z[e] = 0.f;
+      st_atom<kA>(agg, (uint64_t)(i & ~(kA - 1u)), z, G);
     }
     if (j == 0 || zmap_word(ip) != zmap_word(i)) zmap[zmap_word(i)] = 0u;
   }
 }
 
+// kPeers as in k_decode_ar: 0 local lists, 1 two-rank direct sum (own
+// contribution + the peer's in the inbox), 2 the reduced list (reduce-scatter
+// or tree root), after the same publish waits.
+template <int kPeers, int kA>
 __global__ void k_agg_write(const unsigned* __restrict__ idx, uint64_t k,
                             const float* __restrict__ lists, int nlists, uint64_t list_stride,
                             int divide, float divisor, float* __restrict__ agg,
-                            unsigned* __restrict__ zmap, unsigned* __restrict__ keep, uint64_t G) {
+                            unsigned* __restrict__ zmap, unsigned* __restrict__ keep, uint64_t G,
+                            PeerBufs pb, int par, unsigned long long epoch, int wait_root,
+                            const int* __restrict__ dsel) {
   pdl_wait();
+  constexpr unsigned kSh = kA == 8 ? 3 : kA == 16 ? 4 : 5;
+  if (kPeers) {
+    if (wait_root == -1) {
+      if (!wait_all(pb, kPeers, epoch)) return;  // timeout reported
+    } else {
+      bool ok = true;
+      if (threadIdx.x == 0) ok = wait_from(pb, wait_root >= 0 ? wait_root : *dsel, kPeers, epoch);
+      if (!__syncthreads_and(ok)) return;
+    }
+  }
   auto value = [&](uint64_t j) {
-    float v = lists[j];  // v = c_0; v += c_r (r ascending), collectives.hpp:82-87
-    for (int l = 1; l < nlists; ++l) v += lists[(uint64_t)l * list_stride + j];
+    float v;
+    if (kPeers == 1) {  // c_0 + c_1 (collectives.hpp:82-87; two terms: order-free)
+      v = __ldcg(pb.contrib[pb.rank] + (uint64_t)par * pb.kmax + j) +
+          __ldcg(inbox_of(pb, pb.rank, 1 - pb.rank, par) + j);
+    } else if (kPeers == 2) {
+      v = __ldcg(pb.reduced[pb.rank] + (uint64_t)par * pb.kmax + j);
+    } else {
+      v = lists[j];  // v = c_0; v += c_r (r ascending), collectives.hpp:82-87
+      for (int l = 1; l < nlists; ++l) v += lists[(uint64_t)l * list_stride + j];
+    }
     return divide ? v / divisor : v;
   };
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < k;
@@ -2549,21 +2588,23 @@ __global__ void k_agg_write(const unsigned* __restrict__ idx, uint64_t k,
     const unsigned i = idx[j];
     const unsigned ip = j ? idx[j - 1] : 0u;
     keep[j] = i;  // the support the next step clears
-    if (j == 0 || (ip >> 3) != (i >> 3)) {
-      // this sector's entries are j, j+1, ... (at most 8)
-      float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (j == 0 || (ip >> kSh) != (i >> kSh)) {
+      // this atom's entries are j, j+1, ... (at most kA)
+      float v[kA];
+#pragma unroll
+      for (int e = 0; e < kA; ++e) v[e] = 0.f;
       unsigned m = i;
-      for (uint64_t q = j; q < k && q < j + 8; ++q) {
+      for (uint64_t q = j; q < k && q < j + kA; ++q) {
         if (q > j) {
           m = idx[q];
-          if ((m >> 3) != (i >> 3)) break;
+          if ((m >> kSh) != (i >> kSh)) break;
         }
         const float x = value(q);
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-          if ((m & 7u) == (unsigned)e) v[e] = x;
+        for (int e = 0; e < kA; ++e)
+          if ((m & (kA - 1u)) == (unsigned)e) v[e] = x;
       }
-      st_sector(agg, (uint64_t)(i & ~7u), v, G);
+      st_atom<kA>(agg, (uint64_t)(i & ~(kA - 1u)), v, G);
     }
     if (j == 0 || zmap_word(ip) != zmap_word(i)) {
       unsigned bits = zmap_bit(i);
@@ -2577,19 +2618,51 @@ __global__ void k_agg_write(const unsigned* __restrict__ idx, uint64_t k,
   }
 }
 
+static unsigned agg_grid(uint64_t n) {
+  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + kThreads - 1) / kThreads, num_sms() * 16ull));
+}
+
+// The in-place update writes whole 32-byte sectors: measured against 64- and
+// 128-byte granules (C3, CR 0.003 / 0.01 / 0.02: 0.350 / 0.408 / 0.479 ms per
+// step vs 0.362 / 0.441 / 0.545 and 0.412 / 0.556 / 0.699), the extra bytes
+// of a wider granule cost more than its fewer, larger writes save.
+constexpr int kAggAtom = 8;
+
+static void agg_update(const PeerBufs& pb, int peers, int par, unsigned long long epoch, const unsigned* prev,
+                       uint64_t kp, const unsigned* idx, uint64_t k, const float* lists, int nlists,
+                       uint64_t list_stride, int divide, float divisor, float* agg, uint64_t G, unsigned* zmap,
+                       unsigned* keep, int wait_root, const int* dsel, cudaStream_t s) {
+  if (kp) {
+    launch_pdl(k_agg_clear<kAggAtom>, agg_grid(kp), kThreads, 0, s, prev, kp, agg, zmap, G);
+    count_launch();
+  }
+  if (peers == 0)
+    launch_pdl(k_agg_write<0, kAggAtom>, agg_grid(k), kThreads, 0, s, idx, k, lists, nlists, list_stride, divide,
+               divisor, agg, zmap, keep, G, pb, par, epoch, wait_root, dsel);
+  else if (peers == 1)
+    launch_pdl(k_agg_write<1, kAggAtom>, agg_grid(k), kThreads, 0, s, idx, k, lists, nlists, list_stride, divide,
+               divisor, agg, zmap, keep, G, pb, par, epoch, wait_root, dsel);
+  else
+    launch_pdl(k_agg_write<2, kAggAtom>, agg_grid(k), kThreads, 0, s, idx, k, lists, nlists, list_stride, divide,
+               divisor, agg, zmap, keep, G, pb, par, epoch, wait_root, dsel);
+  count_launch();
+}
+
 void launch_agg_update(const unsigned* prev, uint64_t kp, const unsigned* idx, uint64_t k,
                        const float* lists, int nlists, uint64_t list_stride, int divide,
                        float divisor, float* agg, uint64_t G, unsigned* zmap, unsigned* keep,
                        cudaStream_t s) {
-  if (kp) {
-    const unsigned g = (unsigned)std::min<uint64_t>((kp + kThreads - 1) / kThreads, num_sms() * 16ull);
-    launch_pdl(k_agg_clear, g, kThreads, 0, s, prev, kp, agg, zmap, G);
-    count_launch();
-  }
-  const unsigned g = (unsigned)std::min<uint64_t>((k + kThreads - 1) / kThreads, num_sms() * 16ull);
-  launch_pdl(k_agg_write, g, kThreads, 0, s, idx, k, lists, nlists, list_stride, divide, divisor, agg, zmap,
-             keep, G);
-  count_launch();
+  agg_update(PeerBufs{}, 0, 0, 0ull, prev, kp, idx, k, lists, nlists, list_stride, divide, divisor, agg, G, zmap,
+             keep, -1, nullptr, s);
+}
+
+void launch_agg_update_peers(const PeerBufs& pb, int par, unsigned long long epoch, const unsigned* prev,
+                             uint64_t kp, const unsigned* idx, uint64_t k, int divide, float divisor,
+                             bool reduced, float* agg, uint64_t G, unsigned* zmap, unsigned* keep,
+                             int wait_root, const int* dsel, cudaStream_t s) {
+  // (N = 2 direct sums never take a tree root: wait_root is -1 there)
+  agg_update(pb, reduced ? 2 : 1, par, epoch, prev, kp, idx, k, nullptr, pb.n, k, reduced ? 0 : divide,
+             reduced ? 1.0f : divisor, agg, G, zmap, keep, reduced ? wait_root : -1, dsel, s);
 }
 
 // Materialise owed zeros (before the residual store is read from outside).
@@ -3244,8 +3317,10 @@ void launch_dense_sum(const float* lists, int nlists, uint64_t list_stride, int 
 // EF and select kernels need it, and switching the L1/shared split between
 // consecutive kernels costs an SM drain at each boundary.
 static void prefer_max_smem() {
-  const void* fs[] = {(const void*)k_fill_synth, (const void*)k_gather, (const void*)k_agg_clear,
-                      (const void*)k_agg_write, (const void*)k_zero_at, (const void*)k_bounds,
+  const void* fs[] = {(const void*)k_fill_synth, (const void*)k_gather,
+                      (const void*)k_agg_clear<kAggAtom>, (const void*)k_agg_write<0, kAggAtom>,
+                      (const void*)k_agg_write<1, kAggAtom>, (const void*)k_agg_write<2, kAggAtom>,
+                      (const void*)k_zero_at, (const void*)k_bounds,
                       (const void*)k_decode_ar<0>, (const void*)k_decode_ar<1>, (const void*)k_decode_ar<2>, (const void*)k_decode_ag, (const void*)k_decode_ag_n<1>, (const void*)k_decode_ag_n<2>,
                       (const void*)k_decode_ag_n<4>, (const void*)k_decode_ag_n<8>, (const void*)k_dense_sum,
                       (const void*)k_sum_fixed};

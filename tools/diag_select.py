@@ -25,7 +25,8 @@ with fc.Cluster(1, G, max_cr=max(cr, 0.1), flags=flags) as cl:
               + f" | EF: preamble={(t[10] - t[8]) / 1e3:.1f}us sample+hist1={(t[12] - t[8]) / 1e3:.1f}us flush={(t[13] - t[12]) / 1e3:.1f}us "
               f"barrier={(t[9] - t[13]) / 1e3:.1f}us bound={(t[10] - t[9]) / 1e3:.1f}us "
               f"stream={(t[11] - t[10]) / 1e3:.1f}us EF-end->select-start={(t[0] - t[11]) / 1e3:.1f}us"
-              + (f" | sx: p1pass={(t[16] - t[0]) / 1e3:.1f} flush={(t[17] - t[16]) / 1e3:.1f} "
+              + (f" | sx: setup={(t[22] - t[0]) / 1e3:.1f} idxtma={(t[23] - t[22]) / 1e3:.1f} "
+                 f"p1pass={(t[16] - t[23]) / 1e3:.1f} flush={(t[17] - t[16]) / 1e3:.1f} "
                  f"bar1={(t[1] - t[17]) / 1e3:.1f} p2pass={(t[18] - t[2]) / 1e3:.1f} flush+bar2={(t[3] - t[18]) / 1e3:.1f} "
                  f"idxwait={(t[19] - t[4]) / 1e3:.1f} emit={(t[5] - t[19]) / 1e3:.1f} write={(t[20] - t[5]) / 1e3:.1f} "
                  f"bounds={(t[21] - t[20]) / 1e3:.1f} bsum={(t[6] - t[21]) / 1e3:.1f}" if t[16] else ""))
