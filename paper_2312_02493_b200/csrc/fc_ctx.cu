@@ -85,6 +85,12 @@ struct Worker {
   const float* topk_val = nullptr;
   bool kept_is_topk = false;  // gather skipped: kept energy == ||top-k||^2
   fcb::Pending pz{};          // zeros owed to `ge` (zero map, read by the next EF)
+  // layerwise segments: control blocks (two sets, alternate steps), sample
+  // keys and speculation words per segment
+  fcb::Ctl* seg_ctl[2] = {};
+  unsigned* seg_skeys = nullptr;
+  unsigned* seg_lastb1 = nullptr;
+  int seg_par = 0;
   const unsigned* pz_idx = nullptr;  // the same zeros as a sorted index list
   uint64_t pz_k = 0;
 };
@@ -127,6 +133,7 @@ struct fc_ctx {
   unsigned* bounds = nullptr;  // nlists x (nch + 1)
   unsigned* zmaps = nullptr;   // n_local x (nch * 32) zero maps
   unsigned* agg_support = nullptr;  // indices of agg's nonzero support (incremental decode)
+  unsigned* agg_support_next = nullptr;  // where an in-place step keeps its support (swapped after)
   uint64_t agg_support_k = 0;
   bool agg_incr = false;            // agg == densify(agg_support) and zmap 0 == its bits
   uint64_t incr_div = 80;           // in-place update when k <= G / incr_div (FC_INCR_DIV overrides)
@@ -139,6 +146,14 @@ struct fc_ctx {
   int n_small = 0;
   double small_cr = -1.0;
   uint64_t small_ktot = 0;
+  // layerwise large layers: segment tables per (worker, parity, group),
+  // pinned host copies and their device copies; rebuilt with the CR
+  fcb::SegTab* h_seg = nullptr;
+  fcb::SegTab* d_seg = nullptr;
+  int seg_groups = 0;
+  std::vector<int> seg_blocks;  // co-resident blocks of each group's launches
+  double seg_cr = -1.0;
+  uint64_t seg_ktot = 0;
   double* dnorms = nullptr;
   double* h_norms = nullptr;  // pinned
   // sticky error words (pinned, mapped into the device): set by a kernel whose
@@ -352,6 +367,125 @@ int run_select(fc_ctx* c, int i, uint64_t k, const float* ef_out = nullptr,
   return FC_OK;
 }
 
+// Segment tables of the layerwise large layers (rebuilt when the CR or the
+// selection size changes): layers in map order, groups of up to kMaxSegs;
+// in a group the co-resident blocks are split by layer length (at least one
+// each), and the layers' chunk arrays are consecutive views of the worker's.
+int build_segs(fc_ctx* c, double cr, uint64_t ktot) {
+  if (c->h_seg && c->seg_cr == cr && c->seg_ktot == ktot) return FC_OK;
+  struct Big {
+    uint64_t off, len, k, acc, soff;
+  };
+  std::vector<Big> big;
+  uint64_t acc = 0, soff = 0;
+  for (size_t l = 0; l < c->layer_off.size(); ++l) {
+    const uint64_t off = c->layer_off[l], len = c->layer_len[l], kl = k_of_host(cr, len);
+    if (len > fcb::kSmallLayerMax) {
+      big.push_back(Big{off, len, kl, acc, off % 4 ? soff : ~uint64_t(0)});
+      if (off % 4) soff += (len + 3) & ~uint64_t(3);
+    }
+    acc += kl;
+  }
+  if (soff && !c->scratch) TRY(c->alloc(&c->scratch, c->G + 4 * fcb::kMaxSegs));
+  const int ng = (int)((big.size() + fcb::kMaxSegs - 1) / fcb::kMaxSegs);
+  CUDA_TRY(cudaStreamSynchronize(c->stream));  // the previous tables are no longer read
+  if (c->h_seg) cudaFreeHost(c->h_seg);
+  c->h_seg = nullptr;
+  c->seg_groups = ng;
+  c->seg_blocks.assign(ng, 0);
+  if (ng == 0) {
+    c->seg_cr = cr;
+    c->seg_ktot = ktot;
+    return FC_OK;
+  }
+  const size_t ntab = (size_t)c->n_local * 2 * ng;
+  CUDA_TRY(cudaMallocHost(&c->h_seg, ntab * sizeof(fcb::SegTab)));
+  TRY(c->alloc(&c->d_seg, ntab));
+  const unsigned total = c->w[0].ws.ef_grid;
+  for (int i = 0; i < c->n_local; ++i) {
+    Worker& w = c->w[i];
+    if (!w.seg_ctl[0]) {
+      for (auto& cb : w.seg_ctl) {
+        TRY(c->alloc(&cb, fcb::kMaxSegs));
+        CUDA_TRY(cudaMemsetAsync(cb, 0, fcb::kMaxSegs * sizeof(fcb::Ctl), c->stream));
+      }
+      TRY(c->alloc(&w.seg_skeys, (uint64_t)fcb::kMaxSegs * fcb::kSamples));
+      TRY(c->alloc(&w.seg_lastb1, fcb::kMaxSegs));
+      CUDA_TRY(cudaMemsetAsync(w.seg_lastb1, 0, fcb::kMaxSegs * sizeof(unsigned), c->stream));
+    }
+    float* vals = reinterpret_cast<float*>(w.pack + ktot);
+    for (int g = 0; g < ng; ++g) {
+      const size_t a = (size_t)g * fcb::kMaxSegs, b = std::min(big.size(), a + fcb::kMaxSegs);
+      const int n = (int)(b - a);
+      // blocks by length: at least one each, the rest proportionally
+      uint64_t lsum = 0;
+      for (size_t q = a; q < b; ++q) lsum += big[q].len;
+      std::vector<unsigned> nb(n, 1);
+      unsigned left = total > (unsigned)n ? total - n : 0;
+      unsigned used = 0;
+      for (int q = 0; q < n; ++q) {
+        const unsigned x = (unsigned)((double)left * (double)big[a + q].len / (double)lsum);
+        nb[q] += x;
+        used += x;
+      }
+      for (unsigned r = used; r < left; ++r) {  // remainder to the largest layers' shares
+        int best = 0;
+        double worst = 0.0;
+        for (int q = 0; q < n; ++q) {
+          const double per = (double)big[a + q].len / nb[q];
+          if (per > worst) worst = per, best = q;
+        }
+        ++nb[best];
+      }
+      unsigned b0 = 0;
+      uint64_t co = 0;  // chunk offset of the layer in the worker's arrays
+      for (int p = 0; p < 2; ++p) {
+        fcb::SegTab& t = c->h_seg[((size_t)i * 2 + p) * ng + g];
+        t.n = n;
+        b0 = 0;
+        co = 0;
+        for (int q = 0; q < n; ++q) {
+          const Big& L = big[a + q];
+          fcb::SegEntry& e = t.e[q];
+          const unsigned nch = (unsigned)fcb::nchunks_of(L.len);
+          e.src = L.soff == ~uint64_t(0) ? w.ge + L.off : c->scratch + L.soff;
+          e.len = L.len;
+          e.k = L.k;
+          e.ctl = w.seg_ctl[p] + q;
+          e.ctl_next = w.seg_ctl[p ^ 1] + q;
+          e.ws = w.ws;
+          e.ws.nchunks = nch;
+          e.ws.ef_grid = nb[q];
+          e.ws.batch = fcb::ef_batch(nch, nb[q]);
+          e.ws.cnt = w.ws.cnt + co;
+          e.ws.cand_idx = w.ws.cand_idx + (co << fcb::kChunkShift);
+          e.ws.cand_val = w.ws.cand_val + (co << fcb::kChunkShift);
+          e.ws.cnorm = w.ws.cnorm + c->nch + co;
+          e.ws.segcnt = w.ws.segcnt + co;
+          e.ws.bnorm = w.ws.bnorm + b0;
+          e.ws.tblk = w.ws.tblk + 2 * (uint64_t)b0;
+          e.ws.skeys = w.seg_skeys + (uint64_t)q * fcb::kSamples;
+          e.ws.lastb1 = w.seg_lastb1 + q;
+          e.b0 = b0;
+          e.nb = nb[q];
+          e.idx_base = (unsigned)L.off;
+          e.out_idx = w.pack + L.acc;
+          e.out_val = vals + L.acc;
+          if (!fcb::select_fits(nch, nb[q], e.ws.batch))
+            return fail(FC_ERR_OUT_OF_RANGE, "layer too long for its share of the segmented select");
+          b0 += nb[q];
+          co += nch;
+        }
+      }
+      c->seg_blocks[g] = (int)b0;
+    }
+  }
+  CUDA_TRY(cudaMemcpyAsync(c->d_seg, c->h_seg, ntab * sizeof(fcb::SegTab), cudaMemcpyHostToDevice, c->stream));
+  c->seg_cr = cr;
+  c->seg_ktot = ktot;
+  return FC_OK;
+}
+
 // Layerwise Top-k (inc/compress.hpp:67-79) of worker i's error-fed gradient
 // into its pack [idx ktot | val ktot], layers in map order: every layer of
 // at most kSmallLayerMax elements in ONE launch (k_topk_small, one block per
@@ -360,8 +494,6 @@ int run_select(fc_ctx* c, int i, uint64_t k, const float* ef_out = nullptr,
 int run_layerwise(fc_ctx* c, int i, double cr, uint64_t ktot) {
   Worker& w = c->w[i];
   const int force_fb = std::getenv("FC_FORCE_FALLBACK") != nullptr ? 2 : 0;
-  fcb::ChunkWs ws = w.ws;
-  ws.cnorm = w.ws.cnorm + c->nch;  // keep the full pass's per-chunk norms
   float* vals = reinterpret_cast<float*>(w.pack + ktot);
   // the small layers' table (pinned host -> device), rebuilt when c changes
   const size_t nl = c->layer_off.size();
@@ -389,32 +521,30 @@ int run_layerwise(fc_ctx* c, int i, double cr, uint64_t ktot) {
   }
   fcb::launch_topk_small(w.ge, c->d_small, c->n_small, w.pack, vals, nullptr, c->stream);
   LAUNCHED();
-  uint64_t acc = 0;
-  for (size_t l = 0; l < nl; ++l) {
-    const uint64_t off = c->layer_off[l], len = c->layer_len[l], kl = k_of_host(cr, len);
-    if (len <= fcb::kSmallLayerMax) {
-      acc += kl;
-      continue;
+  // the large layers: segmented launches, up to kMaxSegs layers per EF
+  // emission pass + select pair (the blocks split by layer size)
+  TRY(build_segs(c, cr, ktot));
+  const int par = w.seg_par;
+  w.seg_par ^= 1;
+  {
+    uint64_t soff = 0;
+    for (size_t l = 0; l < nl; ++l) {  // slices the bulk copies cannot read in place
+      const uint64_t off = c->layer_off[l], len = c->layer_len[l];
+      if (len <= fcb::kSmallLayerMax || off % 4 == 0) continue;
+      CUDA_TRY(cudaMemcpyAsync(c->scratch + soff, w.ge + off, len * sizeof(float), cudaMemcpyDeviceToDevice,
+                               c->stream));
+      soff += (len + 3) & ~uint64_t(3);
     }
-    float* src = w.ge + off;
-    if (off % 4) {  // the EF kernel's bulk copies need 16-byte aligned rows
-      if (!c->scratch) TRY(c->alloc(&c->scratch, c->G));
-      CUDA_TRY(cudaMemcpyAsync(c->scratch, src, len * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
-      src = c->scratch;
-    }
-    fcb::Ctl* next = take_ctl(w);
-    ws.nchunks = (unsigned)fcb::nchunks_of(len);
-    ws.batch = fcb::ef_batch(ws.nchunks, ws.ef_grid);
-    int e = fcb::launch_ef(nullptr, src, len, kl, w.ctl, ws, fcb::Pending{}, 0, 1, 1 | force_fb, next,
-                           c->stream);
-    if (e) return fail(FC_ERR_CUDA, std::string("k_ef launch: ") + cudaGetErrorString(static_cast<cudaError_t>(e)));
+  }
+  const bool coop = w.ws.coop != 0;
+  for (int g = 0; g < c->seg_groups; ++g) {
+    const fcb::SegTab* tab = c->d_seg + ((size_t)i * 2 + par) * c->seg_groups + g;
+    int e = fcb::launch_ef_segs(tab, c->seg_blocks[g], 1 | force_fb, coop, c->stream);
+    if (e) return fail(FC_ERR_CUDA, std::string("k_ef (segments) launch: ") + cudaGetErrorString(static_cast<cudaError_t>(e)));
     LAUNCHED();
-    fcb::SelectMode m;
-    m.idx_base = (unsigned)off;
-    e = fcb::launch_select(kl, w.ctl, ws, src, len, w.pack + acc, vals + acc, nullptr, m, c->stream);
-    if (e) return fail(FC_ERR_CUDA, std::string("k_select launch: ") + cudaGetErrorString(static_cast<cudaError_t>(e)));
+    e = fcb::launch_select_segs(tab, c->seg_blocks[g], coop, c->stream);
+    if (e) return fail(FC_ERR_CUDA, std::string("k_select_x (segments) launch: ") + cudaGetErrorString(static_cast<cudaError_t>(e)));
     LAUNCHED();
-    acc += kl;
   }
   // ||g_c||^2 of the whole selection (gain input) into this step's control block
   fcb::launch_sumsq_fixed(vals, ktot, &w.ctl->topk_norm2, c->stream);
@@ -655,6 +785,7 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
   TRY(c->alloc(&c->bounds, nl * (c->nch + 1) + 4));  // (+4: vector pulls of a padded row)
   TRY(c->alloc(&c->zmaps, N * c->nch * 32));
   TRY(c->alloc(&c->agg_support, c->kmax));
+  TRY(c->alloc(&c->agg_support_next, c->kmax));
   CUDA_TRY(cudaMemsetAsync(c->zmaps, 0, N * c->nch * 32 * sizeof(unsigned), c->stream));
   // zero agg == densify(empty support); pipelined contexts always decode densely
   c->agg_incr = !(o->flags & (FC_FLAG_DENSE_DECODE | FC_FLAG_PIPELINE));
@@ -693,15 +824,16 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
     s.coop = (o->flags & FC_FLAG_NO_COOPERATIVE) ? 0u : 1u;
     s.batch = fcb::ef_batch(nch, ef_grid);  // packed candidate layout (EfLayout)
     TRY(c->alloc(&s.off, nch));
-    TRY(c->alloc(&s.cnt, nch));
+    TRY(c->alloc(&s.cnt, nch + fcb::kMaxSegs));
     TRY(c->alloc(&s.btot, 4096));
     TRY(c->alloc(&s.bnorm, 4096));
-    TRY(c->alloc(&s.cand_idx, (uint64_t)nch << fcb::kChunkShift));
-    TRY(c->alloc(&s.cand_val, (uint64_t)nch << fcb::kChunkShift));
-    TRY(c->alloc(&s.cnorm, 2 * (uint64_t)nch));  // [full EF pass | layer passes]
+    // (+kMaxSegs chunks: a segmented layer pass rounds every layer up to whole chunks)
+    TRY(c->alloc(&s.cand_idx, ((uint64_t)nch + fcb::kMaxSegs) << fcb::kChunkShift));
+    TRY(c->alloc(&s.cand_val, ((uint64_t)nch + fcb::kMaxSegs) << fcb::kChunkShift));
+    TRY(c->alloc(&s.cnorm, 2 * (uint64_t)nch + fcb::kMaxSegs));  // [full EF pass | layer passes]
     TRY(c->alloc(&s.g_part, 4096));
     TRY(c->alloc(&s.skeys, fcb::kSamples));
-    TRY(c->alloc(&s.segcnt, nch + 1));
+    TRY(c->alloc(&s.segcnt, nch + 1 + fcb::kMaxSegs));
     TRY(c->alloc(&s.lastb1, 1));
     CUDA_TRY(cudaMemsetAsync(s.lastb1, 0, sizeof(unsigned), c->stream));
     TRY(c->alloc(&s.tblk, 2 * (uint64_t)ef_grid));
@@ -898,6 +1030,7 @@ int fc_destroy(fc_ctx* c) {
   if (c->h_norms) cudaFreeHost(c->h_norms);
   if (c->h_err) cudaFreeHost(c->h_err);
   if (c->h_small) cudaFreeHost(c->h_small);
+  if (c->h_seg) cudaFreeHost(c->h_seg);
   for (float* q : c->f64_stage) cudaFreeHost(q);
   for (cudaEvent_t e : c->f64_ev) cudaEventDestroy(e);
   for (auto& e : c->ev)
@@ -1771,9 +1904,10 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
                               c->w[0].ctl, c->stream);
     const int wait_root = tree ? (mode == FC_STAR ? sel : -2) : -1;
     if (incr_ok && c->agg_incr) {
-      fcb::launch_agg_update_peers(c->pb, par, epoch, c->agg_support, c->agg_support_k, bsrc, k, op == FC_AVG,
-                                   (float)N, rs || tree, aggw, c->G, c->zmaps, c->agg_support, wait_root,
-                                   c->dsel, c->stream);
+      fcb::launch_agg_update_peers(c->pb, par, epoch, c->agg_support, c->agg_support_k, bsrc, k, own_bounds,
+                                   op == FC_AVG, (float)N, rs || tree, aggw, c->G, c->zmaps, c->agg_support_next,
+                                   wait_root, c->dsel, c->stream);
+      std::swap(c->agg_support, c->agg_support_next);
     } else {
       fcb::launch_decode_ar_peers(c->pb, par, epoch, bsrc, own_bounds, k, op == FC_AVG, (float)N, rs || tree,
                                   aggw, c->G, c->zmaps, wait_root, c->dsel, c->stream);
@@ -1783,8 +1917,13 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
     }
   } else if (incr_ok && c->agg_incr) {
     // in place: zero the previous support, write this one (same dense content)
-    fcb::launch_agg_update(c->agg_support, c->agg_support_k, bsrc, k, lists, nlists, lstride,
-                           op == FC_AVG, (float)N, aggw, c->G, c->zmaps, c->agg_support, c->stream);
+    if (!own_bounds) {
+      fcb::launch_bounds(bsrc, k, 0, 1, c->G, c->bounds, c->stream);
+      own_bounds = c->bounds;
+    }
+    fcb::launch_agg_update(c->agg_support, c->agg_support_k, bsrc, k, own_bounds, lists, nlists, lstride,
+                           op == FC_AVG, (float)N, aggw, c->G, c->zmaps, c->agg_support_next, c->stream);
+    std::swap(c->agg_support, c->agg_support_next);
   } else {
     if (!own_bounds) {
       fcb::launch_bounds(bsrc, k, 0, 1, c->G, c->bounds, c->stream);
@@ -1978,6 +2117,11 @@ int fc_set_layer_map(fc_ctx* c, const uint64_t* offsets, const uint64_t* lengths
     c->h_small = nullptr;  // (d_small stays in the context's allocations; a new one is made)
   }
   c->small_cr = -1.0;
+  if (c->h_seg) {
+    cudaFreeHost(c->h_seg);
+    c->h_seg = nullptr;
+  }
+  c->seg_cr = -1.0;
   c->layer_off = std::move(off);
   c->layer_len = std::move(len);
   return FC_OK;

@@ -276,18 +276,19 @@ void launch_gather(const unsigned* bidx, uint64_t k, const float* ge, float* con
 void launch_bounds(const unsigned* idx, uint64_t k, uint64_t list_stride, int nlists, uint64_t G,
                    unsigned* bounds, cudaStream_t s);
 void launch_zero_at(const unsigned* idx, uint64_t k, float* ge, cudaStream_t s);
-// Incremental AR decode: zero the previous support `prev` (kp indices), write
-// this step's k values at idx (loopback: rank-ascending sum of nlists lists),
-// keep the new support in `keep` (may alias prev); owed-zero bits follow.
-void launch_agg_update(const unsigned* prev, uint64_t kp, const unsigned* idx, uint64_t k,
+// In-place AR decode (one kernel): the previous support `prev` (kp indices)
+// zeroed, this step's k values written at idx (chunk bounds `bounds`; local:
+// rank-ascending sum of nlists lists), in whole 32-byte sectors; the new
+// support kept in `keep` (must not alias prev); owed-zero words follow.
+void launch_agg_update(const unsigned* prev, uint64_t kp, const unsigned* idx, uint64_t k, const unsigned* bounds,
                        const float* lists, int nlists, uint64_t list_stride, int divide,
                        float divisor, float* agg, uint64_t G, unsigned* zmap, unsigned* keep,
                        cudaStream_t s);
 // ... the same over the peer exchanges (values as launch_decode_ar_peers
 // reads them, after its publish waits)
 void launch_agg_update_peers(const PeerBufs& pb, int par, unsigned long long epoch, const unsigned* prev,
-                             uint64_t kp, const unsigned* idx, uint64_t k, int divide, float divisor,
-                             bool reduced, float* agg, uint64_t G, unsigned* zmap, unsigned* keep,
+                             uint64_t kp, const unsigned* idx, uint64_t k, const unsigned* bounds, int divide,
+                             float divisor, bool reduced, float* agg, uint64_t G, unsigned* zmap, unsigned* keep,
                              int wait_root, const int* dsel, cudaStream_t s);
 // Decodes also write the zero map(s) of the decoded index list(s).
 void launch_decode_ar(const unsigned* idx, const unsigned* bounds, const float* lists, int nlists,
@@ -306,6 +307,31 @@ struct SmallLayer {
   unsigned off, len, k, out;
 };
 constexpr unsigned kSmallLayerMax = 1u << 20;  // layers up to this many elements take the one-launch path
+
+// Segmented launches (layerwise compressor): one k_ef emission pass and one
+// k_select_x over several large layers at once.  Blocks [b0, b0 + nb) of the
+// launch work on segment s as if they were a whole grid of nb blocks over
+// its own slice, control block, workspace and output slot (grid barriers,
+// look-back and last-block finalisation count the segment's blocks).
+constexpr int kMaxSegs = 16;
+struct SegEntry {
+  const float* src;   // the layer's g_e (16-byte aligned)
+  uint64_t len, k;
+  Ctl* ctl;
+  Ctl* ctl_next;      // zeroed by the EF pass (the segment's next step)
+  ChunkWs ws;         // the segment's chunk arrays (offset views of the worker's)
+  unsigned b0, nb;
+  unsigned idx_base;  // the layer's offset, added to the output indices
+  unsigned* out_idx;
+  float* out_val;
+};
+struct SegTab {
+  int n;
+  SegEntry e[kMaxSegs];
+};
+int launch_ef_segs(const SegTab* d_tab, int nblocks, int opts, bool coop, cudaStream_t s);
+int launch_select_segs(const SegTab* d_tab, int nblocks, bool coop, cudaStream_t s);
+bool select_fits(unsigned nch, unsigned nblocks, unsigned batch);
 void launch_topk_small(const float* ge, const SmallLayer* layers, int nlayers, unsigned* out_idx, float* out_val,
                        double* norms, cudaStream_t s);
 int ef_grid_size();

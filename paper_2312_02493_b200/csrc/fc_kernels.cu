@@ -183,15 +183,16 @@ __device__ __forceinline__ double block_sum_array(const double* a, unsigned n, d
 }
 
 // All blocks call this at their end; true in exactly one (the last) block.
-__device__ __forceinline__ bool last_block_done(unsigned* counter) {
+__device__ __forceinline__ bool last_block_done(unsigned* counter, unsigned nblk) {
   __shared__ int s_last;
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) s_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  if (threadIdx.x == 0) s_last = (atomicAdd(counter, 1u) == nblk - 1);
   __syncthreads();
   if (s_last) __threadfence();
   return s_last;
 }
+__device__ __forceinline__ bool last_block_done(unsigned* counter) { return last_block_done(counter, gridDim.x); }
 
 // Scanning a histogram from its top bin down, find the bin b with
 //   above(b) < target <= above(b) + hist[b]
@@ -266,9 +267,10 @@ __device__ __forceinline__ void report_error(unsigned* err, int which) {
   asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(err + which), "r"(1u) : "memory");
 }
 constexpr unsigned long long kBarrierTimeoutNs = 4000000000ull;  // 4 s: blocks are not co-resident
-__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned& target, unsigned* err) {
+// (nblk: the blocks taking part -- the grid, or one segment of it)
+__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned& target, unsigned* err, unsigned nblk) {
   __syncthreads();
-  target += gridDim.x;
+  target += nblk;
   if (threadIdx.x == 0) {
     __threadfence();
     atomicAdd(ctr, 1u);
@@ -285,6 +287,9 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned& target, un
     __threadfence();
   }
   __syncthreads();
+}
+__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned& target, unsigned* err) {
+  grid_barrier(ctr, target, err, gridDim.x);
 }
 
 // System-scope epoch flags of the peer exchange (written over NVLink by the
@@ -367,7 +372,7 @@ __device__ __forceinline__ double sample_target(uint64_t G, uint64_t k) {
 }
 
 #define EF_MARK(i) \
-  if (blockIdx.x == 0 && threadIdx.x == 0) ctl->tphase_ef[i] = gtimer()
+  if (bid == 0 && threadIdx.x == 0) ctl->tphase_ef[i] = gtimer()
 
 // ---------------------------------------------------------- error feedback ---
 // g_e = g_o + residual, written in place over the residual (12 B/element):
@@ -436,15 +441,30 @@ __device__ __forceinline__ void fence_proxy_async() {
 // barrier between sampling and streaming); bit 1: force the
 // fallback (tests).  ctl_next (nullable): the worker's other control block,
 // zeroed here for the next step.
-template <bool kAdd, bool kEmit, bool kPend>
+template <bool kAdd, bool kEmit, bool kPend, bool kSeg = false>
 __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_o,
                                                     float* __restrict__ ge, uint64_t G, uint64_t k,
                                                     Ctl* __restrict__ ctl, ChunkWs w, Pending pz,
-                                                    int opts, Ctl* __restrict__ ctl_next) {
+                                                    int opts, Ctl* __restrict__ ctl_next,
+                                                    const SegTab* __restrict__ seg) {
   pdl_wait();
   extern __shared__ __align__(128) unsigned char s_ring[];
+  unsigned bid = blockIdx.x, nblk = gridDim.x;  // this block within its (segment's) grid
+  if (kSeg) {
+    int si = 0;
+    while (si + 1 < seg->n && blockIdx.x >= seg->e[si + 1].b0) ++si;
+    const SegEntry& se = seg->e[si];
+    bid = blockIdx.x - se.b0;
+    nblk = se.nb;
+    ge = const_cast<float*>(se.src);
+    G = se.len;
+    k = se.k;
+    ctl = se.ctl;
+    ctl_next = se.ctl_next;
+    w = se.ws;
+  }
   EF_MARK(0);
-  if (threadIdx.x == 0) w.tblk[2 * blockIdx.x] = gtimer();
+  if (threadIdx.x == 0) w.tblk[2 * bid] = gtimer();
   __shared__ unsigned s_hist[kEmit ? kBins1 : 1];  // sample histogram, then the bound's staging
   __shared__ unsigned s_sub[kEmit ? kSpecBins * 256 : 1];  // speculative level-2 histograms
   __shared__ __align__(8) unsigned long long s_bar[kEfWarps][kEfStages];
@@ -459,7 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
   }
   if (ctl_next) {
     unsigned* z = reinterpret_cast<unsigned*>(ctl_next);
-    for (unsigned q = blockIdx.x * kThreads + tid; q < sizeof(Ctl) / 4; q += gridDim.x * kThreads) z[q] = 0u;
+    for (unsigned q = bid * kThreads + tid; q < sizeof(Ctl) / 4; q += nblk * kThreads) z[q] = 0u;
   }
   const bool sampling = kEmit && (opts & 1);
   const unsigned lastb1 = sampling ? __ldcg(w.lastb1) : 0u;  // previous step's target bucket + 1 (0: none)
@@ -473,7 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
     if (kAdd) v = __fadd_rn(g_o[i], v);
     return v;
   };
-  const unsigned q0 = blockIdx.x * kThreads + tid, qstride = gridDim.x * kThreads;
+  const unsigned q0 = bid * kThreads + tid, qstride = nblk * kThreads;
   float sv = 0.f;
   if (sampling && q0 < (unsigned)kSamples) sv = sample_at(q0);
 
@@ -553,15 +573,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
         add_sample(kq);
       }
       __syncthreads();
-      if (blockIdx.x == 0 && threadIdx.x == 0) ctl->tphase_ef2[0] = gtimer();
+      if (bid == 0 && threadIdx.x == 0) ctl->tphase_ef2[0] = gtimer();
       for (int b = tid; b < kBins1; b += kThreads)
         if (s_hist[b]) atomicAdd(&ctl->hist_s[b], s_hist[b]);
       if (lastb1)
         for (int b = tid; b < kSpecBins * 256; b += kThreads)
           if (s_sub[b]) atomicAdd(&ctl->hist_s2w[b], s_sub[b]);
-      if (blockIdx.x == 0 && threadIdx.x == 0) ctl->tphase_ef2[1] = gtimer();
+      if (bid == 0 && threadIdx.x == 0) ctl->tphase_ef2[1] = gtimer();
       unsigned bar = 0;
-      grid_barrier(&ctl->bar_ef, bar, w.err);
+      grid_barrier(&ctl->bar_ef, bar, w.err, nblk);
       EF_MARK(1);
       const double target = sample_target(G, k);
       if (opts & 2) {
@@ -590,7 +610,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
             f2 = block_select_top<kThreads>(s_hist, 256, tgt - above1, b2, above2, s_hist);
           }
           Lkey = (b1 << kShift1) | ((f2 ? b2 : 0u) << 11);
-          if (blockIdx.x == 0 && tid == 0) *w.lastb1 = b1 + 1u;  // (every block read it before the barrier)
+          if (bid == 0 && tid == 0) *w.lastb1 = b1 + 1u;  // (every block read it before the barrier)
         } else {
           Lkey = 0u;
         }
@@ -598,9 +618,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
         Lkey = 0u;
       }
       EF_MARK(2);
-      if (blockIdx.x == 0 && tid == 0) ctl->Lkey = Lkey;
+      if (bid == 0 && tid == 0) ctl->Lkey = Lkey;
     } else if (opts & 4) {  // every element is a candidate
-      if (blockIdx.x == 0 && tid == 0) ctl->Lkey = 0;
+      if (bid == 0 && tid == 0) ctl->Lkey = 0;
       Lkey = 0u;
     } else {
       Lkey = *(volatile unsigned*)&ctl->Lkey;
@@ -721,7 +741,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
 
   if (kEmit && lane == 0 && ncand) atomicAdd(&ctl->cand_count, ncand);
   EF_MARK(3);
-  if (threadIdx.x == 0) w.tblk[2 * blockIdx.x + 1] = gtimer();
+  if (threadIdx.x == 0) w.tblk[2 * bid + 1] = gtimer();
   // ||g_e||^2 is reduced from w.cnorm when asked for (launch_sum_fixed); a
   // candidate set smaller than k (sampled bound missed) is detected by k_select
 }
@@ -736,9 +756,33 @@ static int launch_ef_t(const float* g_o, float* ge, uint64_t G, uint64_t k, Ctl*
     attr = true;
   }
   ChunkWs ws = w;
-  void* args[] = {&g_o, &ge, &G, &k, &ctl, &ws, &pz, &opts, &ctl_next};
+  const SegTab* seg = nullptr;
+  void* args[] = {&g_o, &ge, &G, &k, &ctl, &ws, &pz, &opts, &ctl_next, &seg};
   return (int)launch_grid_sync((const void*)k_ef<A, E, P>, dim3(w.ef_grid), dim3(kThreads), kEfRingBytes, s,
                                args, w.coop != 0);
+}
+
+// Segmented emission pass (no residual add, no owed zeros): d_tab's
+// segments over `nblocks` co-resident blocks.
+int launch_ef_segs(const SegTab* d_tab, int nblocks, int opts, bool coop, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_ef<false, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kEfRingBytes);
+    attr = true;
+  }
+  const float* g_o = nullptr;
+  float* ge = nullptr;
+  uint64_t G = 0, k = 0;
+  Ctl* ctl = nullptr;
+  ChunkWs ws{};
+  Pending pz{};
+  Ctl* ctl_next = nullptr;
+  void* args[] = {&g_o, &ge, &G, &k, &ctl, &ws, &pz, &opts, &ctl_next, &d_tab};
+  const int e = (int)launch_grid_sync((const void*)k_ef<false, true, false, true>, dim3(nblocks), dim3(kThreads),
+                                      kEfRingBytes, s, args, coop);
+  count_launch();
+  return e;
 }
 
 int ef_grid_size() { return num_sms(); }
@@ -1482,7 +1526,9 @@ constexpr int kSxWarps = kSxThreads / 32;
 constexpr unsigned kSxListCap = kSelBins / 2;  // u32 entries in the upper half of s_h
 
 #define SX_MARK(i) \
-  if (blockIdx.x == 0 && threadIdx.x == 0) ctl->tphase_sx[i] = gtimer()
+  if (bid == 0 && threadIdx.x == 0) ctl->tphase_sx[i] = gtimer()
+#define SXP_MARK(i) \
+  if (bid == 0 && threadIdx.x == 0) ctl->tphase[i] = gtimer()
 
 // Block -> chunk ranges of the select.  Blocks [0, nbA) own whole batches
 // of the aligned region [0, bnd) (cpbA chunks each, a multiple of B); blocks
@@ -1530,12 +1576,32 @@ __device__ __forceinline__ unsigned u4c(const uint4& v, int e) {
   return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
 }
 
+template <bool kSeg = false>
 __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __restrict__ ctl, ChunkWs w,
                                                             const float* __restrict__ ef_out, uint64_t G,
                                                             unsigned* __restrict__ out_idx,
                                                             float* __restrict__ out_val,
-                                                            unsigned* __restrict__ bounds_out, SelectMode mode) {
+                                                            unsigned* __restrict__ bounds_out, SelectMode mode,
+                                                            const SegTab* __restrict__ seg) {
   pdl_wait();
+  unsigned bid = blockIdx.x, nblk = gridDim.x;  // this block within its (segment's) grid
+  if (kSeg) {
+    int si = 0;
+    while (si + 1 < seg->n && blockIdx.x >= seg->e[si + 1].b0) ++si;
+    const SegEntry& se = seg->e[si];
+    bid = blockIdx.x - se.b0;
+    nblk = se.nb;
+    k = se.k;
+    ctl = se.ctl;
+    w = se.ws;
+    ef_out = se.src;
+    G = se.len;
+    out_idx = se.out_idx;
+    out_val = se.out_val;
+    bounds_out = nullptr;
+    mode = SelectMode{};
+    mode.idx_base = se.idx_base;
+  }
   extern __shared__ __align__(16) unsigned char s_dyn[];
   __shared__ __align__(16) unsigned s_h[kSelBins];
   __shared__ unsigned long long s_red[kSxWarps];
@@ -1547,12 +1613,12 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned lt = lanemask_lt();
   unsigned bar = 0;  // grid barrier target (ctl->bar_sel)
-  SEL_MARK(0);
+  SXP_MARK(0);
   const unsigned nch = w.nchunks;
   const EfLayout lay(nch, w.batch);
-  const SxGeom geo(nch, gridDim.x, lay);
+  const SxGeom geo(nch, nblk, lay);
   unsigned c0, c1;
-  geo.range(blockIdx.x, nch, lay.bnd, c0, c1);
+  geo.range(bid, nch, lay.bnd, c0, c1);
   const unsigned al_end = min(c1, lay.bnd);
   const unsigned nal = c0 < al_end ? (al_end - c0 + lay.B - 1) / lay.B : 0u;
   const unsigned sg0 = max(c0, lay.bnd);
@@ -1581,28 +1647,28 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
   const bool fb = M < k;
   unsigned Lb = fb ? 0u : Lk0;  // every candidate has key >= Lb
   if (fb) {
-    if (blockIdx.x == 0 && tid == 0) ctl->fallback = 1;
+    if (bid == 0 && tid == 0) ctl->fallback = 1;
     for (int b = tid; b < kBins1; b += kSxThreads) s_h[b] = 0;
     __syncthreads();
     const uint64_t n4 = G / 4;
     const float4* src4 = reinterpret_cast<const float4*>(ef_out);
-    for (uint64_t i = blockIdx.x * (uint64_t)kSxThreads + tid; i < n4; i += (uint64_t)gridDim.x * kSxThreads) {
+    for (uint64_t i = bid * (uint64_t)kSxThreads + tid; i < n4; i += (uint64_t)nblk * kSxThreads) {
       const float4 x = __ldcg(src4 + i);
       atomicAdd(&s_h[key_of(x.x) >> kShift1], 1u);
       atomicAdd(&s_h[key_of(x.y) >> kShift1], 1u);
       atomicAdd(&s_h[key_of(x.z) >> kShift1], 1u);
       atomicAdd(&s_h[key_of(x.w) >> kShift1], 1u);
     }
-    if (blockIdx.x == 0) {
+    if (bid == 0) {
       for (uint64_t i = n4 * 4 + tid; i < G; i += kSxThreads) atomicAdd(&s_h[key_of(ef_out[i]) >> kShift1], 1u);
     }
     flush_hist(s_h, ctl->hist_fb, kBins1);
-    grid_barrier(&ctl->bar_sel, bar, w.err);
+    grid_barrier(&ctl->bar_sel, bar, w.err, nblk);
     unsigned bin;
     unsigned long long above;
     block_select_top<kSxThreads>(ctl->hist_fb, kBins1, k, bin, above, s_h);
     const unsigned Lk = bin << kShift1;
-    if (blockIdx.x == 0 && tid == 0) ctl->Lkey = Lk;
+    if (bid == 0 && tid == 0) ctl->Lkey = Lk;
     // re-emit this block's segments in the packed layout (warp per segment)
     for (unsigned j = warp; j < S; j += kSxWarps) {
       const unsigned a = seg_c0(j), e = seg_c1(j);
@@ -1764,11 +1830,11 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
   });
   SX_MARK(0);
   __syncthreads();
-  if (tid == 0) reinterpret_cast<unsigned long long*>(w.g_part)[2048 + 2 * blockIdx.x] = gtimer();  // (diagnostics)
+  if (!kSeg && tid == 0) reinterpret_cast<unsigned long long*>(w.g_part)[2048 + 2 * bid] = gtimer();  // (diagnostics)
   flush_hist(s_h, ctl->hist_w, kSelBins);
   SX_MARK(1);
-  grid_barrier(&ctl->bar_sel, bar, w.err);
-  SEL_MARK(1);
+  grid_barrier(&ctl->bar_sel, bar, w.err, nblk);
+  SXP_MARK(1);
   {
     unsigned bin;
     unsigned long long above;
@@ -1779,7 +1845,7 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
       prefix = wb + bin;
     }
   }
-  SEL_MARK(2);
+  SXP_MARK(2);
   unsigned T = 0;
   unsigned long long needT = 0;
   bool counted = false;  // per-warp (gt, eq) in s_wgt / s_weq
@@ -1810,10 +1876,10 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
     }
     SX_MARK(2);
     __syncthreads();
-    if (tid == 0) reinterpret_cast<unsigned long long*>(w.g_part)[2048 + 2 * blockIdx.x + 1] = gtimer();
+    if (!kSeg && tid == 0) reinterpret_cast<unsigned long long*>(w.g_part)[2048 + 2 * bid + 1] = gtimer();
     flush_hist(s_h, ctl->hist3, 2048);
-    grid_barrier(&ctl->bar_sel, bar, w.err);
-    SEL_MARK(3);
+    grid_barrier(&ctl->bar_sel, bar, w.err, nblk);
+    SXP_MARK(3);
     unsigned bin;
     unsigned long long above;
     block_select_top<kSxThreads>(ctl->hist3, 2048, need, bin, above, s_h);
@@ -1846,7 +1912,7 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
         }
       });
       flush_hist(s_h, ghs[d], nb);
-      grid_barrier(&ctl->bar_sel, bar, w.err);
+      grid_barrier(&ctl->bar_sel, bar, w.err, nblk);
       unsigned bin;
       unsigned long long above;
       block_select_top<kSxThreads>(ghs[d], nb, need, bin, above, s_h);
@@ -1854,7 +1920,7 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
       prefix = (prefix << widths[d]) | bin;
       as = sh;
     }
-    SEL_MARK(3);
+    SXP_MARK(3);
   }
   T = prefix;
   needT = need;
@@ -1886,12 +1952,12 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
   __syncthreads();
   const unsigned long long btot = s_wpre[kSxWarps];
   if (tid == 0) {
-    ctl->lb_tot[blockIdx.x] = btot;
+    ctl->lb_tot[bid] = btot;
     __threadfence();
-    atomicExch(&ctl->lb_flag[blockIdx.x], 1u);
+    atomicExch(&ctl->lb_flag[bid], 1u);
   }
   unsigned long long mine = 0;
-  if (tid < (int)blockIdx.x) {
+  if (tid < (int)bid) {
     if (ld_acquire(&ctl->lb_flag[tid]) == 0u) {
       const unsigned long long t0 = gtimer();
       while (ld_acquire(&ctl->lb_flag[tid]) == 0u) {
@@ -1905,7 +1971,7 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
     mine = __ldcg(&ctl->lb_tot[tid]);
   }
   const unsigned long long bp = block_sum_u64<kSxThreads>(mine, s_red);
-  SEL_MARK(4);
+  SXP_MARK(4);
   const unsigned long long bgt_pre = bp >> 32, beq_pre = bp & 0xffffffffull;
   const unsigned long long avail = needT > beq_pre ? needT - beq_pre : 0ull;  // ties this block may keep
   const unsigned long long obase = bgt_pre + min(beq_pre, needT);
@@ -1990,7 +2056,7 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
     });
   }
   __syncthreads();
-  SEL_MARK(5);
+  SXP_MARK(5);
   if (staged)
     for (unsigned i = tid; i < nsel; i += kSxThreads) {
       out_idx[obase + i] = s_oidx[i];
@@ -2026,13 +2092,13 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
   SX_MARK(5);
   const double bsum = block_sum<kSxThreads>(acc, s_dred);
   if (tid == 0) {
-    w.bnorm[blockIdx.x] = bsum;
+    w.bnorm[bid] = bsum;
     if (mode.publish) __threadfence_system();  // this block's output before the publish
   }
   pdl_trigger();
-  SEL_MARK(6);
-  if (!last_block_done(&ctl->done_sel)) return;
-  const double tot = block_sum_array<kSxThreads>(w.bnorm, gridDim.x, s_dred);
+  SXP_MARK(6);
+  if (!last_block_done(&ctl->done_sel, nblk)) return;
+  const double tot = block_sum_array<kSxThreads>(w.bnorm, nblk, s_dred);
   if (tid == 0) {
     ctl->topk_norm2 = tot;
     ctl->T = T;
@@ -2048,7 +2114,7 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
       if (mode.publish_contrib) publish_all(mode.pb, 1, mode.epoch);
     }
   }
-  SEL_MARK(7);
+  SXP_MARK(7);
 }
 
 // Grid of the select: one resident 1024-thread block per SM.
@@ -2059,18 +2125,19 @@ int launch_select(uint64_t k, Ctl* ctl, const ChunkWs& w, const float* ef_out, u
   if (grid > kMaxGrid) return (int)cudaErrorInvalidValue;
   ChunkWs ws = w;
   SelectMode mode = m;
-  void* args[] = {&k, &ctl, &ws, &ef_out, &G, &out_idx, &out_val, &bounds_out, &mode};
+  const SegTab* seg = nullptr;
+  void* args[] = {&k, &ctl, &ws, &ef_out, &G, &out_idx, &out_val, &bounds_out, &mode, &seg};
   cudaError_t e;
   if (m.rounds == 0) {
     // exact Top-k: k_select_x over the packed candidate layout
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_select_x, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelSmemMax);
+      cudaFuncSetAttribute(k_select_x<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelSmemMax);
       attr = true;
     }
     const unsigned cpb = SxGeom(w.nchunks, grid, EfLayout(w.nchunks, w.batch)).max_chunks();
     if (2ull * cpb + 8 > kSelSmemMax / 4) return (int)cudaErrorInvalidValue;
-    e = launch_grid_sync((const void*)k_select_x, dim3(grid), dim3(kSxThreads), kSelSmemMax, s, args,
+    e = launch_grid_sync((const void*)k_select_x<false>, dim3(grid), dim3(kSxThreads), kSelSmemMax, s, args,
                          w.coop != 0);
   } else {
     // threshold compressor: k_select (bisection), per-chunk candidate slots
@@ -2087,6 +2154,35 @@ int launch_select(uint64_t k, Ctl* ctl, const ChunkWs& w, const float* ef_out, u
     // barriers (grid_barrier); cooperative unless the context opted out
     e = launch_grid_sync((const void*)k_select, dim3(grid), dim3(kSelThreads), smem, s, args, w.coop != 0);
   }
+  count_launch();
+  return e == cudaSuccess ? 0 : (int)e;
+}
+
+// The select's per-block position table fits shared memory for this split.
+bool select_fits(unsigned nch, unsigned nblocks, unsigned batch) {
+  const unsigned cpb = SxGeom(nch, nblocks, EfLayout(nch, batch)).max_chunks();
+  return 2ull * cpb + 8 <= kSelSmemMax / 4;
+}
+
+// Segmented exact select (layerwise compressor): d_tab's segments over
+// `nblocks` co-resident blocks, one launch.
+int launch_select_segs(const SegTab* d_tab, int nblocks, bool coop, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_select_x<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSelSmemMax);
+    attr = true;
+  }
+  uint64_t k = 0, G = 0;
+  Ctl* ctl = nullptr;
+  ChunkWs ws{};
+  const float* ef_out = nullptr;
+  unsigned* out_idx = nullptr;
+  float* out_val = nullptr;
+  unsigned* bounds_out = nullptr;
+  SelectMode mode{};
+  void* args[] = {&k, &ctl, &ws, &ef_out, &G, &out_idx, &out_val, &bounds_out, &mode, &d_tab};
+  const cudaError_t e = launch_grid_sync((const void*)k_select_x<true>, dim3(nblocks), dim3(kSxThreads),
+                                         kSelSmemMax, s, args, coop);
   count_launch();
   return e == cudaSuccess ? 0 : (int)e;
 }
@@ -2508,59 +2604,45 @@ void launch_gather(const unsigned* bidx, uint64_t k, const float* ge, float* con
 
 // ------------------------------------------------------ incremental decode ---
 // The dense aggregate buffer is library-owned, so after the first full decode
-// it can be kept equal to densify(this step) by touching only the supports:
-// (1) every 32-byte sector holding a previous index is zeroed and every owed-
-// zero word holding one cleared, (2) every sector holding a new index is
-// rewritten whole (its new values, zeros elsewhere) and every owed-zero word
-// holding one rewritten.  Each sector / word is written by the thread of its
-// first list entry (the lists are sorted), so all writes are plain full-
-// sector stores -- no atomics, and no partial sectors for the memory system
-// to merge.  For k << G this replaces the 4G-byte dense write with ~2 x 32k
-// bytes; the buffer content is identical to a full decode.
-template <int kA>
-__device__ __forceinline__ void st_atom(float* __restrict__ agg, uint64_t b, const float (&v)[kA], uint64_t G) {
-  if (b + kA <= G) {
+// it can be kept equal to densify(this step) by touching only the supports,
+// in ONE kernel whose threads own disjoint 32-byte sectors / owed-zero words:
+//   * a thread of this step's list whose entry is the first in its sector
+//     writes the whole sector (its entries' values, zeros elsewhere); the
+//     first in its owed-zero word writes the whole word;
+//   * a thread of the previous step's list whose entry is the first in its
+//     sector (word) zeroes the sector (word) -- unless this step's list has an
+//     entry there (found among this step's entries of the same chunk, via
+//     the chunk bounds), whose thread writes it instead.
+// Every write is a plain full-sector (full-word) store, no atomics, no order
+// between the two lists.  For k << G this replaces the 4G-byte dense write
+// with ~2 x 32k bytes; the buffer content is identical to a full decode.
+constexpr int kAggAtom = 8;  // floats per write: measured against 16 and 32
+
+__device__ __forceinline__ void st_sector(float* __restrict__ agg, uint64_t b, const float (&v)[kAggAtom],
+                                          uint64_t G) {
+  if (b + kAggAtom <= G) {
     float4* p = reinterpret_cast<float4*>(agg + b);
-#pragma unroll
-    for (int q = 0; q < kA / 4; ++q) p[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    p[0] = make_float4(v[0], v[1], v[2], v[3]);
+    p[1] = make_float4(v[4], v[5], v[6], v[7]);
   } else {
 #pragma unroll
-    for (int e = 0; e < kA; ++e)
+    for (int e = 0; e < kAggAtom; ++e)
       if (b + e < G) agg[b + e] = v[e];
-  }
-}
-
-template <int kA>
-__global__ void k_agg_clear(const unsigned* __restrict__ prev, uint64_t kp, float* __restrict__ agg,
-                            unsigned* __restrict__ zmap, uint64_t G) {
-  pdl_wait();
-  constexpr unsigned kSh = kA == 8 ? 3 : kA == 16 ? 4 : 5;
-  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < kp;
-       j += (uint64_t)gridDim.x * blockDim.x) {
-    const unsigned i = __ldcs(prev + j);
-    const unsigned ip = j ? __ldcs(prev + j - 1) : 0u;
-    if (j == 0 || (ip >> kSh) != (i >> kSh)) {
-      float z[kA];
-#pragma unroll
-      for (int e = 0; e < kA; ++e) z[e] = 0.f;
-      st_atom<kA>(agg, (uint64_t)(i & ~(kA - 1u)), z, G);
-    }
-    if (j == 0 || zmap_word(ip) != zmap_word(i)) zmap[zmap_word(i)] = 0u;
   }
 }
 
 // kPeers as in k_decode_ar: 0 local lists, 1 two-rank direct sum (own
 // contribution + the peer's in the inbox), 2 the reduced list (reduce-scatter
 // or tree root), after the same publish waits.
-template <int kPeers, int kA>
-__global__ void k_agg_write(const unsigned* __restrict__ idx, uint64_t k,
-                            const float* __restrict__ lists, int nlists, uint64_t list_stride,
-                            int divide, float divisor, float* __restrict__ agg,
-                            unsigned* __restrict__ zmap, unsigned* __restrict__ keep, uint64_t G,
-                            PeerBufs pb, int par, unsigned long long epoch, int wait_root,
-                            const int* __restrict__ dsel) {
+template <int kPeers>
+__global__ void k_agg_update(const unsigned* __restrict__ prev, uint64_t kp, const unsigned* __restrict__ idx,
+                             uint64_t k, const unsigned* __restrict__ bounds,
+                             const float* __restrict__ lists, int nlists, uint64_t list_stride,
+                             int divide, float divisor, float* __restrict__ agg,
+                             unsigned* __restrict__ zmap, unsigned* __restrict__ keep, uint64_t G,
+                             PeerBufs pb, int par, unsigned long long epoch, int wait_root,
+                             const int* __restrict__ dsel) {
   pdl_wait();
-  constexpr unsigned kSh = kA == 8 ? 3 : kA == 16 ? 4 : 5;
   if (kPeers) {
     if (wait_root == -1) {
       if (!wait_all(pb, kPeers, epoch)) return;  // timeout reported
@@ -2583,28 +2665,51 @@ __global__ void k_agg_write(const unsigned* __restrict__ idx, uint64_t k,
     }
     return divide ? v / divisor : v;
   };
-  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < k;
-       j += (uint64_t)gridDim.x * blockDim.x) {
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < kp + k;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    if (t < kp) {  // the previous support
+      const uint64_t j = t;
+      const unsigned i = __ldcs(prev + j);
+      const unsigned ip = j ? __ldcs(prev + j - 1) : 0u;
+      const bool fs = j == 0 || (ip >> 3) != (i >> 3);
+      const bool fw = j == 0 || zmap_word(ip) != zmap_word(i);
+      if (!fs && !fw) continue;
+      // this step's entries in the same chunk (sorted): any in the sector / word?
+      const unsigned c = i >> kChunkShift;
+      const unsigned lo = __ldg(bounds + c), hi = __ldg(bounds + c + 1);
+      bool ins = false, inw = false;
+      for (unsigned q = lo; q < hi; ++q) {
+        const unsigned m = __ldg(idx + q);
+        if (m > (i | 31u)) break;
+        inw |= zmap_word(m) == zmap_word(i);
+        ins |= (m >> 3) == (i >> 3);
+      }
+      if (fs && !ins) {
+        const float z[kAggAtom] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        st_sector(agg, (uint64_t)(i & ~7u), z, G);
+      }
+      if (fw && !inw) zmap[zmap_word(i)] = 0u;
+      continue;
+    }
+    const uint64_t j = t - kp;  // this step's list
     const unsigned i = idx[j];
     const unsigned ip = j ? idx[j - 1] : 0u;
     keep[j] = i;  // the support the next step clears
-    if (j == 0 || (ip >> kSh) != (i >> kSh)) {
-      // this atom's entries are j, j+1, ... (at most kA)
-      float v[kA];
-#pragma unroll
-      for (int e = 0; e < kA; ++e) v[e] = 0.f;
+    if (j == 0 || (ip >> 3) != (i >> 3)) {
+      // this sector's entries are j, j+1, ... (at most 8)
+      float v[kAggAtom] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       unsigned m = i;
-      for (uint64_t q = j; q < k && q < j + kA; ++q) {
+      for (uint64_t q = j; q < k && q < j + kAggAtom; ++q) {
         if (q > j) {
           m = idx[q];
-          if ((m >> kSh) != (i >> kSh)) break;
+          if ((m >> 3) != (i >> 3)) break;
         }
         const float x = value(q);
 #pragma unroll
-        for (int e = 0; e < kA; ++e)
-          if ((m & (kA - 1u)) == (unsigned)e) v[e] = x;
+        for (int e = 0; e < kAggAtom; ++e)
+          if ((m & (kAggAtom - 1u)) == (unsigned)e) v[e] = x;
       }
-      st_atom<kA>(agg, (uint64_t)(i & ~(kA - 1u)), v, G);
+      st_sector(agg, (uint64_t)(i & ~7u), v, G);
     }
     if (j == 0 || zmap_word(ip) != zmap_word(i)) {
       unsigned bits = zmap_bit(i);
@@ -2622,47 +2727,27 @@ static unsigned agg_grid(uint64_t n) {
   return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + kThreads - 1) / kThreads, num_sms() * 16ull));
 }
 
-// The in-place update writes whole 32-byte sectors: measured against 64- and
-// 128-byte granules (C3, CR 0.003 / 0.01 / 0.02: 0.350 / 0.408 / 0.479 ms per
-// step vs 0.362 / 0.441 / 0.545 and 0.412 / 0.556 / 0.699), the extra bytes
-// of a wider granule cost more than its fewer, larger writes save.
-constexpr int kAggAtom = 8;
-
-static void agg_update(const PeerBufs& pb, int peers, int par, unsigned long long epoch, const unsigned* prev,
-                       uint64_t kp, const unsigned* idx, uint64_t k, const float* lists, int nlists,
-                       uint64_t list_stride, int divide, float divisor, float* agg, uint64_t G, unsigned* zmap,
-                       unsigned* keep, int wait_root, const int* dsel, cudaStream_t s) {
-  if (kp) {
-    launch_pdl(k_agg_clear<kAggAtom>, agg_grid(kp), kThreads, 0, s, prev, kp, agg, zmap, G);
-    count_launch();
-  }
-  if (peers == 0)
-    launch_pdl(k_agg_write<0, kAggAtom>, agg_grid(k), kThreads, 0, s, idx, k, lists, nlists, list_stride, divide,
-               divisor, agg, zmap, keep, G, pb, par, epoch, wait_root, dsel);
-  else if (peers == 1)
-    launch_pdl(k_agg_write<1, kAggAtom>, agg_grid(k), kThreads, 0, s, idx, k, lists, nlists, list_stride, divide,
-               divisor, agg, zmap, keep, G, pb, par, epoch, wait_root, dsel);
-  else
-    launch_pdl(k_agg_write<2, kAggAtom>, agg_grid(k), kThreads, 0, s, idx, k, lists, nlists, list_stride, divide,
-               divisor, agg, zmap, keep, G, pb, par, epoch, wait_root, dsel);
-  count_launch();
-}
-
-void launch_agg_update(const unsigned* prev, uint64_t kp, const unsigned* idx, uint64_t k,
+void launch_agg_update(const unsigned* prev, uint64_t kp, const unsigned* idx, uint64_t k, const unsigned* bounds,
                        const float* lists, int nlists, uint64_t list_stride, int divide,
                        float divisor, float* agg, uint64_t G, unsigned* zmap, unsigned* keep,
                        cudaStream_t s) {
-  agg_update(PeerBufs{}, 0, 0, 0ull, prev, kp, idx, k, lists, nlists, list_stride, divide, divisor, agg, G, zmap,
-             keep, -1, nullptr, s);
+  launch_pdl(k_agg_update<0>, agg_grid(kp + k), kThreads, 0, s, prev, kp, idx, k, bounds, lists, nlists,
+             list_stride, divide, divisor, agg, zmap, keep, G, PeerBufs{}, 0, 0ull, -1, (const int*)nullptr);
+  count_launch();
 }
 
 void launch_agg_update_peers(const PeerBufs& pb, int par, unsigned long long epoch, const unsigned* prev,
-                             uint64_t kp, const unsigned* idx, uint64_t k, int divide, float divisor,
-                             bool reduced, float* agg, uint64_t G, unsigned* zmap, unsigned* keep,
+                             uint64_t kp, const unsigned* idx, uint64_t k, const unsigned* bounds, int divide,
+                             float divisor, bool reduced, float* agg, uint64_t G, unsigned* zmap, unsigned* keep,
                              int wait_root, const int* dsel, cudaStream_t s) {
   // (N = 2 direct sums never take a tree root: wait_root is -1 there)
-  agg_update(pb, reduced ? 2 : 1, par, epoch, prev, kp, idx, k, nullptr, pb.n, k, reduced ? 0 : divide,
-             reduced ? 1.0f : divisor, agg, G, zmap, keep, reduced ? wait_root : -1, dsel, s);
+  if (reduced)
+    launch_pdl(k_agg_update<2>, agg_grid(kp + k), kThreads, 0, s, prev, kp, idx, k, bounds, (const float*)nullptr,
+               pb.n, k, 0, 1.0f, agg, zmap, keep, G, pb, par, epoch, wait_root, dsel);
+  else
+    launch_pdl(k_agg_update<1>, agg_grid(kp + k), kThreads, 0, s, prev, kp, idx, k, bounds, (const float*)nullptr,
+               pb.n, k, divide, divisor, agg, zmap, keep, G, pb, par, epoch, -1, (const int*)nullptr);
+  count_launch();
 }
 
 // Materialise owed zeros (before the residual store is read from outside).
@@ -3318,8 +3403,7 @@ void launch_dense_sum(const float* lists, int nlists, uint64_t list_stride, int 
 // consecutive kernels costs an SM drain at each boundary.
 static void prefer_max_smem() {
   const void* fs[] = {(const void*)k_fill_synth, (const void*)k_gather,
-                      (const void*)k_agg_clear<kAggAtom>, (const void*)k_agg_write<0, kAggAtom>,
-                      (const void*)k_agg_write<1, kAggAtom>, (const void*)k_agg_write<2, kAggAtom>,
+                      (const void*)k_agg_update<0>, (const void*)k_agg_update<1>, (const void*)k_agg_update<2>,
                       (const void*)k_zero_at, (const void*)k_bounds,
                       (const void*)k_decode_ar<0>, (const void*)k_decode_ar<1>, (const void*)k_decode_ar<2>, (const void*)k_decode_ag, (const void*)k_decode_ag_n<1>, (const void*)k_decode_ag_n<2>,
                       (const void*)k_decode_ag_n<4>, (const void*)k_decode_ag_n<8>, (const void*)k_dense_sum,

@@ -70,6 +70,26 @@ def test_layerwise_small_and_large_layers(fc, f32):
     run_traj(fc, f32, 2, g, fc.LAYERWISE, [0.01, 0.001, 0.1], layers, dist=1, seed=77, max_cr=0.1)
 
 
+def test_layerwise_segment_groups(fc, f32, monkeypatch):
+    """More large layers than one segmented launch holds (kMaxSegs = 16):
+    two EF-emission + select groups; large layers at offsets that are not
+    16-byte aligned (staged through scratch), uneven lengths (the block split
+    by size), small layers between them; then the same with the sampled
+    bound forced to miss (every segment's select falls back)."""
+    rng = np.random.default_rng(5)
+    layers, off = [], 0
+    for q in range(19):
+        m = int(rng.integers(1_048_577, 1_600_000)) if q != 7 else 5_000_003
+        layers.append((off, m))
+        off += m
+        if q % 3 == 0:  # a small layer in between (shifts the next offset off 4-alignment)
+            layers.append((off, 3 + q))
+            off += 3 + q
+    run_traj(fc, f32, 1, off, fc.LAYERWISE, [0.01, 0.002], layers, seed=21, max_cr=0.05)
+    monkeypatch.setenv("FC_FORCE_FALLBACK", "1")
+    run_traj(fc, f32, 1, off, fc.LAYERWISE, [0.01], layers[:9], seed=22, max_cr=0.05)
+
+
 def test_layerwise_vgg16_map(fc, f32):
     """VGG-16's 32-layer map (13 conv + 3 FC, weights then biases) scaled to
     a ~27M-element gradient (convolutions at full size, FC layers shrunk),
