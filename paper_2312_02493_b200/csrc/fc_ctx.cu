@@ -87,9 +87,10 @@ struct Worker {
   fcb::Pending pz{};          // zeros owed to `ge` (zero map, read by the next EF)
   // layerwise segments: control blocks (two sets, alternate steps), sample
   // keys and speculation words per segment
-  fcb::Ctl* seg_ctl[2] = {};
+  fcb::Ctl* seg_ctl[2] = {};  // [group * kMaxSegs + segment]
   unsigned* seg_skeys = nullptr;
   unsigned* seg_lastb1 = nullptr;
+  int seg_cap = 0;             // groups the arrays hold
   int seg_par = 0;
   const unsigned* pz_idx = nullptr;  // the same zeros as a sorted index list
   uint64_t pz_k = 0;
@@ -404,15 +405,22 @@ int build_segs(fc_ctx* c, double cr, uint64_t ktot) {
   const unsigned total = c->w[0].ws.ef_grid;
   for (int i = 0; i < c->n_local; ++i) {
     Worker& w = c->w[i];
-    if (!w.seg_ctl[0]) {
+    if (w.seg_cap < ng) {  // every (group, segment) has its own control blocks: the groups run in turn
+      const uint64_t ns = (uint64_t)ng * fcb::kMaxSegs;
       for (auto& cb : w.seg_ctl) {
-        TRY(c->alloc(&cb, fcb::kMaxSegs));
-        CUDA_TRY(cudaMemsetAsync(cb, 0, fcb::kMaxSegs * sizeof(fcb::Ctl), c->stream));
+        TRY(c->alloc(&cb, ns));
+        CUDA_TRY(cudaMemsetAsync(cb, 0, ns * sizeof(fcb::Ctl), c->stream));
       }
-      TRY(c->alloc(&w.seg_skeys, (uint64_t)fcb::kMaxSegs * fcb::kSamples));
-      TRY(c->alloc(&w.seg_lastb1, fcb::kMaxSegs));
-      CUDA_TRY(cudaMemsetAsync(w.seg_lastb1, 0, fcb::kMaxSegs * sizeof(unsigned), c->stream));
+      TRY(c->alloc(&w.seg_skeys, ns * fcb::kSamples));
+      TRY(c->alloc(&w.seg_lastb1, ns));
+      CUDA_TRY(cudaMemsetAsync(w.seg_lastb1, 0, ns * sizeof(unsigned), c->stream));
+      w.seg_cap = ng;
     }
+    // (a new table may use a segment's control blocks in the other parity
+    // order than their last use: start from clean ones)
+    for (auto& cb : w.seg_ctl)
+      CUDA_TRY(cudaMemsetAsync(cb, 0, (uint64_t)w.seg_cap * fcb::kMaxSegs * sizeof(fcb::Ctl), c->stream));
+    w.seg_par = 0;
     float* vals = reinterpret_cast<float*>(w.pack + ktot);
     for (int g = 0; g < ng; ++g) {
       const size_t a = (size_t)g * fcb::kMaxSegs, b = std::min(big.size(), a + fcb::kMaxSegs);
@@ -451,8 +459,9 @@ int build_segs(fc_ctx* c, double cr, uint64_t ktot) {
           e.src = L.soff == ~uint64_t(0) ? w.ge + L.off : c->scratch + L.soff;
           e.len = L.len;
           e.k = L.k;
-          e.ctl = w.seg_ctl[p] + q;
-          e.ctl_next = w.seg_ctl[p ^ 1] + q;
+          const uint64_t sq = (uint64_t)g * fcb::kMaxSegs + q;
+          e.ctl = w.seg_ctl[p] + sq;
+          e.ctl_next = w.seg_ctl[p ^ 1] + sq;
           e.ws = w.ws;
           e.ws.nchunks = nch;
           e.ws.ef_grid = nb[q];
@@ -464,8 +473,8 @@ int build_segs(fc_ctx* c, double cr, uint64_t ktot) {
           e.ws.segcnt = w.ws.segcnt + co;
           e.ws.bnorm = w.ws.bnorm + b0;
           e.ws.tblk = w.ws.tblk + 2 * (uint64_t)b0;
-          e.ws.skeys = w.seg_skeys + (uint64_t)q * fcb::kSamples;
-          e.ws.lastb1 = w.seg_lastb1 + q;
+          e.ws.skeys = w.seg_skeys + sq * fcb::kSamples;
+          e.ws.lastb1 = w.seg_lastb1 + sq;
           e.b0 = b0;
           e.nb = nb[q];
           e.idx_base = (unsigned)L.off;

@@ -2644,6 +2644,7 @@ __global__ void k_agg_update(const unsigned* __restrict__ prev, uint64_t kp, con
                              const int* __restrict__ dsel) {
   pdl_wait();
   if (kPeers) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) g_tdiag[5] = gtimer();  // (diagnostics: wait start)
     if (wait_root == -1) {
       if (!wait_all(pb, kPeers, epoch)) return;  // timeout reported
     } else {
@@ -2652,6 +2653,7 @@ __global__ void k_agg_update(const unsigned* __restrict__ prev, uint64_t kp, con
       if (!__syncthreads_and(ok)) return;
     }
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_tdiag[0] = gtimer();
   auto value = [&](uint64_t j) {
     float v;
     if (kPeers == 1) {  // c_0 + c_1 (collectives.hpp:82-87; two terms: order-free)
@@ -2721,6 +2723,7 @@ __global__ void k_agg_update(const unsigned* __restrict__ prev, uint64_t kp, con
       zmap[zmap_word(i)] = bits;
     }
   }
+  if (threadIdx.x == 0) atomicMax(&g_tdiag[1], gtimer());
 }
 
 static unsigned agg_grid(uint64_t n) {

@@ -3,7 +3,7 @@ exchange (%globaltimer marks; the GPUs of one node share the clock closely
 enough for a microsecond view).  Run under torchrun:
 
     torchrun --nproc-per-node N --master-addr 127.0.0.1 --master-port P \\
-        tools/diag_mp_timeline.py [star|var] [G] [cr]
+        tools/diag_mp_timeline.py [star|var] [ring|tree] [G] [cr]
 """
 import ctypes as C
 import os
@@ -16,6 +16,7 @@ from paper_2312_02493_b200 import flexcomm as fc  # noqa: E402
 from paper_2312_02493_b200._abi import check, lib  # noqa: E402
 
 mode = fc.VAR if "var" in sys.argv[1:] else fc.STAR
+algo = fc.TREE if "tree" in sys.argv[1:] else fc.RING
 nums = [a for a in sys.argv[1:] if a[0].isdigit()]
 G = int(nums[0]) if nums else 138_000_000
 cr = float(nums[1]) if len(nums) > 1 else 0.01
@@ -30,21 +31,21 @@ with fc.Cluster.nccl(env.world, env.rank, uid, G, device=env.local_rank, max_cr=
     cl.set_ef_timing_period(1 << 30)
     cl.fill_synthetic(0, 42, env.rank, 0)
     for s in range(8):
-        cl.artopk_step(cr, mode, fc.RING, s, stats=False)
+        cl.artopk_step(cr, mode, algo, s, stats=False)
     cl.sync()
     torch.distributed.barrier()
     st = torch.cuda.ExternalStream(cl.stream_ptr())
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
     for s in range(20):
-        cl.artopk_step(cr, mode, fc.RING, 8 + s, stats=False)
+        cl.artopk_step(cr, mode, algo, 8 + s, stats=False)
     e1.record(st)
     cl.sync()
     period = e0.elapsed_time(e1) / 20 * 1e3
     rows = []
     for s in range(4):  # one step at a time (synchronised): marks of that step
         torch.distributed.barrier()
-        stt = cl.artopk_step(cr, mode, fc.RING, 28 + s, stats=False)
+        stt = cl.artopk_step(cr, mode, algo, 28 + s, stats=False)
         cl.sync()
         ng = 2 * 148 * 8
         tb = (C.c_uint64 * (2 * nb + 8 + ng))()
