@@ -556,7 +556,7 @@ int run_layerwise(fc_ctx* c, int i, double cr, uint64_t ktot) {
     LAUNCHED();
   }
   // ||g_c||^2 of the whole selection (gain input) into this step's control block
-  fcb::launch_sumsq_fixed(vals, ktot, &w.ctl->topk_norm2, c->stream);
+  fcb::launch_sumsq_fixed(vals, ktot, &w.ctl->topk_norm2, w.ws.g_part, c->stream);
   LAUNCHED();
   w.has_topk = true;
   w.topk_k = ktot;
@@ -1319,7 +1319,7 @@ int fc_get_worker_stats(fc_ctx* c, int worker, fc_worker_stats* out) {
   // ||g_e||^2 of the last EF pass, summed over its per-chunk partials in chunk order
   fcb::launch_sum_fixed(wk.ws.cnorm, c->nch, &wk.ctl->ge_norm2, c->stream);
   // ||kept||^2 of a peer gather: over its contribution list, in list order
-  if (wk.kept_vals) fcb::launch_sumsq_fixed(wk.kept_vals, wk.kept_k, &wk.ctl->kept_norm2, c->stream);
+  if (wk.kept_vals) fcb::launch_sumsq_fixed(wk.kept_vals, wk.kept_k, &wk.ctl->kept_norm2, wk.ws.g_part, c->stream);
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   fcb::Ctl h;
   CUDA_TRY(cudaMemcpy(&h, wk.ctl, offsetof(fcb::Ctl, hist_s), cudaMemcpyDeviceToHost));

@@ -207,7 +207,7 @@ int launch_select(uint64_t k, Ctl* ctl, const ChunkWs& w, const float* ef_out, u
 // out = sum of parts[0..n) in a fixed order (one block), e.g. ||g_e||^2 from
 // the per-chunk partials of the last EF pass.
 void launch_sum_fixed(const double* parts, uint64_t n, double* out, cudaStream_t s);
-void launch_sumsq_fixed(const float* v, uint64_t n, double* out, cudaStream_t s);
+void launch_sumsq_fixed(const float* v, uint64_t n, double* out, double* parts, cudaStream_t s);
 // diagnostics: %globaltimer marks of the last decode (start, end)
 void read_tdiag(unsigned long long* out8);
 // Peer memory, STAR non-selected ranks (sel >= 0) or every rank in VAR (sel <
@@ -306,7 +306,12 @@ void launch_dense_sum(const float* lists, int nlists, uint64_t list_stride, int 
 struct SmallLayer {
   unsigned off, len, k, out;
 };
-constexpr unsigned kSmallLayerMax = 1u << 20;  // layers up to this many elements take the one-launch path
+// Layers up to this many elements take the one-launch small-layer path (one
+// block per layer, staged whole in its shared memory); longer ones the
+// segmented EF-emission + select, whose blocks are split by layer length
+// (round 2: with the bound at 1M, VGG-16's 590K-element convolutions kept
+// one SM busy for 820 us while the rest of the GPU idled).
+constexpr unsigned kSmallLayerMax = 49152;
 
 // Segmented launches (layerwise compressor): one k_ef emission pass and one
 // k_select_x over several large layers at once.  Blocks [b0, b0 + nb) of the

@@ -2198,6 +2198,7 @@ int launch_select_segs(const SegTab* d_tab, int nblocks, bool coop, cudaStream_t
 // pairs go to the layer's slot of the pack (indices + the layer offset).
 constexpr int kSlThreads = 1024;
 constexpr unsigned kSlSmem = 200 * 1024;  // layer staging (floats)
+static_assert(kSmallLayerMax <= kSlSmem / 4, "small layers are staged whole");
 
 __global__ void __launch_bounds__(kSlThreads, 1) k_topk_small(const float* __restrict__ ge,
                                                               const SmallLayer* __restrict__ layers,
@@ -2309,19 +2310,32 @@ __global__ void __launch_bounds__(1024) k_sum_fixed(const double* __restrict__ p
   if (threadIdx.x == 0) *out = t;
 }
 
-// out = sum of v[i]^2 (fp64) in a fixed order (one block).
+// out[b] = sum of v[i]^2 (fp64) over block b's fixed slice [b n / B, (b+1) n / B)
+// of a grid of B blocks, in a fixed order; B = 1 gives the whole sum.
 __global__ void __launch_bounds__(1024) k_sumsq_fixed(const float* __restrict__ v, uint64_t n,
                                                        double* __restrict__ out) {
   pdl_wait();
   __shared__ double s_red[32];
+  const uint64_t a = n * blockIdx.x / gridDim.x, e = n * (blockIdx.x + 1) / gridDim.x;
   double acc = 0.0;
-  for (uint64_t i = threadIdx.x; i < n; i += 1024) acc = fma((double)v[i], (double)v[i], acc);
+  for (uint64_t i = a + threadIdx.x; i < e; i += 1024) acc = fma((double)v[i], (double)v[i], acc);
   const double t = block_sum<1024>(acc, s_red);
-  if (threadIdx.x == 0) *out = t;
+  if (threadIdx.x == 0) out[blockIdx.x] = t;
 }
 
-void launch_sumsq_fixed(const float* v, uint64_t n, double* out, cudaStream_t s) {
-  launch_pdl(k_sumsq_fixed, 1, 1024, 0, s, v, n, out);
+// Reproducible sum of squares: a fixed split into kSumsqParts slices (not
+// the SM count, so the order is the same on any GPU), then their sum in
+// slice order.  `parts` holds kSumsqParts doubles.
+constexpr unsigned kSumsqParts = 256;
+void launch_sumsq_fixed(const float* v, uint64_t n, double* out, double* parts, cudaStream_t s) {
+  if (n < 64 * 1024 || !parts) {
+    launch_pdl(k_sumsq_fixed, 1, 1024, 0, s, v, n, out);
+    count_launch();
+    return;
+  }
+  launch_pdl(k_sumsq_fixed, kSumsqParts, 1024, 0, s, v, n, parts);
+  count_launch();
+  launch_pdl(k_sum_fixed, 1, 1024, 0, s, (const double*)parts, (uint64_t)kSumsqParts, out);
   count_launch();
 }
 

@@ -62,7 +62,7 @@ def test_layerwise_trajectory(fc, f32, n):
 
 
 def test_layerwise_small_and_large_layers(fc, f32):
-    """Layers above kSmallLayerMax (1M elements) go through the EF-emission
+    """Layers above kSmallLayerMax (49152 elements) go through the segmented EF-emission
     + k_select_x path, the rest through the one-launch small-layer kernel;
     mixed maps (unaligned offsets, a tie-heavy input) stay bit-exact."""
     g = 3_200_003
