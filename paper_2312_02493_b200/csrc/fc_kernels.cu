@@ -1538,9 +1538,15 @@ constexpr unsigned kSxListCap = kSelBins / 2;  // u32 entries in the upper half 
 // split, and no block waits at the barriers for a slow tail block.
 struct SxGeom {
   unsigned nbA, cpbA, cpbS;
+  bool whole;  // one block owns every chunk (a one-block segment)
   __host__ __device__ SxGeom(unsigned nch, unsigned grid, const EfLayout& lay) {
     const unsigned A = lay.bnd, Sg = nch - lay.bnd;
-    if (Sg == 0) {
+    whole = grid <= 1;
+    if (whole) {
+      nbA = 0;
+      cpbA = lay.B;
+      cpbS = nch;
+    } else if (Sg == 0) {
       cpbA = ((A + grid - 1) / grid + lay.B - 1) / lay.B * lay.B;
       nbA = cpbA ? (A + cpbA - 1) / cpbA : 0u;
       cpbS = 1;
@@ -1558,7 +1564,10 @@ struct SxGeom {
     }
   }
   __host__ __device__ void range(unsigned b, unsigned nch, unsigned bnd, unsigned& c0, unsigned& c1) const {
-    if (b < nbA) {
+    if (whole) {
+      c0 = 0;
+      c1 = nch;
+    } else if (b < nbA) {
       c0 = min(bnd, b * cpbA);
       c1 = min(bnd, c0 + cpbA);
     } else {
@@ -1566,7 +1575,7 @@ struct SxGeom {
       c1 = min(nch, c0 + cpbS);
     }
   }
-  __host__ __device__ unsigned max_chunks() const { return cpbA > cpbS ? cpbA : cpbS; }
+  __host__ __device__ unsigned max_chunks() const { return whole ? cpbS : cpbA > cpbS ? cpbA : cpbS; }
 };
 
 __device__ __forceinline__ float f4c(const float4& v, int e) {
