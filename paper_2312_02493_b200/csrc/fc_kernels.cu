@@ -354,20 +354,21 @@ void launch_fill_synth(float* dst, uint64_t G, uint64_t key, int dist, cudaStrea
 }
 
 // ------------------------------------------------------------------ sample ---
-// Candidate bound from a strided sample of 32768 error-fed magnitudes (fused
+// Candidate bound from a strided sample of 32768 error-fed magnitudes (4 per
+// thread on grids of fewer than 32 blocks: layerwise segments; fused
 // into the EF kernel, before it streams): the largest key bound L (12-bit
 // bucket, then 8 more bits inside it) such that the sample holds at least
 // sample_target = 1.05*mean + 4*sqrt(mean) + 8 values >= L, mean = k/G * 32768.  The bound only decides how many elements EF copies
 // out; exactness never depends on it (a miss triggers the fallback in k_select).
-__device__ __forceinline__ uint64_t sample_pos(uint64_t s, uint64_t G) {
-  return ((2 * s + 1) * G) / (2ull * kSamples);
+__device__ __forceinline__ uint64_t sample_pos(uint64_t s, uint64_t G, unsigned ns) {
+  return ((2 * s + 1) * G) / (2ull * ns);
 }
 
 // The bound's sample count: mean + 4 sigma of sampling noise + 5 % + 8 (a
 // bound above the true threshold -- probability ~1e-5 -- only costs the
 // fallback in k_select).
-__device__ __forceinline__ double sample_target(uint64_t G, uint64_t k) {
-  const double mean = (double)k / (double)G * (double)kSamples;
+__device__ __forceinline__ double sample_target(uint64_t G, uint64_t k, unsigned ns) {
+  const double mean = (double)k / (double)G * (double)ns;
   return 1.05 * mean + 4.0 * sqrt(mean) + 8.0;
 }
 
@@ -485,9 +486,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
   const unsigned lastb1 = sampling ? __ldcg(w.lastb1) : 0u;  // previous step's target bucket + 1 (0: none)
   __syncthreads();
 
-  // the sample's loads go out first, ahead of the stream's first stages
+  // the sample's loads go out first, ahead of the stream's first stages.
+  // Sample size: kSamples, or 4 per thread on small grids (a one-block
+  // segment would otherwise chase 128 dependent loads per thread)
+  const unsigned ns = min((unsigned)kSamples, nblk * kThreads * 4u);
   auto sample_at = [&](unsigned q) -> float {
-    const uint64_t i = sample_pos(q, G);
+    const uint64_t i = sample_pos(q, G, ns);
     float v = ge[i];
     if (kPend && pending_has(pz, i)) v = 0.0f;
     if (kAdd) v = __fadd_rn(g_o[i], v);
@@ -495,7 +499,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
   };
   const unsigned q0 = bid * kThreads + tid, qstride = nblk * kThreads;
   float sv = 0.f;
-  if (sampling && q0 < (unsigned)kSamples) sv = sample_at(q0);
+  if (sampling && q0 < ns) sv = sample_at(q0);
 
   // Chunks are handed out dynamically: SMs do not stream at equal rates, and
   // a static split leaves a long tail.  Lane 0 takes a ticket (one atomic):
@@ -563,14 +567,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
         const unsigned d = (kq >> kShift1) - slo;
         if (lastb1 && d < (unsigned)kSpecBins) atomicAdd(&s_sub[d * 256 + ((kq >> 11) & 255u)], 1u);
       };
-      if (q0 < (unsigned)kSamples) {
+      if (q0 < ns) {
         w.skeys[q0] = key_of(sv);
         add_sample(key_of(sv));
       }
-      for (unsigned q = q0 + qstride; q < (unsigned)kSamples; q += qstride) {  // small grids only
-        const unsigned kq = key_of(sample_at(q));
-        w.skeys[q] = kq;
-        add_sample(kq);
+      for (unsigned q = q0 + qstride; q < ns; q += 3 * qstride) {  // small grids only: 3 loads in flight
+        float x[3];
+#pragma unroll
+        for (int u = 0; u < 3; ++u) x[u] = q + u * qstride < ns ? sample_at(q + u * qstride) : 0.f;
+#pragma unroll
+        for (int u = 0; u < 3; ++u)
+          if (q + u * qstride < ns) {
+            const unsigned kq = key_of(x[u]);
+            w.skeys[q + u * qstride] = kq;
+            add_sample(kq);
+          }
       }
       __syncthreads();
       if (bid == 0 && threadIdx.x == 0) ctl->tphase_ef2[0] = gtimer();
@@ -583,10 +594,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
       unsigned bar = 0;
       grid_barrier(&ctl->bar_ef, bar, w.err, nblk);
       EF_MARK(1);
-      const double target = sample_target(G, k);
+      const double target = sample_target(G, k, ns);
       if (opts & 2) {
         Lkey = (unsigned)(kBins1 - 1) << kShift1;  // forced miss (tests)
-      } else if (target < (double)kSamples) {
+      } else if (target < (double)ns) {
         unsigned b1, b2;
         unsigned long long above1, above2;
         const unsigned long long tgt = (unsigned long long)target;
@@ -598,10 +609,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
             for (int b = tid; b < 256; b += kThreads) s_hist[b] = 0u;
             __syncthreads();
             const uint4* k4 = reinterpret_cast<const uint4*>(w.skeys);
-            constexpr int kQ = kSamples / 4 / kThreads;  // uint4 loads per thread
 #pragma unroll 8
-            for (int i = 0; i < kQ; ++i) {
-              const uint4 x = __ldcg(k4 + i * kThreads + tid);
+            for (unsigned i = tid; i < ns / 4; i += kThreads) {  // (ns: a multiple of 4)
+              const uint4 x = __ldcg(k4 + i);
               const unsigned kk[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
               for (int e = 0; e < 4; ++e)
