@@ -1802,6 +1802,13 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
       if (c->h_norms[r] > c->h_norms[sel]) sel = r;
   }
 
+  // in-place update of the aggregate (§3.5): ~2k whole-sector writes
+  // (32 B each, scattered) against the 4G-byte dense write; the measured
+  // break-even sets incr_div
+  const bool incr_ok = !(c->flags & FC_FLAG_DENSE_DECODE) && c->nbuf == 1 && c->incr_div &&
+                       k * c->incr_div <= c->G;
+  bool early_clear = false;  // the previous support cleared before the exchange's waits
+
   // (3) broadcast of the selected index set, gather, allreduce of the k
   //     values (artopk.hpp:87-104); the zeros at bidx become owed zeros
   const unsigned* bsrc = nullptr;
@@ -1823,6 +1830,15 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
     }
     LAUNCHED();
     bsrc = c->pb.list[c->rank] + par * c->pb.kmax;  // local copy of the selected list
+    if (incr_ok && c->agg_incr && c->agg_support_k) {
+      // the previous support needs no exchanged value: clear it now, in the
+      // time this rank waits for its peers (contributions / reduced list)
+      int ob0 = 0;
+      TRY(agg_target(c, &ob0));
+      fcb::launch_agg_clear(c->agg_support, c->agg_support_k, bsrc, k, own_bounds, c->agg_buf[ob0], c->G,
+                            c->zmaps, c->stream);
+      early_clear = true;
+    }
   } else if (c->nccl && N == 1) {
     // a single rank: broadcast and allreduce are identities
     Worker& w = c->w[0];
@@ -1889,10 +1905,6 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
   const float* lists = (c->nccl || N == 1) ? (N == 1 ? contrib0 : c->reduced) : c->contrib_all;
   const int nlists = c->nccl ? 1 : N;
   const uint64_t lstride = c->nccl ? 0 : c->kmax;
-  // in-place update: ~2k whole-sector writes (32 B each, scattered) against
-  // the 4G-byte dense write; measured break-even sets incr_div
-  const bool incr_ok = !(c->flags & FC_FLAG_DENSE_DECODE) && c->nbuf == 1 && c->incr_div &&
-                       k * c->incr_div <= c->G;
   int ob = 0;
   TRY(agg_target(c, &ob));
   float* aggw = c->agg_buf[ob];
@@ -1913,7 +1925,8 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
                               c->w[0].ctl, c->stream);
     const int wait_root = tree ? (mode == FC_STAR ? sel : -2) : -1;
     if (incr_ok && c->agg_incr) {
-      fcb::launch_agg_update_peers(c->pb, par, epoch, c->agg_support, c->agg_support_k, bsrc, k, own_bounds,
+      fcb::launch_agg_update_peers(c->pb, par, epoch, c->agg_support, early_clear ? 0 : c->agg_support_k, bsrc, k,
+                                   own_bounds,
                                    op == FC_AVG, (float)N, rs || tree, aggw, c->G, c->zmaps, c->agg_support_next,
                                    wait_root, c->dsel, c->stream);
       std::swap(c->agg_support, c->agg_support_next);

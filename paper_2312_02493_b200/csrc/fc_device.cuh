@@ -284,6 +284,11 @@ void launch_agg_update(const unsigned* prev, uint64_t kp, const unsigned* idx, u
                        const float* lists, int nlists, uint64_t list_stride, int divide,
                        float divisor, float* agg, uint64_t G, unsigned* zmap, unsigned* keep,
                        cudaStream_t s);
+// The previous support's part alone (sectors / words this step's list does
+// not own), needing no exchanged value: the peer paths launch it before
+// their waits and the rest with kp = 0 after them.
+void launch_agg_clear(const unsigned* prev, uint64_t kp, const unsigned* idx, uint64_t k, const unsigned* bounds,
+                      float* agg, uint64_t G, unsigned* zmap, cudaStream_t s);
 // ... the same over the peer exchanges (values as launch_decode_ar_peers
 // reads them, after its publish waits)
 void launch_agg_update_peers(const PeerBufs& pb, int par, unsigned long long epoch, const unsigned* prev,

@@ -2674,7 +2674,7 @@ __global__ void k_agg_update(const unsigned* __restrict__ prev, uint64_t kp, con
                              int divide, float divisor, float* __restrict__ agg,
                              unsigned* __restrict__ zmap, unsigned* __restrict__ keep, uint64_t G,
                              PeerBufs pb, int par, unsigned long long epoch, int wait_root,
-                             const int* __restrict__ dsel) {
+                             const int* __restrict__ dsel, int write_new) {
   pdl_wait();
   if (kPeers) {
     if (blockIdx.x == 0 && threadIdx.x == 0) g_tdiag[5] = gtimer();  // (diagnostics: wait start)
@@ -2700,7 +2700,8 @@ __global__ void k_agg_update(const unsigned* __restrict__ prev, uint64_t kp, con
     }
     return divide ? v / divisor : v;
   };
-  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < kp + k;
+  const uint64_t nt = kp + (write_new ? k : 0);  // (write_new = 0: the previous support only)
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < nt;
        t += (uint64_t)gridDim.x * blockDim.x) {
     if (t < kp) {  // the previous support
       const uint64_t j = t;
@@ -2768,7 +2769,15 @@ void launch_agg_update(const unsigned* prev, uint64_t kp, const unsigned* idx, u
                        float divisor, float* agg, uint64_t G, unsigned* zmap, unsigned* keep,
                        cudaStream_t s) {
   launch_pdl(k_agg_update<0>, agg_grid(kp + k), kThreads, 0, s, prev, kp, idx, k, bounds, lists, nlists,
-             list_stride, divide, divisor, agg, zmap, keep, G, PeerBufs{}, 0, 0ull, -1, (const int*)nullptr);
+             list_stride, divide, divisor, agg, zmap, keep, G, PeerBufs{}, 0, 0ull, -1, (const int*)nullptr, 1);
+  count_launch();
+}
+
+void launch_agg_clear(const unsigned* prev, uint64_t kp, const unsigned* idx, uint64_t k, const unsigned* bounds,
+                      float* agg, uint64_t G, unsigned* zmap, cudaStream_t s) {
+  if (!kp) return;
+  launch_pdl(k_agg_update<0>, agg_grid(kp), kThreads, 0, s, prev, kp, idx, k, bounds, (const float*)nullptr, 1,
+             (uint64_t)0, 0, 1.0f, agg, zmap, (unsigned*)nullptr, G, PeerBufs{}, 0, 0ull, -1, (const int*)nullptr, 0);
   count_launch();
 }
 
@@ -2779,10 +2788,10 @@ void launch_agg_update_peers(const PeerBufs& pb, int par, unsigned long long epo
   // (N = 2 direct sums never take a tree root: wait_root is -1 there)
   if (reduced)
     launch_pdl(k_agg_update<2>, agg_grid(kp + k), kThreads, 0, s, prev, kp, idx, k, bounds, (const float*)nullptr,
-               pb.n, k, 0, 1.0f, agg, zmap, keep, G, pb, par, epoch, wait_root, dsel);
+               pb.n, k, 0, 1.0f, agg, zmap, keep, G, pb, par, epoch, wait_root, dsel, 1);
   else
     launch_pdl(k_agg_update<1>, agg_grid(kp + k), kThreads, 0, s, prev, kp, idx, k, bounds, (const float*)nullptr,
-               pb.n, k, divide, divisor, agg, zmap, keep, G, pb, par, epoch, -1, (const int*)nullptr);
+               pb.n, k, divide, divisor, agg, zmap, keep, G, pb, par, epoch, -1, (const int*)nullptr, 1);
   count_launch();
 }
 

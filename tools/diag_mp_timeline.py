@@ -50,7 +50,7 @@ with fc.Cluster.nccl(env.world, env.rank, uid, G, device=env.local_rank, max_cr=
         ng = 2 * 148 * 8
         tb = (C.c_uint64 * (2 * nb + 8 + ng))()
         check(lib.fc_diag_ef_blocks(cl._ctx, 0, tb, 2 * nb + 8 + ng))
-        ts = (C.c_uint64 * 16)()
+        ts = (C.c_uint64 * 24)()
         check(lib.fc_diag_select_phases(cl._ctx, 0, ts))
         ef0 = min(tb[2 * b] for b in range(nb))
         ef1 = max(tb[2 * b + 1] for b in range(nb))
