@@ -151,6 +151,7 @@ struct fc_ctx {
   // pinned host copies and their device copies; rebuilt with the CR
   fcb::SegTab* h_seg = nullptr;
   fcb::SegTab* d_seg = nullptr;
+  size_t seg_tab_cap = 0;       // tables h_seg / d_seg hold
   int seg_groups = 0;
   std::vector<int> seg_blocks;  // co-resident blocks of each group's launches
   double seg_cr = -1.0;
@@ -373,7 +374,7 @@ int run_select(fc_ctx* c, int i, uint64_t k, const float* ef_out = nullptr,
 // in a group the co-resident blocks are split by layer length (at least one
 // each), and the layers' chunk arrays are consecutive views of the worker's.
 int build_segs(fc_ctx* c, double cr, uint64_t ktot) {
-  if (c->h_seg && c->seg_cr == cr && c->seg_ktot == ktot) return FC_OK;
+  if (c->seg_cr == cr && c->seg_ktot == ktot) return FC_OK;
   struct Big {
     uint64_t off, len, k, acc, soff;
   };
@@ -390,18 +391,21 @@ int build_segs(fc_ctx* c, double cr, uint64_t ktot) {
   if (soff && !c->scratch) TRY(c->alloc(&c->scratch, c->G + 4 * fcb::kMaxSegs));
   const int ng = (int)((big.size() + fcb::kMaxSegs - 1) / fcb::kMaxSegs);
   CUDA_TRY(cudaStreamSynchronize(c->stream));  // the previous tables are no longer read
-  if (c->h_seg) cudaFreeHost(c->h_seg);
-  c->h_seg = nullptr;
   c->seg_groups = ng;
   c->seg_blocks.assign(ng, 0);
+  const size_t ntab = (size_t)c->n_local * 2 * ng;
+  if (ntab > c->seg_tab_cap) {  // (kept across CR changes; grown only for a map with more groups)
+    if (c->h_seg) cudaFreeHost(c->h_seg);
+    c->h_seg = nullptr;
+    CUDA_TRY(cudaMallocHost(&c->h_seg, ntab * sizeof(fcb::SegTab)));
+    TRY(c->alloc(&c->d_seg, ntab));
+    c->seg_tab_cap = ntab;
+  }
   if (ng == 0) {
     c->seg_cr = cr;
     c->seg_ktot = ktot;
     return FC_OK;
   }
-  const size_t ntab = (size_t)c->n_local * 2 * ng;
-  CUDA_TRY(cudaMallocHost(&c->h_seg, ntab * sizeof(fcb::SegTab)));
-  TRY(c->alloc(&c->d_seg, ntab));
   const unsigned total = c->w[0].ws.ef_grid;
   for (int i = 0; i < c->n_local; ++i) {
     Worker& w = c->w[i];
@@ -2139,11 +2143,7 @@ int fc_set_layer_map(fc_ctx* c, const uint64_t* offsets, const uint64_t* lengths
     c->h_small = nullptr;  // (d_small stays in the context's allocations; a new one is made)
   }
   c->small_cr = -1.0;
-  if (c->h_seg) {
-    cudaFreeHost(c->h_seg);
-    c->h_seg = nullptr;
-  }
-  c->seg_cr = -1.0;
+  c->seg_cr = -1.0;  // (tables rebuilt on the next layerwise step)
   c->layer_off = std::move(off);
   c->layer_len = std::move(len);
   return FC_OK;
