@@ -1834,9 +1834,12 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
     }
     LAUNCHED();
     bsrc = c->pb.list[c->rank] + par * c->pb.kmax;  // local copy of the selected list
-    if (incr_ok && c->agg_incr && c->agg_support_k) {
-      // the previous support needs no exchanged value: clear it now, in the
-      // time this rank waits for its peers (contributions / reduced list)
+    // the previous support needs no exchanged value: clear it while this
+    // rank waits for its peers -- here, before the contributions / reduced
+    // list arrive; ART-Ring ranks that run a reduce-scatter slice first do
+    // it after their slice (the next wait), so no slice waits for a clear
+    const bool ring_slice = algo != FC_TREE && N > 2 && (mode == FC_VAR || c->rank != sel);
+    if (incr_ok && c->agg_incr && c->agg_support_k && !ring_slice) {
       int ob0 = 0;
       TRY(agg_target(c, &ob0));
       fcb::launch_agg_clear(c->agg_support, c->agg_support_k, bsrc, k, own_bounds, c->agg_buf[ob0], c->G,
@@ -1924,6 +1927,13 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
     if (rs)
       fcb::launch_reduce_slice(c->pb, par, epoch, k, op == FC_AVG, (float)N, mode == FC_STAR ? sel : -1,
                                c->w[0].ctl, c->stream);
+    if (rs && incr_ok && c->agg_incr && c->agg_support_k && !early_clear) {  // (see the early clear)
+      int ob0 = 0;
+      TRY(agg_target(c, &ob0));
+      fcb::launch_agg_clear(c->agg_support, c->agg_support_k, bsrc, k, own_bounds, c->agg_buf[ob0], c->G,
+                            c->zmaps, c->stream);
+      early_clear = true;
+    }
     if (tree && (mode == FC_VAR || c->rank == sel))  // (VAR: only the winner works; found on the device)
       fcb::launch_reduce_root(c->pb, par, epoch, k, op == FC_AVG, (float)N, mode == FC_STAR ? sel : -1, c->dsel,
                               c->w[0].ctl, c->stream);
