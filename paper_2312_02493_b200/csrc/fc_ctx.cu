@@ -1834,10 +1834,14 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
     }
     LAUNCHED();
     bsrc = c->pb.list[c->rank] + par * c->pb.kmax;  // local copy of the selected list
-    // the previous support needs no exchanged value: clear it while this
-    // rank waits for its peers -- here, before the contributions / reduced
-    // list arrive; ART-Ring ranks that run a reduce-scatter slice first do
-    // it after their slice (the next wait), so no slice waits for a clear
+    // the previous support needs no exchanged value: clear it now, while
+    // this rank waits for its peers (the selected rank for the others'
+    // contributions, the others for the root's or the peer's values).  An
+    // ART-Ring rank that reduces a slice for the others has no such window
+    // (before its slice the clear delays everyone's decode, after it its
+    // own): it updates in one kernel after the waits (timelines: N = 4
+    // ring 0.521 merged, 0.525 / 0.532 ms with the clear before / after the
+    // slice)
     const bool ring_slice = algo != FC_TREE && N > 2 && (mode == FC_VAR || c->rank != sel);
     if (incr_ok && c->agg_incr && c->agg_support_k && !ring_slice) {
       int ob0 = 0;
@@ -1927,13 +1931,6 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
     if (rs)
       fcb::launch_reduce_slice(c->pb, par, epoch, k, op == FC_AVG, (float)N, mode == FC_STAR ? sel : -1,
                                c->w[0].ctl, c->stream);
-    if (rs && incr_ok && c->agg_incr && c->agg_support_k && !early_clear) {  // (see the early clear)
-      int ob0 = 0;
-      TRY(agg_target(c, &ob0));
-      fcb::launch_agg_clear(c->agg_support, c->agg_support_k, bsrc, k, own_bounds, c->agg_buf[ob0], c->G,
-                            c->zmaps, c->stream);
-      early_clear = true;
-    }
     if (tree && (mode == FC_VAR || c->rank == sel))  // (VAR: only the winner works; found on the device)
       fcb::launch_reduce_root(c->pb, par, epoch, k, op == FC_AVG, (float)N, mode == FC_STAR ? sel : -1, c->dsel,
                               c->w[0].ctl, c->stream);
