@@ -135,12 +135,6 @@ struct fc_ctx {
   unsigned* zmaps = nullptr;   // n_local x (nch * 32) zero maps
   unsigned* agg_support = nullptr;  // indices of agg's nonzero support (incremental decode)
   unsigned* agg_support_next = nullptr;  // where an in-place step keeps its support (swapped after)
-  // one-worker AR steps: the select writes its chunk bounds into these two
-  // rows in turn, so the next step's fused in-place update finds the
-  // previous support's bounds (agg_prev_bounds; nullptr: not available)
-  unsigned* bounds_sel[2] = {};
-  int bsel_par = 0;
-  const unsigned* agg_prev_bounds = nullptr;
   uint64_t agg_support_k = 0;
   bool agg_incr = false;            // agg == densify(agg_support) and zmap 0 == its bits
   uint64_t incr_div = 80;           // in-place update when k <= G / incr_div (FC_INCR_DIV overrides)
@@ -805,7 +799,6 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
   TRY(c->alloc(&c->zmaps, N * c->nch * 32));
   TRY(c->alloc(&c->agg_support, c->kmax));
   TRY(c->alloc(&c->agg_support_next, c->kmax));
-  for (auto& b : c->bounds_sel) TRY(c->alloc(&b, c->nch + 1 + 4));
   CUDA_TRY(cudaMemsetAsync(c->zmaps, 0, N * c->nch * 32 * sizeof(unsigned), c->stream));
   // zero agg == densify(empty support); pipelined contexts always decode densely
   c->agg_incr = !(o->flags & (FC_FLAG_DENSE_DECODE | FC_FLAG_PIPELINE));
@@ -1772,16 +1765,6 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
   const int par = (int)(epoch & 1);
 
   if (!p2p_star) TRY(need_comm(c, "this step"));
-  // in-place update of the aggregate (§3.5): ~2k whole-sector writes
-  // (32 B each, scattered) against the 4G-byte dense write; the measured
-  // break-even (DESIGN §3.5) sets incr_div
-  const bool incr_ok = !(c->flags & FC_FLAG_DENSE_DECODE) && c->nbuf == 1 && c->incr_div &&
-                       k * c->incr_div <= c->G;
-  // one worker: the select writes its bounds into the alternating rows and,
-  // with the previous support's bounds at hand, updates the aggregate itself
-  const bool one = N == 1 && c->n_local == 1;
-  unsigned* bcur = one ? c->bounds_sel[c->bsel_par] : nullptr;
-  const bool fused = one && incr_ok && c->agg_incr && (c->agg_support_k == 0 || c->agg_prev_bounds);
   // (1) error feedback on every worker; Top-k where its result is consumed
   record(c, 0);
   for (int i = 0; i < c->n_local; ++i) {
@@ -1801,18 +1784,6 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
       m.publish_contrib = mode == FC_STAR;  // VAR: contributions come from the gather
       TRY(run_select(c, i, k, nullptr, m, c->pb.list[c->rank] + par * c->pb.kmax,
                      c->pb.contrib[c->rank] + par * c->pb.kmax, c->pb.bounds[c->rank] + par * c->pb.nbs));
-    } else if (one) {
-      fcb::SelectMode m;
-      if (fused) {
-        int ob0 = 0;
-        TRY(agg_target(c, &ob0));
-        m.agg = c->agg_buf[ob0];
-        m.zmap = c->zmaps;
-        m.prev = c->agg_support;
-        m.prev_bounds = c->agg_support_k ? c->agg_prev_bounds : nullptr;
-        m.keep = c->agg_support_next;
-      }
-      TRY(run_select(c, i, k, nullptr, m, nullptr, nullptr, bcur));
     } else {
       TRY(run_select(c, i, k));
     }
@@ -1835,6 +1806,11 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
       if (c->h_norms[r] > c->h_norms[sel]) sel = r;
   }
 
+  // in-place update of the aggregate (§3.5): ~2k whole-sector writes
+  // (32 B each, scattered) against the 4G-byte dense write; the measured
+  // break-even (DESIGN §3.5) sets incr_div
+  const bool incr_ok = !(c->flags & FC_FLAG_DENSE_DECODE) && c->nbuf == 1 && c->incr_div &&
+                       k * c->incr_div <= c->G;
   bool early_clear = false;  // the previous support cleared before the exchange's waits
 
   // (3) broadcast of the selected index set, gather, allreduce of the k
@@ -1880,7 +1856,7 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
     bsrc = w.pack;
     contrib0 = reinterpret_cast<const float*>(w.pack + k);
     w.kept_is_topk = true;
-    own_bounds = bcur;
+    own_bounds = c->bounds;
   } else if (var_device) {
     // VAR: allgather of the N scores, winner on the device, its list
     // broadcast as a sum-allreduce of (winner ? list : 0); every rank
@@ -1918,7 +1894,7 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
                            algo == FC_TREE ? c->comm_tree : c->comm_ring, c->stream));
   } else {
     bsrc = c->w[sel].pack;
-    own_bounds = one ? bcur : c->bounds + (uint64_t)sel * (c->nch + 1);
+    own_bounds = c->bounds + (uint64_t)sel * (c->nch + 1);
     for (int i = 0; i < c->n_local; ++i) {
       Worker& w = c->w[i];
       if (i == sel) {
@@ -1972,10 +1948,6 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
         CUDA_TRY(cudaMemcpyAsync(c->agg_support, bsrc, k * sizeof(unsigned), cudaMemcpyDeviceToDevice,
                                  c->stream));
     }
-  } else if (fused) {
-    // the select updated the aggregate in place (one worker) and kept its
-    // list in agg_support_next
-    std::swap(c->agg_support, c->agg_support_next);
   } else if (incr_ok && c->agg_incr) {
     // in place: zero the previous support, write this one (same dense content)
     if (!own_bounds) {
@@ -1999,8 +1971,6 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
   LAUNCHED();
   c->agg_incr = incr_ok;
   c->agg_support_k = incr_ok ? k : 0;
-  c->agg_prev_bounds = one && incr_ok ? bcur : nullptr;  // (the bounds of agg_support's list)
-  if (one) c->bsel_par ^= 1;
   record(c, 4);
   c->has_agg = true;
   TRY(agg_written(c, ob));

@@ -200,15 +200,6 @@ struct SelectMode {
   PeerBufs pb;
   unsigned long long epoch = 0;
   bool publish_contrib = true;  // the values are this rank's contribution (STAR's selected rank)
-  // one worker (N = 1): the in-place aggregate update (§3.5) fused into the
-  // select -- the previous support (list `prev`, chunk bounds `prev_bounds`;
-  // nullptr: none) zeroed, this selection written (whole 32-byte sectors,
-  // owed-zero words) and kept in `keep` for the next step
-  float* agg = nullptr;
-  unsigned* zmap = nullptr;
-  const unsigned* prev = nullptr;
-  const unsigned* prev_bounds = nullptr;
-  unsigned* keep = nullptr;
 };
 int launch_select(uint64_t k, Ctl* ctl, const ChunkWs& w, const float* ef_out, uint64_t G,
                   unsigned* out_idx, float* out_val, unsigned* bounds_out, const SelectMode& m,

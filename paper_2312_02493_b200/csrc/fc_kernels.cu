@@ -1500,22 +1500,6 @@ __global__ void __launch_bounds__(kSelThreads, 1) k_select(uint64_t k, Ctl* __re
   }
 }
 
-// Whole 32-byte sector stores of the in-place aggregate (§3.5).
-constexpr int kAggAtom = 8;  // floats per write: measured against 16 and 32 (DESIGN §3.5)
-
-__device__ __forceinline__ void st_sector(float* __restrict__ agg, uint64_t b, const float (&v)[kAggAtom],
-                                          uint64_t G) {
-  if (b + kAggAtom <= G) {
-    float4* p = reinterpret_cast<float4*>(agg + b);
-    p[0] = make_float4(v[0], v[1], v[2], v[3]);
-    p[1] = make_float4(v[4], v[5], v[6], v[7]);
-  } else {
-#pragma unroll
-    for (int e = 0; e < kAggAtom; ++e)
-      if (b + e < G) agg[b + e] = v[e];
-  }
-}
-
 // ---------------------------------------------------------------- select (x) ---
 // Exact Top-k of the EF pass's candidates (select_topk_indices,
 // inc/compress.hpp:38-53): the k largest |g_e|, ties to the lower index,
@@ -1867,22 +1851,6 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
   __syncthreads();
   if (!kSeg && tid == 0) reinterpret_cast<unsigned long long*>(w.g_part)[2048 + 2 * bid] = gtimer();  // (diagnostics)
   flush_hist(s_h, ctl->hist_w, kSelBins);
-  if (mode.agg && mode.prev_bounds) {
-    // N = 1 in-place aggregate, the previous support's half: every sector /
-    // owed-zero word holding a previous index of this block's chunks is
-    // zeroed (fire-and-forget stores while the grid meets at the barrier;
-    // this block rewrites the ones its own selection holds at the end)
-    const unsigned pb0 = __ldcg(mode.prev_bounds + c0), pb1 = __ldcg(mode.prev_bounds + c1);
-    for (unsigned j = pb0 + tid; j < pb1; j += kSxThreads) {
-      const unsigned i = __ldcg(mode.prev + j);
-      const unsigned ip = j > pb0 ? __ldcg(mode.prev + j - 1) : 0u;
-      if (j == pb0 || (ip >> 3) != (i >> 3)) {
-        const float z[kAggAtom] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        st_sector(mode.agg, (uint64_t)(i & ~7u), z, G);
-      }
-      if (j == pb0 || zmap_word(ip) != zmap_word(i)) mode.zmap[zmap_word(i)] = 0u;
-    }
-  }
   SX_MARK(1);
   grid_barrier(&ctl->bar_sel, bar, w.err, nblk);
   SXP_MARK(1);
@@ -2113,44 +2081,6 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
       out_idx[obase + i] = s_oidx[i];
       out_val[obase + i] = s_oval[i];
     }
-  if (mode.agg) {
-    // N = 1 in-place aggregate, this selection's half: the block's output
-    // range is its chunks' selection in index order; the thread of a pair
-    // first in its sector (word) writes the whole sector (word) -- after
-    // the block's previous-support zeros (block barriers in between).  The
-    // aggregate value is the selected value itself (one worker: /1).
-    __syncthreads();  // (unstaged output pairs are in global memory)
-    auto gi = [&](unsigned long long p) -> unsigned { return staged ? s_oidx[p] : __ldcg(out_idx + obase + p); };
-    auto gv = [&](unsigned long long p) -> float { return staged ? s_oval[p] : __ldcg(out_val + obase + p); };
-    for (unsigned long long p = tid; p < nsel; p += kSxThreads) {
-      const unsigned i = gi(p), ip = p ? gi(p - 1) : 0u;
-      mode.keep[obase + p] = i;
-      if (p == 0 || (ip >> 3) != (i >> 3)) {
-        float v[kAggAtom] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        unsigned m = i;
-        for (unsigned long long q = p; q < nsel && q < p + kAggAtom; ++q) {
-          if (q > p) {
-            m = gi(q);
-            if ((m >> 3) != (i >> 3)) break;
-          }
-          const float x = gv(q);
-#pragma unroll
-          for (int e = 0; e < kAggAtom; ++e)
-            if ((m & (kAggAtom - 1u)) == (unsigned)e) v[e] = x;
-        }
-        st_sector(mode.agg, (uint64_t)(i & ~7u), v, G);
-      }
-      if (p == 0 || zmap_word(ip) != zmap_word(i)) {
-        unsigned bits = zmap_bit(i);
-        for (unsigned long long q = p + 1; q < nsel && q < p + 32; ++q) {
-          const unsigned m = gi(q);
-          if (zmap_word(m) != zmap_word(i)) break;
-          bits |= zmap_bit(m);
-        }
-        mode.zmap[zmap_word(i)] = bits;
-      }
-    }
-  }
   SX_MARK(4);
   // the decode's chunk bounds of [c0, c1): bounds[c] = first output position
   // whose index is >= c * kChunk = obase + selected pairs in earlier chunks
@@ -2719,6 +2649,21 @@ void launch_gather(const unsigned* bidx, uint64_t k, const float* ge, float* con
 // Every write is a plain full-sector (full-word) store, no atomics, no order
 // between the two lists.  For k << G this replaces the 4G-byte dense write
 // with ~2 x 32k bytes; the buffer content is identical to a full decode.
+constexpr int kAggAtom = 8;  // floats per write: measured against 16 and 32 (DESIGN §3.5)
+
+__device__ __forceinline__ void st_sector(float* __restrict__ agg, uint64_t b, const float (&v)[kAggAtom],
+                                          uint64_t G) {
+  if (b + kAggAtom <= G) {
+    float4* p = reinterpret_cast<float4*>(agg + b);
+    p[0] = make_float4(v[0], v[1], v[2], v[3]);
+    p[1] = make_float4(v[4], v[5], v[6], v[7]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < kAggAtom; ++e)
+      if (b + e < G) agg[b + e] = v[e];
+  }
+}
+
 // kPeers as in k_decode_ar: 0 local lists, 1 two-rank direct sum (own
 // contribution + the peer's in the inbox), 2 the reduced list (reduce-scatter
 // or tree root), after the same publish waits.
