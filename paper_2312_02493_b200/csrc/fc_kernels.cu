@@ -1750,10 +1750,12 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
   float4* s_val4 = reinterpret_cast<float4*>(s_val);
   unsigned* s_idx = reinterpret_cast<unsigned*>(s_val + P);
   uint4* s_idx4 = reinterpret_cast<uint4*>(s_idx);
-  if (cached) {
-    // the indices are needed only by the emission: one TMA bulk copy per
-    // segment (runs padded to 16 bytes; a segment's slots are never
-    // overrun), completing on one mbarrier in the background of P1-P3
+  // the indices are needed only by the emission: one TMA bulk copy per
+  // segment (runs padded to 16 bytes; a segment's slots are never overrun),
+  // completing on one mbarrier in the background of P2-P3; issued after
+  // the P1 pass, while the grid meets at the first barrier
+  auto issue_idx = [&]() {
+    if (!cached) return;
     if (tid == 0) {
       mbar_init(&s_mbar, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1764,7 +1766,7 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
       const unsigned bytes = ((s_sct[j] + 3u) & ~3u) * 4u;
       if (bytes) bulk_g2s(s_idx + s_pos[j], w.cand_idx + ((uint64_t)seg_c0(j) << kChunkShift), bytes, &s_mbar);
     }
-  }
+  };
   SX_MARK(7);
   // warp-contiguous ranges of 128-position steps
   const unsigned R = (P + kSxWarps * 128 - 1) / (kSxWarps * 128) * 128;
@@ -1850,6 +1852,7 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
   SX_MARK(0);
   __syncthreads();
   if (!kSeg && tid == 0) reinterpret_cast<unsigned long long*>(w.g_part)[2048 + 2 * bid] = gtimer();  // (diagnostics)
+  issue_idx();
   flush_hist(s_h, ctl->hist_w, kSelBins);
   SX_MARK(1);
   grid_barrier(&ctl->bar_sel, bar, w.err, nblk);

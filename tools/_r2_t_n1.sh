@@ -1,0 +1,6 @@
+timeout 300 python tools/diag_select.py > gpurun_out/r2t_sel.txt 2>&1
+timeout 300 python bench.py > gpurun_out/r2t_bench_n1.json 2> gpurun_out/r2t_bench_n1.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv --log-file gpurun_out/r2t_launches.csv \
+  python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/r2t_ncu.log 2>&1
+timeout 2400 python -m pytest tests -m gpu -x -q > gpurun_out/r2t_pytest_gpu.log 2>&1; echo rc=$? >> gpurun_out/r2t_pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2t_smoke.log 2>&1; echo rc=$? >> gpurun_out/r2t_smoke.log
