@@ -1,0 +1,7 @@
+timeout 300 python bench.py --no-cpu-baseline > gpurun_out/r2v_bench_n1.json 2> gpurun_out/r2v_bench_n1.err
+timeout 300 python tools/diag_select.py > gpurun_out/r2v_sel.txt 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv --log-file gpurun_out/r2v_launches.csv \
+  python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/r2v_ncu.log 2>&1
+timeout 2400 python -m pytest tests -m gpu -x -q > gpurun_out/r2v_pytest_gpu.log 2>&1; echo rc=$? >> gpurun_out/r2v_pytest_gpu.log
+timeout 300 python bench.py --mode ag --compressor layerwise --no-cpu-baseline --no-e2e > gpurun_out/r2v_bench_layerwise.json 2>/dev/null
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2v_smoke.log 2>&1; echo rc=$? >> gpurun_out/r2v_smoke.log
