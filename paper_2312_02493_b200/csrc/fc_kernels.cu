@@ -241,47 +241,6 @@ __device__ bool block_select_top(const unsigned* hist, int nb, unsigned long lon
   return f;
 }
 
-// block_select_top for one warp (the other warps of the block elsewhere):
-// s_stage holds nb words of this warp's shared memory.
-__device__ bool warp_select_top(const unsigned* hist, int nb, unsigned long long target, unsigned& bin,
-                                unsigned long long& above, unsigned* s_stage) {
-  const int lane = threadIdx.x & 31;
-  if (hist != s_stage) {
-#pragma unroll 16
-    for (int b = lane; b < nb; b += 32) s_stage[b] = __ldcg(hist + b);
-  }
-  __syncwarp();
-  const int per = (nb + 31) / 32;
-  const int top = nb - per * lane;
-  const int bot = top - per < 0 ? 0 : top - per;
-  unsigned long long sum = 0;
-  for (int b = top - 1; b >= bot; --b) sum += s_stage[b];
-  const unsigned long long ex = warp_incl_scan(sum) - sum;
-  int found = 0;
-  unsigned fb = 0;
-  unsigned long long fa = 0;
-  if (top > bot && ex < target && target <= ex + sum) {
-    unsigned long long acc = ex;
-    for (int b = top - 1; b >= bot; --b) {
-      const unsigned h = s_stage[b];
-      if (target <= acc + h) {
-        fb = (unsigned)b;
-        fa = acc;
-        found = 1;
-        break;
-      }
-      acc += h;
-    }
-  }
-  const unsigned bal = __ballot_sync(0xffffffffu, found);
-  __syncwarp();
-  if (!bal) return false;
-  const int src = __ffs(bal) - 1;
-  bin = __shfl_sync(0xffffffffu, fb, src);
-  above = __shfl_sync(0xffffffffu, fa, src);
-  return true;
-}
-
 // Grid barrier for the kernels that run exactly one block per SM (grid = SM
 // count, shared memory sized so that no second block fits).  They are
 // launched with the cooperative attribute by default (co-residency
@@ -331,29 +290,6 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned& target, un
 }
 __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned& target, unsigned* err) {
   grid_barrier(ctr, target, err, gridDim.x);
-}
-// The same barrier taken by one warp of each block (the block's other
-// warps keep working): lane 0 arrives and waits.
-__device__ __forceinline__ void warp_grid_barrier(unsigned* ctr, unsigned& target, unsigned* err,
-                                                  unsigned nblk) {
-  __syncwarp();
-  target += nblk;
-  if ((threadIdx.x & 31) == 0) {
-    __threadfence();
-    atomicAdd(ctr, 1u);
-    if (ld_acquire(ctr) < target) {
-      const unsigned long long t0 = gtimer();
-      while (ld_acquire(ctr) < target) {
-        __nanosleep(64);
-        if (gtimer() - t0 > kBarrierTimeoutNs) {
-          report_error(err, kErrBarrier);
-          break;
-        }
-      }
-    }
-    __threadfence();
-  }
-  __syncwarp();
 }
 
 // System-scope epoch flags of the peer exchange (written over NVLink by the
@@ -458,7 +394,6 @@ __device__ __forceinline__ double sample_target(uint64_t G, uint64_t k, unsigned
 constexpr int kEfStages = 3;
 constexpr int kEfWarps = kThreads / 32;
 constexpr unsigned kStageBytes = 2 * kChunk * 4 + 128;  // residual/g_e | g_o | zero-map words
-constexpr unsigned kMaxDefer = 64;  // chunks a warp streams before the sampled bound, at most
 constexpr unsigned kEfRingBytes = kEfWarps * kEfStages * kStageBytes;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -535,12 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
   __shared__ unsigned s_sub[kEmit ? kSpecBins * 256 : 1];  // speculative level-2 histograms
   __shared__ __align__(8) unsigned long long s_bar[kEfWarps][kEfStages];
   __shared__ unsigned s_chunk[kEfWarps][kEfStages];  // chunk held by each stage
-  // sampled bound: warp 0 derives it while the other warps stream; chunks
-  // streamed before it is known have their candidates emitted afterwards
-  __shared__ unsigned s_lk_ready, s_lkey;
-  __shared__ unsigned s_def[kEmit ? kEfWarps : 1][kEmit ? kMaxDefer : 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_lk_ready = 0u;
   const unsigned sw = lane & 7;  // LDS.128 swizzle
   unsigned char* ring = s_ring + warp * kEfStages * kStageBytes;
   unsigned ncand = 0;  // candidates emitted by this warp (lane 0)
@@ -567,6 +497,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
     if (kAdd) v = __fadd_rn(g_o[i], v);
     return v;
   };
+  const unsigned q0 = bid * kThreads + tid, qstride = nblk * kThreads;
+  float sv = 0.f;
+  if (sampling && q0 < ns) sv = sample_at(q0);
 
   // Chunks are handed out dynamically: SMs do not stream at equal rates, and
   // a static split leaves a long tail.  Lane 0 takes a ticket (one atomic):
@@ -611,102 +544,91 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
     for (int s = 0; s < kEfStages; ++s) issue(s);
   __syncwarp();
 
-  // candidate bound.  Sampled (opts & 1): warp 0 of every block derives it
-  // from the sample while warps 1..7 stream (their chunks' emission
-  // deferred until it is published in shared memory); otherwise given.
+  // candidate bound: derived while the first stages are in flight, before any
+  // block writes g_e back over the residual
   unsigned Lkey = 0u;
-  bool ready = true;  // (warp-uniform) Lkey is this warp's
   if (kEmit) {
     if (opts & 1) {
-      ready = false;
-      if (warp == 0) {
-        // Level 1 (12-bit buckets): each block histograms its share of the
-        // sample and flushes it (one grid barrier, taken by this warp).
-        // Level 2 (the next 8 bits inside the target bucket) is
-        // speculative: the 8-bit histograms of the buckets around the
-        // previous step's target bucket travel with the level-1 flush, and
-        // when the new target bucket is among them no second pass is needed.
-        // Otherwise every sampled key is also in the shared sample array:
-        // the warp re-reads all of them from L2 and histograms the few in
-        // the bucket (no second flush or barrier either way).
-        const unsigned pb1 = lastb1 ? lastb1 - 1u : 0u;
-        const unsigned slo = pb1 > kSpecBins / 2 ? pb1 - kSpecBins / 2 : 0u;  // speculative buckets [slo, slo + kSpecBins)
-        for (int b = lane; b < kBins1; b += 32) s_hist[b] = 0u;
-        for (int b = lane; b < kSpecBins * 256; b += 32) s_sub[b] = 0u;
-        __syncwarp();
-        auto add_sample = [&](unsigned kq) {
-          atomicAdd(&s_hist[kq >> kShift1], 1u);
-          const unsigned d = (kq >> kShift1) - slo;
-          if (lastb1 && d < (unsigned)kSpecBins) atomicAdd(&s_sub[d * 256 + ((kq >> 11) & 255u)], 1u);
-        };
-        const unsigned wq0 = bid * 32 + lane, wst = nblk * 32;  // this warp's share of the sample
-        for (unsigned q = wq0; q < ns; q += 8 * wst) {  // 8 loads in flight per lane
-          float x[8];
+      // Level 1 (12-bit buckets): each block histograms its own samples and
+      // flushes them (one grid barrier).  Level 2 (the next 8 bits inside the
+      // target bucket) is speculative: the 8-bit histograms of the buckets
+      // around the previous step's target bucket travel with the level-1
+      // flush, and when the new target bucket is among them no second pass
+      // is needed.  Otherwise every sampled key is also in the shared sample
+      // array: each block re-reads all 32768 from L2 and histograms the few
+      // in the bucket (no second flush or barrier either way).
+      const unsigned pb1 = lastb1 ? lastb1 - 1u : 0u;
+      const unsigned slo = pb1 > kSpecBins / 2 ? pb1 - kSpecBins / 2 : 0u;  // speculative buckets [slo, slo + kSpecBins)
+      for (int b = tid; b < kBins1; b += kThreads) s_hist[b] = 0u;
+      for (int b = tid; b < kSpecBins * 256; b += kThreads) s_sub[b] = 0u;
+      __syncthreads();
+      auto add_sample = [&](unsigned kq) {
+        atomicAdd(&s_hist[kq >> kShift1], 1u);
+        const unsigned d = (kq >> kShift1) - slo;
+        if (lastb1 && d < (unsigned)kSpecBins) atomicAdd(&s_sub[d * 256 + ((kq >> 11) & 255u)], 1u);
+      };
+      if (q0 < ns) {
+        w.skeys[q0] = key_of(sv);
+        add_sample(key_of(sv));
+      }
+      for (unsigned q = q0 + qstride; q < ns; q += 3 * qstride) {  // small grids only: 3 loads in flight
+        float x[3];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) x[u] = q + u * wst < ns ? sample_at(q + u * wst) : 0.f;
+        for (int u = 0; u < 3; ++u) x[u] = q + u * qstride < ns ? sample_at(q + u * qstride) : 0.f;
 #pragma unroll
-          for (int u = 0; u < 8; ++u)
-            if (q + u * wst < ns) {
-              const unsigned kq = key_of(x[u]);
-              w.skeys[q + u * wst] = kq;
-              add_sample(kq);
-            }
-        }
-        __syncwarp();
-        if (bid == 0 && lane == 0) ctl->tphase_ef2[0] = gtimer();
-        for (int b = lane; b < kBins1; b += 32)
-          if (s_hist[b]) atomicAdd(&ctl->hist_s[b], s_hist[b]);
-        if (lastb1)
-          for (int b = lane; b < kSpecBins * 256; b += 32)
-            if (s_sub[b]) atomicAdd(&ctl->hist_s2w[b], s_sub[b]);
-        if (bid == 0 && lane == 0) ctl->tphase_ef2[1] = gtimer();
-        unsigned bar = 0;
-        warp_grid_barrier(&ctl->bar_ef, bar, w.err, nblk);
-        EF_MARK(1);
-        const double target = sample_target(G, k, ns);
-        if (opts & 2) {
-          Lkey = (unsigned)(kBins1 - 1) << kShift1;  // forced miss (tests)
-        } else if (target < (double)ns) {
-          unsigned b1, b2;
-          unsigned long long above1, above2;
-          const unsigned long long tgt = (unsigned long long)target;
-          if (warp_select_top(ctl->hist_s, kBins1, tgt, b1, above1, s_hist)) {
-            bool f2;
-            if (lastb1 && b1 - slo < (unsigned)kSpecBins) {  // speculation hit: level 2 is in
-              f2 = warp_select_top(ctl->hist_s2w + (b1 - slo) * 256, 256, tgt - above1, b2, above2, s_hist);
-            } else {
-              for (int b = lane; b < 256; b += 32) s_hist[b] = 0u;
-              __syncwarp();
-              const uint4* k4 = reinterpret_cast<const uint4*>(w.skeys);
-#pragma unroll 8
-              for (unsigned i = lane; i < ns / 4; i += 32) {  // (ns: a multiple of 4)
-                const uint4 x = __ldcg(k4 + i);
-                const unsigned kk[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                  if ((kk[e] >> kShift1) == b1) atomicAdd(&s_hist[(kk[e] >> 11) & 255u], 1u);
-              }
-              __syncwarp();
-              f2 = warp_select_top(s_hist, 256, tgt - above1, b2, above2, s_hist);
-            }
-            Lkey = (b1 << kShift1) | ((f2 ? b2 : 0u) << 11);
-            if (bid == 0 && lane == 0) *w.lastb1 = b1 + 1u;  // (every block read it before the barrier)
-          } else {
-            Lkey = 0u;
+        for (int u = 0; u < 3; ++u)
+          if (q + u * qstride < ns) {
+            const unsigned kq = key_of(x[u]);
+            w.skeys[q + u * qstride] = kq;
+            add_sample(kq);
           }
+      }
+      __syncthreads();
+      if (bid == 0 && threadIdx.x == 0) ctl->tphase_ef2[0] = gtimer();
+      for (int b = tid; b < kBins1; b += kThreads)
+        if (s_hist[b]) atomicAdd(&ctl->hist_s[b], s_hist[b]);
+      if (lastb1)
+        for (int b = tid; b < kSpecBins * 256; b += kThreads)
+          if (s_sub[b]) atomicAdd(&ctl->hist_s2w[b], s_sub[b]);
+      if (bid == 0 && threadIdx.x == 0) ctl->tphase_ef2[1] = gtimer();
+      unsigned bar = 0;
+      grid_barrier(&ctl->bar_ef, bar, w.err, nblk);
+      EF_MARK(1);
+      const double target = sample_target(G, k, ns);
+      if (opts & 2) {
+        Lkey = (unsigned)(kBins1 - 1) << kShift1;  // forced miss (tests)
+      } else if (target < (double)ns) {
+        unsigned b1, b2;
+        unsigned long long above1, above2;
+        const unsigned long long tgt = (unsigned long long)target;
+        if (block_select_top<kThreads>(ctl->hist_s, kBins1, tgt, b1, above1, s_hist)) {
+          bool f2;
+          if (lastb1 && b1 - slo < (unsigned)kSpecBins) {  // speculation hit: level 2 is in
+            f2 = block_select_top<kThreads>(ctl->hist_s2w + (b1 - slo) * 256, 256, tgt - above1, b2, above2, s_hist);
+          } else {
+            for (int b = tid; b < 256; b += kThreads) s_hist[b] = 0u;
+            __syncthreads();
+            const uint4* k4 = reinterpret_cast<const uint4*>(w.skeys);
+#pragma unroll 8
+            for (unsigned i = tid; i < ns / 4; i += kThreads) {  // (ns: a multiple of 4)
+              const uint4 x = __ldcg(k4 + i);
+              const unsigned kk[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if ((kk[e] >> kShift1) == b1) atomicAdd(&s_hist[(kk[e] >> 11) & 255u], 1u);
+            }
+            f2 = block_select_top<kThreads>(s_hist, 256, tgt - above1, b2, above2, s_hist);
+          }
+          Lkey = (b1 << kShift1) | ((f2 ? b2 : 0u) << 11);
+          if (bid == 0 && tid == 0) *w.lastb1 = b1 + 1u;  // (every block read it before the barrier)
         } else {
           Lkey = 0u;
         }
-        EF_MARK(2);
-        if (lane == 0) {
-          if (bid == 0) ctl->Lkey = Lkey;
-          s_lkey = Lkey;
-          __threadfence_block();
-          *(volatile unsigned*)&s_lk_ready = 1u;
-        }
-        __syncwarp();
-        ready = true;
+      } else {
+        Lkey = 0u;
       }
+      EF_MARK(2);
+      if (bid == 0 && tid == 0) ctl->Lkey = Lkey;
     } else if (opts & 4) {  // every element is a candidate
       if (bid == 0 && tid == 0) ctl->Lkey = 0;
       Lkey = 0u;
@@ -715,85 +637,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
     }
   }
 
-  // candidate emission of chunk c, whose values lane l reads as val(p) for
-  // its elements 32 l + p: one warp scan places every candidate (lane order
-  // == index order), runs of one batch back to back from the batch's first
-  // slot (a single chunk: its own slot)
-  auto emit = [&](unsigned c, unsigned mask, auto&& val) {
-    const uint64_t base = (uint64_t)c << kChunkShift;
-    const unsigned n = __popc(mask);
-    unsigned incl = n;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned x = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += x;
-    }
-    const unsigned run = __shfl_sync(0xffffffffu, incl, 31);
-    if (lane == 0) {
-      w.cnt[c] = run;
-      ncand += run;
-    }
-    if (lay.seg_start(c)) brun = 0;
-    unsigned pos = (lay.seg_base(c) << kChunkShift) + brun + incl - n;
-    brun += run;
-    if (lane == 0 && lay.seg_last(c, nchunks)) w.segcnt[lay.seg_id(c)] = brun;  // the segment's total
-    for (unsigned m = mask; m; m &= m - 1) {
-      const int p = __ffs(m) - 1;
-      w.cand_idx[pos] = (unsigned)(base + (uint64_t)lane * 32 + p);
-      w.cand_val[pos] = val(p);
-      ++pos;
-    }
-  };
-  // deferred chunks (streamed before the bound was known): their g_e is in
-  // HBM / L2 by now (bulk stores waited for); emitted in streaming order
-  unsigned ndef = 0;
-  auto catch_up = [&]() {
-    if (!ndef) return;
-    if (kAdd && lane == 0) {
-      bulk_wait0();
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-    }
-    __syncwarp();
-    for (unsigned d = 0; d < ndef; ++d) {
-      const unsigned c = s_def[warp][d];
-      const float* src = ge + ((uint64_t)c << kChunkShift) + (uint64_t)lane * 32;
-      const uint64_t i0 = ((uint64_t)c << kChunkShift) + (uint64_t)lane * 32;
-      unsigned mask = 0;
-      if (c < nfull) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float4 r = __ldcg(reinterpret_cast<const float4*>(src) + j);
-          mask |= ((key_of(r.x) >= Lkey ? 1u : 0u) | (key_of(r.y) >= Lkey ? 2u : 0u) |
-                   (key_of(r.z) >= Lkey ? 4u : 0u) | (key_of(r.w) >= Lkey ? 8u : 0u)) << (4 * j);
-        }
-      } else {
-        for (int p = 0; p < 32; ++p)
-          if (i0 + p < G && key_of(__ldcg(src + p)) >= Lkey) mask |= 1u << p;
-      }
-      emit(c, mask, [&](int p) { return __ldcg(src + p); });
-    }
-    ndef = 0;
-  };
-  auto poll = [&]() {  // (warp-uniform) has warp 0 published the bound?
-    unsigned r = 0;
-    if (lane == 0) r = *(volatile unsigned*)&s_lk_ready;
-    r = __shfl_sync(0xffffffffu, r, 0);
-    if (r) {
-      ready = true;
-      Lkey = s_lkey;
-    }
-    return r != 0;
-  };
-
   for (unsigned it = 0;; ++it) {
     const unsigned c = s_chunk[warp][it % kEfStages];
     if (c >= nchunks) break;
-    if (kEmit && !ready) {
-      if (!poll() && ndef == kMaxDefer) {  // the deferral list is full: wait for the bound
-        while (!poll()) __nanosleep(64);
-      }
-      if (ready) catch_up();
-    }
     double nacc = 0.0;
     const uint64_t base = (uint64_t)c << kChunkShift;
     const unsigned s = it % kEfStages;
@@ -828,7 +674,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
         t = fmaf(r.z, r.z, t);
         t = fmaf(r.w, r.w, t);
         nacc += (double)t;
-        if (kEmit && ready) {
+        if (kEmit) {
           const unsigned m4 = (key_of(r.x) >= Lkey ? 1u : 0u) | (key_of(r.y) >= Lkey ? 2u : 0u) |
                               (key_of(r.z) >= Lkey ? 4u : 0u) | (key_of(r.w) >= Lkey ? 8u : 0u);
           mask |= m4 << (q * 4);
@@ -852,7 +698,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
             r = __fadd_rn(g_o[i], r);
             ge[i] = r;
           }
-          if (kEmit && ready && key_of(r) >= Lkey) mask |= 1u << p;
+          if (kEmit && key_of(r) >= Lkey) mask |= 1u << p;
         }
         sge[lane * 32 + p] = r;
         nacc += (double)(r * r);
@@ -864,12 +710,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
       if (lane == 0) w.cnorm[c] = nacc;
     }
     if (kEmit) {
-      if (ready) {
-        const float* my = sge + lane * 32;
-        emit(c, mask, [&](int p) { return my[p]; });
-      } else {
-        if (lane == 0) s_def[warp][ndef] = c;
-        ++ndef;
+      // lane order == index order: one warp scan places every candidate
+      const unsigned n = __popc(mask);
+      unsigned incl = n;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned x = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += x;
+      }
+      const unsigned run = __shfl_sync(0xffffffffu, incl, 31);
+      if (lane == 0) {
+        w.cnt[c] = run;
+        ncand += run;
+      }
+      // packed candidate layout: the runs of one batch back to back from the
+      // batch's first slot (a single chunk: its own slot)
+      if (lay.seg_start(c)) brun = 0;
+      unsigned pos = (lay.seg_base(c) << kChunkShift) + brun + incl - n;
+      brun += run;
+      if (lane == 0 && lay.seg_last(c, nchunks)) w.segcnt[lay.seg_id(c)] = brun;  // the segment's total
+      const float* my = sge + lane * 32;
+      for (unsigned m = mask; m; m &= m - 1) {
+        const int p = __ffs(m) - 1;
+        const float x = my[p];
+        w.cand_idx[pos] = (unsigned)(base + (uint64_t)lane * 32 + p);
+        w.cand_val[pos] = x;
+        ++pos;
       }
     }
     if (c < nfull) {
@@ -879,10 +745,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
         issue(it + kEfStages);
       }
     }
-  }
-  if (kEmit && !ready) {  // every chunk of this warp streamed before the bound
-    while (!poll()) __nanosleep(64);
-    catch_up();
   }
   pdl_trigger();
   if (lane == 0 && kAdd) bulk_wait0();
