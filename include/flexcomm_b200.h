@@ -376,6 +376,11 @@ int fc_diag_kernel_ms(fc_ctx* ctx, int which, int iters, double* ms_out);
  * (values loaded, window flushed, in-bin pass, indices staged, output
  * written, bounds fixed, 2 spare): out12 holds 24 values (block 0). */
 int fc_diag_select_phases(fc_ctx* ctx, int worker, uint64_t* out12);
+/* Layerwise segments of the last FC_LAYERWISE step (diagnostics): per
+ * segment 26 words -- layer length, blocks, and the 24 phase marks of
+ * fc_diag_select_phases from the segment's own control block; at most nmax
+ * segments, their number in *nseg. */
+int fc_diag_seg_phases(fc_ctx* ctx, int worker, uint64_t* out, int nmax, int* nseg);
 /* Diagnostics: %globaltimer (ns) at the start and end of every EF block of the
  * last step (2 x grid values, grid = number of SMs), followed (as n allows) by
  * the last decode's start and end and the peer exchange's marks: fetch-gather

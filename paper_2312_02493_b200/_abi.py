@@ -165,6 +165,7 @@ def _load() -> C.CDLL:
         "fc_moo_metrics": ([P, i, C.POINTER(fc_step_stats), C.POINTER(d), C.POINTER(d)], i),
         "fc_peer_exchange": ([P, C.POINTER(i)], i),
         "fc_aggregate_in_place": ([P, C.POINTER(i)], i),
+        "fc_diag_seg_phases": ([P, i, C.POINTER(u64), i, C.POINTER(i)], i),
         "fc_set_peer_timeout": ([P, d], i),
         "fc_diag_exchange_ms": ([P, i, u64, i, C.POINTER(d)], i),
         "fc_set_grad_f64": ([P, i, P], i),
@@ -196,7 +197,7 @@ EXPORTS = [
     "fc_derive_m_from_ag",
     "fc_controller_config_validate", "fc_round_3sig", "fc_candidate_ladder", "fc_trigger_gain",
     "fc_pareto_front", "fc_choose_cr", "fc_network_changed", "fc_moo_metrics", "fc_peer_exchange",
-    "fc_aggregate_in_place",
+    "fc_aggregate_in_place", "fc_diag_seg_phases",
     "fc_set_peer_timeout", "fc_diag_exchange_ms", "fc_set_grad_f64", "fc_set_residual_f64",
     "fc_get_residual_f64", "fc_get_aggregate_f64", "fc_peer_handle", "fc_peer_attach",
 ]

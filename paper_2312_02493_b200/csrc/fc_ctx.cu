@@ -1681,6 +1681,31 @@ int fc_diag_select_phases(fc_ctx* c, int worker, uint64_t* out12) {
   return FC_OK;
 }
 
+int fc_diag_seg_phases(fc_ctx* c, int worker, uint64_t* out, int nmax, int* nseg) {
+  TRY(check_worker(c, worker));
+  if (!out || !nseg || nmax < 0) return fail(FC_ERR_INVALID_ARGUMENT, "bad output");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  Worker& w = c->w[worker];
+  *nseg = 0;
+  if (!c->h_seg || c->seg_groups == 0 || !w.seg_ctl[0]) return FC_OK;
+  const int par = w.seg_par ^ 1;  // the parity the last layerwise step used
+  int n = 0;
+  for (int g = 0; g < c->seg_groups; ++g) {
+    const fcb::SegTab& t = c->h_seg[((size_t)worker * 2 + par) * c->seg_groups + g];
+    for (int q = 0; q < t.n && n < nmax; ++q, ++n) {
+      // per segment: len, blocks, then 24 marks (select tphase[8],
+      // tphase_ef[4], tphase_ef2[4], tphase_sx[8]) of its block 0
+      uint64_t* o = out + (size_t)n * 26;
+      o[0] = t.e[q].len;
+      o[1] = t.e[q].nb;
+      CUDA_TRY(cudaMemcpy(o + 2, &t.e[q].ctl->tphase[0], 24 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    }
+  }
+  *nseg = n;
+  return FC_OK;
+}
+
 int fc_diag_ef_blocks(fc_ctx* c, int worker, uint64_t* out, int n) {
   TRY(check_worker(c, worker));
   if (!out || n < 0) return fail(FC_ERR_INVALID_ARGUMENT, "bad output");
