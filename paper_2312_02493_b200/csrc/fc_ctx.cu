@@ -152,8 +152,9 @@ struct fc_ctx {
   fcb::SegTab* h_seg = nullptr;
   fcb::SegTab* d_seg = nullptr;
   size_t seg_tab_cap = 0;       // tables h_seg / d_seg hold
+  size_t seg_ntab = 0;          // EF tables; the select's follow them
   int seg_groups = 0;
-  std::vector<int> seg_blocks;  // co-resident blocks of each group's launches
+  std::vector<int> seg_blocks, seg_blocks_sel;  // co-resident blocks of each group's EF / select launch
   double seg_cr = -1.0;
   uint64_t seg_ktot = 0;
   double* dnorms = nullptr;
@@ -393,14 +394,18 @@ int build_segs(fc_ctx* c, double cr, uint64_t ktot) {
   CUDA_TRY(cudaStreamSynchronize(c->stream));  // the previous tables are no longer read
   c->seg_groups = ng;
   c->seg_blocks.assign(ng, 0);
+  c->seg_blocks_sel.assign(ng, 0);
+  // tables [EF | select] x (worker, parity, group): the two launches split
+  // the blocks differently (below)
   const size_t ntab = (size_t)c->n_local * 2 * ng;
-  if (ntab > c->seg_tab_cap) {  // (kept across CR changes; grown only for a map with more groups)
+  if (2 * ntab > c->seg_tab_cap) {  // (kept across CR changes; grown only for a map with more groups)
     if (c->h_seg) cudaFreeHost(c->h_seg);
     c->h_seg = nullptr;
-    CUDA_TRY(cudaMallocHost(&c->h_seg, ntab * sizeof(fcb::SegTab)));
-    TRY(c->alloc(&c->d_seg, ntab));
-    c->seg_tab_cap = ntab;
+    CUDA_TRY(cudaMallocHost(&c->h_seg, 2 * ntab * sizeof(fcb::SegTab)));
+    TRY(c->alloc(&c->d_seg, 2 * ntab));
+    c->seg_tab_cap = 2 * ntab;
   }
+  c->seg_ntab = ntab;
   if (ng == 0) {
     c->seg_cr = cr;
     c->seg_ktot = ktot;
@@ -429,26 +434,34 @@ int build_segs(fc_ctx* c, double cr, uint64_t ktot) {
     for (int g = 0; g < ng; ++g) {
       const size_t a = (size_t)g * fcb::kMaxSegs, b = std::min(big.size(), a + fcb::kMaxSegs);
       const int n = (int)(b - a);
-      // blocks by length: at least one each, the rest proportionally
+      // blocks by length, at least `floor` each, the rest proportionally.
+      // The EF pass streams (its time ~ the longest per-block slice):
+      // floor 1.  The select is latency-bound per block (a one-block
+      // segment runs every phase over all its candidates alone): floor 3.
       uint64_t lsum = 0;
       for (size_t q = a; q < b; ++q) lsum += big[q].len;
-      std::vector<unsigned> nb(n, 1);
-      unsigned left = total > (unsigned)n ? total - n : 0;
-      unsigned used = 0;
-      for (int q = 0; q < n; ++q) {
-        const unsigned x = (unsigned)((double)left * (double)big[a + q].len / (double)lsum);
-        nb[q] += x;
-        used += x;
-      }
-      for (unsigned r = used; r < left; ++r) {  // remainder to the largest layers' shares
-        int best = 0;
-        double worst = 0.0;
+      auto split = [&](unsigned floor) {
+        if ((unsigned)n * floor > total) floor = 1;
+        std::vector<unsigned> nb(n, floor);
+        unsigned left = total > (unsigned)n * floor ? total - n * floor : 0;
+        unsigned used = 0;
         for (int q = 0; q < n; ++q) {
-          const double per = (double)big[a + q].len / nb[q];
-          if (per > worst) worst = per, best = q;
+          const unsigned x = (unsigned)((double)left * (double)big[a + q].len / (double)lsum);
+          nb[q] += x;
+          used += x;
         }
-        ++nb[best];
-      }
+        for (unsigned r = used; r < left; ++r) {  // remainder to the largest layers' shares
+          int best = 0;
+          double worst = 0.0;
+          for (int q = 0; q < n; ++q) {
+            const double per = (double)big[a + q].len / nb[q];
+            if (per > worst) worst = per, best = q;
+          }
+          ++nb[best];
+        }
+        return nb;
+      };
+      const std::vector<unsigned> nb = split(1), nbs = split(3);
       unsigned b0 = 0;
       uint64_t co = 0;  // chunk offset of the layer in the worker's arrays
       for (int p = 0; p < 2; ++p) {
@@ -484,16 +497,29 @@ int build_segs(fc_ctx* c, double cr, uint64_t ktot) {
           e.idx_base = (unsigned)L.off;
           e.out_idx = w.pack + L.acc;
           e.out_val = vals + L.acc;
-          if (!fcb::select_fits(nch, nb[q], e.ws.batch))
-            return fail(FC_ERR_OUT_OF_RANGE, "layer too long for its share of the segmented select");
           b0 += nb[q];
           co += nch;
         }
+        // the select's table: the same segments over its own block split
+        fcb::SegTab& ts = c->h_seg[ntab + ((size_t)i * 2 + p) * ng + g];
+        ts = t;
+        unsigned s0 = 0;
+        for (int q = 0; q < n; ++q) {
+          fcb::SegEntry& e = ts.e[q];
+          e.ws.bnorm = w.ws.bnorm + s0;
+          e.ws.tblk = w.ws.tblk + 2 * (uint64_t)s0;
+          e.b0 = s0;
+          e.nb = nbs[q];
+          if (!fcb::select_fits(e.ws.nchunks, nbs[q], e.ws.batch))
+            return fail(FC_ERR_OUT_OF_RANGE, "layer too long for its share of the segmented select");
+          s0 += nbs[q];
+        }
+        c->seg_blocks_sel[g] = (int)s0;
       }
       c->seg_blocks[g] = (int)b0;
     }
   }
-  CUDA_TRY(cudaMemcpyAsync(c->d_seg, c->h_seg, ntab * sizeof(fcb::SegTab), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->d_seg, c->h_seg, 2 * ntab * sizeof(fcb::SegTab), cudaMemcpyHostToDevice, c->stream));
   c->seg_cr = cr;
   c->seg_ktot = ktot;
   return FC_OK;
@@ -555,7 +581,7 @@ int run_layerwise(fc_ctx* c, int i, double cr, uint64_t ktot) {
     int e = fcb::launch_ef_segs(tab, c->seg_blocks[g], 1 | force_fb, coop, c->stream);
     if (e) return fail(FC_ERR_CUDA, std::string("k_ef (segments) launch: ") + cudaGetErrorString(static_cast<cudaError_t>(e)));
     LAUNCHED();
-    e = fcb::launch_select_segs(tab, c->seg_blocks[g], coop, c->stream);
+    e = fcb::launch_select_segs(tab + c->seg_ntab, c->seg_blocks_sel[g], coop, c->stream);
     if (e) return fail(FC_ERR_CUDA, std::string("k_select_x (segments) launch: ") + cudaGetErrorString(static_cast<cudaError_t>(e)));
     LAUNCHED();
   }

@@ -450,6 +450,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
                                                     const SegTab* __restrict__ seg) {
   pdl_wait();
   extern __shared__ __align__(128) unsigned char s_ring[];
+  // ring per warp: 3 stages of (g_e | g_o | zero map) when adding; the
+  // emission-only pass (layer segments) loads g_e alone, so the same bytes
+  // hold 6 stages of one chunk -- twice the loads in flight per SM
+  constexpr int kSt = kAdd ? kEfStages : 2 * kEfStages;
+  constexpr unsigned kSB = kAdd ? kStageBytes : kStageBytes / 2;
+  static_assert(kAdd || !kPend, "the emission-only ring has no zero-map slot");
   unsigned bid = blockIdx.x, nblk = gridDim.x;  // this block within its (segment's) grid
   if (kSeg) {
     int si = 0;
@@ -468,14 +474,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
   if (threadIdx.x == 0) w.tblk[2 * bid] = gtimer();
   __shared__ unsigned s_hist[kEmit ? kBins1 : 1];  // sample histogram, then the bound's staging
   __shared__ unsigned s_sub[kEmit ? kSpecBins * 256 : 1];  // speculative level-2 histograms
-  __shared__ __align__(8) unsigned long long s_bar[kEfWarps][kEfStages];
-  __shared__ unsigned s_chunk[kEfWarps][kEfStages];  // chunk held by each stage
+  __shared__ __align__(8) unsigned long long s_bar[kEfWarps][2 * kEfStages];
+  __shared__ unsigned s_chunk[kEfWarps][2 * kEfStages];  // chunk held by each stage
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned sw = lane & 7;  // LDS.128 swizzle
-  unsigned char* ring = s_ring + warp * kEfStages * kStageBytes;
+  unsigned char* ring = s_ring + warp * kSt * kSB;
   unsigned ncand = 0;  // candidates emitted by this warp (lane 0)
   if (lane == 0) {
-    for (int s = 0; s < kEfStages; ++s) mbar_init(&s_bar[warp][s], 1);
+    for (int s = 0; s < kSt; ++s) mbar_init(&s_bar[warp][s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (ctl_next) {
@@ -527,13 +533,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
     return q_next++;
   };
   unsigned brun = 0;  // candidates this warp emitted so far in the current batch
-  auto issue = [&](unsigned it) {  // lane 0 only: take the next chunk into stage it % kEfStages
-    const unsigned s = it % kEfStages;
+  auto issue = [&](unsigned it) {  // lane 0 only: take the next chunk into stage it % kSt
+    const unsigned s = it % kSt;
     const unsigned c = take();
     s_chunk[warp][s] = c;
     if (c >= nfull) return;  // past the end, or the partial last chunk (plain loads)
     unsigned long long* bar = &s_bar[warp][s];
-    unsigned char* st = ring + s * kStageBytes;
+    unsigned char* st = ring + s * kSB;
     const uint64_t base = (uint64_t)c << kChunkShift;
     mbar_expect_tx(bar, kTx);
     bulk_g2s(st, ge + base, kChunk * 4, bar);
@@ -541,7 +547,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
     if (kPend) bulk_g2s(st + 2 * kChunk * 4, pz.zmap + ((uint64_t)c << 5), 128, bar);
   };
   if (lane == 0)
-    for (int s = 0; s < kEfStages; ++s) issue(s);
+    for (int s = 0; s < kSt; ++s) issue(s);
   __syncwarp();
 
   // candidate bound: derived while the first stages are in flight, before any
@@ -638,15 +644,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
   }
 
   for (unsigned it = 0;; ++it) {
-    const unsigned c = s_chunk[warp][it % kEfStages];
+    const unsigned c = s_chunk[warp][it % kSt];
     if (c >= nchunks) break;
     double nacc = 0.0;
     const uint64_t base = (uint64_t)c << kChunkShift;
-    const unsigned s = it % kEfStages;
-    float* sge = reinterpret_cast<float*>(ring + s * kStageBytes);
+    const unsigned s = it % kSt;
+    float* sge = reinterpret_cast<float*>(ring + s * kSB);
     unsigned mask = 0;  // bit p: element base + 32*lane + p is a candidate
     if (c < nfull) {
-      mbar_wait(&s_bar[warp][s], (it / kEfStages) & 1u);
+      mbar_wait(&s_bar[warp][s], (it / kSt) & 1u);
       float4* r4 = reinterpret_cast<float4*>(sge) + lane * 8;
       const float4* a4 = reinterpret_cast<const float4*>(sge + kChunk) + lane * 8;
       const unsigned zm = kPend ? reinterpret_cast<const unsigned*>(sge + 2 * kChunk)[lane] : 0u;
@@ -742,7 +748,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
       __syncwarp();  // all lanes done with stage s
       if (lane == 0) {
         if (kAdd) bulk_wait_read0();  // the g_e bulk store has read the stage
-        issue(it + kEfStages);
+        issue(it + kSt);
       }
     }
   }
@@ -1827,6 +1833,7 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
   using U1 = std::integral_constant<int, 1>;
   using U2 = std::integral_constant<int, 2>;
   using U4 = std::integral_constant<int, 4>;
+  using U8 = std::integral_constant<int, 8>;
   // passes over the shared-memory-staged candidates run one 128-position
   // group per loop iteration (a pass's instruction footprint is one f body:
   // 1.5 us less per select than 4 unrolled copies); global-memory passes
@@ -1843,7 +1850,7 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
   const unsigned wb = Lb >> 11;
   for (int b = tid; b < kSelBins; b += kSxThreads) s_h[b] = 0;
   __syncthreads();
-  pass(U4{}, false, false, cached, [&](const float4& v, const uint4&, unsigned nv) {
+  pass(U8{}, false, false, cached, [&](const float4& v, const uint4&, unsigned nv) {
     for (unsigned e = 0; e < nv; ++e) {
       const unsigned hi = key_of(f4c(v, e)) >> 11;
       if (hi >= wb) atomicAdd(&s_h[min(hi - wb, (unsigned)kSelBins - 1u)], 1u);
@@ -2023,7 +2030,7 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
   {
     unsigned long long grun = s_wpre[warp] >> 32, erun = s_wpre[warp] & 0xffffffffull;
     const unsigned ibase = mode.idx_base;
-    run(U2{}, cached, true, false, [&](const float4& v, const uint4& id, unsigned nv) {
+    run(U4{}, cached, true, false, [&](const float4& v, const uint4& id, unsigned nv) {
       unsigned gm = 0, em = 0;
       for (unsigned e = 0; e < nv; ++e) {
         const unsigned key = key_of(f4c(v, e));
