@@ -440,8 +440,9 @@ __device__ __forceinline__ void fence_proxy_async() {
 
 // opts bit 0: derive the candidate bound from a fused sample (one grid
 // barrier between sampling and streaming); bit 1: force the
-// fallback (tests).  ctl_next (nullable): the worker's other control block,
-// zeroed here for the next step.
+// fallback (tests); bit 2: every element is a candidate; bit 3 (emission-
+// only passes): skip the per-chunk ||g_e||^2.  ctl_next (nullable): the
+// worker's other control block, zeroed here for the next step.
 template <bool kAdd, bool kEmit, bool kPend, bool kSeg = false>
 __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_o,
                                                     float* __restrict__ ge, uint64_t G, uint64_t k,
@@ -489,6 +490,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
     for (unsigned q = bid * kThreads + tid; q < sizeof(Ctl) / 4; q += nblk * kThreads) z[q] = 0u;
   }
   const bool sampling = kEmit && (opts & 1);
+  const bool want_norm = kAdd || !(opts & 8);  // opts & 8: no per-chunk ||g_e||^2 (layer segments)
   const unsigned lastb1 = sampling ? __ldcg(w.lastb1) : 0u;  // previous step's target bucket + 1 (0: none)
   __syncthreads();
 
@@ -675,11 +677,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
           r.w = __fadd_rn(a.w, r.w);
           r4[q] = r;  // g_e back into the stage, for the bulk store
         }
-        float t = r.x * r.x;
-        t = fmaf(r.y, r.y, t);
-        t = fmaf(r.z, r.z, t);
-        t = fmaf(r.w, r.w, t);
-        nacc += (double)t;
+        if (want_norm) {
+          float t = r.x * r.x;
+          t = fmaf(r.y, r.y, t);
+          t = fmaf(r.z, r.z, t);
+          t = fmaf(r.w, r.w, t);
+          nacc += (double)t;
+        }
         if (kEmit) {
           const unsigned m4 = (key_of(r.x) >= Lkey ? 1u : 0u) | (key_of(r.y) >= Lkey ? 2u : 0u) |
                               (key_of(r.z) >= Lkey ? 4u : 0u) | (key_of(r.w) >= Lkey ? 8u : 0u);
@@ -710,7 +714,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
         nacc += (double)(r * r);
       }
     }
-    {  // this chunk's sum of squares (fixed lane tree: reproducible per chunk)
+    if (want_norm) {  // this chunk's sum of squares (fixed lane tree: reproducible per chunk)
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) nacc += __shfl_xor_sync(0xffffffffu, nacc, o);
       if (lane == 0) w.cnorm[c] = nacc;
@@ -794,6 +798,7 @@ int launch_ef_segs(const SegTab* d_tab, int nblocks, int opts, bool coop, cudaSt
   ChunkWs ws{};
   Pending pz{};
   Ctl* ctl_next = nullptr;
+  opts |= 8;  // (the layers' norms are never read: ||g_e||^2 comes from the full pass)
   void* args[] = {&g_o, &ge, &G, &k, &ctl, &ws, &pz, &opts, &ctl_next, &d_tab};
   const int e = (int)launch_grid_sync((const void*)k_ef<false, true, false, true>, dim3(nblocks), dim3(kThreads),
                                       kEfRingBytes, s, args, coop);
@@ -1833,7 +1838,6 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
   using U1 = std::integral_constant<int, 1>;
   using U2 = std::integral_constant<int, 2>;
   using U4 = std::integral_constant<int, 4>;
-  using U8 = std::integral_constant<int, 8>;
   // passes over the shared-memory-staged candidates run one 128-position
   // group per loop iteration (a pass's instruction footprint is one f body:
   // 1.5 us less per select than 4 unrolled copies); global-memory passes
@@ -1850,7 +1854,7 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
   const unsigned wb = Lb >> 11;
   for (int b = tid; b < kSelBins; b += kSxThreads) s_h[b] = 0;
   __syncthreads();
-  pass(U8{}, false, false, cached, [&](const float4& v, const uint4&, unsigned nv) {
+  pass(U4{}, false, false, cached, [&](const float4& v, const uint4&, unsigned nv) {
     for (unsigned e = 0; e < nv; ++e) {
       const unsigned hi = key_of(f4c(v, e)) >> 11;
       if (hi >= wb) atomicAdd(&s_h[min(hi - wb, (unsigned)kSelBins - 1u)], 1u);
@@ -2030,7 +2034,7 @@ __global__ void __launch_bounds__(kSxThreads, 1) k_select_x(uint64_t k, Ctl* __r
   {
     unsigned long long grun = s_wpre[warp] >> 32, erun = s_wpre[warp] & 0xffffffffull;
     const unsigned ibase = mode.idx_base;
-    run(U4{}, cached, true, false, [&](const float4& v, const uint4& id, unsigned nv) {
+    run(U2{}, cached, true, false, [&](const float4& v, const uint4& id, unsigned nv) {
       unsigned gm = 0, em = 0;
       for (unsigned e = 0; e < nv; ++e) {
         const unsigned key = key_of(f4c(v, e));
