@@ -25,11 +25,16 @@ def _run(nproc, script, args, extra_env=None, marker="MP_CHECK PASS", min_gpus=N
     need = nproc if min_gpus is None else min_gpus
     if torch.cuda.device_count() < need:
         pytest.skip(f"needs {need} GPUs")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
-           f"--nproc-per-node={nproc}", "--master-addr", "127.0.0.1",
-           "--master-port", str(_free_port()), str(ROOT / script), *args]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
-                       env={**os.environ, "OMP_NUM_THREADS": "1", **(extra_env or {})})
+    for attempt in range(3):
+        # (a port found free can be taken by another process before the
+        # rendezvous binds it: retry with a new one on EADDRINUSE only)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={nproc}", "--master-addr", "127.0.0.1",
+               "--master-port", str(_free_port()), str(ROOT / script), *args]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600,
+                           env={**os.environ, "OMP_NUM_THREADS": "1", **(extra_env or {})})
+        if r.returncode == 0 or "EADDRINUSE" not in r.stdout + r.stderr:
+            break
     assert r.returncode == 0 and marker in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
 
 
