@@ -2690,9 +2690,6 @@ __global__ void k_agg_update(const unsigned* __restrict__ prev, uint64_t kp, con
                              PeerBufs pb, int par, unsigned long long epoch, int wait_root,
                              const int* __restrict__ dsel, int write_new) {
   pdl_wait();
-  // the next step's EF may be scheduled now: its own griddepcontrol.wait
-  // still waits for this grid's completion and memory (launch latency hidden)
-  pdl_trigger();
   if (kPeers) {
     if (blockIdx.x == 0 && threadIdx.x == 0) g_tdiag[5] = gtimer();  // (diagnostics: wait start)
     if (wait_root == -1) {
