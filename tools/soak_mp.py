@@ -1,6 +1,7 @@
 """Long-run soak of the multi-GPU exchange (peer memory or NCCL): STEPS
-back-to-back steps cycling STAR / VAR (Ring), STAR / VAR (Tree) and AG with
-the residual carried, one
+back-to-back steps cycling STAR / VAR (Ring), STAR / VAR (Tree) and AG, and
+CR 0.01 / 0.003 / 0.05 (the aggregate updated in place, then rewritten
+whole, then in place again), with the residual carried, one
 rank per GPU.  Rank 0 follows the same trajectory with the fp32 oracle (the
 checker) and compares every rank's aggregate and residual bit-exact every
 CHECK steps and at the last step — exercises the mailbox epochs and parity
@@ -31,13 +32,14 @@ def main():
     f32 = oracle.F32() if env.rank == 0 else None
     res = np.zeros((env.world, G), np.float32) if env.rank == 0 else None
     kinds = ("star", "var", "ag", "star-tree", "var-tree")
-    c = 0.01
+    crs = (0.01, 0.003, 0.05)
     failures, checks = [], 0
     t0 = time.time()
     with fc.Cluster.nccl(env.world, env.rank, uid, G, device=env.local_rank, max_cr=0.05) as cl:
         p2p = cl.peer_exchange
         for s in range(steps):
-            kind = kinds[s % 3]
+            kind = kinds[s % len(kinds)]
+            c = crs[(s // len(kinds)) % len(crs)]
             cl.fill_synthetic(0, 99, env.rank, s)
             sel = -1
             if kind == "ag":
