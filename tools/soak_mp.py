@@ -48,7 +48,7 @@ def main():
                 sel = cl.artopk_step(c, fc.STAR if kind.startswith("star") else fc.VAR,
                                      fc.TREE if kind.endswith("tree") else fc.RING, s, fc.AVG).selected_rank
             last = s == steps - 1
-            do_check = last or (s + 1) % check == 0
+            do_check = last or (s + 1) % check == 0 or s < 2 * len(kinds)
             if do_check:
                 aggs = env.gather_arrays(cl.aggregate())
                 resid = env.gather_arrays(cl.residual(0))
@@ -72,7 +72,12 @@ def main():
                 if exact and not np.array_equal(aggs[r].view(np.uint32), ref.view(np.uint32)):
                     failures.append(f"step {s} {kind}: aggregate on rank {r} not bit-exact")
                 if not exact and not np.allclose(aggs[r], ref, rtol=1e-5, atol=1e-30):
-                    failures.append(f"step {s} {kind}: aggregate on rank {r} off")
+                    d = np.abs(aggs[r].astype(np.float64) - ref)
+                    j = int(np.argmax(d))
+                    bad = ~np.isclose(aggs[r], ref, rtol=1e-5, atol=1e-30)
+                    failures.append(f"step {s} {kind} c={c}: aggregate on rank {r} off: {int(bad.sum())} elements, "
+                                    f"max |diff| {d[j]:.3g} at {j} (got {aggs[r][j]:.9g}, want {ref[j]:.9g}), "
+                                    f"nonzero got/want {int((aggs[r] != 0).sum())}/{int((ref != 0).sum())}")
     if env.rank == 0:
         print(f"[soak_mp] world={env.world} G={G} steps={steps} peer={p2p} checks={checks} "
               f"failures={len(failures)} wall={time.time() - t0:.1f}s", flush=True)
