@@ -71,12 +71,14 @@ def main():
                 exact = kind == "ag" or p2p
                 if exact and not np.array_equal(aggs[r].view(np.uint32), ref.view(np.uint32)):
                     failures.append(f"step {s} {kind}: aggregate on rank {r} not bit-exact")
-                if not exact and not np.allclose(aggs[r], ref, rtol=1e-5, atol=1e-30):
-                    d = np.abs(aggs[r].astype(np.float64) - ref)
-                    j = int(np.argmax(d))
-                    bad = ~np.isclose(aggs[r], ref, rtol=1e-5, atol=1e-30)
+                # NCCL sums in its own order: 1e-5 relative, cancellation-safe
+                # (a sum that cancels to ~0 keeps the summands' rounding)
+                tol = 1e-5 * np.abs(ref) + 1e-6 * float(np.abs(ref).max(initial=0.0)) + 1e-30
+                bad = np.abs(aggs[r].astype(np.float64) - ref) > tol
+                if not exact and bad.any():
+                    j = int(np.argmax(bad))
                     failures.append(f"step {s} {kind} c={c}: aggregate on rank {r} off: {int(bad.sum())} elements, "
-                                    f"max |diff| {d[j]:.3g} at {j} (got {aggs[r][j]:.9g}, want {ref[j]:.9g}), "
+                                    f"first at {j} (got {aggs[r][j]:.9g}, want {ref[j]:.9g}), "
                                     f"nonzero got/want {int((aggs[r] != 0).sum())}/{int((ref != 0).sum())}")
     if env.rank == 0:
         print(f"[soak_mp] world={env.world} G={G} steps={steps} peer={p2p} checks={checks} "
