@@ -2591,10 +2591,18 @@ __global__ void __launch_bounds__(kThreads) k_fetch_gather(PeerBufs pb, int sel,
     if (peer4) {
       __stcg(peer4 + q, g4);
     } else if (slices) {
-      const float g[4] = {g4.x, g4.y, g4.z, g4.w};
+      // the quad's four values go to their slice owners' inboxes: one
+      // 16-byte push when one owner holds all four (every quad but the few
+      // straddling a slice edge), else four 4-byte pushes
+      const int o0 = slice_owner(j, k, n);
+      if (j + 3 < k && slice_owner(j + 3, k, n) == o0) {
+        __stcg(reinterpret_cast<float4*>(inbox_of(pb, o0, me, par) + j), g4);
+      } else {
+        const float g[4] = {g4.x, g4.y, g4.z, g4.w};
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (j + e < k) __stcg(inbox_of(pb, slice_owner(j + e, k, n), me, par) + j + e, g[e]);
+        for (int e = 0; e < 4; ++e)
+          if (j + e < k) __stcg(inbox_of(pb, slice_owner(j + e, k, n), me, par) + j + e, g[e]);
+      }
     }
     ci = ni;
     cv = nv;
