@@ -108,6 +108,10 @@ struct fc_ctx {
   // FC_HOST_ASYNC copies: an upload stream and a download stream, ordered
   // against the compute stream with events
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  // ART-Ring slice ranks clear the previous support beside their
+  // reduce-scatter kernel: fork / join events around this stream
+  cudaStream_t s_aux = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // per (gradient set, worker): upload done / last kernel reading it done
   std::vector<cudaEvent_t> ev_go_ready, ev_go_free;
   std::vector<char> go_pending, go_read;
@@ -789,6 +793,9 @@ static int create_impl(fc_ctx* c, const fc_opts* o) {
   CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   CUDA_TRY(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
   CUDA_TRY(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&c->s_aux, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
   for (int b = 0; b < 2; ++b) {
     CUDA_TRY(cudaEventCreateWithFlags(&c->ev_agg_ready[b], cudaEventDisableTiming));
@@ -1048,6 +1055,7 @@ int fc_destroy(fc_ctx* c) {
   if (c->s_h2d) cudaStreamSynchronize(c->s_h2d);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->s_d2h) cudaStreamSynchronize(c->s_d2h);
+  if (c->s_aux) cudaStreamSynchronize(c->s_aux);
   // Peer memory: a peer may still be reading this rank's exchange buffer
   // (AG's collect_packs waits only for the publish, not for the readers), so
   // every rank first passes a barrier that is stream-ordered after all of its
@@ -1082,6 +1090,9 @@ int fc_destroy(fc_ctx* c) {
   if (c->stream) cudaStreamDestroy(c->stream);
   if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
   if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
+  if (c->s_aux) cudaStreamDestroy(c->s_aux);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   for (auto e : c->ev_go_ready)
     if (e) cudaEventDestroy(e);
   for (auto e : c->ev_go_free)
@@ -1862,7 +1873,8 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
   // break-even sets incr_div
   const bool incr_ok = !(c->flags & FC_FLAG_DENSE_DECODE) && c->nbuf == 1 && c->incr_div &&
                        k * c->incr_div <= c->G;
-  bool early_clear = false;  // the previous support cleared before the exchange's waits
+  bool early_clear = false;
+  bool aux_join = false;  // the clear ran on s_aux: join before the write  // the previous support cleared before the exchange's waits
 
   // (3) broadcast of the selected index set, gather, allreduce of the k
   //     values (artopk.hpp:87-104); the zeros at bidx become owed zeros
@@ -1889,16 +1901,26 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
     // this rank waits for its peers (the selected rank for the others'
     // contributions, the others for the root's or the peer's values).  An
     // ART-Ring rank that reduces a slice for the others has no such window
-    // (before its slice the clear delays everyone's decode, after it its
-    // own): it updates in one kernel after the waits (timelines: N = 4
-    // ring 0.521 merged, 0.525 / 0.532 ms with the clear before / after the
-    // slice)
+    // on its stream (the clear would delay its slice, hence everyone's
+    // decode: N = 4 0.525 ms): it clears on the auxiliary stream beside
+    // the slice kernel
     const bool ring_slice = algo != FC_TREE && N > 2 && (mode == FC_VAR || c->rank != sel);
-    if (incr_ok && c->agg_incr && c->agg_support_k && !ring_slice) {
+    if (incr_ok && c->agg_incr && c->agg_support_k) {
       int ob0 = 0;
       TRY(agg_target(c, &ob0));
-      fcb::launch_agg_clear(c->agg_support, c->agg_support_k, bsrc, k, own_bounds, c->agg_buf[ob0], c->G,
-                            c->zmaps, c->stream);
+      if (!ring_slice) {
+        fcb::launch_agg_clear(c->agg_support, c->agg_support_k, bsrc, k, own_bounds, c->agg_buf[ob0], c->G,
+                              c->zmaps, c->stream);
+      } else {
+        // beside the reduce-scatter slice (an NVLink-bound kernel), on the
+        // auxiliary stream; the write joins it after the waits
+        CUDA_TRY(cudaEventRecord(c->ev_fork, c->stream));
+        CUDA_TRY(cudaStreamWaitEvent(c->s_aux, c->ev_fork, 0));
+        fcb::launch_agg_clear(c->agg_support, c->agg_support_k, bsrc, k, own_bounds, c->agg_buf[ob0], c->G,
+                              c->zmaps, c->s_aux);
+        CUDA_TRY(cudaEventRecord(c->ev_join, c->s_aux));
+        aux_join = true;
+      }
       early_clear = true;
     }
   } else if (c->nccl && N == 1) {
@@ -1986,6 +2008,7 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
       fcb::launch_reduce_root(c->pb, par, epoch, k, op == FC_AVG, (float)N, mode == FC_STAR ? sel : -1, c->dsel,
                               c->w[0].ctl, c->stream);
     const int wait_root = tree ? (mode == FC_STAR ? sel : -2) : -1;
+    if (aux_join) CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
     if (incr_ok && c->agg_incr) {
       fcb::launch_agg_update_peers(c->pb, par, epoch, c->agg_support, early_clear ? 0 : c->agg_support_k, bsrc, k,
                                    own_bounds,
