@@ -66,7 +66,6 @@ struct Ctl {
   unsigned hist_w[4096];     // window histogram: key bits 30..11 relative to Lkey (k_select)
   unsigned done_sel;         // k_select_x: last-block counter (finalisation)
   unsigned done_slice;       // k_fetch_gather two-stage broadcast: slice pulled
-  unsigned gq_next;          // k_fetch_gather: next quad batch (ticket)
   unsigned lb_flag[kMaxGrid];             // k_select_x look-back: block b's total is in
   unsigned long long lb_tot[kMaxGrid];    // ... (gt << 32) | eq of block b
 };

@@ -2391,7 +2391,6 @@ __device__ __forceinline__ float ld_scattered(const float* p) {
 // sum_j g_e[bidx[j]]^2 for the gain (trainer.hpp:387-396).  The residual
 // zeros at bidx are owed, not written (Pending).
 constexpr int kGatherUnroll = 4;
-constexpr unsigned kGatherBatch = 128;  // quads per ticket of the peer gather (4 per lane)
 __global__ void __launch_bounds__(kThreads) k_gather(const unsigned* __restrict__ bidx, uint64_t k,
                                                      const float* __restrict__ ge,
                                                      float* __restrict__ contrib,
@@ -2560,12 +2559,26 @@ __global__ void __launch_bounds__(kThreads) k_fetch_gather(PeerBufs pb, int sel,
       publish_all(pb, 3, epoch);  // my slice is in my list (the other helpers pull it)
     }
   }
-  // groups of 4 consecutive list positions (quads); warps take batches of
-  // kGatherBatch quads from a ticket counter (no straggler blocks: a block
-  // that drew slow NVLink / DRAM work takes fewer batches), lanes on
-  // consecutive quads, a batch's remote loads all issued before its local
-  // gathers (NVLink latency overlapped)
-  auto gather_quad = [&](uint64_t q, uint4 ci, uint4 cv) {
+  // groups of 4 consecutive list positions per thread, lanes on consecutive
+  // groups; the next group's remote loads are issued before this one's local
+  // gather (NVLink latency overlapped)
+  uint64_t q = t0;
+  uint4 ci = make_uint4(0, 0, 0, 0), cv = make_uint4(0, 0, 0, 0);
+  if (q < nq) {
+    const uint4* a = src_quad(q);
+    if (!a) return;  // (peer timeout reported)
+    ci = __ldcv(a);
+    if (pull_sel) cv = __ldcv(selv4 + q);
+  }
+  for (; q < nq; q += nt) {
+    const uint64_t qn = q + nt;
+    uint4 ni = make_uint4(0, 0, 0, 0), nv = make_uint4(0, 0, 0, 0);
+    if (qn < nq) {
+      const uint4* a = src_quad(qn);
+      if (!a) return;
+      ni = __ldcv(a);
+      if (pull_sel) nv = __ldcv(selv4 + qn);
+    }
     const uint64_t j = 4 * q;
     float4 g4;
     g4.x = ld_scattered(ge + ci.x);
@@ -2591,42 +2604,9 @@ __global__ void __launch_bounds__(kThreads) k_fetch_gather(PeerBufs pb, int sel,
           if (j + e < k) __stcg(inbox_of(pb, slice_owner(j + e, k, n), me, par) + j + e, g[e]);
       }
     }
-  };
-  constexpr unsigned kPerLane = kGatherBatch / 32;
-  const unsigned nbat = (unsigned)((nq + kGatherBatch - 1) / kGatherBatch);
-  const int lane = threadIdx.x & 31;
-  unsigned tk = 0;
-  if (lane == 0) tk = atomicAdd(&ctl->gq_next, 1u);
-  tk = __shfl_sync(0xffffffffu, tk, 0);
-  bool ok = true;
-  while (tk < nbat && ok) {
-    unsigned tn = 0;
-    if (lane == 0) tn = atomicAdd(&ctl->gq_next, 1u);  // the next ticket, drawn ahead
-    uint4 ci[kPerLane], cv[kPerLane];
-#pragma unroll
-    for (unsigned i = 0; i < kPerLane; ++i) {
-      const uint64_t q = (uint64_t)tk * kGatherBatch + i * 32 + lane;
-      ci[i] = make_uint4(0, 0, 0, 0);
-      cv[i] = make_uint4(0, 0, 0, 0);
-      if (q < nq) {
-        const uint4* a = src_quad(q);
-        if (!a) {
-          ok = false;  // (peer timeout reported)
-          continue;
-        }
-        ci[i] = __ldcv(a);
-        if (pull_sel) cv[i] = __ldcv(selv4 + q);
-      }
-    }
-#pragma unroll
-    for (unsigned i = 0; i < kPerLane; ++i) {
-      const uint64_t q = (uint64_t)tk * kGatherBatch + i * 32 + lane;
-      if (ok && q < nq) gather_quad(q, ci[i], cv[i]);
-    }
-    ok = __all_sync(0xffffffffu, ok);
-    tk = __shfl_sync(0xffffffffu, tn, 0);
+    ci = ni;
+    cv = nv;
   }
-  if (!ok) return;
   pdl_trigger();
   __syncthreads();
   if (threadIdx.x == 0) tblk[2 * blockIdx.x + 1] = gtimer();
