@@ -1827,6 +1827,13 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
   const int par = (int)(epoch & 1);
 
   if (!p2p_star) TRY(need_comm(c, "this step"));
+  // in-place update of the aggregate (§3.5): ~2k whole-sector writes
+  // (32 B each, scattered) against the 4G-byte dense write; the measured
+  // break-even (DESIGN §3.5) sets incr_div
+  const bool incr_ok = !(c->flags & FC_FLAG_DENSE_DECODE) && c->nbuf == 1 && c->incr_div &&
+                       k * c->incr_div <= c->G;
+  bool early_clear = false;  // the previous support cleared before the exchange's waits
+  bool aux_join = false;     // ... on s_aux: join before the write
   // (1) error feedback on every worker; Top-k where its result is consumed
   record(c, 0);
   for (int i = 0; i < c->n_local; ++i) {
@@ -1834,6 +1841,17 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
     TRY(run_ef(c, i, k, topk));
   }
   advance_input(c);
+  if (p2p_star && mode == FC_STAR && c->rank != sel && incr_ok && c->agg_incr && c->agg_support_k) {
+    // a STAR rank that does not select waits for the selected rank's list
+    // from here (~its select): the previous support's sectors are zeroed in
+    // that wait -- all of them (this step's list is not known yet; the write
+    // rewrites its own sectors after)
+    int ob0 = 0;
+    TRY(agg_target(c, &ob0));
+    fcb::launch_agg_clear(c->agg_support, c->agg_support_k, nullptr, 0, nullptr, c->agg_buf[ob0], c->G,
+                          c->zmaps, c->stream);
+    early_clear = true;
+  }
   record(c, 1);
   for (int i = 0; i < c->n_local; ++i) {
     const bool topk = mode == FC_VAR || (c->rank + i) == sel;
@@ -1868,13 +1886,6 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
       if (c->h_norms[r] > c->h_norms[sel]) sel = r;
   }
 
-  // in-place update of the aggregate (§3.5): ~2k whole-sector writes
-  // (32 B each, scattered) against the 4G-byte dense write; the measured
-  // break-even (DESIGN §3.5) sets incr_div
-  const bool incr_ok = !(c->flags & FC_FLAG_DENSE_DECODE) && c->nbuf == 1 && c->incr_div &&
-                       k * c->incr_div <= c->G;
-  bool early_clear = false;
-  bool aux_join = false;  // the clear ran on s_aux: join before the write  // the previous support cleared before the exchange's waits
 
   // (3) broadcast of the selected index set, gather, allreduce of the k
   //     values (artopk.hpp:87-104); the zeros at bidx become owed zeros
@@ -1905,7 +1916,7 @@ int fc_artopk_step(fc_ctx* c, double cr, int mode, int algo, long step, int op, 
     // decode: N = 4 0.525 ms): it clears on the auxiliary stream beside
     // the slice kernel
     const bool ring_slice = algo != FC_TREE && N > 2 && (mode == FC_VAR || c->rank != sel);
-    if (incr_ok && c->agg_incr && c->agg_support_k) {
+    if (incr_ok && c->agg_incr && c->agg_support_k && !early_clear) {
       int ob0 = 0;
       TRY(agg_target(c, &ob0));
       if (!ring_slice) {

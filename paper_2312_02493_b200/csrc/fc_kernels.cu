@@ -2732,15 +2732,19 @@ __global__ void k_agg_update(const unsigned* __restrict__ prev, uint64_t kp, con
       const bool fs = j == 0 || (ip >> 3) != (i >> 3);
       const bool fw = j == 0 || zmap_word(ip) != zmap_word(i);
       if (!fs && !fw) continue;
-      // this step's entries in the same chunk (sorted): any in the sector / word?
-      const unsigned c = i >> kChunkShift;
-      const unsigned lo = __ldg(bounds + c), hi = __ldg(bounds + c + 1);
+      // this step's entries in the same chunk (sorted): any in the sector /
+      // word?  (bounds == nullptr: this step's list is not known yet -- the
+      // write launch that follows rewrites its sectors after this one)
       bool ins = false, inw = false;
-      for (unsigned q = lo; q < hi; ++q) {
-        const unsigned m = __ldg(idx + q);
-        if (m > (i | 31u)) break;
-        inw |= zmap_word(m) == zmap_word(i);
-        ins |= (m >> 3) == (i >> 3);
+      if (bounds) {
+        const unsigned c = i >> kChunkShift;
+        const unsigned lo = __ldg(bounds + c), hi = __ldg(bounds + c + 1);
+        for (unsigned q = lo; q < hi; ++q) {
+          const unsigned m = __ldg(idx + q);
+          if (m > (i | 31u)) break;
+          inw |= zmap_word(m) == zmap_word(i);
+          ins |= (m >> 3) == (i >> 3);
+        }
       }
       if (fs && !ins) {
         const float z[kAggAtom] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
