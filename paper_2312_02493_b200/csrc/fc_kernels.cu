@@ -609,15 +609,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_ef(const float* __restrict__ g_
         unsigned b1, b2;
         unsigned long long above1, above2;
         const unsigned long long tgt = (unsigned long long)target;
-        // the speculative level-2 histograms come into shared memory with the
-        // level-1 one (one L2 round trip for both)
-        if (lastb1)
-          for (int b = tid; b < kSpecBins * 256; b += kThreads) s_sub[b] = __ldcg(ctl->hist_s2w + b);
         if (block_select_top<kThreads>(ctl->hist_s, kBins1, tgt, b1, above1, s_hist)) {
           bool f2;
           if (lastb1 && b1 - slo < (unsigned)kSpecBins) {  // speculation hit: level 2 is in
-            unsigned* h2 = s_sub + (b1 - slo) * 256;
-            f2 = block_select_top<kThreads>(h2, 256, tgt - above1, b2, above2, h2);
+            f2 = block_select_top<kThreads>(ctl->hist_s2w + (b1 - slo) * 256, 256, tgt - above1, b2, above2, s_hist);
           } else {
             for (int b = tid; b < 256; b += kThreads) s_hist[b] = 0u;
             __syncthreads();
